@@ -1,0 +1,186 @@
+// Max-pooling and dense (dilated) max-filtering with argmax masks
+// (maxops.hpp:32-182). HBM-bound; one thread per output voxel forward, one
+// thread per input voxel backward (gather formulation: deterministic, no
+// atomics). Mask = int32 flat index into the per-map input volume.
+//
+// Tie rule: the reference resolves ties to the lexicographically smallest
+// (x,y,z) source, i.e. the lowest flat index (maxops.hpp:79-82 strict '>'
+// scan; maxops.hpp:106-110 for the separable filter). A direct window scan
+// in lexicographic order with strict '>' selects the same source, so masks
+// are bit-identical on identical inputs.
+#include "ops.hpp"
+
+namespace znn_gpu {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(int64_t n) {
+    int64_t b = ceil_div(n, kThreads);
+    if (b > 148 * 32) b = 148 * 32;
+    return unsigned(b < 1 ? 1 : b);
+}
+
+__global__ void maxfilter_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny,
+                                int nz, int mx, int my, int mz, int kx, int ky, int kz, int sx,
+                                int sy, int sz, float* __restrict__ y,
+                                int32_t* __restrict__ mask) {
+    const int64_t mv = int64_t(mx) * my * mz;
+    const int64_t nv = int64_t(nx) * ny * nz;
+    const int64_t total = maps * mv;
+    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total;
+         o += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t map = o / mv;
+        const int64_t r = o - map * mv;
+        const int i = int(r / (int64_t(my) * mz));
+        const int j = int((r / mz) % my);
+        const int l = int(r % mz);
+        const float* xm = x + map * nv;
+        int best_idx = (i * ny + j) * nz + l;
+        float best = xm[best_idx];
+        for (int a = 0; a < kx; ++a)
+            for (int b = 0; b < ky; ++b)
+                for (int c = 0; c < kz; ++c) {
+                    const int idx = ((i + sx * a) * ny + (j + sy * b)) * nz + (l + sz * c);
+                    const float v = xm[idx];
+                    if (v > best) {
+                        best = v;
+                        best_idx = idx;
+                    }
+                }
+        y[o] = best;
+        mask[o] = best_idx;
+    }
+}
+
+// dx[t] = sum over windows o whose argmax is t of g[o]; windows visited in
+// ascending flat order of o, the order the reference accumulates in
+// (maxops.hpp:176-181), so fp32 sums match it bit for bit.
+__global__ void maxfilter_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
+                                int64_t maps, int nx, int ny, int nz, int mx, int my, int mz,
+                                int kx, int ky, int kz, int sx, int sy, int sz,
+                                float* __restrict__ dx) {
+    const int64_t mv = int64_t(mx) * my * mz;
+    const int64_t nv = int64_t(nx) * ny * nz;
+    const int64_t total = maps * nv;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t map = t / nv;
+        const int tr = int(t - map * nv);
+        const int ti = tr / (ny * nz);
+        const int tj = (tr / nz) % ny;
+        const int tl = tr % nz;
+        const float* gm = g + map * mv;
+        const int32_t* mm = mask + map * mv;
+        float acc = 0.f;
+        for (int a = kx - 1; a >= 0; --a) {
+            const int oi = ti - sx * a;
+            if (oi < 0 || oi >= mx) continue;
+            for (int b = ky - 1; b >= 0; --b) {
+                const int oj = tj - sy * b;
+                if (oj < 0 || oj >= my) continue;
+                for (int c = kz - 1; c >= 0; --c) {
+                    const int ol = tl - sz * c;
+                    if (ol < 0 || ol >= mz) continue;
+                    const int o = (oi * my + oj) * mz + ol;
+                    if (mm[o] == tr) acc += gm[o];
+                }
+            }
+        }
+        dx[t] = acc;
+    }
+}
+
+__global__ void maxpool_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny, int nz,
+                              int px, int py, int pz, float* __restrict__ y,
+                              int32_t* __restrict__ mask) {
+    const int mx = nx / px, my = ny / py, mz = nz / pz;
+    const int64_t mv = int64_t(mx) * my * mz;
+    const int64_t nv = int64_t(nx) * ny * nz;
+    const int64_t total = maps * mv;
+    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total;
+         o += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t map = o / mv;
+        const int64_t r = o - map * mv;
+        const int bi = int(r / (int64_t(my) * mz));
+        const int bj = int((r / mz) % my);
+        const int bl = int(r % mz);
+        const float* xm = x + map * nv;
+        int best_idx = ((bi * px) * ny + bj * py) * nz + bl * pz;
+        float best = xm[best_idx];
+        for (int a = 0; a < px; ++a)
+            for (int b = 0; b < py; ++b)
+                for (int c = 0; c < pz; ++c) {
+                    const int idx = ((bi * px + a) * ny + (bj * py + b)) * nz + (bl * pz + c);
+                    const float v = xm[idx];
+                    if (v > best) {
+                        best = v;
+                        best_idx = idx;
+                    }
+                }
+        y[o] = best;
+        mask[o] = best_idx;
+    }
+}
+
+__global__ void maxpool_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
+                              int64_t maps, int mx, int my, int mz, int px, int py, int pz,
+                              float* __restrict__ dx) {
+    const int nx = mx * px, ny = my * py, nz = mz * pz;
+    const int64_t mv = int64_t(mx) * my * mz;
+    const int64_t nv = int64_t(nx) * ny * nz;
+    const int64_t total = maps * nv;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t map = t / nv;
+        const int tr = int(t - map * nv);
+        const int ti = tr / (ny * nz);
+        const int tj = (tr / nz) % ny;
+        const int tl = tr % nz;
+        const int o = ((ti / px) * my + (tj / py)) * mz + (tl / pz);
+        dx[t] = (mask[map * mv + o] == tr) ? g[map * mv + o] : 0.f;
+    }
+}
+
+}  // namespace
+
+void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s,
+                   float* y, int32_t* mask) {
+    const dims3 m{n.x - s.x * (k.x - 1), n.y - s.y * (k.y - 1), n.z - s.z * (k.z - 1)};
+    require(m.x > 0 && m.y > 0 && m.z > 0, "maxfilter_forward: effective window exceeds input");
+    require(n.vol() < (int64_t(1) << 31), "maxfilter_forward: map exceeds int32 mask range");
+    maxfilter_fwd_k<<<grid_for(maps * m.vol()), kThreads, 0, st>>>(
+        x, maps, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z), int(k.x),
+        int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), y, mask);
+    launch_check("maxfilter_fwd");
+}
+
+void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
+                   dims3 k, dims3 s, float* dx) {
+    const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
+    maxfilter_bwd_k<<<grid_for(maps * n.vol()), kThreads, 0, st>>>(
+        g, mask, maps, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z), int(k.x),
+        int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), dx);
+    launch_check("maxfilter_bwd");
+}
+
+void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p, float* y,
+                 int32_t* mask) {
+    require(p.x > 0 && p.y > 0 && p.z > 0 && n.x % p.x == 0 && n.y % p.y == 0 && n.z % p.z == 0,
+            "maxpool_forward: dims not divisible by window");
+    const dims3 m{n.x / p.x, n.y / p.y, n.z / p.z};
+    maxpool_fwd_k<<<grid_for(maps * m.vol()), kThreads, 0, st>>>(
+        x, maps, int(n.x), int(n.y), int(n.z), int(p.x), int(p.y), int(p.z), y, mask);
+    launch_check("maxpool_fwd");
+}
+
+void maxpool_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
+                 dims3 p, float* dx) {
+    const int64_t nvol = m.vol() * p.vol();
+    maxpool_bwd_k<<<grid_for(maps * nvol), kThreads, 0, st>>>(
+        g, mask, maps, int(m.x), int(m.y), int(m.z), int(p.x), int(p.y), int(p.z), dx);
+    launch_check("maxpool_bwd");
+}
+
+}  // namespace znn_gpu

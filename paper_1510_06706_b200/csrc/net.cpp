@@ -1,0 +1,552 @@
+#include "net.hpp"
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <sstream>
+
+#include "fft.hpp"
+
+namespace znn_exec {
+
+using znn_gpu::require;
+using znn_host::op;
+using znn_host::role;
+using znn_host::gedge;
+
+namespace {
+dims3 to_d3(v3 v) { return dims3{v.x, v.y, v.z}; }
+const char* kname(lkind k) {
+    switch (k) {
+        case lkind::conv: return "conv";
+        case lkind::transfer: return "transfer";
+        case lkind::pool: return "pool";
+        default: return "filter";
+    }
+}
+const char* ename(int e) {
+    switch (e) {
+        case 0: return "direct";
+        case 1: return "fft";
+        case 2: return "auto";
+        default: return "direct-simt";
+    }
+}
+}  // namespace
+
+executor::executor(const std::string& netspec, const v3* out_dims, const train_cfg& cfg,
+                   cudaStream_t stream)
+    : cfg_(cfg), st_(stream) {
+    require(cfg.batch >= 1 && cfg.global_batch >= cfg.batch, "train config: bad batch sizes");
+    require(cfg.loss == 0 || cfg.loss == 1, "train config: unknown loss");
+    v3 od = out_dims ? *out_dims : v3{0, 0, 0};
+    znn_host::graph g = znn_host::parse_netspec(netspec, od);
+    if (cfg.sliding) {
+        v3 outd{0, 0, 0};
+        for (const auto& n : g.nodes)
+            if (n.r == role::output) outd = n.dims;
+        g = znn_host::sliding_equivalent(g);
+        znn_host::infer_shapes(g, outd);
+    }
+    g_ = std::move(g);
+    build(g_);
+    allocate();
+}
+
+executor::~executor() {
+    for (void* p : owned_) cudaFree(p);
+}
+
+void* executor::dalloc(size_t bytes) {
+    void* p = nullptr;
+    ZNN_CUDA_CHECK(cudaMalloc(&p, bytes < 16 ? 16 : bytes));
+    owned_.push_back(p);
+    return p;
+}
+
+void executor::build(const znn_host::graph& g) {
+    const auto order = g.topo();
+    std::vector<int> depth(g.nodes.size(), 0);
+    for (int v : order)
+        for (int eid : g.nodes[size_t(v)].outs) {
+            const int t = g.edges[size_t(eid)].to;
+            depth[size_t(t)] = std::max(depth[size_t(t)], depth[size_t(v)] + 1);
+        }
+    int D = 0;
+    for (int d : depth) D = std::max(D, d);
+    std::vector<std::vector<int>> byd(size_t(D) + 1);
+    for (size_t v = 0; v < g.nodes.size(); ++v) byd[size_t(depth[v])].push_back(int(v));
+    for (const auto& e : g.edges)
+        require(depth[size_t(e.to)] == depth[size_t(e.from)] + 1,
+                "GPU executor: edge " + e.name + " skips a layer (node groups must be layered)");
+    for (int v : byd[0]) require(g.nodes[size_t(v)].r == role::input, "GPU executor: depth-0 node " + g.nodes[size_t(v)].name + " is not an input");
+    for (size_t v = 0; v < g.nodes.size(); ++v)
+        require((g.nodes[v].r == role::output) == (depth[v] == D),
+                "GPU executor: outputs must be exactly the deepest node group (node " + g.nodes[v].name + ")");
+
+    groups_.resize(size_t(D) + 1);
+    groups_[0].nodes = byd[0];
+    std::vector<int> pos(g.nodes.size(), -1);
+    auto set_group = [&](int d, const std::vector<int>& nodes) {
+        group& G = groups_[size_t(d)];
+        G.nodes = nodes;
+        G.maps = int64_t(nodes.size());
+        const v3 dm = g.nodes[size_t(nodes[0])].dims;
+        for (size_t i = 0; i < nodes.size(); ++i) {
+            require(g.nodes[size_t(nodes[i])].dims == dm, "GPU executor: node group " + std::to_string(d) + " has unequal image dims");
+            pos[size_t(nodes[i])] = int(i);
+        }
+        G.dims = to_d3(dm);
+    };
+    set_group(0, byd[0]);
+
+    for (int d = 0; d < D; ++d) {
+        const auto& heads = byd[size_t(d) + 1];
+        const op kind = g.edges[size_t(g.nodes[size_t(heads[0])].ins[0])].kind;
+        layer L;
+        L.in = d, L.out = d + 1;
+        const group& I = groups_[size_t(d)];
+        if (kind == op::conv) {
+            const gedge& e0 = g.edges[size_t(g.nodes[size_t(heads[0])].ins[0])];
+            for (int h : heads)
+                for (int eid : g.nodes[size_t(h)].ins) {
+                    const auto& e = g.edges[size_t(eid)];
+                    require(e.kind == op::conv && e.k == e0.k && e.s == e0.s,
+                            "GPU executor: conv layer " + std::to_string(d) + " mixes kernels/sparsities/edge types");
+                }
+            std::vector<int> hs = heads;
+            std::sort(hs.begin(), hs.end());
+            set_group(d + 1, hs);
+            // full connectivity: exactly one edge per (head, tail) pair
+            std::vector<int> seen(size_t(I.maps) * hs.size(), -1);
+            for (int h : hs)
+                for (int eid : g.nodes[size_t(h)].ins) {
+                    const auto& e = g.edges[size_t(eid)];
+                    const size_t slot = size_t(pos[size_t(h)]) * size_t(I.maps) + size_t(pos[size_t(e.from)]);
+                    require(seen[slot] < 0, "GPU executor: duplicate conv edge " + e.name);
+                    seen[slot] = eid;
+                }
+            for (int s : seen) require(s >= 0, "GPU executor: conv layer " + std::to_string(d) + " is not fully connected");
+            L.kind = lkind::conv;
+            L.edge_ids = seen;  // [o][i]
+            L.shape = conv_shape::make(cfg_.batch, I.maps, int64_t(hs.size()), I.dims, to_d3(e0.k), to_d3(e0.s));
+            L.engine = cfg_.engine;
+        } else {
+            // element-wise layer: one in-edge per head, one out-edge per tail
+            require(heads.size() == size_t(I.maps), "GPU executor: layer " + std::to_string(d) + " must map tails to heads one-to-one");
+            std::vector<int> hs(heads.size(), -1);
+            std::vector<int> eids(heads.size(), -1);
+            const gedge& e0 = g.edges[size_t(g.nodes[size_t(heads[0])].ins[0])];
+            for (int h : heads) {
+                require(g.nodes[size_t(h)].ins.size() == 1, "GPU executor: node " + g.nodes[size_t(h)].name + " mixes convergent edges with a non-conv layer");
+                const auto& e = g.edges[size_t(g.nodes[size_t(h)].ins[0])];
+                require(e.kind == kind, "GPU executor: layer " + std::to_string(d) + " mixes edge types");
+                if (kind != op::transfer)
+                    require(e.k == e0.k && e.s == e0.s, "GPU executor: layer " + std::to_string(d) + " mixes windows");
+                const int p = pos[size_t(e.from)];
+                require(p >= 0 && hs[size_t(p)] < 0, "GPU executor: layer " + std::to_string(d) + " is not one-to-one");
+                hs[size_t(p)] = h;
+                eids[size_t(p)] = g.nodes[size_t(h)].ins[0];
+            }
+            for (int v : byd[size_t(d)])
+                require(g.nodes[size_t(v)].outs.size() == 1, "GPU executor: node " + g.nodes[size_t(v)].name + " fans out into an element-wise layer");
+            set_group(d + 1, hs);
+            L.edge_ids = eids;
+            if (kind == op::transfer) {
+                L.kind = lkind::transfer;
+                for (int eid : eids) L.kinds.push_back(g.edges[size_t(eid)].fn);
+            } else {
+                L.kind = kind == op::pool ? lkind::pool : lkind::filter;
+                L.k = to_d3(e0.k);
+                L.s = to_d3(e0.s);
+            }
+        }
+        layers_.push_back(std::move(L));
+    }
+
+    // fuse conv -> transfer (uniform kind) into the conv epilogue
+    std::vector<layer> fused;
+    for (size_t i = 0; i < layers_.size(); ++i) {
+        layer L = layers_[i];
+        if (L.kind == lkind::conv && i + 1 < layers_.size() && layers_[i + 1].kind == lkind::transfer) {
+            const layer& T = layers_[i + 1];
+            bool uniform = std::all_of(T.kinds.begin(), T.kinds.end(), [&](int k) { return k == T.kinds[0]; });
+            if (uniform) {
+                L.fused = true;
+                L.fused_act = T.kinds[0];
+                L.kinds = T.kinds;
+                L.transfer_edge_ids = T.edge_ids;
+                groups_[size_t(L.out)].materialized = false;
+                L.out = T.out;
+                ++i;
+            }
+        }
+        fused.push_back(std::move(L));
+    }
+    layers_ = std::move(fused);
+
+    // flat parameter layout and the canonical (reference edge-id) order map
+    std::vector<std::pair<int64_t, int64_t>> edge_slot(g.edges.size(), {-1, 0});
+    flat_ = 0;
+    for (auto& L : layers_) {
+        if (L.kind == lkind::conv) {
+            const int64_t T = L.shape.taps();
+            L.w_off = flat_;
+            for (int64_t o = 0; o < L.shape.f_out; ++o)
+                for (int64_t i = 0; i < L.shape.f_in; ++i)
+                    edge_slot[size_t(L.edge_ids[size_t(o * L.shape.f_in + i)])] = {L.w_off + (o * L.shape.f_in + i) * T, T};
+            flat_ += L.shape.f_out * L.shape.f_in * T;
+            if (L.fused) {
+                L.b_off = flat_;
+                for (size_t o = 0; o < L.transfer_edge_ids.size(); ++o)
+                    edge_slot[size_t(L.transfer_edge_ids[o])] = {L.b_off + int64_t(o), 1};
+                flat_ += L.shape.f_out;
+            }
+        } else if (L.kind == lkind::transfer) {
+            L.b_off = flat_;
+            for (size_t o = 0; o < L.edge_ids.size(); ++o) edge_slot[size_t(L.edge_ids[o])] = {L.b_off + int64_t(o), 1};
+            flat_ += int64_t(L.edge_ids.size());
+        }
+    }
+    canon_.clear();
+    for (size_t eid = 0; eid < g.edges.size(); ++eid) {
+        const auto& e = g.edges[eid];
+        if (e.kind != op::conv && e.kind != op::transfer) continue;
+        for (int64_t t = 0; t < edge_slot[eid].second; ++t) canon_.push_back(edge_slot[eid].first + t);
+    }
+
+    // output ordering: group position -> ordinal among output nodes by id
+    const group& G = groups_.back();
+    std::vector<int> outs;
+    for (size_t v = 0; v < g.nodes.size(); ++v)
+        if (g.nodes[v].r == role::output) outs.push_back(int(v));
+    out_perm_.assign(size_t(G.maps), 0);
+    out_identity_ = true;
+    for (size_t p = 0; p < G.nodes.size(); ++p) {
+        out_perm_[p] = int(std::find(outs.begin(), outs.end(), G.nodes[p]) - outs.begin());
+        if (out_perm_[p] != int(p)) out_identity_ = false;
+    }
+    if (cfg_.loss == 1) {
+        const layer& last = layers_.back();
+        const bool ok = (last.kind == lkind::conv && last.fused && last.fused_act == 0) ||
+                        (last.kind == lkind::transfer &&
+                         std::all_of(last.kinds.begin(), last.kinds.end(), [](int k) { return k == 0; }));
+        require(ok, "cross-entropy loss needs a logistic transfer edge into every output node");
+    }
+
+    std::ostringstream os;
+    for (size_t i = 0; i < groups_.size(); ++i)
+        os << "group " << i << ": maps=" << groups_[i].maps << " dims=" << groups_[i].dims.x << ","
+           << groups_[i].dims.y << "," << groups_[i].dims.z << (groups_[i].materialized ? "" : " (fused)") << "\n";
+    int ci = 0;
+    for (const auto& L : layers_) {
+        os << "layer " << kname(L.kind) << " " << L.in << "->" << L.out;
+        if (L.kind == lkind::conv) {
+            os << " conv#" << ci++ << " f=" << L.shape.f_in << "->" << L.shape.f_out << " k=" << L.shape.k.x << ","
+               << L.shape.k.y << "," << L.shape.k.z << " s=" << L.shape.s.x << "," << L.shape.s.y << "," << L.shape.s.z
+               << " engine=" << ename(L.engine);
+            if (L.fused) os << " +transfer(kind=" << L.fused_act << ")";
+        } else if (L.kind == lkind::pool || L.kind == lkind::filter) {
+            os << " k=" << L.k.x << "," << L.k.y << "," << L.k.z << " s=" << L.s.x << "," << L.s.y << "," << L.s.z;
+        }
+        os << "\n";
+    }
+    desc_ = os.str();
+}
+
+void executor::allocate() {
+    const int64_t B = cfg_.batch;
+    int64_t maxsz = 0;
+    for (size_t j = 0; j < groups_.size(); ++j) {
+        group& G = groups_[j];
+        const int64_t n = B * G.maps * G.dims.vol();
+        maxsz = std::max(maxsz, n);
+        if (j > 0 && G.materialized) G.act = static_cast<float*>(dalloc(sizeof(float) * size_t(n)));
+        if (cfg_.keep_images && G.materialized) G.grad = static_cast<float*>(dalloc(sizeof(float) * size_t(n)));
+    }
+    for (const auto& L : layers_)
+        if (L.kind == lkind::pool || L.kind == lkind::filter) {
+            group& G = groups_[size_t(L.out)];
+            G.mask = static_cast<int32_t*>(dalloc(sizeof(int32_t) * size_t(B * G.maps * G.dims.vol())));
+        }
+    if (!cfg_.keep_images) {
+        gbuf_[0] = static_cast<float*>(dalloc(sizeof(float) * size_t(maxsz)));
+        gbuf_[1] = static_cast<float*>(dalloc(sizeof(float) * size_t(maxsz)));
+    }
+    params_ = static_cast<float*>(dalloc(sizeof(float) * size_t(flat_)));
+    grads_ = static_cast<float*>(dalloc(sizeof(float) * size_t(flat_)));
+    vel_ = static_cast<float*>(dalloc(sizeof(float) * size_t(flat_)));
+    ZNN_CUDA_CHECK(cudaMemsetAsync(params_, 0, sizeof(float) * size_t(flat_), st_));
+    ZNN_CUDA_CHECK(cudaMemsetAsync(grads_, 0, sizeof(float) * size_t(flat_), st_));
+    ZNN_CUDA_CHECK(cudaMemsetAsync(vel_, 0, sizeof(float) * size_t(flat_), st_));
+    for (auto& L : layers_)
+        if (!L.kinds.empty()) {
+            L.kinds_dev = static_cast<int32_t*>(dalloc(sizeof(int32_t) * L.kinds.size()));
+            ZNN_CUDA_CHECK(cudaMemcpy(L.kinds_dev, L.kinds.data(), sizeof(int32_t) * L.kinds.size(),
+                                      cudaMemcpyHostToDevice));
+            const std::vector<int32_t> none(L.kinds.size(), 3);
+            L.none_dev = static_cast<int32_t*>(dalloc(sizeof(int32_t) * none.size()));
+            ZNN_CUDA_CHECK(cudaMemcpy(L.none_dev, none.data(), sizeof(int32_t) * none.size(),
+                                      cudaMemcpyHostToDevice));
+        }
+    const group& G = groups_.back();
+    labels_perm_ = static_cast<float*>(dalloc(sizeof(float) * size_t(B * G.maps * G.dims.vol())));
+    in_stage_ = static_cast<float*>(dalloc(sizeof(float) * size_t(in_per_patch() * B)));
+    lab_stage_ = static_cast<float*>(dalloc(sizeof(float) * size_t(out_per_patch() * B)));
+    loss_dev_ = static_cast<double*>(dalloc(sizeof(double)));
+    groups_[0].act = in_stage_;
+    // grad pointers for the ping-pong scheme: alternate by materialized ordinal
+    if (!cfg_.keep_images) {
+        int q = 0;
+        for (size_t j = 0; j < groups_.size(); ++j)
+            if (groups_[j].materialized) groups_[j].grad = gbuf_[(q++) & 1];
+    }
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+int64_t executor::in_per_patch() const { return groups_.front().maps * groups_.front().dims.vol(); }
+int64_t executor::out_per_patch() const { return groups_.back().maps * groups_.back().dims.vol(); }
+
+void executor::set_params(const float* host) {
+    std::vector<float> flat(size_t(flat_), 0.f);
+    for (size_t c = 0; c < canon_.size(); ++c) flat[size_t(canon_[c])] = host[c];
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(params_, flat.data(), sizeof(float) * size_t(flat_), cudaMemcpyHostToDevice, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+void executor::get_params(float* host) {
+    std::vector<float> flat(static_cast<size_t>(flat_));
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(flat.data(), params_, sizeof(float) * size_t(flat_), cudaMemcpyDeviceToHost, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (size_t c = 0; c < canon_.size(); ++c) host[c] = flat[size_t(canon_[c])];
+}
+
+void executor::get_gradients(float* host) {
+    std::vector<float> flat(static_cast<size_t>(flat_));
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(flat.data(), grads_, sizeof(float) * size_t(flat_), cudaMemcpyDeviceToHost, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (size_t c = 0; c < canon_.size(); ++c) host[c] = flat[size_t(canon_[c])];
+}
+
+void executor::reset_momentum() {
+    ZNN_CUDA_CHECK(cudaMemsetAsync(vel_, 0, sizeof(float) * size_t(flat_), st_));
+}
+
+void executor::set_layer_engine(int conv_layer, int engine) {
+    int ci = 0;
+    for (auto& L : layers_)
+        if (L.kind == lkind::conv) {
+            if (ci == conv_layer) {
+                require(engine == 0 || engine == 1 || engine == 3, "set_layer_engine: unknown engine");
+                L.engine = engine;
+                return;
+            }
+            ++ci;
+        }
+    throw znn_gpu::shape_error("set_layer_engine: no conv layer " + std::to_string(conv_layer));
+}
+
+void executor::run_conv_fwd(const layer& L) {
+    const float* x = groups_[size_t(L.in)].act;
+    float* y = groups_[size_t(L.out)].act;
+    const float* w = params_ + L.w_off;
+    const float* bias = L.fused ? params_ + L.b_off : nullptr;
+    const int act = L.fused ? L.fused_act : 3;
+    if (L.engine == 1) {
+        znn_fft::conv_fwd(st_, L.shape, x, w, bias, act, y, ws_);
+    } else if (L.engine == 0 && znn_gpu::conv_tc_supported(L.shape, 0)) {
+        znn_gpu::conv_fwd_tc(st_, L.shape, x, w, bias, act, y, ws_);
+    } else {
+        znn_gpu::conv_fwd_simt(st_, L.shape, x, w, bias, act, y);
+    }
+}
+
+void executor::run_conv_bwd(const layer& L, float* g_out, float* g_in, bool need_dgrad) {
+    const float* x = groups_[size_t(L.in)].act;
+    const float* w = params_ + L.w_off;
+    float* gw = grads_ + L.w_off;
+    if (L.engine == 1) {
+        znn_fft::conv_bwd(st_, L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_);
+        return;
+    }
+    const bool tc = L.engine == 0;
+    if (tc && znn_gpu::conv_tc_supported(L.shape, 2))
+        znn_gpu::conv_wgrad_tc(st_, L.shape, x, g_out, gw, 1.f, ws_);
+    else
+        znn_gpu::conv_wgrad_simt(st_, L.shape, x, g_out, gw, 1.f, ws_);
+    if (need_dgrad) {
+        if (tc && znn_gpu::conv_tc_supported(L.shape, 1))
+            znn_gpu::conv_dgrad_tc(st_, L.shape, g_out, w, g_in, ws_);
+        else
+            znn_gpu::conv_dgrad_simt(st_, L.shape, g_out, w, g_in);
+    }
+}
+
+void executor::run_forward(const float* in_dev) {
+    groups_[0].act = const_cast<float*>(in_dev);
+    const int64_t B = cfg_.batch;
+    for (const auto& L : layers_) {
+        const group& I = groups_[size_t(L.in)];
+        group& O = groups_[size_t(L.out)];
+        switch (L.kind) {
+            case lkind::conv: run_conv_fwd(L); break;
+            case lkind::transfer:
+                znn_gpu::transfer_fwd(st_, I.act, B, I.maps, I.dims.vol(), L.kinds_dev, params_ + L.b_off, O.act);
+                break;
+            case lkind::pool: znn_gpu::maxpool_fwd(st_, I.act, B * I.maps, I.dims, L.k, O.act, O.mask); break;
+            case lkind::filter:
+                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.mask);
+                break;
+        }
+    }
+}
+
+void executor::forward(const float* in_dev) { run_forward(in_dev); }
+
+double executor::forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss) {
+    const int64_t B = cfg_.batch;
+    run_forward(in_dev);
+    group& G = groups_.back();
+    const int64_t vol = G.dims.vol();
+    const float* lab = labels_dev;
+    if (!out_identity_) {
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t p = 0; p < G.maps; ++p)
+                ZNN_CUDA_CHECK(cudaMemcpyAsync(labels_perm_ + (b * G.maps + p) * vol,
+                                               labels_dev + (b * G.maps + out_perm_[size_t(p)]) * vol,
+                                               sizeof(float) * size_t(vol), cudaMemcpyDeviceToDevice, st_));
+        lab = labels_perm_;
+    }
+    znn_gpu::loss_grad_async(st_, cfg_.loss, G.act, lab, B * G.maps * vol, 1.f / float(cfg_.global_batch),
+                             G.grad, loss_dev_, ws_);
+    // backward in reverse layer order
+    for (size_t li = layers_.size(); li-- > 0;) {
+        const layer& L = layers_[li];
+        group& I = groups_[size_t(L.in)];
+        group& O = groups_[size_t(L.out)];
+        const bool last = li + 1 == layers_.size();
+        const bool ce_here = last && cfg_.loss == 1;
+        switch (L.kind) {
+            case lkind::conv: {
+                if (L.fused) {
+                    // ce: loss already produced the pre-activation gradient a - d
+                    if (ce_here) {
+                        znn_gpu::transfer_bwd(st_, O.grad, O.act, true, B, L.shape.f_out, O.dims.vol(),
+                                              L.none_dev, params_ + L.b_off, O.grad, grads_ + L.b_off, ws_);
+                    } else {
+                        znn_gpu::transfer_bwd(st_, O.grad, O.act, true, B, L.shape.f_out, O.dims.vol(),
+                                              L.kinds_dev, params_ + L.b_off, O.grad, grads_ + L.b_off, ws_);
+                    }
+                }
+                run_conv_bwd(L, O.grad, I.grad, L.in != 0);
+                break;
+            }
+            case lkind::transfer:
+                znn_gpu::transfer_bwd(st_, O.grad, I.act, false, B, I.maps, I.dims.vol(),
+                                      ce_here ? L.none_dev : L.kinds_dev, params_ + L.b_off,
+                                      I.grad ? I.grad : O.grad, grads_ + L.b_off, ws_);
+                break;
+            case lkind::pool:
+                if (L.in != 0) znn_gpu::maxpool_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, I.grad);
+                break;
+            case lkind::filter:
+                if (L.in != 0) znn_gpu::maxfilter_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, L.s, I.grad);
+                break;
+        }
+    }
+    if (!sync_loss) return 0.0;
+    return last_loss_device();
+}
+
+double executor::last_loss_device() {
+    double h = 0.0;
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(&h, loss_dev_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+    return h / double(cfg_.batch);
+}
+
+void executor::apply_update() { znn_gpu::sgd_momentum(st_, params_, vel_, grads_, flat_, cfg_.lr, cfg_.mu); }
+
+double executor::step_host(const float* in_host, const float* labels_host) {
+    const int64_t B = cfg_.batch;
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(in_stage_, in_host, sizeof(float) * size_t(B * in_per_patch()), cudaMemcpyHostToDevice, st_));
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(lab_stage_, labels_host, sizeof(float) * size_t(B * out_per_patch()), cudaMemcpyHostToDevice, st_));
+    forward_backward(in_stage_, lab_stage_, false);
+    apply_update();
+    return last_loss_device();
+}
+
+void executor::copy_outputs(float* host) {
+    const group& G = groups_.back();
+    const int64_t vol = G.dims.vol();
+    std::vector<float> tmp(size_t(cfg_.batch * G.maps * vol));
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), G.act, sizeof(float) * tmp.size(), cudaMemcpyDeviceToHost, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+    for (int64_t b = 0; b < cfg_.batch; ++b)
+        for (int64_t p = 0; p < G.maps; ++p)
+            std::memcpy(host + (b * G.maps + out_perm_[size_t(p)]) * vol, tmp.data() + (b * G.maps + p) * vol,
+                        sizeof(float) * size_t(vol));
+}
+
+void executor::group_image(int gi, int which, float* host) {
+    const group& G = groups_.at(size_t(gi));
+    require(G.materialized, "group image: group " + std::to_string(gi) + " is fused away");
+    const float* src = which == 0 ? G.act : G.grad;
+    require(src != nullptr, "group image: image not available");
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(host, src, sizeof(float) * size_t(cfg_.batch * G.maps * G.dims.vol()),
+                                   cudaMemcpyDeviceToHost, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+void executor::group_mask(int gi, int32_t* host) {
+    const group& G = groups_.at(size_t(gi));
+    require(G.mask != nullptr, "group mask: group " + std::to_string(gi) + " has no argmax record");
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(host, G.mask, sizeof(int32_t) * size_t(cfg_.batch * G.maps * G.dims.vol()),
+                                   cudaMemcpyDeviceToHost, st_));
+    ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+}
+
+std::vector<int> executor::autotune(int trials) {
+    require(trials >= 1, "autotune: trials must be >= 1");
+    std::vector<int> chosen;
+    cudaEvent_t a, b;
+    ZNN_CUDA_CHECK(cudaEventCreate(&a));
+    ZNN_CUDA_CHECK(cudaEventCreate(&b));
+    for (auto& L : layers_) {
+        if (L.kind != lkind::conv) continue;
+        // candidate engines: tensor-core direct, SIMT direct, FFT
+        std::vector<int> cands{0, 3};
+        if (znn_fft::supported(L.shape)) cands.push_back(1);
+        // scratch inputs for the bwd pass: reuse the layer's own buffers
+        float* gout = groups_[size_t(L.out)].grad;
+        float* gin = groups_[size_t(L.in)].grad;
+        float best = 1e30f;
+        int best_e = L.engine;
+        for (int e : cands) {
+            layer T = L;
+            T.engine = e;
+            std::vector<float> ts;
+            for (int t = 0; t <= trials; ++t) {
+                ZNN_CUDA_CHECK(cudaEventRecord(a, st_));
+                run_conv_fwd(T);
+                run_conv_bwd(T, gout, gin, L.in != 0);
+                ZNN_CUDA_CHECK(cudaEventRecord(b, st_));
+                ZNN_CUDA_CHECK(cudaEventSynchronize(b));
+                float ms = 0.f;
+                ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+                if (t > 0) ts.push_back(ms);  // first run warms plans and scratch
+            }
+            std::sort(ts.begin(), ts.end());
+            const float med = ts[ts.size() / 2];
+            if (med < best) best = med, best_e = e;
+        }
+        L.engine = best_e;
+        chosen.push_back(best_e);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    // the timing runs overwrote activations/gradients: not a training step
+    return chosen;
+}
+
+}  // namespace znn_exec

@@ -1,0 +1,127 @@
+// Layer-wave GPU executor: replaces the reference's per-edge task engine
+// (engine.hpp:45-901) for one data-parallel rank. Nodes of the reference
+// graph are grouped by depth into node groups (one device tensor
+// [B][maps][x][y][z] per group); each group-to-group transition is one layer
+// call covering every edge between the two groups and every patch.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "netgraph.hpp"
+#include "ops.hpp"
+
+namespace znn_exec {
+
+using znn_gpu::conv_shape;
+using znn_gpu::dims3;
+using znn_host::v3;
+
+struct group {
+    std::vector<int> nodes;  // graph node ids in map order
+    int64_t maps = 0;
+    dims3 dims{1, 1, 1};
+    float* act = nullptr;    // forward image [B][maps][vol] (null when fused away)
+    float* grad = nullptr;   // backward image (kept per group only with keep_images)
+    int32_t* mask = nullptr; // argmax record when produced by pool/filter
+    bool materialized = true;
+};
+
+enum class lkind { conv, transfer, pool, filter };
+
+struct layer {
+    lkind kind = lkind::conv;
+    int in = -1, out = -1;  // group indices
+    // conv
+    conv_shape shape;
+    int64_t w_off = -1;     // offset of [f_out][f_in][T] in the flat parameter buffer
+    int engine = 0;         // ZNN_CONV_*
+    bool fused = false;     // transfer edge fused into the conv epilogue
+    int fused_act = 3;
+    int64_t b_off = -1;     // bias offset (fused transfer or transfer layer)
+    // transfer
+    std::vector<int32_t> kinds;
+    int32_t* kinds_dev = nullptr;
+    int32_t* none_dev = nullptr;  // identity kinds (CE: loss already gave a - d)
+    // pool / filter
+    dims3 k{1, 1, 1}, s{1, 1, 1};
+    std::vector<int> edge_ids;  // reference edges covered (map order)
+    std::vector<int> transfer_edge_ids;
+};
+
+struct train_cfg {
+    int64_t batch = 1, global_batch = 1;
+    float lr = 0.01f, mu = 0.f;
+    int loss = 0, engine = 0;
+    bool sliding = false;
+    bool keep_images = true;
+};
+
+class executor {
+public:
+    executor(const std::string& netspec, const v3* out_dims, const train_cfg& cfg,
+             cudaStream_t stream);
+    ~executor();
+    executor(const executor&) = delete;
+    executor& operator=(const executor&) = delete;
+
+    void set_stream(cudaStream_t s) { st_ = s; }
+    const std::string& describe() const { return desc_; }
+    int64_t num_params() const { return int64_t(canon_.size()); }
+    int64_t in_per_patch() const;
+    int64_t out_per_patch() const;
+    void set_params(const float* host);
+    void get_params(float* host);
+    void get_gradients(float* host);
+    void reset_momentum();
+    void set_layer_engine(int conv_layer, int engine);
+    std::vector<int> autotune(int trials);
+
+    // inputs/labels are device pointers [B][maps][vol] in input/output-node id order
+    double forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss = true);
+    void apply_update();
+    void forward(const float* in_dev);
+    double step_host(const float* in_host, const float* labels_host);
+    void copy_outputs(float* host);
+    float* grad_buffer() { return grads_; }
+    int64_t flat_size() const { return flat_; }
+    int num_groups() const { return int(groups_.size()); }
+    const group& grp(int i) const { return groups_.at(size_t(i)); }
+    void group_image(int g, int which, float* host);
+    void group_mask(int g, int32_t* host);
+    const std::vector<layer>& layers() const { return layers_; }
+    double last_loss_device();
+
+private:
+    void build(const znn_host::graph& g);
+    void allocate();
+    void run_forward(const float* in_dev);
+    void run_conv_fwd(const layer& L);
+    void run_conv_bwd(const layer& L, float* g_out, float* g_in, bool need_dgrad);
+
+    train_cfg cfg_;
+    cudaStream_t st_ = nullptr;
+    znn_host::graph g_;
+    std::vector<group> groups_;
+    std::vector<layer> layers_;
+    std::string desc_;
+    int64_t flat_ = 0;
+    float* params_ = nullptr;
+    float* grads_ = nullptr;
+    float* vel_ = nullptr;
+    float* gbuf_[2] = {nullptr, nullptr};
+    float* labels_perm_ = nullptr;
+    float* in_stage_ = nullptr;
+    float* lab_stage_ = nullptr;
+    double* loss_dev_ = nullptr;
+    std::vector<int> out_perm_;  // group-position -> output ordinal
+    bool out_identity_ = true;
+    std::vector<int64_t> canon_;  // canonical param index -> flat index
+    znn_gpu::scratch ws_;
+    std::vector<void*> owned_;
+    void* dalloc(size_t bytes);
+};
+
+}  // namespace znn_exec
