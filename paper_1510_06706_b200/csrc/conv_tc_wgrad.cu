@@ -1,0 +1,293 @@
+// Weight gradient of the 3D (dilated) valid convolution as a split-K
+// tcgen05 implicit GEMM, 3xTF32 (kernel_gradient_direct, conv_direct.hpp:108-132,
+// summed over the batch):
+//   dW[o][i][w] = scale * sum_{b,v} g[b][o][v] * x[b][i][v + s*w]
+// GEMM view: rows R = (i, w) (f_in*T of them, 128 per tile), columns = output
+// maps o (<= 128 per tile), K = output voxels of every patch (32 per stage,
+// never straddling a patch). Both operands are produced by warps with fully
+// coalesced row loads (a warp reads 32 consecutive voxels of one row), split
+// into tf32 hi/lo in registers and stored 128B-swizzled. Each CTA owns a
+// contiguous K range (split-K); partial tiles land in a workspace
+// [split][o][R] and a fixed-order reduction sums them (deterministic).
+//
+// Warps: 0-3 operand producers, 4-7 accumulator drain + epilogue, 8 TMEM
+// alloc + MMA issuer.
+#include <cuda.h>
+
+#include "ops.hpp"
+#include "tc_common.cuh"
+
+namespace znn_gpu {
+
+namespace {
+
+using namespace znn_tc;
+
+constexpr int THREADS = 288;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr int CHUNK_KB = 8;
+
+struct wg_params {
+    int f_in, f_out, T, nt;
+    int mrows;          // f_in * T
+    int stages, nbuf, bstride;
+    int64_t kb_per_patch, kb_total, kb_per_split;
+    int64_t nvol, mvol;
+    int ny, nz, my, mz;
+};
+
+template <int NTMAX>
+__global__ void __launch_bounds__(THREADS, 1)
+wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const int* __restrict__ rowoff_g,
+                float* __restrict__ ws, wg_params p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ int rowoff[BM];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* base_ptr = smem_raw + (base - raw);
+    const uint32_t b_bytes = uint32_t(p.nt) * 128u;
+    const uint32_t stage_bytes = 2u * BM * 128u + 2u * b_bytes;
+    const uint32_t bar_base = base + uint32_t(p.stages) * stage_bytes;
+    auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
+    auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(p.stages + s); };
+    auto accf_bar = [&](int b) { return bar_base + 8u * uint32_t(2 * p.stages + b); };
+    auto acce_bar = [&](int b) { return bar_base + 8u * uint32_t(2 * p.stages + 4 + b); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 8));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r0 = blockIdx.x * BM;   // first (i, w) row of this tile
+    const int n0 = blockIdx.y * p.nt;  // first output map
+    const int64_t q0 = int64_t(blockIdx.z) * p.kb_per_split;
+    const int64_t q1 = min(p.kb_total, q0 + p.kb_per_split);
+    const int kblocks = int(q1 - q0);
+    const int nchunks = (kblocks + CHUNK_KB - 1) / CHUNK_KB;
+
+    if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : -1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(full_bar(s), 128);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 4; ++b) {
+            mbar_init(accf_bar(b), 1);
+            mbar_init(acce_bar(b), 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) {
+        // ---------------- producers: lane = voxel, warp strides over rows ----------------
+        // patch index and in-patch voxel advance incrementally (no 64-bit division in the loop)
+        int64_t pb = q0 / p.kb_per_patch;
+        int vbase = int((q0 - pb * p.kb_per_patch) * BK);
+        const int mvol = int(p.mvol);
+        const int myz = p.my * p.mz;
+        for (int kb = 0; kb < kblocks; ++kb) {
+            if (vbase >= mvol) {
+                vbase = 0;
+                ++pb;
+            }
+            const int v = vbase + lane;
+            vbase += BK;
+            const bool vok = v < mvol;
+            int64_t xoff = 0, goff = 0;
+            if (vok) {
+                const int vx = v / myz;
+                const int r2 = v - vx * myz;
+                const int vy = r2 / p.mz;
+                const int vz = r2 - vy * p.mz;
+                xoff = pb * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
+                goff = pb * int64_t(p.f_out) * p.mvol + v;
+            }
+            const int s = kb % p.stages;
+            const uint32_t ph = uint32_t(kb / p.stages) & 1u;
+            const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
+            const uint32_t a_lo = a_hi + BM * 128u;
+            const uint32_t b_hi = a_lo + BM * 128u;
+            const uint32_t b_lo = b_hi + b_bytes;
+            // gather into registers first (loads overlap the wait for the slot)
+            float av[BM / 4];
+#pragma unroll
+            for (int t = 0; t < BM / 4; ++t) {
+                const int r = warp + 4 * t;
+                const int ro = rowoff[r];
+                av[t] = (vok && ro >= 0) ? __ldg(x + xoff + ro) : 0.f;
+            }
+            float bv[NTMAX / 4];
+#pragma unroll
+            for (int t = 0; t < NTMAX / 4; ++t) {
+                const int n = warp + 4 * t;
+                const int o = n0 + n;
+                bv[t] = (n < p.nt && vok && o < p.f_out) ? __ldg(g + goff + int64_t(o) * p.mvol) : 0.f;
+            }
+            mbar_wait(empty_bar(s), ph ^ 1u);
+#pragma unroll
+            for (int t = 0; t < BM / 4; ++t) {
+                const uint32_t off = sw128_off(uint32_t(warp + 4 * t), uint32_t(lane));
+                const float h = tf32_hi(av[t]);
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_hi + off), "f"(h));
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_lo + off), "f"(tf32_rn(av[t] - h)));
+            }
+#pragma unroll
+            for (int t = 0; t < NTMAX / 4; ++t) {
+                const int n = warp + 4 * t;
+                if (n < p.nt) {
+                    const uint32_t off = sw128_off(uint32_t(n), uint32_t(lane));
+                    const float h = tf32_hi(bv[t]);
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(b_hi + off), "f"(h));
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(b_lo + off), "f"(tf32_rn(bv[t] - h)));
+                }
+            }
+            fence_proxy_async();
+            mbar_arrive(full_bar(s));
+        }
+    } else if (warp < 8) {
+        // ---------------- accumulator drain + epilogue ----------------
+        const int r = threadIdx.x - 128;
+        const uint32_t lane_base = tmem + (uint32_t((warp - 4) * 32) << 16);
+        drain_acc<NTMAX> A;
+        A.zero();
+        for (int ch = 0; ch < nchunks; ++ch) {
+            const int b = ch % p.nbuf;
+            mbar_wait(accf_bar(b), uint32_t(ch / p.nbuf) & 1u);
+            tc_fence_after();
+            A.add(lane_base + uint32_t(b * p.bstride), p.nt);
+            tc_fence_before();
+            mbar_arrive(acce_bar(b));
+        }
+        const int R = r0 + r;
+        if (R < p.mrows) {
+            float* wsz = ws + int64_t(blockIdx.z) * p.f_out * p.mrows;
+#pragma unroll
+            for (int q = 0; q < NTMAX; ++q) {
+                const int o = n0 + q;
+                if (q < p.nt && o < p.f_out) wsz[int64_t(o) * p.mrows + R] = A.acc[q];
+            }
+        }
+    } else {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            const uint32_t idesc = idesc_tf32(BM, p.nt);
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int ch = kb / CHUNK_KB;
+                const int b = ch % p.nbuf;
+                const bool first = (kb % CHUNK_KB) == 0;
+                if (first) {
+                    mbar_wait(acce_bar(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
+                    tc_fence_after();
+                }
+                const uint32_t d = tmem + uint32_t(b * p.bstride);
+                const int s = kb % p.stages;
+                mbar_wait(full_bar(s), uint32_t(kb / p.stages) & 1u);
+                tc_fence_after();
+                const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
+                const uint32_t a_lo = a_hi + BM * 128u;
+                const uint32_t b_hi = a_lo + BM * 128u;
+                const uint32_t b_lo = b_hi + b_bytes;
+#pragma unroll
+                for (int kk = 0; kk < BK / 8; ++kk) {
+                    const uint32_t koff = uint32_t(kk) * 32u;
+                    const uint64_t ah = sw128_desc(a_hi + koff), al = sw128_desc(a_lo + koff);
+                    const uint64_t bh = sw128_desc(b_hi + koff), bl = sw128_desc(b_lo + koff);
+                    mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                    mma_tf32(d, ah, bl, idesc, 1u);
+                    mma_tf32(d, al, bh, idesc, 1u);
+                }
+                mma_commit(empty_bar(s));
+                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit(accf_bar(b));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+__global__ void rowoff_k(int* __restrict__ out, int mrows, int T, int ky, int kz, int sx, int sy, int sz, int ny,
+                         int nz, int64_t nvol) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < mrows; r += gridDim.x * blockDim.x) {
+        const int i = r / T, t = r - i * T;
+        const int wx = t / (ky * kz), wy = (t / kz) % ky, wz = t % kz;
+        out[r] = int(int64_t(i) * nvol + (int64_t(sx * wx) * ny + sy * wy) * nz + sz * wz);
+    }
+}
+
+__global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, int64_t len, float scale,
+                                float* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int64_t s = 0; s < splits; ++s) acc += ws[s * len + i];
+        out[i] = scale * acc;
+    }
+}
+
+template <int NTMAX>
+void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const float* x, const float* g, const int* rowoff, float* ws,
+            const wg_params& p) {
+    auto* k = wgrad_tc_kernel<NTMAX>;
+    ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k<<<grid, THREADS, smem, st>>>(x, g, rowoff, ws, p);
+    launch_check("conv_wgrad_tc");
+}
+
+}  // namespace
+
+void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* g, float* dw, float scale,
+                   scratch& ws) {
+    wg_params p;
+    p.f_in = int(c.f_in);
+    p.f_out = int(c.f_out);
+    p.T = int(c.taps());
+    p.mrows = p.f_in * p.T;
+    const int64_t r16 = ceil_div(c.f_out, 16) * 16;
+    p.nt = int(r16 <= 128 ? r16 : 128);
+    const int ntiles = int(ceil_div(c.f_out, p.nt));
+    const int ntmax = p.nt <= 32 ? 32 : (p.nt <= 64 ? 64 : 128);
+    p.bstride = ntmax;
+    p.nbuf = 4;
+    const int stage = 2 * BM * 128 + 2 * p.nt * 128;
+    p.stages = (216 * 1024) / stage;
+    if (p.stages > 6) p.stages = 6;
+    p.nvol = c.n.vol();
+    p.mvol = c.m.vol();
+    p.ny = int(c.n.y), p.nz = int(c.n.z), p.my = int(c.m.y), p.mz = int(c.m.z);
+    p.kb_per_patch = ceil_div(p.mvol, BK);
+    p.kb_total = p.kb_per_patch * c.B;
+    const int mtiles = int(ceil_div(p.mrows, BM));
+    int64_t splits = ceil_div(int64_t(2 * 148), int64_t(mtiles) * ntiles);
+    const int64_t max_splits = ceil_div(p.kb_total, 4 * CHUNK_KB);
+    if (splits > max_splits) splits = max_splits;
+    if (splits < 1) splits = 1;
+    p.kb_per_split = ceil_div(p.kb_total, splits);
+    splits = ceil_div(p.kb_total, p.kb_per_split);
+
+    const size_t part = size_t(splits) * size_t(c.f_out) * size_t(p.mrows);
+    char* wsp = static_cast<char*>(ws.get(sizeof(float) * part + sizeof(int) * size_t(p.mrows) + 256));
+    float* partials = reinterpret_cast<float*>(wsp);
+    int* rowoff = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(partials + part) + 255) & ~uintptr_t(255));
+    rowoff_k<<<unsigned(ceil_div(p.mrows, 256)), 256, 0, st>>>(rowoff, p.mrows, p.T, int(c.k.y), int(c.k.z),
+                                                               int(c.s.x), int(c.s.y), int(c.s.z), p.ny, p.nz,
+                                                               p.nvol);
+    launch_check("conv_wgrad_tc_rowoff");
+    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 8) + 16 + 1024;
+    const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
+    if (ntmax == 32) launch_wgrad<32>(grid, smem, st, x, g, rowoff, partials, p);
+    else if (ntmax == 64) launch_wgrad<64>(grid, smem, st, x, g, rowoff, partials, p);
+    else launch_wgrad<128>(grid, smem, st, x, g, rowoff, partials, p);
+    const int64_t len = c.f_out * int64_t(p.mrows);
+    int64_t rb = ceil_div(len, 256);
+    if (rb > 148 * 8) rb = 148 * 8;
+    reduce_splits_k<<<unsigned(rb), 256, 0, st>>>(partials, splits, len, scale, dw);
+    launch_check("conv_wgrad_tc_reduce");
+}
+
+}  // namespace znn_gpu
