@@ -1,25 +1,27 @@
 // Direct 3D (dilated) convolution as a tcgen05 implicit GEMM, 3xTF32.
 //
 // GEMM view (one CTA = 128 output voxels x NT output maps):
-//   D[v][n] = sum_k A[v][k] * B[n][k]
-//   fwd   : v = output voxel (b, o_xyz), n = output map, k = (input map c, tap w),
-//           A[v][k] = x[b][c][o + s*w]            (conv_direct.hpp:39-68)
-//   dgrad : v = input voxel (b, t_xyz),  n = input map,  k = (output map o, tap w),
-//           A[v][k] = g[b][o][t - s*w] (0 outside) (conv_direct.hpp:74-101 with reflect)
-// The convergent-edge sum of the reference (engine.hpp:345-353,
-// sum_accumulator.hpp) is the K loop, accumulated in TMEM: no atomics, no
-// locks. fp32 accuracy with tensor cores: every operand is split into
-// hi = tf32(x) and lo = tf32(x - hi) and D += Ahi*Bhi + Ahi*Blo + Alo*Bhi.
+//   D[v][n] = sum_k A[v][k] * B[n][k],   A[v][k] = src[b][c][v + s*w]  (k = c*T + w)
+//   fwd   : src = x, B = W                         (conv_direct.hpp:39-68)
+//   dgrad : src = g zero-haloed by s*(k-1) per side, B[i][o*T + w'] = W[o][i][T-1-w']
+//           i.e. conv_full_direct(g, reflect(k)) (conv_direct.hpp:74-101, engine.hpp:681)
+//           computed as a valid convolution: no bounds tests in the hot loop.
+// The reference's convergent-edge sum (engine.hpp:345-353, sum_accumulator.hpp)
+// is the K loop, accumulated in TMEM: no atomics, no locks. fp32 accuracy on
+// tensor cores: operands split into hi = tf32(x), lo = tf32(x - hi) and
+// D += Ahi*Bhi + Ahi*Blo + Alo*Bhi. TMEM accumulation is cut into chunks of
+// CHUNK_KB K-blocks drained into fp32 registers (tensor-core accumulation
+// error grows with the number of accumulating MMAs).
 //
-// Warp roles (192 threads, 1 CTA per SM):
-//   warps 0-3 : im2col producers for A (one voxel row per thread, 32 k per
-//               K-block, hi/lo split in registers, 128B-swizzled K-major
-//               stores), then the epilogue (TMEM -> regs -> bias + transfer
-//               -> coalesced global stores)
-//   warp 4    : TMA producer for B (pre-split weight panels, SWIZZLE_128B)
-//   warp 5    : TMEM allocator + single-thread tcgen05.mma issuer
-// mbarrier ring: full[s] (128 producer arrivals + TMA tx bytes), empty[s]
-// (tcgen05.commit), done (final commit -> epilogue).
+// Warp roles (384 threads, 1 CTA per SM; warps 10-11 idle):
+//   warps 0-7 : im2col producers for A: thread = one voxel row, warps 0-3
+//               k[0,16) and warps 4-7 k[16,32) of every 32-wide K-block; hi/lo
+//               split in registers, 128B-swizzled K-major st.shared.v4
+//               and drain finished TMEM chunks: warp w owns lane quarter
+//               w % 4, warps 0-3 columns [0, NT/2) and 4-7 [NT/2, NT); then
+//               the epilogue (bias + transfer, coalesced stores)
+//   warp 8    : TMA producer for B (pre-split weight panels, SWIZZLE_128B)
+//   warp 9    : TMEM allocator + single-thread tcgen05.mma issuer
 #include <cuda.h>
 
 #include "ops.hpp"
@@ -31,9 +33,9 @@ namespace {
 
 using namespace znn_tc;
 
-constexpr int THREADS = 320;     // 4 producer + 4 drain/epilogue + TMA + MMA warps
+constexpr int THREADS = 384;  // registers are granted per 4-warp group
 constexpr uint32_t TMEM_COLS = 512;
-constexpr int CHUNK_KB = 8;      // K-blocks accumulated per TMEM buffer before a drain
+constexpr int CHUNK_KB = 8;
 
 struct tc_params {
     int f_src;        // channels of the im2col source
@@ -50,11 +52,11 @@ struct tc_params {
     int64_t src_vol;
 };
 
-template <bool DGRAD, int NTMAX>
+template <int NTMAX>
 __global__ void __launch_bounds__(THREADS, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
-               const float* __restrict__ src, const int4* __restrict__ ktab,
-               float* __restrict__ out, const float* __restrict__ bias, int act, tc_params p) {
+               const float* __restrict__ src, const int* __restrict__ koff, float* __restrict__ out,
+               const float* __restrict__ bias, int act, tc_params p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -64,8 +66,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     const uint32_t bar_base = base + uint32_t(p.stages) * stage_bytes;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
     auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(p.stages + s); };
-    auto accf_bar = [&](int b) { return bar_base + 8u * uint32_t(2 * p.stages + b); };
-    auto acce_bar = [&](int b) { return bar_base + 8u * uint32_t(2 * p.stages + 4 + b); };
+    const uint32_t accf0 = bar_base + 8u * uint32_t(2 * p.stages);
+    const uint32_t acce0 = accf0 + 32u;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 8));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -75,12 +77,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 128 + 1);
+            mbar_init(full_bar(s), 256 + 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 4; ++b) {
-            mbar_init(accf_bar(b), 1);
-            mbar_init(acce_bar(b), 128);
+            mbar_init(accf0 + 8u * b, 1);
+            mbar_init(acce0 + 8u * b, 256);
         }
         fence_barrier_init();
     }
@@ -90,61 +92,54 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
-        // ---------------- im2col producer (one voxel row per thread) ----------------
-        const int r = threadIdx.x;
+    if (warp < 8) {
+        // ---------------- im2col producers ----------------
+        const int r = threadIdx.x & 127;
+        const int half = threadIdx.x >> 7;  // which 16 of the 32 k of a block
+        constexpr int NH = NTMAX / 2;
+        const int col0 = half * NH;
+        const int ncols = max(0, min(NH, p.nt - col0));
+        chunk_drainer<NH> D;
+        D.init(accf0, acce0, tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col0), p.nbuf, p.bstride, ncols,
+               nchunks);
         const int64_t v = m0 + r;
         const bool vok = v < p.rows;
-        int64_t sbase = 0;
-        int tx = 0, ty = 0, tz = 0;
+        const float* sp = src;
         if (vok) {
             const int64_t b = v / p.vox_out;
             const int64_t rem = v - b * p.vox_out;
-            tx = int(rem / (int64_t(p.oy) * p.oz));
-            ty = int((rem / p.oz) % p.oy);
-            tz = int(rem % p.oz);
-            sbase = b * int64_t(p.f_src) * p.src_vol;
-            if (!DGRAD) sbase += (int64_t(tx) * p.sy + ty) * p.sz + tz;
+            const int tx = int(rem / (int64_t(p.oy) * p.oz));
+            const int ty = int((rem / p.oz) % p.oy);
+            const int tz = int(rem % p.oz);
+            sp = src + b * int64_t(p.f_src) * p.src_vol + (int64_t(tx) * p.sy + ty) * p.sz + tz;
         }
         const uint32_t row_off = uint32_t(r) * 128u;
         const uint32_t sw = uint32_t(r & 7);
-        const float* sp = src + sbase;  // 32-bit offsets from here on (map * f_src < 2^31)
-        const int syz = p.sy * p.sz;
-        const int tlin = tx * syz + ty * p.sz + tz;
         for (int kb = 0; kb < p.kblocks; ++kb) {
             const int s = kb % p.stages;
             const uint32_t ph = uint32_t(kb / p.stages) & 1u;
-            float vals[BK];
-            const int4* tb = ktab + kb * BK;
+            const int4* tb = reinterpret_cast<const int4*>(koff + kb * BK + 16 * half);
+            float vals[16];
 #pragma unroll
-            for (int j = 0; j < BK; ++j) {
-                const int4 e = __ldg(tb + j);
-                float val = 0.f;
-                if (vok) {
-                    if (!DGRAD) {
-                        val = __ldg(sp + e.x);
-                    } else {
-                        // e = {map offset, s*wx, s*wy, s*wz}; in-bounds test per axis
-                        const int gx = tx - e.y, gy = ty - e.z, gz = tz - e.w;
-                        if (unsigned(gx) < unsigned(p.sx) && unsigned(gy) < unsigned(p.sy) &&
-                            unsigned(gz) < unsigned(p.sz))
-                            val = __ldg(sp + (e.x + tlin));
-                    }
-                }
-                vals[j] = val;
+            for (int q = 0; q < 4; ++q) {
+                const int4 e = __ldg(tb + q);
+                vals[4 * q + 0] = vok ? __ldg(sp + e.x) : 0.f;
+                vals[4 * q + 1] = vok ? __ldg(sp + e.y) : 0.f;
+                vals[4 * q + 2] = vok ? __ldg(sp + e.z) : 0.f;
+                vals[4 * q + 3] = vok ? __ldg(sp + e.w) : 0.f;
             }
-            mbar_wait(empty_bar(s), ph ^ 1u);
+            D.wait_stage(empty_bar(s), ph ^ 1u);
             const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
             const uint32_t a_lo = a_hi + BM * 128u;
 #pragma unroll
-            for (int c = 0; c < BK / 4; ++c) {
+            for (int c = 0; c < 4; ++c) {
                 float h[4], l[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     h[q] = tf32_hi(vals[4 * c + q]);
                     l[q] = tf32_rn(vals[4 * c + q] - h[q]);
                 }
-                const uint32_t off = row_off + ((uint32_t(c) ^ sw) << 4);
+                const uint32_t off = row_off + (((uint32_t(4 * half + c)) ^ sw) << 4);
                 asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_hi + off), "f"(h[0]), "f"(h[1]),
                              "f"(h[2]), "f"(h[3]));
                 asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_lo + off), "f"(l[0]), "f"(l[1]),
@@ -152,33 +147,20 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
             }
             fence_proxy_async();
             mbar_arrive(full_bar(s));
+            D.poll();
         }
-    } else if (warp < 8) {
-        // ---------------- accumulator drain + epilogue ----------------
-        const int r = threadIdx.x - 128;
-        const uint32_t lane_base = tmem + (uint32_t((warp - 4) * 32) << 16);
-        drain_acc<NTMAX> A;
-        A.zero();
-        for (int ch = 0; ch < nchunks; ++ch) {
-            const int b = ch % p.nbuf;
-            mbar_wait(accf_bar(b), uint32_t(ch / p.nbuf) & 1u);
-            tc_fence_after();
-            A.add(lane_base + uint32_t(b * p.bstride), p.nt);
-            tc_fence_before();
-            mbar_arrive(acce_bar(b));
-        }
-        const int64_t v = m0 + r;
-        if (v < p.rows) {
+        // ---------------- remaining drains + epilogue (this warp's columns) ----------------
+        D.finish();
+        if (vok) {
             const int64_t bb = v / p.vox_out;
             const int64_t vin = v - bb * p.vox_out;
-            const int64_t obase = bb * int64_t(p.n_real) * p.vox_out + vin;
+            float* op = out + bb * int64_t(p.n_real) * p.vox_out + vin;
 #pragma unroll
-            for (int q = 0; q < NTMAX; ++q) {
-                const int n = n0 + q;
-                if (q < p.nt && n < p.n_real) {
-                    float val = A.acc[q];
-                    if (!DGRAD) val = act_value(act, val + (bias ? __ldg(bias + n) : 0.f));
-                    out[obase + int64_t(n) * p.vox_out] = val;
+            for (int q = 0; q < NH; ++q) {
+                const int n = n0 + col0 + q;
+                if (q < ncols && n < p.n_real) {
+                    const float val = act_value(act, D.A.acc[q] + (bias ? __ldg(bias + n) : 0.f));
+                    op[int64_t(n) * p.vox_out] = val;
                 }
             }
         }
@@ -195,7 +177,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                 tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), kb * BK, n0);
             }
         }
-    } else {
+    } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(BM, p.nt);
@@ -204,29 +186,28 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                 const int b = ch % p.nbuf;
                 const bool first = (kb % CHUNK_KB) == 0;
                 if (first) {
-                    mbar_wait(acce_bar(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
+                    mbar_wait(acce0 + 8u * uint32_t(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
                     tc_fence_after();
                 }
                 const uint32_t d = tmem + uint32_t(b * p.bstride);
                 const int s = kb % p.stages;
-                const uint32_t ph = uint32_t(kb / p.stages) & 1u;
-                mbar_wait(full_bar(s), ph);
+                mbar_wait(full_bar(s), uint32_t(kb / p.stages) & 1u);
                 tc_fence_after();
                 const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
                 const uint32_t a_lo = a_hi + BM * 128u;
-                const uint32_t b_hi = a_hi + 2u * BM * 128u;
+                const uint32_t b_hi = a_lo + BM * 128u;
                 const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
-                    const uint32_t koff = uint32_t(kk) * 32u;  // 8 tf32 = 32 B along K
-                    const uint64_t ah = sw128_desc(a_hi + koff), al = sw128_desc(a_lo + koff);
-                    const uint64_t bh = sw128_desc(b_hi + koff), bl = sw128_desc(b_lo + koff);
+                    const uint32_t ko = uint32_t(kk) * 32u;  // 8 tf32 = 32 B along K
+                    const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
+                    const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
                     mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
                     mma_tf32(d, ah, bl, idesc, 1u);
                     mma_tf32(d, al, bh, idesc, 1u);
                 }
                 mma_commit(empty_bar(s));
-                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == p.kblocks - 1) mma_commit(accf_bar(b));
+                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == p.kblocks - 1) mma_commit(accf0 + 8u * uint32_t(b));
             }
         }
     }
@@ -240,20 +221,20 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
 }
 
 // Weight panels for the B operand, split hi/lo, zero padded to [npad][kpad].
-//   fwd  : B[n][k] = W[n][k]                (k = c*T + w)
-//   dgrad: B[n][k] = W[o][n][w], k = o*T + w
-__global__ void split_weights_k(const float* __restrict__ w, int n_real, int other, int T, int K, int npad,
-                                int kpad, int dgrad, float* __restrict__ hi, float* __restrict__ lo) {
+//   mode 0 (fwd)  : B[n][k] = W[n][k]                       (k = c*T + w)
+//   mode 1 (dgrad): B[n][k] = W[o][n][T-1-w'], k = o*T + w'  (transposed, reflected)
+__global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_in, int T, int K, int npad,
+                                int kpad, int mode, float* __restrict__ hi, float* __restrict__ lo) {
     const int64_t total = int64_t(npad) * kpad;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int n = int(i / kpad), k = int(i - int64_t(n) * kpad);
         float v = 0.f;
         if (n < n_real && k < K) {
-            if (!dgrad) {
+            if (mode == 0) {
                 v = w[int64_t(n) * K + k];
             } else {
                 const int o = k / T, t = k - o * T;
-                v = w[(int64_t(o) * other + n) * T + t];
+                v = w[(int64_t(o) * f_in + n) * T + (T - 1 - t)];
             }
         }
         const float h = tf32_hi(v);
@@ -262,26 +243,36 @@ __global__ void split_weights_k(const float* __restrict__ w, int n_real, int oth
     }
 }
 
-// K table: fwd {c*src_vol + tap offset, 0,0,0}; dgrad {c*src_vol, sx*wx, sy*wy, sz*wz};
-// padded k: fwd -> offset 0 (weights are zero there), dgrad -> out of bounds.
-__global__ void ktab_k(int4* __restrict__ tab, int K, int kpad, int T, int ky, int kz, int sx, int sy, int sz,
-                       int64_t src_vol, int src_y, int src_z, int dgrad) {
+// im2col offsets: koff[k] = c*src_vol + linear(s*w) in source dims; padded
+// k -> 0 (their weights are zero).
+__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int T, int ky, int kz, int sx, int sy, int sz,
+                       int64_t src_vol, int src_y, int src_z) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
-        int4 e = make_int4(0, 0, 0, 0);
+        int e = 0;
         if (k < K) {
             const int c = k / T, t = k - c * T;
             const int wx = t / (ky * kz), wy = (t / kz) % ky, wz = t % kz;
-            if (!dgrad) {
-                e.x = int(int64_t(c) * src_vol + (int64_t(sx * wx) * src_y + sy * wy) * src_z + sz * wz);
-            } else {
-                // map offset minus the linear tap shift: address = e.x + linear(t)
-                e = make_int4(int(int64_t(c) * src_vol - (int64_t(sx * wx) * src_y + sy * wy) * src_z - sz * wz),
-                              sx * wx, sy * wy, sz * wz);
-            }
-        } else if (dgrad) {
-            e = make_int4(0, 1 << 29, 1 << 29, 1 << 29);
+            e = int(int64_t(c) * src_vol + (int64_t(sx * wx) * src_y + sy * wy) * src_z + sz * wz);
         }
         tab[k] = e;
+    }
+}
+
+// g [maps][m] -> gp [maps][m + 2P] with a zero halo of P = s*(k-1) per side.
+__global__ void pad_halo_k(const float* __restrict__ g, int64_t maps, int mx, int my, int mz, int px, int py, int pz,
+                           float* __restrict__ gp) {
+    const int gx = mx + 2 * px, gy = my + 2 * py, gz = mz + 2 * pz;
+    const int64_t pv = int64_t(gx) * gy * gz;
+    const int64_t mv = int64_t(mx) * my * mz;
+    const int64_t total = maps * pv;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t map = i / pv;
+        const int r = int(i - map * pv);
+        const int x = r / (gy * gz) - px, y = (r / gz) % gy - py, z = r % gz - pz;
+        float v = 0.f;
+        if (unsigned(x) < unsigned(mx) && unsigned(y) < unsigned(my) && unsigned(z) < unsigned(mz))
+            v = g[map * mv + (int64_t(x) * my + y) * mz + z];
+        gp[i] = v;
     }
 }
 
@@ -314,59 +305,42 @@ CUtensorMap make_panel_map(const float* ptr, int kpad, int rows, int nt) {
     return m;
 }
 
-int pick_nt(int64_t n_real) {
-    const int64_t r16 = ceil_div(n_real, 16) * 16;
-    return int(r16 <= 128 ? r16 : 128);
-}
-
-int pick_stages(int nt) {
-    const int stage = 2 * BM * 128 + 2 * nt * 128;
-    int s = (220 * 1024) / stage;
-    if (s > 6) s = 6;
-    return s;
-}
-
-size_t smem_bytes(int nt, int stages) {
-    return size_t(stages) * size_t(2 * BM * 128 + 2 * nt * 128) + 8 * size_t(2 * stages + 8) + 16 + 1024;
-}
-
-template <bool DGRAD, int NTMAX>
+template <int NTMAX>
 void launch_kernel(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mhi, const CUtensorMap& mlo,
-                   const float* srcp, const int4* tab, float* outp, const float* bias, int act, const tc_params& p) {
-    auto* k = conv_tc_kernel<DGRAD, NTMAX>;
+                   const float* srcp, const int* tab, float* outp, const float* bias, int act, const tc_params& p,
+                   const char* what) {
+    auto* k = conv_tc_kernel<NTMAX>;
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k<<<grid, THREADS, smem, st>>>(mhi, mlo, srcp, tab, outp, bias, act, p);
-    launch_check(DGRAD ? "conv_dgrad_tc" : "conv_fwd_tc");
+    launch_check(what);
 }
 
-void launch_tc(cudaStream_t st, bool dgrad, const conv_shape& c, const float* srcp, const float* w,
-               const float* bias, int act, float* outp, scratch& ws) {
-    const int T = int(c.taps());
-    const int f_src = int(dgrad ? c.f_out : c.f_in);
-    const int n_real = int(dgrad ? c.f_in : c.f_out);
+// One valid convolution src[B][f_src][sd] -> out[B][n_real][sd - s(k-1)] on
+// the tensor cores. wmode selects how the B panel is built from w.
+void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w, dims3 sd, dims3 k, dims3 s,
+                  const float* srcp, const float* w, int wmode, const float* bias, int act, float* outp,
+                  char* wsp, const char* what) {
+    const int T = int(k.vol());
     const int K = f_src * T;
     const int kpad = int(ceil_div(K, BK) * BK);
-    const int nt = pick_nt(n_real);
+    const int64_t r16 = ceil_div(n_real, 16) * 16;
+    const int nt = int(r16 <= 128 ? r16 : 128);
     const int ntiles = int(ceil_div(n_real, nt));
     const int npad = ntiles * nt;
-    const dims3 src = dgrad ? c.m : c.n;
-    const dims3 od = dgrad ? c.n : c.m;
+    const dims3 od{sd.x - s.x * (k.x - 1), sd.y - s.y * (k.y - 1), sd.z - s.z * (k.z - 1)};
 
     const size_t panel = size_t(npad) * size_t(kpad);
-    char* wsp = static_cast<char*>(ws.get(sizeof(float) * panel * 2 + sizeof(int4) * size_t(kpad) + 256));
     float* hi = reinterpret_cast<float*>(wsp);
     float* lo = hi + panel;
-    int4* tab = reinterpret_cast<int4*>((reinterpret_cast<uintptr_t>(lo + panel) + 255) & ~uintptr_t(255));
+    int* tab = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(lo + panel) + 255) & ~uintptr_t(255));
 
     int64_t blocks = ceil_div(int64_t(panel), 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    split_weights_k<<<unsigned(blocks), 256, 0, st>>>(w, n_real, int(c.f_in), T, K, npad, kpad, dgrad ? 1 : 0, hi,
-                                                      lo);
+    split_weights_k<<<unsigned(blocks), 256, 0, st>>>(w, n_real, f_in_w, T, K, npad, kpad, wmode, hi, lo);
     launch_check("conv_tc_split_weights");
-    ktab_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, T, int(c.k.y), int(c.k.z), int(c.s.x),
-                                                           int(c.s.y), int(c.s.z), src.vol(), int(src.y),
-                                                           int(src.z), dgrad ? 1 : 0);
-    launch_check("conv_tc_ktab");
+    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, T, int(k.y), int(k.z), int(s.x), int(s.y),
+                                                           int(s.z), sd.vol(), int(sd.y), int(sd.z));
+    launch_check("conv_tc_koff");
 
     const CUtensorMap mhi = make_panel_map(hi, kpad, npad, nt);
     const CUtensorMap mlo = make_panel_map(lo, kpad, npad, nt);
@@ -375,43 +349,63 @@ void launch_tc(cudaStream_t st, bool dgrad, const conv_shape& c, const float* sr
     p.n_real = n_real;
     p.nt = nt;
     p.kblocks = kpad / BK;
-    p.stages = pick_stages(nt);
+    const int stage = 2 * BM * 128 + 2 * nt * 128;
+    p.stages = (216 * 1024) / stage;
+    if (p.stages > 6) p.stages = 6;
     const int ntmax = nt <= 32 ? 32 : (nt <= 64 ? 64 : 128);
     p.bstride = ntmax;
     p.nbuf = 4;  // 4 x NTMAX <= 512 TMEM columns
     p.vox_out = od.vol();
-    p.rows = c.B * p.vox_out;
+    p.rows = Bn * p.vox_out;
     p.ox = int(od.x), p.oy = int(od.y), p.oz = int(od.z);
-    p.sx = int(src.x), p.sy = int(src.y), p.sz = int(src.z);
-    p.src_vol = src.vol();
-    const size_t smem = smem_bytes(nt, p.stages);
-    const dim3 grid(unsigned(ceil_div(p.rows, BM)), unsigned(ntiles));
-    if (dgrad) {
-        if (ntmax == 32) launch_kernel<true, 32>(grid, smem, st, mhi, mlo, srcp, tab, outp, nullptr, 3, p);
-        else if (ntmax == 64) launch_kernel<true, 64>(grid, smem, st, mhi, mlo, srcp, tab, outp, nullptr, 3, p);
-        else launch_kernel<true, 128>(grid, smem, st, mhi, mlo, srcp, tab, outp, nullptr, 3, p);
-    } else {
-        if (ntmax == 32) launch_kernel<false, 32>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p);
-        else if (ntmax == 64) launch_kernel<false, 64>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p);
-        else launch_kernel<false, 128>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p);
-    }
+    p.sx = int(sd.x), p.sy = int(sd.y), p.sz = int(sd.z);
+    p.src_vol = sd.vol();
+    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 8) + 16 + 1024;
+    const dim3 grid{unsigned(ceil_div(p.rows, BM)), unsigned(ntiles), 1u};
+    if (ntmax == 32) launch_kernel<32>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+    else if (ntmax == 64) launch_kernel<64>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+    else launch_kernel<128>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+}
+
+size_t panel_bytes(int f_src, int n_real, int64_t T) {
+    const int64_t kpad = ceil_div(int64_t(f_src) * T, BK) * BK;
+    const int64_t npad = ceil_div(n_real, 16) * 16 + 128;
+    return sizeof(float) * size_t(npad * kpad) * 2 + sizeof(int) * size_t(kpad) + 512;
 }
 
 }  // namespace
 
 bool conv_tc_supported(const conv_shape& c, int pass) {
-    if (pass == 0) return c.f_out >= 16 && c.n.vol() < (int64_t(1) << 31) && c.f_in * c.taps() < (1 << 30);
-    if (pass == 1) return c.f_in >= 16 && c.m.vol() < (int64_t(1) << 31) && c.f_out * c.taps() < (1 << 30);
+    if (pass == 0) return c.f_out >= 16 && c.f_in * c.n.vol() < (int64_t(1) << 31);
+    if (pass == 1) {
+        const int64_t pv = (c.m.x + 2 * c.s.x * (c.k.x - 1)) * (c.m.y + 2 * c.s.y * (c.k.y - 1)) *
+                           (c.m.z + 2 * c.s.z * (c.k.z - 1));
+        return c.f_in >= 16 && c.f_out * pv < (int64_t(1) << 31);
+    }
     return c.f_out >= 16 && c.n.vol() * c.f_in < (int64_t(1) << 31);
 }
 
 void conv_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* w, const float* bias, int act,
                  float* y, scratch& ws) {
-    launch_tc(st, false, c, x, w, bias, act, y, ws);
+    char* wsp = static_cast<char*>(ws.get(panel_bytes(int(c.f_in), int(c.f_out), c.taps())));
+    launch_valid(st, c.B, int(c.f_in), int(c.f_out), int(c.f_in), c.n, c.k, c.s, x, w, 0, bias, act, y, wsp,
+                 "conv_fwd_tc");
 }
 
 void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const float* w, float* dx, scratch& ws) {
-    launch_tc(st, true, c, g, w, nullptr, 3, dx, ws);
+    const dims3 P{c.s.x * (c.k.x - 1), c.s.y * (c.k.y - 1), c.s.z * (c.k.z - 1)};
+    const dims3 gd{c.m.x + 2 * P.x, c.m.y + 2 * P.y, c.m.z + 2 * P.z};
+    const size_t gbytes = sizeof(float) * size_t(c.B * c.f_out * gd.vol());
+    const size_t gpad = (gbytes + 1023) & ~size_t(1023);
+    char* wsp = static_cast<char*>(ws.get(gpad + panel_bytes(int(c.f_out), int(c.f_in), c.taps())));
+    float* gp = reinterpret_cast<float*>(wsp);
+    int64_t blocks = ceil_div(c.B * c.f_out * gd.vol(), 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    pad_halo_k<<<unsigned(blocks), 256, 0, st>>>(g, c.B * c.f_out, int(c.m.x), int(c.m.y), int(c.m.z), int(P.x),
+                                                  int(P.y), int(P.z), gp);
+    launch_check("conv_dgrad_tc_pad");
+    launch_valid(st, c.B, int(c.f_out), int(c.f_in), int(c.f_in), gd, c.k, c.s, gp, w, 1, nullptr, 3, dx,
+                 wsp + gpad, "conv_dgrad_tc");
 }
 
 }  // namespace znn_gpu

@@ -10,8 +10,9 @@
 // contiguous K range (split-K); partial tiles land in a workspace
 // [split][o][R] and a fixed-order reduction sums them (deterministic).
 //
-// Warps: 0-3 operand producers, 4-7 accumulator drain + epilogue, 8 TMEM
-// alloc + MMA issuer.
+// Warps: 0-7 operand producers that also drain finished TMEM chunks (warp w:
+// lane quarter w % 4, column half w / 4) and run the epilogue; 8 TMEM alloc +
+// MMA issuer; 9-11 idle (registers are granted per 4-warp group).
 #include <cuda.h>
 
 #include "ops.hpp"
@@ -23,7 +24,7 @@ namespace {
 
 using namespace znn_tc;
 
-constexpr int THREADS = 288;
+constexpr int THREADS = 384;  // registers are granted per 4-warp group
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CHUNK_KB = 8;
 
@@ -65,12 +66,12 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
     if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : -1;
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 128);
+            mbar_init(full_bar(s), 256);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf_bar(b), 1);
-            mbar_init(acce_bar(b), 128);
+            mbar_init(acce_bar(b), 256);
         }
         fence_barrier_init();
     }
@@ -80,8 +81,14 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
+    if (warp < 8) {
         // ---------------- producers: lane = voxel, warp strides over rows ----------------
+        constexpr int NH = NTMAX / 2;
+        const int col0 = (warp >> 2) * NH;
+        const int ncols = max(0, min(NH, p.nt - col0));
+        chunk_drainer<NH> D;
+        D.init(accf_bar(0), acce_bar(0), tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col0), p.nbuf,
+               p.bstride, ncols, nchunks);
         // patch index and in-patch voxel advance incrementally (no 64-bit division in the loop)
         int64_t pb = q0 / p.kb_per_patch;
         int vbase = int((q0 - pb * p.kb_per_patch) * BK);
@@ -95,14 +102,15 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
             const int v = vbase + lane;
             vbase += BK;
             const bool vok = v < mvol;
-            int64_t xoff = 0, goff = 0;
+            const float* xp = x;
+            const float* gp = g;
             if (vok) {
                 const int vx = v / myz;
                 const int r2 = v - vx * myz;
                 const int vy = r2 / p.mz;
                 const int vz = r2 - vy * p.mz;
-                xoff = pb * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
-                goff = pb * int64_t(p.f_out) * p.mvol + v;
+                xp = x + pb * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
+                gp = g + pb * int64_t(p.f_out) * p.mvol + v;
             }
             const int s = kb % p.stages;
             const uint32_t ph = uint32_t(kb / p.stages) & 1u;
@@ -111,31 +119,30 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
             const uint32_t b_hi = a_lo + BM * 128u;
             const uint32_t b_lo = b_hi + b_bytes;
             // gather into registers first (loads overlap the wait for the slot)
-            float av[BM / 4];
+            float av[BM / 8];
 #pragma unroll
-            for (int t = 0; t < BM / 4; ++t) {
-                const int r = warp + 4 * t;
-                const int ro = rowoff[r];
-                av[t] = (vok && ro >= 0) ? __ldg(x + xoff + ro) : 0.f;
+            for (int t = 0; t < BM / 8; ++t) {
+                const int ro = rowoff[warp + 8 * t];
+                av[t] = (vok && ro >= 0) ? __ldg(xp + ro) : 0.f;
             }
-            float bv[NTMAX / 4];
+            float bv[NTMAX / 8];
 #pragma unroll
-            for (int t = 0; t < NTMAX / 4; ++t) {
-                const int n = warp + 4 * t;
+            for (int t = 0; t < NTMAX / 8; ++t) {
+                const int n = warp + 8 * t;
                 const int o = n0 + n;
-                bv[t] = (n < p.nt && vok && o < p.f_out) ? __ldg(g + goff + int64_t(o) * p.mvol) : 0.f;
+                bv[t] = (n < p.nt && vok && o < p.f_out) ? __ldg(gp + int64_t(o) * p.mvol) : 0.f;
             }
-            mbar_wait(empty_bar(s), ph ^ 1u);
+            D.wait_stage(empty_bar(s), ph ^ 1u);
 #pragma unroll
-            for (int t = 0; t < BM / 4; ++t) {
-                const uint32_t off = sw128_off(uint32_t(warp + 4 * t), uint32_t(lane));
+            for (int t = 0; t < BM / 8; ++t) {
+                const uint32_t off = sw128_off(uint32_t(warp + 8 * t), uint32_t(lane));
                 const float h = tf32_hi(av[t]);
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_hi + off), "f"(h));
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_lo + off), "f"(tf32_rn(av[t] - h)));
             }
 #pragma unroll
-            for (int t = 0; t < NTMAX / 4; ++t) {
-                const int n = warp + 4 * t;
+            for (int t = 0; t < NTMAX / 8; ++t) {
+                const int n = warp + 8 * t;
                 if (n < p.nt) {
                     const uint32_t off = sw128_off(uint32_t(n), uint32_t(lane));
                     const float h = tf32_hi(bv[t]);
@@ -145,31 +152,20 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
             }
             fence_proxy_async();
             mbar_arrive(full_bar(s));
+            D.poll();
         }
-    } else if (warp < 8) {
-        // ---------------- accumulator drain + epilogue ----------------
-        const int r = threadIdx.x - 128;
-        const uint32_t lane_base = tmem + (uint32_t((warp - 4) * 32) << 16);
-        drain_acc<NTMAX> A;
-        A.zero();
-        for (int ch = 0; ch < nchunks; ++ch) {
-            const int b = ch % p.nbuf;
-            mbar_wait(accf_bar(b), uint32_t(ch / p.nbuf) & 1u);
-            tc_fence_after();
-            A.add(lane_base + uint32_t(b * p.bstride), p.nt);
-            tc_fence_before();
-            mbar_arrive(acce_bar(b));
-        }
-        const int R = r0 + r;
+        // ---------------- remaining drains + epilogue (this warp's columns) ----------------
+        D.finish();
+        const int R = r0 + (threadIdx.x & 127);
         if (R < p.mrows) {
             float* wsz = ws + int64_t(blockIdx.z) * p.f_out * p.mrows;
 #pragma unroll
-            for (int q = 0; q < NTMAX; ++q) {
-                const int o = n0 + q;
-                if (q < p.nt && o < p.f_out) wsz[int64_t(o) * p.mrows + R] = A.acc[q];
+            for (int q = 0; q < NH; ++q) {
+                const int o = n0 + col0 + q;
+                if (q < ncols && o < p.f_out) wsz[int64_t(o) * p.mrows + R] = D.A.acc[q];
             }
         }
-    } else {
+    } else if (warp == 8) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(BM, p.nt);

@@ -32,6 +32,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// non-blocking probe of a phase (for warps that poll while doing other work)
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -130,6 +142,55 @@ struct drain_acc {
                 for (int q = 0; q < 16; ++q) acc[c0 + q] += v[q];
             }
         }
+    }
+};
+
+// Drain state for a producer warp that also owns a quarter of the TMEM
+// lanes: chunks are drained opportunistically (poll) between K-blocks and
+// while waiting for a free smem stage, so a producer can never deadlock
+// against an MMA warp that waits for a drained buffer. Warp-uniform control
+// flow: the readiness test is broadcast from lane 0 and every lane then does
+// its own (immediately successful) acquire wait.
+// Every producer warp drains a column range [col0, col0+ncols) of its TMEM
+// lane quarter (warp % 4), so two warps share one quarter and each keeps only
+// NH accumulators in registers.
+template <int NH>
+struct chunk_drainer {
+    drain_acc<NH> A;
+    int next = 0;
+    uint32_t accf0, acce0, lane_base;
+    int nbuf, bstride, ncols, nchunks;
+
+    __device__ __forceinline__ void init(uint32_t f0, uint32_t e0, uint32_t lb, int nb, int bs, int nc_cols,
+                                         int nc) {
+        accf0 = f0, acce0 = e0, lane_base = lb, nbuf = nb, bstride = bs, ncols = nc_cols, nchunks = nc;
+        next = 0;
+        A.zero();
+    }
+    __device__ __forceinline__ void drain_one() {
+        const int b = next % nbuf;
+        mbar_wait(accf0 + 8u * uint32_t(b), uint32_t(next / nbuf) & 1u);
+        tc_fence_after();
+        if (ncols > 0) A.add(lane_base + uint32_t(b * bstride), ncols);
+        tc_fence_before();
+        mbar_arrive(acce0 + 8u * uint32_t(b));
+        ++next;
+    }
+    __device__ __forceinline__ void poll() {
+        while (next < nchunks) {
+            const int b = next % nbuf;
+            const bool ready =
+                __shfl_sync(0xffffffffu, mbar_test(accf0 + 8u * uint32_t(b), uint32_t(next / nbuf) & 1u) ? 1 : 0, 0);
+            if (!ready) break;
+            drain_one();
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        while (next < nchunks) drain_one();
+    }
+    // wait for a free smem stage, draining finished chunks meanwhile
+    __device__ __forceinline__ void wait_stage(uint32_t empty, uint32_t parity) {
+        while (!__all_sync(0xffffffffu, mbar_test(empty, parity))) poll();
     }
 };
 
