@@ -2,7 +2,8 @@
 
 Preferred: the reference's own task-parallel engine (engine<float>,
 engine.hpp:65-254) compiled from /root/reference by oracle/ref/build.sh into
-oracle/_ref/znn_ref_bench (kind "reference"), run on all host cores.
+oracle/_ref/znn_ref (kind "reference"), run on all host cores; configs whose
+round exceeds the budget report the per-edge estimate (see znn_ref.cpp).
 Fallback: the plain-C double oracle (kind "port", 1 core), timed on a
 bounded per-edge sample of every conv layer and extrapolated by edge count.
 """
@@ -16,7 +17,7 @@ import time
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-REF_BIN = os.path.join(_HERE, "_ref", "znn_ref_bench")
+REF_BIN = os.path.join(_HERE, "_ref", "znn_ref")
 
 
 def physical_cores():
@@ -37,19 +38,34 @@ def physical_cores():
     return os.cpu_count() or 1
 
 
-def run(cfg, budget_s=20.0):
+def run(cfg, budget_s=20.0, mode=None):
     if os.path.exists(REF_BIN):
-        return run_reference_engine(cfg, budget_s)
+        return run_reference_engine(cfg, budget_s, mode or ("auto" if cfg.engine == "auto" else "direct"))
     return run_port(cfg, budget_s)
 
 
-def run_reference_engine(cfg, budget_s):
+def run_reference_engine(cfg, budget_s, mode="direct"):
     threads = physical_cores()
     spec_path = os.path.join("/tmp", f"znn_ref_{cfg.name}_{os.getpid()}.spec")
     with open(spec_path, "w") as f:
         f.write(cfg.netspec())
     od = ",".join(str(v) for v in cfg.out_dims)
-    cmd = [REF_BIN, spec_path, od, str(threads), str(budget_s), "direct"]
+    # predicted round time from the reference's own per-edge task bodies
+    est = subprocess.run([REF_BIN, "estimate", spec_path, od, str(threads)], capture_output=True, text=True,
+                         timeout=900)
+    if est.returncode == 0:
+        e = json.loads(est.stdout.strip().splitlines()[-1])
+        if e["round_seconds"] * 2.0 > budget_s:
+            os.unlink(spec_path)
+            out_vox = int(np.prod(cfg.out_dims))
+            return {"value": out_vox / e["round_seconds"], "unit": "voxels/s", "cores": threads,
+                    "kind": "reference", "dtype": "f32", "estimated": True,
+                    "sample": f"one full {cfg.name} round exceeds the {budget_s:.0f}s budget: every edge signature's "
+                              f"reference task bodies (conv_valid_direct + conv_full_direct(reflect) + "
+                              f"kernel_gradient_direct, transfer/filter/pool fwd+bwd; engine.hpp:582-829) timed "
+                              f"single-threaded (median of 3), summed over all {cfg.name} edges and divided by "
+                              f"{threads} threads (the paper's linear speedup, optimistic for the CPU)"}
+    cmd = [REF_BIN, "bench", spec_path, od, str(threads), str(budget_s), mode]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=budget_s * 20 + 600)
     os.unlink(spec_path)
     if out.returncode != 0:
@@ -59,9 +75,10 @@ def run_reference_engine(cfg, budget_s):
     value = out_vox * res["rounds"] / res["seconds"]
     return {"value": value, "unit": "voxels/s", "cores": threads, "kind": "reference",
             "dtype": "f32",
-            "sample": f"{res['rounds']} measured round(s) (1 patch each, after {res['warmup']} warm-up) of "
-                      f"the reference engine<float> on {cfg.name} at full size, direct convolution, "
-                      f"{threads} worker threads, wall time around the measured rounds"}
+            "sample": f"{res['rounds']} measured round(s) (1 patch each, after {res['warmup']} warm-up round) of "
+                      f"the reference engine<float> (compiled from /root/reference, oracle/ref/build.sh) on "
+                      f"{cfg.name} at full size, conv mode {res['mode']}, {threads} worker threads, wall time "
+                      f"around the measured rounds"}
 
 
 def run_port(cfg, budget_s):
