@@ -14,8 +14,8 @@
 // error grows with the number of accumulating MMAs).
 //
 // Warp roles (384 threads, 1 CTA per SM; warps 10-11 idle):
-//   warps 0-7 : im2col producers for A: thread = one voxel row, warps 0-3
-//               k[0,16) and warps 4-7 k[16,32) of every 32-wide K-block; hi/lo
+//   warps 0-7 : im2col producers for A: thread = one voxel row; warps 0-3
+//               fill the even and warps 4-7 the odd 32-wide K-blocks; hi/lo
 //               split in registers, 128B-swizzled K-major st.shared.v4
 //               and drain finished TMEM chunks: warp w owns lane quarter
 //               w % 4, warps 0-3 columns [0, NT/2) and 4-7 [NT/2, NT); then
@@ -77,7 +77,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 256 + 1);
+            mbar_init(full_bar(s), 128 + 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 4; ++b) {
@@ -95,7 +95,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     if (warp < 8) {
         // ---------------- im2col producers ----------------
         const int r = threadIdx.x & 127;
-        const int half = threadIdx.x >> 7;  // which 16 of the 32 k of a block
+        const int half = threadIdx.x >> 7;  // warp group: even (0) / odd (1) K-blocks
         constexpr int NH = NTMAX / 2;
         const int col0 = half * NH;
         const int ncols = max(0, min(NH, p.nt - col0));
@@ -115,31 +115,35 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         }
         const uint32_t row_off = uint32_t(r) * 128u;
         const uint32_t sw = uint32_t(r & 7);
-        for (int kb = 0; kb < p.kblocks; ++kb) {
+        // Warp group `half` produces K-blocks kb = half, half+2, ... (all 32 k),
+        // so two K-blocks are always being gathered. (The proxy fence before
+        // each hand-off is a membar that waits for the thread's outstanding
+        // loads, so overlap has to come from independent warps, not prefetch.)
+        for (int kb = half; kb < p.kblocks; kb += 2) {
             const int s = kb % p.stages;
             const uint32_t ph = uint32_t(kb / p.stages) & 1u;
-            const int4* tb = reinterpret_cast<const int4*>(koff + kb * BK + 16 * half);
-            float vals[16];
+            const int4* tb = reinterpret_cast<const int4*>(koff + kb * BK);
+            float v[BK];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < BK / 4; ++q) {
                 const int4 e = __ldg(tb + q);
-                vals[4 * q + 0] = vok ? __ldg(sp + e.x) : 0.f;
-                vals[4 * q + 1] = vok ? __ldg(sp + e.y) : 0.f;
-                vals[4 * q + 2] = vok ? __ldg(sp + e.z) : 0.f;
-                vals[4 * q + 3] = vok ? __ldg(sp + e.w) : 0.f;
+                v[4 * q + 0] = vok ? __ldg(sp + e.x) : 0.f;
+                v[4 * q + 1] = vok ? __ldg(sp + e.y) : 0.f;
+                v[4 * q + 2] = vok ? __ldg(sp + e.z) : 0.f;
+                v[4 * q + 3] = vok ? __ldg(sp + e.w) : 0.f;
             }
             D.wait_stage(empty_bar(s), ph ^ 1u);
             const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
             const uint32_t a_lo = a_hi + BM * 128u;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < BK / 4; ++c) {
                 float h[4], l[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    h[q] = tf32_hi(vals[4 * c + q]);
-                    l[q] = tf32_rn(vals[4 * c + q] - h[q]);
+                    h[q] = tf32_hi(v[4 * c + q]);
+                    l[q] = tf32_rn(v[4 * c + q] - h[q]);
                 }
-                const uint32_t off = row_off + (((uint32_t(4 * half + c)) ^ sw) << 4);
+                const uint32_t off = row_off + ((uint32_t(c) ^ sw) << 4);
                 asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_hi + off), "f"(h[0]), "f"(h[1]),
                              "f"(h[2]), "f"(h[3]));
                 asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_lo + off), "f"(l[0]), "f"(l[1]),
@@ -292,18 +296,7 @@ encode_fn_t encoder() {
     return fn;
 }
 
-CUtensorMap make_panel_map(const float* ptr, int kpad, int rows, int nt) {
-    CUtensorMap m;
-    const cuuint64_t dims[2] = {cuuint64_t(kpad), cuuint64_t(rows)};
-    const cuuint64_t strides[1] = {cuuint64_t(kpad) * sizeof(float)};
-    const cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(nt)};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
-    return m;
-}
+CUtensorMap make_panel_map(const float* ptr, int kpad, int rows, int nt);
 
 template <int NTMAX>
 void launch_kernel(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mhi, const CUtensorMap& mlo,
@@ -373,6 +366,28 @@ size_t panel_bytes(int f_src, int n_real, int64_t T) {
     return sizeof(float) * size_t(npad * kpad) * 2 + sizeof(int) * size_t(kpad) + 512;
 }
 
+}  // namespace
+
+// 2D TMA map over a row-major fp32 panel [rows][cols] (cols * 4 B a multiple
+// of 16), box = 32 columns (one 128 B swizzle row) x box_rows rows, SWIZZLE_128B.
+CUtensorMap make_panel_map_rows(const float* ptr, int64_t cols, int64_t rows, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(float)};
+    const cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    require(cols % 4 == 0, "tma panel: row pitch must be a multiple of 16 bytes");
+    CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return m;
+}
+
+namespace {
+CUtensorMap make_panel_map(const float* ptr, int kpad, int rows, int nt) {
+    return make_panel_map_rows(ptr, kpad, rows, nt);
+}
 }  // namespace
 
 bool conv_tc_supported(const conv_shape& c, int pass) {

@@ -4,15 +4,20 @@
 //   dW[o][i][w] = scale * sum_{b,v} g[b][o][v] * x[b][i][v + s*w]
 // GEMM view: rows R = (i, w) (f_in*T of them, 128 per tile), columns = output
 // maps o (<= 128 per tile), K = output voxels of every patch (32 per stage,
-// never straddling a patch). Both operands are produced by warps with fully
-// coalesced row loads (a warp reads 32 consecutive voxels of one row), split
-// into tf32 hi/lo in registers and stored 128B-swizzled. Each CTA owns a
-// contiguous K range (split-K); partial tiles land in a workspace
-// [split][o][R] and a fixed-order reduction sums them (deterministic).
+// never straddling a patch).
+//   A (x rows, shifted windows) : gathered by producer warps with coalesced
+//       row loads (a warp reads 32 consecutive voxels of one row), split into
+//       tf32 hi/lo in registers, stored 128B-swizzled;
+//   B (g rows)                  : pre-split into hi/lo panels [B*f_out][mpad]
+//       by one memory-bound pass, then TMA-loaded (SWIZZLE_128B).
+// Each CTA owns a contiguous K range (split-K); partial tiles land in a
+// workspace [split][o][R] and a fixed-order reduction sums them
+// (deterministic).
 //
-// Warps: 0-7 operand producers that also drain finished TMEM chunks (warp w:
-// lane quarter w % 4, column half w / 4) and run the epilogue; 8 TMEM alloc +
-// MMA issuer; 9-11 idle (registers are granted per 4-warp group).
+// Warps: 0-7 producers (warps 0-3 even, 4-7 odd K-blocks) that also drain
+// finished TMEM chunks (warp w: lane quarter w % 4, column half w / 4) and
+// run the epilogue; 8 TMA producer; 9 TMEM alloc + MMA issuer; 10-11 idle
+// (registers are granted per 4-warp group).
 #include <cuda.h>
 
 #include "ops.hpp"
@@ -20,17 +25,19 @@
 
 namespace znn_gpu {
 
+CUtensorMap make_panel_map_rows(const float* ptr, int64_t cols, int64_t rows, int box_rows);
+
 namespace {
 
 using namespace znn_tc;
 
-constexpr int THREADS = 384;  // registers are granted per 4-warp group
+constexpr int THREADS = 384;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CHUNK_KB = 8;
 
 struct wg_params {
     int f_in, f_out, T, nt;
-    int mrows;          // f_in * T
+    int mrows;  // f_in * T
     int stages, nbuf, bstride;
     int64_t kb_per_patch, kb_total, kb_per_split;
     int64_t nvol, mvol;
@@ -39,8 +46,9 @@ struct wg_params {
 
 template <int NTMAX>
 __global__ void __launch_bounds__(THREADS, 1)
-wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const int* __restrict__ rowoff_g,
-                float* __restrict__ ws, wg_params p) {
+wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
+                const float* __restrict__ x, const int* __restrict__ rowoff_g, float* __restrict__ ws,
+                wg_params p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ int rowoff[BM];
     const uint32_t raw = smem_u32(smem_raw);
@@ -51,12 +59,12 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
     const uint32_t bar_base = base + uint32_t(p.stages) * stage_bytes;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
     auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(p.stages + s); };
-    auto accf_bar = [&](int b) { return bar_base + 8u * uint32_t(2 * p.stages + b); };
-    auto acce_bar = [&](int b) { return bar_base + 8u * uint32_t(2 * p.stages + 4 + b); };
+    const uint32_t accf0 = bar_base + 8u * uint32_t(2 * p.stages);
+    const uint32_t acce0 = accf0 + 32u;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 8));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r0 = blockIdx.x * BM;   // first (i, w) row of this tile
+    const int r0 = blockIdx.x * BM;    // first (i, w) row of this tile
     const int n0 = blockIdx.y * p.nt;  // first output map
     const int64_t q0 = int64_t(blockIdx.z) * p.kb_per_split;
     const int64_t q1 = min(p.kb_total, q0 + p.kb_per_split);
@@ -66,89 +74,64 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
     if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : -1;
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 256);
+            mbar_init(full_bar(s), 128 + 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 4; ++b) {
-            mbar_init(accf_bar(b), 1);
-            mbar_init(acce_bar(b), 256);
+            mbar_init(accf0 + 8u * b, 1);
+            mbar_init(acce0 + 8u * b, 256);
         }
         fence_barrier_init();
     }
-    if (warp == 8) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    if (warp == 9) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
     if (warp < 8) {
-        // ---------------- producers: lane = voxel, warp strides over rows ----------------
         constexpr int NH = NTMAX / 2;
-        const int col0 = (warp >> 2) * NH;
+        const int grp = warp >> 2;  // 0: even K-blocks, 1: odd K-blocks
+        const int wq = warp & 3;    // this warp gathers A rows wq, wq+4, ...
+        const int col0 = grp * NH;
         const int ncols = max(0, min(NH, p.nt - col0));
         chunk_drainer<NH> D;
-        D.init(accf_bar(0), acce_bar(0), tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col0), p.nbuf,
-               p.bstride, ncols, nchunks);
-        // patch index and in-patch voxel advance incrementally (no 64-bit division in the loop)
-        int64_t pb = q0 / p.kb_per_patch;
-        int vbase = int((q0 - pb * p.kb_per_patch) * BK);
+        D.init(accf0, acce0, tmem + (uint32_t(wq * 32) << 16) + uint32_t(col0), p.nbuf, p.bstride, ncols, nchunks);
         const int mvol = int(p.mvol);
         const int myz = p.my * p.mz;
-        for (int kb = 0; kb < kblocks; ++kb) {
-            if (vbase >= mvol) {
-                vbase = 0;
-                ++pb;
-            }
-            const int v = vbase + lane;
-            vbase += BK;
+        // rows wq + 4t alternate between two swizzle phases ((row & 7) = wq or wq + 4)
+        const uint32_t offA = sw128_off(uint32_t(wq), uint32_t(lane));
+        const uint32_t offB = sw128_off(uint32_t(wq + 4), uint32_t(lane));
+        for (int kb = grp; kb < kblocks; kb += 2) {
+            const int64_t q = q0 + kb;
+            const int64_t pb = q / p.kb_per_patch;
+            const int v = int(q - pb * p.kb_per_patch) * BK + lane;
             const bool vok = v < mvol;
             const float* xp = x;
-            const float* gp = g;
             if (vok) {
                 const int vx = v / myz;
                 const int r2 = v - vx * myz;
                 const int vy = r2 / p.mz;
                 const int vz = r2 - vy * p.mz;
                 xp = x + pb * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
-                gp = g + pb * int64_t(p.f_out) * p.mvol + v;
+            }
+            float av[BM / 4];
+#pragma unroll
+            for (int t = 0; t < BM / 4; ++t) {
+                const int ro = rowoff[wq + 4 * t];
+                av[t] = (vok && ro >= 0) ? __ldg(xp + ro) : 0.f;
             }
             const int s = kb % p.stages;
             const uint32_t ph = uint32_t(kb / p.stages) & 1u;
+            D.wait_stage(empty_bar(s), ph ^ 1u);
             const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
             const uint32_t a_lo = a_hi + BM * 128u;
-            const uint32_t b_hi = a_lo + BM * 128u;
-            const uint32_t b_lo = b_hi + b_bytes;
-            // gather into registers first (loads overlap the wait for the slot)
-            float av[BM / 8];
 #pragma unroll
-            for (int t = 0; t < BM / 8; ++t) {
-                const int ro = rowoff[warp + 8 * t];
-                av[t] = (vok && ro >= 0) ? __ldg(xp + ro) : 0.f;
-            }
-            float bv[NTMAX / 8];
-#pragma unroll
-            for (int t = 0; t < NTMAX / 8; ++t) {
-                const int n = warp + 8 * t;
-                const int o = n0 + n;
-                bv[t] = (n < p.nt && vok && o < p.f_out) ? __ldg(gp + int64_t(o) * p.mvol) : 0.f;
-            }
-            D.wait_stage(empty_bar(s), ph ^ 1u);
-#pragma unroll
-            for (int t = 0; t < BM / 8; ++t) {
-                const uint32_t off = sw128_off(uint32_t(warp + 8 * t), uint32_t(lane));
+            for (int t = 0; t < BM / 4; ++t) {
+                const uint32_t off = ((t & 1) ? offB : offA) + uint32_t(t >> 1) * 1024u;
                 const float h = tf32_hi(av[t]);
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_hi + off), "f"(h));
                 asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_lo + off), "f"(tf32_rn(av[t] - h)));
-            }
-#pragma unroll
-            for (int t = 0; t < NTMAX / 8; ++t) {
-                const int n = warp + 8 * t;
-                if (n < p.nt) {
-                    const uint32_t off = sw128_off(uint32_t(n), uint32_t(lane));
-                    const float h = tf32_hi(bv[t]);
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(b_hi + off), "f"(h));
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(b_lo + off), "f"(tf32_rn(bv[t] - h)));
-                }
             }
             fence_proxy_async();
             mbar_arrive(full_bar(s));
@@ -156,16 +139,32 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
         }
         // ---------------- remaining drains + epilogue (this warp's columns) ----------------
         D.finish();
-        const int R = r0 + (threadIdx.x & 127);
+        const int R = r0 + wq * 32 + lane;  // TMEM lane = tile row
         if (R < p.mrows) {
             float* wsz = ws + int64_t(blockIdx.z) * p.f_out * p.mrows;
 #pragma unroll
-            for (int q = 0; q < NH; ++q) {
-                const int o = n0 + col0 + q;
-                if (q < ncols && o < p.f_out) wsz[int64_t(o) * p.mrows + R] = D.A.acc[q];
+            for (int qq = 0; qq < NH; ++qq) {
+                const int o = n0 + col0 + qq;
+                if (qq < ncols && o < p.f_out) wsz[int64_t(o) * p.mrows + R] = D.A.acc[qq];
             }
         }
     } else if (warp == 8) {
+        // ---------------- TMA producer: g panels ----------------
+        if (lane == 0) {
+            for (int kb = 0; kb < kblocks; ++kb) {
+                const int64_t q = q0 + kb;
+                const int64_t pb = q / p.kb_per_patch;
+                const int vcol = int(q - pb * p.kb_per_patch) * BK;
+                const int row = int(pb * p.f_out) + n0;
+                const int s = kb % p.stages;
+                mbar_wait(empty_bar(s), (uint32_t(kb / p.stages) & 1u) ^ 1u);
+                const uint32_t b_hi = base + uint32_t(s) * stage_bytes + 2u * BM * 128u;
+                mbar_expect_tx(full_bar(s), 2u * b_bytes);
+                tma_load_2d(b_hi, &tm_hi, full_bar(s), vcol, row);
+                tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), vcol, row);
+            }
+        }
+    } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(BM, p.nt);
@@ -174,7 +173,7 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
                 const int b = ch % p.nbuf;
                 const bool first = (kb % CHUNK_KB) == 0;
                 if (first) {
-                    mbar_wait(acce_bar(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
+                    mbar_wait(acce0 + 8u * uint32_t(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
                     tc_fence_after();
                 }
                 const uint32_t d = tmem + uint32_t(b * p.bstride);
@@ -187,21 +186,21 @@ wgrad_tc_kernel(const float* __restrict__ x, const float* __restrict__ g, const 
                 const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
-                    const uint32_t koff = uint32_t(kk) * 32u;
-                    const uint64_t ah = sw128_desc(a_hi + koff), al = sw128_desc(a_lo + koff);
-                    const uint64_t bh = sw128_desc(b_hi + koff), bl = sw128_desc(b_lo + koff);
+                    const uint32_t ko = uint32_t(kk) * 32u;
+                    const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
+                    const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
                     mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
                     mma_tf32(d, ah, bl, idesc, 1u);
                     mma_tf32(d, al, bh, idesc, 1u);
                 }
                 mma_commit(empty_bar(s));
-                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit(accf_bar(b));
+                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit(accf0 + 8u * uint32_t(b));
             }
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 9) {
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
@@ -217,6 +216,19 @@ __global__ void rowoff_k(int* __restrict__ out, int mrows, int T, int ky, int kz
     }
 }
 
+// g [rows][mvol] -> hi/lo [rows][mpad] (zero padded columns): the TMA panels
+__global__ void split_rows_k(const float* __restrict__ g, int64_t rows, int64_t mvol, int64_t mpad,
+                             float* __restrict__ hi, float* __restrict__ lo) {
+    const int64_t total = rows * mpad;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = i / mpad, c = i - r * mpad;
+        const float v = c < mvol ? g[r * mvol + c] : 0.f;
+        const float h = tf32_hi(v);
+        hi[i] = h;
+        lo[i] = tf32_rn(v - h);
+    }
+}
+
 __global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, int64_t len, float scale,
                                 float* __restrict__ out) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
@@ -227,11 +239,11 @@ __global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, in
 }
 
 template <int NTMAX>
-void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const float* x, const float* g, const int* rowoff, float* ws,
-            const wg_params& p) {
+void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mhi, const CUtensorMap& mlo,
+                  const float* x, const int* rowoff, float* ws, const wg_params& p) {
     auto* k = wgrad_tc_kernel<NTMAX>;
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k<<<grid, THREADS, smem, st>>>(x, g, rowoff, ws, p);
+    k<<<grid, THREADS, smem, st>>>(mhi, mlo, x, rowoff, ws, p);
     launch_check("conv_wgrad_tc");
 }
 
@@ -266,19 +278,30 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     p.kb_per_split = ceil_div(p.kb_total, splits);
     splits = ceil_div(p.kb_total, p.kb_per_split);
 
+    const int64_t mpad = p.kb_per_patch * BK;
+    const int64_t grows = c.B * c.f_out;
+    const size_t panel = size_t(grows) * size_t(mpad);
     const size_t part = size_t(splits) * size_t(c.f_out) * size_t(p.mrows);
-    char* wsp = static_cast<char*>(ws.get(sizeof(float) * part + sizeof(int) * size_t(p.mrows) + 256));
-    float* partials = reinterpret_cast<float*>(wsp);
+    char* wsp = static_cast<char*>(ws.get(sizeof(float) * (2 * panel + part) + sizeof(int) * size_t(p.mrows) + 4096));
+    float* ghi = reinterpret_cast<float*>(wsp);
+    float* glo = ghi + panel;
+    float* partials = glo + panel;
     int* rowoff = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(partials + part) + 255) & ~uintptr_t(255));
+    int64_t sb = ceil_div(int64_t(panel), 256);
+    if (sb > 148 * 16) sb = 148 * 16;
+    split_rows_k<<<unsigned(sb), 256, 0, st>>>(g, grows, p.mvol, mpad, ghi, glo);
+    launch_check("conv_wgrad_tc_split");
     rowoff_k<<<unsigned(ceil_div(p.mrows, 256)), 256, 0, st>>>(rowoff, p.mrows, p.T, int(c.k.y), int(c.k.z),
                                                                int(c.s.x), int(c.s.y), int(c.s.z), p.ny, p.nz,
                                                                p.nvol);
     launch_check("conv_wgrad_tc_rowoff");
+    const CUtensorMap mhi = make_panel_map_rows(ghi, mpad, grows, p.nt);
+    const CUtensorMap mlo = make_panel_map_rows(glo, mpad, grows, p.nt);
     const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 8) + 16 + 1024;
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
-    if (ntmax == 32) launch_wgrad<32>(grid, smem, st, x, g, rowoff, partials, p);
-    else if (ntmax == 64) launch_wgrad<64>(grid, smem, st, x, g, rowoff, partials, p);
-    else launch_wgrad<128>(grid, smem, st, x, g, rowoff, partials, p);
+    if (ntmax == 32) launch_wgrad<32>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+    else if (ntmax == 64) launch_wgrad<64>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+    else launch_wgrad<128>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
     const int64_t len = c.f_out * int64_t(p.mrows);
     int64_t rb = ceil_div(len, 256);
     if (rb > 148 * 8) rb = 148 * 8;
