@@ -162,6 +162,12 @@ int znn_net_set_layer_engine(znn_net net, int conv_layer, int engine);
  * layer with each engine and keeps the faster. Returns chosen engines. */
 int znn_net_autotune(znn_net net, int trials, int32_t* chosen, int max_layers);
 
+/* FFT transform counters of conv layer `conv_layer` (fft.hpp:19-49 phases x
+ * kinds): out[9] = {fwd image, fwd kernel, fwd inverse, bwd image, bwd kernel,
+ * bwd inverse, upd image, upd kernel, upd inverse}. Status 1 if the layer
+ * has not run on the FFT engine. */
+int znn_net_fft_counts(znn_net net, int conv_layer, int64_t* out);
+
 /* Full SGD step through HOST buffers (H2D of inputs/labels, fwd, loss,
  * bwd, update, D2H of the loss): the reference engine::run round. */
 int znn_net_step_host(znn_net net, const float* inputs, const float* labels, double* loss);

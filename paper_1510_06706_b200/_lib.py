@@ -25,7 +25,7 @@ EXPORTS = [
     "znn_loss", "znn_sgd_momentum",
     "znn_net_create", "znn_net_destroy", "znn_net_describe", "znn_net_num_params",
     "znn_net_io_sizes", "znn_net_set_params", "znn_net_get_params", "znn_net_get_gradients",
-    "znn_net_reset_momentum", "znn_net_set_layer_engine", "znn_net_autotune",
+    "znn_net_reset_momentum", "znn_net_set_layer_engine", "znn_net_autotune", "znn_net_fft_counts",
     "znn_net_step_host", "znn_net_forward_backward", "znn_net_apply_update",
     "znn_net_grad_buffer", "znn_net_forward", "znn_net_group_info",
     "znn_net_get_group_image", "znn_net_get_mask",
@@ -99,6 +99,7 @@ def lib():
         "znn_net_reset_momentum": (ci, [vp]),
         "znn_net_set_layer_engine": (ci, [vp, ci, ci]),
         "znn_net_autotune": (ci, [vp, ci, P32, ci]),
+        "znn_net_fft_counts": (ci, [vp, ci, P64]),
         "znn_net_step_host": (ci, [vp, vp, vp, Pd]),
         "znn_net_forward_backward": (ci, [vp, vp, vp, Pd]),
         "znn_net_apply_update": (ci, [vp]),

@@ -120,6 +120,13 @@ class Net:
         self.engines = [int(v) for v in arr[: self.describe().count("conv#")]]
         return self.engines
 
+    def fft_counts(self, conv_layer: int):
+        """FFT transform counters (fwd/bwd/upd x image/kernel/inverse) of a conv layer."""
+        out = (ctypes.c_int64 * 9)()
+        self._c(lib().znn_net_fft_counts(self._h, conv_layer, out))
+        keys = [f"{p}_{k}" for p in ("fwd", "bwd", "upd") for k in ("image", "kernel", "inverse")]
+        return dict(zip(keys, [int(v) for v in out]))
+
     def step_host(self, inputs: np.ndarray, labels: np.ndarray) -> float:
         """One SGD step from HOST arrays (H2D, fwd, loss, bwd, update, loss D2H)."""
         inputs = np.ascontiguousarray(inputs, dtype=np.float32)

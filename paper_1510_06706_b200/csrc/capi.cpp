@@ -151,8 +151,12 @@ int znn_conv_fwd(znn_ctx ctx, const float* x, int64_t B, int64_t f_in, const int
     return guarded(ctx, [&] {
         if (act < 0 || act > 3) throw znn_gpu::shape_error("conv: unknown transfer kind");
         auto c = znn_gpu::conv_shape::make(B, f_in, f_out, D(n), D(k), D(s));
-        if (engine == ZNN_CONV_FFT)
-            znn_fft::conv_fwd(ctx->stream, c, x, w, bias, act, y, ctx->ws);
+        if (engine == ZNN_CONV_FFT) {
+            // op-level forward: a throw-away plan (the executor keeps its plans)
+            auto plan = znn_fft::make_plan(c);
+            znn_fft::conv_fwd(ctx->stream, *plan, c, x, w, bias, act, y, ctx->ws);
+            ZNN_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        }
         else if (engine != ZNN_CONV_DIRECT_SIMT && znn_gpu::conv_tc_supported(c, 0))
             znn_gpu::conv_fwd_tc(ctx->stream, c, x, w, bias, act, y, ctx->ws);
         else
@@ -312,6 +316,16 @@ int znn_net_autotune(znn_net net, int trials, int32_t* chosen, int max_layers) {
         auto c = net->ex->autotune(trials);
         for (size_t i = 0; i < c.size() && int(i) < max_layers; ++i)
             if (chosen) chosen[i] = c[i];
+    });
+}
+
+int znn_net_fft_counts(znn_net net, int conv_layer, int64_t* out) {
+    return guarded(net->ctx, [&] {
+        znn_fft::transform_counts t;
+        if (!net->ex->fft_counts(conv_layer, t)) throw znn_gpu::shape_error("conv layer has no FFT plan");
+        const int64_t v[9] = {t.fwd_image, t.fwd_kernel, t.fwd_inverse, t.bwd_image, t.bwd_kernel,
+                              t.bwd_inverse, t.upd_image, t.upd_kernel, t.upd_inverse};
+        for (int i = 0; i < 9; ++i) out[i] = v[i];
     });
 }
 

@@ -1,8 +1,15 @@
-// FFT-memoised convolution engine (conv_fft.hpp:25-125 / fft.hpp:57-192 of
-// the reference): batched 3D R2C/C2R transforms, per-image spectra reused
-// across the f x f' edges of a layer, per-frequency complex MAC over
-// converging edges. Implemented in fft.cu.
+// FFT-memoised convolution engine (conv_fft.hpp:25-192 / fft.hpp:57-192 of
+// the reference), B200-native: batched 3D transforms by hand-written
+// shared-memory Stockham kernels (radix 2/3/4, pad sizes 2^a 3^b <= 128),
+// per-image spectra memoised from the forward pass into the backward and
+// update passes exactly as the reference's memo_store does (image spectrum
+// once per node, kernel spectrum once per edge per iteration), and the
+// frequency-domain sum over converging edges as a per-frequency complex
+// multiply-accumulate kernel (HBM-bound).
 #pragma once
+
+#include <cstdint>
+#include <memory>
 
 #include "ops.hpp"
 
@@ -10,11 +17,32 @@ namespace znn_fft {
 
 using znn_gpu::conv_shape;
 
+// per-pass transform counters, mirroring fft.hpp:19-49 (phase x kind)
+struct transform_counts {
+    int64_t fwd_image = 0, fwd_kernel = 0, fwd_inverse = 0;
+    int64_t bwd_image = 0, bwd_kernel = 0, bwd_inverse = 0;
+    int64_t upd_image = 0, upd_kernel = 0, upd_inverse = 0;
+};
+
+struct plan;  // pad dims + memoised spectra (device memory)
+struct plan_deleter {
+    void operator()(plan* p) const;
+};
+using plan_ptr = std::unique_ptr<plan, plan_deleter>;
+
 bool supported(const conv_shape& c);
-void conv_fwd(cudaStream_t st, const conv_shape& c, const float* x, const float* w,
+plan_ptr make_plan(const conv_shape& c);
+const transform_counts& counts(const plan& p);
+void pad_dims(const plan& p, int64_t out[3]);
+
+// forward: y = act(bias + sum_i IFFT(X_i * conj(K_oi))) cropped (conv_fft.hpp:38-60);
+// memoises X (image spectra) and K (kernel spectra) in the plan.
+void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w,
               const float* bias, int act, float* y, znn_gpu::scratch& ws);
-// wgrad into gw (overwritten); dgrad into gin when non-null
-void conv_bwd(cudaStream_t st, const conv_shape& c, const float* x, const float* g,
+// backward + update from the memo: gin = IFFT(sum_o G_o * K_oi) (no conjugate,
+// conv_fft.hpp:67-96, skipped when gin == nullptr) and
+// gw = IFFT(sum_b X_bi * conj(G_bo))[s*w] (conv_fft.hpp:98-125).
+void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* g,
               const float* w, float* gw, float* gin, znn_gpu::scratch& ws);
 
 }  // namespace znn_fft

@@ -346,14 +346,32 @@ void executor::set_layer_engine(int conv_layer, int engine) {
     throw znn_gpu::shape_error("set_layer_engine: no conv layer " + std::to_string(conv_layer));
 }
 
-void executor::run_conv_fwd(const layer& L) {
+znn_fft::plan& executor::fft_plan(layer& L) {
+    if (!L.fft) L.fft = std::shared_ptr<znn_fft::plan>(znn_fft::make_plan(L.shape).release(), znn_fft::plan_deleter());
+    return *L.fft;
+}
+
+bool executor::fft_counts(int conv_layer, znn_fft::transform_counts& out) const {
+    int ci = 0;
+    for (const auto& L : layers_)
+        if (L.kind == lkind::conv) {
+            if (ci++ == conv_layer) {
+                if (!L.fft) return false;
+                out = znn_fft::counts(*L.fft);
+                return true;
+            }
+        }
+    return false;
+}
+
+void executor::run_conv_fwd(layer& L) {
     const float* x = groups_[size_t(L.in)].act;
     float* y = groups_[size_t(L.out)].act;
     const float* w = params_ + L.w_off;
     const float* bias = L.fused ? params_ + L.b_off : nullptr;
     const int act = L.fused ? L.fused_act : 3;
     if (L.engine == 1) {
-        znn_fft::conv_fwd(st_, L.shape, x, w, bias, act, y, ws_);
+        znn_fft::conv_fwd(st_, fft_plan(L), L.shape, x, w, bias, act, y, ws_);
     } else if (L.engine == 0 && znn_gpu::conv_tc_supported(L.shape, 0)) {
         znn_gpu::conv_fwd_tc(st_, L.shape, x, w, bias, act, y, ws_);
     } else {
@@ -361,12 +379,12 @@ void executor::run_conv_fwd(const layer& L) {
     }
 }
 
-void executor::run_conv_bwd(const layer& L, float* g_out, float* g_in, bool need_dgrad) {
+void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad) {
     const float* x = groups_[size_t(L.in)].act;
     const float* w = params_ + L.w_off;
     float* gw = grads_ + L.w_off;
     if (L.engine == 1) {
-        znn_fft::conv_bwd(st_, L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_);
+        znn_fft::conv_bwd(st_, fft_plan(L), L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_);
         return;
     }
     const bool tc = L.engine == 0;
@@ -385,7 +403,7 @@ void executor::run_conv_bwd(const layer& L, float* g_out, float* g_in, bool need
 void executor::run_forward(const float* in_dev) {
     groups_[0].act = const_cast<float*>(in_dev);
     const int64_t B = cfg_.batch;
-    for (const auto& L : layers_) {
+    for (auto& L : layers_) {
         const group& I = groups_[size_t(L.in)];
         group& O = groups_[size_t(L.out)];
         switch (L.kind) {
@@ -421,7 +439,7 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                              G.grad, loss_dev_, ws_);
     // backward in reverse layer order
     for (size_t li = layers_.size(); li-- > 0;) {
-        const layer& L = layers_[li];
+        layer& L = layers_[li];
         group& I = groups_[size_t(L.in)];
         group& O = groups_[size_t(L.out)];
         const bool last = li + 1 == layers_.size();

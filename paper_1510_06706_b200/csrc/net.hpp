@@ -7,9 +7,11 @@
 
 #include <cuda_runtime.h>
 
+#include <memory>
 #include <string>
 #include <vector>
 
+#include "fft.hpp"
 #include "netgraph.hpp"
 #include "ops.hpp"
 
@@ -38,6 +40,7 @@ struct layer {
     conv_shape shape;
     int64_t w_off = -1;     // offset of [f_out][f_in][T] in the flat parameter buffer
     int engine = 0;         // ZNN_CONV_*
+    std::shared_ptr<znn_fft::plan> fft;  // memoised spectra when engine == FFT
     bool fused = false;     // transfer edge fused into the conv epilogue
     int fused_act = 3;
     int64_t b_off = -1;     // bias offset (fused transfer or transfer layer)
@@ -92,14 +95,17 @@ public:
     void group_image(int g, int which, float* host);
     void group_mask(int g, int32_t* host);
     const std::vector<layer>& layers() const { return layers_; }
+    // transform counts of conv layer `conv_layer` (FFT engine), test hook
+    bool fft_counts(int conv_layer, znn_fft::transform_counts& out) const;
     double last_loss_device();
 
 private:
     void build(const znn_host::graph& g);
     void allocate();
     void run_forward(const float* in_dev);
-    void run_conv_fwd(const layer& L);
-    void run_conv_bwd(const layer& L, float* g_out, float* g_in, bool need_dgrad);
+    void run_conv_fwd(layer& L);
+    void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad);
+    znn_fft::plan& fft_plan(layer& L);
 
     train_cfg cfg_;
     cudaStream_t st_ = nullptr;

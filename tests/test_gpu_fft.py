@@ -1,0 +1,138 @@
+"""FFT engine parity (conv_fft.hpp semantics) against the double oracle, the
+memoised-transform budget (test_engine.cpp:277-330 restated for layer
+waves), FFT-vs-direct training equivalence (test_engine.cpp:240-257) and the
+device autotuner choosing FFT for config c4's 7^3 layers."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda", dtype=torch.float32)
+
+
+CASES = [
+    (1, 1, 1, (5, 5, 5), (3, 3, 3), (1, 1, 1)),
+    (2, 3, 4, (9, 8, 10), (3, 2, 3), (1, 2, 1)),
+    (1, 4, 3, (16, 12, 14), (4, 3, 2), (2, 2, 3)),
+    (2, 5, 6, (1, 17, 19), (1, 5, 5), (1, 2, 2)),   # 2-D: x = 1
+    (1, 2, 2, (20, 18, 16), (7, 7, 7), (2, 2, 2)),
+]
+
+
+@pytest.mark.parametrize("shape", CASES, ids=str)
+def test_fft_conv_fwd_matches_oracle(ctx, shape):
+    """test_conv.cpp:199-221 (fft vs direct < 1e-5) restated against the double oracle."""
+    from paper_1510_06706_b200 import ops
+    B, fi, fo, n, k, s = shape
+    rng = np.random.default_rng(sum(n) + fo)
+    x = rng.uniform(0, 1, size=(B, fi) + n).astype(np.float32)
+    w = rng.uniform(-1, 1, size=(fo, fi) + k).astype(np.float32)
+    bias = rng.uniform(-0.2, 0.2, size=fo).astype(np.float32)
+    y = ops.conv_fwd(ctx, cuda(x), cuda(w), k, s, bias=cuda(bias), act="tanh", engine="fft").cpu().numpy()
+    for b in range(B):
+        for o in range(fo):
+            ref = np.tanh(sum(O.conv_valid(x[b, i], w[o, i], s) for i in range(fi)) + bias[o])
+            assert O.max_rel_error(y[b, o], ref) < 1e-4
+
+
+def _net_one_step(ctx, cfg, engines, seed=5):
+    from paper_1510_06706_b200 import Net, configs
+    rng = np.random.default_rng(seed)
+    params = configs.init_params(cfg, seed)
+    x = rng.uniform(0, 1, size=(cfg.batch, cfg.in_maps) + tuple(cfg.in_dims)).astype(np.float32)
+    nout = cfg.layers[-1].width
+    lab = (rng.uniform(size=(cfg.batch, nout) + tuple(cfg.out_dims)) < 0.5).astype(np.float32)
+    net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=cfg.batch, lr=cfg.lr, momentum=cfg.momentum,
+              loss=cfg.loss)
+    for li, e in enumerate(engines):
+        net.set_layer_engine(li, e)
+    net.set_params(params)
+    loss = net.forward_backward(cuda(x), cuda(lab))
+    grads = net.get_gradients()
+    net.apply_update()
+    return net, params, x, lab, loss, grads, net.get_params()
+
+
+@pytest.mark.parametrize("name,wd,od", [("c4", 16, (2, 2, 2)), ("c2", 8, (1, 6, 6)), ("c5", 30, (1, 1, 1))])
+def test_fft_engine_one_step_parity(ctx, name, wd, od):
+    from paper_1510_06706_b200 import configs as C
+    cfg = C.scaled(name, wd, od, batch=2)
+    nconv = len(cfg.conv_layers())
+    engines = ["fft"] * (nconv - 1) + ["direct"]  # 1^3 output layer stays direct
+    net, params, x, lab, loss, grads, newp = _net_one_step(ctx, cfg, engines)
+    g = O.parse_netspec(cfg.netspec(), cfg.out_dims)
+    ins = [[x[b, 0]] for b in range(cfg.batch)]
+    labs = [[lab[b, o] for o in range(lab.shape[1])] for b in range(cfg.batch)]
+    rl, rg, rp, _ = O.train_step(g, params.astype(np.float64), np.zeros(params.size), ins, labs, cfg.lr,
+                                 cfg.momentum, cfg.loss)
+    assert abs(loss - rl) / (abs(rl) + 1) < 1e-4
+    assert O.max_rel_error(grads, rg) < 1e-3
+    assert O.max_rel_error(newp, rp) < 1e-3
+
+
+def test_fft_transform_budget(ctx):
+    """Memoised transform counts per fully connected layer (test_engine.cpp:313-329):
+    forward f image + f*f' kernel + f' inverse, backward f' image + 0 kernel + f
+    inverse, update f*f' gradient inverses (per patch; x batch here). The FFT
+    layer is the second conv so its input gradient is needed."""
+    from paper_1510_06706_b200 import Net
+    spec = ("[node in] role=input\n"
+            + "".join(f"[node h{i}]\n[node t{i}]\n" for i in range(3))
+            + "[node o0] role=output\n[node o1] role=output\n"
+            + "".join(f"[edge c{i}] from=in to=h{i} type=conv kernel=1,1,1\n" for i in range(3))
+            + "".join(f"[edge t{i}] from=h{i} to=t{i} type=transfer fn=tanh\n" for i in range(3))
+            + "".join(f"[edge e{i}{j}] from=t{i} to=o{j} type=conv kernel=3,3,3\n" for i in range(3) for j in range(2)))
+    B, rounds = 2, 2
+    net = Net(ctx, spec, (6, 6, 6), batch=B, loss="l2")
+    net.set_layer_engine(1, "fft")
+    rng = np.random.default_rng(1)
+    net.set_params(rng.uniform(-0.3, 0.3, size=net.num_params).astype(np.float32))
+    for _ in range(rounds):
+        net.step_host(rng.uniform(0, 1, size=(B, 1, 8, 8, 8)).astype(np.float32),
+                      rng.uniform(0, 1, size=(B, 2, 6, 6, 6)).astype(np.float32))
+    c = net.fft_counts(1)
+    f, fp = 3, 2
+    assert c["fwd_image"] == f * B * rounds and c["fwd_kernel"] == f * fp * rounds
+    assert c["fwd_inverse"] == fp * B * rounds
+    assert c["bwd_image"] == fp * B * rounds and c["bwd_kernel"] == 0 and c["bwd_inverse"] == f * B * rounds
+    assert c["upd_image"] == 0 and c["upd_kernel"] == 0 and c["upd_inverse"] == f * fp * rounds
+
+
+def test_fft_and_direct_train_to_matching_losses(ctx):
+    """test_engine.cpp:240-257: 10 rounds, losses within 1e-3 relative."""
+    from paper_1510_06706_b200 import Net, configs as C
+    cfg = C.scaled("c4", 16, (2, 2, 2), batch=2)
+    rng = np.random.default_rng(9)
+    params = C.init_params(cfg, 9)
+    x = rng.uniform(0, 1, size=(2, 1) + tuple(cfg.in_dims)).astype(np.float32)
+    lab = (rng.uniform(size=(2, 3) + tuple(cfg.out_dims)) < 0.5).astype(np.float32)
+    losses = {}
+    for mode in ("direct", "fft"):
+        net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=2, lr=cfg.lr, momentum=cfg.momentum, loss="ce")
+        if mode == "fft":
+            for li in range(3):
+                net.set_layer_engine(li, "fft")
+        net.set_params(params)
+        losses[mode] = [net.step_host(x, lab) for _ in range(10)]
+    for a, b in zip(losses["direct"], losses["fft"]):
+        assert abs(a - b) <= 1e-3 * abs(a)
+
+
+def test_autotuner_picks_fft_for_c4_7cubed_layers(ctx):
+    """North star: the per-layer device autotuner chooses FFT for c4's 7^3 layers."""
+    from paper_1510_06706_b200 import Net, configs as C
+    cfg = C.CONFIGS["c4"]
+    net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=cfg.batch, lr=cfg.lr, momentum=cfg.momentum,
+              loss=cfg.loss)
+    net.set_params(C.init_params(cfg, 1))
+    rng = np.random.default_rng(2)
+    x = cuda(rng.uniform(0, 1, size=(cfg.batch, 1) + tuple(cfg.in_dims)))
+    lab = cuda((rng.uniform(size=(cfg.batch, 3) + tuple(cfg.out_dims)) < 0.5))
+    net.forward_backward(x, lab)  # realistic activations in the buffers
+    chosen = net.autotune(trials=2)
+    assert chosen[:3] == [1, 1, 1], chosen  # 1 = ZNN_CONV_FFT
