@@ -530,8 +530,11 @@ std::vector<int> executor::autotune(int trials) {
     cudaEvent_t a, b;
     ZNN_CUDA_CHECK(cudaEventCreate(&a));
     ZNN_CUDA_CHECK(cudaEventCreate(&b));
+    std::ostringstream report;  // appended to describe(): per-layer median fwd+bwd+upd times
+    int ci = 0;
     for (auto& L : layers_) {
         if (L.kind != lkind::conv) continue;
+        report << "autotune conv#" << ci++ << " (median of " << trials << "):";
         // candidate engines: tensor-core direct, SIMT direct, FFT
         std::vector<int> cands{0, 3};
         if (znn_fft::supported(L.shape)) cands.push_back(1);
@@ -556,13 +559,16 @@ std::vector<int> executor::autotune(int trials) {
             }
             std::sort(ts.begin(), ts.end());
             const float med = ts[ts.size() / 2];
+            report << (e == 0 ? " direct " : e == 1 ? " fft " : " direct-simt ") << med << "ms";
             if (med < best) best = med, best_e = e;
         }
+        report << " -> " << ename(best_e) << "\n";
         L.engine = best_e;
         chosen.push_back(best_e);
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    desc_ += report.str();
     // the timing runs overwrote activations/gradients: not a training step
     return chosen;
 }
