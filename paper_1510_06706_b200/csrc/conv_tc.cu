@@ -1,11 +1,16 @@
 // Direct 3D (dilated) convolution as a tcgen05 implicit GEMM, 3xTF32.
 //
 // GEMM view (one CTA = 128 output voxels x NT output maps):
-//   D[v][n] = sum_k A[v][k] * B[n][k],   A[v][k] = src[b][c][v + s*w]  (k = c*T + w)
+//   D[v][n] = sum_k A[v][k] * B[n][k],   A[v][k] = src[b][c][v + s*w]
 //   fwd   : src = x, B = W                         (conv_direct.hpp:39-68)
-//   dgrad : src = g zero-haloed by s*(k-1) per side, B[i][o*T + w'] = W[o][i][T-1-w']
+//   dgrad : src = g zero-haloed by s*(k-1) per side, B[i][(o, w')] = W[o][i][T-1-w']
 //           i.e. conv_full_direct(g, reflect(k)) (conv_direct.hpp:74-101, engine.hpp:681)
 //           computed as a valid convolution: no bounds tests in the hot loop.
+// K order: k = ((wx*ky + wy)*f + c)*kz + wz — kernel rows (wx, wy) outermost,
+// so a 32-wide K-block touches one or two (wx, wy) rows of taps. A tile whose
+// voxels only see the zero halo through a tap row skips that K-block (dgrad of
+// the sparse layers spends up to 70% of its taps in the halo otherwise); the
+// inner (c, wz) order keeps a K-block's gathers on a few overlapping z-runs.
 // The reference's convergent-edge sum (engine.hpp:345-353, sum_accumulator.hpp)
 // is the K loop, accumulated in TMEM: no atomics, no locks. fp32 accuracy on
 // tensor cores: operands split into hi = tf32(x), lo = tf32(x - hi) and
@@ -13,14 +18,21 @@
 // CHUNK_KB K-blocks drained into fp32 registers (tensor-core accumulation
 // error grows with the number of accumulating MMAs).
 //
+// Operands: A (the im2col tile, hi|lo) lives in TMEM — the producers write it
+// with tcgen05.st and the MMA reads it from there (kind::tf32, A in TMEM), so
+// shared memory only carries B (pre-split weight panels, TMA, SWIZZLE_128B).
+// With both operands in shared memory the 3 MMAs per K-step read 8 KB per
+// 64 cycles — the whole shared-memory bandwidth — before any operand is written.
+//
+// TMEM columns: [0, nbuf*bstride) accumulator chunks, then NA A buffers of
+// 64 columns (32 hi + 32 lo).
 // Warp roles (384 threads, 1 CTA per SM; warps 10-11 idle):
-//   warps 0-7 : im2col producers for A: thread = one voxel row; warps 0-3
-//               fill the even and warps 4-7 the odd 32-wide K-blocks; hi/lo
-//               split in registers, 128B-swizzled K-major st.shared.v4
-//               and drain finished TMEM chunks: warp w owns lane quarter
-//               w % 4, warps 0-3 columns [0, NT/2) and 4-7 [NT/2, NT); then
-//               the epilogue (bias + transfer, coalesced stores)
-//   warp 8    : TMA producer for B (pre-split weight panels, SWIZZLE_128B)
+//   warps 0-7 : im2col producers: thread = one voxel row = one TMEM lane
+//               (warp w owns lane quarter w % 4); warps 0-3 fill the even and
+//               4-7 the odd active K-blocks; they also drain finished
+//               accumulator chunks (warps 0-3 columns [0, NT/2), 4-7
+//               [NT/2, NT)) and run the epilogue (bias + transfer, coalesced)
+//   warp 8    : TMA producer for B
 //   warp 9    : TMEM allocator + single-thread tcgen05.mma issuer
 #include <cuda.h>
 
@@ -42,14 +54,19 @@ struct tc_params {
     int n_real;       // real N (output maps of this GEMM)
     int nt;           // N tile (multiple of 16, <= NTMAX)
     int kblocks;
+    int K;            // real K (f_src * T)
     int stages;
     int nbuf;         // TMEM accumulator buffers
     int bstride;      // TMEM columns per buffer
+    int na;           // TMEM A buffers (64 columns each)
     int64_t rows;     // B * vox_out
     int64_t vox_out;  // voxels per output map
     int ox, oy, oz;   // output dims
     int sx, sy, sz;   // source dims
     int64_t src_vol;
+    // tap-row skipping: K group = one (wx, wy) kernel row, gsize = f_src*kz
+    int gsize, ky, dsx, dsy;
+    int vx0, vx1, vy0, vy1;  // source region that can be nonzero (inclusive)
 };
 
 template <int NTMAX>
@@ -58,50 +75,89 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                const float* __restrict__ src, const int* __restrict__ koff, float* __restrict__ out,
                const float* __restrict__ bias, int act, tc_params p) {
     extern __shared__ uint8_t smem_raw[];
+    __shared__ int s_nact;
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* base_ptr = smem_raw + (base - raw);
     const uint32_t b_bytes = uint32_t(p.nt) * 128u;
-    const uint32_t stage_bytes = 2u * BM * 128u + 2u * b_bytes;
+    const uint32_t stage_bytes = 2u * b_bytes;
     const uint32_t bar_base = base + uint32_t(p.stages) * stage_bytes;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
     auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(p.stages + s); };
     const uint32_t accf0 = bar_base + 8u * uint32_t(2 * p.stages);
     const uint32_t acce0 = accf0 + 32u;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 8));
+    const uint32_t af0 = acce0 + 32u;  // A buffer written (128 producer arrivals)
+    const uint32_t ae0 = af0 + 32u;    // A buffer consumed (MMA commit)
+    uint8_t* tail = base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 16);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tail);
+    uint16_t* list = reinterpret_cast<uint16_t*>(tail + 16);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t m0 = int64_t(blockIdx.x) * BM;
     const int n0 = blockIdx.y * p.nt;
-    const int nchunks = (p.kblocks + CHUNK_KB - 1) / CHUNK_KB;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 128 + 1);
+            mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8u * b, 1);
             mbar_init(acce0 + 8u * b, 256);
+            mbar_init(af0 + 8u * b, 128);
+            mbar_init(ae0 + 8u * b, 1);
         }
         fence_barrier_init();
     }
     if (warp == 9) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    if (warp == 10) {
+        // active K-blocks of this tile: a (wx, wy) tap row is live iff the
+        // tile's bounding box shifted by s*w meets the nonzero source region
+        const int64_t va = m0, vb = min(m0 + BM, p.rows) - 1;
+        const int64_t ba = va / p.vox_out, bb = vb / p.vox_out;
+        int x0 = 0, x1 = p.ox - 1, y0 = 0, y1 = p.oy - 1;
+        if (ba == bb) {
+            const int64_t ra = va - ba * p.vox_out, rb = vb - bb * p.vox_out;
+            const int64_t plane = int64_t(p.oy) * p.oz;
+            x0 = int(ra / plane), x1 = int(rb / plane);
+            if (x0 == x1) y0 = int((ra / p.oz) % p.oy), y1 = int((rb / p.oz) % p.oy);
+        }
+        int cnt = 0;
+        for (int kb0 = 0; kb0 < p.kblocks; kb0 += 32) {
+            const int kb = kb0 + lane;
+            bool act_kb = false;
+            if (kb < p.kblocks) {
+                const int g0 = (kb * BK) / p.gsize, g1 = (min(kb * BK + BK, p.K) - 1) / p.gsize;
+                for (int g = g0; g <= g1 && !act_kb; ++g) {
+                    const int wx = g / p.ky, wy = g - (g / p.ky) * p.ky;
+                    act_kb = x0 + p.dsx * wx <= p.vx1 && x1 + p.dsx * wx >= p.vx0 && y0 + p.dsy * wy <= p.vy1 &&
+                             y1 + p.dsy * wy >= p.vy0;
+                }
+            }
+            const uint32_t m = __ballot_sync(0xffffffffu, act_kb);
+            if (act_kb) list[cnt + __popc(m & ((1u << lane) - 1u))] = uint16_t(kb);
+            cnt += __popc(m);
+        }
+        if (lane == 0) s_nact = cnt;
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const int nact = s_nact;
+    const int nchunks = (nact + CHUNK_KB - 1) / CHUNK_KB;
+    const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
 
     if (warp < 8) {
-        // ---------------- im2col producers ----------------
+        // ---------------- im2col producers -> TMEM ----------------
         const int r = threadIdx.x & 127;
-        const int half = threadIdx.x >> 7;  // warp group: even (0) / odd (1) K-blocks
+        const int half = threadIdx.x >> 7;  // warp group: even (0) / odd (1) active K-blocks
         constexpr int NH = NTMAX / 2;
         const int col0 = half * NH;
         const int ncols = max(0, min(NH, p.nt - col0));
+        const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
         chunk_drainer<NH> D;
-        D.init(accf0, acce0, tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(col0), p.nbuf, p.bstride, ncols,
-               nchunks);
+        D.init(accf0, acce0, tmem + lane_base + uint32_t(col0), p.nbuf, p.bstride, ncols, nchunks);
         const int64_t v = m0 + r;
         const bool vok = v < p.rows;
         const float* sp = src;
@@ -113,15 +169,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
             const int tz = int(rem % p.oz);
             sp = src + b * int64_t(p.f_src) * p.src_vol + (int64_t(tx) * p.sy + ty) * p.sz + tz;
         }
-        const uint32_t row_off = uint32_t(r) * 128u;
-        const uint32_t sw = uint32_t(r & 7);
-        // Warp group `half` produces K-blocks kb = half, half+2, ... (all 32 k),
-        // so two K-blocks are always being gathered. (The proxy fence before
-        // each hand-off is a membar that waits for the thread's outstanding
-        // loads, so overlap has to come from independent warps, not prefetch.)
-        for (int kb = half; kb < p.kblocks; kb += 2) {
-            const int s = kb % p.stages;
-            const uint32_t ph = uint32_t(kb / p.stages) & 1u;
+        // this group's A buffers: half, half + 2, ... (< na); (a, use parity) tracked incrementally
+        int a = half;
+        uint32_t u = 0;
+        for (int j = half; j < nact; j += 2) {
+            const int kb = list[j];
             const int4* tb = reinterpret_cast<const int4*>(koff + kb * BK);
             float v[BK];
 #pragma unroll
@@ -132,25 +184,25 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                 v[4 * q + 2] = vok ? __ldg(sp + e.z) : 0.f;
                 v[4 * q + 3] = vok ? __ldg(sp + e.w) : 0.f;
             }
-            D.wait_stage(empty_bar(s), ph ^ 1u);
-            const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
-            const uint32_t a_lo = a_hi + BM * 128u;
+            D.wait_stage(ae0 + 8u * uint32_t(a), u ^ 1u);
+            tc_fence_after();
+            const uint32_t acol = tmem + lane_base + a_col0 + uint32_t(a) * 64u;
 #pragma unroll
-            for (int c = 0; c < BK / 4; ++c) {
-                float h[4], l[4];
+            for (int c = 0; c < BK / 8; ++c) {
+                float h[8], l[8];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    h[q] = tf32_hi(v[4 * c + q]);
-                    l[q] = tf32_rn(v[4 * c + q] - h[q]);
+                for (int q = 0; q < 8; ++q) {  // lo is exact in fp32; the MMA keeps its top tf32 bits
+                    h[q] = tf32_hi(v[8 * c + q]);
+                    l[q] = v[8 * c + q] - h[q];
                 }
-                const uint32_t off = row_off + ((uint32_t(c) ^ sw) << 4);
-                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_hi + off), "f"(h[0]), "f"(h[1]),
-                             "f"(h[2]), "f"(h[3]));
-                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_lo + off), "f"(l[0]), "f"(l[1]),
-                             "f"(l[2]), "f"(l[3]));
+                tmem_st8(acol + uint32_t(8 * c), h);
+                tmem_st8(acol + 32u + uint32_t(8 * c), l);
             }
-            fence_proxy_async();
-            mbar_arrive(full_bar(s));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(af0 + 8u * uint32_t(a));
+            a += 2;
+            if (a >= p.na) a = half, u ^= 1u;
             D.poll();
         }
         // ---------------- remaining drains + epilogue (this warp's columns) ----------------
@@ -171,47 +223,55 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     } else if (warp == 8) {
         // ---------------- TMA producer (pre-split weight panels) ----------------
         if (lane == 0) {
-            for (int kb = 0; kb < p.kblocks; ++kb) {
-                const int s = kb % p.stages;
-                const uint32_t ph = uint32_t(kb / p.stages) & 1u;
+            int s = 0;
+            uint32_t ph = 0;
+            for (int j = 0; j < nact; ++j) {
+                const int kb = list[j];
                 mbar_wait(empty_bar(s), ph ^ 1u);
-                const uint32_t b_hi = base + uint32_t(s) * stage_bytes + 2u * BM * 128u;
+                const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 mbar_expect_tx(full_bar(s), 2u * b_bytes);
                 tma_load_2d(b_hi, &tm_hi, full_bar(s), kb * BK, n0);
                 tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), kb * BK, n0);
+                if (++s == p.stages) s = 0, ph ^= 1u;
             }
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(BM, p.nt);
-            for (int kb = 0; kb < p.kblocks; ++kb) {
-                const int ch = kb / CHUNK_KB;
-                const int b = ch % p.nbuf;
-                const bool first = (kb % CHUNK_KB) == 0;
+            int b = 0, s = 0, a = 0, kc = 0;
+            uint32_t bph = 0, sph = 0, aph = 0;
+            for (int j = 0; j < nact; ++j) {
+                const bool first = kc == 0;
                 if (first) {
-                    mbar_wait(acce0 + 8u * uint32_t(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
+                    mbar_wait(acce0 + 8u * uint32_t(b), bph ^ 1u);
                     tc_fence_after();
                 }
                 const uint32_t d = tmem + uint32_t(b * p.bstride);
-                const int s = kb % p.stages;
-                mbar_wait(full_bar(s), uint32_t(kb / p.stages) & 1u);
+                mbar_wait(full_bar(s), sph);
+                mbar_wait(af0 + 8u * uint32_t(a), aph);
                 tc_fence_after();
-                const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
-                const uint32_t a_lo = a_hi + BM * 128u;
-                const uint32_t b_hi = a_lo + BM * 128u;
+                const uint32_t a_hi = tmem + a_col0 + uint32_t(a) * 64u;
+                const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
                     const uint32_t ko = uint32_t(kk) * 32u;  // 8 tf32 = 32 B along K
-                    const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
                     const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
-                    mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
-                    mma_tf32(d, ah, bl, idesc, 1u);
-                    mma_tf32(d, al, bh, idesc, 1u);
+                    const uint32_t ah = a_hi + uint32_t(8 * kk), al = a_hi + 32u + uint32_t(8 * kk);
+                    mma_tf32_ts(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                    mma_tf32_ts(d, ah, bl, idesc, 1u);
+                    mma_tf32_ts(d, al, bh, idesc, 1u);
                 }
                 mma_commit(empty_bar(s));
-                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == p.kblocks - 1) mma_commit(accf0 + 8u * uint32_t(b));
+                mma_commit(ae0 + 8u * uint32_t(a));
+                if (kc == CHUNK_KB - 1 || j == nact - 1) mma_commit(accf0 + 8u * uint32_t(b));
+                if (++s == p.stages) s = 0, sph ^= 1u;
+                if (++a == p.na) a = 0, aph ^= 1u;
+                if (++kc == CHUNK_KB) {
+                    kc = 0;
+                    if (++b == p.nbuf) b = 0, bph ^= 1u;
+                }
             }
         }
     }
@@ -224,22 +284,30 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     }
 }
 
+// K index -> (source channel c, tap t) for the (wx, wy)-outer order
+__device__ __forceinline__ void k_decode(int k, int f, int ky, int kz, int& c, int& t) {
+    const int gsize = f * kz;
+    const int g = k / gsize, rem = k - g * gsize;
+    c = rem / kz;
+    const int wz = rem - c * kz;
+    t = g * kz + wz;  // g = wx*ky + wy, so t = (wx*ky + wy)*kz + wz
+    (void)ky;
+}
+
 // Weight panels for the B operand, split hi/lo, zero padded to [npad][kpad].
-//   mode 0 (fwd)  : B[n][k] = W[n][k]                       (k = c*T + w)
-//   mode 1 (dgrad): B[n][k] = W[o][n][T-1-w'], k = o*T + w'  (transposed, reflected)
-__global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_in, int T, int K, int npad,
-                                int kpad, int mode, float* __restrict__ hi, float* __restrict__ lo) {
+//   mode 0 (fwd)  : B[n][(c, t)] = W[n][c][t]
+//   mode 1 (dgrad): B[n][(o, t)] = W[o][n][T-1-t]   (transposed, reflected)
+__global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_src, int f_in, int T, int ky, int kz,
+                                int K, int npad, int kpad, int mode, float* __restrict__ hi, float* __restrict__ lo) {
     const int64_t total = int64_t(npad) * kpad;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int n = int(i / kpad), k = int(i - int64_t(n) * kpad);
         float v = 0.f;
         if (n < n_real && k < K) {
-            if (mode == 0) {
-                v = w[int64_t(n) * K + k];
-            } else {
-                const int o = k / T, t = k - o * T;
-                v = w[(int64_t(o) * f_in + n) * T + (T - 1 - t)];
-            }
+            int c, t;
+            k_decode(k, f_src, ky, kz, c, t);
+            if (mode == 0) v = w[(int64_t(n) * f_src + c) * T + t];
+            else v = w[(int64_t(c) * f_in + n) * T + (T - 1 - t)];
         }
         const float h = tf32_hi(v);
         hi[i] = h;
@@ -249,12 +317,13 @@ __global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_i
 
 // im2col offsets: koff[k] = c*src_vol + linear(s*w) in source dims; padded
 // k -> 0 (their weights are zero).
-__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int T, int ky, int kz, int sx, int sy, int sz,
+__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int ky, int kz, int sx, int sy, int sz,
                        int64_t src_vol, int src_y, int src_z) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
         int e = 0;
         if (k < K) {
-            const int c = k / T, t = k - c * T;
+            int c, t;
+            k_decode(k, f_src, ky, kz, c, t);
             const int wx = t / (ky * kz), wy = (t / kz) % ky, wz = t % kz;
             e = int(int64_t(c) * src_vol + (int64_t(sx * wx) * src_y + sy * wy) * src_z + sz * wz);
         }
@@ -309,10 +378,11 @@ void launch_kernel(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& m
 }
 
 // One valid convolution src[B][f_src][sd] -> out[B][n_real][sd - s(k-1)] on
-// the tensor cores. wmode selects how the B panel is built from w.
+// the tensor cores. wmode selects how the B panel is built from w; only the
+// source box [v0, v0 + vn) can be nonzero (the rest is zero halo).
 void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w, dims3 sd, dims3 k, dims3 s,
                   const float* srcp, const float* w, int wmode, const float* bias, int act, float* outp,
-                  char* wsp, const char* what) {
+                  char* wsp, dims3 v0, dims3 vn, const char* what) {
     const int T = int(k.vol());
     const int K = f_src * T;
     const int kpad = int(ceil_div(K, BK) * BK);
@@ -321,6 +391,7 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     const int ntiles = int(ceil_div(n_real, nt));
     const int npad = ntiles * nt;
     const dims3 od{sd.x - s.x * (k.x - 1), sd.y - s.y * (k.y - 1), sd.z - s.z * (k.z - 1)};
+    require(kpad / BK < 65536, "conv_tc: too many K-blocks");
 
     const size_t panel = size_t(npad) * size_t(kpad);
     float* hi = reinterpret_cast<float*>(wsp);
@@ -329,10 +400,11 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
 
     int64_t blocks = ceil_div(int64_t(panel), 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    split_weights_k<<<unsigned(blocks), 256, 0, st>>>(w, n_real, f_in_w, T, K, npad, kpad, wmode, hi, lo);
+    split_weights_k<<<unsigned(blocks), 256, 0, st>>>(w, n_real, f_src, f_in_w, T, int(k.y), int(k.z), K, npad, kpad,
+                                                      wmode, hi, lo);
     launch_check("conv_tc_split_weights");
-    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, T, int(k.y), int(k.z), int(s.x), int(s.y),
-                                                           int(s.z), sd.vol(), int(sd.y), int(sd.z));
+    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, f_src, int(k.y), int(k.z), int(s.x),
+                                                           int(s.y), int(s.z), sd.vol(), int(sd.y), int(sd.z));
     launch_check("conv_tc_koff");
 
     const CUtensorMap mhi = make_panel_map(hi, kpad, npad, nt);
@@ -342,18 +414,26 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     p.n_real = n_real;
     p.nt = nt;
     p.kblocks = kpad / BK;
-    const int stage = 2 * BM * 128 + 2 * nt * 128;
-    p.stages = (216 * 1024) / stage;
-    if (p.stages > 6) p.stages = 6;
+    p.K = K;
     const int ntmax = nt <= 32 ? 32 : (nt <= 64 ? 64 : 128);
     p.bstride = ntmax;
-    p.nbuf = 4;  // 4 x NTMAX <= 512 TMEM columns
+    p.nbuf = ntmax == 128 ? 2 : 4;  // + na x 64 A columns <= 512 TMEM columns
+    p.na = 4;                       // two A buffers per producer group: a group writes ahead of the MMA
     p.vox_out = od.vol();
     p.rows = Bn * p.vox_out;
     p.ox = int(od.x), p.oy = int(od.y), p.oz = int(od.z);
     p.sx = int(sd.x), p.sy = int(sd.y), p.sz = int(sd.z);
     p.src_vol = sd.vol();
-    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 8) + 16 + 1024;
+    p.gsize = f_src * int(k.z);
+    p.ky = int(k.y);
+    p.dsx = int(s.x), p.dsy = int(s.y);
+    p.vx0 = int(v0.x), p.vx1 = int(v0.x + vn.x - 1), p.vy0 = int(v0.y), p.vy1 = int(v0.y + vn.y - 1);
+    const int stage = 2 * nt * 128;
+    const size_t fixed = 1024 + 8 * size_t(16) + 16 + 2 * size_t(p.kblocks) + 64;
+    p.stages = int((size_t(220) * 1024 - fixed) / size_t(stage + 16));
+    if (p.stages > 8) p.stages = 8;
+    require(p.stages >= 2, "conv_tc: K too long for the shared-memory budget");
+    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
     const dim3 grid{unsigned(ceil_div(p.rows, BM)), unsigned(ntiles), 1u};
     if (ntmax == 32) launch_kernel<32>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
     else if (ntmax == 64) launch_kernel<64>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
@@ -404,7 +484,7 @@ void conv_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const flo
                  float* y, scratch& ws) {
     char* wsp = static_cast<char*>(ws.get(panel_bytes(int(c.f_in), int(c.f_out), c.taps())));
     launch_valid(st, c.B, int(c.f_in), int(c.f_out), int(c.f_in), c.n, c.k, c.s, x, w, 0, bias, act, y, wsp,
-                 "conv_fwd_tc");
+                 dims3{0, 0, 0}, c.n, "conv_fwd_tc");
 }
 
 void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const float* w, float* dx, scratch& ws) {
@@ -420,7 +500,7 @@ void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const f
                                                   int(P.y), int(P.z), gp);
     launch_check("conv_dgrad_tc_pad");
     launch_valid(st, c.B, int(c.f_out), int(c.f_in), int(c.f_in), gd, c.k, c.s, gp, w, 1, nullptr, 3, dx,
-                 wsp + gpad, "conv_dgrad_tc");
+                 wsp + gpad, P, c.m, "conv_dgrad_tc");
 }
 
 }  // namespace znn_gpu

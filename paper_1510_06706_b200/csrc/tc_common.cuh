@@ -74,6 +74,16 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::tf32 (A read from TMEM: lane = row,
+// one 32-bit column per K element)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -116,6 +126,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+// 8 consecutive 32-bit TMEM columns of this thread's lane (warp-collective)
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+                 "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Accumulator drain: tensor-core fp32 accumulation loses precision roughly
@@ -158,29 +177,29 @@ template <int NH>
 struct chunk_drainer {
     drain_acc<NH> A;
     int next = 0;
+    int buf = 0;          // next % nbuf, tracked incrementally (no integer division in the poll loop)
+    uint32_t phase = 0;   // (next / nbuf) & 1
     uint32_t accf0, acce0, lane_base;
     int nbuf, bstride, ncols, nchunks;
 
     __device__ __forceinline__ void init(uint32_t f0, uint32_t e0, uint32_t lb, int nb, int bs, int nc_cols,
                                          int nc) {
         accf0 = f0, acce0 = e0, lane_base = lb, nbuf = nb, bstride = bs, ncols = nc_cols, nchunks = nc;
-        next = 0;
+        next = 0, buf = 0, phase = 0;
         A.zero();
     }
     __device__ __forceinline__ void drain_one() {
-        const int b = next % nbuf;
-        mbar_wait(accf0 + 8u * uint32_t(b), uint32_t(next / nbuf) & 1u);
+        mbar_wait(accf0 + 8u * uint32_t(buf), phase);
         tc_fence_after();
-        if (ncols > 0) A.add(lane_base + uint32_t(b * bstride), ncols);
+        if (ncols > 0) A.add(lane_base + uint32_t(buf * bstride), ncols);
         tc_fence_before();
-        mbar_arrive(acce0 + 8u * uint32_t(b));
+        mbar_arrive(acce0 + 8u * uint32_t(buf));
         ++next;
+        if (++buf == nbuf) buf = 0, phase ^= 1u;
     }
     __device__ __forceinline__ void poll() {
         while (next < nchunks) {
-            const int b = next % nbuf;
-            const bool ready =
-                __shfl_sync(0xffffffffu, mbar_test(accf0 + 8u * uint32_t(b), uint32_t(next / nbuf) & 1u) ? 1 : 0, 0);
+            const bool ready = __shfl_sync(0xffffffffu, mbar_test(accf0 + 8u * uint32_t(buf), phase) ? 1 : 0, 0);
             if (!ready) break;
             drain_one();
         }
