@@ -5,19 +5,21 @@
 // GEMM view: rows R = (i, w) (f_in*T of them, 128 per tile), columns = output
 // maps o (<= 128 per tile), K = output voxels of every patch (32 per stage,
 // never straddling a patch).
-//   A (x rows, shifted windows) : gathered by producer warps with coalesced
-//       row loads (a warp reads 32 consecutive voxels of one row), split into
-//       tf32 hi/lo in registers, stored 128B-swizzled;
+//   A (x rows, shifted windows) : in TMEM. Each producer warp owns 32 rows (its
+//       TMEM lane quarter): it gathers them with coalesced row loads (lane =
+//       voxel), transposes the 32x32 block through a private shared-memory
+//       tile (conflict-free, pitch 33), splits hi/lo and writes its lanes with
+//       tcgen05.st; the MMA reads A from TMEM (kind::tf32).
 //   B (g rows)                  : pre-split into hi/lo panels [B*f_out][mpad]
 //       by one memory-bound pass, then TMA-loaded (SWIZZLE_128B).
 // Each CTA owns a contiguous K range (split-K); partial tiles land in a
 // workspace [split][o][R] and a fixed-order reduction sums them
 // (deterministic).
 //
-// Warps: 0-7 producers (warps 0-3 even, 4-7 odd K-blocks) that also drain
-// finished TMEM chunks (warp w: lane quarter w % 4, column half w / 4) and
-// run the epilogue; 8 TMA producer; 9 TMEM alloc + MMA issuer; 10-11 idle
-// (registers are granted per 4-warp group).
+// Warps: 0-7 producers (warps 0-3 even, 4-7 odd K-blocks; warp w owns A rows
+// / TMEM lanes 32*(w%4)..+31) that also drain finished TMEM chunks (column
+// half w / 4) and run the epilogue; 8 TMA producer; 9 TMEM alloc + MMA
+// issuer; 10-11 idle (registers are granted per 4-warp group).
 #include <cuda.h>
 
 #include "ops.hpp"
@@ -34,11 +36,12 @@ using namespace znn_tc;
 constexpr int THREADS = 384;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CHUNK_KB = 8;
+constexpr int TP = 33;  // transpose tile pitch (floats)
 
 struct wg_params {
     int f_in, f_out, T, nt;
     int mrows;  // f_in * T
-    int stages, nbuf, bstride;
+    int stages, nbuf, bstride, na;
     int64_t kb_per_patch, kb_total, kb_per_split;
     int64_t nvol, mvol;
     int ny, nz, my, mz;
@@ -55,13 +58,17 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* base_ptr = smem_raw + (base - raw);
     const uint32_t b_bytes = uint32_t(p.nt) * 128u;
-    const uint32_t stage_bytes = 2u * BM * 128u + 2u * b_bytes;
+    const uint32_t stage_bytes = 2u * b_bytes;
     const uint32_t bar_base = base + uint32_t(p.stages) * stage_bytes;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
     auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(p.stages + s); };
     const uint32_t accf0 = bar_base + 8u * uint32_t(2 * p.stages);
     const uint32_t acce0 = accf0 + 32u;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 8));
+    const uint32_t af0 = acce0 + 32u;
+    const uint32_t ae0 = af0 + 32u;
+    uint8_t* tail = base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 16);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tail);
+    float* tpose = reinterpret_cast<float*>(tail + 16);  // 8 warps x [32][TP]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r0 = blockIdx.x * BM;    // first (i, w) row of this tile
@@ -74,12 +81,14 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : -1;
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 128 + 1);
+            mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8u * b, 1);
             mbar_init(acce0 + 8u * b, 256);
+            mbar_init(af0 + 8u * b, 128);
+            mbar_init(ae0 + 8u * b, 1);
         }
         fence_barrier_init();
     }
@@ -88,20 +97,25 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
 
     if (warp < 8) {
         constexpr int NH = NTMAX / 2;
         const int grp = warp >> 2;  // 0: even K-blocks, 1: odd K-blocks
-        const int wq = warp & 3;    // this warp gathers A rows wq, wq+4, ...
+        const int wq = warp & 3;    // rows / TMEM lanes 32*wq .. 32*wq + 31
         const int col0 = grp * NH;
         const int ncols = max(0, min(NH, p.nt - col0));
+        const uint32_t lane_base = uint32_t(wq * 32) << 16;
         chunk_drainer<NH> D;
-        D.init(accf0, acce0, tmem + (uint32_t(wq * 32) << 16) + uint32_t(col0), p.nbuf, p.bstride, ncols, nchunks);
+        D.init(accf0, acce0, tmem + lane_base + uint32_t(col0), p.nbuf, p.bstride, ncols, nchunks);
         const int mvol = int(p.mvol);
         const int myz = p.my * p.mz;
-        // rows wq + 4t alternate between two swizzle phases ((row & 7) = wq or wq + 4)
-        const uint32_t offA = sw128_off(uint32_t(wq), uint32_t(lane));
-        const uint32_t offB = sw128_off(uint32_t(wq + 4), uint32_t(lane));
+        float* tp = tpose + warp * (32 * TP);
+        int ro[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
+        int a = grp;
+        uint32_t u = 0;
         for (int kb = grp; kb < kblocks; kb += 2) {
             const int64_t q = q0 + kb;
             const int64_t pb = q / p.kb_per_patch;
@@ -115,26 +129,35 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 const int vz = r2 - vy * p.mz;
                 xp = x + pb * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
             }
-            float av[BM / 4];
+            float av[32];
 #pragma unroll
-            for (int t = 0; t < BM / 4; ++t) {
-                const int ro = rowoff[wq + 4 * t];
-                av[t] = (vok && ro >= 0) ? __ldg(xp + ro) : 0.f;
-            }
-            const int s = kb % p.stages;
-            const uint32_t ph = uint32_t(kb / p.stages) & 1u;
-            D.wait_stage(empty_bar(s), ph ^ 1u);
-            const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
-            const uint32_t a_lo = a_hi + BM * 128u;
+            for (int t = 0; t < 32; ++t) av[t] = (vok && ro[t] >= 0) ? __ldg(xp + ro[t]) : 0.f;
+            // 32x32 transpose through this warp's tile: row t, voxel lane -> lane t, column voxel
+            __syncwarp();
 #pragma unroll
-            for (int t = 0; t < BM / 4; ++t) {
-                const uint32_t off = ((t & 1) ? offB : offA) + uint32_t(t >> 1) * 1024u;
-                const float h = tf32_hi(av[t]);
-                asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_hi + off), "f"(h));
-                asm volatile("st.shared.f32 [%0], %1;" ::"r"(a_lo + off), "f"(tf32_rn(av[t] - h)));
+            for (int t = 0; t < 32; ++t) tp[t * TP + lane] = av[t];
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) av[c] = tp[lane * TP + c];
+            D.wait_stage(ae0 + 8u * uint32_t(a), u ^ 1u);
+            tc_fence_after();
+            const uint32_t acol = tmem + lane_base + a_col0 + uint32_t(a) * 64u;
+#pragma unroll
+            for (int c = 0; c < BK / 8; ++c) {
+                float h[8], l[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {  // lo is exact in fp32; the MMA keeps its top tf32 bits
+                    h[e] = tf32_hi(av[8 * c + e]);
+                    l[e] = av[8 * c + e] - h[e];
+                }
+                tmem_st8(acol + uint32_t(8 * c), h);
+                tmem_st8(acol + 32u + uint32_t(8 * c), l);
             }
-            fence_proxy_async();
-            mbar_arrive(full_bar(s));
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(af0 + 8u * uint32_t(a));
+            a += 2;
+            if (a >= p.na) a = grp, u ^= 1u;
             D.poll();
         }
         // ---------------- remaining drains + epilogue (this warp's columns) ----------------
@@ -151,50 +174,58 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     } else if (warp == 8) {
         // ---------------- TMA producer: g panels ----------------
         if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
             for (int kb = 0; kb < kblocks; ++kb) {
                 const int64_t q = q0 + kb;
                 const int64_t pb = q / p.kb_per_patch;
                 const int vcol = int(q - pb * p.kb_per_patch) * BK;
                 const int row = int(pb * p.f_out) + n0;
-                const int s = kb % p.stages;
-                mbar_wait(empty_bar(s), (uint32_t(kb / p.stages) & 1u) ^ 1u);
-                const uint32_t b_hi = base + uint32_t(s) * stage_bytes + 2u * BM * 128u;
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 mbar_expect_tx(full_bar(s), 2u * b_bytes);
                 tma_load_2d(b_hi, &tm_hi, full_bar(s), vcol, row);
                 tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), vcol, row);
+                if (++s == p.stages) s = 0, ph ^= 1u;
             }
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(BM, p.nt);
+            int b = 0, s = 0, a = 0, kc = 0;
+            uint32_t bph = 0, sph = 0, aph = 0;
             for (int kb = 0; kb < kblocks; ++kb) {
-                const int ch = kb / CHUNK_KB;
-                const int b = ch % p.nbuf;
-                const bool first = (kb % CHUNK_KB) == 0;
+                const bool first = kc == 0;
                 if (first) {
-                    mbar_wait(acce0 + 8u * uint32_t(b), (uint32_t(ch / p.nbuf) & 1u) ^ 1u);
+                    mbar_wait(acce0 + 8u * uint32_t(b), bph ^ 1u);
                     tc_fence_after();
                 }
                 const uint32_t d = tmem + uint32_t(b * p.bstride);
-                const int s = kb % p.stages;
-                mbar_wait(full_bar(s), uint32_t(kb / p.stages) & 1u);
+                mbar_wait(full_bar(s), sph);
+                mbar_wait(af0 + 8u * uint32_t(a), aph);
                 tc_fence_after();
-                const uint32_t a_hi = base + uint32_t(s) * stage_bytes;
-                const uint32_t a_lo = a_hi + BM * 128u;
-                const uint32_t b_hi = a_lo + BM * 128u;
+                const uint32_t a_hi = tmem + a_col0 + uint32_t(a) * 64u;
+                const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 const uint32_t b_lo = b_hi + b_bytes;
 #pragma unroll
                 for (int kk = 0; kk < BK / 8; ++kk) {
                     const uint32_t ko = uint32_t(kk) * 32u;
-                    const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
                     const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
-                    mma_tf32(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
-                    mma_tf32(d, ah, bl, idesc, 1u);
-                    mma_tf32(d, al, bh, idesc, 1u);
+                    const uint32_t ah = a_hi + uint32_t(8 * kk), al = a_hi + 32u + uint32_t(8 * kk);
+                    mma_tf32_ts(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                    mma_tf32_ts(d, ah, bl, idesc, 1u);
+                    mma_tf32_ts(d, al, bh, idesc, 1u);
                 }
                 mma_commit(empty_bar(s));
-                if ((kb % CHUNK_KB) == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit(accf0 + 8u * uint32_t(b));
+                mma_commit(ae0 + 8u * uint32_t(a));
+                if (kc == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit(accf0 + 8u * uint32_t(b));
+                if (++s == p.stages) s = 0, sph ^= 1u;
+                if (++a == p.na) a = 0, aph ^= 1u;
+                if (++kc == CHUNK_KB) {
+                    kc = 0;
+                    if (++b == p.nbuf) b = 0, bph ^= 1u;
+                }
             }
         }
     }
@@ -261,10 +292,12 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     const int ntiles = int(ceil_div(c.f_out, p.nt));
     const int ntmax = p.nt <= 32 ? 32 : (p.nt <= 64 ? 64 : 128);
     p.bstride = ntmax;
-    p.nbuf = 4;
-    const int stage = 2 * BM * 128 + 2 * p.nt * 128;
-    p.stages = (216 * 1024) / stage;
-    if (p.stages > 6) p.stages = 6;
+    p.nbuf = ntmax == 128 ? 2 : 4;  // + na x 64 A columns <= 512 TMEM columns
+    p.na = 4;
+    const int stage = 2 * p.nt * 128;
+    const size_t fixed = 1024 + 8 * size_t(16) + 16 + sizeof(float) * 8 * 32 * TP + 64;
+    p.stages = int((size_t(220) * 1024 - fixed) / size_t(stage + 16));
+    if (p.stages > 8) p.stages = 8;
     p.nvol = c.n.vol();
     p.mvol = c.m.vol();
     p.ny = int(c.n.y), p.nz = int(c.n.z), p.my = int(c.m.y), p.mz = int(c.m.z);
@@ -297,7 +330,7 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     launch_check("conv_wgrad_tc_rowoff");
     const CUtensorMap mhi = make_panel_map_rows(ghi, mpad, grows, p.nt);
     const CUtensorMap mlo = make_panel_map_rows(glo, mpad, grows, p.nt);
-    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 8) + 16 + 1024;
+    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
     if (ntmax == 32) launch_wgrad<32>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
     else if (ntmax == 64) launch_wgrad<64>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
