@@ -332,21 +332,24 @@ __global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int ky
 }
 
 // g [maps][m] -> gp [maps][m + 2P] with a zero halo of P = s*(k-1) per side.
+// grid: x over the padded voxels of one map (32-bit index math), y over maps.
 __global__ void pad_halo_k(const float* __restrict__ g, int64_t maps, int mx, int my, int mz, int px, int py, int pz,
                            float* __restrict__ gp) {
     const int gx = mx + 2 * px, gy = my + 2 * py, gz = mz + 2 * pz;
-    const int64_t pv = int64_t(gx) * gy * gz;
+    const unsigned pv = unsigned(gx) * unsigned(gy) * unsigned(gz);
+    const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= pv) return;
+    const unsigned gyz = unsigned(gy) * unsigned(gz);
+    const int x = int(r / gyz);
+    const unsigned r2 = r - unsigned(x) * gyz;
+    const int y = int(r2 / unsigned(gz));
+    const int z = int(r2 - unsigned(y) * unsigned(gz));
+    const int ux = x - px, uy = y - py, uz = z - pz;
+    const bool in = unsigned(ux) < unsigned(mx) && unsigned(uy) < unsigned(my) && unsigned(uz) < unsigned(mz);
+    const int src = (ux * my + uy) * mz + uz;
     const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t total = maps * pv;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t map = i / pv;
-        const int r = int(i - map * pv);
-        const int x = r / (gy * gz) - px, y = (r / gz) % gy - py, z = r % gz - pz;
-        float v = 0.f;
-        if (unsigned(x) < unsigned(mx) && unsigned(y) < unsigned(my) && unsigned(z) < unsigned(mz))
-            v = g[map * mv + (int64_t(x) * my + y) * mz + z];
-        gp[i] = v;
-    }
+    for (int64_t map = blockIdx.y; map < maps; map += gridDim.y)
+        gp[map * int64_t(pv) + r] = in ? __ldg(g + map * mv + src) : 0.f;
 }
 
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -494,10 +497,9 @@ void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const f
     const size_t gpad = (gbytes + 1023) & ~size_t(1023);
     char* wsp = static_cast<char*>(ws.get(gpad + panel_bytes(int(c.f_out), int(c.f_in), c.taps())));
     float* gp = reinterpret_cast<float*>(wsp);
-    int64_t blocks = ceil_div(c.B * c.f_out * gd.vol(), 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    pad_halo_k<<<unsigned(blocks), 256, 0, st>>>(g, c.B * c.f_out, int(c.m.x), int(c.m.y), int(c.m.z), int(P.x),
-                                                  int(P.y), int(P.z), gp);
+    const int64_t pmaps = c.B * c.f_out;
+    const dim3 pgrid(unsigned(ceil_div(gd.vol(), 256)), unsigned(pmaps < 65535 ? pmaps : 65535), 1u);
+    pad_halo_k<<<pgrid, 256, 0, st>>>(g, pmaps, int(c.m.x), int(c.m.y), int(c.m.z), int(P.x), int(P.y), int(P.z), gp);
     launch_check("conv_dgrad_tc_pad");
     launch_valid(st, c.B, int(c.f_out), int(c.f_in), int(c.f_in), gd, c.k, c.s, gp, w, 1, nullptr, 3, dx,
                  wsp + gpad, P, c.m, "conv_dgrad_tc");

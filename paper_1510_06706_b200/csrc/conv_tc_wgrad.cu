@@ -22,6 +22,8 @@
 // issuer; 10-11 idle (registers are granted per 4-warp group).
 #include <cuda.h>
 
+#include <algorithm>
+
 #include "ops.hpp"
 #include "tc_common.cuh"
 
@@ -247,16 +249,24 @@ __global__ void rowoff_k(int* __restrict__ out, int mrows, int T, int ky, int kz
     }
 }
 
-// g [rows][mvol] -> hi/lo [rows][mpad] (zero padded columns): the TMA panels
+// g [rows][mvol] -> hi/lo [rows][mpad] (zero padded columns): the TMA panels.
+// grid: x over columns (float4 groups), y over rows.
 __global__ void split_rows_k(const float* __restrict__ g, int64_t rows, int64_t mvol, int64_t mpad,
                              float* __restrict__ hi, float* __restrict__ lo) {
-    const int64_t total = rows * mpad;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = i / mpad, c = i - r * mpad;
-        const float v = c < mvol ? g[r * mvol + c] : 0.f;
-        const float h = tf32_hi(v);
-        hi[i] = h;
-        lo[i] = tf32_rn(v - h);
+    const int64_t c0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (c0 >= mpad) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const float* src = g + r * mvol;
+        float v[4], h[4], l[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = c0 + q < mvol ? __ldg(src + c0 + q) : 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            h[q] = tf32_hi(v[q]);
+            l[q] = tf32_rn(v[q] - h[q]);
+        }
+        *reinterpret_cast<float4*>(hi + r * mpad + c0) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(lo + r * mpad + c0) = make_float4(l[0], l[1], l[2], l[3]);
     }
 }
 
@@ -304,10 +314,23 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     p.kb_per_patch = ceil_div(p.mvol, BK);
     p.kb_total = p.kb_per_patch * c.B;
     const int mtiles = int(ceil_div(p.mrows, BM));
-    int64_t splits = ceil_div(int64_t(2 * 148), int64_t(mtiles) * ntiles);
-    const int64_t max_splits = ceil_div(p.kb_total, 4 * CHUNK_KB);
-    if (splits > max_splits) splits = max_splits;
-    if (splits < 1) splits = 1;
+    // split-K factor: fill whole waves of 148 SMs (one CTA each). The first
+    // split count >= 2 waves whose last wave is >= 97% full, else the best
+    // fill up to max(32, 8 waves' worth) splits (a 2.4-wave grid idles 20% of the GPU in its tail).
+    const int64_t tiles = int64_t(mtiles) * ntiles;
+    const int64_t max_splits = std::max<int64_t>(
+        1, std::min<int64_t>(std::max<int64_t>(32, ceil_div(8 * 148, tiles)), ceil_div(p.kb_total, 4 * CHUNK_KB)));
+    int64_t splits = 1;
+    double best = -1.0;
+    for (int64_t sp = 1; sp <= max_splits; ++sp) {
+        const int64_t ctas = tiles * sp;
+        const double eff = double(ctas) / double(ceil_div(ctas, 148) * 148);
+        if (ctas >= 2 * 148 && eff >= 0.97) {
+            splits = sp;
+            break;
+        }
+        if (eff > best + 1e-9) best = eff, splits = sp;
+    }
     p.kb_per_split = ceil_div(p.kb_total, splits);
     splits = ceil_div(p.kb_total, p.kb_per_split);
 
@@ -320,9 +343,8 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     float* glo = ghi + panel;
     float* partials = glo + panel;
     int* rowoff = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(partials + part) + 255) & ~uintptr_t(255));
-    int64_t sb = ceil_div(int64_t(panel), 256);
-    if (sb > 148 * 16) sb = 148 * 16;
-    split_rows_k<<<unsigned(sb), 256, 0, st>>>(g, grows, p.mvol, mpad, ghi, glo);
+    const dim3 sgrid(unsigned(ceil_div(mpad / 4, 256)), unsigned(grows < 65535 ? grows : 65535), 1u);
+    split_rows_k<<<sgrid, 256, 0, st>>>(g, grows, p.mvol, mpad, ghi, glo);
     launch_check("conv_wgrad_tc_split");
     rowoff_k<<<unsigned(ceil_div(p.mrows, 256)), 256, 0, st>>>(rowoff, p.mrows, p.T, int(c.k.y), int(c.k.z),
                                                                int(c.s.x), int(c.s.y), int(c.s.z), p.ny, p.nz,

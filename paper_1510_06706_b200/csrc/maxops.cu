@@ -16,61 +16,63 @@ namespace {
 
 constexpr int kThreads = 256;
 
-inline unsigned grid_for(int64_t n) {
-    int64_t b = ceil_div(n, kThreads);
-    if (b > 148 * 32) b = 148 * 32;
-    return unsigned(b < 1 ? 1 : b);
+// Grid: x covers the voxels of one map (32-bit index math only — 64-bit
+// division per voxel made these kernels issue-bound at ~15% of HBM), y the
+// maps (grid-strided past 65535).
+inline dim3 grid2(int64_t per_map, int64_t maps) {
+    const int64_t gx = ceil_div(per_map, kThreads);
+    return dim3(unsigned(gx < 1 ? 1 : gx), unsigned(maps < 65535 ? (maps < 1 ? 1 : maps) : 65535), 1u);
 }
 
-__global__ void maxfilter_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny,
-                                int nz, int mx, int my, int mz, int kx, int ky, int kz, int sx,
-                                int sy, int sz, float* __restrict__ y,
-                                int32_t* __restrict__ mask) {
-    const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t nv = int64_t(nx) * ny * nz;
-    const int64_t total = maps * mv;
-    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total;
-         o += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t map = o / mv;
-        const int64_t r = o - map * mv;
-        const int i = int(r / (int64_t(my) * mz));
-        const int j = int((r / mz) % my);
-        const int l = int(r % mz);
-        const float* xm = x + map * nv;
-        int best_idx = (i * ny + j) * nz + l;
-        float best = xm[best_idx];
+__global__ void __launch_bounds__(kThreads) maxfilter_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny,
+                                                            int nz, int mx, int my, int mz, int kx, int ky, int kz,
+                                                            int sx, int sy, int sz, float* __restrict__ y,
+                                                            int32_t* __restrict__ mask) {
+    const unsigned mv = unsigned(mx) * unsigned(my) * unsigned(mz);
+    const unsigned r = blockIdx.x * kThreads + threadIdx.x;
+    if (r >= mv) return;
+    const unsigned myz = unsigned(my) * unsigned(mz);
+    const int i = int(r / myz);
+    const unsigned r2 = r - unsigned(i) * myz;
+    const int j = int(r2 / unsigned(mz));
+    const int l = int(r2 - unsigned(j) * unsigned(mz));
+    const int base = (i * ny + j) * nz + l;
+    for (int64_t map = blockIdx.y; map < maps; map += gridDim.y) {
+        const float* xm = x + map * (int64_t(nx) * ny * nz);
+        int best_idx = base;
+        float best = __ldg(xm + base);
         for (int a = 0; a < kx; ++a)
             for (int b = 0; b < ky; ++b)
                 for (int c = 0; c < kz; ++c) {
-                    const int idx = ((i + sx * a) * ny + (j + sy * b)) * nz + (l + sz * c);
-                    const float v = xm[idx];
+                    const int idx = base + (sx * a * ny + sy * b) * nz + sz * c;
+                    const float v = __ldg(xm + idx);
                     if (v > best) {
                         best = v;
                         best_idx = idx;
                     }
                 }
-        y[o] = best;
-        mask[o] = best_idx;
+        y[map * int64_t(mv) + r] = best;
+        mask[map * int64_t(mv) + r] = best_idx;
     }
 }
 
 // dx[t] = sum over windows o whose argmax is t of g[o]; windows visited in
 // ascending flat order of o, the order the reference accumulates in
 // (maxops.hpp:176-181), so fp32 sums match it bit for bit.
-__global__ void maxfilter_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
-                                int64_t maps, int nx, int ny, int nz, int mx, int my, int mz,
-                                int kx, int ky, int kz, int sx, int sy, int sz,
-                                float* __restrict__ dx) {
+__global__ void __launch_bounds__(kThreads) maxfilter_bwd_k(const float* __restrict__ g,
+                                                            const int32_t* __restrict__ mask, int64_t maps, int nx,
+                                                            int ny, int nz, int mx, int my, int mz, int kx, int ky,
+                                                            int kz, int sx, int sy, int sz, float* __restrict__ dx) {
+    const unsigned nv = unsigned(nx) * unsigned(ny) * unsigned(nz);
+    const unsigned tr = blockIdx.x * kThreads + threadIdx.x;
+    if (tr >= nv) return;
+    const unsigned nyz = unsigned(ny) * unsigned(nz);
+    const int ti = int(tr / nyz);
+    const unsigned r2 = tr - unsigned(ti) * nyz;
+    const int tj = int(r2 / unsigned(nz));
+    const int tl = int(r2 - unsigned(tj) * unsigned(nz));
     const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t nv = int64_t(nx) * ny * nz;
-    const int64_t total = maps * nv;
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
-         t += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t map = t / nv;
-        const int tr = int(t - map * nv);
-        const int ti = tr / (ny * nz);
-        const int tj = (tr / nz) % ny;
-        const int tl = tr % nz;
+    for (int64_t map = blockIdx.y; map < maps; map += gridDim.y) {
         const float* gm = g + map * mv;
         const int32_t* mm = mask + map * mv;
         float acc = 0.f;
@@ -84,63 +86,62 @@ __global__ void maxfilter_bwd_k(const float* __restrict__ g, const int32_t* __re
                     const int ol = tl - sz * c;
                     if (ol < 0 || ol >= mz) continue;
                     const int o = (oi * my + oj) * mz + ol;
-                    if (mm[o] == tr) acc += gm[o];
+                    if (__ldg(mm + o) == int(tr)) acc += __ldg(gm + o);
                 }
             }
         }
-        dx[t] = acc;
+        dx[map * int64_t(nv) + tr] = acc;
     }
 }
 
-__global__ void maxpool_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny, int nz,
-                              int px, int py, int pz, float* __restrict__ y,
-                              int32_t* __restrict__ mask) {
+__global__ void __launch_bounds__(kThreads) maxpool_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny,
+                                                          int nz, int px, int py, int pz, float* __restrict__ y,
+                                                          int32_t* __restrict__ mask) {
     const int mx = nx / px, my = ny / py, mz = nz / pz;
-    const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t nv = int64_t(nx) * ny * nz;
-    const int64_t total = maps * mv;
-    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < total;
-         o += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t map = o / mv;
-        const int64_t r = o - map * mv;
-        const int bi = int(r / (int64_t(my) * mz));
-        const int bj = int((r / mz) % my);
-        const int bl = int(r % mz);
-        const float* xm = x + map * nv;
-        int best_idx = ((bi * px) * ny + bj * py) * nz + bl * pz;
-        float best = xm[best_idx];
+    const unsigned mv = unsigned(mx) * unsigned(my) * unsigned(mz);
+    const unsigned r = blockIdx.x * kThreads + threadIdx.x;
+    if (r >= mv) return;
+    const unsigned myz = unsigned(my) * unsigned(mz);
+    const int bi = int(r / myz);
+    const unsigned r2 = r - unsigned(bi) * myz;
+    const int bj = int(r2 / unsigned(mz));
+    const int bl = int(r2 - unsigned(bj) * unsigned(mz));
+    const int base = ((bi * px) * ny + bj * py) * nz + bl * pz;
+    for (int64_t map = blockIdx.y; map < maps; map += gridDim.y) {
+        const float* xm = x + map * (int64_t(nx) * ny * nz);
+        int best_idx = base;
+        float best = __ldg(xm + base);
         for (int a = 0; a < px; ++a)
             for (int b = 0; b < py; ++b)
                 for (int c = 0; c < pz; ++c) {
-                    const int idx = ((bi * px + a) * ny + (bj * py + b)) * nz + (bl * pz + c);
-                    const float v = xm[idx];
+                    const int idx = base + (a * ny + b) * nz + c;
+                    const float v = __ldg(xm + idx);
                     if (v > best) {
                         best = v;
                         best_idx = idx;
                     }
                 }
-        y[o] = best;
-        mask[o] = best_idx;
+        y[map * int64_t(mv) + r] = best;
+        mask[map * int64_t(mv) + r] = best_idx;
     }
 }
 
-__global__ void maxpool_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
-                              int64_t maps, int mx, int my, int mz, int px, int py, int pz,
-                              float* __restrict__ dx) {
+__global__ void __launch_bounds__(kThreads) maxpool_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
+                                                          int64_t maps, int mx, int my, int mz, int px, int py, int pz,
+                                                          float* __restrict__ dx) {
     const int nx = mx * px, ny = my * py, nz = mz * pz;
+    const unsigned nv = unsigned(nx) * unsigned(ny) * unsigned(nz);
+    const unsigned tr = blockIdx.x * kThreads + threadIdx.x;
+    if (tr >= nv) return;
+    const unsigned nyz = unsigned(ny) * unsigned(nz);
+    const int ti = int(tr / nyz);
+    const unsigned r2 = tr - unsigned(ti) * nyz;
+    const int tj = int(r2 / unsigned(nz));
+    const int tl = int(r2 - unsigned(tj) * unsigned(nz));
+    const int o = ((ti / px) * my + (tj / py)) * mz + (tl / pz);
     const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t nv = int64_t(nx) * ny * nz;
-    const int64_t total = maps * nv;
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
-         t += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t map = t / nv;
-        const int tr = int(t - map * nv);
-        const int ti = tr / (ny * nz);
-        const int tj = (tr / nz) % ny;
-        const int tl = tr % nz;
-        const int o = ((ti / px) * my + (tj / py)) * mz + (tl / pz);
-        dx[t] = (mask[map * mv + o] == tr) ? g[map * mv + o] : 0.f;
-    }
+    for (int64_t map = blockIdx.y; map < maps; map += gridDim.y)
+        dx[map * int64_t(nv) + tr] = (__ldg(mask + map * mv + o) == int(tr)) ? __ldg(g + map * mv + o) : 0.f;
 }
 
 }  // namespace
@@ -150,7 +151,7 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
     const dims3 m{n.x - s.x * (k.x - 1), n.y - s.y * (k.y - 1), n.z - s.z * (k.z - 1)};
     require(m.x > 0 && m.y > 0 && m.z > 0, "maxfilter_forward: effective window exceeds input");
     require(n.vol() < (int64_t(1) << 31), "maxfilter_forward: map exceeds int32 mask range");
-    maxfilter_fwd_k<<<grid_for(maps * m.vol()), kThreads, 0, st>>>(
+    maxfilter_fwd_k<<<grid2(m.vol(), maps), kThreads, 0, st>>>(
         x, maps, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z), int(k.x),
         int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), y, mask);
     launch_check("maxfilter_fwd");
@@ -159,7 +160,7 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
 void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
                    dims3 k, dims3 s, float* dx) {
     const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
-    maxfilter_bwd_k<<<grid_for(maps * n.vol()), kThreads, 0, st>>>(
+    maxfilter_bwd_k<<<grid2(n.vol(), maps), kThreads, 0, st>>>(
         g, mask, maps, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z), int(k.x),
         int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), dx);
     launch_check("maxfilter_bwd");
@@ -170,7 +171,7 @@ void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p
     require(p.x > 0 && p.y > 0 && p.z > 0 && n.x % p.x == 0 && n.y % p.y == 0 && n.z % p.z == 0,
             "maxpool_forward: dims not divisible by window");
     const dims3 m{n.x / p.x, n.y / p.y, n.z / p.z};
-    maxpool_fwd_k<<<grid_for(maps * m.vol()), kThreads, 0, st>>>(
+    maxpool_fwd_k<<<grid2(m.vol(), maps), kThreads, 0, st>>>(
         x, maps, int(n.x), int(n.y), int(n.z), int(p.x), int(p.y), int(p.z), y, mask);
     launch_check("maxpool_fwd");
 }
@@ -178,7 +179,7 @@ void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p
 void maxpool_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
                  dims3 p, float* dx) {
     const int64_t nvol = m.vol() * p.vol();
-    maxpool_bwd_k<<<grid_for(maps * nvol), kThreads, 0, st>>>(
+    maxpool_bwd_k<<<grid2(nvol, maps), kThreads, 0, st>>>(
         g, mask, maps, int(m.x), int(m.y), int(m.z), int(p.x), int(p.y), int(p.z), dx);
     launch_check("maxpool_bwd");
 }

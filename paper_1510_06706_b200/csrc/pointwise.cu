@@ -39,16 +39,16 @@ __global__ void transfer_bwd_k(const float* __restrict__ g, const float* __restr
     const int64_t map = blockIdx.y;
     const int kind = kinds[map];
     const float b = bias ? bias[map] : 0.f;
-    const int64_t per_map = B * vox;  // elements of this map over the batch
     float acc = 0.f;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < per_map;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t bb = e / vox, v = e - bb * vox;
-        const int64_t i = (bb * f + map) * vox + v;
-        const float d = from_output ? act_deriv_out(kind, xy[i]) : act_deriv_in(kind, xy[i] + b);
-        const float r = g[i] * d;
-        gx[i] = r;
-        acc += r;
+    for (int64_t bb = 0; bb < B; ++bb) {  // no per-element 64-bit division
+        const int64_t off = (bb * f + map) * vox;
+        for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < vox; v += int64_t(gridDim.x) * blockDim.x) {
+            const int64_t i = off + v;
+            const float d = from_output ? act_deriv_out(kind, xy[i]) : act_deriv_in(kind, xy[i] + b);
+            const float r = g[i] * d;
+            gx[i] = r;
+            acc += r;
+        }
     }
     if (part) {
         __shared__ float red[kThreads / 32];
@@ -151,8 +151,7 @@ void transfer_fwd(cudaStream_t st, const float* x, int64_t B, int64_t f, int64_t
 void transfer_bwd(cudaStream_t st, const float* g, const float* xy, bool from_output, int64_t B,
                   int64_t f, int64_t vox, const int32_t* kinds_dev, const float* bias,
                   float* gx, float* dbias, scratch& ws) {
-    const int64_t per_map = B * vox;
-    int64_t chunks = ceil_div(per_map, kThreads * 8);
+    int64_t chunks = ceil_div(vox, kThreads * 2);
     const int64_t cap = (148 * 8 + f - 1) / f;
     if (chunks > cap) chunks = cap;
     if (chunks < 1) chunks = 1;
