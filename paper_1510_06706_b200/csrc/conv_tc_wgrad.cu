@@ -23,6 +23,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.hpp"
 #include "tc_common.cuh"
@@ -44,6 +45,7 @@ struct wg_params {
     int f_in, f_out, T, nt;
     int mrows;  // f_in * T
     int stages, nbuf, bstride, na;
+    int csize;  // CTAs per cluster along the row tiles: they share (multicast) every g tile
     int64_t kb_per_patch, kb_total, kb_per_split;
     int64_t nvol, mvol;
     int ny, nz, my, mz;
@@ -84,7 +86,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), 1);
+            mbar_init(empty_bar(s), uint32_t(p.csize));  // every CTA of the cluster consumed slot s
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8u * b, 1);
@@ -97,6 +99,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     if (warp == 9) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
     tc_fence_before();
     __syncthreads();
+    if (p.csize > 1) cluster_sync();  // peers' barriers exist before any multicast lands
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
@@ -175,19 +178,32 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         }
     } else if (warp == 8) {
         // ---------------- TMA producer: g panels ----------------
+        // Cluster rank r loads rows [r*nt/C, (r+1)*nt/C) of the g tile and
+        // multicasts them to every CTA of the cluster (same K range, other
+        // row tiles): each tile leaves L2 once per cluster.
         if (lane == 0) {
+            const int C = p.csize;
+            const uint32_t rank = C > 1 ? cluster_ctarank() : 0u;
+            const int rows_per = p.nt / C;
+            const uint32_t part = uint32_t(rows_per) * 128u;
+            const uint16_t mask = uint16_t((1u << C) - 1u);
             int s = 0;
             uint32_t ph = 0;
             for (int kb = 0; kb < kblocks; ++kb) {
                 const int64_t q = q0 + kb;
                 const int64_t pb = q / p.kb_per_patch;
                 const int vcol = int(q - pb * p.kb_per_patch) * BK;
-                const int row = int(pb * p.f_out) + n0;
+                const int row = int(pb * p.f_out) + n0 + int(rank) * rows_per;
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 mbar_expect_tx(full_bar(s), 2u * b_bytes);
-                tma_load_2d(b_hi, &tm_hi, full_bar(s), vcol, row);
-                tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), vcol, row);
+                if (C > 1) {
+                    tma_load_2d_mc(b_hi + rank * part, &tm_hi, full_bar(s), vcol, row, mask);
+                    tma_load_2d_mc(b_hi + b_bytes + rank * part, &tm_lo, full_bar(s), vcol, row, mask);
+                } else {
+                    tma_load_2d(b_hi, &tm_hi, full_bar(s), vcol, row);
+                    tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), vcol, row);
+                }
                 if (++s == p.stages) s = 0, ph ^= 1u;
             }
         }
@@ -219,7 +235,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                     mma_tf32_ts(d, ah, bl, idesc, 1u);
                     mma_tf32_ts(d, al, bh, idesc, 1u);
                 }
-                mma_commit(empty_bar(s));
+                if (p.csize > 1) mma_commit_mc(empty_bar(s), uint16_t((1u << p.csize) - 1u));
+                else mma_commit(empty_bar(s));
                 mma_commit(ae0 + 8u * uint32_t(a));
                 if (kc == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit(accf0 + 8u * uint32_t(b));
                 if (++s == p.stages) s = 0, sph ^= 1u;
@@ -238,6 +255,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
+    if (p.csize > 1) cluster_sync();  // no CTA leaves while peers may still arrive on its barriers
 }
 
 __global__ void rowoff_k(int* __restrict__ out, int mrows, int T, int ky, int kz, int sx, int sy, int sz, int ny,
@@ -284,8 +302,50 @@ void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mh
                   const float* x, const int* rowoff, float* ws, const wg_params& p) {
     auto* k = wgrad_tc_kernel<NTMAX>;
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k<<<grid, THREADS, smem, st>>>(mhi, mlo, x, rowoff, ws, p);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(p.csize);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ZNN_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, mhi, mlo, x, rowoff, ws, p));
     launch_check("conv_wgrad_tc");
+}
+
+// CTAs resident at once (one per SM; clusters cannot use every SM of a GPC)
+int64_t resident_ctas(int ntmax, size_t smem, int csize) {
+    static int64_t cache[3][3] = {};
+    const int ti = ntmax == 32 ? 0 : (ntmax == 64 ? 1 : 2), ci = csize == 1 ? 0 : (csize == 2 ? 1 : 2);
+    if (cache[ti][ci]) return cache[ti][ci];
+    int64_t r = 148;
+    if (csize > 1) {
+        const void* k = ntmax == 32 ? reinterpret_cast<const void*>(wgrad_tc_kernel<32>)
+                        : ntmax == 64 ? reinterpret_cast<const void*>(wgrad_tc_kernel<64>)
+                                      : reinterpret_cast<const void*>(wgrad_tc_kernel<128>);
+        ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(unsigned(csize) * 64, 1, 1);
+        cfg.blockDim = dim3(THREADS, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = unsigned(csize);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) == cudaSuccess && nc > 0) r = int64_t(nc) * csize;
+        else cudaGetLastError();
+    }
+    cache[ti][ci] = r;
+    return r;
 }
 
 }  // namespace
@@ -313,19 +373,28 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     p.ny = int(c.n.y), p.nz = int(c.n.z), p.my = int(c.m.y), p.mz = int(c.m.z);
     p.kb_per_patch = ceil_div(p.mvol, BK);
     p.kb_total = p.kb_per_patch * c.B;
-    const int mtiles = int(ceil_div(p.mrows, BM));
+    // clusters of csize row tiles share every g tile by TMA multicast (the
+    // g panel is streamed once per cluster instead of once per row tile)
+    int csize = 2;  // measured on c5: 2 beats 4 (cluster placement) and 1 (L2 misses)
+    if (const char* e = std::getenv("ZNN_WGRAD_CLUSTER")) csize = std::atoi(e);
+    while (csize > 1 && (p.nt % (8 * csize) != 0 || ceil_div(p.mrows, BM) < csize)) csize /= 2;
+    if (csize != 1 && csize != 2 && csize != 4) csize = 1;
+    p.csize = csize;
+    const int mtiles = int(ceil_div(ceil_div(p.mrows, BM), csize) * csize);
     // split-K factor: fill whole waves of 148 SMs (one CTA each). The first
     // split count >= 2 waves whose last wave is >= 97% full, else the best
     // fill up to max(32, 8 waves' worth) splits (a 2.4-wave grid idles 20% of the GPU in its tail).
     const int64_t tiles = int64_t(mtiles) * ntiles;
+    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
+    const int64_t wave = resident_ctas(ntmax, smem, csize);
     const int64_t max_splits = std::max<int64_t>(
         1, std::min<int64_t>(std::max<int64_t>(32, ceil_div(8 * 148, tiles)), ceil_div(p.kb_total, 4 * CHUNK_KB)));
     int64_t splits = 1;
     double best = -1.0;
     for (int64_t sp = 1; sp <= max_splits; ++sp) {
         const int64_t ctas = tiles * sp;
-        const double eff = double(ctas) / double(ceil_div(ctas, 148) * 148);
-        if (ctas >= 2 * 148 && eff >= 0.97) {
+        const double eff = double(ctas) / double(ceil_div(ctas, wave) * wave);
+        if (ctas >= 2 * wave && eff >= 0.97) {
             splits = sp;
             break;
         }
@@ -350,9 +419,8 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
                                                                int(c.s.x), int(c.s.y), int(c.s.z), p.ny, p.nz,
                                                                p.nvol);
     launch_check("conv_wgrad_tc_rowoff");
-    const CUtensorMap mhi = make_panel_map_rows(ghi, mpad, grows, p.nt);
-    const CUtensorMap mlo = make_panel_map_rows(glo, mpad, grows, p.nt);
-    const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
+    const CUtensorMap mhi = make_panel_map_rows(ghi, mpad, grows, p.nt / csize);
+    const CUtensorMap mlo = make_panel_map_rows(glo, mpad, grows, p.nt / csize);
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
     if (ntmax == 32) launch_wgrad<32>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
     else if (ntmax == 64) launch_wgrad<64>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
