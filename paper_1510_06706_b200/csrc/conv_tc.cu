@@ -237,7 +237,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
-        if (lane == 0) {
+        {  // the whole warp runs the loop (converged); one elected lane issues
             const uint32_t idesc = idesc_tf32(BM, p.nt);
             int b = 0, s = 0, a = 0, kc = 0;
             uint32_t bph = 0, sph = 0, aph = 0;
@@ -259,13 +259,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                     const uint32_t ko = uint32_t(kk) * 32u;  // 8 tf32 = 32 B along K
                     const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
                     const uint32_t ah = a_hi + uint32_t(8 * kk), al = a_hi + 32u + uint32_t(8 * kk);
-                    mma_tf32_ts(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
-                    mma_tf32_ts(d, ah, bl, idesc, 1u);
-                    mma_tf32_ts(d, al, bh, idesc, 1u);
+                    mma_tf32_ts_w(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                    mma_tf32_ts_w(d, ah, bl, idesc, 1u);
+                    mma_tf32_ts_w(d, al, bh, idesc, 1u);
                 }
-                mma_commit(empty_bar(s));
-                mma_commit(ae0 + 8u * uint32_t(a));
-                if (kc == CHUNK_KB - 1 || j == nact - 1) mma_commit(accf0 + 8u * uint32_t(b));
+                mma_commit_w(empty_bar(s));
+                mma_commit_w(ae0 + 8u * uint32_t(a));
+                if (kc == CHUNK_KB - 1 || j == nact - 1) mma_commit_w(accf0 + 8u * uint32_t(b));
                 if (++s == p.stages) s = 0, sph ^= 1u;
                 if (++a == p.na) a = 0, aph ^= 1u;
                 if (++kc == CHUNK_KB) {
