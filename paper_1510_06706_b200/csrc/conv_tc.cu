@@ -222,16 +222,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         }
     } else if (warp == 8) {
         // ---------------- TMA producer (pre-split weight panels) ----------------
-        if (lane == 0) {
+        {  // converged warp, one elected lane issues
             int s = 0;
             uint32_t ph = 0;
             for (int j = 0; j < nact; ++j) {
                 const int kb = list[j];
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
-                mbar_expect_tx(full_bar(s), 2u * b_bytes);
-                tma_load_2d(b_hi, &tm_hi, full_bar(s), kb * BK, n0);
-                tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), kb * BK, n0);
+                tma_pair_w(full_bar(s), 2u * b_bytes, b_hi, &tm_hi, b_hi + b_bytes, &tm_lo, kb * BK, n0);
                 if (++s == p.stages) s = 0, ph ^= 1u;
             }
         }

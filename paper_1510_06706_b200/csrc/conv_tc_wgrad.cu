@@ -121,10 +121,12 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
         int a = grp;
         uint32_t u = 0;
+        int64_t pb = (q0 + grp) / p.kb_per_patch;  // patch and K-block within it, tracked incrementally
+        int vkb = int(q0 + grp - pb * p.kb_per_patch);
         for (int kb = grp; kb < kblocks; kb += 2) {
-            const int64_t q = q0 + kb;
-            const int64_t pb = q / p.kb_per_patch;
-            const int v = int(q - pb * p.kb_per_patch) * BK + lane;
+            const int v = vkb * BK + lane;
+            const int64_t pcur = pb;
+            for (vkb += 2; vkb >= p.kb_per_patch; vkb -= int(p.kb_per_patch)) ++pb;
             const bool vok = v < mvol;
             const float* xp = x;
             if (vok) {
@@ -132,7 +134,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 const int r2 = v - vx * myz;
                 const int vy = r2 / p.mz;
                 const int vz = r2 - vy * p.mz;
-                xp = x + pb * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
+                xp = x + pcur * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
             }
             float av[32];
 #pragma unroll
@@ -181,7 +183,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         // Cluster rank r loads rows [r*nt/C, (r+1)*nt/C) of the g tile and
         // multicasts them to every CTA of the cluster (same K range, other
         // row tiles): each tile leaves L2 once per cluster.
-        if (lane == 0) {
+        {  // converged warp, one elected lane issues
             const int C = p.csize;
             const uint32_t rank = C > 1 ? cluster_ctarank() : 0u;
             const int rows_per = p.nt / C;
@@ -189,22 +191,20 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
             const uint16_t mask = uint16_t((1u << C) - 1u);
             int s = 0;
             uint32_t ph = 0;
+            int64_t pb = q0 / p.kb_per_patch;
+            int vkb = int(q0 - pb * p.kb_per_patch);
             for (int kb = 0; kb < kblocks; ++kb) {
-                const int64_t q = q0 + kb;
-                const int64_t pb = q / p.kb_per_patch;
-                const int vcol = int(q - pb * p.kb_per_patch) * BK;
+                const int vcol = vkb * BK;
                 const int row = int(pb * p.f_out) + n0 + int(rank) * rows_per;
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
-                mbar_expect_tx(full_bar(s), 2u * b_bytes);
-                if (C > 1) {
-                    tma_load_2d_mc(b_hi + rank * part, &tm_hi, full_bar(s), vcol, row, mask);
-                    tma_load_2d_mc(b_hi + b_bytes + rank * part, &tm_lo, full_bar(s), vcol, row, mask);
-                } else {
-                    tma_load_2d(b_hi, &tm_hi, full_bar(s), vcol, row);
-                    tma_load_2d(b_hi + b_bytes, &tm_lo, full_bar(s), vcol, row);
-                }
+                if (C > 1)
+                    tma_pair_mc_w(full_bar(s), 2u * b_bytes, b_hi + rank * part, &tm_hi, b_hi + b_bytes + rank * part,
+                                  &tm_lo, vcol, row, mask);
+                else
+                    tma_pair_w(full_bar(s), 2u * b_bytes, b_hi, &tm_hi, b_hi + b_bytes, &tm_lo, vcol, row);
                 if (++s == p.stages) s = 0, ph ^= 1u;
+                if (++vkb == p.kb_per_patch) vkb = 0, ++pb;  // TMA side: one K-block per step
             }
         }
     } else if (warp == 9) {

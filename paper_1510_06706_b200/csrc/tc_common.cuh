@@ -144,6 +144,33 @@ __device__ __forceinline__ void mma_commit_mc_w(uint32_t bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+// converged-warp TMA issue (one elected lane arms the barrier and loads)
+__device__ __forceinline__ void tma_pair_w(uint32_t bar, uint32_t bytes, uint32_t dst0, const CUtensorMap* m0,
+                                           uint32_t dst1, const CUtensorMap* m1, int c0, int c1) {
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@pe cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%2], [%3, {%6, %7}], [%0];\n\t"
+        "@pe cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%4], [%5, {%6, %7}], [%0];\n\t}" ::"r"(
+            bar),
+        "r"(bytes), "r"(dst0), "l"(reinterpret_cast<uint64_t>(m0)), "r"(dst1), "l"(reinterpret_cast<uint64_t>(m1)),
+        "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma_pair_mc_w(uint32_t bar, uint32_t bytes, uint32_t dst0, const CUtensorMap* m0,
+                                              uint32_t dst1, const CUtensorMap* m1, int c0, int c1, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t"
+        "@pe cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%2], [%3, {%6, %7}], [%0], %8;\n\t"
+        "@pe cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%4], [%5, {%6, %7}], [%0], %8;\n\t}" ::"r"(
+            bar),
+        "r"(bytes), "r"(dst0), "l"(reinterpret_cast<uint64_t>(m0)), "r"(dst1), "l"(reinterpret_cast<uint64_t>(m1)),
+        "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
 // arrive on the same mbarrier offset in every CTA of ctaMask when this
 // thread's prior MMAs complete
 __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
