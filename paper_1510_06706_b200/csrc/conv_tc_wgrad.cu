@@ -104,6 +104,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     const uint32_t tmem = *tmem_slot;
     const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
 
+    if (warp < 8) setmaxnreg_inc<224>();
+    else setmaxnreg_dec<56>();
     if (warp < 8) {
         constexpr int NH = NTMAX / 2;
         const int grp = warp >> 2;  // 0: even K-blocks, 1: odd K-blocks
@@ -116,14 +118,11 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         const int mvol = int(p.mvol);
         const int myz = p.my * p.mz;
         float* tp = tpose + warp * (32 * TP);
-        int ro[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
         int a = grp;
         uint32_t u = 0;
-        int64_t pb = (q0 + grp) / p.kb_per_patch;  // patch and K-block within it, tracked incrementally
+        int64_t pb = (q0 + grp) / p.kb_per_patch;  // patch / K-block of the next gather, tracked incrementally
         int vkb = int(q0 + grp - pb * p.kb_per_patch);
-        for (int kb = grp; kb < kblocks; kb += 2) {
+        auto gather = [&](float (&av)[32]) {
             const int v = vkb * BK + lane;
             const int64_t pcur = pb;
             for (vkb += 2; vkb >= p.kb_per_patch; vkb -= int(p.kb_per_patch)) ++pb;
@@ -136,9 +135,13 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 const int vz = r2 - vy * p.mz;
                 xp = x + pcur * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
             }
-            float av[32];
 #pragma unroll
-            for (int t = 0; t < 32; ++t) av[t] = (vok && ro[t] >= 0) ? __ldg(xp + ro[t]) : 0.f;
+            for (int t = 0; t < 32; ++t) {
+                const int ro = rowoff[wq * 32 + t];
+                av[t] = (vok && ro >= 0) ? __ldg(xp + ro) : 0.f;
+            }
+        };
+        auto put = [&](float (&av)[32]) {
             // 32x32 transpose through this warp's tile: row t, voxel lane -> lane t, column voxel
             __syncwarp();
 #pragma unroll
@@ -166,6 +169,16 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
             a += 2;
             if (a >= p.na) a = grp, u ^= 1u;
             D.poll();
+        };
+        // two K-blocks of gathers in flight per warp (registers from setmaxnreg)
+        float va[32], vb[32];
+        if (grp < kblocks) gather(va);
+        for (int kb = grp; kb < kblocks; kb += 4) {
+            if (kb + 2 < kblocks) gather(vb);
+            put(va);
+            if (kb + 2 >= kblocks) break;
+            if (kb + 4 < kblocks) gather(va);
+            put(vb);
         }
         // ---------------- remaining drains + epilogue (this warp's columns) ----------------
         D.finish();
