@@ -346,8 +346,8 @@ __global__ void pad_halo_k(const float* __restrict__ g, int64_t maps, int mx, in
     const bool in = unsigned(ux) < unsigned(mx) && unsigned(uy) < unsigned(my) && unsigned(uz) < unsigned(mz);
     const int src = (ux * my + uy) * mz + uz;
     const int64_t mv = int64_t(mx) * my * mz;
-    for (int64_t map = blockIdx.y; map < maps; map += gridDim.y)
-        gp[map * int64_t(pv) + r] = in ? __ldg(g + map * mv + src) : 0.f;
+    const int64_t map = blockIdx.y + int64_t(blockIdx.z) * gridDim.y;
+    if (map < maps) gp[map * int64_t(pv) + r] = in ? __ldg(g + map * mv + src) : 0.f;
 }
 
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -496,7 +496,8 @@ void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const f
     char* wsp = static_cast<char*>(ws.get(gpad + panel_bytes(int(c.f_out), int(c.f_in), c.taps())));
     float* gp = reinterpret_cast<float*>(wsp);
     const int64_t pmaps = c.B * c.f_out;
-    const dim3 pgrid(unsigned(ceil_div(gd.vol(), 256)), unsigned(pmaps < 65535 ? pmaps : 65535), 1u);
+    const int64_t pgy = pmaps < 65535 ? pmaps : 65535;
+    const dim3 pgrid(unsigned(ceil_div(gd.vol(), 256)), unsigned(pgy), unsigned(ceil_div(pmaps, pgy)));
     pad_halo_k<<<pgrid, 256, 0, st>>>(g, pmaps, int(c.m.x), int(c.m.y), int(c.m.z), int(P.x), int(P.y), int(P.z), gp);
     launch_check("conv_dgrad_tc_pad");
     launch_valid(st, c.B, int(c.f_out), int(c.f_in), int(c.f_in), gd, c.k, c.s, gp, w, 1, nullptr, 3, dx,

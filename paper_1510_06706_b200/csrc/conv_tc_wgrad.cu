@@ -286,7 +286,9 @@ __global__ void split_rows_k(const float* __restrict__ g, int64_t rows, int64_t 
                              float* __restrict__ hi, float* __restrict__ lo) {
     const int64_t c0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
     if (c0 >= mpad) return;
-    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    {
+        const int64_t r = blockIdx.y + int64_t(blockIdx.z) * gridDim.y;
+        if (r >= rows) return;
         const float* src = g + r * mvol;
         float v[4], h[4], l[4];
 #pragma unroll
@@ -425,7 +427,8 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     float* glo = ghi + panel;
     float* partials = glo + panel;
     int* rowoff = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(partials + part) + 255) & ~uintptr_t(255));
-    const dim3 sgrid(unsigned(ceil_div(mpad / 4, 256)), unsigned(grows < 65535 ? grows : 65535), 1u);
+    const int64_t sgy = grows < 65535 ? grows : 65535;
+    const dim3 sgrid(unsigned(ceil_div(mpad / 4, 256)), unsigned(sgy), unsigned(ceil_div(grows, sgy)));
     split_rows_k<<<sgrid, 256, 0, st>>>(g, grows, p.mvol, mpad, ghi, glo);
     launch_check("conv_wgrad_tc_split");
     rowoff_k<<<unsigned(ceil_div(p.mrows, 256)), 256, 0, st>>>(rowoff, p.mrows, p.T, int(c.k.y), int(c.k.z),

@@ -168,9 +168,11 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
     fill_twiddles<P>(tw);
     int64_t img = 0;
     int x = 0, y = 0;
-    if (ok) {
-        img = line / (int64_t(nx) * ny);
-        const int r = int(line - img * nx * int64_t(ny));
+    if (ok) {  // 32-bit decode (nlines < 2^32, checked on the host)
+        const uint32_t pl = uint32_t(nx) * uint32_t(ny);
+        const uint32_t im = uint32_t(line) / pl;
+        img = im;
+        const int r = int(uint32_t(line) - im * pl);
         x = r / ny;
         y = r - x * ny;
         const float* src = in + img * in_img_stride + (int64_t(x) * ny + y) * nz;
@@ -258,10 +260,11 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
     fill_twiddles<P>(tw);
     int64_t img = 0;
     int xi = 0, yi = 0;
-    if (ok) {
-        const int64_t per = int64_t(g.x_cnt) * g.y_cnt;
-        img = line / per;
-        const int r = int(line - img * per);
+    if (ok) {  // 32-bit decode (nlines < 2^32, checked on the host)
+        const uint32_t per = uint32_t(g.x_cnt) * uint32_t(g.y_cnt);
+        const uint32_t im = uint32_t(line) / per;
+        img = im;
+        const int r = int(uint32_t(line) - im * per);
         xi = r / g.y_cnt;
         yi = r - xi * g.y_cnt;
         const float2* src = spec + img * g.spec_img_stride + (int64_t(xi * g.x_step) * g.Py + yi * g.y_step) * Zh;
@@ -298,7 +301,7 @@ __global__ void dilate_k(const float* __restrict__ w, int64_t nker, int kx, int 
     const int64_t ev = int64_t(ex) * ey * ez;
     const int64_t total = nker * ev;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t kk = i / ev;
+        const int64_t kk = i < (int64_t(1) << 32) ? int64_t(uint32_t(i) / uint32_t(ev)) : i / ev;
         const int r = int(i - kk * ev);
         const int x = r / (ey * ez), y = (r / ez) % ey, z = r % ez;
         float v = 0.f;
@@ -515,6 +518,7 @@ void col_pass(cudaStream_t st, const plan& p, float2* spec, int64_t imgs, bool x
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
                float2* spec) {
     const int64_t nlines = imgs * n.x * n.y;
+    require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
         allow_smem(fft_z_fwd_k<PP>, PP);
@@ -543,6 +547,7 @@ void inverse3d(cudaStream_t st, const plan& p, float2* spec, int64_t imgs, dims3
     g.y_step = int(step.y), g.y_cnt = int(cnt.y);
     g.z_step = int(step.z), g.z_cnt = int(cnt.z);
     g.nlines = imgs * cnt.x * cnt.y;
+    require(g.nlines < (int64_t(1) << 32), "fft: too many transform lines");
     g.scale = float(1.0 / double(p.P.x * p.P.y * p.P.z));
     g.out_img_stride = out_img_stride;
     g.oy = int(cnt.y), g.oz = int(cnt.z);

@@ -19,15 +19,17 @@ inline int grid_for(int64_t n, int per_thread = 1) {
     return int(blocks);
 }
 
-__global__ void transfer_fwd_k(const float* __restrict__ x, int64_t f, int64_t vox,
-                               int64_t total, const int32_t* __restrict__ kinds,
-                               const float* __restrict__ bias, float* __restrict__ y) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t map = (i / vox) % f;
-        const float b = bias ? bias[map] : 0.f;
-        y[i] = act_value(kinds[map], x[i] + b);
-    }
+// grid: x over the voxels of one map, y/z over (patch, map) planes
+__global__ void transfer_fwd_k(const float* __restrict__ x, int64_t f, int64_t vox, int64_t planes,
+                               const int32_t* __restrict__ kinds, const float* __restrict__ bias,
+                               float* __restrict__ y) {
+    const int64_t plane = blockIdx.y + int64_t(blockIdx.z) * gridDim.y;
+    const int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (plane >= planes || v >= vox) return;
+    const int map = int(plane % f);
+    const float b = bias ? bias[map] : 0.f;
+    const int64_t i = plane * vox + v;
+    y[i] = act_value(kinds[map], x[i] + b);
 }
 
 // One block-row per (map, chunk): g * phi'(.) written to gx, per-block
@@ -143,8 +145,10 @@ __global__ void zero_k(float* p, int64_t count) {
 
 void transfer_fwd(cudaStream_t st, const float* x, int64_t B, int64_t f, int64_t vox,
                   const int32_t* kinds_dev, const float* bias, float* y) {
-    const int64_t total = B * f * vox;
-    transfer_fwd_k<<<grid_for(total), kThreads, 0, st>>>(x, f, vox, total, kinds_dev, bias, y);
+    const int64_t planes = B * f;
+    const int64_t gy = planes < 65535 ? (planes < 1 ? 1 : planes) : 65535;
+    const dim3 grid(unsigned(ceil_div(vox, kThreads)), unsigned(gy), unsigned(ceil_div(planes, gy)));
+    transfer_fwd_k<<<grid, kThreads, 0, st>>>(x, f, vox, planes, kinds_dev, bias, y);
     launch_check("transfer_fwd");
 }
 
