@@ -1,15 +1,23 @@
 // FFT-memoised convolution engine (see fft.hpp). All transforms are
 // hand-written: a 1D transform of one line runs in shared memory as a
-// Stockham autosort FFT (radix 4/2/3 stages compiled per pad size, twiddles
-// from a per-CTA table), 32 lines per 256-thread CTA. A 3D transform is three
-// passes over a spectrum laid out [image][Px][Py][Pz/2+1] (complex64):
-//   z : real -> half spectrum (R2C), one line per (x, y) of the VALID input
-//   y : columns of 32 consecutive z-bins, rows y; rows beyond the valid
-//       input are known zeros and are never read
-//   x : same, rows x
-// Inverses run x, y then z (C2R) and only write the rows / planes / voxels
-// that the consumer keeps (crop to the valid output, or the s*w taps of a
-// kernel gradient), so pruning comes for free from the row selections.
+// Stockham autosort FFT (radix 8/4/2/3 stages compiled per pad size, twiddles
+// from a per-CTA table), 32 lines per 256-thread CTA.
+//
+// Spectrum layout, per image: [Pz/2+1][Px][Py] complex64 (z-bin major), so an
+// (x, y) plane of one z-bin is contiguous. A 3D forward transform is two
+// passes over HBM:
+//   z  : real lines (x, y) of the VALID input -> half spectra (R2C), stored
+//        transposed into the z-bin planes (only the valid (x, y) entries)
+//   xy : one CTA per z-bin plane: loads the valid region, row FFTs (y) on the
+//        valid rows, column FFTs (x) on every column, writes the whole plane
+// and the inverse mirrors it:
+//   xy : loads a plane, column inverse FFTs, keeps the selected rows, row
+//        inverse FFTs on those, keeps the selected columns and writes the
+//        compact kept block (the crop of a valid output or the s*w taps of a
+//        kernel gradient)
+//   z  : C2R lines of the kept (x, y) with the consumer's crop / tap stride
+//        and the fused bias + transfer epilogue.
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <type_traits>
@@ -115,183 +123,321 @@ __device__ __forceinline__ void fill_twiddles(float2* tw) {
     }
 }
 
-// One Stockham stage (Govindaraju et al. formulation): sub-transform size
-// Ns grows by the stage radix R (4 while possible, then 2, then 3). All
-// sizes are compile-time so index math folds to shifts / constant divides.
-// Every thread of the CTA calls this (uniform __syncthreads).
-template <int P, int Ns, bool INV>
-__device__ __forceinline__ float2* fft_stages(float2* src, float2* dst, int t, const float2* tw) {
-    if constexpr (Ns >= P) {
-        return src;
+// W_P^m (conjugated for the inverse) from the table
+template <int P, bool INV>
+__device__ __forceinline__ float2 twid(const float2* tw, int m) {
+    float2 w = tw[m % P];
+    if (INV) w.y = -w.y;
+    return w;
+}
+
+// DFT of R points held in registers (R in {1,2,3,4,6,8,9,12,16}); composite
+// sizes are split R = A*B in registers (n = a + A b, k = kb + B ka) with
+// twiddles W_R^(a kb) = W_P^(a kb P/R) from the line's table.
+template <int R, int P, bool INV>
+__device__ __forceinline__ void dft_r(float2* v, const float2* tw) {
+    if constexpr (R == 1) {
+        return;
+    } else if constexpr (R == 2 || R == 3 || R == 4 || R == 8) {
+        dft_small<R, INV>(v);
     } else {
-        constexpr int rem = P / Ns;
-        constexpr int R = (rem % 8 == 0) ? 8 : (rem % 4 == 0) ? 4 : ((rem % 2 == 0) ? 2 : 3);
-        constexpr int nb = P / R;
-        constexpr int tstep = P / (Ns * R);  // stage twiddle w^(k q) = tw[k q tstep]
+        constexpr int A = (R % 4 == 0) ? 4 : ((R % 3 == 0) ? 3 : 2);
+        constexpr int B = R / A;
+        float2 t[R];
 #pragma unroll
-        for (int j0 = 0; j0 < nb; j0 += TPL) {
-            const int j = j0 + t;
-            if (nb % TPL == 0 || j < nb) {
-                float2 v[R];
-                const int k = j % Ns;
-                v[0] = src[j];
+        for (int a = 0; a < A; ++a) {
+            float2 u[B];
 #pragma unroll
-                for (int q = 1; q < R; ++q) {
-                    float2 w = tw[k * q * tstep];
-                    if (INV) w.y = -w.y;
-                    v[q] = cmul(src[j + q * nb], w);
-                }
-                dft_small<R, INV>(v);
-                const int d = (j / Ns) * Ns * R + k;
+            for (int b = 0; b < B; ++b) u[b] = v[a + A * b];
+            dft_r<B, P, INV>(u, tw);
 #pragma unroll
-                for (int q = 0; q < R; ++q) dst[d + q * Ns] = v[q];
-            }
+            for (int kb = 0; kb < B; ++kb) t[a * B + kb] = (a * kb == 0) ? u[kb] : cmul(u[kb], twid<P, INV>(tw, a * kb * (P / R)));
         }
-        __syncthreads();
-        return fft_stages<P, Ns * R, INV>(dst, src, t, tw);
+#pragma unroll
+        for (int kb = 0; kb < B; ++kb) {
+            float2 w[A];
+#pragma unroll
+            for (int a = 0; a < A; ++a) w[a] = t[a * B + kb];
+            dft_r<A, P, INV>(w, tw);
+#pragma unroll
+            for (int ka = 0; ka < A; ++ka) v[kb + B * ka] = w[ka];
+        }
     }
 }
 
-// ---- z pass, forward (R2C): lines (img, x < nx, y < ny) of the real input ----
+// One P-point line transform by the TPL = 8 threads of a line (all in one
+// warp), four-step P = R1 * R2: thread n1 < R1 holds v[n2] = x[n1 + R1 n2]
+// and does an R2-point DFT in registers; twiddle W_P^(n1 k2); one exchange
+// through the line's shared buffer xb (P complex); then R1-point DFTs in
+// registers for k2 = t, t + 8, ..., and emit(k2 + R2 k1, X) for every output.
+template <int P>
+struct line_shape {
+    static constexpr int R1 = (P % 8 == 0) ? 8 : ((P % 4 == 0) ? 4 : 2);
+    static constexpr int R2 = P / R1;
+};
+
+template <int P, bool INV, typename Emit>
+__device__ __forceinline__ void line_fft(float2* v, float2* xb, const float2* tw, int t, Emit&& emit) {
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    if (t < R1) {
+        dft_r<R2, P, INV>(v, tw);
+#pragma unroll
+        for (int k2 = 0; k2 < R2; ++k2) xb[k2 * R1 + t] = (k2 == 0) ? v[k2] : cmul(v[k2], twid<P, INV>(tw, t * k2));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k2 = t; k2 < R2; k2 += TPL) {
+        float2 w[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) w[n1] = xb[k2 * R1 + n1];
+        dft_r<R1, P, INV>(w, tw);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) emit(k2 + R2 * k1, w[k1]);
+    }
+    __syncwarp();
+}
+
+// ---- z pass, forward (R2C): lines (img, x < nx, y < ny) of the real input,
+// half spectra stored transposed: spec[img][zb][x][y] ----
 template <int P>
 __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__ in, int64_t in_img_stride, int nx,
                                                         int ny, int nz, int64_t nlines, float2* __restrict__ spec,
-                                                        int64_t spec_img_stride, int Py) {
+                                                        int Px, int Py) {
     constexpr int Zh = P / 2 + 1;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
+    __shared__ int64_t obase[LINES];
+    float2* tw = sm;                   // P
+    float2* xbuf = tw + P;             // LINES x P
+    float2* stash = xbuf + LINES * P;  // LINES x (Zh + 1)
+    fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     const int64_t line = int64_t(blockIdx.x) * LINES + l;
     const bool ok = line < nlines;
-    float2* a = sm + l * (2 * P + 1);
-    float2* b = a + P;
-    float2* tw = sm + LINES * (2 * P + 1);
-    fill_twiddles<P>(tw);
-    int64_t img = 0;
-    int x = 0, y = 0;
+    float2 v[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) v[n2] = make_float2(0.f, 0.f);
     if (ok) {  // 32-bit decode (nlines < 2^32, checked on the host)
         const uint32_t pl = uint32_t(nx) * uint32_t(ny);
         const uint32_t im = uint32_t(line) / pl;
-        img = im;
         const int r = int(uint32_t(line) - im * pl);
-        x = r / ny;
-        y = r - x * ny;
-        const float* src = in + img * in_img_stride + (int64_t(x) * ny + y) * nz;
-        for (int j = t; j < P; j += TPL) a[j] = make_float2(j < nz ? src[j] : 0.f, 0.f);
+        const int x = r / ny, y = r - (r / ny) * ny;
+        const float* src = in + int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
+        if (t < R1)
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) {
+                const int j = t + R1 * n2;
+                if (j < nz) v[n2].x = __ldg(src + j);
+            }
+        if (t == 0) obase[l] = (int64_t(im) * Zh * Px + x) * Py + y;
     }
+    __syncthreads();  // twiddles
+    float2* st = stash + l * (Zh + 1);
+    line_fft<P, false>(v, xbuf + l * P, tw, t, [&](int k, float2 val) {
+        if (k < Zh) st[k] = val;
+    });
     __syncthreads();
-    float2* res = fft_stages<P, 1, false>(a, b, t, tw);
-    if (ok) {
-        float2* dst = spec + img * spec_img_stride + (int64_t(x) * Py + y) * Zh;
-        for (int j = t; j < Zh; j += TPL) dst[j] = res[j];
+    // transposed store: a warp writes one z-bin of 32 consecutive lines
+    const int64_t zstride = int64_t(Px) * Py;
+    for (int idx = threadIdx.x; idx < LINES * Zh; idx += THREADS) {
+        const int l2 = idx % LINES, zb = idx / LINES;
+        if (int64_t(blockIdx.x) * LINES + l2 < nlines) spec[obase[l2] + zb * zstride] = stash[l2 * (Zh + 1) + zb];
     }
 }
 
-struct col_args {
-    int rows_in;                       // rows >= rows_in are zero (never read)
-    int out_first, out_step, out_cnt;  // rows written
-    int zh;                            // contiguous columns per plane (z-bins)
-    int a_first, a_step, a_cnt;        // planes of the other spatial axis folded into the columns
-    int64_t a_stride;
-    int64_t row_stride;
-    int64_t img_stride;
-    int64_t imgs;
-};
-
-// ---- column pass (y or x axis), in place on the spectrum. Columns are
-// (plane a, z-bin) pairs flattened, 32 per CTA, so no tile is mostly empty.
-template <int P, bool INV>
-__global__ void __launch_bounds__(THREADS) fft_col_k(float2* __restrict__ spec, col_args g) {
+// ---- xy pass, forward: one CTA per z-bin plane [PX][PY] (PX == PY, or PX == 1)
+// rows (y transforms) of the valid rows x < nx read straight from HBM into
+// the plane, then columns (x transforms) written straight back ----
+template <int PX, int PY>
+__global__ void __launch_bounds__(THREADS) fft_xy_fwd_k(float2* __restrict__ spec, int64_t planes, int nx, int ny) {
+    constexpr int PYP = PY + 1;
+    constexpr int RY1 = line_shape<PY>::R1, RY2 = line_shape<PY>::R2;
+    constexpr int RX1 = line_shape<PX>::R1, RX2 = line_shape<PX>::R2;
     extern __shared__ float2 sm[];
-    const int64_t img = blockIdx.y + int64_t(blockIdx.z) * gridDim.y;
-    if (img >= g.imgs) return;  // uniform per CTA
-    const int ncols = g.a_cnt * g.zh;
-    const int lc = threadIdx.x % LINES, lr = threadIdx.x / LINES;  // 8 rows per sweep
-    const int c = blockIdx.x * LINES + lc;
-    const bool cok = c < ncols;
-    int64_t coff = 0;
-    if (cok) {
-        const int ai = c / g.zh;
-        coff = int64_t(g.a_first + ai * g.a_step) * g.a_stride + (c - ai * g.zh);
-    }
-    float2* base = spec + img * g.img_stride + coff;
-    float2* tw = sm + LINES * (2 * P + 1);
-    fill_twiddles<P>(tw);
-    for (int j = lr; j < P; j += THREADS / LINES) {
-        float2 v = make_float2(0.f, 0.f);
-        if (j < g.rows_in && cok) v = base[int64_t(j) * g.row_stride];
-        sm[lc * (2 * P + 1) + j] = v;
-    }
+    float2* twy = sm;                 // PY
+    float2* twx = twy + PY;           // PX
+    float2* xbuf = twx + PX;          // LINES x max(PX, PY)
+    constexpr int PM = PX > PY ? PX : PY;
+    float2* pl = xbuf + LINES * PM;   // [PX][PYP]
+    const int64_t q = blockIdx.x + int64_t(blockIdx.y) * gridDim.x;
+    if (q >= planes) return;  // uniform per CTA
+    float2* g = spec + q * (int64_t(PX) * PY);
+    fill_twiddles<PY>(twy);
+    if constexpr (PX > 1) fill_twiddles<PX>(twx);
     __syncthreads();
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* la = sm + l * (2 * P + 1);
-    float2* res = fft_stages<P, 1, INV>(la, la + P, t, tw);
-    const int half = int(res - la);  // 0 or P, same for every line
-    if (cok)
-        for (int q = lr; q < g.out_cnt; q += THREADS / LINES) {
-            const int j = g.out_first + q * g.out_step;
-            base[int64_t(j) * g.row_stride] = sm[lc * (2 * P + 1) + half + j];
+    float2* xb = xbuf + l * PM;
+    for (int r0 = 0; r0 < nx; r0 += LINES) {
+        const int x = r0 + l;
+        const bool ok = x < nx;
+        float2 v[RY2];
+#pragma unroll
+        for (int n2 = 0; n2 < RY2; ++n2) {
+            const int y = t + RY1 * n2;
+            v[n2] = (ok && t < RY1 && y < ny) ? g[x * PY + y] : make_float2(0.f, 0.f);
         }
+        if constexpr (PX == 1) {
+            line_fft<PY, false>(v, xb, twy, t, [&](int k, float2 val) {
+                if (ok) g[k] = val;
+            });
+        } else {
+            line_fft<PY, false>(v, xb, twy, t, [&](int k, float2 val) {
+                if (ok) pl[x * PYP + k] = val;
+            });
+        }
+    }
+    if constexpr (PX > 1) {
+        __syncthreads();
+        for (int c0 = 0; c0 < PY; c0 += LINES) {
+            const int y = c0 + l;
+            const bool ok = y < PY;
+            float2 v[RX2];
+#pragma unroll
+            for (int n2 = 0; n2 < RX2; ++n2) {
+                const int x = t + RX1 * n2;
+                v[n2] = (ok && t < RX1 && x < nx) ? pl[x * PYP + y] : make_float2(0.f, 0.f);
+            }
+            line_fft<PX, false>(v, xb, twx, t, [&](int k, float2 val) {
+                if (ok) g[k * PY + y] = val;
+            });
+        }
+    }
+}
+
+// ---- xy pass, inverse: plane -> compact kept block [xc][yc] (rows x_step*i,
+// columns y_step*j) written to out plane q ----
+template <int PX, int PY>
+__global__ void __launch_bounds__(THREADS) fft_xy_inv_k(const float2* __restrict__ spec, float2* __restrict__ out,
+                                                         int64_t planes, int x_step, int xc, int y_step, int yc) {
+    constexpr int PYP = PY + 1;
+    constexpr int RY1 = line_shape<PY>::R1, RY2 = line_shape<PY>::R2;
+    constexpr int RX1 = line_shape<PX>::R1, RX2 = line_shape<PX>::R2;
+    extern __shared__ float2 sm[];
+    float2* twy = sm;
+    float2* twx = twy + PY;
+    float2* xbuf = twx + PX;
+    constexpr int PM = PX > PY ? PX : PY;
+    float2* pl = xbuf + LINES * PM;
+    const int64_t q = blockIdx.x + int64_t(blockIdx.y) * gridDim.x;
+    if (q >= planes) return;
+    const float2* g = spec + q * (int64_t(PX) * PY);
+    float2* o = out + q * (int64_t(xc) * yc);
+    fill_twiddles<PY>(twy);
+    if constexpr (PX > 1) fill_twiddles<PX>(twx);
+    __syncthreads();
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * PM;
+    if constexpr (PX > 1) {
+        // column inverses straight from HBM; keep rows x_step * i (i < xc)
+        for (int c0 = 0; c0 < PY; c0 += LINES) {
+            const int y = c0 + l;
+            const bool ok = y < PY;
+            float2 v[RX2];
+#pragma unroll
+            for (int n2 = 0; n2 < RX2; ++n2) {
+                const int x = t + RX1 * n2;
+                v[n2] = (ok && t < RX1) ? __ldcs(g + x * PY + y) : make_float2(0.f, 0.f);
+            }
+            line_fft<PX, true>(v, xb, twx, t, [&](int k, float2 val) {
+                const int i = k / x_step;
+                if (ok && i * x_step == k && i < xc) pl[i * PYP + y] = val;
+            });
+        }
+        __syncthreads();
+    }
+    // row inverses of the kept rows; keep columns y_step * j (j < yc)
+    for (int r0 = 0; r0 < xc; r0 += LINES) {
+        const int i = r0 + l;
+        const bool ok = i < xc;
+        float2 v[RY2];
+#pragma unroll
+        for (int n2 = 0; n2 < RY2; ++n2) {
+            const int y = t + RY1 * n2;
+            float2 val = make_float2(0.f, 0.f);
+            if (ok && t < RY1) val = (PX > 1) ? pl[i * PYP + y] : __ldcs(g + y);
+            v[n2] = val;
+        }
+        line_fft<PY, true>(v, xb, twy, t, [&](int k, float2 val) {
+            const int j = k / y_step;
+            if (ok && j * y_step == k && j < yc) o[i * yc + j] = val;
+        });
+    }
 }
 
 struct zinv_args {
-    int Py;
-    int64_t spec_img_stride;
-    int x_step, x_cnt, y_step, y_cnt, z_step, z_cnt;  // selections start at 0
-    int64_t nlines;                                   // images * x_cnt * y_cnt
+    int xc, yc;                        // kept block per z-bin plane (compact input)
+    int z_step, z_cnt;                 // kept z voxels (selection starts at 0)
+    int64_t nlines;                    // images * xc * yc
     float scale;
     int64_t out_img_stride;
-    int oy, oz;                                       // output box dims (y, z)
-    int act;                                          // ZNN_ACT_* (3 = none)
-    int bias_mod;                                     // bias index = img % bias_mod
+    int oy, oz;                        // output box dims (y, z)
+    int act;                           // ZNN_ACT_* (3 = none)
+    int bias_mod;                      // bias index = img % bias_mod
 };
 
-// ---- z pass, inverse (C2R) with crop / tap selection and fused epilogue ----
+// ---- z pass, inverse (C2R) of the compact kept lines, crop / tap selection
+// and fused epilogue ----
 template <int P>
-__global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict__ spec, zinv_args g,
+__global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict__ cspec, zinv_args g,
                                                         const float* __restrict__ bias, float* __restrict__ out) {
     constexpr int Zh = P / 2 + 1;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
+    __shared__ int64_t ibase[LINES], obase[LINES];
+    __shared__ float bvals[LINES];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* stash = xbuf + LINES * P;  // LINES x (Zh + 1)
+    fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     const int64_t line = int64_t(blockIdx.x) * LINES + l;
     const bool ok = line < g.nlines;
-    float2* a = sm + l * (2 * P + 1);
-    float2* b = a + P;
-    float2* tw = sm + LINES * (2 * P + 1);
-    fill_twiddles<P>(tw);
-    int64_t img = 0;
-    int xi = 0, yi = 0;
-    if (ok) {  // 32-bit decode (nlines < 2^32, checked on the host)
-        const uint32_t per = uint32_t(g.x_cnt) * uint32_t(g.y_cnt);
+    if (ok && t == 0) {  // 32-bit decode (nlines < 2^32, checked on the host)
+        const uint32_t per = uint32_t(g.xc) * uint32_t(g.yc);
         const uint32_t im = uint32_t(line) / per;
-        img = im;
         const int r = int(uint32_t(line) - im * per);
-        xi = r / g.y_cnt;
-        yi = r - xi * g.y_cnt;
-        const float2* src = spec + img * g.spec_img_stride + (int64_t(xi * g.x_step) * g.Py + yi * g.y_step) * Zh;
-        for (int j = t; j < P; j += TPL) {
-            float2 v;
-            if (j < Zh) {
-                v = src[j];
-            } else {
-                const float2 c = src[P - j];  // Hermitian symmetry of a real signal
-                v = make_float2(c.x, -c.y);
-            }
-            a[j] = v;
-        }
+        const int xi = r / g.yc, yi = r - (r / g.yc) * g.yc;
+        ibase[l] = int64_t(im) * Zh * per + r;
+        obase[l] = int64_t(im) * g.out_img_stride + (int64_t(xi) * g.oy + yi) * g.oz;
+        bvals[l] = bias ? bias[im % uint32_t(g.bias_mod)] : 0.f;
     }
     __syncthreads();
-    float2* res = fft_stages<P, 1, true>(a, b, t, tw);
-    if (ok) {
-        float* dst = out + img * g.out_img_stride + (int64_t(xi) * g.oy + yi) * g.oz;
-        const float bv = bias ? bias[img % g.bias_mod] : 0.f;
-        for (int q = t; q < g.z_cnt; q += TPL) {
-            float v = res[q * g.z_step].x * g.scale + bv;
-            if (g.act == 2) v = v > 0.f ? v : 0.f;
-            else if (g.act == 0) v = 1.f / (1.f + expf(-v));
-            else if (g.act == 1) v = tanhf(v);
-            dst[q] = v;
-        }
+    // coalesced gather: a warp reads one z-bin of 32 consecutive lines
+    const int64_t zstride = int64_t(g.xc) * g.yc;
+    for (int idx = threadIdx.x; idx < LINES * Zh; idx += THREADS) {
+        const int l2 = idx % LINES, zb = idx / LINES;
+        if (int64_t(blockIdx.x) * LINES + l2 < g.nlines)
+            stash[l2 * (Zh + 1) + zb] = __ldcs(cspec + ibase[l2] + zb * zstride);
     }
+    __syncthreads();
+    const float2* st = stash + l * (Zh + 1);
+    float2 v[R2];
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+        const int j = t + R1 * n2;
+        float2 val = make_float2(0.f, 0.f);
+        if (ok && t < R1) {
+            if (j < Zh) {
+                val = st[j];
+            } else {  // Hermitian symmetry of a real signal
+                const float2 c = st[P - j];
+                val = make_float2(c.x, -c.y);
+            }
+        }
+        v[n2] = val;
+    }
+    float* dst = out + (ok ? obase[l] : 0);
+    const float bv = ok ? bvals[l] : 0.f;
+    line_fft<P, true>(v, xbuf + l * P, tw, t, [&](int k, float2 val) {
+        const int q = k / g.z_step;
+        if (ok && q * g.z_step == k && q < g.z_cnt) {
+            float r = val.x * g.scale + bv;
+            if (g.act == 2) r = r > 0.f ? r : 0.f;
+            else if (g.act == 0) r = 1.f / (1.f + expf(-r));
+            else if (g.act == 1) r = tanhf(r);
+            dst[q] = r;
+        }
+    });
 }
 
 // dilated kernels: dil[e][f_in][s*w] = w[e][f_in][w], zeros elsewhere (conv_direct.hpp:137-151)
@@ -312,111 +458,168 @@ __global__ void dilate_k(const float* __restrict__ w, int64_t nker, int kx, int 
 }
 
 // ---- per-frequency complex multiply-accumulate over converging edges ----
-constexpr int CM_T = 128;  // threads (= frequency bins) per CTA
-// register tile: 8 x 8 complex accumulators per thread; the shared operand
-// (X, G) is re-read f/8 times, from L2 (tiles of one frequency block are
-// adjacent in launch order), the per-edge kernel spectrum exactly once
-constexpr int TA = 8, TB = 8;
+constexpr int TA = 8;  // patches per CTA in the fwd / bwd CMAC
 
-// fwd: Y[b][o] = sum_i X[b][i] * conj(K[o][i])      (tile TA b x TB o)
-__global__ void __launch_bounds__(CM_T) cmac_fwd_k(const float2* __restrict__ X, const float2* __restrict__ K,
-                                                    float2* __restrict__ Y, int B, int f, int fo, int64_t bins) {
-    const int64_t w = int64_t(blockIdx.y) * CM_T + threadIdx.x;  // tiles on x: L2 reuse of shared operands
-    if (w >= bins) return;
-    const int o0 = blockIdx.x * TB, b0 = blockIdx.z * TA;
-    float2 acc[TA][TB];
+// fwd / bwd CMAC with the shared operand staged in shared memory:
+//   fwd: Y[b][o]  = sum_i X[b][i] * conj(K[o][i])   (S = X, n = o, r = i)
+//   bwd: DX[b][i] = sum_o G[b][o] * K[o][i]         (S = G, n = i, r = o)
+// A CTA owns SB = 64 frequency bins (2 per lane: 16-byte loads) x SW*ST
+// outputs n (ST per warp) x TA patches. The shared operand S[b][r][bins] is
+// staged IC reduction steps at a time with cp.async (double buffered); the
+// per-edge kernel spectra K stream from HBM exactly once, a whole chunk of
+// 16-byte loads issued before its FMAs.
+constexpr int SB = 64, SW = 8, ST = 2, IC = 8;
+constexpr int SS_THREADS = SW * 32;
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    const int n = pred ? 16 : 0;  // zero-fill when out of range
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <bool CONJ>
+__global__ void __launch_bounds__(SS_THREADS, 1) cmac_ss_k(const float2* __restrict__ S, const float2* __restrict__ K,
+                                                           float2* __restrict__ O, int B, int nr, int nn, int64_t kn,
+                                                           int64_t kr, int64_t bins) {
+    extern __shared__ float4 sst[];  // [2][TA][IC][SB/2] float4 (2 bins each)
+    constexpr int UNITS = TA * IC * (SB / 2);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t w0 = int64_t(blockIdx.y) * SB;   // n blocks of one bin block are adjacent: S stays in L2
+    const int n0 = blockIdx.x * (SW * ST) + warp * ST;
+    const int b0 = blockIdx.z * TA;
+    const int64_t wl = w0 + 2 * lane;  // this lane's two bins
+    const bool wok = wl < bins;        // bins is even
+    auto stage = [&](int c, int buf) {
+        for (int u = threadIdx.x; u < UNITS; u += SS_THREADS) {
+            const int b = u / (IC * (SB / 2)), rem = u - b * (IC * (SB / 2));
+            const int rr = rem / (SB / 2), q = rem - rr * (SB / 2);
+            const int r = c * IC + rr;
+            const int64_t w = w0 + 2 * q;
+            const bool ok = b0 + b < B && r < nr && w < bins;
+            const float2* src = ok ? S + (int64_t(b0 + b) * nr + r) * bins + w : S;
+            cp_async16(sst + ((buf * TA + b) * IC + rr) * (SB / 2) + q, src, ok);
+        }
+        cp_async_commit();
+    };
+    float4 acc[TA][ST];  // (re, im) of bin 0, (re, im) of bin 1
 #pragma unroll
-    for (int a = 0; a < TA; ++a)
+    for (int b = 0; b < TA; ++b)
 #pragma unroll
-        for (int c = 0; c < TB; ++c) acc[a][c] = make_float2(0.f, 0.f);
-    for (int i = 0; i < f; ++i) {
-        float2 xv[TA], kv[TB];
+        for (int t = 0; t < ST; ++t) acc[b][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nchunks = (nr + IC - 1) / IC;
+    stage(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        // this chunk's kernel-spectrum loads, all in flight before the FMAs
+        float4 kv[IC][ST];
 #pragma unroll
-        for (int a = 0; a < TA; ++a) xv[a] = (b0 + a < B) ? X[(int64_t(b0 + a) * f + i) * bins + w] : make_float2(0.f, 0.f);
+        for (int rr = 0; rr < IC; ++rr)
 #pragma unroll
-        for (int c = 0; c < TB; ++c) kv[c] = (o0 + c < fo) ? K[(int64_t(o0 + c) * f + i) * bins + w] : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int a = 0; a < TA; ++a)
-#pragma unroll
-            for (int c = 0; c < TB; ++c) {
-                const float2 p = cmulc(xv[a], kv[c]);
-                acc[a][c].x += p.x;
-                acc[a][c].y += p.y;
+            for (int t = 0; t < ST; ++t) {
+                const int r = c * IC + rr, n = n0 + t;
+                kv[rr][t] = (wok && r < nr && n < nn)
+                                ? __ldcs(reinterpret_cast<const float4*>(K + (int64_t(n) * kn + int64_t(r) * kr) * bins + wl))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
             }
+        if (c + 1 < nchunks) {
+            stage(c + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int rr = 0; rr < IC; ++rr)
+#pragma unroll
+            for (int b = 0; b < TA; ++b) {
+                const float4 sv = sst[((buf * TA + b) * IC + rr) * (SB / 2) + lane];
+#pragma unroll
+                for (int t = 0; t < ST; ++t) {
+                    const float2 p0 = CONJ ? cmulc(make_float2(sv.x, sv.y), make_float2(kv[rr][t].x, kv[rr][t].y))
+                                           : cmul(make_float2(sv.x, sv.y), make_float2(kv[rr][t].x, kv[rr][t].y));
+                    const float2 p1 = CONJ ? cmulc(make_float2(sv.z, sv.w), make_float2(kv[rr][t].z, kv[rr][t].w))
+                                           : cmul(make_float2(sv.z, sv.w), make_float2(kv[rr][t].z, kv[rr][t].w));
+                    acc[b][t].x += p0.x, acc[b][t].y += p0.y, acc[b][t].z += p1.x, acc[b][t].w += p1.y;
+                }
+            }
+        __syncthreads();  // the buffer is refilled two chunks later
     }
+    if (!wok) return;
 #pragma unroll
-    for (int a = 0; a < TA; ++a)
+    for (int b = 0; b < TA; ++b)
 #pragma unroll
-        for (int c = 0; c < TB; ++c)
-            if (b0 + a < B && o0 + c < fo) Y[(int64_t(b0 + a) * fo + o0 + c) * bins + w] = acc[a][c];
+        for (int t = 0; t < ST; ++t)
+            if (b0 + b < B && n0 + t < nn)
+                *reinterpret_cast<float4*>(O + (int64_t(b0 + b) * nn + n0 + t) * bins + wl) = acc[b][t];
 }
 
-// bwd: dX[b][i] = sum_o G[b][o] * K[o][i]    (tile TA b x TB i)
-__global__ void __launch_bounds__(CM_T) cmac_bwd_k(const float2* __restrict__ G, const float2* __restrict__ K,
-                                                    float2* __restrict__ DX, int B, int f, int fo, int64_t bins) {
-    const int64_t w = int64_t(blockIdx.y) * CM_T + threadIdx.x;  // tiles on x: L2 reuse of shared operands
-    if (w >= bins) return;
-    const int i0 = blockIdx.x * TB, b0 = blockIdx.z * TA;
-    float2 acc[TA][TB];
-#pragma unroll
-    for (int a = 0; a < TA; ++a)
-#pragma unroll
-        for (int c = 0; c < TB; ++c) acc[a][c] = make_float2(0.f, 0.f);
-    for (int o = 0; o < fo; ++o) {
-        float2 gv[TA], kv[TB];
-#pragma unroll
-        for (int a = 0; a < TA; ++a) gv[a] = (b0 + a < B) ? G[(int64_t(b0 + a) * fo + o) * bins + w] : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < TB; ++c) kv[c] = (i0 + c < f) ? K[(int64_t(o) * f + i0 + c) * bins + w] : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int a = 0; a < TA; ++a)
-#pragma unroll
-            for (int c = 0; c < TB; ++c) {
-                const float2 p = cmul(gv[a], kv[c]);
-                acc[a][c].x += p.x;
-                acc[a][c].y += p.y;
-            }
+// upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]) — a rank-B update per bin,
+// bound by writing dK once. A CTA owns SB = 64 bins (2 per lane) x a 16 o x
+// 16 i block; X[b][i-block] and G[b][o-block] of its bins are staged in
+// shared memory (cp.async) and each thread accumulates 4 o x 8 i x 2 bins.
+// Grid: (i, o) blocks of one bin block adjacent, so X / G stay in L2.
+constexpr int UO = 16, UI = 16, TUO = 4, TUI = 8;  // 256 threads = (UO/TUO) x (UI/TUI) x 32 lanes
+__global__ void __launch_bounds__(SS_THREADS, 1) cmac_upd_ss_k(const float2* __restrict__ X,
+                                                               const float2* __restrict__ G, float2* __restrict__ DK,
+                                                               int B, int f, int fo, int64_t bins) {
+    extern __shared__ float4 sst[];  // X: [B][UI][SB/2], then G: [B][UO][SB/2]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nib = (f + UI - 1) / UI;
+    const int ib = blockIdx.x % nib, ob = blockIdx.x / nib;
+    const int64_t w0 = int64_t(blockIdx.y) * SB;
+    const int64_t wl = w0 + 2 * lane;
+    const bool wok = wl < bins;
+    const int i_base = ib * UI, o_base = ob * UO;
+    float4* xs = sst;
+    float4* gs = sst + B * UI * (SB / 2);
+    for (int u = threadIdx.x; u < B * UI * (SB / 2); u += SS_THREADS) {
+        const int b = u / (UI * (SB / 2)), rem = u - b * (UI * (SB / 2));
+        const int ii = rem / (SB / 2), q = rem - ii * (SB / 2);
+        const int64_t w = w0 + 2 * q;
+        const bool ok = i_base + ii < f && w < bins;
+        cp_async16(xs + u, ok ? X + (int64_t(b) * f + i_base + ii) * bins + w : X, ok);
     }
+    for (int u = threadIdx.x; u < B * UO * (SB / 2); u += SS_THREADS) {
+        const int b = u / (UO * (SB / 2)), rem = u - b * (UO * (SB / 2));
+        const int oo = rem / (SB / 2), q = rem - oo * (SB / 2);
+        const int64_t w = w0 + 2 * q;
+        const bool ok = o_base + oo < fo && w < bins;
+        cp_async16(gs + u, ok ? G + (int64_t(b) * fo + o_base + oo) * bins + w : G, ok);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    const int oq = warp / (UI / TUI), iq = warp % (UI / TUI);  // this warp's 4 o x 8 i sub-block
+    float4 acc[TUO][TUI];
 #pragma unroll
-    for (int a = 0; a < TA; ++a)
+    for (int a = 0; a < TUO; ++a)
 #pragma unroll
-        for (int c = 0; c < TB; ++c)
-            if (b0 + a < B && i0 + c < f) DX[(int64_t(b0 + a) * f + i0 + c) * bins + w] = acc[a][c];
-}
-
-// upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o])   (tile TU o x TU i; only B terms per
-// output, so a smaller tile keeps occupancy up for the output-write-bound pass)
-constexpr int TU = 4;
-__global__ void __launch_bounds__(CM_T) cmac_upd_k(const float2* __restrict__ X, const float2* __restrict__ G,
-                                                    float2* __restrict__ DK, int B, int f, int fo, int64_t bins) {
-    const int64_t w = int64_t(blockIdx.y) * CM_T + threadIdx.x;  // tiles on x: L2 reuse of shared operands
-    if (w >= bins) return;
-    const int i0 = blockIdx.x * TU, o0 = blockIdx.z * TU;
-    float2 acc[TU][TU];
-#pragma unroll
-    for (int a = 0; a < TU; ++a)
-#pragma unroll
-        for (int c = 0; c < TU; ++c) acc[a][c] = make_float2(0.f, 0.f);
+        for (int c = 0; c < TUI; ++c) acc[a][c] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int b = 0; b < B; ++b) {
-        float2 gv[TU], xv[TU];
+        float4 gv[TUO], xv[TUI];
 #pragma unroll
-        for (int a = 0; a < TU; ++a) gv[a] = (o0 + a < fo) ? G[(int64_t(b) * fo + o0 + a) * bins + w] : make_float2(0.f, 0.f);
+        for (int a = 0; a < TUO; ++a) gv[a] = gs[(b * UO + oq * TUO + a) * (SB / 2) + lane];
 #pragma unroll
-        for (int c = 0; c < TU; ++c) xv[c] = (i0 + c < f) ? X[(int64_t(b) * f + i0 + c) * bins + w] : make_float2(0.f, 0.f);
+        for (int c = 0; c < TUI; ++c) xv[c] = xs[(b * UI + iq * TUI + c) * (SB / 2) + lane];
 #pragma unroll
-        for (int a = 0; a < TU; ++a)
+        for (int a = 0; a < TUO; ++a)
 #pragma unroll
-            for (int c = 0; c < TU; ++c) {
-                const float2 p = cmulc(xv[c], gv[a]);
-                acc[a][c].x += p.x;
-                acc[a][c].y += p.y;
+            for (int c = 0; c < TUI; ++c) {
+                const float2 p0 = cmulc(make_float2(xv[c].x, xv[c].y), make_float2(gv[a].x, gv[a].y));
+                const float2 p1 = cmulc(make_float2(xv[c].z, xv[c].w), make_float2(gv[a].z, gv[a].w));
+                acc[a][c].x += p0.x, acc[a][c].y += p0.y, acc[a][c].z += p1.x, acc[a][c].w += p1.y;
             }
     }
+    if (!wok) return;
 #pragma unroll
-    for (int a = 0; a < TU; ++a)
+    for (int a = 0; a < TUO; ++a)
 #pragma unroll
-        for (int c = 0; c < TU; ++c)
-            if (o0 + a < fo && i0 + c < f) DK[(int64_t(o0 + a) * f + i0 + c) * bins + w] = acc[a][c];
+        for (int c = 0; c < TUI; ++c) {
+            const int o = o_base + oq * TUO + a, i = i_base + iq * TUI + c;
+            if (o < fo && i < f) __stcs(reinterpret_cast<float4*>(DK + (int64_t(o) * f + i) * bins + wl), acc[a][c]);
+        }
 }
 
 }  // namespace
@@ -448,13 +651,23 @@ constexpr int64_t kMaxSpectrumBytes = int64_t(24) << 30;  // kernel spectra budg
 
 int64_t pad_axis(int64_t n) { return n <= 1 ? 1 : good_size(n); }
 
+// Any pad >= n per axis is exact (the circular wrap only touches zeros,
+// conv_fft.hpp:67-71). x and y share one pad (square xy planes, one compiled
+// plane kernel per size) unless the volume is 2-D (x = 1).
 dims3 pads_for(const conv_shape& c) {
     dims3 P{pad_axis(c.n.x), pad_axis(c.n.y), pad_axis(c.n.z)};
+    if (P.x > 1) P.x = P.y = std::max(P.x, P.y);
     if (P.z % 2) P.z = good_size(P.z + 1);  // R2C axis must be even
     return P;
 }
 
-size_t smem_for(int P) { return sizeof(float2) * (size_t(LINES) * size_t(2 * P + 1) + size_t(P)); }
+// z passes: twiddles + per-line exchange buffers + the half-spectrum stash
+size_t smem_for(int P) { return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(P) + size_t(LINES) * size_t(P / 2 + 2)); }
+// xy passes: twiddles + exchange buffers + the [PX][PY+1] plane
+size_t smem_xy(int PX, int PY) {
+    const int PM = PX > PY ? PX : PY;
+    return sizeof(float2) * (size_t(PX + PY) + size_t(LINES) * size_t(PM) + size_t(PX) * size_t(PY + 1));
+}
 
 // compile-time pad dispatch: f(std::integral_constant<int, P>) for P in kPads
 template <typename F>
@@ -477,74 +690,75 @@ void dispatch_pad(int P, F&& f) {
 }
 
 template <typename K>
-void allow_smem(K* k, int P) {
-    ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_for(P))));
+void allow_smem(K* k, size_t bytes) {
+    ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
-void col_pass(cudaStream_t st, const plan& p, float2* spec, int64_t imgs, bool x_axis, bool inv, int rows_in,
-              int out_first, int out_step, int out_cnt, int a_first, int a_step, int a_cnt) {
-    const int P = int(x_axis ? p.P.x : p.P.y);
-    if (P == 1) return;  // 1-point DFT: identity
-    col_args g;
-    g.rows_in = rows_in;
-    g.out_first = out_first, g.out_step = out_step, g.out_cnt = out_cnt;
-    g.zh = int(p.Zh);
-    g.img_stride = p.bins;
-    if (x_axis) {
-        g.row_stride = p.P.y * p.Zh;
-        g.a_stride = p.Zh;  // the folded axis is y
+void cmac_ss(cudaStream_t st, const float2* S, const float2* K, float2* O, int B, int nr, int nn, int64_t kn,
+             int64_t kr, int64_t bins, bool conj) {
+    require(bins % 2 == 0, "fft cmac: odd bin count");
+    const size_t smem = sizeof(float4) * size_t(2 * TA * IC * (SB / 2));
+    const dim3 grid(unsigned(ceil_div(nn, SW * ST)), unsigned(ceil_div(bins, SB)), unsigned(ceil_div(B, TA)));
+    if (conj) {
+        allow_smem(cmac_ss_k<true>, smem);
+        cmac_ss_k<true><<<grid, SS_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
     } else {
-        g.row_stride = p.Zh;
-        g.a_stride = p.P.y * p.Zh;  // the folded axis is x
+        allow_smem(cmac_ss_k<false>, smem);
+        cmac_ss_k<false><<<grid, SS_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
     }
-    g.a_first = a_first, g.a_step = a_step, g.a_cnt = a_cnt;
-    g.imgs = imgs;
-    const int64_t gy = imgs < 65535 ? imgs : 65535;
-    const dim3 grid{unsigned(ceil_div(int64_t(a_cnt) * p.Zh, LINES)), unsigned(gy), unsigned(ceil_div(imgs, gy))};
-    dispatch_pad(P, [&](auto pc) {
-        constexpr int PP = decltype(pc)::value;
-        if (inv) {
-            allow_smem(fft_col_k<PP, true>, PP);
-            fft_col_k<PP, true><<<grid, THREADS, smem_for(PP), st>>>(spec, g);
-        } else {
-            allow_smem(fft_col_k<PP, false>, PP);
-            fft_col_k<PP, false><<<grid, THREADS, smem_for(PP), st>>>(spec, g);
-        }
-    });
-    launch_check("fft_col");
 }
 
-// forward 3D R2C of imgs real volumes (valid dims n, image stride in floats)
+// forward 3D R2C of imgs real volumes (valid dims n, image stride in floats):
+// z pass (transposed store) + fused xy pass
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
                float2* spec) {
     const int64_t nlines = imgs * n.x * n.y;
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
-        allow_smem(fft_z_fwd_k<PP>, PP);
+        allow_smem(fft_z_fwd_k<PP>, smem_for(PP));
         fft_z_fwd_k<PP><<<unsigned(ceil_div(nlines, LINES)), THREADS, smem_for(PP), st>>>(
-            in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, p.bins, int(p.P.y));
+            in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y));
     });
     launch_check("fft_z_fwd");
-    // y: planes x < n.x, rows y < n.y valid -> all Py rows
-    col_pass(st, p, spec, imgs, false, false, int(n.y), 0, 1, int(p.P.y), 0, 1, int(n.x));
-    // x: every y row, planes x < n.x valid -> all Px planes
-    col_pass(st, p, spec, imgs, true, false, int(n.x), 0, 1, int(p.P.x), 0, 1, int(p.P.y));
+    const int64_t planes = imgs * p.Zh;
+    dispatch_pad(int(p.P.y), [&](auto pc) {
+        constexpr int PY = decltype(pc)::value;
+        if (p.P.x == 1) {
+            allow_smem(fft_xy_fwd_k<1, PY>, smem_xy(1, PY));
+            fft_xy_fwd_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(spec, planes, int(n.x), int(n.y));
+        } else {
+            allow_smem(fft_xy_fwd_k<PY, PY>, smem_xy(PY, PY));
+            fft_xy_fwd_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(spec, planes, int(n.x),
+                                                                                      int(n.y));
+        }
+    });
+    launch_check("fft_xy_fwd");
 }
 
 // inverse 3D C2R keeping voxels (x,y,z) = (step*i) for i < cnt per axis,
-// written as a dense box [imgs][cnt.x][cnt.y][cnt.z] (image stride given)
-void inverse3d(cudaStream_t st, const plan& p, float2* spec, int64_t imgs, dims3 step, dims3 cnt, float* out,
-               int64_t out_img_stride, const float* bias, int bias_mod, int act) {
-    // x: all rows in, keep planes step.x * i
-    col_pass(st, p, spec, imgs, true, true, int(p.P.x), 0, int(step.x), int(cnt.x), 0, 1, int(p.P.y));
-    // y: on the kept planes, keep rows step.y * i
-    col_pass(st, p, spec, imgs, false, true, int(p.P.y), 0, int(step.y), int(cnt.y), 0, int(step.x), int(cnt.x));
+// written as a dense box [imgs][cnt.x][cnt.y][cnt.z] (image stride given);
+// cbuf holds the compact kept planes between the two passes
+void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs, dims3 step, dims3 cnt, float* out,
+               int64_t out_img_stride, const float* bias, int bias_mod, int act, float2* cbuf) {
+    require(step.x * (cnt.x - 1) < p.P.x && step.y * (cnt.y - 1) < p.P.y && step.z * (cnt.z - 1) < p.P.z,
+            "fft: kept voxels outside the padded volume");
+    const int64_t planes = imgs * p.Zh;
+    dispatch_pad(int(p.P.y), [&](auto pc) {
+        constexpr int PY = decltype(pc)::value;
+        if (p.P.x == 1) {
+            allow_smem(fft_xy_inv_k<1, PY>, smem_xy(1, PY));
+            fft_xy_inv_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(
+                spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
+        } else {
+            allow_smem(fft_xy_inv_k<PY, PY>, smem_xy(PY, PY));
+            fft_xy_inv_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(
+                spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
+        }
+    });
+    launch_check("fft_xy_inv");
     zinv_args g;
-    g.Py = int(p.P.y);
-    g.spec_img_stride = p.bins;
-    g.x_step = int(step.x), g.x_cnt = int(cnt.x);
-    g.y_step = int(step.y), g.y_cnt = int(cnt.y);
+    g.xc = int(cnt.x), g.yc = int(cnt.y);
     g.z_step = int(step.z), g.z_cnt = int(cnt.z);
     g.nlines = imgs * cnt.x * cnt.y;
     require(g.nlines < (int64_t(1) << 32), "fft: too many transform lines");
@@ -555,8 +769,8 @@ void inverse3d(cudaStream_t st, const plan& p, float2* spec, int64_t imgs, dims3
     g.bias_mod = bias_mod > 0 ? bias_mod : 1;
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
-        allow_smem(fft_z_inv_k<PP>, PP);
-        fft_z_inv_k<PP><<<unsigned(ceil_div(g.nlines, LINES)), THREADS, smem_for(PP), st>>>(spec, g, bias, out);
+        allow_smem(fft_z_inv_k<PP>, smem_for(PP));
+        fft_z_inv_k<PP><<<unsigned(ceil_div(g.nlines, LINES)), THREADS, smem_for(PP), st>>>(cbuf, g, bias, out);
     });
     launch_check("fft_z_inv");
 }
@@ -572,6 +786,7 @@ float2* carve(char*& cur, int64_t count) {
 bool supported(const conv_shape& c) {
     const dims3 P = pads_for(c);
     if (P.x > MAXP || P.y > MAXP || P.z > MAXP) return false;
+    if ((P.x != P.y && P.x != 1) || P.y < 2) return false;  // compiled xy planes: square, or 2-D (x = 1)
     const int64_t bins = P.x * P.y * (P.z / 2 + 1);
     if (c.f_in * c.f_out * bins * int64_t(sizeof(float2)) > kMaxSpectrumBytes) return false;
     return true;
@@ -608,39 +823,46 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     forward3d(st, p, p.dil, e.vol(), e, nker, p.K);
     p.cnt.fwd_kernel += nker;
     // Y = sum_i X * conj(K), one inverse per output node, crop + bias + transfer
-    char* cur = static_cast<char*>(ws.get(sizeof(float2) * size_t(c.B * c.f_out * p.bins) + 512));
+    const int64_t ccount = c.B * c.f_out * p.Zh * c.m.x * c.m.y;  // compact kept planes
+    char* cur = static_cast<char*>(ws.get(sizeof(float2) * size_t(c.B * c.f_out * p.bins + ccount) + 1024));
     float2* Y = carve(cur, c.B * c.f_out * p.bins);
-    const dim3 grid{unsigned(ceil_div(c.f_out, TB)), unsigned(ceil_div(p.bins, CM_T)), unsigned(ceil_div(c.B, TA))};
-    cmac_fwd_k<<<grid, CM_T, 0, st>>>(p.X, p.K, Y, int(c.B), int(c.f_in), int(c.f_out), p.bins);
+    float2* CB = carve(cur, ccount);
+    cmac_ss(st, p.X, p.K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
     launch_check("fft_cmac_fwd");
-    inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act);
+    inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB);
     p.cnt.fwd_inverse += c.B * c.f_out;
 }
 
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float*, float* gw,
               float* gin, znn_gpu::scratch& ws) {
     const int64_t nB = c.B;
+    const int64_t ccount = std::max(nB * c.f_in * p.Zh * c.n.x * c.n.y, c.f_out * c.f_in * p.Zh * c.k.x * c.k.y);
     const size_t need = sizeof(float2) * size_t(nB * c.f_out * p.bins + nB * c.f_in * p.bins +
-                                                 c.f_out * c.f_in * p.bins) + 1024;
+                                                 c.f_out * c.f_in * p.bins + ccount) + 2048;
     char* cur = static_cast<char*>(ws.get(need));
     float2* G = carve(cur, nB * c.f_out * p.bins);
     float2* DX = carve(cur, nB * c.f_in * p.bins);
     float2* DK = carve(cur, c.f_out * c.f_in * p.bins);
+    float2* CB = carve(cur, ccount);
     // backward image spectra, padded to the tail dims (engine.hpp:757-759)
     forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G);
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
-        const dim3 grid{unsigned(ceil_div(c.f_in, TB)), unsigned(ceil_div(p.bins, CM_T)), unsigned(ceil_div(nB, TA))};
-        cmac_bwd_k<<<grid, CM_T, 0, st>>>(G, p.K, DX, int(nB), int(c.f_in), int(c.f_out), p.bins);
+        cmac_ss(st, G, p.K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
         launch_check("fft_cmac_bwd");
-        inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3);
+        inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB);
         p.cnt.bwd_inverse += nB * c.f_in;
     }
     // kernel gradient: one gradient-specific inverse per edge, sampled at s*w
-    const dim3 gu{unsigned(ceil_div(c.f_in, TU)), unsigned(ceil_div(p.bins, CM_T)), unsigned(ceil_div(c.f_out, TU))};
-    cmac_upd_k<<<gu, CM_T, 0, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
+    {
+        require(nB <= 16, "fft cmac_upd: batch per GPU > 16 (shared-memory staging)");
+        const size_t smem = sizeof(float4) * size_t(nB * (UI + UO) * (SB / 2));
+        const dim3 gu(unsigned(ceil_div(c.f_in, UI) * ceil_div(c.f_out, UO)), unsigned(ceil_div(p.bins, SB)), 1u);
+        allow_smem(cmac_upd_ss_k, smem);
+        cmac_upd_ss_k<<<gu, SS_THREADS, smem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
+    }
     launch_check("fft_cmac_upd");
-    inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3);
+    inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
     p.cnt.upd_inverse += c.f_out * c.f_in;
 }
 
