@@ -298,8 +298,15 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_k(float2* __restrict__ spe
                 v[n2] = (ok && t < RX1 && x < nx) ? pl[x * PYP + y] : make_float2(0.f, 0.f);
             }
             line_fft<PX, false>(v, xb, twx, t, [&](int k, float2 val) {
-                if (ok) g[k * PY + y] = val;
+                if (ok) pl[k * PYP + y] = val;  // the column was consumed into registers
             });
+        }
+        __syncthreads();
+        // coalesced write-back of the whole plane, 2 bins per 16-byte store
+        for (int idx = threadIdx.x; idx < PX * PY / 2; idx += THREADS) {
+            const int e = 2 * idx, x = e / PY, y = e - (e / PY) * PY;
+            const float2 a = pl[x * PYP + y], b = pl[x * PYP + y + 1];
+            reinterpret_cast<float4*>(g)[idx] = make_float4(a.x, a.y, b.x, b.y);
         }
     }
 }
@@ -328,7 +335,15 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_k(const float2* __restrict
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     float2* xb = xbuf + l * PM;
     if constexpr (PX > 1) {
-        // column inverses straight from HBM; keep rows x_step * i (i < xc)
+        // coalesced load of the whole plane (16-byte loads), then column
+        // inverses from shared memory; keep rows x_step * i (i < xc)
+        for (int idx = threadIdx.x; idx < PX * PY / 2; idx += THREADS) {
+            const int e = 2 * idx, x = e / PY, y = e - (e / PY) * PY;
+            const float4 a = __ldcs(reinterpret_cast<const float4*>(g) + idx);
+            pl[x * PYP + y] = make_float2(a.x, a.y);
+            pl[x * PYP + y + 1] = make_float2(a.z, a.w);
+        }
+        __syncthreads();
         for (int c0 = 0; c0 < PY; c0 += LINES) {
             const int y = c0 + l;
             const bool ok = y < PY;
@@ -336,7 +351,7 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_k(const float2* __restrict
 #pragma unroll
             for (int n2 = 0; n2 < RX2; ++n2) {
                 const int x = t + RX1 * n2;
-                v[n2] = (ok && t < RX1) ? __ldcs(g + x * PY + y) : make_float2(0.f, 0.f);
+                v[n2] = (ok && t < RX1) ? pl[x * PYP + y] : make_float2(0.f, 0.f);
             }
             line_fft<PX, true>(v, xb, twx, t, [&](int k, float2 val) {
                 const int i = k / x_step;

@@ -1,5 +1,5 @@
 """Run W+K training steps of a config with fixed per-layer engines (profiling
-helper, not a test): python tests/_net_steps.py c4 fft,fft,fft,direct [steps]"""
+helper, not a test): python tests/_net_steps.py c4 fft,fft,fft,direct|auto [steps]"""
 import sys
 import time
 
@@ -20,10 +20,14 @@ x = torch.as_tensor(rng.uniform(0, 1, size=(B, cfg.in_maps) + cfg.in_dims).astyp
 nout = cfg.layers[-1].width
 lab = torch.as_tensor((rng.uniform(size=(B, nout) + cfg.out_dims) < 0.5).astype(np.float32), device='cuda')
 net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=B, lr=cfg.lr, momentum=cfg.momentum, loss=cfg.loss)
-if engines:
+net.set_params(C.init_params(cfg, 1))
+if engines == ['auto']:
+    net.forward_backward(x, lab)
+    print(net.autotune(3), flush=True)
+    print('\n'.join(l for l in net.describe().splitlines() if 'autotune' in l), flush=True)
+elif engines:
     for i, e in enumerate(engines):
         net.set_layer_engine(i, e)
-net.set_params(C.init_params(cfg, 1))
 for i in range(steps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
