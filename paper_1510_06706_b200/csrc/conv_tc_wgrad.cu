@@ -51,7 +51,7 @@ struct wg_params {
     int ny, nz, my, mz;
 };
 
-template <int NTMAX>
+template <int NTMAX, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
 wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
                 const float* __restrict__ x, const int* __restrict__ rowoff_g, float* __restrict__ ws,
@@ -61,7 +61,9 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* base_ptr = smem_raw + (base - raw);
-    const uint32_t b_bytes = uint32_t(p.nt) * 128u;
+    // PAIR: this CTA holds half of the g tile (nt/2 output maps); the pair MMA
+    // reads both halves. Otherwise the whole tile (multicast to the cluster).
+    const uint32_t b_bytes = uint32_t(PAIR ? p.nt / 2 : p.nt) * 128u;
     const uint32_t stage_bytes = 2u * b_bytes;
     const uint32_t bar_base = base + uint32_t(p.stages) * stage_bytes;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
@@ -84,25 +86,32 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
 
     if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : -1;
     if (threadIdx.x == 0) {
+        // PAIR: the leader's full / A-written / drained barriers collect both
+        // CTAs (elected remote arrives); every CTA's empty / A-free /
+        // chunk-ready barriers receive the leader's multicast commits.
         for (int s = 0; s < p.stages; ++s) {
-            mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), uint32_t(p.csize));  // every CTA of the cluster consumed slot s
+            mbar_init(full_bar(s), PAIR ? 2u : 1u);
+            mbar_init(empty_bar(s), PAIR ? 1u : uint32_t(p.csize));  // every CTA of the cluster consumed slot s
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8u * b, 1);
-            mbar_init(acce0 + 8u * b, 256);
-            mbar_init(af0 + 8u * b, 128);
+            mbar_init(acce0 + 8u * b, PAIR ? 16u : 256u);
+            mbar_init(af0 + 8u * b, PAIR ? 8u : 128u);
             mbar_init(ae0 + 8u * b, 1);
         }
         fence_barrier_init();
     }
-    if (warp == 9) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    if (warp == 9) {
+        if constexpr (PAIR) tmem_alloc_pair(smem_u32(tmem_slot), TMEM_COLS);
+        else tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    }
     tc_fence_before();
     __syncthreads();
     if (p.csize > 1) cluster_sync();  // peers' barriers exist before any multicast lands
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
+    const uint32_t rank = p.csize > 1 ? cluster_ctarank() : 0u;
 
     if (warp < 8) setmaxnreg_inc<224>();
     else setmaxnreg_dec<56>();
@@ -115,6 +124,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         const uint32_t lane_base = uint32_t(wq * 32) << 16;
         chunk_drainer<NH> D;
         D.init(accf0, acce0, tmem + lane_base + uint32_t(col0), p.nbuf, p.bstride, ncols, nchunks);
+        if constexpr (PAIR) D.acce_leader = mapa_u32(acce0, 0);
+        const uint32_t af_leader = PAIR ? mapa_u32(af0, 0) : 0u;
         const int mvol = int(p.mvol);
         const int myz = p.my * p.mz;
         float* tp = tpose + warp * (32 * TP);
@@ -165,7 +176,12 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
             }
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(af0 + 8u * uint32_t(a));
+            if constexpr (PAIR) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(af_leader + 8u * uint32_t(a));
+            } else {
+                mbar_arrive(af0 + 8u * uint32_t(a));
+            }
             a += 2;
             if (a >= p.na) a = grp, u ^= 1u;
             D.poll();
@@ -198,7 +214,6 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         // row tiles): each tile leaves L2 once per cluster.
         {  // converged warp, one elected lane issues
             const int C = p.csize;
-            const uint32_t rank = C > 1 ? cluster_ctarank() : 0u;
             const int rows_per = p.nt / C;
             const uint32_t part = uint32_t(rows_per) * 128u;
             const uint16_t mask = uint16_t((1u << C) - 1u);
@@ -211,19 +226,29 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 const int row = int(pb * p.f_out) + n0 + int(rank) * rows_per;
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
-                if (C > 1)
+                if constexpr (PAIR) {
+                    // own half tile into own smem, bytes counted on the leader's barrier
+                    const uint32_t fl = mapa_u32(full_bar(s), 0);
+                    if (elect_one()) {
+                        mbar_expect_tx_cluster(fl, 2u * b_bytes);
+                        tma_load_2d_pair(b_hi, &tm_hi, fl, vcol, row);
+                        tma_load_2d_pair(b_hi + b_bytes, &tm_lo, fl, vcol, row);
+                    }
+                    __syncwarp();
+                } else if (C > 1) {
                     tma_pair_mc_w(full_bar(s), 2u * b_bytes, b_hi + rank * part, &tm_hi, b_hi + b_bytes + rank * part,
                                   &tm_lo, vcol, row, mask);
-                else
+                } else {
                     tma_pair_w(full_bar(s), 2u * b_bytes, b_hi, &tm_hi, b_hi + b_bytes, &tm_lo, vcol, row);
+                }
                 if (++s == p.stages) s = 0, ph ^= 1u;
                 if (++vkb == p.kb_per_patch) vkb = 0, ++pb;  // TMA side: one K-block per step
             }
         }
     } else if (warp == 9) {
         // ---------------- MMA issuer ----------------
-        {  // the whole warp runs the loop (converged); one elected lane issues
-            const uint32_t idesc = idesc_tf32(BM, p.nt);
+        if (!PAIR || rank == 0) {  // the whole warp runs the loop (converged); one elected lane issues
+            const uint32_t idesc = idesc_tf32(PAIR ? 2 * BM : BM, p.nt);
             int b = 0, s = 0, a = 0, kc = 0;
             uint32_t bph = 0, sph = 0, aph = 0;
             for (int kb = 0; kb < kblocks; ++kb) {
@@ -244,14 +269,26 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                     const uint32_t ko = uint32_t(kk) * 32u;
                     const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
                     const uint32_t ah = a_hi + uint32_t(8 * kk), al = a_hi + 32u + uint32_t(8 * kk);
-                    mma_tf32_ts_w(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
-                    mma_tf32_ts_w(d, ah, bl, idesc, 1u);
-                    mma_tf32_ts_w(d, al, bh, idesc, 1u);
+                    if constexpr (PAIR) {
+                        mma_tf32_ts_pair_w(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                        mma_tf32_ts_pair_w(d, ah, bl, idesc, 1u);
+                        mma_tf32_ts_pair_w(d, al, bh, idesc, 1u);
+                    } else {
+                        mma_tf32_ts_w(d, ah, bh, idesc, (first && kk == 0) ? 0u : 1u);
+                        mma_tf32_ts_w(d, ah, bl, idesc, 1u);
+                        mma_tf32_ts_w(d, al, bh, idesc, 1u);
+                    }
                 }
-                if (p.csize > 1) mma_commit_mc_w(empty_bar(s), uint16_t((1u << p.csize) - 1u));
-                else mma_commit_w(empty_bar(s));
-                mma_commit_w(ae0 + 8u * uint32_t(a));
-                if (kc == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit_w(accf0 + 8u * uint32_t(b));
+                if constexpr (PAIR) {
+                    mma_commit_pair_mc_w(empty_bar(s), 3);
+                    mma_commit_pair_mc_w(ae0 + 8u * uint32_t(a), 3);
+                    if (kc == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit_pair_mc_w(accf0 + 8u * uint32_t(b), 3);
+                } else {
+                    if (p.csize > 1) mma_commit_mc_w(empty_bar(s), uint16_t((1u << p.csize) - 1u));
+                    else mma_commit_w(empty_bar(s));
+                    mma_commit_w(ae0 + 8u * uint32_t(a));
+                    if (kc == CHUNK_KB - 1 || kb == kblocks - 1) mma_commit_w(accf0 + 8u * uint32_t(b));
+                }
                 if (++s == p.stages) s = 0, sph ^= 1u;
                 if (++a == p.na) a = 0, aph ^= 1u;
                 if (++kc == CHUNK_KB) {
@@ -263,12 +300,13 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     }
     tc_fence_before();
     __syncthreads();
+    if (p.csize > 1) cluster_sync();  // no CTA leaves (or frees TMEM) while its peer still uses it
     if (warp == 9) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc(tmem, TMEM_COLS);
+        if constexpr (PAIR) tmem_dealloc_pair(tmem, TMEM_COLS);
+        else tmem_dealloc(tmem, TMEM_COLS);
     }
-    if (p.csize > 1) cluster_sync();  // no CTA leaves while peers may still arrive on its barriers
 }
 
 __global__ void rowoff_k(int* __restrict__ out, int mrows, int T, int ky, int kz, int sx, int sy, int sz, int ny,
@@ -312,10 +350,10 @@ __global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, in
     }
 }
 
-template <int NTMAX>
+template <int NTMAX, bool PAIR>
 void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mhi, const CUtensorMap& mlo,
                   const float* x, const int* rowoff, float* ws, const wg_params& p) {
-    auto* k = wgrad_tc_kernel<NTMAX>;
+    auto* k = wgrad_tc_kernel<NTMAX, PAIR>;
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -334,15 +372,18 @@ void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mh
 }
 
 // CTAs resident at once (one per SM; clusters cannot use every SM of a GPC)
-int64_t resident_ctas(int ntmax, size_t smem, int csize) {
-    static int64_t cache[3][3] = {};
+int64_t resident_ctas(int ntmax, size_t smem, int csize, bool pair) {
+    static int64_t cache[3][3][2] = {};
     const int ti = ntmax == 32 ? 0 : (ntmax == 64 ? 1 : 2), ci = csize == 1 ? 0 : (csize == 2 ? 1 : 2);
-    if (cache[ti][ci]) return cache[ti][ci];
+    if (cache[ti][ci][pair]) return cache[ti][ci][pair];
     int64_t r = 148;
     if (csize > 1) {
-        const void* k = ntmax == 32 ? reinterpret_cast<const void*>(wgrad_tc_kernel<32>)
-                        : ntmax == 64 ? reinterpret_cast<const void*>(wgrad_tc_kernel<64>)
-                                      : reinterpret_cast<const void*>(wgrad_tc_kernel<128>);
+        const void* k = pair ? (ntmax == 32   ? reinterpret_cast<const void*>(wgrad_tc_kernel<32, true>)
+                                : ntmax == 64 ? reinterpret_cast<const void*>(wgrad_tc_kernel<64, true>)
+                                              : reinterpret_cast<const void*>(wgrad_tc_kernel<128, true>))
+                             : (ntmax == 32   ? reinterpret_cast<const void*>(wgrad_tc_kernel<32, false>)
+                                : ntmax == 64 ? reinterpret_cast<const void*>(wgrad_tc_kernel<64, false>)
+                                              : reinterpret_cast<const void*>(wgrad_tc_kernel<128, false>));
         ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(csize) * 64, 1, 1);
@@ -359,7 +400,7 @@ int64_t resident_ctas(int ntmax, size_t smem, int csize) {
         if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) == cudaSuccess && nc > 0) r = int64_t(nc) * csize;
         else cudaGetLastError();
     }
-    cache[ti][ci] = r;
+    cache[ti][ci][pair] = r;
     return r;
 }
 
@@ -379,10 +420,6 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     p.bstride = ntmax;
     p.nbuf = ntmax == 128 ? 2 : 4;  // + na x 64 A columns <= 512 TMEM columns
     p.na = 4;
-    const int stage = 2 * p.nt * 128;
-    const size_t fixed = 1024 + 8 * size_t(16) + 16 + sizeof(float) * 8 * 32 * TP + 64;
-    p.stages = int((size_t(220) * 1024 - fixed) / size_t(stage + 16));
-    if (p.stages > 8) p.stages = 8;
     p.nvol = c.n.vol();
     p.mvol = c.m.vol();
     p.ny = int(c.n.y), p.nz = int(c.n.z), p.my = int(c.m.y), p.mz = int(c.m.z);
@@ -395,13 +432,23 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     while (csize > 1 && (p.nt % (8 * csize) != 0 || ceil_div(p.mrows, BM) < csize)) csize /= 2;
     if (csize != 1 && csize != 2 && csize != 4) csize = 1;
     p.csize = csize;
+    // CTA pairs (cta_group::2, M = 256): each CTA stages half of the g tile
+    // and the pair MMA reads both halves, halving B's shared-memory traffic.
+    // Parity-green but measured slower on c5 (conv2 wgrad 232 vs 197 ms: the
+    // pair MMA waits for the slower CTA's producers), so opt-in only.
+    bool pair = false;
+    if (const char* e = std::getenv("ZNN_WGRAD_PAIR")) pair = csize == 2 && p.nt % 32 == 0 && std::atoi(e) != 0;
+    const int stage = 2 * (pair ? p.nt / 2 : p.nt) * 128;
+    const size_t fixed = 1024 + 8 * size_t(16) + 16 + sizeof(float) * 8 * 32 * TP + 64;
+    p.stages = int((size_t(220) * 1024 - fixed) / size_t(stage + 16));
+    if (p.stages > 8) p.stages = 8;
     const int mtiles = int(ceil_div(ceil_div(p.mrows, BM), csize) * csize);
     // split-K factor: fill whole waves of 148 SMs (one CTA each). The first
     // split count >= 2 waves whose last wave is >= 97% full, else the best
     // fill up to max(32, 8 waves' worth) splits (a 2.4-wave grid idles 20% of the GPU in its tail).
     const int64_t tiles = int64_t(mtiles) * ntiles;
     const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
-    const int64_t wave = resident_ctas(ntmax, smem, csize);
+    const int64_t wave = resident_ctas(ntmax, smem, csize, pair);
     const int64_t max_splits = std::max<int64_t>(
         1, std::min<int64_t>(std::max<int64_t>(32, ceil_div(8 * 148, tiles)), ceil_div(p.kb_total, 4 * CHUNK_KB)));
     int64_t splits = 1;
@@ -438,9 +485,15 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     const CUtensorMap mhi = make_panel_map_rows(ghi, mpad, grows, p.nt / csize);
     const CUtensorMap mlo = make_panel_map_rows(glo, mpad, grows, p.nt / csize);
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
-    if (ntmax == 32) launch_wgrad<32>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
-    else if (ntmax == 64) launch_wgrad<64>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
-    else launch_wgrad<128>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+    if (pair) {
+        if (ntmax == 32) launch_wgrad<32, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else if (ntmax == 64) launch_wgrad<64, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else launch_wgrad<128, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+    } else {
+        if (ntmax == 32) launch_wgrad<32, false>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else if (ntmax == 64) launch_wgrad<64, false>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else launch_wgrad<128, false>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+    }
     const int64_t len = c.f_out * int64_t(p.mrows);
     int64_t rb = ceil_div(len, 256);
     if (rb > 148 * 8) rb = 148 * 8;

@@ -73,6 +73,67 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, pe;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+// ---- CTA-pair (cta_group::2) helpers ----
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster),
+                 "r"(bytes)
+                 : "memory");
+}
+// TMA into this CTA's shared memory, completion counted on the pair leader's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+        "[%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t slot_smem, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot_smem), "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t tmem, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+// pair MMA (issued by the leader CTA): M = 256 rows (128 from each CTA's
+// TMEM), B halves from both CTAs' shared memory, D in both CTAs' TMEM
+__device__ __forceinline__ void mma_tf32_ts_pair_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                                   uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred pe, pa;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "setp.ne.b32 pa, %4, 0;\n\t"
+        "@pe tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, pa;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_pair_mc_w(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "@pe tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            bar),
+        "h"(mask)
+        : "memory");
+}
+
 // warpgroup register rebalancing (all 128 threads of the warpgroup execute it)
 template <int N>
 __device__ __forceinline__ void setmaxnreg_inc() {
@@ -280,12 +341,18 @@ struct chunk_drainer {
         next = 0, buf = 0, phase = 0;
         A.zero();
     }
+    uint32_t acce_leader = 0;  // != 0: CTA pair, one elected arrive per warp on the leader's barrier
     __device__ __forceinline__ void drain_one() {
         mbar_wait(accf0 + 8u * uint32_t(buf), phase);
         tc_fence_after();
         if (ncols > 0) A.add(lane_base + uint32_t(buf * bstride), ncols);
         tc_fence_before();
-        mbar_arrive(acce0 + 8u * uint32_t(buf));
+        if (acce_leader) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(acce_leader + 8u * uint32_t(buf));
+        } else {
+            mbar_arrive(acce0 + 8u * uint32_t(buf));
+        }
         ++next;
         if (++buf == nbuf) buf = 0, phase ^= 1u;
     }
