@@ -325,12 +325,27 @@ def dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream):
         src = "measured in-run: cuBLAS TF32 dense 8192^3 (MEASURED_PEAKS.json has bf16 only)"
     except Exception:
         peak, src = 1100.0, "nominal TF32 dense (fallback)"
-    return {"bound": "tensor", "kernel": f"conv_{dom} f={fi}->{fo} n={tuple(n)} k={tuple(k)} s={tuple(s)} B={Bl}",
+    shape = f"conv f={fi}->{fo} n={tuple(n)} k={tuple(k)} s={tuple(s)} B={Bl}"
+    traffic, traffic_src = None, None
+    # DRAM bytes of this launch from the committed ncu capture of the same
+    # shape (profiles/r01_traffic_*.json), when one exists
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json"))):
+        try:
+            with open(f) as fh:
+                cap = json.load(fh)
+            if cap.get("shape") == shape and dom in cap.get("per_launch", {}):
+                traffic = cap["per_launch"][dom]["dram_bytes"]
+                traffic_src = os.path.relpath(f, ROOT) + " (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
+        except Exception:
+            pass
+    return {"bound": "tensor", "kernel": f"conv_{dom} " + shape[5:],
             "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "achieved_is": "algorithmic fp32 FLOP/s (2 f f' n'^3 k^3 per launch / CUDA-event duration); "
                            "3xTF32 issues 3 tensor MMAs per MAC, so tensor-pipe work is 3x this",
             "tensor_pipe_frac": 3 * achieved / peak,
-            "peak_source": src, "launch_ms": dur * 1e3, "traffic": None,
+            "peak_source": src, "launch_ms": dur * 1e3, "traffic": traffic, "traffic_unit": "bytes per launch",
+            "traffic_source": traffic_src,
             "passes_tflops": {p: flops / t / 1e12 for p, t in times.items()}}
 
 
