@@ -10,8 +10,9 @@
 //       voxel), transposes the 32x32 block through a private shared-memory
 //       tile (conflict-free, pitch 33), splits hi/lo and writes its lanes with
 //       tcgen05.st; the MMA reads A from TMEM (kind::tf32).
-//   B (g rows)                  : pre-split into hi/lo panels [B*f_out][mpad]
-//       by one memory-bound pass, then TMA-loaded (SWIZZLE_128B).
+//   B (g rows)                  : pre-split into hi/lo tiles [B][map tile][K-block][nt][32]
+//       by one memory-bound pass (each TMA box one contiguous block), then
+//       TMA-loaded (SWIZZLE_128B), multicast to the 2 CTAs of a cluster.
 // Each CTA owns a contiguous K range (split-K); partial tiles land in a
 // workspace [split][o][R] and a fixed-order reduction sums them
 // (deterministic).
@@ -45,6 +46,7 @@ struct wg_params {
     int f_in, f_out, T, nt;
     int mrows;  // f_in * T
     int stages, nbuf, bstride, na;
+    int ntiles; // output-map tiles (grid y)
     int csize;  // CTAs per cluster along the row tiles: they share (multicast) every g tile
     int64_t kb_per_patch, kb_total, kb_per_split;
     int64_t nvol, mvol;
@@ -222,8 +224,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
             int64_t pb = q0 / p.kb_per_patch;
             int vkb = int(q0 - pb * p.kb_per_patch);
             for (int kb = 0; kb < kblocks; ++kb) {
-                const int vcol = vkb * BK;
-                const int row = int(pb * p.f_out) + n0 + int(rank) * rows_per;
+                // g tiles are stored contiguously ([patch][map tile][K-block][nt rows][32]),
+                // so a box is one 16 KB DRAM stream instead of nt scattered 128 B rows
+                const int vcol = 0;
+                const int row = int(((pb * p.ntiles + blockIdx.y) * p.kb_per_patch + vkb) * p.nt) + int(rank) * rows_per;
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 if constexpr (PAIR) {
@@ -318,27 +322,32 @@ __global__ void rowoff_k(int* __restrict__ out, int mrows, int T, int ky, int kz
     }
 }
 
-// g [rows][mvol] -> hi/lo [rows][mpad] (zero padded columns): the TMA panels.
-// grid: x over columns (float4 groups), y over rows.
-__global__ void split_rows_k(const float* __restrict__ g, int64_t rows, int64_t mvol, int64_t mpad,
-                             float* __restrict__ hi, float* __restrict__ lo) {
-    const int64_t c0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
-    if (c0 >= mpad) return;
-    {
-        const int64_t r = blockIdx.y + int64_t(blockIdx.z) * gridDim.y;
-        if (r >= rows) return;
-        const float* src = g + r * mvol;
-        float v[4], h[4], l[4];
+// g [B][f_out][mvol] -> hi/lo tiles [B][map tile][K-block][R rows][32] (zero
+// padded rows / columns): one TMA box per (patch, map tile, K-block) is a
+// contiguous 128*R-byte block. grid: x = float4 in a tile, y = K-block,
+// z = patch * map tiles + map tile.
+__global__ void split_tiles_k(const float* __restrict__ g, int f_out, int64_t mvol, int R, int ntiles, int64_t kbpp,
+                              float* __restrict__ hi, float* __restrict__ lo) {
+    const int e4 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e4 >= R * (BK / 4)) return;
+    const int r = e4 / (BK / 4), c4 = e4 - r * (BK / 4);
+    const int64_t q = blockIdx.y;
+    const int64_t z = blockIdx.z;
+    const int64_t pb = z / ntiles;
+    const int o = int(z - pb * ntiles) * R + r;
+    const int64_t col = q * BK + c4 * 4;
+    float v[4], h[4], l[4];
+    const float* src = g + (pb * f_out + o) * mvol;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = c0 + q < mvol ? __ldg(src + c0 + q) : 0.f;
+    for (int k = 0; k < 4; ++k) v[k] = (o < f_out && col + k < mvol) ? __ldg(src + col + k) : 0.f;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            h[q] = tf32_hi(v[q]);
-            l[q] = tf32_rn(v[q] - h[q]);
-        }
-        *reinterpret_cast<float4*>(hi + r * mpad + c0) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(lo + r * mpad + c0) = make_float4(l[0], l[1], l[2], l[3]);
+    for (int k = 0; k < 4; ++k) {
+        h[k] = tf32_hi(v[k]);
+        l[k] = tf32_rn(v[k] - h[k]);
     }
+    const int64_t dst = ((z * kbpp + q) * R + r) * BK + c4 * 4;
+    *reinterpret_cast<float4*>(hi + dst) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(lo + dst) = make_float4(l[0], l[1], l[2], l[3]);
 }
 
 __global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, int64_t len, float scale,
@@ -465,25 +474,25 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     p.kb_per_split = ceil_div(p.kb_total, splits);
     splits = ceil_div(p.kb_total, p.kb_per_split);
 
-    const int64_t mpad = p.kb_per_patch * BK;
-    const int64_t grows = c.B * c.f_out;
-    const size_t panel = size_t(grows) * size_t(mpad);
+    p.ntiles = ntiles;
+    const int64_t gtiles = c.B * ntiles * p.kb_per_patch;  // (patch, map tile, K-block) tiles
+    const size_t panel = size_t(gtiles) * size_t(p.nt) * BK;
     const size_t part = size_t(splits) * size_t(c.f_out) * size_t(p.mrows);
     char* wsp = static_cast<char*>(ws.get(sizeof(float) * (2 * panel + part) + sizeof(int) * size_t(p.mrows) + 4096));
     float* ghi = reinterpret_cast<float*>(wsp);
     float* glo = ghi + panel;
     float* partials = glo + panel;
     int* rowoff = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(partials + part) + 255) & ~uintptr_t(255));
-    const int64_t sgy = grows < 65535 ? grows : 65535;
-    const dim3 sgrid(unsigned(ceil_div(mpad / 4, 256)), unsigned(sgy), unsigned(ceil_div(grows, sgy)));
-    split_rows_k<<<sgrid, 256, 0, st>>>(g, grows, p.mvol, mpad, ghi, glo);
+    require(p.kb_per_patch < 65536 && c.B * ntiles < 65536, "wgrad: volume too large for the tile grid");
+    const dim3 sgrid(unsigned(ceil_div(p.nt * (BK / 4), 256)), unsigned(p.kb_per_patch), unsigned(c.B * ntiles));
+    split_tiles_k<<<sgrid, 256, 0, st>>>(g, int(c.f_out), p.mvol, p.nt, ntiles, p.kb_per_patch, ghi, glo);
     launch_check("conv_wgrad_tc_split");
     rowoff_k<<<unsigned(ceil_div(p.mrows, 256)), 256, 0, st>>>(rowoff, p.mrows, p.T, int(c.k.y), int(c.k.z),
                                                                int(c.s.x), int(c.s.y), int(c.s.z), p.ny, p.nz,
                                                                p.nvol);
     launch_check("conv_wgrad_tc_rowoff");
-    const CUtensorMap mhi = make_panel_map_rows(ghi, mpad, grows, p.nt / csize);
-    const CUtensorMap mlo = make_panel_map_rows(glo, mpad, grows, p.nt / csize);
+    const CUtensorMap mhi = make_panel_map_rows(ghi, BK, gtiles * p.nt, p.nt / csize);
+    const CUtensorMap mlo = make_panel_map_rows(glo, BK, gtiles * p.nt, p.nt / csize);
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
     if (pair) {
         if (ntmax == 32) launch_wgrad<32, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
