@@ -330,24 +330,21 @@ __global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int ky
 }
 
 // g [maps][m] -> gp [maps][m + 2P] with a zero halo of P = s*(k-1) per side.
-// grid: x over the padded voxels of one map (32-bit index math), y over maps.
-__global__ void pad_halo_k(const float* __restrict__ g, int64_t maps, int mx, int my, int mz, int px, int py, int pz,
-                           float* __restrict__ gp) {
+// block = 32 z-lanes x 8 padded y-rows; grid = (y tiles, padded x, maps).
+__global__ void __launch_bounds__(256) pad_halo_k(const float* __restrict__ g, int mx, int my, int mz, int px, int py,
+                                                  int pz, float* __restrict__ gp) {
     const int gx = mx + 2 * px, gy = my + 2 * py, gz = mz + 2 * pz;
-    const unsigned pv = unsigned(gx) * unsigned(gy) * unsigned(gz);
-    const unsigned r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= pv) return;
-    const unsigned gyz = unsigned(gy) * unsigned(gz);
-    const int x = int(r / gyz);
-    const unsigned r2 = r - unsigned(x) * gyz;
-    const int y = int(r2 / unsigned(gz));
-    const int z = int(r2 - unsigned(y) * unsigned(gz));
-    const int ux = x - px, uy = y - py, uz = z - pz;
-    const bool in = unsigned(ux) < unsigned(mx) && unsigned(uy) < unsigned(my) && unsigned(uz) < unsigned(mz);
-    const int src = (ux * my + uy) * mz + uz;
-    const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t map = blockIdx.y + int64_t(blockIdx.z) * gridDim.y;
-    if (map < maps) gp[map * int64_t(pv) + r] = in ? __ldg(g + map * mv + src) : 0.f;
+    const int y = blockIdx.x * 8 + threadIdx.y, x = blockIdx.y;
+    if (y >= gy) return;
+    const int64_t map = blockIdx.z;
+    float* dst = gp + map * (int64_t(gx) * gy * gz) + (int64_t(x) * gy + y) * gz;
+    const int ux = x - px, uy = y - py;
+    const bool rin = unsigned(ux) < unsigned(mx) && unsigned(uy) < unsigned(my);
+    const float* src = g + map * (int64_t(mx) * my * mz) + (int64_t(ux) * my + uy) * mz;
+    for (int z = threadIdx.x; z < gz; z += 32) {
+        const int uz = z - pz;
+        __stcs(dst + z, (rin && unsigned(uz) < unsigned(mz)) ? __ldcs(src + uz) : 0.f);
+    }
 }
 
 typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -496,9 +493,10 @@ void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const f
     char* wsp = static_cast<char*>(ws.get(gpad + panel_bytes(int(c.f_out), int(c.f_in), c.taps())));
     float* gp = reinterpret_cast<float*>(wsp);
     const int64_t pmaps = c.B * c.f_out;
-    const int64_t pgy = pmaps < 65535 ? pmaps : 65535;
-    const dim3 pgrid(unsigned(ceil_div(gd.vol(), 256)), unsigned(pgy), unsigned(ceil_div(pmaps, pgy)));
-    pad_halo_k<<<pgrid, 256, 0, st>>>(g, pmaps, int(c.m.x), int(c.m.y), int(c.m.z), int(P.x), int(P.y), int(P.z), gp);
+    require(gd.x < 65536 && pmaps < 65536, "conv_dgrad_tc: halo grid exceeds 65535");
+    const dim3 pgrid(unsigned(ceil_div(gd.y, 8)), unsigned(gd.x), unsigned(pmaps));
+    pad_halo_k<<<pgrid, dim3(32, 8, 1), 0, st>>>(g, int(c.m.x), int(c.m.y), int(c.m.z), int(P.x), int(P.y), int(P.z),
+                                                 gp);
     launch_check("conv_dgrad_tc_pad");
     launch_valid(st, c.B, int(c.f_out), int(c.f_in), int(c.f_in), gd, c.k, c.s, gp, w, 1, nullptr, 3, dx,
                  wsp + gpad, P, c.m, "conv_dgrad_tc");

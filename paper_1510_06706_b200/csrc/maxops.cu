@@ -1,7 +1,7 @@
 // Max-pooling and dense (dilated) max-filtering with argmax masks
-// (maxops.hpp:32-182). HBM-bound; one thread per output voxel forward, one
-// thread per input voxel backward (gather formulation: deterministic, no
-// atomics). Mask = int32 flat index into the per-map input volume.
+// (maxops.hpp:32-182). HBM-bound; a thread per output voxel forward and per
+// input voxel backward (gather formulation: deterministic, no atomics).
+// Mask = int32 flat index into the per-map input volume.
 //
 // Tie rule: the reference resolves ties to the lexicographically smallest
 // (x,y,z) source, i.e. the lowest flat index (maxops.hpp:79-82 strict '>'
@@ -14,42 +14,32 @@ namespace znn_gpu {
 
 namespace {
 
-constexpr int kThreads = 256;
-
-// Grid: x covers the voxels of one map (32-bit index math only — 64-bit
-// division per voxel made these kernels issue-bound at ~15% of HBM), y the
-// maps.
-inline dim3 grid2(int64_t per_map, int64_t maps) {
-    const int64_t gx = ceil_div(per_map, kThreads);
-    const int64_t gy = maps < 65535 ? (maps < 1 ? 1 : maps) : 65535;
-    return dim3(unsigned(gx < 1 ? 1 : gx), unsigned(gy), unsigned(ceil_div(maps < 1 ? 1 : maps, gy)));
+// Volume grid (no per-element index division): a block is 32 z-lanes x 8
+// y-rows of one x-plane of one map; blockIdx = (y tile, x, map). A thread
+// walks its row along z in steps of 32 (coalesced along the contiguous axis).
+constexpr int ZL = 32, YR = 8;
+inline dim3 vgrid(int64_t y, int64_t x, int64_t maps) {
+    require(x < 65536 && maps < 65536, "maxops: volume grid exceeds 65535 planes / maps");
+    return dim3(unsigned(ceil_div(y, YR)), unsigned(x), unsigned(maps));
 }
-// map of this block (y, z fold the map count past 65535): no per-thread loop,
-// whose 64-bit trip-count division cost more than the voxel's work
-__device__ __forceinline__ int64_t block_map() { return blockIdx.y + int64_t(blockIdx.z) * gridDim.y; }
+inline dim3 vblock() { return dim3(ZL, YR, 1); }
 
 // KX/KY/KZ > 0: compile-time window (fully unrolled, the common 2^3 and
 // 1x2x2 filters); 0: runtime window.
 template <int KX, int KY, int KZ>
-__global__ void __launch_bounds__(kThreads) maxfilter_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny,
-                                                            int nz, int mx, int my, int mz, int kx_, int ky_, int kz_,
-                                                            int sx, int sy, int sz, float* __restrict__ y,
-                                                            int32_t* __restrict__ mask) {
+__global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restrict__ x, int nx, int ny, int nz,
+                                                           int mx, int my, int mz, int kx_, int ky_, int kz_, int sx,
+                                                           int sy, int sz, float* __restrict__ y,
+                                                           int32_t* __restrict__ mask) {
     const int kx = KX ? KX : kx_, ky = KY ? KY : ky_, kz = KZ ? KZ : kz_;
-    const unsigned mv = unsigned(mx) * unsigned(my) * unsigned(mz);
-    const unsigned r = blockIdx.x * kThreads + threadIdx.x;
-    if (r >= mv) return;
-    const unsigned myz = unsigned(my) * unsigned(mz);
-    const int i = int(r / myz);
-    const unsigned r2 = r - unsigned(i) * myz;
-    const int j = int(r2 / unsigned(mz));
-    const int l = int(r2 - unsigned(j) * unsigned(mz));
-    const int base = (i * ny + j) * nz + l;
+    const int j = blockIdx.x * YR + threadIdx.y, i = blockIdx.y;
+    if (j >= my) return;
+    const int64_t map = blockIdx.z;
+    const float* xm = x + map * (int64_t(nx) * ny * nz);
+    const int64_t orow = map * (int64_t(mx) * my * mz) + (int64_t(i) * my + j) * mz;
     const int dx = sx * ny * nz, dy = sy * nz;
-    {
-        const int64_t map = block_map();
-        if (map >= maps) return;
-        const float* xm = x + map * (int64_t(nx) * ny * nz);
+    for (int l = threadIdx.x; l < mz; l += ZL) {
+        const int base = (i * ny + j) * nz + l;
         int best_idx = base;
         float best = __ldg(xm + base);
 #pragma unroll
@@ -65,8 +55,8 @@ __global__ void __launch_bounds__(kThreads) maxfilter_fwd_k(const float* __restr
                         best_idx = idx;
                     }
                 }
-        y[map * int64_t(mv) + r] = best;
-        mask[map * int64_t(mv) + r] = best_idx;
+        __stcs(y + orow + l, best);
+        __stcs(mask + orow + l, best_idx);
     }
 }
 
@@ -74,25 +64,20 @@ __global__ void __launch_bounds__(kThreads) maxfilter_fwd_k(const float* __restr
 // ascending flat order of o, the order the reference accumulates in
 // (maxops.hpp:176-181), so fp32 sums match it bit for bit.
 template <int KX, int KY, int KZ>
-__global__ void __launch_bounds__(kThreads) maxfilter_bwd_k(const float* __restrict__ g,
-                                                            const int32_t* __restrict__ mask, int64_t maps, int nx,
-                                                            int ny, int nz, int mx, int my, int mz, int kx_, int ky_,
-                                                            int kz_, int sx, int sy, int sz, float* __restrict__ dx) {
+__global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restrict__ g,
+                                                           const int32_t* __restrict__ mask, int nx, int ny, int nz,
+                                                           int mx, int my, int mz, int kx_, int ky_, int kz_, int sx,
+                                                           int sy, int sz, float* __restrict__ dx) {
     const int kx = KX ? KX : kx_, ky = KY ? KY : ky_, kz = KZ ? KZ : kz_;
-    const unsigned nv = unsigned(nx) * unsigned(ny) * unsigned(nz);
-    const unsigned tr = blockIdx.x * kThreads + threadIdx.x;
-    if (tr >= nv) return;
-    const unsigned nyz = unsigned(ny) * unsigned(nz);
-    const int ti = int(tr / nyz);
-    const unsigned r2 = tr - unsigned(ti) * nyz;
-    const int tj = int(r2 / unsigned(nz));
-    const int tl = int(r2 - unsigned(tj) * unsigned(nz));
+    const int tj = blockIdx.x * YR + threadIdx.y, ti = blockIdx.y;
+    if (tj >= ny) return;
+    const int64_t map = blockIdx.z;
     const int64_t mv = int64_t(mx) * my * mz;
-    {
-        const int64_t map = block_map();
-        if (map >= maps) return;
-        const float* gm = g + map * mv;
-        const int32_t* mm = mask + map * mv;
+    const float* gm = g + map * mv;
+    const int32_t* mm = mask + map * mv;
+    float* drow = dx + map * (int64_t(nx) * ny * nz) + (int64_t(ti) * ny + tj) * nz;
+    for (int tl = threadIdx.x; tl < nz; tl += ZL) {
+        const int tr = (ti * ny + tj) * nz + tl;
         float acc = 0.f;
 #pragma unroll
         for (int a = kx - 1; a >= 0; --a) {
@@ -107,31 +92,25 @@ __global__ void __launch_bounds__(kThreads) maxfilter_bwd_k(const float* __restr
                     const int ol = tl - sz * c;
                     if (ol < 0 || ol >= mz) continue;
                     const int o = (oi * my + oj) * mz + ol;
-                    if (__ldg(mm + o) == int(tr)) acc += __ldg(gm + o);
+                    if (__ldg(mm + o) == tr) acc += __ldg(gm + o);
                 }
             }
         }
-        dx[map * int64_t(nv) + tr] = acc;
+        __stcs(drow + tl, acc);
     }
 }
 
-__global__ void __launch_bounds__(kThreads) maxpool_fwd_k(const float* __restrict__ x, int64_t maps, int nx, int ny,
-                                                          int nz, int px, int py, int pz, float* __restrict__ y,
-                                                          int32_t* __restrict__ mask) {
+__global__ void __launch_bounds__(ZL * YR) maxpool_fwd_k(const float* __restrict__ x, int nx, int ny, int nz, int px,
+                                                         int py, int pz, float* __restrict__ y,
+                                                         int32_t* __restrict__ mask) {
     const int mx = nx / px, my = ny / py, mz = nz / pz;
-    const unsigned mv = unsigned(mx) * unsigned(my) * unsigned(mz);
-    const unsigned r = blockIdx.x * kThreads + threadIdx.x;
-    if (r >= mv) return;
-    const unsigned myz = unsigned(my) * unsigned(mz);
-    const int bi = int(r / myz);
-    const unsigned r2 = r - unsigned(bi) * myz;
-    const int bj = int(r2 / unsigned(mz));
-    const int bl = int(r2 - unsigned(bj) * unsigned(mz));
-    const int base = ((bi * px) * ny + bj * py) * nz + bl * pz;
-    {
-        const int64_t map = block_map();
-        if (map >= maps) return;
-        const float* xm = x + map * (int64_t(nx) * ny * nz);
+    const int bj = blockIdx.x * YR + threadIdx.y, bi = blockIdx.y;
+    if (bj >= my) return;
+    const int64_t map = blockIdx.z;
+    const float* xm = x + map * (int64_t(nx) * ny * nz);
+    const int64_t orow = map * (int64_t(mx) * my * mz) + (int64_t(bi) * my + bj) * mz;
+    for (int bl = threadIdx.x; bl < mz; bl += ZL) {
+        const int base = ((bi * px) * ny + bj * py) * nz + bl * pz;
         int best_idx = base;
         float best = __ldg(xm + base);
         for (int a = 0; a < px; ++a)
@@ -144,28 +123,26 @@ __global__ void __launch_bounds__(kThreads) maxpool_fwd_k(const float* __restric
                         best_idx = idx;
                     }
                 }
-        y[map * int64_t(mv) + r] = best;
-        mask[map * int64_t(mv) + r] = best_idx;
+        y[orow + bl] = best;
+        mask[orow + bl] = best_idx;
     }
 }
 
-__global__ void __launch_bounds__(kThreads) maxpool_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
-                                                          int64_t maps, int mx, int my, int mz, int px, int py, int pz,
-                                                          float* __restrict__ dx) {
+__global__ void __launch_bounds__(ZL * YR) maxpool_bwd_k(const float* __restrict__ g, const int32_t* __restrict__ mask,
+                                                         int mx, int my, int mz, int px, int py, int pz,
+                                                         float* __restrict__ dx) {
     const int nx = mx * px, ny = my * py, nz = mz * pz;
-    const unsigned nv = unsigned(nx) * unsigned(ny) * unsigned(nz);
-    const unsigned tr = blockIdx.x * kThreads + threadIdx.x;
-    if (tr >= nv) return;
-    const unsigned nyz = unsigned(ny) * unsigned(nz);
-    const int ti = int(tr / nyz);
-    const unsigned r2 = tr - unsigned(ti) * nyz;
-    const int tj = int(r2 / unsigned(nz));
-    const int tl = int(r2 - unsigned(tj) * unsigned(nz));
-    const int o = ((ti / px) * my + (tj / py)) * mz + (tl / pz);
+    const int tj = blockIdx.x * YR + threadIdx.y, ti = blockIdx.y;
+    if (tj >= ny) return;
+    const int64_t map = blockIdx.z;
     const int64_t mv = int64_t(mx) * my * mz;
-    const int64_t map = block_map();
-    if (map < maps)
-        dx[map * int64_t(nv) + tr] = (__ldg(mask + map * mv + o) == int(tr)) ? __ldg(g + map * mv + o) : 0.f;
+    const int64_t orow = map * mv + (int64_t(ti / px) * my + (tj / py)) * mz;
+    float* drow = dx + map * (int64_t(nx) * ny * nz) + (int64_t(ti) * ny + tj) * nz;
+    for (int tl = threadIdx.x; tl < nz; tl += ZL) {
+        const int tr = (ti * ny + tj) * nz + tl;
+        const int64_t o = orow + tl / pz;
+        drow[tl] = (__ldg(mask + o) == tr) ? __ldg(g + o) : 0.f;
+    }
 }
 
 }  // namespace
@@ -178,9 +155,9 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
     auto* kf = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_fwd_k<2, 2, 2>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2>
                                                     : maxfilter_fwd_k<0, 0, 0>;
-    kf<<<grid2(m.vol(), maps), kThreads, 0, st>>>(x, maps, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y),
-                                                 int(m.z), int(k.x), int(k.y), int(k.z), int(s.x), int(s.y),
-                                                 int(s.z), y, mask);
+    kf<<<vgrid(m.y, m.x, maps), vblock(), 0, st>>>(x, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
+                                                  int(k.x), int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), y,
+                                                  mask);
     launch_check("maxfilter_fwd");
 }
 
@@ -190,9 +167,9 @@ void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t
     auto* kb = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_bwd_k<2, 2, 2>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_bwd_k<1, 2, 2>
                                                     : maxfilter_bwd_k<0, 0, 0>;
-    kb<<<grid2(n.vol(), maps), kThreads, 0, st>>>(g, mask, maps, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y),
-                                                 int(m.z), int(k.x), int(k.y), int(k.z), int(s.x), int(s.y),
-                                                 int(s.z), dx);
+    kb<<<vgrid(n.y, n.x, maps), vblock(), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y),
+                                                  int(m.z), int(k.x), int(k.y), int(k.z), int(s.x), int(s.y),
+                                                  int(s.z), dx);
     launch_check("maxfilter_bwd");
 }
 
@@ -201,16 +178,15 @@ void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p
     require(p.x > 0 && p.y > 0 && p.z > 0 && n.x % p.x == 0 && n.y % p.y == 0 && n.z % p.z == 0,
             "maxpool_forward: dims not divisible by window");
     const dims3 m{n.x / p.x, n.y / p.y, n.z / p.z};
-    maxpool_fwd_k<<<grid2(m.vol(), maps), kThreads, 0, st>>>(
-        x, maps, int(n.x), int(n.y), int(n.z), int(p.x), int(p.y), int(p.z), y, mask);
+    maxpool_fwd_k<<<vgrid(m.y, m.x, maps), vblock(), 0, st>>>(x, int(n.x), int(n.y), int(n.z), int(p.x), int(p.y),
+                                                             int(p.z), y, mask);
     launch_check("maxpool_fwd");
 }
 
 void maxpool_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
                  dims3 p, float* dx) {
-    const int64_t nvol = m.vol() * p.vol();
-    maxpool_bwd_k<<<grid2(nvol, maps), kThreads, 0, st>>>(
-        g, mask, maps, int(m.x), int(m.y), int(m.z), int(p.x), int(p.y), int(p.z), dx);
+    maxpool_bwd_k<<<vgrid(m.y * p.y, m.x * p.x, maps), vblock(), 0, st>>>(g, mask, int(m.x), int(m.y), int(m.z),
+                                                                         int(p.x), int(p.y), int(p.z), dx);
     launch_check("maxpool_bwd");
 }
 

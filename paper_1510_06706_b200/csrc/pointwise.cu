@@ -32,23 +32,29 @@ __global__ void transfer_fwd_k(const float* __restrict__ x, int64_t f, int64_t v
     y[i] = act_value(kinds[map], x[i] + b);
 }
 
-// One block-row per (map, chunk): g * phi'(.) written to gx, per-block
-// partial of the bias gradient written to part[map * chunks + chunk].
-__global__ void transfer_bwd_k(const float* __restrict__ g, const float* __restrict__ xy,
-                               int from_output, int64_t B, int64_t f, int64_t vox,
-                               const int32_t* __restrict__ kinds,
-                               const float* __restrict__ bias, float* gx, float* part) {
-    const int64_t map = blockIdx.y;
+// grid (voxel chunks, map, patch): g * phi'(.) written to gx, each thread 4
+// voxels strided by the block; per-block partial of the bias gradient written
+// to part[(map * B + patch) * chunks + chunk].
+constexpr int TB_E = 4;
+__global__ void __launch_bounds__(kThreads) transfer_bwd_k(const float* __restrict__ g, const float* __restrict__ xy,
+                                                           int from_output, int64_t B, int64_t f, int64_t vox,
+                                                           const int32_t* __restrict__ kinds,
+                                                           const float* __restrict__ bias, float* gx, float* part) {
+    const int64_t map = blockIdx.y, bb = blockIdx.z;
     const int kind = kinds[map];
     const float b = bias ? bias[map] : 0.f;
+    const int64_t off = (bb * f + map) * vox;
     float acc = 0.f;
-    for (int64_t bb = 0; bb < B; ++bb) {  // no per-element 64-bit division
-        const int64_t off = (bb * f + map) * vox;
-        for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < vox; v += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v0 = int64_t(blockIdx.x) * (kThreads * TB_E) + threadIdx.x;
+#pragma unroll
+    for (int e = 0; e < TB_E; ++e) {
+        const int64_t v = v0 + e * kThreads;
+        if (v < vox) {
             const int64_t i = off + v;
-            const float d = from_output ? act_deriv_out(kind, xy[i]) : act_deriv_in(kind, xy[i] + b);
-            const float r = g[i] * d;
-            gx[i] = r;
+            const float yv = __ldcs(xy + i), gv = __ldcs(g + i);
+            const float d = from_output ? act_deriv_out(kind, yv) : act_deriv_in(kind, yv + b);
+            const float r = gv * d;
+            __stcs(gx + i, r);
             acc += r;
         }
     }
@@ -60,7 +66,7 @@ __global__ void transfer_bwd_k(const float* __restrict__ g, const float* __restr
         if (threadIdx.x < 32) {
             float t = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.f;
             for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (threadIdx.x == 0) part[map * gridDim.x + blockIdx.x] = t;
+            if (threadIdx.x == 0) part[(map * B + bb) * gridDim.x + blockIdx.x] = t;
         }
     }
 }
@@ -155,17 +161,14 @@ void transfer_fwd(cudaStream_t st, const float* x, int64_t B, int64_t f, int64_t
 void transfer_bwd(cudaStream_t st, const float* g, const float* xy, bool from_output, int64_t B,
                   int64_t f, int64_t vox, const int32_t* kinds_dev, const float* bias,
                   float* gx, float* dbias, scratch& ws) {
-    int64_t chunks = ceil_div(vox, kThreads * 2);
-    const int64_t cap = (148 * 8 + f - 1) / f;
-    if (chunks > cap) chunks = cap;
-    if (chunks < 1) chunks = 1;
-    float* part = dbias ? static_cast<float*>(ws.get(sizeof(float) * size_t(f * chunks)))
-                        : nullptr;
-    transfer_bwd_k<<<dim3(unsigned(chunks), unsigned(f)), kThreads, 0, st>>>(
+    const int64_t chunks = ceil_div(vox, int64_t(kThreads) * TB_E);
+    require(f < 65536 && B < 65536, "transfer_bwd: grid exceeds 65535 maps / patches");
+    float* part = dbias ? static_cast<float*>(ws.get(sizeof(float) * size_t(f * B * chunks))) : nullptr;
+    transfer_bwd_k<<<dim3(unsigned(chunks), unsigned(f), unsigned(B)), kThreads, 0, st>>>(
         g, xy, from_output ? 1 : 0, B, f, vox, kinds_dev, bias, gx, part);
     launch_check("transfer_bwd");
     if (dbias) {
-        reduce_rows_k<<<unsigned(f), 128, 0, st>>>(part, f, chunks, dbias);
+        reduce_rows_k<<<unsigned(f), 128, 0, st>>>(part, f, B * chunks, dbias);
         launch_check("transfer_bwd_reduce");
     }
 }
