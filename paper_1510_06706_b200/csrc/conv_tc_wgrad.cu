@@ -41,6 +41,7 @@ constexpr int THREADS = 384;
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CHUNK_KB = 8;
 constexpr int TP = 33;  // transpose tile pitch (floats)
+constexpr int kPrefetch = 16;  // g tiles prefetched into L2 this many K-blocks ahead
 
 struct wg_params {
     int f_in, f_out, T, nt;
@@ -228,6 +229,19 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 // so a box is one 16 KB DRAM stream instead of nt scattered 128 B rows
                 const int vcol = 0;
                 const int row = int(((pb * p.ntiles + blockIdx.y) * p.kb_per_patch + vkb) * p.nt) + int(rank) * rows_per;
+                if (kb + kPrefetch < kblocks && (kb % 2) == int(rank) && elect_one()) {
+                    // pull the tile kPrefetch K-blocks ahead from HBM into L2 (the
+                    // cluster ranks alternate), so the TMA below finds it there
+                    int64_t ppb = pb;
+                    int pvkb = vkb + kPrefetch;
+                    while (pvkb >= p.kb_per_patch) pvkb -= int(p.kb_per_patch), ++ppb;
+                    const int prow = int(((ppb * p.ntiles + blockIdx.y) * p.kb_per_patch + pvkb) * p.nt);
+                    for (int h = 0; h < C; ++h) {  // the map's box is one rank's part of the tile
+                        tma_prefetch_2d(&tm_hi, 0, prow + h * rows_per);
+                        tma_prefetch_2d(&tm_lo, 0, prow + h * rows_per);
+                    }
+                }
+                __syncwarp();
                 mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t b_hi = base + uint32_t(s) * stage_bytes;
                 if constexpr (PAIR) {

@@ -205,6 +205,13 @@ __device__ __forceinline__ void mma_commit_mc_w(uint32_t bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+// L2 prefetch of a TMA box (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 // converged-warp TMA issue (one elected lane arms the barrier and loads)
 __device__ __forceinline__ void tma_pair_w(uint32_t bar, uint32_t bytes, uint32_t dst0, const CUtensorMap* m0,
                                            uint32_t dst1, const CUtensorMap* m1, int c0, int c1) {
