@@ -36,6 +36,9 @@
 //   warp 9    : TMEM allocator + single-thread tcgen05.mma issuer
 #include <cuda.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "ops.hpp"
 #include "tc_common.cuh"
 
@@ -67,6 +70,11 @@ struct tc_params {
     // tap-row skipping: K group = one (wx, wy) kernel row, gsize = f_src*kz
     int gsize, ky, dsx, dsy;
     int vx0, vx1, vy0, vy1;  // source region that can be nonzero (inclusive)
+    // box tiles (dgrad): a tile is a bxs x bys x bzs box of output voxels and
+    // K is tap-major (k = tap * f + c), so whole taps are skipped along all
+    // three axes; box == 0: tiles are 128 consecutive voxels, K (wx, wy)-outer
+    int box, bxs, bys, bzs, tnx, tny, tnz;
+    int kz, dsz, vz0, vz1;
 };
 
 template <int NTMAX>
@@ -113,14 +121,22 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     if (warp == 10) {
         // active K-blocks of this tile: a (wx, wy) tap row is live iff the
         // tile's bounding box shifted by s*w meets the nonzero source region
-        const int64_t va = m0, vb = min(m0 + BM, p.rows) - 1;
-        const int64_t ba = va / p.vox_out, bb = vb / p.vox_out;
-        int x0 = 0, x1 = p.ox - 1, y0 = 0, y1 = p.oy - 1;
-        if (ba == bb) {
-            const int64_t ra = va - ba * p.vox_out, rb = vb - bb * p.vox_out;
-            const int64_t plane = int64_t(p.oy) * p.oz;
-            x0 = int(ra / plane), x1 = int(rb / plane);
-            if (x0 == x1) y0 = int((ra / p.oz) % p.oy), y1 = int((rb / p.oz) % p.oy);
+        int x0 = 0, x1 = p.ox - 1, y0 = 0, y1 = p.oy - 1, z0 = 0, z1 = p.oz - 1;
+        if (p.box) {
+            const int t = blockIdx.x % (p.tnx * p.tny * p.tnz);
+            const int ix = t / (p.tny * p.tnz), iy = (t / p.tnz) % p.tny, iz = t % p.tnz;
+            x0 = ix * p.bxs, x1 = min(x0 + p.bxs, p.ox) - 1;
+            y0 = iy * p.bys, y1 = min(y0 + p.bys, p.oy) - 1;
+            z0 = iz * p.bzs, z1 = min(z0 + p.bzs, p.oz) - 1;
+        } else {
+            const int64_t va = m0, vb = min(m0 + BM, p.rows) - 1;
+            const int64_t ba = va / p.vox_out, bb = vb / p.vox_out;
+            if (ba == bb) {
+                const int64_t ra = va - ba * p.vox_out, rb = vb - bb * p.vox_out;
+                const int64_t plane = int64_t(p.oy) * p.oz;
+                x0 = int(ra / plane), x1 = int(rb / plane);
+                if (x0 == x1) y0 = int((ra / p.oz) % p.oy), y1 = int((rb / p.oz) % p.oy);
+            }
         }
         int cnt = 0;
         for (int kb0 = 0; kb0 < p.kblocks; kb0 += 32) {
@@ -129,9 +145,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
             if (kb < p.kblocks) {
                 const int g0 = (kb * BK) / p.gsize, g1 = (min(kb * BK + BK, p.K) - 1) / p.gsize;
                 for (int g = g0; g <= g1 && !act_kb; ++g) {
-                    const int wx = g / p.ky, wy = g - (g / p.ky) * p.ky;
+                    // group g: a (wx, wy) tap row, or (box tiles) a single tap (wx, wy, wz)
+                    int wz = 0, gr = g;
+                    if (p.box) wz = g % p.kz, gr = g / p.kz;
+                    const int wx = gr / p.ky, wy = gr - (gr / p.ky) * p.ky;
                     act_kb = x0 + p.dsx * wx <= p.vx1 && x1 + p.dsx * wx >= p.vx0 && y0 + p.dsy * wy <= p.vy1 &&
-                             y1 + p.dsy * wy >= p.vy0;
+                             y1 + p.dsy * wy >= p.vy0 && z0 + p.dsz * wz <= p.vz1 && z1 + p.dsz * wz >= p.vz0;
                 }
             }
             const uint32_t m = __ballot_sync(0xffffffffu, act_kb);
@@ -158,17 +177,31 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
         chunk_drainer<NH> D;
         D.init(accf0, acce0, tmem + lane_base + uint32_t(col0), p.nbuf, p.bstride, ncols, nchunks);
-        const int64_t v = m0 + r;
-        const bool vok = v < p.rows;
-        const float* sp = src;
-        if (vok) {
-            const int64_t b = v / p.vox_out;
-            const int64_t rem = v - b * p.vox_out;
-            const int tx = int(rem / (int64_t(p.oy) * p.oz));
-            const int ty = int((rem / p.oz) % p.oy);
-            const int tz = int(rem % p.oz);
-            sp = src + b * int64_t(p.f_src) * p.src_vol + (int64_t(tx) * p.sy + ty) * p.sz + tz;
+        // this row's output voxel: patch vb, in-volume index vin
+        bool vok;
+        int64_t vb, vin;
+        int tx, ty, tz;
+        if (p.box) {
+            const int per = p.tnx * p.tny * p.tnz;
+            vb = blockIdx.x / per;
+            const int t = blockIdx.x - int(vb) * per;
+            const int ix = t / (p.tny * p.tnz), iy = (t / p.tnz) % p.tny, iz = t % p.tnz;
+            tx = ix * p.bxs + r / (p.bys * p.bzs);
+            ty = iy * p.bys + (r / p.bzs) % p.bys;
+            tz = iz * p.bzs + r % p.bzs;
+            vok = tx < p.ox && ty < p.oy && tz < p.oz;
+            vin = (int64_t(tx) * p.oy + ty) * p.oz + tz;
+        } else {
+            const int64_t v = m0 + r;
+            vok = v < p.rows;
+            vb = vok ? v / p.vox_out : 0;
+            vin = v - vb * p.vox_out;
+            tx = int(vin / (int64_t(p.oy) * p.oz));
+            ty = int((vin / p.oz) % p.oy);
+            tz = int(vin % p.oz);
         }
+        const float* sp = src;
+        if (vok) sp = src + vb * int64_t(p.f_src) * p.src_vol + (int64_t(tx) * p.sy + ty) * p.sz + tz;
         // this group's A buffers: half, half + 2, ... (< na); (a, use parity) tracked incrementally
         int a = half;
         uint32_t u = 0;
@@ -208,9 +241,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         // ---------------- remaining drains + epilogue (this warp's columns) ----------------
         D.finish();
         if (vok) {
-            const int64_t bb = v / p.vox_out;
-            const int64_t vin = v - bb * p.vox_out;
-            float* op = out + bb * int64_t(p.n_real) * p.vox_out + vin;
+            float* op = out + vb * int64_t(p.n_real) * p.vox_out + vin;
 #pragma unroll
             for (int q = 0; q < NH; ++q) {
                 const int n = n0 + col0 + q;
@@ -282,8 +313,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     }
 }
 
-// K index -> (source channel c, tap t) for the (wx, wy)-outer order
-__device__ __forceinline__ void k_decode(int k, int f, int ky, int kz, int& c, int& t) {
+// K index -> (source channel c, tap t): order 0 = (wx, wy)-outer with (c, wz)
+// inner (k = ((wx*ky + wy)*f + c)*kz + wz), order 1 = tap-major (k = t*f + c)
+__device__ __forceinline__ void k_decode(int k, int f, int ky, int kz, int order, int& c, int& t) {
+    if (order) {
+        t = k / f;
+        c = k - t * f;
+        return;
+    }
     const int gsize = f * kz;
     const int g = k / gsize, rem = k - g * gsize;
     c = rem / kz;
@@ -296,14 +333,15 @@ __device__ __forceinline__ void k_decode(int k, int f, int ky, int kz, int& c, i
 //   mode 0 (fwd)  : B[n][(c, t)] = W[n][c][t]
 //   mode 1 (dgrad): B[n][(o, t)] = W[o][n][T-1-t]   (transposed, reflected)
 __global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_src, int f_in, int T, int ky, int kz,
-                                int K, int npad, int kpad, int mode, float* __restrict__ hi, float* __restrict__ lo) {
+                                int K, int npad, int kpad, int mode, int order, float* __restrict__ hi,
+                                float* __restrict__ lo) {
     const int64_t total = int64_t(npad) * kpad;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int n = int(i / kpad), k = int(i - int64_t(n) * kpad);
         float v = 0.f;
         if (n < n_real && k < K) {
             int c, t;
-            k_decode(k, f_src, ky, kz, c, t);
+            k_decode(k, f_src, ky, kz, order, c, t);
             if (mode == 0) v = w[(int64_t(n) * f_src + c) * T + t];
             else v = w[(int64_t(c) * f_in + n) * T + (T - 1 - t)];
         }
@@ -315,13 +353,13 @@ __global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_s
 
 // im2col offsets: koff[k] = c*src_vol + linear(s*w) in source dims; padded
 // k -> 0 (their weights are zero).
-__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int ky, int kz, int sx, int sy, int sz,
-                       int64_t src_vol, int src_y, int src_z) {
+__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int ky, int kz, int order, int sx, int sy,
+                       int sz, int64_t src_vol, int src_y, int src_z) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
         int e = 0;
         if (k < K) {
             int c, t;
-            k_decode(k, f_src, ky, kz, c, t);
+            k_decode(k, f_src, ky, kz, order, c, t);
             const int wx = t / (ky * kz), wy = (t / kz) % ky, wz = t % kz;
             e = int(int64_t(c) * src_vol + (int64_t(sx * wx) * src_y + sy * wy) * src_z + sz * wz);
         }
@@ -375,6 +413,41 @@ void launch_kernel(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& m
     launch_check(what);
 }
 
+// Rows x taps computed along one axis when output tiles of extent L skip the
+// taps whose shifted tile misses the nonzero source interval [v0, v0 + vn).
+int64_t axis_work(int64_t n_out, int64_t L, int64_t s, int64_t k, int64_t v0, int64_t vn) {
+    int64_t tot = 0;
+    for (int64_t t0 = 0; t0 < n_out; t0 += L) {
+        const int64_t t1 = std::min(t0 + L, n_out) - 1;
+        int64_t act = 0;
+        for (int64_t w = 0; w < k; ++w) act += (t0 + s * w <= v0 + vn - 1 && t1 + s * w >= v0) ? 1 : 0;
+        tot += act * L;
+    }
+    return tot;
+}
+
+struct box_choice {
+    int box = 0, bx = 0, by = 0, bz = 0;
+};
+
+// Box tiles (with tap-major K) for a convolution whose source has a zero halo,
+// when they cut the computed MMA work by >= 8% against the flattened tiles
+// (whose bounding box is ~1 x 2 x full-z voxels).
+box_choice choose_box(dims3 od, dims3 k, dims3 s, dims3 v0, dims3 vn) {
+    box_choice best;
+    const double flat = double(axis_work(od.x, 1, s.x, k.x, v0.x, vn.x)) *
+                        double(axis_work(od.y, 2, s.y, k.y, v0.y, vn.y)) * double(od.z * k.z);
+    double bw = 0.92 * flat;
+    static const int shapes[][3] = {{4, 4, 8}, {2, 8, 8}, {2, 4, 16}, {1, 8, 16}, {4, 8, 4}, {8, 4, 4}, {1, 4, 32}};
+    for (const auto& sh : shapes) {
+        const double w = double(axis_work(od.x, sh[0], s.x, k.x, v0.x, vn.x)) *
+                         double(axis_work(od.y, sh[1], s.y, k.y, v0.y, vn.y)) *
+                         double(axis_work(od.z, sh[2], s.z, k.z, v0.z, vn.z));
+        if (w < bw) bw = w, best.box = 1, best.bx = sh[0], best.by = sh[1], best.bz = sh[2];
+    }
+    return best;
+}
+
 // One valid convolution src[B][f_src][sd] -> out[B][n_real][sd - s(k-1)] on
 // the tensor cores. wmode selects how the B panel is built from w; only the
 // source box [v0, v0 + vn) can be nonzero (the rest is zero halo).
@@ -390,6 +463,13 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     const int npad = ntiles * nt;
     const dims3 od{sd.x - s.x * (k.x - 1), sd.y - s.y * (k.y - 1), sd.z - s.z * (k.z - 1)};
     require(kpad / BK < 65536, "conv_tc: too many K-blocks");
+    box_choice bc;
+    const bool halo = v0.x > 0 || v0.y > 0 || v0.z > 0;
+    // measured on c5's s = 4 layers: box tiles cut the MMAs by 15-25% but the
+    // tap-major gathers lose the L1 reuse of the (wx, wy)-outer order and the
+    // pass gets ~4% slower, so box tiles are opt-in (ZNN_CONV_BOX=1)
+    if (halo && std::getenv("ZNN_CONV_BOX")) bc = choose_box(od, k, s, v0, vn);
+    const int order = bc.box;  // box tiles skip single taps: tap-major K
 
     const size_t panel = size_t(npad) * size_t(kpad);
     float* hi = reinterpret_cast<float*>(wsp);
@@ -399,9 +479,9 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     int64_t blocks = ceil_div(int64_t(panel), 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
     split_weights_k<<<unsigned(blocks), 256, 0, st>>>(w, n_real, f_src, f_in_w, T, int(k.y), int(k.z), K, npad, kpad,
-                                                      wmode, hi, lo);
+                                                      wmode, order, hi, lo);
     launch_check("conv_tc_split_weights");
-    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, f_src, int(k.y), int(k.z), int(s.x),
+    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, f_src, int(k.y), int(k.z), order, int(s.x),
                                                            int(s.y), int(s.z), sd.vol(), int(sd.y), int(sd.z));
     launch_check("conv_tc_koff");
 
@@ -422,17 +502,23 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     p.ox = int(od.x), p.oy = int(od.y), p.oz = int(od.z);
     p.sx = int(sd.x), p.sy = int(sd.y), p.sz = int(sd.z);
     p.src_vol = sd.vol();
-    p.gsize = f_src * int(k.z);
-    p.ky = int(k.y);
-    p.dsx = int(s.x), p.dsy = int(s.y);
+    p.gsize = order ? f_src : f_src * int(k.z);
+    p.ky = int(k.y), p.kz = int(k.z);
+    p.dsx = int(s.x), p.dsy = int(s.y), p.dsz = int(s.z);
     p.vx0 = int(v0.x), p.vx1 = int(v0.x + vn.x - 1), p.vy0 = int(v0.y), p.vy1 = int(v0.y + vn.y - 1);
+    p.vz0 = int(v0.z), p.vz1 = int(v0.z + vn.z - 1);
+    p.box = bc.box, p.bxs = bc.bx, p.bys = bc.by, p.bzs = bc.bz;
+    p.tnx = bc.box ? int(ceil_div(od.x, bc.bx)) : 0;
+    p.tny = bc.box ? int(ceil_div(od.y, bc.by)) : 0;
+    p.tnz = bc.box ? int(ceil_div(od.z, bc.bz)) : 0;
     const int stage = 2 * nt * 128;
     const size_t fixed = 1024 + 8 * size_t(16) + 16 + 2 * size_t(p.kblocks) + 64;
     p.stages = int((size_t(220) * 1024 - fixed) / size_t(stage + 16));
     if (p.stages > 8) p.stages = 8;
     require(p.stages >= 2, "conv_tc: K too long for the shared-memory budget");
     const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
-    const dim3 grid{unsigned(ceil_div(p.rows, BM)), unsigned(ntiles), 1u};
+    const int64_t mtiles = bc.box ? Bn * p.tnx * p.tny * p.tnz : ceil_div(p.rows, BM);
+    const dim3 grid{unsigned(mtiles), unsigned(ntiles), 1u};
     if (ntmax == 32) launch_kernel<32>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
     else if (ntmax == 64) launch_kernel<64>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
     else launch_kernel<128>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
