@@ -87,7 +87,8 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     const int kblocks = int(q1 - q0);
     const int nchunks = (kblocks + CHUNK_KB - 1) / CHUNK_KB;
 
-    if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : -1;
+    // rows past f_in * T read a valid dummy offset: their D rows are never stored
+    if (threadIdx.x < BM) rowoff[threadIdx.x] = (r0 + threadIdx.x < p.mrows) ? rowoff_g[r0 + threadIdx.x] : 0;
     if (threadIdx.x == 0) {
         // PAIR: the leader's full / A-written / drained barriers collect both
         // CTAs (elected remote arrives); every CTA's empty / A-free /
@@ -136,6 +137,9 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         uint32_t u = 0;
         int64_t pb = (q0 + grp) / p.kb_per_patch;  // patch / K-block of the next gather, tracked incrementally
         int vkb = int(q0 + grp - pb * p.kb_per_patch);
+        int ro[32];  // this warp's 32 row offsets (tap window starts), kept in registers
+#pragma unroll
+        for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
         auto gather = [&](float (&av)[32]) {
             const int v = vkb * BK + lane;
             const int64_t pcur = pb;
@@ -149,10 +153,12 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 const int vz = r2 - vy * p.mz;
                 xp = x + pcur * int64_t(p.f_in) * p.nvol + (vx * p.ny + vy) * p.nz + vz;
             }
+            if (vok) {  // voxels past the patch (its last K-block) must contribute zeros
 #pragma unroll
-            for (int t = 0; t < 32; ++t) {
-                const int ro = rowoff[wq * 32 + t];
-                av[t] = (vok && ro >= 0) ? __ldg(xp + ro) : 0.f;
+                for (int t = 0; t < 32; ++t) av[t] = __ldg(xp + ro[t]);
+            } else {
+#pragma unroll
+                for (int t = 0; t < 32; ++t) av[t] = 0.f;
             }
         };
         auto put = [&](float (&av)[32]) {
