@@ -74,7 +74,7 @@ struct tc_params {
     // K is tap-major (k = tap * f + c), so whole taps are skipped along all
     // three axes; box == 0: tiles are 128 consecutive voxels, K (wx, wy)-outer
     int box, bxs, bys, bzs, tnx, tny, tnz;
-    int kz, dsz, vz0, vz1;
+    int kz, dsz, vz0, vz1, taps;
 };
 
 template <int NTMAX>
@@ -147,7 +147,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                 for (int g = g0; g <= g1 && !act_kb; ++g) {
                     // group g: a (wx, wy) tap row, or (box tiles) a single tap (wx, wy, wz)
                     int wz = 0, gr = g;
-                    if (p.box) wz = g % p.kz, gr = g / p.kz;
+                    if (p.box) {
+                        const int t = g % p.taps;  // group = (channel block, tap)
+                        wz = t % p.kz, gr = t / p.kz;
+                    }
                     const int wx = gr / p.ky, wy = gr - (gr / p.ky) * p.ky;
                     act_kb = x0 + p.dsx * wx <= p.vx1 && x1 + p.dsx * wx >= p.vx0 && y0 + p.dsy * wy <= p.vy1 &&
                              y1 + p.dsy * wy >= p.vy0 && z0 + p.dsz * wz <= p.vz1 && z1 + p.dsz * wz >= p.vz0;
@@ -314,11 +317,15 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
 }
 
 // K index -> (source channel c, tap t): order 0 = (wx, wy)-outer with (c, wz)
-// inner (k = ((wx*ky + wy)*f + c)*kz + wz), order 1 = tap-major (k = t*f + c)
-__device__ __forceinline__ void k_decode(int k, int f, int ky, int kz, int order, int& c, int& t) {
+// inner (k = ((wx*ky + wy)*f + c)*kz + wz); order CB > 0 = channel blocks of
+// CB, taps, channels in the block (k = (cb*T + t)*CB + ci): a K-block covers
+// one or two taps of one channel block, and consecutive K-blocks walk the taps
+// of the same channels (their gathers overlap in L1)
+__device__ __forceinline__ void k_decode(int k, int f, int T, int kz, int order, int& c, int& t) {
     if (order) {
-        t = k / f;
-        c = k - t * f;
+        const int cb = k / (T * order), rem = k - cb * (T * order);
+        t = rem / order;
+        c = cb * order + (rem - t * order);
         return;
     }
     const int gsize = f * kz;
@@ -326,7 +333,6 @@ __device__ __forceinline__ void k_decode(int k, int f, int ky, int kz, int order
     c = rem / kz;
     const int wz = rem - c * kz;
     t = g * kz + wz;  // g = wx*ky + wy, so t = (wx*ky + wy)*kz + wz
-    (void)ky;
 }
 
 // Weight panels for the B operand, split hi/lo, zero padded to [npad][kpad].
@@ -341,7 +347,7 @@ __global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_s
         float v = 0.f;
         if (n < n_real && k < K) {
             int c, t;
-            k_decode(k, f_src, ky, kz, order, c, t);
+            k_decode(k, f_src, T, kz, order, c, t);
             if (mode == 0) v = w[(int64_t(n) * f_src + c) * T + t];
             else v = w[(int64_t(c) * f_in + n) * T + (T - 1 - t)];
         }
@@ -353,13 +359,13 @@ __global__ void split_weights_k(const float* __restrict__ w, int n_real, int f_s
 
 // im2col offsets: koff[k] = c*src_vol + linear(s*w) in source dims; padded
 // k -> 0 (their weights are zero).
-__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int ky, int kz, int order, int sx, int sy,
-                       int sz, int64_t src_vol, int src_y, int src_z) {
+__global__ void koff_k(int* __restrict__ tab, int K, int kpad, int f_src, int kx, int ky, int kz, int order, int sx,
+                       int sy, int sz, int64_t src_vol, int src_y, int src_z) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < kpad; k += gridDim.x * blockDim.x) {
         int e = 0;
         if (k < K) {
             int c, t;
-            k_decode(k, f_src, ky, kz, order, c, t);
+            k_decode(k, f_src, ky * kz * kx, kz, order, c, t);
             const int wx = t / (ky * kz), wy = (t / kz) % ky, wz = t % kz;
             e = int(int64_t(c) * src_vol + (int64_t(sx * wx) * src_y + sy * wy) * src_z + sz * wz);
         }
@@ -469,7 +475,17 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     // tap-major gathers lose the L1 reuse of the (wx, wy)-outer order and the
     // pass gets ~4% slower, so box tiles are opt-in (ZNN_CONV_BOX=1)
     if (halo && std::getenv("ZNN_CONV_BOX")) bc = choose_box(od, k, s, v0, vn);
-    const int order = bc.box;  // box tiles skip single taps: tap-major K
+    // box tiles skip single taps: channel-blocked tap-major K (block = the
+    // largest divisor of f_src <= 32)
+    int order = 0;
+    if (bc.box) {
+        order = 1;
+        for (int cb = std::min(f_src, 32); cb >= 1; --cb)
+            if (f_src % cb == 0) {
+                order = cb;
+                break;
+            }
+    }
 
     const size_t panel = size_t(npad) * size_t(kpad);
     float* hi = reinterpret_cast<float*>(wsp);
@@ -481,7 +497,8 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     split_weights_k<<<unsigned(blocks), 256, 0, st>>>(w, n_real, f_src, f_in_w, T, int(k.y), int(k.z), K, npad, kpad,
                                                       wmode, order, hi, lo);
     launch_check("conv_tc_split_weights");
-    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, f_src, int(k.y), int(k.z), order, int(s.x),
+    koff_k<<<unsigned(ceil_div(kpad, 256)), 256, 0, st>>>(tab, K, kpad, f_src, int(k.x), int(k.y), int(k.z), order,
+                                                           int(s.x),
                                                            int(s.y), int(s.z), sd.vol(), int(sd.y), int(sd.z));
     launch_check("conv_tc_koff");
 
@@ -502,7 +519,8 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     p.ox = int(od.x), p.oy = int(od.y), p.oz = int(od.z);
     p.sx = int(sd.x), p.sy = int(sd.y), p.sz = int(sd.z);
     p.src_vol = sd.vol();
-    p.gsize = order ? f_src : f_src * int(k.z);
+    p.gsize = order ? order : f_src * int(k.z);
+    p.taps = T;
     p.ky = int(k.y), p.kz = int(k.z);
     p.dsx = int(s.x), p.dsy = int(s.y), p.dsz = int(s.z);
     p.vx0 = int(v0.x), p.vx1 = int(v0.x + vn.x - 1), p.vy0 = int(v0.y), p.vy1 = int(v0.y + vn.y - 1);
