@@ -379,6 +379,153 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_k(const float2* __restrict
     }
 }
 
+// ---- persistent, double-buffered xy passes (square planes, PX == PY > 1) ----
+// A CTA walks planes q, q + G, ...; the next plane streams into the second
+// shared buffer with cp.async while the current one is transformed, so HBM
+// traffic overlaps the shared-memory FFT work. Rows have an even pitch so
+// 16-byte copies stay aligned.
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16p(void* smem, const void* gmem) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int P>
+__global__ void __launch_bounds__(THREADS) fft_xy_inv_pipe_k(const float2* __restrict__ spec, float2* __restrict__ out,
+                                                              int64_t planes, int x_step, int xc, int y_step, int yc) {
+    constexpr int PP = P + 2;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;                       // P
+    float2* xbuf = tw + P;                 // LINES x P
+    float2* plb0 = xbuf + LINES * P;       // [P][PP]
+    float2* plb1 = plb0 + P * PP;
+    fill_twiddles<P>(tw);
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * P;
+    auto issue = [&](int64_t qq, float2* dst) {
+        if (qq < planes) {
+            const float2* g = spec + qq * (int64_t(P) * P);
+            for (int idx = threadIdx.x; idx < P * P / 2; idx += THREADS) {
+                const int e = 2 * idx, x = e / P, y = e - (e / P) * P;
+                cp_async16p(dst + x * PP + y, g + e);
+            }
+        }
+        cp_commit();
+    };
+    int64_t q = blockIdx.x;
+    issue(q, plb0);
+    int buf = 0;
+    for (; q < planes; q += gridDim.x) {
+        float2* pl = buf ? plb1 : plb0;
+        issue(q + gridDim.x, buf ? plb0 : plb1);
+        cp_wait<1>();
+        __syncthreads();
+        // column inverses; keep rows x_step * i (i < xc), compacted into rows i
+        for (int c0 = 0; c0 < P; c0 += LINES) {
+            const int y = c0 + l;
+            const bool ok = y < P;  // planes narrower than LINES
+            float2 v[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? pl[(t + R1 * n2) * PP + y] : make_float2(0.f, 0.f);
+            line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+                const int i = k / x_step;
+                if (ok && i * x_step == k && i < xc) pl[i * PP + y] = val;
+            });
+        }
+        __syncthreads();
+        float2* o = out + q * (int64_t(xc) * yc);
+        for (int r0 = 0; r0 < xc; r0 += LINES) {
+            const int i = r0 + l;
+            const bool ok = i < xc;
+            float2 v[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? pl[i * PP + t + R1 * n2] : make_float2(0.f, 0.f);
+            line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+                const int j = k / y_step;
+                if (ok && j * y_step == k && j < yc) o[i * yc + j] = val;
+            });
+        }
+        __syncthreads();  // this buffer is refilled by the next iteration's prefetch
+        buf ^= 1;
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(THREADS) fft_xy_fwd_pipe_k(float2* __restrict__ spec, int64_t planes, int nx, int ny) {
+    constexpr int PP = P + 2;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* plb0 = xbuf + LINES * P;
+    float2* plb1 = plb0 + P * PP;
+    fill_twiddles<P>(tw);
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * P;
+    auto issue = [&](int64_t qq, float2* dst) {  // the valid nx x ny region written by the z pass
+        if (qq < planes) {
+            const float2* g = spec + qq * (int64_t(P) * P);
+            for (int idx = threadIdx.x; idx < nx * ny; idx += THREADS) {
+                const int x = idx / ny, y = idx - (idx / ny) * ny;
+                cp_async8(dst + x * PP + y, g + x * P + y);
+            }
+        }
+        cp_commit();
+    };
+    int64_t q = blockIdx.x;
+    issue(q, plb0);
+    int buf = 0;
+    for (; q < planes; q += gridDim.x) {
+        float2* pl = buf ? plb1 : plb0;
+        issue(q + gridDim.x, buf ? plb0 : plb1);
+        cp_wait<1>();
+        __syncthreads();
+        for (int r0 = 0; r0 < nx; r0 += LINES) {  // rows (y transforms) of the valid rows
+            const int x = r0 + l;
+            const bool ok = x < nx;
+            float2 v[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) {
+                const int y = t + R1 * n2;
+                v[n2] = (ok && t < R1 && y < ny) ? pl[x * PP + y] : make_float2(0.f, 0.f);
+            }
+            line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+                if (ok) pl[x * PP + k] = val;
+            });
+        }
+        __syncthreads();
+        for (int c0 = 0; c0 < P; c0 += LINES) {  // columns (x transforms); rows >= nx are zero
+            const int y = c0 + l;
+            const bool ok = y < P;  // planes narrower than LINES
+            float2 v[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) {
+                const int x = t + R1 * n2;
+                v[n2] = (ok && t < R1 && x < nx) ? pl[x * PP + y] : make_float2(0.f, 0.f);
+            }
+            line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+                if (ok) pl[k * PP + y] = val;
+            });
+        }
+        __syncthreads();
+        float4* g4 = reinterpret_cast<float4*>(spec + q * (int64_t(P) * P));
+        for (int idx = threadIdx.x; idx < P * P / 2; idx += THREADS) {
+            const int e = 2 * idx, x = e / P, y = e - (e / P) * P;
+            const float2 a = pl[x * PP + y], b = pl[x * PP + y + 1];
+            __stcs(g4 + idx, make_float4(a.x, a.y, b.x, b.y));
+        }
+        __syncthreads();  // this buffer is refilled by the next iteration's prefetch
+        buf ^= 1;
+    }
+}
+
 struct zinv_args {
     int xc, yc;                        // kept block per z-bin plane (compact input)
     int z_step, z_cnt;                 // kept z voxels (selection starts at 0)
@@ -704,6 +851,19 @@ void dispatch_pad(int P, F&& f) {
     }
 }
 
+// persistent double-buffered xy passes: twiddles + exchange buffers + 2 planes
+size_t smem_pipe(int P) {
+    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(P) + 2 * size_t(P) * size_t(P + 2));
+}
+// as many CTAs as fit on the 148 SMs at once (never more than planes)
+unsigned pipe_grid(int64_t planes, size_t smem) {
+    int64_t per_sm = int64_t(220 * 1024) / int64_t(smem + 1024);
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 8) per_sm = 8;
+    const int64_t g = 148 * per_sm;
+    return unsigned(planes < g ? planes : g);
+}
+
 template <typename K>
 void allow_smem(K* k, size_t bytes) {
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
@@ -742,10 +902,14 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         if (p.P.x == 1) {
             allow_smem(fft_xy_fwd_k<1, PY>, smem_xy(1, PY));
             fft_xy_fwd_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(spec, planes, int(n.x), int(n.y));
-        } else {
+        } else if (smem_pipe(PY) > size_t(220) * 1024) {  // two 128^2 planes do not fit: single buffer
             allow_smem(fft_xy_fwd_k<PY, PY>, smem_xy(PY, PY));
             fft_xy_fwd_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(spec, planes, int(n.x),
                                                                                       int(n.y));
+        } else {
+            const size_t sm = smem_pipe(PY);
+            allow_smem(fft_xy_fwd_pipe_k<PY>, sm);
+            fft_xy_fwd_pipe_k<PY><<<pipe_grid(planes, sm), THREADS, sm, st>>>(spec, planes, int(n.x), int(n.y));
         }
     });
     launch_check("fft_xy_fwd");
@@ -765,10 +929,15 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
             allow_smem(fft_xy_inv_k<1, PY>, smem_xy(1, PY));
             fft_xy_inv_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
-        } else {
+        } else if (smem_pipe(PY) > size_t(220) * 1024) {
             allow_smem(fft_xy_inv_k<PY, PY>, smem_xy(PY, PY));
             fft_xy_inv_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
+        } else {
+            const size_t sm = smem_pipe(PY);
+            allow_smem(fft_xy_inv_pipe_k<PY>, sm);
+            fft_xy_inv_pipe_k<PY><<<pipe_grid(planes, sm), THREADS, sm, st>>>(spec, cbuf, planes, int(step.x),
+                                                                              int(cnt.x), int(step.y), int(cnt.y));
         }
     });
     launch_check("fft_xy_inv");
