@@ -76,9 +76,29 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
     const float* gm = g + map * mv;
     const int32_t* mm = mask + map * mv;
     float* drow = dx + map * (int64_t(nx) * ny * nz) + (int64_t(ti) * ny + tj) * nz;
+    // rows whose every window origin t - s*w is inside the output volume skip
+    // the per-window bounds tests (the common case away from the faces)
+    const bool row_in = ti >= sx * (kx - 1) && ti < mx && tj >= sy * (ky - 1) && tj < my;
     for (int tl = threadIdx.x; tl < nz; tl += ZL) {
         const int tr = (ti * ny + tj) * nz + tl;
         float acc = 0.f;
+        if (KX && row_in && tl >= sz * (kz - 1) && tl < mz) {
+            const int o0 = (ti * my + tj) * mz + tl;
+#pragma unroll
+            for (int a = kx - 1; a >= 0; --a)
+#pragma unroll
+                for (int b = ky - 1; b >= 0; --b)
+#pragma unroll
+                    for (int c = kz - 1; c >= 0; --c) {
+                        // both loads issued together: no mask -> g dependent round trip
+                        const int o = o0 - (sx * a * my + sy * b) * mz - sz * c;
+                        const int mv = __ldg(mm + o);
+                        const float gv = __ldg(gm + o);
+                        acc += (mv == tr) ? gv : 0.f;
+                    }
+            __stcs(drow + tl, acc);
+            continue;
+        }
 #pragma unroll
         for (int a = kx - 1; a >= 0; --a) {
             const int oi = ti - sx * a;
