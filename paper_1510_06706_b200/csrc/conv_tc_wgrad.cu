@@ -37,7 +37,10 @@ namespace {
 
 using namespace znn_tc;
 
-constexpr int THREADS = 384;
+// NG producer warpgroups (one warp per TMEM lane quarter each) + one control
+// warpgroup (TMA, MMA, 2 idle): 32 * 4 * (NG + 1) threads
+template <int NG>
+constexpr int threads_for() { return 128 * (NG + 1); }
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CHUNK_KB = 8;
 constexpr int TP = 33;  // transpose tile pitch (floats)
@@ -54,8 +57,8 @@ struct wg_params {
     int ny, nz, my, mz;
 };
 
-template <int NTMAX, bool PAIR>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int NTMAX, bool PAIR, int NG>
+__global__ void __launch_bounds__(threads_for<NG>(), 1)
 wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
                 const float* __restrict__ x, const int* __restrict__ rowoff_g, float* __restrict__ ws,
                 wg_params p) {
@@ -77,7 +80,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     const uint32_t ae0 = af0 + 32u;
     uint8_t* tail = base_ptr + (bar_base - base) + 8u * uint32_t(2 * p.stages + 16);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tail);
-    float* tpose = reinterpret_cast<float*>(tail + 16);  // 8 warps x [32][TP]
+    float* tpose = reinterpret_cast<float*>(tail + 16);  // producer warps x [32][TP]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r0 = blockIdx.x * BM;    // first (i, w) row of this tile
@@ -99,13 +102,14 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8u * b, 1);
-            mbar_init(acce0 + 8u * b, PAIR ? 16u : 256u);
+            mbar_init(acce0 + 8u * b, PAIR ? 16u : 128u * NG);
             mbar_init(af0 + 8u * b, PAIR ? 8u : 128u);
             mbar_init(ae0 + 8u * b, 1);
         }
         fence_barrier_init();
     }
-    if (warp == 9) {
+    constexpr int PW = 4 * NG;  // producer warps; then TMA warp PW, MMA warp PW + 1
+    if (warp == PW + 1) {
         if constexpr (PAIR) tmem_alloc_pair(smem_u32(tmem_slot), TMEM_COLS);
         else tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
     }
@@ -117,11 +121,14 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
     const uint32_t rank = p.csize > 1 ? cluster_ctarank() : 0u;
 
-    if (warp < 8) setmaxnreg_inc<224>();
+    static_assert(NG == 2 || NG == 3, "2 or 3 producer warpgroups");
+    if (warp < PW) setmaxnreg_inc<NG == 2 ? 224 : 152>();
     else setmaxnreg_dec<56>();
-    if (warp < 8) {
-        constexpr int NH = NTMAX / 2;
-        const int grp = warp >> 2;  // 0: even K-blocks, 1: odd K-blocks
+    if (warp < PW) {
+        // group grp takes K-blocks grp, grp + NG, ...; the NG warps of one lane
+        // quarter split its accumulator columns (NH each)
+        constexpr int NH = ((NTMAX + NG - 1) / NG + 15) / 16 * 16;
+        const int grp = warp >> 2;
         const int wq = warp & 3;    // rows / TMEM lanes 32*wq .. 32*wq + 31
         const int col0 = grp * NH;
         const int ncols = max(0, min(NH, p.nt - col0));
@@ -137,13 +144,16 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         uint32_t u = 0;
         int64_t pb = (q0 + grp) / p.kb_per_patch;  // patch / K-block of the next gather, tracked incrementally
         int vkb = int(q0 + grp - pb * p.kb_per_patch);
-        int ro[32];  // this warp's 32 row offsets (tap window starts), kept in registers
+        int ro[32];  // this warp's 32 row offsets (tap window starts)
+        if constexpr (NG == 2) {
 #pragma unroll
-        for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
+            for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
+        }
+        auto rowo = [&](int t) { return NG == 2 ? ro[t] : rowoff[wq * 32 + t]; };
         auto gather = [&](float (&av)[32]) {
             const int v = vkb * BK + lane;
             const int64_t pcur = pb;
-            for (vkb += 2; vkb >= p.kb_per_patch; vkb -= int(p.kb_per_patch)) ++pb;
+            for (vkb += NG; vkb >= p.kb_per_patch; vkb -= int(p.kb_per_patch)) ++pb;
             const bool vok = v < mvol;
             const float* xp = x;
             if (vok) {
@@ -155,7 +165,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
             }
             if (vok) {  // voxels past the patch (its last K-block) must contribute zeros
 #pragma unroll
-                for (int t = 0; t < 32; ++t) av[t] = __ldg(xp + ro[t]);
+                for (int t = 0; t < 32; ++t) av[t] = __ldg(xp + rowo(t));
             } else {
 #pragma unroll
                 for (int t = 0; t < 32; ++t) av[t] = 0.f;
@@ -191,19 +201,27 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
             } else {
                 mbar_arrive(af0 + 8u * uint32_t(a));
             }
-            a += 2;
+            a += NG;
             if (a >= p.na) a = grp, u ^= 1u;
             D.poll();
         };
         // two K-blocks of gathers in flight per warp (registers from setmaxnreg)
-        float va[32], vb[32];
-        if (grp < kblocks) gather(va);
-        for (int kb = grp; kb < kblocks; kb += 4) {
-            if (kb + 2 < kblocks) gather(vb);
-            put(va);
-            if (kb + 2 >= kblocks) break;
-            if (kb + 4 < kblocks) gather(va);
-            put(vb);
+        if constexpr (NG == 2) {  // two K-blocks of gathers in flight per warp
+            float va[32], vb[32];
+            if (grp < kblocks) gather(va);
+            for (int kb = grp; kb < kblocks; kb += 2 * NG) {
+                if (kb + NG < kblocks) gather(vb);
+                put(va);
+                if (kb + NG >= kblocks) break;
+                if (kb + 2 * NG < kblocks) gather(va);
+                put(vb);
+            }
+        } else {  // three groups already keep three K-blocks in flight
+            float va[32];
+            for (int kb = grp; kb < kblocks; kb += NG) {
+                gather(va);
+                put(va);
+            }
         }
         // ---------------- remaining drains + epilogue (this warp's columns) ----------------
         D.finish();
@@ -216,7 +234,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 if (qq < ncols && o < p.f_out) wsz[int64_t(o) * p.mrows + R] = D.A.acc[qq];
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == PW) {
         // ---------------- TMA producer: g panels ----------------
         // Cluster rank r loads rows [r*nt/C, (r+1)*nt/C) of the g tile and
         // multicasts them to every CTA of the cluster (same K range, other
@@ -269,7 +287,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
                 if (++vkb == p.kb_per_patch) vkb = 0, ++pb;  // TMA side: one K-block per step
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == PW + 1) {
         // ---------------- MMA issuer ----------------
         if (!PAIR || rank == 0) {  // the whole warp runs the loop (converged); one elected lane issues
             const uint32_t idesc = idesc_tf32(PAIR ? 2 * BM : BM, p.nt);
@@ -325,7 +343,7 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
     tc_fence_before();
     __syncthreads();
     if (p.csize > 1) cluster_sync();  // no CTA leaves (or frees TMEM) while its peer still uses it
-    if (warp == 9) {
+    if (warp == PW + 1) {
         __syncwarp();
         tc_fence_after();
         if constexpr (PAIR) tmem_dealloc_pair(tmem, TMEM_COLS);
@@ -379,14 +397,14 @@ __global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, in
     }
 }
 
-template <int NTMAX, bool PAIR>
+template <int NTMAX, bool PAIR, int NG>
 void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mhi, const CUtensorMap& mlo,
                   const float* x, const int* rowoff, float* ws, const wg_params& p) {
-    auto* k = wgrad_tc_kernel<NTMAX, PAIR>;
+    auto* k = wgrad_tc_kernel<NTMAX, PAIR, NG>;
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(THREADS, 1, 1);
+    cfg.blockDim = dim3(threads_for<NG>(), 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -400,23 +418,31 @@ void launch_wgrad(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mh
     launch_check("conv_wgrad_tc");
 }
 
+template <int NTMAX, bool PAIR, int NG>
+const void* wgrad_kernel_ptr() {
+    return reinterpret_cast<const void*>(wgrad_tc_kernel<NTMAX, PAIR, NG>);
+}
+template <bool PAIR, int NG>
+const void* wgrad_kernel_ptr(int ntmax) {
+    return ntmax == 32 ? wgrad_kernel_ptr<32, PAIR, NG>()
+                       : (ntmax == 64 ? wgrad_kernel_ptr<64, PAIR, NG>() : wgrad_kernel_ptr<128, PAIR, NG>());
+}
+
 // CTAs resident at once (one per SM; clusters cannot use every SM of a GPC)
-int64_t resident_ctas(int ntmax, size_t smem, int csize, bool pair) {
-    static int64_t cache[3][3][2] = {};
+int64_t resident_ctas(int ntmax, size_t smem, int csize, bool pair, int ng) {
+    static int64_t cache[3][3][2][2] = {};
     const int ti = ntmax == 32 ? 0 : (ntmax == 64 ? 1 : 2), ci = csize == 1 ? 0 : (csize == 2 ? 1 : 2);
-    if (cache[ti][ci][pair]) return cache[ti][ci][pair];
+    int64_t& slot = cache[ti][ci][pair][ng == 3];
+    if (slot) return slot;
     int64_t r = 148;
     if (csize > 1) {
-        const void* k = pair ? (ntmax == 32   ? reinterpret_cast<const void*>(wgrad_tc_kernel<32, true>)
-                                : ntmax == 64 ? reinterpret_cast<const void*>(wgrad_tc_kernel<64, true>)
-                                              : reinterpret_cast<const void*>(wgrad_tc_kernel<128, true>))
-                             : (ntmax == 32   ? reinterpret_cast<const void*>(wgrad_tc_kernel<32, false>)
-                                : ntmax == 64 ? reinterpret_cast<const void*>(wgrad_tc_kernel<64, false>)
-                                              : reinterpret_cast<const void*>(wgrad_tc_kernel<128, false>));
+        const void* k = pair      ? wgrad_kernel_ptr<true, 2>(ntmax)
+                         : ng == 3 ? wgrad_kernel_ptr<false, 3>(ntmax)
+                                   : wgrad_kernel_ptr<false, 2>(ntmax);
         ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(csize) * 64, 1, 1);
-        cfg.blockDim = dim3(THREADS, 1, 1);
+        cfg.blockDim = dim3(unsigned(128 * (ng + 1)), 1, 1);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -429,7 +455,7 @@ int64_t resident_ctas(int ntmax, size_t smem, int csize, bool pair) {
         if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) == cudaSuccess && nc > 0) r = int64_t(nc) * csize;
         else cudaGetLastError();
     }
-    cache[ti][ci][pair] = r;
+    slot = r;
     return r;
 }
 
@@ -448,7 +474,10 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     const int ntmax = p.nt <= 32 ? 32 : (p.nt <= 64 ? 64 : 128);
     p.bstride = ntmax;
     p.nbuf = ntmax == 128 ? 2 : 4;  // + na x 64 A columns <= 512 TMEM columns
-    p.na = 4;
+    // producer warpgroups: 3 measured ~7% faster than 2 on c5 (the gather +
+    // transpose chain is latency-bound with one producer warp per SMSP)
+    int ng = 3;
+    if (const char* e = std::getenv("ZNN_WGRAD_NG")) ng = std::atoi(e) == 2 ? 2 : 3;
     p.nvol = c.n.vol();
     p.mvol = c.m.vol();
     p.ny = int(c.n.y), p.nz = int(c.n.z), p.my = int(c.m.y), p.mz = int(c.m.z);
@@ -468,7 +497,9 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     bool pair = false;
     if (const char* e = std::getenv("ZNN_WGRAD_PAIR")) pair = csize == 2 && p.nt % 32 == 0 && std::atoi(e) != 0;
     const int stage = 2 * (pair ? p.nt / 2 : p.nt) * 128;
-    const size_t fixed = 1024 + 8 * size_t(16) + 16 + sizeof(float) * 8 * 32 * TP + 64;
+    if (pair) ng = 2;
+    p.na = ng == 3 ? 3 : 4;  // A buffers: a multiple of the producer groups
+    const size_t fixed = 1024 + 8 * size_t(16) + 16 + sizeof(float) * 4 * ng * 32 * TP + 64;
     p.stages = int((size_t(220) * 1024 - fixed) / size_t(stage + 16));
     if (p.stages > 8) p.stages = 8;
     const int mtiles = int(ceil_div(ceil_div(p.mrows, BM), csize) * csize);
@@ -477,7 +508,7 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     // fill up to max(32, 8 waves' worth) splits (a 2.4-wave grid idles 20% of the GPU in its tail).
     const int64_t tiles = int64_t(mtiles) * ntiles;
     const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
-    const int64_t wave = resident_ctas(ntmax, smem, csize, pair);
+    const int64_t wave = resident_ctas(ntmax, smem, csize, pair, ng);
     const int64_t max_splits = std::max<int64_t>(
         1, std::min<int64_t>(std::max<int64_t>(32, ceil_div(8 * 148, tiles)), ceil_div(p.kb_total, 4 * CHUNK_KB)));
     int64_t splits = 1;
@@ -515,13 +546,17 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     const CUtensorMap mlo = make_panel_map_rows(glo, BK, gtiles * p.nt, p.nt / csize);
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), unsigned(splits)};
     if (pair) {
-        if (ntmax == 32) launch_wgrad<32, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
-        else if (ntmax == 64) launch_wgrad<64, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
-        else launch_wgrad<128, true>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        if (ntmax == 32) launch_wgrad<32, true, 2>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else if (ntmax == 64) launch_wgrad<64, true, 2>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else launch_wgrad<128, true, 2>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+    } else if (ng == 3) {
+        if (ntmax == 32) launch_wgrad<32, false, 3>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else if (ntmax == 64) launch_wgrad<64, false, 3>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else launch_wgrad<128, false, 3>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
     } else {
-        if (ntmax == 32) launch_wgrad<32, false>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
-        else if (ntmax == 64) launch_wgrad<64, false>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
-        else launch_wgrad<128, false>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        if (ntmax == 32) launch_wgrad<32, false, 2>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else if (ntmax == 64) launch_wgrad<64, false, 2>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
+        else launch_wgrad<128, false, 2>(grid, smem, st, mhi, mlo, x, rowoff, partials, p);
     }
     const int64_t len = c.f_out * int64_t(p.mrows);
     int64_t rb = ceil_div(len, 256);
