@@ -48,7 +48,10 @@ namespace {
 
 using namespace znn_tc;
 
-constexpr int THREADS = 384;  // registers are granted per 4-warp group
+// NG producer warpgroups (one warp per TMEM lane quarter each) + one control
+// warpgroup (TMA, MMA, K-block list, idle): 128 * (NG + 1) threads
+template <int NG>
+constexpr int conv_threads() { return 128 * (NG + 1); }
 constexpr uint32_t TMEM_COLS = 512;
 constexpr int CHUNK_KB = 8;
 
@@ -77,8 +80,8 @@ struct tc_params {
     int kz, dsz, vz0, vz1, taps;
 };
 
-template <int NTMAX>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int NTMAX, int NG>
+__global__ void __launch_bounds__(conv_threads<NG>(), 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant__ CUtensorMap tm_lo,
                const float* __restrict__ src, const int* __restrict__ koff, float* __restrict__ out,
                const float* __restrict__ bias, int act, tc_params p) {
@@ -111,14 +114,15 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         }
         for (int b = 0; b < 4; ++b) {
             mbar_init(accf0 + 8u * b, 1);
-            mbar_init(acce0 + 8u * b, 256);
+            mbar_init(acce0 + 8u * b, 128u * NG);
             mbar_init(af0 + 8u * b, 128);
             mbar_init(ae0 + 8u * b, 1);
         }
         fence_barrier_init();
     }
-    if (warp == 9) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
-    if (warp == 10) {
+    constexpr int PW = 4 * NG;  // producer warps; TMA warp PW, MMA warp PW + 1, list warp PW + 2
+    if (warp == PW + 1) tmem_alloc(smem_u32(tmem_slot), TMEM_COLS);
+    if (warp == PW + 2) {
         // active K-blocks of this tile: a (wx, wy) tap row is live iff the
         // tile's bounding box shifted by s*w meets the nonzero source region
         int x0 = 0, x1 = p.ox - 1, y0 = 0, y1 = p.oy - 1, z0 = 0, z1 = p.oz - 1;
@@ -170,11 +174,15 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     const int nchunks = (nact + CHUNK_KB - 1) / CHUNK_KB;
     const uint32_t a_col0 = uint32_t(p.nbuf * p.bstride);
 
-    if (warp < 8) {
+    if constexpr (NG == 3) {  // producers need the registers of a fourth warpgroup
+        if (warp < PW) setmaxnreg_inc<152>();
+        else setmaxnreg_dec<56>();
+    }
+    if (warp < PW) {
         // ---------------- im2col producers -> TMEM ----------------
         const int r = threadIdx.x & 127;
-        const int half = threadIdx.x >> 7;  // warp group: even (0) / odd (1) active K-blocks
-        constexpr int NH = NTMAX / 2;
+        const int half = threadIdx.x >> 7;  // producer group: active K-blocks half, half + NG, ...
+        constexpr int NH = ((NTMAX + NG - 1) / NG + 15) / 16 * 16;
         const int col0 = half * NH;
         const int ncols = max(0, min(NH, p.nt - col0));
         const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
@@ -208,7 +216,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
         // this group's A buffers: half, half + 2, ... (< na); (a, use parity) tracked incrementally
         int a = half;
         uint32_t u = 0;
-        for (int j = half; j < nact; j += 2) {
+        for (int j = half; j < nact; j += NG) {
             const int kb = list[j];
             const int4* tb = reinterpret_cast<const int4*>(koff + kb * BK);
             float v[BK];
@@ -237,7 +245,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(af0 + 8u * uint32_t(a));
-            a += 2;
+            a += NG;
             if (a >= p.na) a = half, u ^= 1u;
             D.poll();
         }
@@ -254,7 +262,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                 }
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == PW) {
         // ---------------- TMA producer (pre-split weight panels) ----------------
         {  // converged warp, one elected lane issues
             int s = 0;
@@ -267,7 +275,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
                 if (++s == p.stages) s = 0, ph ^= 1u;
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == PW + 1) {
         // ---------------- MMA issuer ----------------
         {  // the whole warp runs the loop (converged); one elected lane issues
             const uint32_t idesc = idesc_tf32(BM, p.nt);
@@ -309,7 +317,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant_
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == PW + 1) {
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
@@ -409,13 +417,13 @@ encode_fn_t encoder() {
 
 CUtensorMap make_panel_map(const float* ptr, int kpad, int rows, int nt);
 
-template <int NTMAX>
+template <int NTMAX, int NG>
 void launch_kernel(dim3 grid, size_t smem, cudaStream_t st, const CUtensorMap& mhi, const CUtensorMap& mlo,
                    const float* srcp, const int* tab, float* outp, const float* bias, int act, const tc_params& p,
                    const char* what) {
-    auto* k = conv_tc_kernel<NTMAX>;
+    auto* k = conv_tc_kernel<NTMAX, NG>;
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k<<<grid, THREADS, smem, st>>>(mhi, mlo, srcp, tab, outp, bias, act, p);
+    k<<<grid, conv_threads<NG>(), smem, st>>>(mhi, mlo, srcp, tab, outp, bias, act, p);
     launch_check(what);
 }
 
@@ -513,7 +521,11 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     const int ntmax = nt <= 32 ? 32 : (nt <= 64 ? 64 : 128);
     p.bstride = ntmax;
     p.nbuf = ntmax == 128 ? 2 : 4;  // + na x 64 A columns <= 512 TMEM columns
-    p.na = 4;                       // two A buffers per producer group: a group writes ahead of the MMA
+    // producer warpgroups: 3 for short K (gathers dominate: c5's first layer
+    // 9.0 -> 7.9 ms), 2 for long K (the MMA dominates; 3 measured ~1% slower)
+    int ng = p.kblocks <= 64 ? 3 : 2;
+    if (const char* e = std::getenv("ZNN_CONV_NG")) ng = std::atoi(e) == 3 ? 3 : 2;
+    p.na = ng == 3 ? 3 : 4;  // A buffers: two per group (NG = 2) or one per group (NG = 3)
     p.vox_out = od.vol();
     p.rows = Bn * p.vox_out;
     p.ox = int(od.x), p.oy = int(od.y), p.oz = int(od.z);
@@ -537,9 +549,15 @@ void launch_valid(cudaStream_t st, int64_t Bn, int f_src, int n_real, int f_in_w
     const size_t smem = size_t(p.stages) * size_t(stage) + 8 * size_t(2 * p.stages + 16) + fixed;
     const int64_t mtiles = bc.box ? Bn * p.tnx * p.tny * p.tnz : ceil_div(p.rows, BM);
     const dim3 grid{unsigned(mtiles), unsigned(ntiles), 1u};
-    if (ntmax == 32) launch_kernel<32>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
-    else if (ntmax == 64) launch_kernel<64>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
-    else launch_kernel<128>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+    if (ng == 3) {
+        if (ntmax == 32) launch_kernel<32, 3>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+        else if (ntmax == 64) launch_kernel<64, 3>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+        else launch_kernel<128, 3>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+    } else {
+        if (ntmax == 32) launch_kernel<32, 2>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+        else if (ntmax == 64) launch_kernel<64, 2>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+        else launch_kernel<128, 2>(grid, smem, st, mhi, mlo, srcp, tab, outp, bias, act, p, what);
+    }
 }
 
 size_t panel_bytes(int f_src, int n_real, int64_t T) {
