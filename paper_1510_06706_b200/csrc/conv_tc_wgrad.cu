@@ -144,12 +144,10 @@ wgrad_tc_kernel(const __grid_constant__ CUtensorMap tm_hi, const __grid_constant
         uint32_t u = 0;
         int64_t pb = (q0 + grp) / p.kb_per_patch;  // patch / K-block of the next gather, tracked incrementally
         int vkb = int(q0 + grp - pb * p.kb_per_patch);
-        int ro[32];  // this warp's 32 row offsets (tap window starts)
-        if constexpr (NG == 2) {
+        int ro[32];  // this warp's 32 row offsets (tap window starts), kept in registers
 #pragma unroll
-            for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
-        }
-        auto rowo = [&](int t) { return NG == 2 ? ro[t] : rowoff[wq * 32 + t]; };
+        for (int t = 0; t < 32; ++t) ro[t] = rowoff[wq * 32 + t];
+        auto rowo = [&](int t) { return ro[t]; };
         auto gather = [&](float (&av)[32]) {
             const int v = vkb * BK + lane;
             const int64_t pcur = pb;
