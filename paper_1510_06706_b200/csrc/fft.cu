@@ -526,6 +526,140 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_pipe_k(float2* __restrict_
     }
 }
 
+// ---- single-input-map layers (f_in = 1): the CMACs have no reduction over
+// input maps, so they fuse into the plane passes and the product spectra
+// never touch HBM ----
+// forward: Y[b][o] = X[b] * conj(K[o]) formed while loading each plane, then
+// the inverse xy pass (keep rows / columns) -> compact planes
+template <int P>
+__global__ void __launch_bounds__(THREADS) fft_xy_inv_mul1_k(const float2* __restrict__ X, const float2* __restrict__ K,
+                                                              float2* __restrict__ out, int64_t planes, int fo, int Zh,
+                                                              int x_step, int xc, int y_step, int yc) {
+    constexpr int PP = P + 2;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* pl = xbuf + LINES * P;  // [P][PP]
+    fill_twiddles<P>(tw);
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * P;
+    for (int64_t q = blockIdx.x; q < planes; q += gridDim.x) {
+        const int64_t img = q / Zh;
+        const int zb = int(q - img * Zh);
+        const int64_t b = img / fo, o = img - (img / fo) * fo;
+        const float4* xs = reinterpret_cast<const float4*>(X + (b * Zh + zb) * int64_t(P) * P);
+        const float4* ks = reinterpret_cast<const float4*>(K + (o * Zh + zb) * int64_t(P) * P);
+        __syncthreads();  // previous plane fully consumed
+        for (int idx = threadIdx.x; idx < P * P / 2; idx += THREADS) {
+            const int e = 2 * idx, x = e / P, y = e - (e / P) * P;
+            const float4 a = __ldg(xs + idx), kk = __ldg(ks + idx);
+            pl[x * PP + y] = cmulc(make_float2(a.x, a.y), make_float2(kk.x, kk.y));
+            pl[x * PP + y + 1] = cmulc(make_float2(a.z, a.w), make_float2(kk.z, kk.w));
+        }
+        __syncthreads();
+        for (int c0 = 0; c0 < P; c0 += LINES) {  // column inverses, keep rows x_step * i
+            const int y = c0 + l;
+            const bool ok = y < P;
+            float2 v[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? pl[(t + R1 * n2) * PP + y] : make_float2(0.f, 0.f);
+            line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+                const int i = k / x_step;
+                if (ok && i * x_step == k && i < xc) pl[i * PP + y] = val;
+            });
+        }
+        __syncthreads();
+        float2* o_ = out + q * (int64_t(xc) * yc);
+        for (int r0 = 0; r0 < xc; r0 += LINES) {  // row inverses of the kept rows
+            const int i = r0 + l;
+            const bool ok = i < xc;
+            float2 v[R2];
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? pl[i * PP + t + R1 * n2] : make_float2(0.f, 0.f);
+            line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+                const int j = k / y_step;
+                if (ok && j * y_step == k && j < yc) o_[i * yc + j] = val;
+            });
+        }
+    }
+}
+
+// backward (no input gradient): for each (o, z-bin) the CTA transforms the
+// z-pass planes G[b][o] of every patch (rows, then columns) and accumulates
+// dK[o] = sum_b X[b] * conj(G[b][o]) in registers; only dK is written
+template <int P>
+__global__ void __launch_bounds__(THREADS) fft_xy_fwd_upd1_k(const float2* __restrict__ gz, const float2* __restrict__ X,
+                                                              float2* __restrict__ DK, int64_t planes, int B, int fo,
+                                                              int Zh, int nx, int ny) {
+    constexpr int PP = P + 2;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    constexpr int E = (P * P + THREADS - 1) / THREADS;  // plane elements per thread
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* pl = xbuf + LINES * P;
+    fill_twiddles<P>(tw);
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * P;
+    for (int64_t q = blockIdx.x; q < planes; q += gridDim.x) {  // q = o * Zh + zb
+        const int64_t o = q / Zh;
+        const int zb = int(q - o * Zh);
+        float2 acc[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) acc[i] = make_float2(0.f, 0.f);
+        for (int b = 0; b < B; ++b) {
+            const float2* g = gz + ((int64_t(b) * fo + o) * Zh + zb) * int64_t(P) * P;
+            __syncthreads();  // previous plane fully consumed
+            for (int r0 = 0; r0 < nx; r0 += LINES) {  // rows (y transforms) of the valid rows, from HBM
+                const int x = r0 + l;
+                const bool ok = x < nx;
+                float2 v[R2];
+#pragma unroll
+                for (int n2 = 0; n2 < R2; ++n2) {
+                    const int y = t + R1 * n2;
+                    v[n2] = (ok && t < R1 && y < ny) ? __ldcs(g + x * P + y) : make_float2(0.f, 0.f);
+                }
+                line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+                    if (ok) pl[x * PP + k] = val;
+                });
+            }
+            __syncthreads();
+            for (int c0 = 0; c0 < P; c0 += LINES) {  // columns (x transforms); rows >= nx are zero
+                const int y = c0 + l;
+                const bool ok = y < P;
+                float2 v[R2];
+#pragma unroll
+                for (int n2 = 0; n2 < R2; ++n2) {
+                    const int x = t + R1 * n2;
+                    v[n2] = (ok && t < R1 && x < nx) ? pl[x * PP + y] : make_float2(0.f, 0.f);
+                }
+                line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+                    if (ok) pl[k * PP + y] = val;
+                });
+            }
+            __syncthreads();
+            const float2* xs = X + (int64_t(b) * Zh + zb) * int64_t(P) * P;
+#pragma unroll
+            for (int i = 0; i < E; ++i) {
+                const int e = threadIdx.x + i * THREADS;
+                if (e < P * P) {
+                    const int x = e / P, y = e - (e / P) * P;
+                    const float2 p = cmulc(__ldg(xs + e), pl[x * PP + y]);
+                    acc[i].x += p.x;
+                    acc[i].y += p.y;
+                }
+            }
+        }
+        float2* dk = DK + q * int64_t(P) * P;
+#pragma unroll
+        for (int i = 0; i < E; ++i) {
+            const int e = threadIdx.x + i * THREADS;
+            if (e < P * P) dk[e] = acc[i];
+        }
+    }
+}
+
 struct zinv_args {
     int xc, yc;                        // kept block per z-bin plane (compact input)
     int z_step, z_cnt;                 // kept z voxels (selection starts at 0)
@@ -886,7 +1020,7 @@ void cmac_ss(cudaStream_t st, const float2* S, const float2* K, float2* O, int B
 // forward 3D R2C of imgs real volumes (valid dims n, image stride in floats):
 // z pass (transposed store) + fused xy pass
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
-               float2* spec) {
+               float2* spec, bool z_only = false) {
     const int64_t nlines = imgs * n.x * n.y;
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
@@ -896,6 +1030,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
             in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y));
     });
     launch_check("fft_z_fwd");
+    if (z_only) return;
     const int64_t planes = imgs * p.Zh;
     dispatch_pad(int(p.P.y), [&](auto pc) {
         constexpr int PY = decltype(pc)::value;
@@ -914,6 +1049,9 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
     });
     launch_check("fft_xy_fwd");
 }
+
+void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 cnt, float* out, int64_t out_img_stride,
+               const float* bias, int bias_mod, int act, const float2* cbuf);
 
 // inverse 3D C2R keeping voxels (x,y,z) = (step*i) for i < cnt per axis,
 // written as a dense box [imgs][cnt.x][cnt.y][cnt.z] (image stride given);
@@ -941,6 +1079,12 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         }
     });
     launch_check("fft_xy_inv");
+    inverse_z(st, p, imgs, step, cnt, out, out_img_stride, bias, bias_mod, act, cbuf);
+}
+
+// z pass of an inverse: C2R of the compact kept planes in cbuf
+void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 cnt, float* out, int64_t out_img_stride,
+               const float* bias, int bias_mod, int act, const float2* cbuf) {
     zinv_args g;
     g.xc = int(cnt.x), g.yc = int(cnt.y);
     g.z_step = int(step.z), g.z_cnt = int(cnt.z);
@@ -957,6 +1101,14 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         fft_z_inv_k<PP><<<unsigned(ceil_div(g.nlines, LINES)), THREADS, smem_for(PP), st>>>(cbuf, g, bias, out);
     });
     launch_check("fft_z_inv");
+}
+
+// f_in = 1 fused paths need a square plane kernel with one plane buffer
+bool fused1_ok(const plan& p, const conv_shape& c) {
+    return c.f_in == 1 && p.P.x == p.P.y && p.P.x > 1 && p.P.x <= 96 && !std::getenv("ZNN_FFT_NOFUSE1");
+}
+size_t smem_plane1(int P) {
+    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(P) + size_t(P) * size_t(P + 2));
 }
 
 float2* carve(char*& cur, int64_t count) {
@@ -1008,6 +1160,23 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     p.cnt.fwd_kernel += nker;
     // Y = sum_i X * conj(K), one inverse per output node, crop + bias + transfer
     const int64_t ccount = c.B * c.f_out * p.Zh * c.m.x * c.m.y;  // compact kept planes
+    if (fused1_ok(p, c)) {  // f_in = 1: Y = X * conj(K) formed inside the inverse xy pass
+        float2* CB = static_cast<float2*>(ws.get(sizeof(float2) * size_t(ccount) + 256));
+        const int64_t planes = c.B * c.f_out * p.Zh;
+        dispatch_pad(int(p.P.y), [&](auto pc) {
+            constexpr int PY = decltype(pc)::value;
+            if constexpr (PY <= 96) {
+                const size_t sm = smem_plane1(PY);
+                allow_smem(fft_xy_inv_mul1_k<PY>, sm);
+                fft_xy_inv_mul1_k<PY><<<pipe_grid(planes, sm), THREADS, sm, st>>>(
+                    p.X, p.K, CB, planes, int(c.f_out), int(p.Zh), 1, int(c.m.x), 1, int(c.m.y));
+            }
+        });
+        launch_check("fft_xy_inv_mul1");
+        inverse_z(st, p, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB);
+        p.cnt.fwd_inverse += c.B * c.f_out;
+        return;
+    }
     char* cur = static_cast<char*>(ws.get(sizeof(float2) * size_t(c.B * c.f_out * p.bins + ccount) + 1024));
     float2* Y = carve(cur, c.B * c.f_out * p.bins);
     float2* CB = carve(cur, ccount);
@@ -1029,6 +1198,26 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     float2* DK = carve(cur, c.f_out * c.f_in * p.bins);
     float2* CB = carve(cur, ccount);
     // backward image spectra, padded to the tail dims (engine.hpp:757-759)
+    if (!gin && fused1_ok(p, c)) {
+        // f_in = 1, no input gradient: the xy pass of every G[b][o] feeds
+        // dK[o] = sum_b X[b] * conj(G[b][o]) directly (G never reaches HBM)
+        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, /*z_only=*/true);
+        p.cnt.bwd_image += nB * c.f_out;
+        const int64_t planes = c.f_out * p.Zh;
+        dispatch_pad(int(p.P.y), [&](auto pc) {
+            constexpr int PY = decltype(pc)::value;
+            if constexpr (PY <= 96) {
+                const size_t sm = smem_plane1(PY);
+                allow_smem(fft_xy_fwd_upd1_k<PY>, sm);
+                fft_xy_fwd_upd1_k<PY><<<pipe_grid(planes, sm), THREADS, sm, st>>>(
+                    G, p.X, DK, planes, int(nB), int(c.f_out), int(p.Zh), int(c.m.x), int(c.m.y));
+            }
+        });
+        launch_check("fft_xy_fwd_upd1");
+        inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
+        p.cnt.upd_inverse += c.f_out * c.f_in;
+        return;
+    }
     forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G);
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
