@@ -177,6 +177,14 @@ int znn_net_step_host(znn_net net, const float* inputs, const float* labels, dou
 int znn_net_forward_backward(znn_net net, const float* inputs_dev, const float* labels_dev,
                              double* loss);
 int znn_net_apply_update(znn_net net);
+/* Single-process SGD step from DEVICE buffers: forward + loss + backward with
+ * the SGD+momentum update applied layer by layer as each gradient becomes
+ * final (fused into the tensor-core weight-gradient epilogue; the weights a
+ * layer's data gradient reads are updated only after it). Same result as
+ * znn_net_forward_backward + znn_net_apply_update; the reference likewise
+ * updates each edge as soon as its gradient task ran (run_update_body,
+ * engine.hpp:772-829). */
+int znn_net_train_step(znn_net net, const float* inputs_dev, const float* labels_dev, double* loss);
 /* device pointer + length of the flat gradient buffer (allreduce target) */
 int znn_net_grad_buffer(znn_net net, float** dptr, int64_t* count);
 /* forward only; outputs [B][f_out][m] copied to host when host_out != NULL */

@@ -26,7 +26,7 @@ EXPORTS = [
     "znn_net_create", "znn_net_destroy", "znn_net_describe", "znn_net_num_params",
     "znn_net_io_sizes", "znn_net_set_params", "znn_net_get_params", "znn_net_get_gradients",
     "znn_net_reset_momentum", "znn_net_set_layer_engine", "znn_net_autotune", "znn_net_fft_counts",
-    "znn_net_step_host", "znn_net_forward_backward", "znn_net_apply_update",
+    "znn_net_step_host", "znn_net_forward_backward", "znn_net_apply_update", "znn_net_train_step",
     "znn_net_grad_buffer", "znn_net_forward", "znn_net_group_info",
     "znn_net_get_group_image", "znn_net_get_mask",
 ]
@@ -103,6 +103,7 @@ def lib():
         "znn_net_step_host": (ci, [vp, vp, vp, Pd]),
         "znn_net_forward_backward": (ci, [vp, vp, vp, Pd]),
         "znn_net_apply_update": (ci, [vp]),
+        "znn_net_train_step": (ci, [vp, vp, vp, Pd]),
         "znn_net_grad_buffer": (ci, [vp, ctypes.POINTER(vp), P64]),
         "znn_net_forward": (ci, [vp, vp, Pf]),
         "znn_net_group_info": (ci, [vp, ci, P64, P64]),

@@ -156,6 +156,18 @@ class Net:
         self._c(lib().znn_net_forward_backward(self._h, ctypes.c_void_p(ip), ctypes.c_void_p(lp), None))
         return None
 
+    def train_step(self, inputs_dev, labels_dev, sync_loss=True):
+        """One SGD step from device buffers with the update fused layer by
+        layer (single process; = forward_backward + apply_update)."""
+        ip = inputs_dev if isinstance(inputs_dev, int) else inputs_dev.data_ptr()
+        lp = labels_dev if isinstance(labels_dev, int) else labels_dev.data_ptr()
+        if sync_loss:
+            loss = ctypes.c_double()
+            self._c(lib().znn_net_train_step(self._h, ctypes.c_void_p(ip), ctypes.c_void_p(lp), ctypes.byref(loss)))
+            return loss.value
+        self._c(lib().znn_net_train_step(self._h, ctypes.c_void_p(ip), ctypes.c_void_p(lp), None))
+        return None
+
     def apply_update(self):
         self._c(lib().znn_net_apply_update(self._h))
 

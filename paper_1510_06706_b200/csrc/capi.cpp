@@ -346,6 +346,14 @@ int znn_net_forward_backward(znn_net net, const float* inputs_dev, const float* 
     });
 }
 
+int znn_net_train_step(znn_net net, const float* inputs_dev, const float* labels_dev, double* loss) {
+    return guarded(net->ctx, [&] {
+        net->ex->set_stream(net->ctx->stream);
+        const double l = net->ex->forward_backward(inputs_dev, labels_dev, loss != nullptr, true);
+        if (loss) *loss = l;
+    });
+}
+
 int znn_net_apply_update(znn_net net) {
     return guarded(net->ctx, [&] { net->ex->set_stream(net->ctx->stream); net->ex->apply_update(); });
 }

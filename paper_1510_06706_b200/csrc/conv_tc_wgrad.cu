@@ -386,12 +386,21 @@ __global__ void split_tiles_k(const float* __restrict__ g, int f_out, int64_t mv
     *reinterpret_cast<float4*>(lo + dst) = make_float4(l[0], l[1], l[2], l[3]);
 }
 
+// fixed-order sum of the split-K partials; with w != nullptr also the
+// SGD+momentum update of those weights (the fused weight-gradient epilogue)
 __global__ void reduce_splits_k(const float* __restrict__ ws, int64_t splits, int64_t len, float scale,
-                                float* __restrict__ out) {
+                                float* __restrict__ out, float* __restrict__ w, float* __restrict__ v, float lr,
+                                float mu) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
         float acc = 0.f;
         for (int64_t s = 0; s < splits; ++s) acc += ws[s * len + i];
-        out[i] = scale * acc;
+        const float g = scale * acc;
+        out[i] = g;
+        if (w) {
+            const float nv = mu * v[i] + g;
+            v[i] = nv;
+            w[i] -= lr * nv;
+        }
     }
 }
 
@@ -460,7 +469,7 @@ int64_t resident_ctas(int ntmax, size_t smem, int csize, bool pair, int ng) {
 }  // namespace
 
 void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* g, float* dw, float scale,
-                   scratch& ws) {
+                   scratch& ws, const sgd_fuse* upd) {
     wg_params p;
     p.f_in = int(c.f_in);
     p.f_out = int(c.f_out);
@@ -559,7 +568,9 @@ void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const f
     const int64_t len = c.f_out * int64_t(p.mrows);
     int64_t rb = ceil_div(len, 256);
     if (rb > 148 * 8) rb = 148 * 8;
-    reduce_splits_k<<<unsigned(rb), 256, 0, st>>>(partials, splits, len, scale, dw);
+    reduce_splits_k<<<unsigned(rb), 256, 0, st>>>(partials, splits, len, scale, dw, upd ? upd->w : nullptr,
+                                                  upd ? upd->v : nullptr, upd ? upd->lr : 0.f,
+                                                  upd ? upd->mu : 0.f);
     launch_check("conv_wgrad_tc_reduce");
 }
 

@@ -379,25 +379,33 @@ void executor::run_conv_fwd(layer& L) {
     }
 }
 
-void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad) {
+void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update) {
     const float* x = groups_[size_t(L.in)].act;
-    const float* w = params_ + L.w_off;
+    float* w = params_ + L.w_off;
     float* gw = grads_ + L.w_off;
+    const int64_t wcount = L.shape.f_out * L.shape.f_in * L.shape.taps();
     if (L.engine == 1) {
         znn_fft::conv_bwd(st_, fft_plan(L), L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_);
+        if (update) znn_gpu::sgd_momentum(st_, w, vel_ + L.w_off, gw, wcount, cfg_.lr, cfg_.mu);
         return;
     }
     const bool tc = L.engine == 0;
-    if (tc && znn_gpu::conv_tc_supported(L.shape, 2))
-        znn_gpu::conv_wgrad_tc(st_, L.shape, x, g_out, gw, 1.f, ws_);
-    else
-        znn_gpu::conv_wgrad_simt(st_, L.shape, x, g_out, gw, 1.f, ws_);
-    if (need_dgrad) {
+    auto dgrad = [&] {
         if (tc && znn_gpu::conv_tc_supported(L.shape, 1))
             znn_gpu::conv_dgrad_tc(st_, L.shape, g_out, w, g_in, ws_);
         else
             znn_gpu::conv_dgrad_simt(st_, L.shape, g_out, w, g_in);
+    };
+    // with the update fused, the data gradient must read the weights first
+    if (need_dgrad && update) dgrad();
+    if (tc && znn_gpu::conv_tc_supported(L.shape, 2)) {
+        znn_gpu::sgd_fuse upd{w, vel_ + L.w_off, cfg_.lr, cfg_.mu};
+        znn_gpu::conv_wgrad_tc(st_, L.shape, x, g_out, gw, 1.f, ws_, update ? &upd : nullptr);
+    } else {
+        znn_gpu::conv_wgrad_simt(st_, L.shape, x, g_out, gw, 1.f, ws_);
+        if (update) znn_gpu::sgd_momentum(st_, w, vel_ + L.w_off, gw, wcount, cfg_.lr, cfg_.mu);
     }
+    if (need_dgrad && !update) dgrad();
 }
 
 void executor::run_forward(const float* in_dev) {
@@ -421,7 +429,7 @@ void executor::run_forward(const float* in_dev) {
 
 void executor::forward(const float* in_dev) { run_forward(in_dev); }
 
-double executor::forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss) {
+double executor::forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss, bool update) {
     const int64_t B = cfg_.batch;
     run_forward(in_dev);
     group& G = groups_.back();
@@ -456,13 +464,20 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                                               L.kinds_dev, params_ + L.b_off, O.grad, grads_ + L.b_off, ws_);
                     }
                 }
-                run_conv_bwd(L, O.grad, I.grad, L.in != 0);
+                // the bias gradient is final here (transfer_bwd above): update it
+                if (update && L.fused)
+                    znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off,
+                                          L.shape.f_out, cfg_.lr, cfg_.mu);
+                run_conv_bwd(L, O.grad, I.grad, L.in != 0, update);
                 break;
             }
             case lkind::transfer:
                 znn_gpu::transfer_bwd(st_, O.grad, I.act, false, B, I.maps, I.dims.vol(),
                                       ce_here ? L.none_dev : L.kinds_dev, params_ + L.b_off,
                                       I.grad ? I.grad : O.grad, grads_ + L.b_off, ws_);
+                if (update)
+                    znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off, I.maps,
+                                          cfg_.lr, cfg_.mu);
                 break;
             case lkind::pool:
                 if (L.in != 0) znn_gpu::maxpool_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, I.grad);
@@ -489,8 +504,7 @@ double executor::step_host(const float* in_host, const float* labels_host) {
     const int64_t B = cfg_.batch;
     ZNN_CUDA_CHECK(cudaMemcpyAsync(in_stage_, in_host, sizeof(float) * size_t(B * in_per_patch()), cudaMemcpyHostToDevice, st_));
     ZNN_CUDA_CHECK(cudaMemcpyAsync(lab_stage_, labels_host, sizeof(float) * size_t(B * out_per_patch()), cudaMemcpyHostToDevice, st_));
-    forward_backward(in_stage_, lab_stage_, false);
-    apply_update();
+    forward_backward(in_stage_, lab_stage_, false, true);
     return last_loss_device();
 }
 
@@ -550,7 +564,7 @@ std::vector<int> executor::autotune(int trials) {
             for (int t = 0; t <= trials; ++t) {
                 ZNN_CUDA_CHECK(cudaEventRecord(a, st_));
                 run_conv_fwd(T);
-                run_conv_bwd(T, gout, gin, L.in != 0);
+                run_conv_bwd(T, gout, gin, L.in != 0, false);
                 ZNN_CUDA_CHECK(cudaEventRecord(b, st_));
                 ZNN_CUDA_CHECK(cudaEventSynchronize(b));
                 float ms = 0.f;

@@ -83,7 +83,11 @@ public:
     std::vector<int> autotune(int trials);
 
     // inputs/labels are device pointers [B][maps][vol] in input/output-node id order
-    double forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss = true);
+    // update: apply SGD+momentum layer by layer as each gradient becomes final
+    // (fused into the tensor-core weight-gradient epilogue); single-process
+    // training only — data parallelism needs the summed gradient first
+    double forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss = true,
+                            bool update = false);
     void apply_update();
     void forward(const float* in_dev);
     double step_host(const float* in_host, const float* labels_host);
@@ -104,7 +108,7 @@ private:
     void allocate();
     void run_forward(const float* in_dev);
     void run_conv_fwd(layer& L);
-    void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad);
+    void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update);
     znn_fft::plan& fft_plan(layer& L);
 
     train_cfg cfg_;

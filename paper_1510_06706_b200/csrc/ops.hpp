@@ -47,8 +47,17 @@ void conv_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const flo
                  const float* bias, int act, float* y, scratch& ws);
 void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const float* w,
                    float* dx, scratch& ws);
+// SGD(+momentum) applied in a kernel epilogue right where the gradient is
+// final (v = mu v + g; w -= lr v, the arithmetic of sgd_momentum)
+struct sgd_fuse {
+    float* w = nullptr;
+    float* v = nullptr;
+    float lr = 0.f, mu = 0.f;
+};
+// upd != nullptr: the split-K reduction also applies the update to the
+// weights (dw is still written)
 void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* g,
-                   float* dw, float scale, scratch& ws);
+                   float* dw, float scale, scratch& ws, const sgd_fuse* upd = nullptr);
 
 // ---- pointwise (pointwise.cu) ----
 void transfer_fwd(cudaStream_t st, const float* x, int64_t B, int64_t f, int64_t vox,

@@ -38,6 +38,9 @@ class DataParallelStep:
         return self._grad
 
     def __call__(self, inputs, labels, sync_loss=False):
+        if self.world == 1 and hasattr(self.net, "train_step"):
+            # nothing to sum: the update is fused into the backward pass
+            return self.net.train_step(inputs, labels, sync_loss=sync_loss)
         loss = self.net.forward_backward(inputs, labels, sync_loss=sync_loss)
         if self.world > 1:
             import torch.distributed as dist

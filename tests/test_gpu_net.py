@@ -157,3 +157,35 @@ def test_netspec_layered_and_errors(ctx):
         Net(ctx, skip, (2, 2, 2))  # not layered: edge a->c skips a node group
     with pytest.raises(ShapeError):
         Net(ctx, "[layered] seq=CT width=2 kernel=5,5,5 fn=relu output=3,3,3\n", loss="ce")  # ce needs logistic
+
+
+@pytest.mark.parametrize("engine", ["direct", "simt", "fft"])
+@pytest.mark.parametrize("ci", [2, 3, 4], ids=["c3", "c4", "c5"])
+def test_fused_update_matches_phase_split(ctx, ci, engine):
+    """train_step (SGD+momentum fused layer by layer, in the tensor-core
+    weight-gradient epilogue) == forward_backward + apply_update, bit for bit,
+    over three momentum steps."""
+    from paper_1510_06706_b200._lib import ShapeError
+    cfg = cases()[ci]
+    params, x, lab = make_case(cfg, 5)
+    xd, ld = torch.as_tensor(x, device="cuda"), torch.as_tensor(lab, device="cuda")
+    nets = []
+    for fused in (False, True):
+        try:
+            net = gpu_net(ctx, cfg, engine)
+        except ShapeError as e:  # FFT unsupported for a layer shape of this config
+            pytest.skip(str(e))
+        net.set_params(params)
+        losses = []
+        for _ in range(3):
+            if fused:
+                losses.append(net.train_step(xd, ld))
+            else:
+                losses.append(net.forward_backward(xd, ld))
+                net.apply_update()
+        nets.append((net.get_params(), net.get_gradients(), losses))
+    (p0, g0, l0), (p1, g1, l1) = nets
+    assert l0 == l1
+    assert np.array_equal(g0, g1)
+    assert np.array_equal(p0, p1)
+    assert not np.array_equal(p1, params)
