@@ -50,6 +50,20 @@ int64_t good_size(int64_t n) {
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
 // a * conj(b)
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) { return make_float2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y); }
+// acc += a * b and acc += a * conj(b) as four dependent-pair FMAs (the
+// product-then-add form costs six FP32 instructions per complex MAC)
+__device__ __forceinline__ void cmac(float& re, float& im, float ax, float ay, float bx, float by) {
+    re = fmaf(ax, bx, re);
+    re = fmaf(-ay, by, re);
+    im = fmaf(ax, by, im);
+    im = fmaf(ay, bx, im);
+}
+__device__ __forceinline__ void cmacc(float& re, float& im, float ax, float ay, float bx, float by) {
+    re = fmaf(ax, bx, re);
+    re = fmaf(ay, by, re);
+    im = fmaf(ay, bx, im);
+    im = fmaf(-ax, by, im);
+}
 
 template <int R, bool INV>
 __device__ __forceinline__ void dft_small(float2* v);
@@ -645,9 +659,8 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_upd1_k(const float2* __res
                 const int e = threadIdx.x + i * THREADS;
                 if (e < P * P) {
                     const int x = e / P, y = e - (e / P) * P;
-                    const float2 p = cmulc(__ldg(xs + e), pl[x * PP + y]);
-                    acc[i].x += p.x;
-                    acc[i].y += p.y;
+                    const float2 xv = __ldg(xs + e), kv = pl[x * PP + y];
+                    cmacc(acc[i].x, acc[i].y, xv.x, xv.y, kv.x, kv.y);
                 }
             }
         }
@@ -833,11 +846,15 @@ __global__ void __launch_bounds__(SS_THREADS, 1) cmac_ss_k(const float2* __restr
                 const float4 sv = sst[((buf * TA + b) * IC + rr) * (SB / 2) + lane];
 #pragma unroll
                 for (int t = 0; t < ST; ++t) {
-                    const float2 p0 = CONJ ? cmulc(make_float2(sv.x, sv.y), make_float2(kv[rr][t].x, kv[rr][t].y))
-                                           : cmul(make_float2(sv.x, sv.y), make_float2(kv[rr][t].x, kv[rr][t].y));
-                    const float2 p1 = CONJ ? cmulc(make_float2(sv.z, sv.w), make_float2(kv[rr][t].z, kv[rr][t].w))
-                                           : cmul(make_float2(sv.z, sv.w), make_float2(kv[rr][t].z, kv[rr][t].w));
-                    acc[b][t].x += p0.x, acc[b][t].y += p0.y, acc[b][t].z += p1.x, acc[b][t].w += p1.y;
+                    const float4 k = kv[rr][t];
+                    float4& a = acc[b][t];
+                    if (CONJ) {
+                        cmacc(a.x, a.y, sv.x, sv.y, k.x, k.y);
+                        cmacc(a.z, a.w, sv.z, sv.w, k.z, k.w);
+                    } else {
+                        cmac(a.x, a.y, sv.x, sv.y, k.x, k.y);
+                        cmac(a.z, a.w, sv.z, sv.w, k.z, k.w);
+                    }
                 }
             }
         __syncthreads();  // the buffer is refilled two chunks later
@@ -903,9 +920,8 @@ __global__ void __launch_bounds__(SS_THREADS, 1) cmac_upd_ss_k(const float2* __r
         for (int a = 0; a < TUO; ++a)
 #pragma unroll
             for (int c = 0; c < TUI; ++c) {
-                const float2 p0 = cmulc(make_float2(xv[c].x, xv[c].y), make_float2(gv[a].x, gv[a].y));
-                const float2 p1 = cmulc(make_float2(xv[c].z, xv[c].w), make_float2(gv[a].z, gv[a].w));
-                acc[a][c].x += p0.x, acc[a][c].y += p0.y, acc[a][c].z += p1.x, acc[a][c].w += p1.y;
+                cmacc(acc[a][c].x, acc[a][c].y, xv[c].x, xv[c].y, gv[a].x, gv[a].y);
+                cmacc(acc[a][c].z, acc[a][c].w, xv[c].z, xv[c].w, gv[a].z, gv[a].w);
             }
     }
     if (!wok) return;
