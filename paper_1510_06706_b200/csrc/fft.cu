@@ -777,7 +777,7 @@ constexpr int TA = 8;  // patches per CTA in the fwd / bwd CMAC
 // staged IC reduction steps at a time with cp.async (double buffered); the
 // per-edge kernel spectra K stream from HBM exactly once, a whole chunk of
 // 16-byte loads issued before its FMAs.
-constexpr int SB = 64, SW = 8, ST = 2, IC = 8;
+constexpr int SB = 64, SW = 8, ST = 2, IC = 4;
 constexpr int SS_THREADS = SW * 32;
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -789,7 +789,7 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <bool CONJ>
-__global__ void __launch_bounds__(SS_THREADS, 1) cmac_ss_k(const float2* __restrict__ S, const float2* __restrict__ K,
+__global__ void __launch_bounds__(SS_THREADS, 2) cmac_ss_k(const float2* __restrict__ S, const float2* __restrict__ K,
                                                            float2* __restrict__ O, int B, int nr, int nn, int64_t kn,
                                                            int64_t kr, int64_t bins) {
     extern __shared__ float4 sst[];  // [2][TA][IC][SB/2] float4 (2 bins each)
@@ -870,11 +870,13 @@ __global__ void __launch_bounds__(SS_THREADS, 1) cmac_ss_k(const float2* __restr
 
 // upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]) — a rank-B update per bin,
 // bound by writing dK once. A CTA owns SB = 64 bins (2 per lane) x a 16 o x
-// 16 i block; X[b][i-block] and G[b][o-block] of its bins are staged in
-// shared memory (cp.async) and each thread accumulates 4 o x 8 i x 2 bins.
+// 8 i block; X[b][i-block] and G[b][o-block] of its bins are staged in
+// shared memory (cp.async) and each thread accumulates 4 o x 4 i x 2 bins.
+// Two CTAs per SM (<= 128 registers, 96 KB of staging at B = 8), so one
+// CTA's staging and dK stores overlap the other's FMAs.
 // Grid: (i, o) blocks of one bin block adjacent, so X / G stay in L2.
-constexpr int UO = 16, UI = 16, TUO = 4, TUI = 8;  // 256 threads = (UO/TUO) x (UI/TUI) x 32 lanes
-__global__ void __launch_bounds__(SS_THREADS, 1) cmac_upd_ss_k(const float2* __restrict__ X,
+constexpr int UO = 16, UI = 8, TUO = 4, TUI = 4;  // 256 threads = (UO/TUO) x (UI/TUI) x 32 lanes
+__global__ void __launch_bounds__(SS_THREADS, 2) cmac_upd_ss_k(const float2* __restrict__ X,
                                                                const float2* __restrict__ G, float2* __restrict__ DK,
                                                                int B, int f, int fo, int64_t bins) {
     extern __shared__ float4 sst[];  // X: [B][UI][SB/2], then G: [B][UO][SB/2]
@@ -1244,8 +1246,8 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     }
     // kernel gradient: one gradient-specific inverse per edge, sampled at s*w
     {
-        require(nB <= 16, "fft cmac_upd: batch per GPU > 16 (shared-memory staging)");
         const size_t smem = sizeof(float4) * size_t(nB * (UI + UO) * (SB / 2));
+        require(smem <= 227 * 1024, "fft cmac_upd: batch per GPU > 18 (shared-memory staging)");
         const dim3 gu(unsigned(ceil_div(c.f_in, UI) * ceil_div(c.f_out, UO)), unsigned(ceil_div(p.bins, SB)), 1u);
         allow_smem(cmac_upd_ss_k, smem);
         cmac_upd_ss_k<<<gu, SS_THREADS, smem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
