@@ -38,25 +38,63 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
     const float* xm = x + map * (int64_t(nx) * ny * nz);
     const int64_t orow = map * (int64_t(mx) * my * mz) + (int64_t(i) * my + j) * mz;
     const int dx = sx * ny * nz, dy = sy * nz;
-    for (int l = threadIdx.x; l < mz; l += ZL) {
-        const int base = (i * ny + j) * nz + l;
-        int best_idx = base;
-        float best = __ldg(xm + base);
+    const int rbase = (i * ny + j) * nz;
+    const float* xr = xm + rbase;
+    float* yr = y + orow;
+    int32_t* mr = mask + orow;
+    if constexpr (KX > 0) {
+        // one 64-bit pointer per window row (a, b), advanced along z: the
+        // loads need no per-element 64-bit index arithmetic
+        const float* q[KX][KY];
 #pragma unroll
-        for (int a = 0; a < kx; ++a)
+        for (int a = 0; a < KX; ++a)
 #pragma unroll
-            for (int b = 0; b < ky; ++b)
+            for (int b = 0; b < KY; ++b) q[a][b] = xr + a * dx + b * dy + threadIdx.x;
+        for (int l = threadIdx.x; l < mz; l += ZL) {
+            float v[KX][KY][KZ];
 #pragma unroll
-                for (int c = 0; c < kz; ++c) {
-                    const int idx = base + a * dx + b * dy + c * sz;
-                    const float v = __ldg(xm + idx);
-                    if (v > best) {  // strict: ties keep the lexicographically first source
-                        best = v;
-                        best_idx = idx;
+            for (int a = 0; a < KX; ++a)
+#pragma unroll
+                for (int b = 0; b < KY; ++b)
+#pragma unroll
+                    for (int c = 0; c < KZ; ++c) v[a][b][c] = __ldg(q[a][b] + c * sz);
+            float best = v[0][0][0];
+            int best_off = 0;
+#pragma unroll
+            for (int a = 0; a < KX; ++a)
+#pragma unroll
+                for (int b = 0; b < KY; ++b)
+#pragma unroll
+                    for (int c = 0; c < KZ; ++c)
+                        if (v[a][b][c] > best) {  // strict: ties keep the lexicographically first source
+                            best = v[a][b][c];
+                            best_off = a * dx + b * dy + c * sz;
+                        }
+            __stcs(yr + l, best);
+            __stcs(mr + l, rbase + l + best_off);
+#pragma unroll
+            for (int a = 0; a < KX; ++a)
+#pragma unroll
+                for (int b = 0; b < KY; ++b) q[a][b] += ZL;
+        }
+    } else {
+        for (int l = threadIdx.x; l < mz; l += ZL) {
+            const int base = rbase + l;
+            int best_idx = base;
+            float best = __ldg(xm + base);
+            for (int a = 0; a < kx; ++a)
+                for (int b = 0; b < ky; ++b)
+                    for (int c = 0; c < kz; ++c) {
+                        const int idx = base + a * dx + b * dy + c * sz;
+                        const float v = __ldg(xm + idx);
+                        if (v > best) {  // strict: ties keep the lexicographically first source
+                            best = v;
+                            best_idx = idx;
+                        }
                     }
-                }
-        __stcs(y + orow + l, best);
-        __stcs(mask + orow + l, best_idx);
+            __stcs(yr + l, best);
+            __stcs(mr + l, best_idx);
+        }
     }
 }
 
@@ -117,6 +155,77 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
             }
         }
         __stcs(drow + tl, acc);
+    }
+}
+
+// Backward of the 2^3 max-filter with x-stride SX (1 or 2): a thread owns one
+// (y, z) column of the input and walks its x-planes; output plane oi's
+// window-row (mask, g) pairs are loaded once (one plane ahead of use) and
+// serve input planes oi and oi + SX, half the loads of maxfilter_bwd_k.
+// Block = 32 z-lanes x 8 y-rows, grid = (y tiles, maps). Sums in ascending
+// window order like maxfilter_bwd_k.
+template <int SX>
+__global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restrict__ g,
+                                                            const int32_t* __restrict__ mask, int nx, int ny,
+                                                            int nz, int mx, int my, int mz, int sy, int sz,
+                                                            float* __restrict__ dx) {
+    const int tj = blockIdx.x * YR + threadIdx.y;
+    if (tj >= ny) return;
+    const int64_t map = blockIdx.y;
+    const int64_t pin = int64_t(ny) * nz, pout = int64_t(my) * mz;
+    const float* gm = g + map * (pout * mx);
+    const int32_t* mm = mask + map * (pout * mx);
+    float* dm = dx + map * (pin * nx);
+    for (int tl = threadIdx.x; tl < nz; tl += ZL) {
+        // window rows (b, c) in descending order = ascending output index
+        int roff[4];
+        bool rok[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int b = 1 - (q >> 1), c = 1 - (q & 1);
+            const int oj = tj - sy * b, ol = tl - sz * c;
+            rok[q] = oj >= 0 && oj < my && ol >= 0 && ol < mz;
+            roff[q] = rok[q] ? oj * mz + ol : 0;
+        }
+        // ring[k]: (mask, g) of output plane ti - SX + k, k <= SX + 1 (the
+        // last one is the next iteration's plane, loaded a plane ahead)
+        int rm[SX + 2][4];
+        float rg[SX + 2][4];
+#pragma unroll
+        for (int k = 0; k < SX; ++k)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rm[k][q] = -1, rg[k][q] = 0.f;
+        const int32_t* mp = mm;
+        const float* gp = gm;
+        auto fetch = [&](int oi, int slot) {
+            const bool pok = oi < mx;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool ok = pok && rok[q];
+                rm[slot][q] = ok ? __ldg(mp + roff[q]) : -1;
+                rg[slot][q] = ok ? __ldg(gp + roff[q]) : 0.f;
+            }
+            mp += pout;
+            gp += pout;
+        };
+        fetch(0, SX);
+        float* dp = dm + tj * nz + tl;
+        int tr = tj * nz + tl;
+        for (int ti = 0; ti < nx; ++ti) {
+            fetch(ti + 1, SX + 1);
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += (rm[0][q] == tr) ? rg[0][q] : 0.f;  // a = 1: plane ti - SX
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += (rm[SX][q] == tr) ? rg[SX][q] : 0.f;  // a = 0: plane ti
+            __stcs(dp, acc);
+            dp += pin;
+            tr += int(pin);
+#pragma unroll
+            for (int k = 0; k <= SX; ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rm[k][q] = rm[k + 1][q], rg[k][q] = rg[k + 1][q];
+        }
     }
 }
 
@@ -184,6 +293,14 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
 void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
                    dims3 k, dims3 s, float* dx) {
     const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
+    if (k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2) && maps < 65536) {
+        const dim3 grid(unsigned(ceil_div(n.y, YR)), unsigned(maps));
+        auto* kk = s.x == 1 ? maxfilter2_bwd_k<1> : maxfilter2_bwd_k<2>;
+        kk<<<grid, vblock(), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
+                                      int(s.y), int(s.z), dx);
+        launch_check("maxfilter_bwd");
+        return;
+    }
     auto* kb = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_bwd_k<2, 2, 2>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_bwd_k<1, 2, 2>
                                                     : maxfilter_bwd_k<0, 0, 0>;
