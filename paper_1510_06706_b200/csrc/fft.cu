@@ -184,10 +184,20 @@ __device__ __forceinline__ void dft_r(float2* v, const float2* tw) {
 // and does an R2-point DFT in registers; twiddle W_P^(n1 k2); one exchange
 // through the line's shared buffer xb (P complex); then R1-point DFTs in
 // registers for k2 = t, t + 8, ..., and emit(k2 + R2 k1, X) for every output.
+__host__ __device__ constexpr int line_r1(int P) { return (P % 8 == 0) ? 8 : ((P % 4 == 0) ? 4 : 2); }
+// Exchange-buffer layout: group k2 of R1 values at k2 * (R1 + 1) (the
+// transposed reads of thread t, xb[t * (R1 + 1) + n1], hit distinct banks)
+// and a line pitch = 8 mod 16 float2, so the two lines of a half-warp (one
+// 64-bit shared-memory wavefront) use disjoint bank halves.
+__host__ __device__ constexpr int xpitch(int P) {
+    const int v = (P / line_r1(P)) * (line_r1(P) + 1);
+    return v <= 8 ? 8 : ((v - 8 + 15) / 16) * 16 + 8;
+}
 template <int P>
 struct line_shape {
-    static constexpr int R1 = (P % 8 == 0) ? 8 : ((P % 4 == 0) ? 4 : 2);
+    static constexpr int R1 = line_r1(P);
     static constexpr int R2 = P / R1;
+    static constexpr int XP = xpitch(P);
 };
 
 template <int P, bool INV, typename Emit>
@@ -196,14 +206,14 @@ __device__ __forceinline__ void line_fft(float2* v, float2* xb, const float2* tw
     if (t < R1) {
         dft_r<R2, P, INV>(v, tw);
 #pragma unroll
-        for (int k2 = 0; k2 < R2; ++k2) xb[k2 * R1 + t] = (k2 == 0) ? v[k2] : cmul(v[k2], twid<P, INV>(tw, t * k2));
+        for (int k2 = 0; k2 < R2; ++k2) xb[k2 * (R1 + 1) + t] = (k2 == 0) ? v[k2] : cmul(v[k2], twid<P, INV>(tw, t * k2));
     }
     __syncwarp();
 #pragma unroll
     for (int k2 = t; k2 < R2; k2 += TPL) {
         float2 w[R1];
 #pragma unroll
-        for (int n1 = 0; n1 < R1; ++n1) w[n1] = xb[k2 * R1 + n1];
+        for (int n1 = 0; n1 < R1; ++n1) w[n1] = xb[k2 * (R1 + 1) + n1];
         dft_r<R1, P, INV>(w, tw);
 #pragma unroll
         for (int k1 = 0; k1 < R1; ++k1) emit(k2 + R2 * k1, w[k1]);
@@ -223,7 +233,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
     __shared__ int64_t obase[LINES];
     float2* tw = sm;                   // P
     float2* xbuf = tw + P;             // LINES x P
-    float2* stash = xbuf + LINES * P;  // LINES x (Zh + 1)
+    float2* stash = xbuf + LINES * line_shape<P>::XP;  // LINES x (Zh + 1)
     fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     const int64_t line = int64_t(blockIdx.x) * LINES + l;
@@ -247,7 +257,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
     }
     __syncthreads();  // twiddles
     float2* st = stash + l * (Zh + 1);
-    line_fft<P, false>(v, xbuf + l * P, tw, t, [&](int k, float2 val) {
+    line_fft<P, false>(v, xbuf + l * line_shape<P>::XP, tw, t, [&](int k, float2 val) {
         if (k < Zh) st[k] = val;
     });
     __syncthreads();
@@ -270,8 +280,8 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_k(float2* __restrict__ spe
     extern __shared__ float2 sm[];
     float2* twy = sm;                 // PY
     float2* twx = twy + PY;           // PX
-    float2* xbuf = twx + PX;          // LINES x max(PX, PY)
-    constexpr int PM = PX > PY ? PX : PY;
+    float2* xbuf = twx + PX;          // LINES x max exchange pitch
+    constexpr int PM = line_shape<PX>::XP > line_shape<PY>::XP ? line_shape<PX>::XP : line_shape<PY>::XP;
     float2* pl = xbuf + LINES * PM;   // [PX][PYP]
     const int64_t q = blockIdx.x + int64_t(blockIdx.y) * gridDim.x;
     if (q >= planes) return;  // uniform per CTA
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_k(const float2* __restrict
     float2* twy = sm;
     float2* twx = twy + PY;
     float2* xbuf = twx + PX;
-    constexpr int PM = PX > PY ? PX : PY;
+    constexpr int PM = line_shape<PX>::XP > line_shape<PY>::XP ? line_shape<PX>::XP : line_shape<PY>::XP;
     float2* pl = xbuf + LINES * PM;
     const int64_t q = blockIdx.x + int64_t(blockIdx.y) * gridDim.x;
     if (q >= planes) return;
@@ -418,11 +428,11 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_pipe_k(const float2* __res
     extern __shared__ float2 sm[];
     float2* tw = sm;                       // P
     float2* xbuf = tw + P;                 // LINES x P
-    float2* plb0 = xbuf + LINES * P;       // [P][PP]
+    float2* plb0 = xbuf + LINES * line_shape<P>::XP;       // [P][PP]
     float2* plb1 = plb0 + P * PP;
     fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* xb = xbuf + l * P;
+    float2* xb = xbuf + l * line_shape<P>::XP;
     auto issue = [&](int64_t qq, float2* dst) {
         if (qq < planes) {
             const float2* g = spec + qq * (int64_t(P) * P);
@@ -478,11 +488,11 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_pipe_k(float2* __restrict_
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* xbuf = tw + P;
-    float2* plb0 = xbuf + LINES * P;
+    float2* plb0 = xbuf + LINES * line_shape<P>::XP;
     float2* plb1 = plb0 + P * PP;
     fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* xb = xbuf + l * P;
+    float2* xb = xbuf + l * line_shape<P>::XP;
     auto issue = [&](int64_t qq, float2* dst) {  // the valid nx x ny region written by the z pass
         if (qq < planes) {
             const float2* g = spec + qq * (int64_t(P) * P);
@@ -554,10 +564,10 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_mul1_k(const float2* __res
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* xbuf = tw + P;
-    float2* pl = xbuf + LINES * P;  // [P][PP]
+    float2* pl = xbuf + LINES * line_shape<P>::XP;  // [P][PP]
     fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* xb = xbuf + l * P;
+    float2* xb = xbuf + l * line_shape<P>::XP;
     for (int64_t q = blockIdx.x; q < planes; q += gridDim.x) {
         const int64_t img = q / Zh;
         const int zb = int(q - img * Zh);
@@ -612,10 +622,10 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_upd1_k(const float2* __res
     extern __shared__ float2 sm[];
     float2* tw = sm;
     float2* xbuf = tw + P;
-    float2* pl = xbuf + LINES * P;
+    float2* pl = xbuf + LINES * line_shape<P>::XP;
     fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* xb = xbuf + l * P;
+    float2* xb = xbuf + l * line_shape<P>::XP;
     for (int64_t q = blockIdx.x; q < planes; q += gridDim.x) {  // q = o * Zh + zb
         const int64_t o = q / Zh;
         const int zb = int(q - o * Zh);
@@ -696,7 +706,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
     __shared__ float bvals[LINES];
     float2* tw = sm;
     float2* xbuf = tw + P;
-    float2* stash = xbuf + LINES * P;  // LINES x (Zh + 1)
+    float2* stash = xbuf + LINES * line_shape<P>::XP;  // LINES x (Zh + 1)
     fill_twiddles<P>(tw);
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     const int64_t line = int64_t(blockIdx.x) * LINES + l;
@@ -737,7 +747,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
     }
     float* dst = out + (ok ? obase[l] : 0);
     const float bv = ok ? bvals[l] : 0.f;
-    line_fft<P, true>(v, xbuf + l * P, tw, t, [&](int k, float2 val) {
+    line_fft<P, true>(v, xbuf + l * line_shape<P>::XP, tw, t, [&](int k, float2 val) {
         const int q = k / g.z_step;
         if (ok && q * g.z_step == k && q < g.z_cnt) {
             float r = val.x * g.scale + bv;
@@ -976,10 +986,10 @@ dims3 pads_for(const conv_shape& c) {
 }
 
 // z passes: twiddles + per-line exchange buffers + the half-spectrum stash
-size_t smem_for(int P) { return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(P) + size_t(LINES) * size_t(P / 2 + 2)); }
+size_t smem_for(int P) { return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(xpitch(P)) + size_t(LINES) * size_t(P / 2 + 2)); }
 // xy passes: twiddles + exchange buffers + the [PX][PY+1] plane
 size_t smem_xy(int PX, int PY) {
-    const int PM = PX > PY ? PX : PY;
+    const int PM = xpitch(PX) > xpitch(PY) ? xpitch(PX) : xpitch(PY);
     return sizeof(float2) * (size_t(PX + PY) + size_t(LINES) * size_t(PM) + size_t(PX) * size_t(PY + 1));
 }
 
@@ -1005,7 +1015,7 @@ void dispatch_pad(int P, F&& f) {
 
 // persistent double-buffered xy passes: twiddles + exchange buffers + 2 planes
 size_t smem_pipe(int P) {
-    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(P) + 2 * size_t(P) * size_t(P + 2));
+    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(xpitch(P)) + 2 * size_t(P) * size_t(P + 2));
 }
 // as many CTAs as fit on the 148 SMs at once (never more than planes)
 unsigned pipe_grid(int64_t planes, size_t smem) {
@@ -1126,7 +1136,7 @@ bool fused1_ok(const plan& p, const conv_shape& c) {
     return c.f_in == 1 && p.P.x == p.P.y && p.P.x > 1 && p.P.x <= 96 && !std::getenv("ZNN_FFT_NOFUSE1");
 }
 size_t smem_plane1(int P) {
-    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(P) + size_t(P) * size_t(P + 2));
+    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(xpitch(P)) + size_t(P) * size_t(P + 2));
 }
 
 float2* carve(char*& cur, int64_t count) {
