@@ -760,19 +760,17 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
 }
 
 // dilated kernels: dil[e][f_in][s*w] = w[e][f_in][w], zeros elsewhere (conv_direct.hpp:137-151)
-__global__ void dilate_k(const float* __restrict__ w, int64_t nker, int kx, int ky, int kz, int sx, int sy, int sz,
+// dilated kernels [nker][ex][ey][ez]: the volume is zeroed by a memset, then
+// one thread per tap (coalesced reads of w) scatters it to its lattice site
+__global__ void dilate_k(const float* __restrict__ w, int64_t ntaps, int kx, int ky, int kz, int sx, int sy, int sz,
                          float* __restrict__ dil) {
     const int ex = sx * (kx - 1) + 1, ey = sy * (ky - 1) + 1, ez = sz * (kz - 1) + 1;
-    const int64_t ev = int64_t(ex) * ey * ez;
-    const int64_t total = nker * ev;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t kk = i < (int64_t(1) << 32) ? int64_t(uint32_t(i) / uint32_t(ev)) : i / ev;
-        const int r = int(i - kk * ev);
-        const int x = r / (ey * ez), y = (r / ez) % ey, z = r % ez;
-        float v = 0.f;
-        if (x % sx == 0 && y % sy == 0 && z % sz == 0)
-            v = w[kk * (int64_t(kx) * ky * kz) + ((x / sx) * ky + y / sy) * kz + z / sz];
-        dil[i] = v;
+    const int T = kx * ky * kz;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < ntaps; i += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t kk = i / T;
+        const int t = int(i - kk * T);
+        const int wx = t / (ky * kz), r = t - wx * (ky * kz), wy = r / kz, wz = r - wy * kz;
+        dil[((kk * ex + sx * wx) * ey + sy * wy) * int64_t(ez) + sz * wz] = __ldg(w + i);
     }
 }
 
@@ -1179,10 +1177,10 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X);
     p.cnt.fwd_image += c.B * c.f_in;
     // kernel spectra of the dilated kernels (memoised for the backward pass)
-    int64_t blocks = ceil_div(nker * e.vol(), 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    dilate_k<<<unsigned(blocks), 256, 0, st>>>(w, nker, int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y),
-                                               int(c.s.z), p.dil);
+    ZNN_CUDA_CHECK(cudaMemsetAsync(p.dil, 0, sizeof(float) * size_t(nker * e.vol()), st));
+    const int64_t ntaps = nker * c.k.vol();
+    dilate_k<<<unsigned(std::min<int64_t>(ceil_div(ntaps, 256), 148 * 16)), 256, 0, st>>>(
+        w, ntaps, int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y), int(c.s.z), p.dil);
     launch_check("fft_dilate");
     forward3d(st, p, p.dil, e.vol(), e, nker, p.K);
     p.cnt.fwd_kernel += nker;
