@@ -38,7 +38,7 @@ constexpr int THREADS = 256;  // 8 threads per line
 constexpr int TPL = THREADS / LINES;
 constexpr int MAXP = 128;
 // pad sizes with compiled transforms (2^a 3^b, every stage radix 4, 2 or 3)
-constexpr int kPads[] = {2, 4, 8, 12, 16, 24, 32, 48, 64, 72, 96, 128};
+constexpr int kPads[] = {2, 4, 8, 12, 16, 20, 24, 32, 40, 48, 64, 72, 80, 96, 128};
 
 // smallest compiled pad >= n
 int64_t good_size(int64_t n) {
@@ -110,6 +110,30 @@ __device__ __forceinline__ void dft_small(float2* v) {
             v[1] = make_float2(t1.x - t3.y, t1.y + t3.x);
             v[3] = make_float2(t1.x + t3.y, t1.y - t3.x);
         }
+    } else if constexpr (R == 5) {
+        // X1,4 = a1 -/+ i b1, X2,3 = a2 -/+ i b2 (signs of i flipped for the inverse)
+        const float c1 = 0.30901699437494745f, c2 = -0.8090169943749473f;
+        const float s1 = 0.9510565162951535f, s2 = 0.5877852522924732f;
+        const float2 t1 = make_float2(v[1].x + v[4].x, v[1].y + v[4].y);
+        const float2 t2 = make_float2(v[2].x + v[3].x, v[2].y + v[3].y);
+        const float2 t3 = make_float2(v[1].x - v[4].x, v[1].y - v[4].y);
+        const float2 t4 = make_float2(v[2].x - v[3].x, v[2].y - v[3].y);
+        const float2 a1 = make_float2(v[0].x + c1 * t1.x + c2 * t2.x, v[0].y + c1 * t1.y + c2 * t2.y);
+        const float2 a2 = make_float2(v[0].x + c2 * t1.x + c1 * t2.x, v[0].y + c2 * t1.y + c1 * t2.y);
+        const float2 b1 = make_float2(s1 * t3.x + s2 * t4.x, s1 * t3.y + s2 * t4.y);
+        const float2 b2 = make_float2(s2 * t3.x - s1 * t4.x, s2 * t3.y - s1 * t4.y);
+        v[0] = make_float2(v[0].x + t1.x + t2.x, v[0].y + t1.y + t2.y);
+        if (!INV) {  // -i b = (b.y, -b.x)
+            v[1] = make_float2(a1.x + b1.y, a1.y - b1.x);
+            v[4] = make_float2(a1.x - b1.y, a1.y + b1.x);
+            v[2] = make_float2(a2.x + b2.y, a2.y - b2.x);
+            v[3] = make_float2(a2.x - b2.y, a2.y + b2.x);
+        } else {
+            v[1] = make_float2(a1.x - b1.y, a1.y + b1.x);
+            v[4] = make_float2(a1.x + b1.y, a1.y - b1.x);
+            v[2] = make_float2(a2.x - b2.y, a2.y + b2.x);
+            v[3] = make_float2(a2.x + b2.y, a2.y - b2.x);
+        }
     } else {  // R == 3
         const float s = 0.8660254037844386f;
         const float2 a = v[0], b = v[1], c = v[2];
@@ -145,17 +169,17 @@ __device__ __forceinline__ float2 twid(const float2* tw, int m) {
     return w;
 }
 
-// DFT of R points held in registers (R in {1,2,3,4,6,8,9,12,16}); composite
+// DFT of R points held in registers (R in {1,2,3,4,5,6,8,9,10,12,15,16,...}); composite
 // sizes are split R = A*B in registers (n = a + A b, k = kb + B ka) with
 // twiddles W_R^(a kb) = W_P^(a kb P/R) from the line's table.
 template <int R, int P, bool INV>
 __device__ __forceinline__ void dft_r(float2* v, const float2* tw) {
     if constexpr (R == 1) {
         return;
-    } else if constexpr (R == 2 || R == 3 || R == 4 || R == 8) {
+    } else if constexpr (R == 2 || R == 3 || R == 4 || R == 5 || R == 8) {
         dft_small<R, INV>(v);
     } else {
-        constexpr int A = (R % 4 == 0) ? 4 : ((R % 3 == 0) ? 3 : 2);
+        constexpr int A = (R % 4 == 0) ? 4 : ((R % 3 == 0) ? 3 : ((R % 2 == 0) ? 2 : 5));
         constexpr int B = R / A;
         float2 t[R];
 #pragma unroll
@@ -969,7 +993,7 @@ void pad_dims(const plan& p, int64_t out[3]) { out[0] = p.P.x, out[1] = p.P.y, o
 
 namespace {
 
-constexpr int64_t kMaxSpectrumBytes = int64_t(24) << 30;  // kernel spectra budget per layer
+constexpr int64_t kMaxSpectrumBytes = int64_t(32) << 30;  // kernel spectra budget per layer (c5 conv3 at P = 80: 30.2 GB)
 
 int64_t pad_axis(int64_t n) { return n <= 1 ? 1 : good_size(n); }
 
@@ -1000,11 +1024,14 @@ void dispatch_pad(int P, F&& f) {
         case 8: f(std::integral_constant<int, 8>{}); break;
         case 12: f(std::integral_constant<int, 12>{}); break;
         case 16: f(std::integral_constant<int, 16>{}); break;
+        case 20: f(std::integral_constant<int, 20>{}); break;
         case 24: f(std::integral_constant<int, 24>{}); break;
         case 32: f(std::integral_constant<int, 32>{}); break;
+        case 40: f(std::integral_constant<int, 40>{}); break;
         case 48: f(std::integral_constant<int, 48>{}); break;
         case 64: f(std::integral_constant<int, 64>{}); break;
         case 72: f(std::integral_constant<int, 72>{}); break;
+        case 80: f(std::integral_constant<int, 80>{}); break;
         case 96: f(std::integral_constant<int, 96>{}); break;
         case 128: f(std::integral_constant<int, 128>{}); break;
         default: throw znn_gpu::shape_error("fft: no compiled transform for pad " + std::to_string(P));

@@ -21,6 +21,9 @@ CASES = [
     (1, 4, 3, (16, 12, 14), (4, 3, 2), (2, 2, 3)),
     (2, 5, 6, (1, 17, 19), (1, 5, 5), (1, 2, 2)),   # 2-D: x = 1
     (1, 2, 2, (20, 18, 16), (7, 7, 7), (2, 2, 2)),
+    (1, 1, 2, (19, 17, 18), (3, 3, 3), (1, 1, 1)),   # pads 20 (radix 4 x 5)
+    (1, 2, 1, (37, 39, 33), (5, 5, 5), (2, 2, 2)),   # pads 40 (8 x 5)
+    (1, 1, 1, (75, 70, 66), (5, 5, 5), (4, 4, 4)),   # xy pad 80 (8 x 10 = 8 x 2 x 5)
 ]
 
 

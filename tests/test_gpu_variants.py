@@ -93,3 +93,38 @@ def test_fft_large_pads(ctx, shape):
     for o in range(fo):
         ref = sum(O.conv_valid(x[0, i], w[o, i], s) for i in range(fi))
         assert O.max_rel_error(y[0, o], ref) < FWD_TOL
+
+
+@pytest.mark.parametrize("od", [(26, 25, 12), (4, 3, 65)], ids=["pads40x40x20", "pads12x12x80"])
+def test_fft_radix5_pads_backward(ctx, od):
+    """One SGD step of a net whose FFT layer has pads with a factor 5 (20, 40,
+    80), data and weight gradients included, against the double oracle. The
+    FFT layer (3 -> 2 maps, 5^3 sparsity 2) is the second conv, so its input
+    gradient is needed."""
+    from paper_1510_06706_b200 import Net
+    spec = ("[node in] role=input\n"
+            + "".join(f"[node h{i}]\n[node t{i}]\n" for i in range(3))
+            + "[node o0] role=output\n[node o1] role=output\n"
+            + "".join(f"[edge c{i}] from=in to=h{i} type=conv kernel=1,1,1\n" for i in range(3))
+            + "".join(f"[edge t{i}] from=h{i} to=t{i} type=transfer fn=tanh\n" for i in range(3))
+            + "".join(f"[edge e{i}{j}] from=t{i} to=o{j} type=conv kernel=5,5,5 sparsity=2,2,2\n"
+                      for i in range(3) for j in range(2)))
+    n = tuple(d + 8 for d in od)
+    B = 2
+    net = Net(ctx, spec, od, batch=B, loss="l2", lr=0.01)
+    net.set_layer_engine(1, "fft")
+    rng = np.random.default_rng(17)
+    params = rng.uniform(-0.3, 0.3, size=net.num_params).astype(np.float32)
+    net.set_params(params)
+    x = rng.uniform(0, 1, size=(B, 1) + n).astype(np.float32)
+    lab = rng.uniform(0, 1, size=(B, 2) + od).astype(np.float32)
+    loss = net.forward_backward(cuda(x), cuda(lab))
+    grads = net.get_gradients()
+    net.apply_update()
+    g = O.parse_netspec(spec, od)
+    rl, rg, rp, _ = O.train_step(g, params.astype(np.float64), np.zeros(params.size),
+                                 [[x[b, 0]] for b in range(B)], [[lab[b, o] for o in range(2)] for b in range(B)],
+                                 0.01, 0.0, "l2")
+    assert abs(loss - rl) / (abs(rl) + 1) < FWD_TOL
+    assert O.max_rel_error(grads, rg) < GRAD_TOL
+    assert O.max_rel_error(net.get_params(), rp) < GRAD_TOL
