@@ -827,9 +827,12 @@ __global__ void __launch_bounds__(SS_THREADS, 2) cmac_ss_k(const float2* __restr
     extern __shared__ float4 sst[];  // [2][TA][IC][SB/2] float4 (2 bins each)
     constexpr int UNITS = TA * IC * (SB / 2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t w0 = int64_t(blockIdx.y) * SB;   // n blocks of one bin block are adjacent: S stays in L2
-    const int n0 = blockIdx.x * (SW * ST) + warp * ST;
-    const int b0 = blockIdx.z * TA;
+    // patch blocks of one (n block, bin block) are adjacent in the grid, then
+    // the n blocks of one bin block: K and S are re-read from L2, not HBM
+    const int nbb = (B + TA - 1) / TA;
+    const int64_t w0 = int64_t(blockIdx.y) * SB;
+    const int n0 = int(blockIdx.x / nbb) * (SW * ST) + warp * ST;
+    const int b0 = int(blockIdx.x % nbb) * TA;
     const int64_t wl = w0 + 2 * lane;  // this lane's two bins
     const bool wok = wl < bins;        // bins is even
     auto stage = [&](int c, int buf) {
@@ -900,18 +903,22 @@ __global__ void __launch_bounds__(SS_THREADS, 2) cmac_ss_k(const float2* __restr
                 *reinterpret_cast<float4*>(O + (int64_t(b0 + b) * nn + n0 + t) * bins + wl) = acc[b][t];
 }
 
-// upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]) — a rank-B update per bin,
-// bound by writing dK once. A CTA owns SB = 64 bins (2 per lane) x a 16 o x
-// 8 i block; X[b][i-block] and G[b][o-block] of its bins are staged in
-// shared memory (cp.async) and each thread accumulates 4 o x 4 i x 2 bins.
-// Two CTAs per SM (<= 128 registers, 96 KB of staging at B = 8), so one
-// CTA's staging and dK stores overlap the other's FMAs.
+// upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]) — a rank-B update per bin.
+// A CTA owns SB = 64 bins (2 per lane) x a 16 o x 8 i block; each thread
+// accumulates 4 o x 4 i x 2 bins. X[b][i-block] and G[b][o-block] of its
+// bins stream through shared memory UB patches at a time (cp.async, double
+// buffered: 2 x 48 KB whatever B is), so two CTAs per SM overlap staging,
+// FMAs and dK stores.
 // Grid: (i, o) blocks of one bin block adjacent, so X / G stay in L2.
 constexpr int UO = 16, UI = 8, TUO = 4, TUI = 4;  // 256 threads = (UO/TUO) x (UI/TUI) x 32 lanes
+constexpr int UB = 4;                             // patches per pipeline stage
+constexpr size_t kUpdSmem = sizeof(float4) * size_t(2 * UB * (UI + UO) * (SB / 2));
 __global__ void __launch_bounds__(SS_THREADS, 2) cmac_upd_ss_k(const float2* __restrict__ X,
                                                                const float2* __restrict__ G, float2* __restrict__ DK,
                                                                int B, int f, int fo, int64_t bins) {
-    extern __shared__ float4 sst[];  // X: [B][UI][SB/2], then G: [B][UO][SB/2]
+    extern __shared__ float4 sst[];  // [2 stages][UB][UI + UO][SB/2] (X rows, then G rows)
+    constexpr int ROWS = UI + UO;
+    constexpr int STAGE = UB * ROWS * (SB / 2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nib = (f + UI - 1) / UI;
     const int ib = blockIdx.x % nib, ob = blockIdx.x / nib;
@@ -919,44 +926,59 @@ __global__ void __launch_bounds__(SS_THREADS, 2) cmac_upd_ss_k(const float2* __r
     const int64_t wl = w0 + 2 * lane;
     const bool wok = wl < bins;
     const int i_base = ib * UI, o_base = ob * UO;
-    float4* xs = sst;
-    float4* gs = sst + B * UI * (SB / 2);
-    for (int u = threadIdx.x; u < B * UI * (SB / 2); u += SS_THREADS) {
-        const int b = u / (UI * (SB / 2)), rem = u - b * (UI * (SB / 2));
-        const int ii = rem / (SB / 2), q = rem - ii * (SB / 2);
-        const int64_t w = w0 + 2 * q;
-        const bool ok = i_base + ii < f && w < bins;
-        cp_async16(xs + u, ok ? X + (int64_t(b) * f + i_base + ii) * bins + w : X, ok);
-    }
-    for (int u = threadIdx.x; u < B * UO * (SB / 2); u += SS_THREADS) {
-        const int b = u / (UO * (SB / 2)), rem = u - b * (UO * (SB / 2));
-        const int oo = rem / (SB / 2), q = rem - oo * (SB / 2);
-        const int64_t w = w0 + 2 * q;
-        const bool ok = o_base + oo < fo && w < bins;
-        cp_async16(gs + u, ok ? G + (int64_t(b) * fo + o_base + oo) * bins + w : G, ok);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    const int oq = warp / (UI / TUI), iq = warp % (UI / TUI);  // this warp's 4 o x 8 i sub-block
+    auto stage = [&](int c, int buf) {
+        for (int u = threadIdx.x; u < STAGE; u += SS_THREADS) {
+            const int bb = u / (ROWS * (SB / 2)), rem = u - bb * (ROWS * (SB / 2));
+            const int row = rem / (SB / 2), q = rem - row * (SB / 2);
+            const int b = c * UB + bb;
+            const int64_t w = w0 + 2 * q;
+            const float2* src;
+            bool ok;
+            if (row < UI) {
+                ok = b < B && i_base + row < f && w < bins;
+                src = X + (int64_t(b) * f + i_base + row) * bins + w;
+            } else {
+                ok = b < B && o_base + row - UI < fo && w < bins;
+                src = G + (int64_t(b) * fo + o_base + row - UI) * bins + w;
+            }
+            cp_async16(sst + buf * STAGE + u, ok ? src : X, ok);
+        }
+        cp_async_commit();
+    };
+    const int oq = warp / (UI / TUI), iq = warp % (UI / TUI);  // this warp's 4 o x 4 i sub-block
     float4 acc[TUO][TUI];
 #pragma unroll
     for (int a = 0; a < TUO; ++a)
 #pragma unroll
         for (int c = 0; c < TUI; ++c) acc[a][c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int b = 0; b < B; ++b) {
-        float4 gv[TUO], xv[TUI];
+    const int nchunks = (B + UB - 1) / UB;
+    stage(0, 0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nchunks) {
+            stage(c + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const float4* xs = sst + buf * STAGE;
 #pragma unroll
-        for (int a = 0; a < TUO; ++a) gv[a] = gs[(b * UO + oq * TUO + a) * (SB / 2) + lane];
+        for (int bb = 0; bb < UB; ++bb) {
+            float4 gv[TUO], xv[TUI];
 #pragma unroll
-        for (int c = 0; c < TUI; ++c) xv[c] = xs[(b * UI + iq * TUI + c) * (SB / 2) + lane];
+            for (int a = 0; a < TUO; ++a) gv[a] = xs[(bb * ROWS + UI + oq * TUO + a) * (SB / 2) + lane];
 #pragma unroll
-        for (int a = 0; a < TUO; ++a)
+            for (int c2 = 0; c2 < TUI; ++c2) xv[c2] = xs[(bb * ROWS + iq * TUI + c2) * (SB / 2) + lane];
 #pragma unroll
-            for (int c = 0; c < TUI; ++c) {
-                cmacc(acc[a][c].x, acc[a][c].y, xv[c].x, xv[c].y, gv[a].x, gv[a].y);
-                cmacc(acc[a][c].z, acc[a][c].w, xv[c].z, xv[c].w, gv[a].z, gv[a].w);
-            }
+            for (int a = 0; a < TUO; ++a)
+#pragma unroll
+                for (int c2 = 0; c2 < TUI; ++c2) {
+                    cmacc(acc[a][c2].x, acc[a][c2].y, xv[c2].x, xv[c2].y, gv[a].x, gv[a].y);
+                    cmacc(acc[a][c2].z, acc[a][c2].w, xv[c2].z, xv[c2].w, gv[a].z, gv[a].w);
+                }
+        }
+        __syncthreads();  // the buffer is refilled by the next iteration's stage
     }
     if (!wok) return;
 #pragma unroll
@@ -975,16 +997,31 @@ struct plan {
     int64_t Zh = 1, bins = 1;
     int64_t B = 0, f = 0, fo = 0;
     float2* X = nullptr;  // memo: image spectra of the layer input [B*f][bins]
-    float2* K = nullptr;  // memo: kernel spectra [fo*f][bins]
+    float2* K = nullptr;  // memo: kernel spectra [fo*f][bins] (own buffer; null when pooled)
     float* dil = nullptr; // dilated kernels [fo*f][e^3]
+    std::shared_ptr<kpool> pool;  // shared kernel-spectrum buffer (recomputed in bwd if clobbered)
+    bool k_valid = false;         // own K holds the spectra of the current weights
     transform_counts cnt;
 };
+
+kpool::~kpool() { cudaFree(buf); }
+float2* kpool::get(int64_t need) {
+    if (need > bytes) {
+        if (buf) ZNN_CUDA_CHECK(cudaFree(buf));
+        buf = nullptr;
+        ZNN_CUDA_CHECK(cudaMalloc(&buf, size_t(need)));
+        bytes = need;
+        owner = nullptr;
+    }
+    return buf;
+}
 
 void plan_deleter::operator()(plan* p) const {
     if (!p) return;
     cudaFree(p->X);
     cudaFree(p->K);
     cudaFree(p->dil);
+    if (p->pool && p->pool->owner == p) p->pool->owner = nullptr;
     delete p;
 }
 
@@ -993,7 +1030,7 @@ void pad_dims(const plan& p, int64_t out[3]) { out[0] = p.P.x, out[1] = p.P.y, o
 
 namespace {
 
-constexpr int64_t kMaxSpectrumBytes = int64_t(32) << 30;  // kernel spectra budget per layer (c5 conv3 at P = 80: 30.2 GB)
+constexpr int64_t kMaxSpectrumBytes = int64_t(64) << 30;  // kernel spectra per layer (c5 conv2 at P = 96: 52 GB)
 
 int64_t pad_axis(int64_t n) { return n <= 1 ? 1 : good_size(n); }
 
@@ -1060,7 +1097,7 @@ void cmac_ss(cudaStream_t st, const float2* S, const float2* K, float2* O, int B
              int64_t kr, int64_t bins, bool conj) {
     require(bins % 2 == 0, "fft cmac: odd bin count");
     const size_t smem = sizeof(float4) * size_t(2 * TA * IC * (SB / 2));
-    const dim3 grid(unsigned(ceil_div(nn, SW * ST)), unsigned(ceil_div(bins, SB)), unsigned(ceil_div(B, TA)));
+    const dim3 grid(unsigned(ceil_div(nn, SW * ST) * ceil_div(B, TA)), unsigned(ceil_div(bins, SB)), 1u);
     if (conj) {
         allow_smem(cmac_ss_k<true>, smem);
         cmac_ss_k<true><<<grid, SS_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
@@ -1172,16 +1209,20 @@ float2* carve(char*& cur, int64_t count) {
 
 }  // namespace
 
+int64_t kernel_spectrum_bytes(const conv_shape& c) {
+    const dims3 P = pads_for(c);
+    return c.f_in * c.f_out * P.x * P.y * (P.z / 2 + 1) * int64_t(sizeof(float2));
+}
+
 bool supported(const conv_shape& c) {
     const dims3 P = pads_for(c);
     if (P.x > MAXP || P.y > MAXP || P.z > MAXP) return false;
     if ((P.x != P.y && P.x != 1) || P.y < 2) return false;  // compiled xy planes: square, or 2-D (x = 1)
-    const int64_t bins = P.x * P.y * (P.z / 2 + 1);
-    if (c.f_in * c.f_out * bins * int64_t(sizeof(float2)) > kMaxSpectrumBytes) return false;
+    if (kernel_spectrum_bytes(c) > kMaxSpectrumBytes) return false;
     return true;
 }
 
-plan_ptr make_plan(const conv_shape& c) {
+plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool) {
     require(supported(c), "fft engine: layer unsupported (pad > 128 or spectra exceed the memory budget)");
     plan_ptr p(new plan);
     p->P = pads_for(c);
@@ -1190,27 +1231,57 @@ plan_ptr make_plan(const conv_shape& c) {
     p->B = c.B, p->f = c.f_in, p->fo = c.f_out;
     const dims3 e{c.s.x * (c.k.x - 1) + 1, c.s.y * (c.k.y - 1) + 1, c.s.z * (c.k.z - 1) + 1};
     ZNN_CUDA_CHECK(cudaMalloc(&p->X, sizeof(float2) * size_t(c.B * c.f_in * p->bins)));
-    ZNN_CUDA_CHECK(cudaMalloc(&p->K, sizeof(float2) * size_t(c.f_out * c.f_in * p->bins)));
+    p->pool = std::move(pool);
+    if (!p->pool) ZNN_CUDA_CHECK(cudaMalloc(&p->K, sizeof(float2) * size_t(c.f_out * c.f_in * p->bins)));
     ZNN_CUDA_CHECK(cudaMalloc(&p->dil, sizeof(float) * size_t(c.f_out * c.f_in * e.vol())));
     return p;
 }
 
-void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
-              int act, float* y, znn_gpu::scratch& ws) {
-    require(p.B == c.B && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
+namespace {
+
+// the kernel-spectrum buffer of a plan (own, or the shared pool's)
+float2* kbuf(plan& p) {
+    return p.pool ? p.pool->get(int64_t(sizeof(float2)) * p.f * p.fo * p.bins) : p.K;
+}
+bool k_current(const plan& p) { return p.pool ? p.pool->owner == &p : p.k_valid; }
+void k_clobbered(plan& p) {
+    if (p.pool) {
+        if (p.pool->owner == &p) p.pool->owner = nullptr;
+    } else {
+        p.k_valid = false;
+    }
+}
+
+// kernel spectra of the dilated kernels into kbuf(p)
+void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* w) {
     const dims3 e{c.s.x * (c.k.x - 1) + 1, c.s.y * (c.k.y - 1) + 1, c.s.z * (c.k.z - 1) + 1};
     const int64_t nker = c.f_out * c.f_in;
-    // image spectra (memoised for the backward / update passes)
-    forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X);
-    p.cnt.fwd_image += c.B * c.f_in;
-    // kernel spectra of the dilated kernels (memoised for the backward pass)
+    float2* K = kbuf(p);
     ZNN_CUDA_CHECK(cudaMemsetAsync(p.dil, 0, sizeof(float) * size_t(nker * e.vol()), st));
     const int64_t ntaps = nker * c.k.vol();
     dilate_k<<<unsigned(std::min<int64_t>(ceil_div(ntaps, 256), 148 * 16)), 256, 0, st>>>(
         w, ntaps, int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y), int(c.s.z), p.dil);
     launch_check("fft_dilate");
-    forward3d(st, p, p.dil, e.vol(), e, nker, p.K);
+    forward3d(st, p, p.dil, e.vol(), e, nker, K);
+    if (p.pool)
+        p.pool->owner = &p;
+    else
+        p.k_valid = true;
+}
+
+}  // namespace
+
+void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
+              int act, float* y, znn_gpu::scratch& ws) {
+    require(p.B == c.B && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
+    const int64_t nker = c.f_out * c.f_in;
+    // image spectra (memoised for the backward / update passes)
+    forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X);
+    p.cnt.fwd_image += c.B * c.f_in;
+    // kernel spectra of the dilated kernels (memoised for the backward pass)
+    kernel_spectra(st, p, c, w);
     p.cnt.fwd_kernel += nker;
+    const float2* K = kbuf(p);
     // Y = sum_i X * conj(K), one inverse per output node, crop + bias + transfer
     const int64_t ccount = c.B * c.f_out * p.Zh * c.m.x * c.m.y;  // compact kept planes
     if (fused1_ok(p, c)) {  // f_in = 1: Y = X * conj(K) formed inside the inverse xy pass
@@ -1222,7 +1293,7 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
                 const size_t sm = smem_plane1(PY);
                 allow_smem(fft_xy_inv_mul1_k<PY>, sm);
                 fft_xy_inv_mul1_k<PY><<<pipe_grid(planes, sm), THREADS, sm, st>>>(
-                    p.X, p.K, CB, planes, int(c.f_out), int(p.Zh), 1, int(c.m.x), 1, int(c.m.y));
+                    p.X, K, CB, planes, int(c.f_out), int(p.Zh), 1, int(c.m.x), 1, int(c.m.y));
             }
         });
         launch_check("fft_xy_inv_mul1");
@@ -1233,23 +1304,31 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     char* cur = static_cast<char*>(ws.get(sizeof(float2) * size_t(c.B * c.f_out * p.bins + ccount) + 1024));
     float2* Y = carve(cur, c.B * c.f_out * p.bins);
     float2* CB = carve(cur, ccount);
-    cmac_ss(st, p.X, p.K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
+    cmac_ss(st, p.X, K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
     launch_check("fft_cmac_fwd");
     inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB);
     p.cnt.fwd_inverse += c.B * c.f_out;
 }
 
-void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float*, float* gw,
+void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float* w, float* gw,
               float* gin, znn_gpu::scratch& ws) {
     const int64_t nB = c.B;
     const int64_t ccount = std::max(nB * c.f_in * p.Zh * c.n.x * c.n.y, c.f_out * c.f_in * p.Zh * c.k.x * c.k.y);
-    const size_t need = sizeof(float2) * size_t(nB * c.f_out * p.bins + nB * c.f_in * p.bins +
-                                                 c.f_out * c.f_in * p.bins + ccount) + 2048;
+    const size_t need = sizeof(float2) * size_t(nB * c.f_out * p.bins + (gin ? nB * c.f_in * p.bins : 0) + ccount) +
+                        2048;
     char* cur = static_cast<char*>(ws.get(need));
     float2* G = carve(cur, nB * c.f_out * p.bins);
-    float2* DX = carve(cur, nB * c.f_in * p.bins);
-    float2* DK = carve(cur, c.f_out * c.f_in * p.bins);
+    float2* DX = gin ? carve(cur, nB * c.f_in * p.bins) : nullptr;
     float2* CB = carve(cur, ccount);
+    // the data gradient needs this layer's kernel spectra: recompute them if a
+    // layer sharing the buffer overwrote them after this layer's forward
+    if (gin && !k_current(p)) {
+        kernel_spectra(st, p, c, w);
+        p.cnt.bwd_kernel += c.f_out * c.f_in;
+    }
+    const float2* K = kbuf(p);
+    // dK (product spectra of the update) reuse the kernel-spectrum buffer
+    float2* DK = kbuf(p);
     // backward image spectra, padded to the tail dims (engine.hpp:757-759)
     if (!gin && fused1_ok(p, c)) {
         // f_in = 1, no input gradient: the xy pass of every G[b][o] feeds
@@ -1267,6 +1346,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
             }
         });
         launch_check("fft_xy_fwd_upd1");
+        k_clobbered(p);
         inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
         p.cnt.upd_inverse += c.f_out * c.f_in;
         return;
@@ -1274,20 +1354,19 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G);
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
-        cmac_ss(st, G, p.K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
+        cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
         launch_check("fft_cmac_bwd");
         inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB);
         p.cnt.bwd_inverse += nB * c.f_in;
     }
     // kernel gradient: one gradient-specific inverse per edge, sampled at s*w
     {
-        const size_t smem = sizeof(float4) * size_t(nB * (UI + UO) * (SB / 2));
-        require(smem <= 227 * 1024, "fft cmac_upd: batch per GPU > 18 (shared-memory staging)");
         const dim3 gu(unsigned(ceil_div(c.f_in, UI) * ceil_div(c.f_out, UO)), unsigned(ceil_div(p.bins, SB)), 1u);
-        allow_smem(cmac_upd_ss_k, smem);
-        cmac_upd_ss_k<<<gu, SS_THREADS, smem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
+        allow_smem(cmac_upd_ss_k, kUpdSmem);
+        cmac_upd_ss_k<<<gu, SS_THREADS, kUpdSmem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
     }
     launch_check("fft_cmac_upd");
+    k_clobbered(p);
     inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
     p.cnt.upd_inverse += c.f_out * c.f_in;
 }

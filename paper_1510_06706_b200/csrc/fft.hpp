@@ -30,8 +30,24 @@ struct plan_deleter {
 };
 using plan_ptr = std::unique_ptr<plan, plan_deleter>;
 
+// Kernel spectra are the big per-layer object (f_in*f_out*bins complex: 52 GB
+// for c5 conv2). A layer either keeps its own (memoised from the forward into
+// the backward, conv_fft.hpp:38-96) or borrows one buffer shared by several
+// layers; a borrowed buffer is recomputed in the backward pass when another
+// layer has overwritten it since this layer's forward. Either way the weight
+// gradient's product spectra dK reuse the kernel-spectrum buffer (K is dead
+// once the data gradient is formed).
+struct kpool {
+    float2* buf = nullptr;
+    int64_t bytes = 0;
+    const void* owner = nullptr;  // plan whose current K the buffer holds
+    ~kpool();
+    float2* get(int64_t need);
+};
+
+int64_t kernel_spectrum_bytes(const conv_shape& c);
 bool supported(const conv_shape& c);
-plan_ptr make_plan(const conv_shape& c);
+plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool = nullptr);
 const transform_counts& counts(const plan& p);
 void pad_dims(const plan& p, int64_t out[3]);
 

@@ -346,8 +346,42 @@ void executor::set_layer_engine(int conv_layer, int engine) {
     throw znn_gpu::shape_error("set_layer_engine: no conv layer " + std::to_string(conv_layer));
 }
 
+// Kernel spectra stay resident per layer (the reference's memo) while their
+// sum fits ZNN_FFT_RESIDENT_GB (default 48); beyond that the largest layers
+// share one buffer and recompute their spectra in the backward pass when
+// another layer overwrote them (c5: conv2 52 GB + conv3 30 GB share one
+// 52 GB buffer, conv4-6 keep 22 GB resident).
+bool executor::fft_pooled(const layer& L) const {
+    const bool member = &L >= layers_.data() && &L < layers_.data() + layers_.size();
+    if (!member) return false;  // autotune trial copies own their spectra
+    double budget_gb = 48.0;
+    if (const char* e = std::getenv("ZNN_FFT_RESIDENT_GB")) budget_gb = std::atof(e);
+    std::vector<std::pair<int64_t, const layer*>> sz;
+    int64_t total = 0;
+    for (const auto& M : layers_)
+        if (M.kind == lkind::conv && M.engine == 1 && znn_fft::supported(M.shape)) {
+            sz.emplace_back(znn_fft::kernel_spectrum_bytes(M.shape), &M);
+            total += sz.back().first;
+        }
+    std::sort(sz.begin(), sz.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    const double budget = budget_gb * double(int64_t(1) << 30);
+    for (const auto& [bytes, M] : sz) {
+        if (double(total) <= budget) break;
+        if (M == &L) return true;
+        total -= bytes;
+    }
+    return false;
+}
+
 znn_fft::plan& executor::fft_plan(layer& L) {
-    if (!L.fft) L.fft = std::shared_ptr<znn_fft::plan>(znn_fft::make_plan(L.shape).release(), znn_fft::plan_deleter());
+    if (!L.fft) {
+        std::shared_ptr<znn_fft::kpool> pool;
+        if (fft_pooled(L)) {
+            if (!kpool_) kpool_ = std::make_shared<znn_fft::kpool>();
+            pool = kpool_;
+        }
+        L.fft = std::shared_ptr<znn_fft::plan>(znn_fft::make_plan(L.shape, pool).release(), znn_fft::plan_deleter());
+    }
     return *L.fft;
 }
 
@@ -550,8 +584,9 @@ std::vector<int> executor::autotune(int trials) {
         if (L.kind != lkind::conv) continue;
         report << "autotune conv#" << ci++ << " (median of " << trials << "):";
         // candidate engines: tensor-core direct, SIMT direct, FFT
-        std::vector<int> cands{0, 3};
+        std::vector<int> cands{0};
         if (znn_fft::supported(L.shape)) cands.push_back(1);
+        cands.push_back(3);
         // scratch inputs for the bwd pass: reuse the layer's own buffers
         float* gout = groups_[size_t(L.out)].grad;
         float* gin = groups_[size_t(L.in)].grad;
@@ -570,10 +605,17 @@ std::vector<int> executor::autotune(int trials) {
                 float ms = 0.f;
                 ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
                 if (t > 0) ts.push_back(ms);  // first run warms plans and scratch
+                // a candidate whose warm-up run is already 4x the best so far cannot
+                // win: skip its trials (SIMT on a 120->120 layer takes seconds)
+                if (t == 0 && ms > 4.f * best) {
+                    ts.push_back(ms);
+                    break;
+                }
             }
             std::sort(ts.begin(), ts.end());
             const float med = ts[ts.size() / 2];
-            report << (e == 0 ? " direct " : e == 1 ? " fft " : " direct-simt ") << med << "ms";
+            report << (e == 0 ? " direct " : e == 1 ? " fft " : " direct-simt ") << med << "ms"
+                   << (ts.size() == 1 && trials > 1 ? "(pruned)" : "");
             if (med < best) best = med, best_e = e;
         }
         report << " -> " << ename(best_e) << "\n";

@@ -110,6 +110,8 @@ private:
     void run_conv_fwd(layer& L);
     void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update);
     znn_fft::plan& fft_plan(layer& L);
+    bool fft_pooled(const layer& L) const;
+    std::shared_ptr<znn_fft::kpool> kpool_;  // kernel spectra shared by the largest FFT layers
 
     train_cfg cfg_;
     cudaStream_t st_ = nullptr;

@@ -144,3 +144,32 @@ def test_autotuner_picks_fft_for_c4_7cubed_layers(ctx):
     # timing; round 1 measures direct ~18% ahead there.
     assert chosen[1:3] == [1, 1], (chosen, net.describe())
     assert "autotune conv#0" in net.describe()
+
+
+@pytest.mark.parametrize("batch", [5, 10])
+def test_fft_pooled_kernel_spectra_parity(ctx, monkeypatch, batch):
+    """Kernel spectra shared by all FFT layers (ZNN_FFT_RESIDENT_GB=0): each
+    layer's data gradient recomputes its spectra when a later layer overwrote
+    the shared buffer, and dK reuses it. One step at an odd batch (5: partial
+    patch blocks in the fwd/bwd and update CMACs) matches the oracle, and only
+    the layers whose spectra were clobbered count a backward kernel transform."""
+    from paper_1510_06706_b200 import configs as C
+    monkeypatch.setenv("ZNN_FFT_RESIDENT_GB", "0")
+    cfg = C.scaled("c4", 16, (2, 2, 2), batch=batch)
+    nconv = len(cfg.conv_layers())
+    engines = ["fft"] * (nconv - 1) + ["direct"]
+    net, params, x, lab, loss, grads, newp = _net_one_step(ctx, cfg, engines)
+    g = O.parse_netspec(cfg.netspec(), cfg.out_dims)
+    ins = [[x[b, 0]] for b in range(cfg.batch)]
+    labs = [[lab[b, o] for o in range(lab.shape[1])] for b in range(cfg.batch)]
+    rl, rg, rp, _ = O.train_step(g, params.astype(np.float64), np.zeros(params.size), ins, labs, cfg.lr,
+                                 cfg.momentum, cfg.loss)
+    assert abs(loss - rl) / (abs(rl) + 1) < 1e-4
+    assert O.max_rel_error(grads, rg) < 1e-3
+    assert O.max_rel_error(newp, rp) < 1e-3
+    counts = [net.fft_counts(li) for li in range(nconv - 1)]
+    # the last FFT layer ran its forward last: its spectra were still in the buffer
+    assert counts[-1]["bwd_kernel"] == 0
+    # earlier layers with an input gradient recomputed theirs (conv0 has none)
+    for c in counts[1:-1]:
+        assert c["bwd_kernel"] == c["fwd_kernel"]
