@@ -799,74 +799,102 @@ __global__ void dilate_k(const float* __restrict__ w, int64_t ntaps, int kx, int
 }
 
 // ---- per-frequency complex multiply-accumulate over converging edges ----
-constexpr int TA = 8;  // patches per CTA in the fwd / bwd CMAC
-
-// fwd / bwd CMAC with the shared operand staged in shared memory:
-//   fwd: Y[b][o]  = sum_i X[b][i] * conj(K[o][i])   (S = X, n = o, r = i)
-//   bwd: DX[b][i] = sum_o G[b][o] * K[o][i]         (S = G, n = i, r = o)
-// A CTA owns SB = 64 frequency bins (2 per lane: 16-byte loads) x SW*ST
-// outputs n (ST per warp) x TA patches. The shared operand S[b][r][bins] is
-// staged IC reduction steps at a time with cp.async (double buffered); the
-// per-edge kernel spectra K stream from HBM exactly once, a whole chunk of
-// 16-byte loads issued before its FMAs.
-constexpr int SB = 64, SW = 8, ST = 2, IC = 4;
-constexpr int SS_THREADS = SW * 32;
+//
+// Per frequency bin the sum over converging edges is a small complex matrix
+// product (fwd: Y[b][o] = sum_i X[b][i] conj(K[o][i]); bwd: DX[b][i] =
+// sum_o G[b][o] K[o][i]; upd: dK[o][i] = sum_b X[b][i] conj(G[b][o])). At
+// B = 16 every kernel-spectrum element feeds 16 complex MACs, so these run
+// near the FP32 FMA roofline, not the HBM one, and the register tiling has to
+// keep shared-memory wavefronts well below the FMA issue rate:
+//   * a CTA owns 16 bins; warp w owns bin pair w (float4 = 2 complex);
+//   * lanes form an 8 x 4 grid over the two output dims, each thread a 4 x TB
+//     (or 4 x 4) tile, so one reduction step is 8 shared loads (each touching
+//     only 4 or 8 distinct 16-byte words: one wavefront, rows padded to an odd
+//     16-byte pitch) against 128 FMAs per thread;
+//   * operand rows of 16 bins (128 B) stream in by cp.async, double buffered;
+//   * results leave through shared memory as whole 128-byte bin rows.
+constexpr int CBINS = 16;     // bins per CTA
+constexpr int CPR = 8;     // float4 pairs per bin row
+constexpr int CPP = 9;     // padded row pitch (float4 units, odd: conflict-free)
+constexpr int C_THREADS = 256;
+constexpr int CNB = 32;    // fwd/bwd: outputs n per CTA (8 lanes x 4)
+constexpr int CRC = 8;     // fwd/bwd: reduction steps per stage
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    const int n = pred ? 16 : 0;  // zero-fill when out of range
+    const int n = int(pred) << 4;  // 16 bytes, or zero-fill when out of range
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(n) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <bool CONJ>
-__global__ void __launch_bounds__(SS_THREADS, 2) cmac_ss_k(const float2* __restrict__ S, const float2* __restrict__ K,
-                                                           float2* __restrict__ O, int B, int nr, int nn, int64_t kn,
-                                                           int64_t kr, int64_t bins) {
-    extern __shared__ float4 sst[];  // [2][TA][IC][SB/2] float4 (2 bins each)
-    constexpr int UNITS = TA * IC * (SB / 2);
+template <int TB>
+constexpr size_t cmac_smem() {
+    return sizeof(float4) * size_t(2 * CRC * (CNB + 4 * TB) * CPP);
+}
+
+// fwd / bwd: O[b][n] = sum_r S[b][r] * op(K[n*kn + r*kr]), op = conj when CONJ.
+// CTA: CNB n x 4*TB patches x CBINS bins. Grid x = (n block, patch block) with
+// the patch blocks of one n block adjacent; grid y = bin blocks.
+template <bool CONJ, int TB>
+__global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restrict__ S, const float2* __restrict__ K,
+                                                          float2* __restrict__ O, int B, int nr, int nn, int64_t kn,
+                                                          int64_t kr, int64_t bins) {
+    constexpr int BB = 4 * TB;
+    constexpr int KST = CRC * CNB * CPP, SST = CRC * BB * CPP;  // float4 per stage
+    extern __shared__ float4 csm[];  // [2][K stage] then [2][S stage]
+    float4* ks = csm;
+    float4* ss = csm + 2 * KST;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // patch blocks of one (n block, bin block) are adjacent in the grid, then
-    // the n blocks of one bin block: K and S are re-read from L2, not HBM
-    const int nbb = (B + TA - 1) / TA;
-    const int64_t w0 = int64_t(blockIdx.y) * SB;
-    const int n0 = int(blockIdx.x / nbb) * (SW * ST) + warp * ST;
-    const int b0 = int(blockIdx.x % nbb) * TA;
-    const int64_t wl = w0 + 2 * lane;  // this lane's two bins
-    const bool wok = wl < bins;        // bins is even
+    const int nl = lane & 7, bl = lane >> 3;
+    const int nbb = (B + BB - 1) / BB;
+    const int n0 = int(blockIdx.x / nbb) * CNB, b0 = int(blockIdx.x % nbb) * BB;
+    const int64_t w0 = int64_t(blockIdx.y) * CBINS;
+    // staging: thread -> (row, pair q); K rows (rr, n) for rr = j, S rows
+    // (rr, b) for rr = rs + j * (32 / BB); per chunk the sources advance by
+    // CRC reduction steps
+    const int q = threadIdx.x & 7, trow = threadIdx.x >> 3;  // trow < 32
+    const int64_t w = w0 + 2 * q;
+    const bool wok = w < bins;
+    const bool kok = wok && n0 + trow < nn;
+    const float2* kp = K + (int64_t(n0 + trow) * kn) * bins + w;
+    const int64_t kstep = kr * bins;
+    constexpr int SJ = (CRC * BB * CPR) / C_THREADS;  // S pieces per thread
+    constexpr int RSTEP = 32 / BB;                     // rr advance per S piece
+    const int sb_ = trow % BB, rs = trow / BB;
+    const bool sok = wok && b0 + sb_ < B;
+    const float2* sp = S + (int64_t(b0 + sb_) * nr + rs) * bins + w;
+    float4* kdst = ks + trow * CPP + q;
+    float4* sdst = ss + (rs * BB + sb_) * CPP + q;
+    // running source pointers: one 64-bit add per piece
+    const float2* kcur = kp;
+    const float2* scur = sp;
+    const int64_t sstep = int64_t(RSTEP) * bins;
     auto stage = [&](int c, int buf) {
-        for (int u = threadIdx.x; u < UNITS; u += SS_THREADS) {
-            const int b = u / (IC * (SB / 2)), rem = u - b * (IC * (SB / 2));
-            const int rr = rem / (SB / 2), q = rem - rr * (SB / 2);
-            const int r = c * IC + rr;
-            const int64_t w = w0 + 2 * q;
-            const bool ok = b0 + b < B && r < nr && w < bins;
-            const float2* src = ok ? S + (int64_t(b0 + b) * nr + r) * bins + w : S;
-            cp_async16(sst + ((buf * TA + b) * IC + rr) * (SB / 2) + q, src, ok);
+        const int r0 = c * CRC;
+#pragma unroll
+        for (int j = 0; j < CRC; ++j) {
+            const bool ok = kok && r0 + j < nr;
+            cp_async16(kdst + buf * KST + j * (CNB * CPP), ok ? kcur : K, ok);
+            kcur += kstep;
+        }
+#pragma unroll
+        for (int j = 0; j < SJ; ++j) {
+            const bool ok = sok && r0 + rs + j * RSTEP < nr;
+            cp_async16(sdst + buf * SST + j * (RSTEP * BB * CPP), ok ? scur : S, ok);
+            scur += sstep;
         }
         cp_async_commit();
     };
-    float4 acc[TA][ST];  // (re, im) of bin 0, (re, im) of bin 1
+    float4 acc[TB][4];
 #pragma unroll
-    for (int b = 0; b < TA; ++b)
+    for (int u = 0; u < TB; ++u)
 #pragma unroll
-        for (int t = 0; t < ST; ++t) acc[b][t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int nchunks = (nr + IC - 1) / IC;
+        for (int t = 0; t < 4; ++t) acc[u][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int nchunks = (nr + CRC - 1) / CRC;
     stage(0, 0);
     for (int c = 0; c < nchunks; ++c) {
         const int buf = c & 1;
-        // this chunk's kernel-spectrum loads, all in flight before the FMAs
-        float4 kv[IC][ST];
-#pragma unroll
-        for (int rr = 0; rr < IC; ++rr)
-#pragma unroll
-            for (int t = 0; t < ST; ++t) {
-                const int r = c * IC + rr, n = n0 + t;
-                kv[rr][t] = (wok && r < nr && n < nn)
-                                ? __ldcs(reinterpret_cast<const float4*>(K + (int64_t(n) * kn + int64_t(r) * kr) * bins + wl))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
         if (c + 1 < nchunks) {
             stage(c + 1, buf ^ 1);
             cp_async_wait<1>();
@@ -874,83 +902,101 @@ __global__ void __launch_bounds__(SS_THREADS, 2) cmac_ss_k(const float2* __restr
             cp_async_wait<0>();
         }
         __syncthreads();
+        const float4* kb = ks + buf * KST + warp;
+        const float4* sb = ss + buf * SST + warp;
+#pragma unroll 1
+        for (int rr = 0; rr < CRC; ++rr) {
+            float4 kv[4], sv[TB];
 #pragma unroll
-        for (int rr = 0; rr < IC; ++rr)
+            for (int t = 0; t < 4; ++t) kv[t] = kb[(rr * CNB + nl + 8 * t) * CPP];
 #pragma unroll
-            for (int b = 0; b < TA; ++b) {
-                const float4 sv = sst[((buf * TA + b) * IC + rr) * (SB / 2) + lane];
+            for (int u = 0; u < TB; ++u) sv[u] = sb[(rr * BB + bl + 4 * u) * CPP];
 #pragma unroll
-                for (int t = 0; t < ST; ++t) {
-                    const float4 k = kv[rr][t];
-                    float4& a = acc[b][t];
+            for (int u = 0; u < TB; ++u)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    float4& a = acc[u][t];
                     if (CONJ) {
-                        cmacc(a.x, a.y, sv.x, sv.y, k.x, k.y);
-                        cmacc(a.z, a.w, sv.z, sv.w, k.z, k.w);
+                        cmacc(a.x, a.y, sv[u].x, sv[u].y, kv[t].x, kv[t].y);
+                        cmacc(a.z, a.w, sv[u].z, sv[u].w, kv[t].z, kv[t].w);
                     } else {
-                        cmac(a.x, a.y, sv.x, sv.y, k.x, k.y);
-                        cmac(a.z, a.w, sv.z, sv.w, k.z, k.w);
+                        cmac(a.x, a.y, sv[u].x, sv[u].y, kv[t].x, kv[t].y);
+                        cmac(a.z, a.w, sv[u].z, sv[u].w, kv[t].z, kv[t].w);
                     }
                 }
-            }
-        __syncthreads();  // the buffer is refilled two chunks later
+        }
+        __syncthreads();  // the buffer is refilled by the next iteration's stage
     }
-    if (!wok) return;
+    // epilogue: [BB][CNB] rows of 8 pairs through shared memory, whole rows out
+    float4* es = csm;
 #pragma unroll
-    for (int b = 0; b < TA; ++b)
+    for (int u = 0; u < TB; ++u)
 #pragma unroll
-        for (int t = 0; t < ST; ++t)
-            if (b0 + b < B && n0 + t < nn)
-                *reinterpret_cast<float4*>(O + (int64_t(b0 + b) * nn + n0 + t) * bins + wl) = acc[b][t];
+        for (int t = 0; t < 4; ++t) es[((bl + 4 * u) * CNB + nl + 8 * t) * CPP + warp] = acc[u][t];
+    __syncthreads();
+    for (int u = threadIdx.x; u < BB * CNB * CPR; u += C_THREADS) {
+        const int qq = u & 7, row = u >> 3;
+        const int nn_ = row % CNB, bb = row / CNB;
+        const int b = b0 + bb, n = n0 + nn_;
+        const int64_t ww = w0 + 2 * qq;
+        if (b < B && n < nn && ww < bins)
+            *reinterpret_cast<float4*>(O + (int64_t(b) * nn + n) * bins + ww) = es[(bb * CNB + nn_) * CPP + qq];
+    }
 }
 
-// upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]) — a rank-B update per bin.
-// A CTA owns SB = 64 bins (2 per lane) x a 16 o x 8 i block; each thread
-// accumulates 4 o x 4 i x 2 bins. X[b][i-block] and G[b][o-block] of its
-// bins stream through shared memory UB patches at a time (cp.async, double
-// buffered: 2 x 48 KB whatever B is), so two CTAs per SM overlap staging,
-// FMAs and dK stores.
-// Grid: (i, o) blocks of one bin block adjacent, so X / G stay in L2.
-constexpr int UO = 16, UI = 8, TUO = 4, TUI = 4;  // 256 threads = (UO/TUO) x (UI/TUI) x 32 lanes
-constexpr int UB = 4;                             // patches per pipeline stage
-constexpr size_t kUpdSmem = sizeof(float4) * size_t(2 * UB * (UI + UO) * (SB / 2));
-__global__ void __launch_bounds__(SS_THREADS, 2) cmac_upd_ss_k(const float2* __restrict__ X,
-                                                               const float2* __restrict__ G, float2* __restrict__ DK,
-                                                               int B, int f, int fo, int64_t bins) {
-    extern __shared__ float4 sst[];  // [2 stages][UB][UI + UO][SB/2] (X rows, then G rows)
-    constexpr int ROWS = UI + UO;
-    constexpr int STAGE = UB * ROWS * (SB / 2);
+// upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]). CTA: 32 o x 16 i x CBINS bins,
+// lanes 8 (o) x 4 (i), thread tile 4 o x 4 i x 2 bins; X / G rows stream in
+// UB-patch stages. Grid x = (o block, i block) with the i blocks of one o
+// block adjacent (G rows re-read from L2); grid y = bin blocks.
+constexpr int UO = 32, UI = 16, UB = 4;
+constexpr size_t kUpdSmem = sizeof(float4) * size_t(2 * UB * (UO + UI) * CPP > UO * UI * CPP ? 2 * UB * (UO + UI) * CPP : UO * UI * CPP);
+__global__ void __launch_bounds__(C_THREADS, 2) cmac_upd_ss_k(const float2* __restrict__ X,
+                                                              const float2* __restrict__ G, float2* __restrict__ DK,
+                                                              int B, int f, int fo, int64_t bins) {
+    constexpr int ROWS = UO + UI;              // G rows then X rows per patch
+    constexpr int STG = UB * ROWS * CPP;       // float4 per stage
+    extern __shared__ float4 csm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ol = lane & 7, il = lane >> 3;
     const int nib = (f + UI - 1) / UI;
-    const int ib = blockIdx.x % nib, ob = blockIdx.x / nib;
-    const int64_t w0 = int64_t(blockIdx.y) * SB;
-    const int64_t wl = w0 + 2 * lane;
-    const bool wok = wl < bins;
-    const int i_base = ib * UI, o_base = ob * UO;
+    const int i0 = int(blockIdx.x % nib) * UI, o0 = int(blockIdx.x / nib) * UO;
+    const int64_t w0 = int64_t(blockIdx.y) * CBINS;
+    // staging: thread -> (row, pair q); G rows (bb = j, o = trow), X rows
+    // (bb = xb + 2 j, i = trow % 16); per chunk the sources advance UB patches
+    const int q = threadIdx.x & 7, trow = threadIdx.x >> 3;  // trow < 32
+    const int64_t w = w0 + 2 * q;
+    const bool wok = w < bins;
+    const bool gok = wok && o0 + trow < fo;
+    const int xi = trow & 15, xb = trow >> 4;
+    const bool xok = wok && i0 + xi < f;
+    const float2* gp = G + int64_t(o0 + trow) * bins + w;
+    const float2* xp = X + (int64_t(xb) * f + i0 + xi) * bins + w;
+    const int64_t gstep = int64_t(fo) * bins, xstep = int64_t(f) * bins;
+    float4* gdst = csm + trow * CPP + q;
+    float4* xdst = csm + (xb * ROWS + UO + xi) * CPP + q;
+    const float2* gcur = gp;
+    const float2* xcur = xp;
     auto stage = [&](int c, int buf) {
-        for (int u = threadIdx.x; u < STAGE; u += SS_THREADS) {
-            const int bb = u / (ROWS * (SB / 2)), rem = u - bb * (ROWS * (SB / 2));
-            const int row = rem / (SB / 2), q = rem - row * (SB / 2);
-            const int b = c * UB + bb;
-            const int64_t w = w0 + 2 * q;
-            const float2* src;
-            bool ok;
-            if (row < UI) {
-                ok = b < B && i_base + row < f && w < bins;
-                src = X + (int64_t(b) * f + i_base + row) * bins + w;
-            } else {
-                ok = b < B && o_base + row - UI < fo && w < bins;
-                src = G + (int64_t(b) * fo + o_base + row - UI) * bins + w;
-            }
-            cp_async16(sst + buf * STAGE + u, ok ? src : X, ok);
+        const int bc = c * UB;
+#pragma unroll
+        for (int j = 0; j < UB; ++j) {
+            const bool ok = gok && bc + j < B;
+            cp_async16(gdst + buf * STG + j * (ROWS * CPP), ok ? gcur : G, ok);
+            gcur += gstep;
+        }
+#pragma unroll
+        for (int j = 0; j < UB / 2; ++j) {
+            const bool ok = xok && bc + xb + 2 * j < B;
+            cp_async16(xdst + buf * STG + 2 * j * (ROWS * CPP), ok ? xcur : X, ok);
+            xcur += 2 * xstep;
         }
         cp_async_commit();
     };
-    const int oq = warp / (UI / TUI), iq = warp % (UI / TUI);  // this warp's 4 o x 4 i sub-block
-    float4 acc[TUO][TUI];
+    float4 acc[4][4];  // [o t][i u]
 #pragma unroll
-    for (int a = 0; a < TUO; ++a)
+    for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int c = 0; c < TUI; ++c) acc[a][c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < 4; ++u) acc[t][u] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nchunks = (B + UB - 1) / UB;
     stage(0, 0);
     for (int c = 0; c < nchunks; ++c) {
@@ -962,32 +1008,40 @@ __global__ void __launch_bounds__(SS_THREADS, 2) cmac_upd_ss_k(const float2* __r
             cp_async_wait<0>();
         }
         __syncthreads();
-        const float4* xs = sst + buf * STAGE;
+        const float4* base = csm + buf * STG + warp;
+        const int nb = min(UB, B - c * UB);
+#pragma unroll 1
+        for (int bb = 0; bb < nb; ++bb) {
+            float4 gv[4], xv[4];
 #pragma unroll
-        for (int bb = 0; bb < UB; ++bb) {
-            float4 gv[TUO], xv[TUI];
+            for (int t = 0; t < 4; ++t) gv[t] = base[(bb * ROWS + ol + 8 * t) * CPP];
 #pragma unroll
-            for (int a = 0; a < TUO; ++a) gv[a] = xs[(bb * ROWS + UI + oq * TUO + a) * (SB / 2) + lane];
+            for (int u = 0; u < 4; ++u) xv[u] = base[(bb * ROWS + UO + il + 4 * u) * CPP];
 #pragma unroll
-            for (int c2 = 0; c2 < TUI; ++c2) xv[c2] = xs[(bb * ROWS + iq * TUI + c2) * (SB / 2) + lane];
+            for (int t = 0; t < 4; ++t)
 #pragma unroll
-            for (int a = 0; a < TUO; ++a)
-#pragma unroll
-                for (int c2 = 0; c2 < TUI; ++c2) {
-                    cmacc(acc[a][c2].x, acc[a][c2].y, xv[c2].x, xv[c2].y, gv[a].x, gv[a].y);
-                    cmacc(acc[a][c2].z, acc[a][c2].w, xv[c2].z, xv[c2].w, gv[a].z, gv[a].w);
+                for (int u = 0; u < 4; ++u) {
+                    cmacc(acc[t][u].x, acc[t][u].y, xv[u].x, xv[u].y, gv[t].x, gv[t].y);
+                    cmacc(acc[t][u].z, acc[t][u].w, xv[u].z, xv[u].w, gv[t].z, gv[t].w);
                 }
         }
-        __syncthreads();  // the buffer is refilled by the next iteration's stage
+        __syncthreads();
     }
-    if (!wok) return;
+    // epilogue: [UO][UI] rows of 8 pairs through shared memory
+    float4* es = csm;
 #pragma unroll
-    for (int a = 0; a < TUO; ++a)
+    for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int c = 0; c < TUI; ++c) {
-            const int o = o_base + oq * TUO + a, i = i_base + iq * TUI + c;
-            if (o < fo && i < f) __stcs(reinterpret_cast<float4*>(DK + (int64_t(o) * f + i) * bins + wl), acc[a][c]);
-        }
+        for (int u = 0; u < 4; ++u) es[((il + 4 * u) * UO + ol + 8 * t) * CPP + warp] = acc[t][u];
+    __syncthreads();
+    for (int u = threadIdx.x; u < UO * UI * CPR; u += C_THREADS) {
+        const int qq = u & 7, row = u >> 3;
+        const int ii = row % UI, oo = row / UI;
+        const int o = o0 + oo, i = i0 + ii;
+        const int64_t ww = w0 + 2 * qq;
+        if (o < fo && i < f && ww < bins)
+            __stcs(reinterpret_cast<float4*>(DK + (int64_t(o) * f + i) * bins + ww), es[(ii * UO + oo) * CPP + qq]);
+    }
 }
 
 }  // namespace
@@ -1093,18 +1147,32 @@ void allow_smem(K* k, size_t bytes) {
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
 }
 
+template <bool CONJ, int TB>
+void cmac_ss_launch(cudaStream_t st, const float2* S, const float2* K, float2* O, int B, int nr, int nn, int64_t kn,
+                    int64_t kr, int64_t bins) {
+    constexpr size_t smem = cmac_smem<TB>();
+    const dim3 grid(unsigned(ceil_div(nn, CNB) * ceil_div(B, 4 * TB)), unsigned(ceil_div(bins, CBINS)), 1u);
+    allow_smem(cmac_ss_k<CONJ, TB>, smem);
+    cmac_ss_k<CONJ, TB><<<grid, C_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
+}
+
 void cmac_ss(cudaStream_t st, const float2* S, const float2* K, float2* O, int B, int nr, int nn, int64_t kn,
              int64_t kr, int64_t bins, bool conj) {
     require(bins % 2 == 0, "fft cmac: odd bin count");
-    const size_t smem = sizeof(float4) * size_t(2 * TA * IC * (SB / 2));
-    const dim3 grid(unsigned(ceil_div(nn, SW * ST) * ceil_div(B, TA)), unsigned(ceil_div(bins, SB)), 1u);
-    if (conj) {
-        allow_smem(cmac_ss_k<true>, smem);
-        cmac_ss_k<true><<<grid, SS_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
-    } else {
-        allow_smem(cmac_ss_k<false>, smem);
-        cmac_ss_k<false><<<grid, SS_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
-    }
+    // patch tile 4*TB: the smallest that covers B (whole batch per CTA up to 16)
+    auto go = [&](auto tb) {
+        constexpr int TB = decltype(tb)::value;
+        if (conj)
+            cmac_ss_launch<true, TB>(st, S, K, O, B, nr, nn, kn, kr, bins);
+        else
+            cmac_ss_launch<false, TB>(st, S, K, O, B, nr, nn, kn, kr, bins);
+    };
+    if (B <= 4)
+        go(std::integral_constant<int, 1>{});
+    else if (B <= 8)
+        go(std::integral_constant<int, 2>{});
+    else
+        go(std::integral_constant<int, 4>{});
 }
 
 // forward 3D R2C of imgs real volumes (valid dims n, image stride in floats):
@@ -1361,9 +1429,9 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     }
     // kernel gradient: one gradient-specific inverse per edge, sampled at s*w
     {
-        const dim3 gu(unsigned(ceil_div(c.f_in, UI) * ceil_div(c.f_out, UO)), unsigned(ceil_div(p.bins, SB)), 1u);
+        const dim3 gu(unsigned(ceil_div(c.f_in, UI) * ceil_div(c.f_out, UO)), unsigned(ceil_div(p.bins, CBINS)), 1u);
         allow_smem(cmac_upd_ss_k, kUpdSmem);
-        cmac_upd_ss_k<<<gu, SS_THREADS, kUpdSmem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
+        cmac_upd_ss_k<<<gu, C_THREADS, kUpdSmem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
     }
     launch_check("fft_cmac_upd");
     k_clobbered(p);
