@@ -798,6 +798,165 @@ __global__ void dilate_k(const float* __restrict__ w, int64_t ntaps, int kx, int
     }
 }
 
+// ---- sparse-tap plane DFTs for kernel spectra and kernel gradients ----
+// A (dilated) kernel has kx*ky*kz nonzeros on an s-strided grid, so its
+// spectrum needs no padded volume and no FFT: per z-bin plane
+//   K[wx][wy] = sum_a e(-wx a sx) sum_b e(-wy b sy) T[a][b],
+//   T[a][b]   = sum_c e(-wz c sz) w[a][b][c]                  (e(m) = exp(2 pi i m / P))
+// is kx complex MACs per output bin, so the kernel-spectrum pass is one
+// streaming write of K. Its adjoint, the kernel-gradient inverse, keeps only
+// the kx*ky tap positions of each dK plane:
+//   C[a][b] = sum_wy e(+wy b sy) sum_wx e(+wx a sx) dK[wx][wy]
+// (the z inverse of the compact C planes then runs as before), so the dK
+// pass is one streaming read. Square planes (P_x = P_y = P), taps <= KMAX.
+constexpr int KMAX = 8;
+constexpr int KS_THREADS = 256;
+
+template <int P>
+__global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ w, int64_t planes, int Zh, int Pz,
+                                                      int kx, int ky, int kz, int sx, int sy, int sz,
+                                                      float2* __restrict__ K) {
+    __shared__ float2 tw[P];           // exp(-2 pi i m / P)
+    __shared__ float2 twz[MAXP];       // exp(-2 pi i m / Pz)
+    __shared__ float2 T[KMAX * KMAX];  // [a][b]
+    __shared__ float2 U[KMAX * P];     // [a][wy]
+    for (int m = threadIdx.x; m < P; m += KS_THREADS) {
+        float sn, cs;
+        sincospif(-2.f * float(m) / float(P), &sn, &cs);
+        tw[m] = make_float2(cs, sn);
+    }
+    for (int m = threadIdx.x; m < Pz; m += KS_THREADS) {
+        float sn, cs;
+        sincospif(-2.f * float(m) / float(Pz), &sn, &cs);
+        twz[m] = make_float2(cs, sn);
+    }
+    const int taps = kx * ky * kz;
+    for (int64_t q = blockIdx.x; q < planes; q += gridDim.x) {
+        const int64_t ker = q / Zh;
+        const int wz = int(q - ker * Zh);
+        __syncthreads();  // twiddles ready / previous plane's U consumed
+        if (threadIdx.x < kx * ky) {
+            const float* wk = w + ker * taps + threadIdx.x * kz;
+            const int mz = (wz * sz) % Pz;
+            float2 acc = make_float2(0.f, 0.f);
+            int m = 0;
+            for (int c = 0; c < kz; ++c) {
+                const float v = __ldg(wk + c);
+                const float2 e = twz[m];
+                acc.x = fmaf(v, e.x, acc.x);
+                acc.y = fmaf(v, e.y, acc.y);
+                m += mz;
+                if (m >= Pz) m -= Pz;
+            }
+            T[threadIdx.x] = acc;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < kx * P; t += KS_THREADS) {
+            const int a = t / P, wy = t - (t / P) * P;
+            const int my = (wy * sy) % P;
+            float2 acc = make_float2(0.f, 0.f);
+            int m = 0;
+            for (int b = 0; b < ky; ++b) {
+                const float2 v = T[a * ky + b], e = tw[m];
+                cmac(acc.x, acc.y, v.x, v.y, e.x, e.y);
+                m += my;
+                if (m >= P) m -= P;
+            }
+            U[t] = acc;
+        }
+        __syncthreads();
+        float4* out = reinterpret_cast<float4*>(K + q * (int64_t(P) * P));
+        for (int idx = threadIdx.x; idx < P * P / 2; idx += KS_THREADS) {
+            const int wx = idx / (P / 2), wy = 2 * (idx - (idx / (P / 2)) * (P / 2));
+            const int mx = (wx * sx) % P;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            int m = 0;
+            for (int a = 0; a < kx; ++a) {
+                const float2 e = tw[m];
+                const float2 u0 = U[a * P + wy], u1 = U[a * P + wy + 1];
+                cmac(acc.x, acc.y, u0.x, u0.y, e.x, e.y);
+                cmac(acc.z, acc.w, u1.x, u1.y, e.x, e.y);
+                m += mx;
+                if (m >= P) m -= P;
+            }
+            __stcs(out + idx, acc);
+        }
+    }
+}
+
+// kernel-gradient inverse, xy part: a CTA takes G = 256 / (P/2) planes at a
+// time, one thread per (plane, column pair) walking the rows (coalesced 16-B
+// loads, kx column sums in registers), then the kx*ky outputs per plane as
+// warp dot products over the columns. out: compact [plane][a][b].
+template <int P>
+__global__ void __launch_bounds__(KS_THREADS) dkinv_xy_k(const float2* __restrict__ DK, int64_t planes, int kx,
+                                                         int ky, int sx, int sy, float2* __restrict__ out) {
+    constexpr int CP = P / 2;                  // column pairs per plane
+    constexpr int G = KS_THREADS / CP;         // planes per CTA step
+    __shared__ float2 tw[P];                   // exp(-2 pi i m / P); the inverse uses conj
+    __shared__ float2 W[G * KMAX * P];         // [g][a][wy]
+    for (int m = threadIdx.x; m < P; m += KS_THREADS) {
+        float sn, cs;
+        sincospif(-2.f * float(m) / float(P), &sn, &cs);
+        tw[m] = make_float2(cs, sn);
+    }
+    const int g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int da[KMAX];
+#pragma unroll
+    for (int a = 0; a < KMAX; ++a) da[a] = (a * sx) % P;
+    for (int64_t q0 = int64_t(blockIdx.x) * G; q0 < planes; q0 += int64_t(gridDim.x) * G) {
+        __syncthreads();  // twiddles ready / previous W consumed
+        const int64_t q = q0 + g;
+        if (g < G && q < planes) {
+            const float4* src = reinterpret_cast<const float4*>(DK + q * (int64_t(P) * P)) + cp;
+            float4 acc[KMAX];
+            int m[KMAX];
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f), m[a] = 0;
+#pragma unroll 4
+            for (int wx = 0; wx < P; ++wx) {
+                const float4 v = __ldcs(src + wx * CP);
+#pragma unroll
+                for (int a = 0; a < KMAX; ++a) {
+                    if (a < kx) {
+                        const float2 e = tw[m[a]];  // conj(e) = exp(+2 pi i m / P)
+                        cmacc(acc[a].x, acc[a].y, v.x, v.y, e.x, e.y);
+                        cmacc(acc[a].z, acc[a].w, v.z, v.w, e.x, e.y);
+                        m[a] += da[a];
+                        if (m[a] >= P) m[a] -= P;
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a)
+                if (a < kx) {
+                    W[(g * KMAX + a) * P + 2 * cp] = make_float2(acc[a].x, acc[a].y);
+                    W[(g * KMAX + a) * P + 2 * cp + 1] = make_float2(acc[a].z, acc[a].w);
+                }
+        }
+        __syncthreads();
+        // outputs (g, a, b): warp dot products over wy
+        const int nout = G * kx * ky;
+        for (int o = warp; o < nout; o += KS_THREADS / 32) {
+            const int gg = o / (kx * ky), r = o - gg * (kx * ky), a = r / ky, b = r - (r / ky) * ky;
+            const int64_t qq = q0 + gg;
+            float2 acc = make_float2(0.f, 0.f);
+            const int mb = (b * sy) % P;
+            for (int wy = lane; wy < P; wy += 32) {
+                const float2 v = W[(gg * KMAX + a) * P + wy], e = tw[(wy * mb) % P];
+                cmacc(acc.x, acc.y, v.x, v.y, e.x, e.y);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+            }
+            if (lane == 0 && qq < planes) out[qq * (kx * ky) + a * ky + b] = acc;
+        }
+    }
+}
+
 // ---- per-frequency complex multiply-accumulate over converging edges ----
 //
 // Per frequency bin the sum over converging edges is a small complex matrix
@@ -1301,7 +1460,7 @@ plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool) {
     ZNN_CUDA_CHECK(cudaMalloc(&p->X, sizeof(float2) * size_t(c.B * c.f_in * p->bins)));
     p->pool = std::move(pool);
     if (!p->pool) ZNN_CUDA_CHECK(cudaMalloc(&p->K, sizeof(float2) * size_t(c.f_out * c.f_in * p->bins)));
-    ZNN_CUDA_CHECK(cudaMalloc(&p->dil, sizeof(float) * size_t(c.f_out * c.f_in * e.vol())));
+    (void)e;  // the dilated-kernel buffer is allocated on first use (dense-kernel path only)
     return p;
 }
 
@@ -1320,11 +1479,33 @@ void k_clobbered(plan& p) {
     }
 }
 
+// sparse-tap plane DFTs apply: square xy planes, <= KMAX taps per axis
+bool sparse_taps(const plan& p, const conv_shape& c) {
+    return p.P.x == p.P.y && p.P.x > 1 && c.k.x <= KMAX && c.k.y <= KMAX && c.k.z <= KMAX &&
+           !std::getenv("ZNN_FFT_DENSE_KERNELS");
+}
+
 // kernel spectra of the dilated kernels into kbuf(p)
 void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* w) {
     const dims3 e{c.s.x * (c.k.x - 1) + 1, c.s.y * (c.k.y - 1) + 1, c.s.z * (c.k.z - 1) + 1};
     const int64_t nker = c.f_out * c.f_in;
     float2* K = kbuf(p);
+    if (sparse_taps(p, c)) {  // straight from the weights: one streaming write of K
+        const int64_t planes = nker * p.Zh;
+        dispatch_pad(int(p.P.y), [&](auto pc) {
+            constexpr int PY = decltype(pc)::value;
+            kspec_k<PY><<<unsigned(std::min<int64_t>(planes, 148 * 8)), KS_THREADS, 0, st>>>(
+                w, planes, int(p.Zh), int(p.P.z), int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y),
+                int(c.s.z), K);
+        });
+        launch_check("fft_kspec");
+        if (p.pool)
+            p.pool->owner = &p;
+        else
+            p.k_valid = true;
+        return;
+    }
+    if (!p.dil) ZNN_CUDA_CHECK(cudaMalloc(&p.dil, sizeof(float) * size_t(nker * e.vol())));
     ZNN_CUDA_CHECK(cudaMemsetAsync(p.dil, 0, sizeof(float) * size_t(nker * e.vol()), st));
     const int64_t ntaps = nker * c.k.vol();
     dilate_k<<<unsigned(std::min<int64_t>(ceil_div(ntaps, 256), 148 * 16)), 256, 0, st>>>(
@@ -1378,6 +1559,26 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     p.cnt.fwd_inverse += c.B * c.f_out;
 }
 
+// kernel-gradient inverse: dK spectra -> gw[o][i] taps (scaled), sampled at s*w
+void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c, const float2* DK, float* gw,
+                             float2* CB) {
+    const int64_t nker = c.f_out * c.f_in;
+    if (sparse_taps(p, c)) {
+        const int64_t planes = nker * p.Zh;
+        dispatch_pad(int(p.P.y), [&](auto pc) {
+            constexpr int PY = decltype(pc)::value;
+            constexpr int G = KS_THREADS / (PY / 2);
+            const int64_t steps = (planes + G - 1) / G;
+            dkinv_xy_k<PY><<<unsigned(std::min<int64_t>(steps, 148 * 8)), KS_THREADS, 0, st>>>(
+                DK, planes, int(c.k.x), int(c.k.y), int(c.s.x), int(c.s.y), CB);
+        });
+        launch_check("fft_dkinv_xy");
+        inverse_z(st, p, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
+        return;
+    }
+    inverse3d(st, p, DK, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
+}
+
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float* w, float* gw,
               float* gin, znn_gpu::scratch& ws) {
     const int64_t nB = c.B;
@@ -1415,7 +1616,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
         });
         launch_check("fft_xy_fwd_upd1");
         k_clobbered(p);
-        inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
+        kernel_gradient_inverse(st, p, c, DK, gw, CB);
         p.cnt.upd_inverse += c.f_out * c.f_in;
         return;
     }
@@ -1435,7 +1636,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     }
     launch_check("fft_cmac_upd");
     k_clobbered(p);
-    inverse3d(st, p, DK, c.f_out * c.f_in, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
+    kernel_gradient_inverse(st, p, c, DK, gw, CB);
     p.cnt.upd_inverse += c.f_out * c.f_in;
 }
 
