@@ -811,15 +811,24 @@ __global__ void dilate_k(const float* __restrict__ w, int64_t ntaps, int kx, int
 // pass is one streaming read. Square planes (P_x = P_y = P), taps <= KMAX.
 constexpr int KMAX = 8;
 constexpr int KS_THREADS = 256;
+// planes per CTA step: one thread per column pair, at most 16 planes
+__host__ __device__ constexpr int ks_planes(int P) { return KS_THREADS / (P / 2) < 16 ? KS_THREADS / (P / 2) : 16; }
 
+// kernel spectra: a CTA takes G = 256 / (P/2) planes at a time. T and U of
+// those planes go to shared memory, then each thread owns one column pair
+// of one plane, keeps its U[a][wy..wy+1] in registers and walks the rows:
+// K[wx] = sum_a U[a] t^a with t = e(-wx sx) by Horner (one broadcast twiddle
+// load and 8 kx FMAs per 16-byte store).
 template <int P>
 __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ w, int64_t planes, int Zh, int Pz,
                                                       int kx, int ky, int kz, int sx, int sy, int sz,
                                                       float2* __restrict__ K) {
-    __shared__ float2 tw[P];           // exp(-2 pi i m / P)
-    __shared__ float2 twz[MAXP];       // exp(-2 pi i m / Pz)
-    __shared__ float2 T[KMAX * KMAX];  // [a][b]
-    __shared__ float2 U[KMAX * P];     // [a][wy]
+    constexpr int CP = P / 2;
+    constexpr int G = ks_planes(P);
+    __shared__ float2 tw[P];                  // exp(-2 pi i m / P)
+    __shared__ float2 twz[MAXP];              // exp(-2 pi i m / Pz)
+    __shared__ float2 T[G * KMAX * KMAX];     // [g][a][b]
+    __shared__ float4 U[G * KMAX * CP];       // [g][a][pair]
     for (int m = threadIdx.x; m < P; m += KS_THREADS) {
         float sn, cs;
         sincospif(-2.f * float(m) / float(P), &sn, &cs);
@@ -830,102 +839,142 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
         sincospif(-2.f * float(m) / float(Pz), &sn, &cs);
         twz[m] = make_float2(cs, sn);
     }
-    const int taps = kx * ky * kz;
-    for (int64_t q = blockIdx.x; q < planes; q += gridDim.x) {
-        const int64_t ker = q / Zh;
-        const int wz = int(q - ker * Zh);
-        __syncthreads();  // twiddles ready / previous plane's U consumed
-        if (threadIdx.x < kx * ky) {
-            const float* wk = w + ker * taps + threadIdx.x * kz;
-            const int mz = (wz * sz) % Pz;
+    const int taps = kx * ky * kz, kxy = kx * ky;
+    const int g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
+    const int mx = sx % P;
+    for (int64_t q0 = int64_t(blockIdx.x) * G; q0 < planes; q0 += int64_t(gridDim.x) * G) {
+        __syncthreads();  // twiddles ready / previous planes' U consumed
+        // T[g][a][b] = sum_c w[a][b][c] e(-wz c sz)
+        for (int t = threadIdx.x; t < G * kxy; t += KS_THREADS) {
+            const int gg = t / kxy, ab = t - gg * kxy;
+            const int64_t q = q0 + gg;
             float2 acc = make_float2(0.f, 0.f);
-            int m = 0;
-            for (int c = 0; c < kz; ++c) {
-                const float v = __ldg(wk + c);
-                const float2 e = twz[m];
-                acc.x = fmaf(v, e.x, acc.x);
-                acc.y = fmaf(v, e.y, acc.y);
-                m += mz;
-                if (m >= Pz) m -= Pz;
+            if (q < planes) {
+                const int64_t ker = q / Zh;
+                const int wz = int(q - ker * Zh);
+                const float* wk = w + ker * taps + ab * kz;
+                const int mz = (wz * sz) % Pz;
+                int m = 0;
+                for (int c = 0; c < kz; ++c) {
+                    const float v = __ldg(wk + c);
+                    const float2 e = twz[m];
+                    acc.x = fmaf(v, e.x, acc.x);
+                    acc.y = fmaf(v, e.y, acc.y);
+                    m += mz;
+                    if (m >= Pz) m -= Pz;
+                }
             }
-            T[threadIdx.x] = acc;
+            T[gg * (KMAX * KMAX) + ab] = acc;
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < kx * P; t += KS_THREADS) {
-            const int a = t / P, wy = t - (t / P) * P;
-            const int my = (wy * sy) % P;
-            float2 acc = make_float2(0.f, 0.f);
-            int m = 0;
-            for (int b = 0; b < ky; ++b) {
-                const float2 v = T[a * ky + b], e = tw[m];
-                cmac(acc.x, acc.y, v.x, v.y, e.x, e.y);
-                m += my;
-                if (m >= P) m -= P;
-            }
-            U[t] = acc;
-        }
-        __syncthreads();
-        float4* out = reinterpret_cast<float4*>(K + q * (int64_t(P) * P));
-        for (int idx = threadIdx.x; idx < P * P / 2; idx += KS_THREADS) {
-            const int wx = idx / (P / 2), wy = 2 * (idx - (idx / (P / 2)) * (P / 2));
-            const int mx = (wx * sx) % P;
+        // U[g][a][wy] = sum_b T[g][a][b] e(-wy b sy), two columns per entry
+        for (int t = threadIdx.x; t < G * kx * CP; t += KS_THREADS) {
+            const int gg = t / (kx * CP), r = t - gg * (kx * CP), a = r / CP, pr = r - (r / CP) * CP;
+            const int my0 = (2 * pr * sy) % P, my1 = ((2 * pr + 1) * sy) % P;
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            int m0 = 0, m1 = 0;
+            for (int b = 0; b < ky; ++b) {
+                const float2 v = T[gg * (KMAX * KMAX) + a * ky + b], e0 = tw[m0], e1 = tw[m1];
+                cmac(acc.x, acc.y, v.x, v.y, e0.x, e0.y);
+                cmac(acc.z, acc.w, v.x, v.y, e1.x, e1.y);
+                m0 += my0;
+                if (m0 >= P) m0 -= P;
+                m1 += my1;
+                if (m1 >= P) m1 -= P;
+            }
+            U[(gg * KMAX + a) * CP + pr] = acc;
+        }
+        __syncthreads();
+        const int64_t q = q0 + g;
+        if (g < G && q < planes) {
+            float4 u[KMAX];
+#pragma unroll
+            for (int a = 0; a < KMAX; ++a) u[a] = a < kx ? U[(g * KMAX + a) * CP + cp] : make_float4(0.f, 0.f, 0.f, 0.f);
+            float4* out = reinterpret_cast<float4*>(K + q * (int64_t(P) * P)) + cp;
             int m = 0;
-            for (int a = 0; a < kx; ++a) {
-                const float2 e = tw[m];
-                const float2 u0 = U[a * P + wy], u1 = U[a * P + wy + 1];
-                cmac(acc.x, acc.y, u0.x, u0.y, e.x, e.y);
-                cmac(acc.z, acc.w, u1.x, u1.y, e.x, e.y);
+            for (int wx = 0; wx < P; ++wx) {
+                const float2 t = tw[m];
+                // Horner, entered at the kx-th coefficient (uniform branch)
+                auto hs = [&](float4 acc, const float4& c) {  // acc * t + c
+                    return make_float4(fmaf(acc.x, t.x, fmaf(-acc.y, t.y, c.x)), fmaf(acc.x, t.y, fmaf(acc.y, t.x, c.y)),
+                                       fmaf(acc.z, t.x, fmaf(-acc.w, t.y, c.z)), fmaf(acc.z, t.y, fmaf(acc.w, t.x, c.w)));
+                };
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                switch (kx) {
+                    case 8: acc = u[7]; [[fallthrough]];
+                    case 7: acc = hs(acc, u[6]); [[fallthrough]];
+                    case 6: acc = hs(acc, u[5]); [[fallthrough]];
+                    case 5: acc = hs(acc, u[4]); [[fallthrough]];
+                    case 4: acc = hs(acc, u[3]); [[fallthrough]];
+                    case 3: acc = hs(acc, u[2]); [[fallthrough]];
+                    case 2: acc = hs(acc, u[1]); [[fallthrough]];
+                    default: acc = hs(acc, u[0]);
+                }
+                __stcs(out + wx * CP, acc);
                 m += mx;
                 if (m >= P) m -= P;
             }
-            __stcs(out + idx, acc);
         }
     }
 }
 
 // kernel-gradient inverse, xy part: a CTA takes G = 256 / (P/2) planes at a
 // time, one thread per (plane, column pair) walking the rows (coalesced 16-B
-// loads, kx column sums in registers), then the kx*ky outputs per plane as
-// warp dot products over the columns. out: compact [plane][a][b].
+// loads; the kx column sums in registers, twiddles of row wx read in pairs
+// from a [wx][a] table), then the kx*ky outputs per plane as warp dot
+// products over the columns. out: compact [plane][a][b].
 template <int P>
-__global__ void __launch_bounds__(KS_THREADS) dkinv_xy_k(const float2* __restrict__ DK, int64_t planes, int kx,
+__global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __restrict__ DK, int64_t planes, int kx,
                                                          int ky, int sx, int sy, float2* __restrict__ out) {
     constexpr int CP = P / 2;                  // column pairs per plane
-    constexpr int G = KS_THREADS / CP;         // planes per CTA step
+    constexpr int G = ks_planes(P);            // planes per CTA step
     __shared__ float2 tw[P];                   // exp(-2 pi i m / P); the inverse uses conj
+    __shared__ float4 tw2[P * (KMAX / 2)];     // [wx][a pair]: e(-wx a sx), e(-wx (a+1) sx)
     __shared__ float2 W[G * KMAX * P];         // [g][a][wy]
     for (int m = threadIdx.x; m < P; m += KS_THREADS) {
         float sn, cs;
         sincospif(-2.f * float(m) / float(P), &sn, &cs);
         tw[m] = make_float2(cs, sn);
     }
+    __syncthreads();
+    for (int t = threadIdx.x; t < P * (KMAX / 2); t += KS_THREADS) {
+        const int wx = t / (KMAX / 2), ap = t - wx * (KMAX / 2);
+        const float2 e0 = tw[(wx * 2 * ap * sx) % P], e1 = tw[(wx * (2 * ap + 1) * sx) % P];
+        tw2[t] = make_float4(e0.x, e0.y, e1.x, e1.y);
+    }
     const int g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int da[KMAX];
-#pragma unroll
-    for (int a = 0; a < KMAX; ++a) da[a] = (a * sx) % P;
     for (int64_t q0 = int64_t(blockIdx.x) * G; q0 < planes; q0 += int64_t(gridDim.x) * G) {
-        __syncthreads();  // twiddles ready / previous W consumed
+        __syncthreads();  // tables ready / previous W consumed
         const int64_t q = q0 + g;
         if (g < G && q < planes) {
             const float4* src = reinterpret_cast<const float4*>(DK + q * (int64_t(P) * P)) + cp;
             float4 acc[KMAX];
-            int m[KMAX];
 #pragma unroll
-            for (int a = 0; a < KMAX; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f), m[a] = 0;
-#pragma unroll 4
-            for (int wx = 0; wx < P; ++wx) {
-                const float4 v = __ldcs(src + wx * CP);
+            for (int a = 0; a < KMAX; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+            // rows in groups of RG, all loads of a group in flight before its FMAs
+            constexpr int RG = P % 8 == 0 ? 8 : (P % 4 == 0 ? 4 : 2);
+#pragma unroll 1
+            for (int wx0 = 0; wx0 < P; wx0 += RG) {
+                float4 vr[RG];
 #pragma unroll
-                for (int a = 0; a < KMAX; ++a) {
-                    if (a < kx) {
-                        const float2 e = tw[m[a]];  // conj(e) = exp(+2 pi i m / P)
-                        cmacc(acc[a].x, acc[a].y, v.x, v.y, e.x, e.y);
-                        cmacc(acc[a].z, acc[a].w, v.z, v.w, e.x, e.y);
-                        m[a] += da[a];
-                        if (m[a] >= P) m[a] -= P;
+                for (int j = 0; j < RG; ++j) vr[j] = __ldcs(src + (wx0 + j) * CP);
+#pragma unroll
+                for (int j = 0; j < RG; ++j) {
+                const int wx = wx0 + j;
+                const float4 v = vr[j];
+#pragma unroll
+                for (int ap = 0; ap < KMAX / 2; ++ap) {
+                    if (2 * ap < kx) {
+                        const float4 e = tw2[wx * (KMAX / 2) + ap];
+                        cmacc(acc[2 * ap].x, acc[2 * ap].y, v.x, v.y, e.x, e.y);
+                        cmacc(acc[2 * ap].z, acc[2 * ap].w, v.z, v.w, e.x, e.y);
+                        if (2 * ap + 1 < kx) {
+                            cmacc(acc[2 * ap + 1].x, acc[2 * ap + 1].y, v.x, v.y, e.z, e.w);
+                            cmacc(acc[2 * ap + 1].z, acc[2 * ap + 1].w, v.z, v.w, e.z, e.w);
+                        }
                     }
+                }
                 }
             }
 #pragma unroll
@@ -1105,10 +1154,16 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
 
 // upd: dK[o][i] = sum_b X[b][i] * conj(G[b][o]). CTA: 32 o x 16 i x CBINS bins,
 // lanes 8 (o) x 4 (i), thread tile 4 o x 4 i x 2 bins; X / G rows stream in
-// UB-patch stages. Grid x = (o block, i block) with the i blocks of one o
-// block adjacent (G rows re-read from L2); grid y = bin blocks.
-constexpr int UO = 32, UI = 16, UB = 4;
-constexpr size_t kUpdSmem = sizeof(float4) * size_t(2 * UB * (UO + UI) * CPP > UO * UI * CPP ? 2 * UB * (UO + UI) * CPP : UO * UI * CPP);
+// UB-patch stages through a USTAGES-deep ring: the reduction is short (B =
+// 16 is four stages), so all of a CTA's loads are in flight before its
+// first FMA and only the first stage's latency is exposed (the other CTA on
+// the SM covers it). A 2-deep ring left the SMs waiting (67 ms vs 47 ms for
+// the equal-FLOP fwd CMAC on c5). Grid x = (o block, i block) with the i
+// blocks of one o block adjacent (G rows re-read from L2); grid y = bin blocks.
+constexpr int UO = 32, UI = 16, UB = 4, USTAGES = 4;
+constexpr size_t kUpdSmem = sizeof(float4) * size_t(USTAGES * UB * (UO + UI) * CPP > UO * UI * CPP
+                                                        ? USTAGES * UB * (UO + UI) * CPP
+                                                        : UO * UI * CPP);
 __global__ void __launch_bounds__(C_THREADS, 2) cmac_upd_ss_k(const float2* __restrict__ X,
                                                               const float2* __restrict__ G, float2* __restrict__ DK,
                                                               int B, int f, int fo, int64_t bins) {
@@ -1157,16 +1212,22 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_upd_ss_k(const float2* __re
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc[t][u] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nchunks = (B + UB - 1) / UB;
-    stage(0, 0);
+    // ring prologue: stages 0 .. USTAGES-2 (one commit group each, empty past the end)
+#pragma unroll
+    for (int c = 0; c < USTAGES - 1; ++c) {
+        if (c < nchunks)
+            stage(c, c);
+        else
+            cp_async_commit();
+    }
     for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c + 1 < nchunks) {
-            stage(c + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
+        const int buf = c % USTAGES;
+        cp_async_wait<USTAGES - 2>();  // stage c landed
+        __syncthreads();               // ... for every thread; buffer (c-1) % USTAGES is free
+        if (c + USTAGES - 1 < nchunks)
+            stage(c + USTAGES - 1, (c + USTAGES - 1) % USTAGES);
+        else
+            cp_async_commit();
         const float4* base = csm + buf * STG + warp;
         const int nb = min(UB, B - c * UB);
 #pragma unroll 1
@@ -1184,8 +1245,9 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_upd_ss_k(const float2* __re
                     cmacc(acc[t][u].z, acc[t][u].w, xv[u].z, xv[u].w, gv[t].z, gv[t].w);
                 }
         }
-        __syncthreads();
     }
+    cp_async_wait<0>();
+    __syncthreads();  // every warp done with the ring before it holds the epilogue
     // epilogue: [UO][UI] rows of 8 pairs through shared memory
     float4* es = csm;
 #pragma unroll
@@ -1494,7 +1556,8 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
         const int64_t planes = nker * p.Zh;
         dispatch_pad(int(p.P.y), [&](auto pc) {
             constexpr int PY = decltype(pc)::value;
-            kspec_k<PY><<<unsigned(std::min<int64_t>(planes, 148 * 8)), KS_THREADS, 0, st>>>(
+            constexpr int G = ks_planes(PY);
+            kspec_k<PY><<<unsigned(std::min<int64_t>((planes + G - 1) / G, 148 * 8)), KS_THREADS, 0, st>>>(
                 w, planes, int(p.Zh), int(p.P.z), int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y),
                 int(c.s.z), K);
         });
@@ -1567,7 +1630,7 @@ void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c
         const int64_t planes = nker * p.Zh;
         dispatch_pad(int(p.P.y), [&](auto pc) {
             constexpr int PY = decltype(pc)::value;
-            constexpr int G = KS_THREADS / (PY / 2);
+            constexpr int G = ks_planes(PY);
             const int64_t steps = (planes + G - 1) / G;
             dkinv_xy_k<PY><<<unsigned(std::min<int64_t>(steps, 148 * 8)), KS_THREADS, 0, st>>>(
                 DK, planes, int(c.k.x), int(c.k.y), int(c.s.x), int(c.s.y), CB);
