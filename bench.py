@@ -248,19 +248,25 @@ def run_ours(args):
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3) / e2e_steps)
     e2e_value = B * out_vox / (e2e_ms * 1e-3)
 
+    engines = list(getattr(net, "engines", []) or [])
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel (largest conv layer fwd, same engine) ----
-    roof = dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream)
+    # ---- roofline of the dominant kernel of the largest conv layer, on the
+    # engine that layer runs (the net's device memory is released first) ----
+    net.close()
+    torch.cuda.empty_cache()
+    roof = dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream, engines)
     line = {
         "metric": "train_output_voxels_per_s", "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "global_batch": B, "per_gpu_batch": Bl, "in_dims": cfg.in_dims,
                    "out_dims": cfg.out_dims, "parallelism": f"dp{world}", "engine": engine,
+                   "conv_engines": [{0: "direct", 1: "fft", 3: "direct-simt"}.get(e, str(e)) for e in engines]
+                   if engines else None,
                    "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
                    "conv_tflops_per_step": configs.conv_flops_per_patch(cfg) * B / 1e12},
         "conv_tflops_algorithmic": configs.conv_flops_per_patch(cfg) * B / (ms * 1e-3) / 1e12,
@@ -281,7 +287,56 @@ def run_ours(args):
     return 0
 
 
-def dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream):
+def fft_cmac_roofline(torch, ctx, ops, Bl, fi, fo, n, k, s):
+    """The FFT engine's dominant kernel is the per-bin complex multiply-
+    accumulate over converging edges. At B = 16 each kernel-
+    spectrum element feeds 16 complex MACs (8 flop per 8 bytes), so it is
+    bound by FP32 FMA issue, not HBM: the roofline is the measured FMA peak,
+    with the HBM view (algorithmic bytes / time) beside it."""
+    peaks, peak_src = measured_peaks()
+    names = {0: "fwd", 1: "dgrad", 2: "upd"}
+    times, bins = {}, None
+    for which in (0, 1, 2):
+        if which == 1 and fi == 1:
+            continue
+        ms, bins = ops.fft_cmac_time(ctx, which, Bl, fi, fo, n, k, s, reps=3)
+        times[names[which]] = ms * 1e-3
+    dom = max(times, key=times.get)
+    dur = times[dom]
+    flops = 8.0 * Bl * fi * fo * bins  # complex MAC = 4 FMA
+    c8 = 8.0 * bins  # bytes per spectrum (complex64)
+    byts = {"fwd": c8 * (fi * fo + Bl * fi + Bl * fo), "dgrad": c8 * (fi * fo + Bl * fo + Bl * fi),
+            "upd": c8 * (Bl * fi + Bl * fo + fi * fo)}[dom]
+    fma_peak = ops.fma_peak_tflops(ctx)
+    achieved = flops / dur / 1e12
+    shape = f"f={fi}->{fo} n={tuple(n)} k={tuple(k)} s={tuple(s)} B={Bl} bins={bins}"
+    traffic, traffic_src = None, None
+    import glob
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json"))):
+        try:
+            with open(f) as fh:
+                cap = json.load(fh)
+            if cap.get("shape") == "cmac " + shape and dom in cap.get("per_launch", {}):
+                traffic = cap["per_launch"][dom]["dram_bytes"]
+                traffic_src = os.path.relpath(f, ROOT) + " (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
+        except Exception:
+            pass
+    return {"bound": "fp32-fma", "kernel": f"fft_cmac_{dom} " + shape,
+            "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s", "frac": achieved / fma_peak,
+            "achieved_is": "algorithmic fp32 FLOP/s (8 B f f' bins per launch: complex MAC = 4 FMA) / "
+                           "CUDA-event duration of the launch",
+            "peak_source": "measured in-run: FP32 FMA issue-rate probe (znn_fma_peak_tflops); "
+                           "MEASURED_PEAKS.json has HBM and bf16 only",
+            "hbm_view": {"algorithmic_bytes": byts, "achieved_gbs": byts / dur / 1e9,
+                         "peak_gbs": peaks["hbm_gbs"], "frac": byts / dur / 1e9 / peaks["hbm_gbs"],
+                         "peak_source": peak_src},
+            "launch_ms": dur * 1e3, "traffic": traffic, "traffic_unit": "bytes per launch",
+            "traffic_source": traffic_src,
+            "passes_ms": {p: t * 1e3 for p, t in times.items()},
+            "passes_tflops": {p: flops / t / 1e12 for p, t in times.items()}}
+
+
+def dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream, engines=None):
     from paper_1510_06706_b200 import configs
     shapes = [s for s in configs.layer_shapes(cfg) if s[0] == "conv"]
 
@@ -289,7 +344,10 @@ def dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream):
         _, fi, fo, n, m, k, _ = s
         return fi * fo * np.prod(m) * np.prod(k)
 
-    kind, fi, fo, n, m, k, s = max(shapes, key=macs)
+    li = max(range(len(shapes)), key=lambda i: macs(shapes[i]))
+    kind, fi, fo, n, m, k, s = shapes[li]
+    if engine == "fft" or (engines and li < len(engines) and engines[li] == 1):
+        return fft_cmac_roofline(torch, ctx, ops, Bl, fi, fo, n, k, s)
     rng = np.random.default_rng(0)
     x = torch.as_tensor(rng.uniform(0, 1, size=(Bl, fi) + tuple(n)).astype(np.float32), device="cuda")
     w = torch.as_tensor(rng.uniform(-0.01, 0.01, size=(fo, fi) + tuple(k)).astype(np.float32), device="cuda")

@@ -168,6 +168,21 @@ int znn_net_autotune(znn_net net, int trials, int32_t* chosen, int max_layers);
  * has not run on the FFT engine. */
 int znn_net_fft_counts(znn_net net, int conv_layer, int64_t* out);
 
+/* Roofline probe (bench.py): average device time of one frequency-domain
+ * CMAC launch of the FFT engine for a conv layer (B patches, f_in -> f_out
+ * maps, input dims n, kernel k, sparsity s; the engine's own pads give the
+ * bin count, returned in *bins), `which` = 0 forward (Y = X conj K, the
+ * merge_payload sum of conv_fft.hpp:38-60), 1 data gradient
+ * (conv_fft.hpp:67-96), 2 kernel-gradient product (conv_fft.hpp:98-125);
+ * timed with CUDA events on the context stream over `reps` launches on
+ * synthetic spectra it allocates ((B f_in + B f_out + f_in f_out) x bins x 8 bytes). */
+int znn_fft_cmac_time(znn_ctx ctx, int which, int64_t B, int64_t f_in, int64_t f_out, const int64_t n[3],
+                      const int64_t k[3], const int64_t s[3], int reps, float* ms, int64_t* bins);
+/* Measured FP32 FMA throughput of the device (TFLOP/s; 16 independent FMA
+ * chains per thread, 2 CTAs of 1024 threads per SM): the denominator of the
+ * CMAC roofline, since MEASURED_PEAKS.json carries HBM and bf16 only. */
+int znn_fma_peak_tflops(znn_ctx ctx, float* tflops);
+
 /* Full SGD step through HOST buffers (H2D of inputs/labels, fwd, loss,
  * bwd, update, D2H of the loss): the reference engine::run round. */
 int znn_net_step_host(znn_net net, const float* inputs, const float* labels, double* loss);

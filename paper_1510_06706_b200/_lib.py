@@ -28,7 +28,7 @@ EXPORTS = [
     "znn_net_reset_momentum", "znn_net_set_layer_engine", "znn_net_autotune", "znn_net_fft_counts",
     "znn_net_step_host", "znn_net_forward_backward", "znn_net_apply_update", "znn_net_train_step",
     "znn_net_grad_buffer", "znn_net_forward", "znn_net_group_info",
-    "znn_net_get_group_image", "znn_net_get_mask",
+    "znn_net_get_group_image", "znn_net_get_mask", "znn_fft_cmac_time", "znn_fma_peak_tflops",
 ]
 
 
@@ -109,6 +109,8 @@ def lib():
         "znn_net_group_info": (ci, [vp, ci, P64, P64]),
         "znn_net_get_group_image": (ci, [vp, ci, ci, Pf]),
         "znn_net_get_mask": (ci, [vp, ci, P32]),
+        "znn_fft_cmac_time": (ci, [vp, ci, i64, i64, i64, P64, P64, P64, ci, Pf, P64]),
+        "znn_fma_peak_tflops": (ci, [vp, Pf]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

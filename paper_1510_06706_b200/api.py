@@ -117,7 +117,8 @@ class Net:
     def autotune(self, trials: int = 3):
         arr = (ctypes.c_int32 * 64)()
         self._c(lib().znn_net_autotune(self._h, trials, arr, 64))
-        self.engines = [int(v) for v in arr[: self.describe().count("conv#")]]
+        nconv = sum(1 for ln in self.describe().splitlines() if "conv#" in ln and not ln.startswith("autotune"))
+        self.engines = [int(v) for v in arr[:nconv]]
         return self.engines
 
     def fft_counts(self, conv_layer: int):
@@ -346,3 +347,21 @@ class ops:
     def sgd_momentum(ctx, w, v, g, lr, mu):
         check(lib().znn_sgd_momentum(ctx.handle, _ptr(w), _ptr(v), _ptr(g), w.numel(), float(lr), float(mu)),
               ctx.handle)
+
+    @staticmethod
+    def fft_cmac_time(ctx, which, B, f_in, f_out, n, k, s=(1, 1, 1), reps=3):
+        """(average device ms, bins) of one FFT-engine CMAC launch (0 fwd,
+        1 data gradient, 2 kernel-gradient product) for a conv layer shape,
+        on synthetic spectra."""
+        ms, bins = ctypes.c_float(), ctypes.c_int64()
+        check(lib().znn_fft_cmac_time(ctx.handle, int(which), int(B), int(f_in), int(f_out), v3(n), v3(k), v3(s),
+                                      int(reps), ctypes.byref(ms), ctypes.byref(bins)), ctx.handle)
+        return ms.value, bins.value
+
+    @staticmethod
+    def fma_peak_tflops(ctx):
+        """Measured FP32 FMA throughput of the device (TFLOP/s)."""
+        t = ctypes.c_float()
+        check(lib().znn_fma_peak_tflops(ctx.handle, ctypes.byref(t)), ctx.handle)
+        return t.value
+

@@ -329,6 +329,22 @@ int znn_net_fft_counts(znn_net net, int conv_layer, int64_t* out) {
     });
 }
 
+int znn_fft_cmac_time(znn_ctx ctx, int which, int64_t B, int64_t f_in, int64_t f_out, const int64_t n[3],
+                      const int64_t k[3], const int64_t s[3], int reps, float* ms, int64_t* bins) {
+    return guarded(ctx, [&] {
+        auto c = znn_gpu::conv_shape::make(B, f_in, f_out, D(n), D(k), D(s));
+        const float t = znn_fft::time_cmac(ctx->stream, which, c, reps, bins);
+        if (ms) *ms = t;
+    });
+}
+
+int znn_fma_peak_tflops(znn_ctx ctx, float* tflops) {
+    return guarded(ctx, [&] {
+        const float t = znn_fft::fma_peak_tflops(ctx->stream);
+        if (tflops) *tflops = t;
+    });
+}
+
 int znn_net_step_host(znn_net net, const float* inputs, const float* labels, double* loss) {
     return guarded(net->ctx, [&] {
         net->ex->set_stream(net->ctx->stream);

@@ -1026,7 +1026,8 @@ constexpr int CPR = 8;     // float4 pairs per bin row
 constexpr int CPP = 9;     // padded row pitch (float4 units, odd: conflict-free)
 constexpr int C_THREADS = 256;
 constexpr int CNB = 32;    // fwd/bwd: outputs n per CTA (8 lanes x 4)
-constexpr int CRC = 8;     // fwd/bwd: reduction steps per stage
+constexpr int CRC = 4;     // fwd/bwd: reduction steps per stage
+constexpr int CSTAGES = 4; // fwd/bwd: cp.async ring depth
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     const int n = int(pred) << 4;  // 16 bytes, or zero-fill when out of range
@@ -1038,7 +1039,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int TB>
 constexpr size_t cmac_smem() {
-    return sizeof(float4) * size_t(2 * CRC * (CNB + 4 * TB) * CPP);
+    return sizeof(float4) * size_t(CSTAGES * CRC * (CNB + 4 * TB) * CPP);
 }
 
 // fwd / bwd: O[b][n] = sum_r S[b][r] * op(K[n*kn + r*kr]), op = conj when CONJ.
@@ -1050,9 +1051,9 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
                                                           int64_t kr, int64_t bins) {
     constexpr int BB = 4 * TB;
     constexpr int KST = CRC * CNB * CPP, SST = CRC * BB * CPP;  // float4 per stage
-    extern __shared__ float4 csm[];  // [2][K stage] then [2][S stage]
+    extern __shared__ float4 csm[];  // [CSTAGES][K stage] then [CSTAGES][S stage]
     float4* ks = csm;
-    float4* ss = csm + 2 * KST;
+    float4* ss = csm + CSTAGES * KST;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nl = lane & 7, bl = lane >> 3;
     const int nbb = (B + BB - 1) / BB;
@@ -1067,7 +1068,7 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
     const bool kok = wok && n0 + trow < nn;
     const float2* kp = K + (int64_t(n0 + trow) * kn) * bins + w;
     const int64_t kstep = kr * bins;
-    constexpr int SJ = (CRC * BB * CPR) / C_THREADS;  // S pieces per thread
+    constexpr int SJ = (CRC * BB + 31) / 32;          // S pieces per thread
     constexpr int RSTEP = 32 / BB;                     // rr advance per S piece
     const int sb_ = trow % BB, rs = trow / BB;
     const bool sok = wok && b0 + sb_ < B;
@@ -1088,10 +1089,12 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
         }
 #pragma unroll
         for (int j = 0; j < SJ; ++j) {
-            const bool ok = sok && r0 + rs + j * RSTEP < nr;
-            cp_async16(sdst + buf * SST + j * (RSTEP * BB * CPP), ok ? scur : S, ok);
-            scur += sstep;
+            if (rs + j * RSTEP < CRC) {  // TB = 1: half the threads stage S
+                const bool ok = sok && r0 + rs + j * RSTEP < nr;
+                cp_async16(sdst + buf * SST + j * (RSTEP * BB * CPP), ok ? scur + j * sstep : S, ok);
+            }
         }
+        scur += int64_t(CRC) * bins;
         cp_async_commit();
     };
     float4 acc[TB][4];
@@ -1100,16 +1103,22 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
 #pragma unroll
         for (int t = 0; t < 4; ++t) acc[u][t] = make_float4(0.f, 0.f, 0.f, 0.f);
     const int nchunks = (nr + CRC - 1) / CRC;
-    stage(0, 0);
+    // ring prologue: stages 0 .. CSTAGES-2 (one commit group each, empty past the end)
+#pragma unroll
+    for (int c = 0; c < CSTAGES - 1; ++c) {
+        if (c < nchunks)
+            stage(c, c);
+        else
+            cp_async_commit();
+    }
     for (int c = 0; c < nchunks; ++c) {
-        const int buf = c & 1;
-        if (c + 1 < nchunks) {
-            stage(c + 1, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
-        __syncthreads();
+        const int buf = c % CSTAGES;
+        cp_async_wait<CSTAGES - 2>();  // stage c landed
+        __syncthreads();               // ... for every thread; buffer (c-1) % CSTAGES is free
+        if (c + CSTAGES - 1 < nchunks)
+            stage(c + CSTAGES - 1, (c + CSTAGES - 1) % CSTAGES);
+        else
+            cp_async_commit();
         const float4* kb = ks + buf * KST + warp;
         const float4* sb = ss + buf * SST + warp;
 #pragma unroll 1
@@ -1133,8 +1142,9 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
                     }
                 }
         }
-        __syncthreads();  // the buffer is refilled by the next iteration's stage
     }
+    cp_async_wait<0>();
+    __syncthreads();  // every warp done with the ring before it holds the epilogue
     // epilogue: [BB][CNB] rows of 8 pairs through shared memory, whole rows out
     float4* es = csm;
 #pragma unroll
@@ -1703,4 +1713,90 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     p.cnt.upd_inverse += c.f_out * c.f_in;
 }
 
+float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64_t* bins_out) {
+    require(which >= 0 && which <= 2 && reps > 0, "fft cmac probe: bad arguments");
+    require(supported(c), "fft cmac probe: layer unsupported by the FFT engine");
+    const dims3 P = pads_for(c);
+    const int64_t bins = P.x * P.y * (P.z / 2 + 1), B = c.B, f = c.f_in, fo = c.f_out;
+    if (bins_out) *bins_out = bins;
+    float2 *X = nullptr, *G = nullptr, *K = nullptr;
+    ZNN_CUDA_CHECK(cudaMalloc(&X, sizeof(float2) * size_t(B * f * bins)));
+    ZNN_CUDA_CHECK(cudaMalloc(&G, sizeof(float2) * size_t(B * fo * bins)));
+    ZNN_CUDA_CHECK(cudaMalloc(&K, sizeof(float2) * size_t(f * fo * bins)));
+    // small finite values (0x3c3c3c3c = 0.0115f); the FMA rate is value-independent
+    ZNN_CUDA_CHECK(cudaMemsetAsync(X, 0x3c, sizeof(float2) * size_t(B * f * bins), st));
+    ZNN_CUDA_CHECK(cudaMemsetAsync(G, 0x3c, sizeof(float2) * size_t(B * fo * bins), st));
+    ZNN_CUDA_CHECK(cudaMemsetAsync(K, 0x3c, sizeof(float2) * size_t(f * fo * bins), st));
+    auto launch = [&] {
+        if (which == 0) {
+            cmac_ss(st, X, K, G, int(B), int(f), int(fo), f, 1, bins, true);
+        } else if (which == 1) {
+            cmac_ss(st, G, K, X, int(B), int(fo), int(f), 1, f, bins, false);
+        } else {
+            const dim3 gu(unsigned(ceil_div(f, UI) * ceil_div(fo, UO)), unsigned(ceil_div(bins, CBINS)), 1u);
+            allow_smem(cmac_upd_ss_k, kUpdSmem);
+            cmac_upd_ss_k<<<gu, C_THREADS, kUpdSmem, st>>>(X, G, K, int(B), int(f), int(fo), bins);
+        }
+        launch_check("fft_cmac_probe");
+    };
+    launch();
+    cudaEvent_t a, b;
+    ZNN_CUDA_CHECK(cudaEventCreate(&a));
+    ZNN_CUDA_CHECK(cudaEventCreate(&b));
+    ZNN_CUDA_CHECK(cudaEventRecord(a, st));
+    for (int r = 0; r < reps; ++r) launch();
+    ZNN_CUDA_CHECK(cudaEventRecord(b, st));
+    ZNN_CUDA_CHECK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(X);
+    cudaFree(G);
+    cudaFree(K);
+    return ms / float(reps);
+}
+
+namespace {
+// FP32 FMA issue-rate probe: 16 independent FMA chains per thread
+__global__ void fma_probe_k(float* out, int iters) {
+    float x[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = threadIdx.x * 1e-3f + j;
+    const float m = 0.9999f, a = 1e-4f;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], m, a);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sum += x[j];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
+}
+}  // namespace
+
+float fma_peak_tflops(cudaStream_t st) {
+    int sms = 0, dev = 0;
+    ZNN_CUDA_CHECK(cudaGetDevice(&dev));
+    ZNN_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int blocks = sms * 2, threads = 1024, iters = 20000;
+    float* out = nullptr;
+    ZNN_CUDA_CHECK(cudaMalloc(&out, sizeof(float) * size_t(blocks) * threads));
+    fma_probe_k<<<blocks, threads, 0, st>>>(out, 100);
+    cudaEvent_t a, b;
+    ZNN_CUDA_CHECK(cudaEventCreate(&a));
+    ZNN_CUDA_CHECK(cudaEventCreate(&b));
+    ZNN_CUDA_CHECK(cudaEventRecord(a, st));
+    fma_probe_k<<<blocks, threads, 0, st>>>(out, iters);
+    ZNN_CUDA_CHECK(cudaEventRecord(b, st));
+    ZNN_CUDA_CHECK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    return float(2.0 * 16.0 * double(iters) * blocks * threads / (double(ms) * 1e-3) / 1e12);
+}
+
 }  // namespace znn_fft
+

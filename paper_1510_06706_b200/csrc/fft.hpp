@@ -61,4 +61,10 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* g,
               const float* w, float* gw, float* gin, znn_gpu::scratch& ws);
 
+// average device time (ms) of one CMAC launch on synthetic spectra (roofline probe)
+float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64_t* bins_out);
+
+// measured FP32 FMA throughput (TFLOP/s) of this GPU: the CMAC roofline
+float fma_peak_tflops(cudaStream_t st);
+
 }  // namespace znn_fft
