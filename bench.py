@@ -325,8 +325,9 @@ def fft_cmac_roofline(torch, ctx, ops, Bl, fi, fo, n, k, s):
             "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s", "frac": achieved / fma_peak,
             "achieved_is": "algorithmic fp32 FLOP/s (8 B f f' bins per launch: complex MAC = 4 FMA) / "
                            "CUDA-event duration of the launch",
-            "peak_source": "measured in-run: FP32 FMA issue-rate probe (znn_fma_peak_tflops); "
-                           "MEASURED_PEAKS.json has HBM and bf16 only",
+            "peak_source": "measured in-run: 3-register FP32 FFMA issue-rate probe (znn_fma_peak_tflops; "
+                           "every CMAC FMA has three register operands; the immediate-operand form peaks at "
+                           "71.9 TFLOP/s, tests/micro/mma_rate.cu); MEASURED_PEAKS.json has HBM and bf16 only",
             "hbm_view": {"algorithmic_bytes": byts, "achieved_gbs": byts / dur / 1e9,
                          "peak_gbs": peaks["hbm_gbs"], "frac": byts / dur / 1e9 / peaks["hbm_gbs"],
                          "peak_source": peak_src},

@@ -178,9 +178,11 @@ int znn_net_fft_counts(znn_net net, int conv_layer, int64_t* out);
  * synthetic spectra it allocates ((B f_in + B f_out + f_in f_out) x bins x 8 bytes). */
 int znn_fft_cmac_time(znn_ctx ctx, int which, int64_t B, int64_t f_in, int64_t f_out, const int64_t n[3],
                       const int64_t k[3], const int64_t s[3], int reps, float* ms, int64_t* bins);
-/* Measured FP32 FMA throughput of the device (TFLOP/s; 16 independent FMA
- * chains per thread, 2 CTAs of 1024 threads per SM): the denominator of the
- * CMAC roofline, since MEASURED_PEAKS.json carries HBM and bf16 only. */
+/* Measured FP32 FMA throughput of the device (TFLOP/s) for 3-register FFMA
+ * (d = a*b + c, all operands in registers, the form the CMACs issue; 16
+ * independent chains per thread, 2 CTAs of 1024 threads per SM): the
+ * denominator of the CMAC roofline, since MEASURED_PEAKS.json carries HBM
+ * and bf16 only. */
 int znn_fma_peak_tflops(znn_ctx ctx, float* tflops);
 
 /* Full SGD step through HOST buffers (H2D of inputs/labels, fwd, loss,

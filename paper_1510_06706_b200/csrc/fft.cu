@@ -1758,15 +1758,19 @@ float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64
 }
 
 namespace {
-// FP32 FMA issue-rate probe: 16 independent FMA chains per thread
-__global__ void fma_probe_k(float* out, int iters) {
-    float x[16];
+// FP32 FMA issue-rate probe: 16 independent chains per thread of the form the
+// CMACs issue, d = a * b + c with all three operands in registers (runtime
+// values, so no immediate form: 3-register FFMA issues at ~2/3 the rate of
+// the immediate form on this GPU, 49.5 vs 71.9 TFLOP/s in tests/micro/mma_rate.cu)
+__global__ void fma_probe_k(float* out, const float* __restrict__ in, int iters) {
+    float x[16], y[4], z[4];
 #pragma unroll
     for (int j = 0; j < 16; ++j) x[j] = threadIdx.x * 1e-3f + j;
-    const float m = 0.9999f, a = 1e-4f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) y[j] = in[j], z[j] = in[4 + j];
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], m, a);
+        for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], y[j & 3], z[(j >> 2) & 3]);
     }
     float sum = 0.f;
 #pragma unroll
@@ -1781,13 +1785,16 @@ float fma_peak_tflops(cudaStream_t st) {
     ZNN_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int blocks = sms * 2, threads = 1024, iters = 20000;
     float* out = nullptr;
-    ZNN_CUDA_CHECK(cudaMalloc(&out, sizeof(float) * size_t(blocks) * threads));
-    fma_probe_k<<<blocks, threads, 0, st>>>(out, 100);
+    ZNN_CUDA_CHECK(cudaMalloc(&out, sizeof(float) * (size_t(blocks) * threads + 8)));
+    float* in = out + size_t(blocks) * threads;
+    const float h[8] = {0.9999f, 0.9998f, 0.9997f, 0.9996f, 1e-4f, 2e-4f, 3e-4f, 4e-4f};
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(in, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    fma_probe_k<<<blocks, threads, 0, st>>>(out, in, 100);
     cudaEvent_t a, b;
     ZNN_CUDA_CHECK(cudaEventCreate(&a));
     ZNN_CUDA_CHECK(cudaEventCreate(&b));
     ZNN_CUDA_CHECK(cudaEventRecord(a, st));
-    fma_probe_k<<<blocks, threads, 0, st>>>(out, iters);
+    fma_probe_k<<<blocks, threads, 0, st>>>(out, in, iters);
     ZNN_CUDA_CHECK(cudaEventRecord(b, st));
     ZNN_CUDA_CHECK(cudaEventSynchronize(b));
     float ms = 0.f;

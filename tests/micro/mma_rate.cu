@@ -28,9 +28,28 @@ __global__ void fma_k(float* out, int iters) {
     for (int j = 0; j < 16; ++j) s += x[j];
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+// 3-register FFMA: every operand a distinct live register (the CMAC's form)
+__global__ void fma3_k(float* out, const float* __restrict__ in, int iters) {
+    float x[16], y[4], z[4];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = threadIdx.x * 0.001f + j;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) y[j] = in[j], z[j] = in[4 + j];  // runtime values: no immediate folding
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) x[j] = fmaf(x[j], y[j & 3], z[(j >> 2) & 3]);
+    }
+    float s = 0;
+    for (int j = 0; j < 16; ++j) s += x[j];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
 int main() {
     float* out;
     cudaMalloc(&out, 148 * 8 * 1024 * sizeof(float));
+    float* in;
+    cudaMalloc(&in, 8 * sizeof(float));
+    const float h[8] = {0.9999f, 0.9998f, 0.9997f, 0.9996f, 1e-4f, 2e-4f, 3e-4f, 4e-4f};
+    cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -57,6 +76,18 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         const double flops = double(blocks) * warps * 32 * iters * 16 * 2.0;
         printf("ffma: %d warps/CTA x %d CTAs: %.1f TFLOP/s\n", warps, blocks, flops / ms / 1e9);
+    }
+    for (int warps : {16, 32}) {
+        const int iters = 20000, blocks = 148 * 2;
+        fma3_k<<<blocks, warps * 32>>>(out, in, 10);
+        cudaEventRecord(e0);
+        fma3_k<<<blocks, warps * 32>>>(out, in, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double flops = double(blocks) * warps * 32 * iters * 16 * 2.0;
+        printf("ffma 3-register: %d warps/CTA x %d CTAs: %.1f TFLOP/s\n", warps, blocks, flops / ms / 1e9);
     }
     return 0;
 }
