@@ -745,12 +745,26 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
         bvals[l] = bias ? bias[im % uint32_t(g.bias_mod)] : 0.f;
     }
     __syncthreads();
-    // coalesced gather: a warp reads one z-bin of 32 consecutive lines
+    // coalesced gather: a warp reads one z-bin of 32 consecutive lines; all of
+    // a thread's loads are issued before any is stored (the pass was bound by
+    // load latency: one load in flight per thread at a time)
     const int64_t zstride = int64_t(g.xc) * g.yc;
-    for (int idx = threadIdx.x; idx < LINES * Zh; idx += THREADS) {
-        const int l2 = idx % LINES, zb = idx / LINES;
-        if (int64_t(blockIdx.x) * LINES + l2 < g.nlines)
-            stash[l2 * (Zh + 1) + zb] = __ldcs(cspec + ibase[l2] + zb * zstride);
+    {
+        constexpr int NE = (LINES * Zh + THREADS - 1) / THREADS;
+        const int64_t lines_left = g.nlines - int64_t(blockIdx.x) * LINES;
+        float2 tmp[NE];
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int idx = threadIdx.x + e * THREADS;
+            const int l2 = idx % LINES, zb = idx / LINES;
+            tmp[e] = (idx < LINES * Zh && l2 < lines_left) ? __ldcs(cspec + ibase[l2] + zb * zstride)
+                                                          : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            const int idx = threadIdx.x + e * THREADS;
+            if (idx < LINES * Zh) stash[(idx % LINES) * (Zh + 1) + idx / LINES] = tmp[e];
+        }
     }
     __syncthreads();
     const float2* st = stash + l * (Zh + 1);
