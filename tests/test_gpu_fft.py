@@ -199,3 +199,16 @@ def test_fft_dense_kernel_transforms_parity(ctx, monkeypatch):
     assert abs(loss - rl) / (abs(rl) + 1) < 1e-4
     assert O.max_rel_error(grads, rg) < 1e-3
     assert O.max_rel_error(newp, rp) < 1e-3
+
+
+def test_roofline_probes(ctx):
+    """bench.py's roofline probes: the CMAC launch timer reports the FFT
+    engine's own bin count for a layer shape, and the measured 3-register
+    FFMA rate is a plausible B200 figure."""
+    from paper_1510_06706_b200 import ops
+    ms, bins = ops.fft_cmac_time(ctx, 2, 4, 8, 6, (20, 18, 16), (3, 3, 3), (2, 2, 2), reps=2)
+    assert ms > 0 and bins == 20 * 20 * (16 // 2 + 1)  # pads: x, y 20 (square planes), z 16
+    for which in (0, 1):
+        assert ops.fft_cmac_time(ctx, which, 4, 8, 6, (20, 18, 16), (3, 3, 3), (2, 2, 2), reps=1)[0] > 0
+    peak = ops.fma_peak_tflops(ctx)
+    assert 20.0 < peak < 200.0
