@@ -945,6 +945,8 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
     __shared__ float2 tw[P];                   // exp(-2 pi i m / P); the inverse uses conj
     __shared__ float4 tw2[P * (KMAX / 2)];     // [wx][a pair]: e(-wx a sx), e(-wx (a+1) sx)
     __shared__ float2 W[G * KMAX * P];         // [g][a][wy]
+    constexpr bool TWB = P <= 96;              // (P = 128: no room under the 48 KB static limit)
+    __shared__ float2 twb[TWB ? KMAX * P : 1]; // [b][wy]: e(-wy b sy) (lanes read consecutive wy)
     for (int m = threadIdx.x; m < P; m += KS_THREADS) {
         float sn, cs;
         sincospif(-2.f * float(m) / float(P), &sn, &cs);
@@ -956,6 +958,11 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
         const float2 e0 = tw[(wx * 2 * ap * sx) % P], e1 = tw[(wx * (2 * ap + 1) * sx) % P];
         tw2[t] = make_float4(e0.x, e0.y, e1.x, e1.y);
     }
+    if constexpr (TWB)
+        for (int t = threadIdx.x; t < ky * P; t += KS_THREADS) {
+            const int b = t / P, wy = t - (t / P) * P;
+            twb[t] = tw[(wy * ((b * sy) % P)) % P];
+        }
     const int g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t q0 = int64_t(blockIdx.x) * G; q0 < planes; q0 += int64_t(gridDim.x) * G) {
@@ -1005,9 +1012,9 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
             const int gg = o / (kx * ky), r = o - gg * (kx * ky), a = r / ky, b = r - (r / ky) * ky;
             const int64_t qq = q0 + gg;
             float2 acc = make_float2(0.f, 0.f);
-            const int mb = (b * sy) % P;
             for (int wy = lane; wy < P; wy += 32) {
-                const float2 v = W[(gg * KMAX + a) * P + wy], e = tw[(wy * mb) % P];
+                const float2 v = W[(gg * KMAX + a) * P + wy];
+                const float2 e = TWB ? twb[TWB ? b * P + wy : 0] : tw[(wy * ((b * sy) % P)) % P];
                 cmacc(acc.x, acc.y, v.x, v.y, e.x, e.y);
             }
 #pragma unroll
