@@ -250,7 +250,7 @@ __device__ __forceinline__ void line_fft(float2* v, float2* xb, const float2* tw
 template <int P>
 __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__ in, int64_t in_img_stride, int nx,
                                                         int ny, int nz, int64_t nlines, float2* __restrict__ spec,
-                                                        int Px, int Py) {
+                                                        int Px, int Py, const float* __restrict__ gate) {
     constexpr int Zh = P / 2 + 1;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
@@ -270,13 +270,23 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
         const uint32_t im = uint32_t(line) / pl;
         const int r = int(uint32_t(line) - im * pl);
         const int x = r / ny, y = r - (r / ny) * ny;
-        const float* src = in + int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
-        if (t < R1)
+        const int64_t off = int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
+        const float* src = in + off;
+        if (t < R1) {
 #pragma unroll
             for (int n2 = 0; n2 < R2; ++n2) {
                 const int j = t + R1 * n2;
                 if (j < nz) v[n2].x = __ldg(src + j);
             }
+            if (gate) {  // fused ReLU backward: g * (y > 0) (transfer.hpp:99-106, ReLU'(0) = 0)
+                const float* gp = gate + off;
+#pragma unroll
+                for (int n2 = 0; n2 < R2; ++n2) {
+                    const int j = t + R1 * n2;
+                    if (j < nz && !(__ldg(gp + j) > 0.f)) v[n2].x = 0.f;
+                }
+            }
+        }
         if (t == 0) obase[l] = (int64_t(im) * Zh * Px + x) * Py + y;
     }
     __syncthreads();  // twiddles
@@ -1429,17 +1439,48 @@ void cmac_ss(cudaStream_t st, const float2* S, const float2* K, float2* O, int B
 
 // forward 3D R2C of imgs real volumes (valid dims n, image stride in floats):
 // z pass (transposed store) + fused xy pass
+// bias gradient of a fused transfer edge from the spectra (transfer.hpp:
+// 108-121): sum over patches and voxels of the gated gradient = the DC term,
+// here the sum over the valid (x, y) lines of the z pass's zb = 0 plane
+__global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec, int B, int fo, int64_t img_stride,
+                                                 int nx, int ny, int py, float* __restrict__ dbias) {
+    const int o = blockIdx.x;
+    double acc = 0.0;
+    const int64_t per = int64_t(nx) * ny, total = int64_t(B) * per;
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+        const int64_t b = i / per, r = i - b * per;
+        const int x = int(r / ny), y = int(r - (r / ny) * ny);
+        acc += double(spec[(b * fo + o) * img_stride + int64_t(x) * py + y].x);
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) dbias[o] = float(red[0]);
+}
+
+// gate: optional ReLU output gating the input (fused transfer backward);
+// dbias (with gate): receives the per-map sum over the batch (imgs = B * dmaps)
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
-               float2* spec, bool z_only = false) {
+               float2* spec, bool z_only = false, const float* gate = nullptr, float* dbias = nullptr,
+               int64_t dmaps = 1) {
     const int64_t nlines = imgs * n.x * n.y;
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
         allow_smem(fft_z_fwd_k<PP>, smem_for(PP));
         fft_z_fwd_k<PP><<<unsigned(ceil_div(nlines, LINES)), THREADS, smem_for(PP), st>>>(
-            in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y));
+            in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate);
     });
     launch_check("fft_z_fwd");
+    if (dbias) {
+        dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y,
+                                                   int(n.x), int(n.y), int(p.P.y), dbias);
+        launch_check("fft_dc_bias");
+    }
     if (z_only) return;
     const int64_t planes = imgs * p.Zh;
     dispatch_pad(int(p.P.y), [&](auto pc) {
@@ -1674,7 +1715,7 @@ void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c
 }
 
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float* w, float* gw,
-              float* gin, znn_gpu::scratch& ws) {
+              float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias) {
     const int64_t nB = c.B;
     const int64_t ccount = std::max(nB * c.f_in * p.Zh * c.n.x * c.n.y, c.f_out * c.f_in * p.Zh * c.k.x * c.k.y);
     const size_t need = sizeof(float2) * size_t(nB * c.f_out * p.bins + (gin ? nB * c.f_in * p.bins : 0) + ccount) +
@@ -1696,7 +1737,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     if (!gin && fused1_ok(p, c)) {
         // f_in = 1, no input gradient: the xy pass of every G[b][o] feeds
         // dK[o] = sum_b X[b] * conj(G[b][o]) directly (G never reaches HBM)
-        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, /*z_only=*/true);
+        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, /*z_only=*/true, relu_y, dbias, c.f_out);
         p.cnt.bwd_image += nB * c.f_out;
         const int64_t planes = c.f_out * p.Zh;
         dispatch_pad(int(p.P.y), [&](auto pc) {
@@ -1714,7 +1755,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
         p.cnt.upd_inverse += c.f_out * c.f_in;
         return;
     }
-    forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G);
+    forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out);
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
         cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);

@@ -57,9 +57,12 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
               const float* bias, int act, float* y, znn_gpu::scratch& ws);
 // backward + update from the memo: gin = IFFT(sum_o G_o * K_oi) (no conjugate,
 // conv_fft.hpp:67-96, skipped when gin == nullptr) and
-// gw = IFFT(sum_b X_bi * conj(G_bo))[s*w] (conv_fft.hpp:98-125).
+// gw = IFFT(sum_b X_bi * conj(G_bo))[s*w] (conv_fft.hpp:98-125). With relu_y,
+// the layer's fused ReLU backward is applied while g is transformed (g * (y > 0))
+// and dbias[o] receives its bias gradient (the DC term summed over patches).
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* g,
-              const float* w, float* gw, float* gin, znn_gpu::scratch& ws);
+              const float* w, float* gw, float* gin, znn_gpu::scratch& ws, const float* relu_y = nullptr,
+              float* dbias = nullptr);
 
 // average device time (ms) of one CMAC launch on synthetic spectra (roofline probe)
 float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64_t* bins_out);

@@ -413,13 +413,14 @@ void executor::run_conv_fwd(layer& L) {
     }
 }
 
-void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update) {
+void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update, const float* relu_y,
+                            float* dbias) {
     const float* x = groups_[size_t(L.in)].act;
     float* w = params_ + L.w_off;
     float* gw = grads_ + L.w_off;
     const int64_t wcount = L.shape.f_out * L.shape.f_in * L.shape.taps();
     if (L.engine == 1) {
-        znn_fft::conv_bwd(st_, fft_plan(L), L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_);
+        znn_fft::conv_bwd(st_, fft_plan(L), L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_, relu_y, dbias);
         if (update) znn_gpu::sgd_momentum(st_, w, vel_ + L.w_off, gw, wcount, cfg_.lr, cfg_.mu);
         return;
     }
@@ -488,6 +489,18 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
         const bool ce_here = last && cfg_.loss == 1;
         switch (L.kind) {
             case lkind::conv: {
+                // FFT layers with a fused ReLU gate the gradient inside their
+                // spectrum pass and take the bias gradient from its DC term
+                // (no separate transfer-backward pass over the activations)
+                const bool fuse_relu = L.fused && L.engine == 1 && !ce_here && L.fused_act == 2 &&
+                                       !std::getenv("ZNN_NO_RELU_FUSION");
+                if (fuse_relu) {
+                    run_conv_bwd(L, O.grad, I.grad, L.in != 0, update, O.act, grads_ + L.b_off);
+                    if (update)
+                        znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off,
+                                              L.shape.f_out, cfg_.lr, cfg_.mu);
+                    break;
+                }
                 if (L.fused) {
                     // ce: loss already produced the pre-activation gradient a - d
                     if (ce_here) {

@@ -108,7 +108,8 @@ private:
     void allocate();
     void run_forward(const float* in_dev);
     void run_conv_fwd(layer& L);
-    void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update);
+    void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update,
+                      const float* relu_y = nullptr, float* dbias = nullptr);
     znn_fft::plan& fft_plan(layer& L);
     bool fft_pooled(const layer& L) const;
     std::shared_ptr<znn_fft::kpool> kpool_;  // kernel spectra shared by the largest FFT layers
