@@ -1488,7 +1488,10 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         if (p.P.x == 1) {
             allow_smem(fft_xy_fwd_k<1, PY>, smem_xy(1, PY));
             fft_xy_fwd_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(spec, planes, int(n.x), int(n.y));
-        } else if (smem_pipe(PY) > size_t(220) * 1024) {  // two 128^2 planes do not fit: single buffer
+        } else if (smem_pipe(PY) > size_t(220) * 1024 || !std::getenv("ZNN_FFT_XY_PIPE")) {
+            // one plane per CTA, two CTAs per SM: faster than the persistent
+            // double-buffered pass for the forward (c5: 9.1 vs 10.5 ms at P = 96,
+            // 5.9 vs 7.0 at 80); the inverse keeps the persistent pass
             allow_smem(fft_xy_fwd_k<PY, PY>, smem_xy(PY, PY));
             fft_xy_fwd_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(spec, planes, int(n.x),
                                                                                       int(n.y));
@@ -1518,7 +1521,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
             allow_smem(fft_xy_inv_k<1, PY>, smem_xy(1, PY));
             fft_xy_inv_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
-        } else if (smem_pipe(PY) > size_t(220) * 1024) {
+        } else if (smem_pipe(PY) > size_t(220) * 1024) {  // two 128^2 planes do not fit: single buffer
             allow_smem(fft_xy_inv_k<PY, PY>, smem_xy(PY, PY));
             fft_xy_inv_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));

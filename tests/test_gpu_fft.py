@@ -212,3 +212,11 @@ def test_roofline_probes(ctx):
         assert ops.fft_cmac_time(ctx, which, 4, 8, 6, (20, 18, 16), (3, 3, 3), (2, 2, 2), reps=1)[0] > 0
     peak = ops.fma_peak_tflops(ctx)
     assert 20.0 < peak < 200.0
+
+
+@pytest.mark.parametrize("shape", [CASES[4], CASES[7]], ids=str)
+def test_fft_xy_pipe_forward_variant(ctx, monkeypatch, shape):
+    """The persistent double-buffered forward xy pass (ZNN_FFT_XY_PIPE=1,
+    opt-in: slower than one plane per CTA for the forward) stays exact."""
+    monkeypatch.setenv("ZNN_FFT_XY_PIPE", "1")
+    test_fft_conv_fwd_matches_oracle(ctx, shape)
