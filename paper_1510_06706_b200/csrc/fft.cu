@@ -1,7 +1,9 @@
 // FFT-memoised convolution engine (see fft.hpp). All transforms are
-// hand-written: a 1D transform of one line runs in shared memory as a
-// Stockham autosort FFT (radix 8/4/2/3 stages compiled per pad size, twiddles
-// from a per-CTA table), 32 lines per 256-thread CTA.
+// hand-written: a 1D transform of one line runs in registers + shared memory
+// as a four-step FFT (P = R1 * R2, radix 2/3/4/5/8 codelets compiled per pad
+// size, twiddles from a per-CTA table), 32 lines per 256-thread CTA. Kernel
+// spectra and kernel-gradient inverses do not use these passes (sparse-tap
+// plane DFTs, see kspec_k / dkinv_xy_k).
 //
 // Spectrum layout, per image: [Pz/2+1][Px][Py] complex64 (z-bin major), so an
 // (x, y) plane of one z-bin is contiguous. A 3D forward transform is two

@@ -1,11 +1,15 @@
 // FFT-memoised convolution engine (conv_fft.hpp:25-192 / fft.hpp:57-192 of
-// the reference), B200-native: batched 3D transforms by hand-written
-// shared-memory Stockham kernels (radix 2/3/4, pad sizes 2^a 3^b <= 128),
+// the reference), B200-native: batched 3D transforms of images by
+// hand-written shared-memory kernels (radix 2/3/4/5/8 codelets, pads
+// 2^a 3^b 5^c <= 128), kernel spectra straight from the weights by
+// sparse-tap plane DFTs and the kernel-gradient inverse as their adjoint,
 // per-image spectra memoised from the forward pass into the backward and
-// update passes exactly as the reference's memo_store does (image spectrum
-// once per node, kernel spectrum once per edge per iteration), and the
-// frequency-domain sum over converging edges as a per-frequency complex
-// multiply-accumulate kernel (HBM-bound).
+// update passes as the reference's memo_store does (image spectrum once per
+// node, kernel spectrum once per edge per iteration; the largest layers
+// share one kernel-spectrum buffer and recompute when it was overwritten),
+// and the frequency-domain sum over converging edges as register-tiled
+// per-frequency complex multiply-accumulate kernels (FP32-FMA bound at
+// 16 patches).
 #pragma once
 
 #include <cstdint>
