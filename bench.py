@@ -119,32 +119,41 @@ def tf32_peak_tflops(torch):
 # ---------------------------------------------------------------------------
 # CPU baseline (oracle/_ref reference engine if built, else the oracle port)
 # ---------------------------------------------------------------------------
-def cpu_baseline(cfg, budget_s=20.0):
+def cpu_baseline(cfg, warmup=1, rounds=1, budget_s=None):
     sys.path.insert(0, ROOT)
     from oracle import cpu_bench
-    return cpu_bench.run(cfg, budget_s=budget_s)
+    if budget_s is None:
+        budget_s = float(os.environ.get("ZNN_CPU_BUDGET_S", "900"))
+    return cpu_bench.run(cfg, warmup=warmup, rounds=rounds, mode="auto", budget_s=budget_s)
 
 
 def run_reference(args):
+    """The reference's own CPU implementation (engine<float>, compiled from
+    /root/reference into oracle/_ref; the oracle port only if that binary is
+    missing) on the same config, all host threads. One step = one reference
+    round = one patch through fwd + bwd + update (engine.hpp:198-254 runs one
+    sample per round): W warm-up rounds, then K measured rounds with wall time
+    around each (stopping early, and saying so in "steps", only if the
+    ZNN_REF_BUDGET_S budget would be exceeded)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from paper_1510_06706_b200 import configs
     cfg = configs.CONFIGS[args.config]
     out_vox = int(np.prod(cfg.out_dims))
-    vals = []
-    cb = None
-    for _ in range(args.steps):
-        cb = cpu_baseline(cfg, budget_s=float(os.environ.get("ZNN_REF_BUDGET_S", "20")))
-        vals.append(cb["value"])
-    v = float(np.median(vals))
-    cb["value"] = v
+    cb = cpu_baseline(cfg, warmup=args.warmup, rounds=args.steps,
+                      budget_s=float(os.environ.get("ZNN_REF_BUDGET_S", "3000")))
+    v = cb["value"]
+    steps = int(cb.get("rounds", args.steps))
     line = {"metric": "train_output_voxels_per_s", "value": v, "unit": "voxels/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": out_vox * cfg.batch / v * 1e3,
+            "steps": steps, "warmup": int(cb.get("warmup_rounds", args.warmup)),
+            "ms_per_step": out_vox / v * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": cb.get("dtype", "f32"),
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg.name, "global_batch": cfg.batch, "in_dims": cfg.in_dims,
-                       "out_dims": cfg.out_dims, "parallelism": "cpu threads"},
+            "config": {"workload": cfg.name, "global_batch": cfg.batch, "patches_per_step": 1,
+                       "in_dims": cfg.in_dims, "out_dims": cfg.out_dims, "parallelism": "cpu threads",
+                       "step": "one reference round = one patch (fwd + bwd + update); voxels/s is per output "
+                               "voxel, so it compares directly with the GPU arm's 16-patch steps"},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -158,7 +167,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1510_06706_b200 import Context, Net, configs, ops
+    from paper_1510_06706_b200 import Comm, Context, Loader, Net, comm_unique_id, configs, mem_stats
+    from paper_1510_06706_b200.api import profile_enable, profile_report
     from paper_1510_06706_b200.distributed import DataParallelStep, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -181,6 +191,11 @@ def run_ours(args):
     net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=Bl, global_batch=B, lr=cfg.lr,
               momentum=cfg.momentum, loss=cfg.loss, engine=engine)
     net.set_params(configs.init_params(cfg, 2026))
+    comm = None
+    if world > 1:  # the library's own NCCL communicator (per-layer allreduce buckets overlap the backward)
+        uid = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = Comm(ctx, uid[0], world, rank)
 
     rng = np.random.default_rng(1000 + rank)
     n_out = cfg.layers[-1].width
@@ -191,7 +206,7 @@ def run_ours(args):
     x_dev = x_host.to("cuda", non_blocking=True)
     y_dev = y_host.to("cuda", non_blocking=True)
     torch.cuda.synchronize()
-    step = DataParallelStep(net, world)
+    step = DataParallelStep(net, world, comm=comm)
 
     def barrier():
         if world > 1:
@@ -204,12 +219,14 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---- device-resident timed region ----
+    # ---- device-resident timed region (in-step kernel events on for the roofline) ----
     for _ in range(args.warmup):
         step(x_dev, y_dev)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
+    profile_report(ctx)  # drop warm-up records
+    profile_enable(ctx, True)
     launches0 = ctx.launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
@@ -220,24 +237,49 @@ def run_ours(args):
         torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
+    profile_enable(ctx, False)
     launches = ctx.launches() - launches0
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    kprof = profile_report(ctx)
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    ms = max_over_ranks(ms_local)
+    mem = mem_stats(ctx)
 
     out_vox = int(np.prod(cfg.out_dims))
     value = B * out_vox / (ms * 1e-3)
 
-    # ---- end-to-end through the C-ABI with HOST buffers ----
+    # ---- CUDA-graph replay of the same step (single process) ----
+    graph_ms = None
+    if world == 1:
+        net.set_graph(True)
+        for _ in range(2):
+            net.train_step(x_dev, y_dev, sync_loss=False)
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(3):
+            net.train_step(x_dev, y_dev, sync_loss=False)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        graph_ms = g0.elapsed_time(g1) / 3
+        net.set_graph(False)
+
+    # ---- end-to-end through the C-ABI from pinned HOST memory: every step's
+    # inputs/labels copied H2D (the data provider's copy stream, overlapped
+    # with the previous step) and the loss read back D2H ----
     e2e_steps = args.e2e_steps or max(2, args.steps // 2)
     h2d = (x_host.numel() + y_host.numel()) * 4
     d2h = 8
+    loader = Loader(net, inputs=x_host, labels=y_host) if world == 1 else None
+    if loader is not None:
+        net.step_loader(loader)  # first batch's staging
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        if world == 1:
-            net.step_host_ptr(x_host.data_ptr(), y_host.data_ptr())  # H2D, fwd, bwd, update, loss D2H
+        if loader is not None:
+            net.step_loader(loader)  # H2D (async, double-buffered), fwd, bwd, update, loss D2H
         else:
             x_dev.copy_(x_host, non_blocking=True)
             y_dev.copy_(y_host, non_blocking=True)
@@ -247,18 +289,19 @@ def run_ours(args):
     wall = time.perf_counter() - t0
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), wall * 1e3) / e2e_steps)
     e2e_value = B * out_vox / (e2e_ms * 1e-3)
+    if loader is not None:
+        loader.close()
 
     engines = list(getattr(net, "engines", []) or [])
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return 0
 
-    # ---- roofline of the dominant kernel of the largest conv layer, on the
-    # engine that layer runs (the net's device memory is released first) ----
-    net.close()
-    torch.cuda.empty_cache()
-    roof = dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream, engines)
+    roof, shares = roofline_from_profile(kprof, args.steps, ms_local)
+    conv_tf = configs.conv_flops_per_patch(cfg) * B / (ms * 1e-3) / 1e12
     line = {
         "metric": "train_output_voxels_per_s", "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -268,144 +311,99 @@ def run_ours(args):
                    "conv_engines": [{0: "direct", 1: "fft", 3: "direct-simt"}.get(e, str(e)) for e in engines]
                    if engines else None,
                    "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
-                   "conv_tflops_per_step": configs.conv_flops_per_patch(cfg) * B / 1e12},
-        "conv_tflops_algorithmic": configs.conv_flops_per_patch(cfg) * B / (ms * 1e-3) / 1e12,
+                   "conv_tflops_per_step_direct_equivalent": configs.conv_flops_per_patch(cfg) * B / 1e12},
+        "conv_tflops_direct_equivalent": conv_tf,
+        "conv_tflops_note": "effective rate: direct-convolution FLOPs (3 x 2 f f' n'^3 k^3 per conv layer) per "
+                            "second of step time; the FFT layers do far fewer flops, so this exceeds the 3xTF32 "
+                            "tensor ceiling and is not a hardware utilisation",
         "e2e": {"value": e2e_value, "unit": "voxels/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_ms, "path": "znn_net_step_loader (pinned host samples, double-buffered H2D)"
+                if world == 1 else "host copy + znn_net_train_step_dp"},
         "gpu_launches": int(launches),
+        "graph_ms_per_step": graph_ms,
+        "memory": {"free_gb_after_step": mem["free"] / 2**30, "library_alloc_gb": mem["alloc_bytes"] / 2**30},
         "clocks": clocks.summary(),
         "roofline": roof,
+        "kernel_shares": shares,
     }
+    net.close()
     if not args.no_cpu_baseline and world == 1:
-        try:
-            line["cpu_baseline"] = cpu_baseline(cfg, budget_s=float(os.environ.get("ZNN_CPU_BUDGET_S", "20")))
+        try:  # 1 warm-up + 1 measured real round of the reference engine (bounded: ~2 rounds)
+            line["cpu_baseline"] = cpu_baseline(cfg, warmup=1, rounds=1)
         except Exception as e:  # the baseline is reported, never the product path
             line["cpu_baseline"] = {"error": str(e)[:200]}
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
-def fft_cmac_roofline(torch, ctx, ops, Bl, fi, fo, n, k, s):
-    """The FFT engine's dominant kernel is the per-bin complex multiply-
-    accumulate over converging edges. At B = 16 each kernel-
-    spectrum element feeds 16 complex MACs (8 flop per 8 bytes), so it is
-    bound by FP32 FMA issue, not HBM: the roofline is the measured FMA peak,
-    with the HBM view (algorithmic bytes / time) beside it."""
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 148 SMs x 128 FP32 lanes x FMA x 1965 MHz = 74.4
+
+
+def roofline_from_profile(kprof, steps, step_ms):
+    """Roofline of the dominant kernel from the in-step CUDA events of the
+    timed region: achieved = algorithmic bytes (or flops) per launch / the
+    average launch duration, against MEASURED_PEAKS' HBM copy bandwidth (FFT
+    passes, CMACs, max-filter) or the in-run cuBLAS TF32 rate (tcgen05
+    direct convolution, 3 MMAs per fp32 MAC)."""
     peaks, peak_src = measured_peaks()
-    names = {0: "fwd", 1: "dgrad", 2: "upd"}
-    times, bins = {}, None
-    for which in (0, 1, 2):
-        if which == 1 and fi == 1:
-            continue
-        ms, bins = ops.fft_cmac_time(ctx, which, Bl, fi, fo, n, k, s, reps=3)
-        times[names[which]] = ms * 1e-3
-    dom = max(times, key=times.get)
-    dur = times[dom]
-    flops = 8.0 * Bl * fi * fo * bins  # complex MAC = 4 FMA
-    c8 = 8.0 * bins  # bytes per spectrum (complex64)
-    byts = {"fwd": c8 * (fi * fo + Bl * fi + Bl * fo), "dgrad": c8 * (fi * fo + Bl * fo + Bl * fi),
-            "upd": c8 * (Bl * fi + Bl * fo + fi * fo)}[dom]
-    fma_peak = ops.fma_peak_tflops(ctx)
-    achieved = flops / dur / 1e12
-    shape = f"f={fi}->{fo} n={tuple(n)} k={tuple(k)} s={tuple(s)} B={Bl} bins={bins}"
-    traffic, traffic_src = None, None
+    hbm = float(peaks["hbm_gbs"])
+    shares = []
+    for e in sorted(kprof, key=lambda e: -e["ms"]):
+        per = e["ms"] / e["launches"]
+        shares.append({"kernel": e["kernel"], "launches_per_step": e["launches"] / steps,
+                       "ms_per_step": e["ms"] / steps, "share_of_step": e["ms"] / steps / step_ms,
+                       "gbs": e["bytes"] / e["launches"] / (per * 1e-3) / 1e9,
+                       "tflops": e["flops"] / e["launches"] / (per * 1e-3) / 1e12 if e["flops"] else None})
+    if not shares:
+        return None, shares
+    dom = shares[0]
+    e = next(x for x in kprof if x["kernel"] == dom["kernel"])
+    per_s = e["ms"] / e["launches"] * 1e-3
+    if dom["kernel"].startswith("conv_") and "_tc" in dom["kernel"]:
+        import torch
+        try:
+            peak, src = tf32_peak_tflops(torch), "measured in-run: cuBLAS TF32 dense 8192^3"
+        except Exception:
+            peak, src = 1100.0, "nominal TF32 dense (fallback)"
+        ach = e["flops"] / e["launches"] / per_s / 1e12
+        roof = {"bound": "tensor", "kernel": dom["kernel"], "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "tensor_pipe_frac": 3 * ach / peak, "peak_source": src,
+                "achieved_is": "algorithmic fp32 FLOP/s per launch; 3xTF32 issues 3 MMAs per MAC"}
+    else:
+        ach = e["bytes"] / e["launches"] / per_s / 1e9
+        roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "peak_source": peak_src + " hbm_gbs (copy bandwidth, burst)",
+                "achieved_is": "algorithmic bytes per launch (DESIGN.md 4.3b) / average in-step launch "
+                               "duration (CUDA events on the executor stream over the timed region)"}
+        if e["flops"]:
+            tf = e["flops"] / e["launches"] / per_s / 1e12
+            roof["fp32_view"] = {"achieved_tflops": tf, "peak_tflops": FP32_NOMINAL_TFLOPS,
+                                 "frac": tf / FP32_NOMINAL_TFLOPS,
+                                 "peak_source": "nominal FP32 FFMA rate (148 SMs x 128 lanes x 2 x 1965 MHz)"}
+    roof["launch_ms"] = per_s * 1e3
+    roof["algorithmic_bytes_per_launch"] = e["bytes"] / e["launches"]
+    roof["traffic"], roof["traffic_source"] = committed_traffic(dom["kernel"])
+    return roof, shares[:16]
+
+
+def committed_traffic(kernel):
+    """DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)
+    from the committed --set full capture of the same kernel label, if any."""
     import glob
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json"))):
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json")), reverse=True):
         try:
             with open(f) as fh:
                 cap = json.load(fh)
-            if cap.get("shape") == "cmac " + shape and dom in cap.get("per_launch", {}):
-                traffic = cap["per_launch"][dom]["dram_bytes"]
-                traffic_src = os.path.relpath(f, ROOT) + " (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
+            if kernel in cap.get("per_kernel", {}):
+                return cap["per_kernel"][kernel]["dram_bytes"], os.path.relpath(f, ROOT) + \
+                    " (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
         except Exception:
             pass
-    return {"bound": "fp32-fma", "kernel": f"fft_cmac_{dom} " + shape,
-            "achieved": achieved, "peak": fma_peak, "unit": "TFLOP/s", "frac": achieved / fma_peak,
-            "achieved_is": "algorithmic fp32 FLOP/s (8 B f f' bins per launch: complex MAC = 4 FMA) / "
-                           "CUDA-event duration of the launch",
-            "peak_source": "measured in-run: 3-register FP32 FFMA issue-rate probe (znn_fma_peak_tflops; "
-                           "every CMAC FMA has three register operands; the immediate-operand form peaks at "
-                           "71.9 TFLOP/s, tests/micro/mma_rate.cu); MEASURED_PEAKS.json has HBM and bf16 only",
-            "hbm_view": {"algorithmic_bytes": byts, "achieved_gbs": byts / dur / 1e9,
-                         "peak_gbs": peaks["hbm_gbs"], "frac": byts / dur / 1e9 / peaks["hbm_gbs"],
-                         "peak_source": peak_src},
-            "launch_ms": dur * 1e3, "traffic": traffic, "traffic_unit": "bytes per launch",
-            "traffic_source": traffic_src,
-            "passes_ms": {p: t * 1e3 for p, t in times.items()},
-            "passes_tflops": {p: flops / t / 1e12 for p, t in times.items()}}
-
-
-def dominant_kernel_roofline(torch, ctx, ops, cfg, Bl, engine, stream, engines=None):
-    from paper_1510_06706_b200 import configs
-    shapes = [s for s in configs.layer_shapes(cfg) if s[0] == "conv"]
-
-    def macs(s):
-        _, fi, fo, n, m, k, _ = s
-        return fi * fo * np.prod(m) * np.prod(k)
-
-    li = max(range(len(shapes)), key=lambda i: macs(shapes[i]))
-    kind, fi, fo, n, m, k, s = shapes[li]
-    if engine == "fft" or (engines and li < len(engines) and engines[li] == 1):
-        return fft_cmac_roofline(torch, ctx, ops, Bl, fi, fo, n, k, s)
-    rng = np.random.default_rng(0)
-    x = torch.as_tensor(rng.uniform(0, 1, size=(Bl, fi) + tuple(n)).astype(np.float32), device="cuda")
-    w = torch.as_tensor(rng.uniform(-0.01, 0.01, size=(fo, fi) + tuple(k)).astype(np.float32), device="cuda")
-    g = torch.as_tensor(rng.uniform(-1, 1, size=(Bl, fo) + tuple(m)).astype(np.float32), device="cuda")
-    eng = "direct" if engine in ("direct", "auto") else engine
-    passes = {
-        "fwd": lambda: ops.conv_fwd(ctx, x, w, k, s, act="relu", engine=eng),
-        "dgrad": lambda: ops.conv_dgrad(ctx, g, w, k, s, engine=eng),
-        "wgrad": lambda: ops.conv_wgrad(ctx, x, g, k, s, engine=eng),
-    }
-    flops = 2.0 * Bl * macs((kind, fi, fo, n, m, k, s))
-    times = {}
-    for name, fn in passes.items():
-        if name == "dgrad" and fi == 1:
-            continue
-        fn()
-        torch.cuda.synchronize()
-        reps = 3
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        b.synchronize()
-        times[name] = a.elapsed_time(b) / reps * 1e-3
-    del x, g
-    torch.cuda.empty_cache()
-    dom = max(times, key=times.get)  # the pass of the largest layer that takes longest
-    dur = times[dom]
-    achieved = flops / dur / 1e12
-    try:
-        peak = tf32_peak_tflops(torch)
-        src = "measured in-run: cuBLAS TF32 dense 8192^3 (MEASURED_PEAKS.json has bf16 only)"
-    except Exception:
-        peak, src = 1100.0, "nominal TF32 dense (fallback)"
-    shape = f"conv f={fi}->{fo} n={tuple(n)} k={tuple(k)} s={tuple(s)} B={Bl}"
-    traffic, traffic_src = None, None
-    # DRAM bytes of this launch from the committed ncu capture of the same
-    # shape (profiles/r01_traffic_*.json), when one exists
-    import glob
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic_*.json"))):
-        try:
-            with open(f) as fh:
-                cap = json.load(fh)
-            if cap.get("shape") == shape and dom in cap.get("per_launch", {}):
-                traffic = cap["per_launch"][dom]["dram_bytes"]
-                traffic_src = os.path.relpath(f, ROOT) + " (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
-        except Exception:
-            pass
-    return {"bound": "tensor", "kernel": f"conv_{dom} " + shape[5:],
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "achieved_is": "algorithmic fp32 FLOP/s (2 f f' n'^3 k^3 per launch / CUDA-event duration); "
-                           "3xTF32 issues 3 tensor MMAs per MAC, so tensor-pipe work is 3x this",
-            "tensor_pipe_frac": 3 * achieved / peak,
-            "peak_source": src, "launch_ms": dur * 1e3, "traffic": traffic, "traffic_unit": "bytes per launch",
-            "traffic_source": traffic_src,
-            "passes_tflops": {p: flops / t / 1e12 for p, t in times.items()}}
+    return None, None
 
 
 def main():

@@ -212,6 +212,95 @@ int znn_net_group_info(znn_net net, int group, int64_t* maps, int64_t dims[3]);
 int znn_net_get_group_image(znn_net net, int group, int which, float* host);
 int znn_net_get_mask(znn_net net, int group, int32_t* host);
 
+/* ---- FFT engine per layer ---------------------------------------------
+ * A plan is the reference's fft_plan_cache + memo_store for one fully
+ * connected layer (fft.hpp:57-192, conv_fft.hpp:127-192): pads, memoised
+ * image spectra X of the layer input and kernel spectra K.
+ * znn_fft_conv_fwd = fwd_image_fft + fwd_kernel_fft + fft_conv_valid_pre
+ *   (conv_fft.hpp:25-60) summed over the f_in converging edges, + bias and
+ *   transfer; memoises X and K.
+ * znn_fft_conv_bwd = fwd_image_fft(g) + fft_conv_full_adjoint_pre
+ *   (conv_fft.hpp:67-96, dx; NULL = skip, e.g. for the input layer) +
+ *   fft_kernel_gradient_pre (conv_fft.hpp:98-125, dw = sum over the batch),
+ *   from the memo of the preceding znn_fft_conv_fwd (status 1 without one).
+ * Shapes and layouts as znn_conv_fwd / _dgrad / _wgrad. */
+typedef struct znn_fft_plan_s* znn_fft_plan;
+int znn_fft_plan_create(znn_ctx ctx, int64_t B, int64_t f_in, int64_t f_out, const int64_t n[3],
+                        const int64_t k[3], const int64_t s[3], znn_fft_plan* out);
+int znn_fft_plan_destroy(znn_fft_plan p);
+/* pads (x, y, z), bins = px*py*(pz/2+1), bytes of the kernel spectra */
+int znn_fft_plan_info(znn_fft_plan p, int64_t pads[3], int64_t* bins, int64_t* kernel_spectrum_bytes);
+int znn_fft_conv_fwd(znn_fft_plan p, const float* x, const float* w, const float* bias, int act, float* y);
+int znn_fft_conv_bwd(znn_fft_plan p, const float* g, const float* w, float* dw, float* dx);
+/* transform counters as znn_net_fft_counts */
+int znn_fft_plan_counts(znn_fft_plan p, int64_t out[9]);
+
+/* ---- autotune one layer (trainer.hpp:181-250 autotune_modes) -----------
+ * Median-of-`trials` device time of fwd + dgrad + wgrad for the layer at
+ * batch B with each candidate engine (tensor-core direct, FFT, SIMT direct
+ * for thin layers); *chosen = the fastest ZNN_CONV_*, ms[3] = {direct, fft,
+ * simt} (-1 = not a candidate or failed). */
+int znn_autotune_layer(znn_ctx ctx, int64_t B, int64_t f_in, int64_t f_out, const int64_t n[3],
+                       const int64_t k[3], const int64_t s[3], int trials, int* chosen, float ms[3]);
+
+/* ---- data parallelism over NCCL (the reference has none) ---
+ * One communicator per rank. Rank 0 creates the 128-byte unique id and the
+ * caller distributes it (MPI, a file, torch.distributed). */
+#define ZNN_COMM_ID_BYTES 128
+typedef struct znn_comm_s* znn_comm;
+int znn_comm_unique_id(void* id /* ZNN_COMM_ID_BYTES */);
+int znn_comm_create(znn_ctx ctx, const void* id, int nranks, int rank, znn_comm* out);
+int znn_comm_destroy(znn_comm comm);
+/* in-place sum over ranks on the context stream (fp32) */
+int znn_allreduce(znn_comm comm, float* buf, int64_t count);
+/* one data-parallel SGD step on this rank's shard (device buffers): forward,
+ * loss (scaled by 1/global_batch), backward with one allreduce per layer
+ * issued on a communication stream as soon as that layer's gradient is final
+ * (overlapping the remaining backward), then the SGD+momentum update. */
+int znn_net_train_step_dp(znn_net net, znn_comm comm, const float* inputs_dev, const float* labels_dev,
+                          double* loss);
+
+/* ---- CUDA graph + memory ------------------------------------------------
+ * Graph mode: znn_net_train_step / step_host / step_loader run the first
+ * step eagerly, then capture the whole step once per input buffer pair and
+ * replay it (no per-launch host work, no allocation: the scratch arena is
+ * frozen and a step that would need more fails with status 2). */
+int znn_net_set_graph(znn_net net, int on);
+int znn_net_graph_captured(znn_net net, int* yes);
+/* out = {device free bytes, device total bytes, device allocations made by
+ * the library so far, bytes of those allocations} */
+int znn_mem_stats(znn_ctx ctx, int64_t out[4]);
+
+/* In-step kernel timing: with profiling on, the library records a CUDA
+ * event pair around each launch of its dominant kernels (FFT CMACs, kernel
+ * spectra, transforms, tensor-core convolutions, max-filter) on the launch
+ * stream (never inside a graph capture). report: JSON array of {kernel,
+ * launches, ms (sum of event durations), bytes, flops (algorithmic, summed
+ * over launches)} since the last report; status 1 if buf is too small. */
+int znn_profile_enable(znn_ctx ctx, int on);
+int znn_profile_report(znn_ctx ctx, char* buf, int64_t len);
+
+/* ---- volume files and the data provider ---------------------------------
+ * ZNNV format (volume_io.hpp:15-86): "ZNNV", u32 version 1, u32 nx, ny, nz,
+ * float32 x-major, little-endian. read: data NULL -> dims only. */
+int znn_volume_write(const char* path, const int64_t dims[3], const float* data);
+int znn_volume_read(const char* path, int64_t dims[3], float* data, int64_t capacity);
+/* Data provider (trainer.hpp:87-166): patch b of step t is sample
+ * (t * global_batch + shard_offset + b) mod samples. From a directory with
+ * inputs/ and labels/ ZNNV files paired by sorted name (every input node
+ * gets the input volume, every output node the label, as from_files does),
+ * or from host arrays [samples][in maps][in vol] / [samples][out maps][out
+ * vol] (pin them for asynchronous copies). Two pinned/device slots: the
+ * next step's files and H2D overlap the current step. */
+typedef struct znn_loader_s* znn_loader;
+int znn_loader_open_dir(znn_net net, const char* dir, int64_t shard_offset, znn_loader* out);
+int znn_loader_open_host(znn_net net, const float* inputs, const float* labels, int64_t samples,
+                         int64_t shard_offset, znn_loader* out);
+int znn_loader_size(znn_loader ld, int64_t* samples);
+int znn_loader_destroy(znn_loader ld);
+/* one SGD step on the loader's next batch (single process; fused update) */
+int znn_net_step_loader(znn_net net, znn_loader ld, double* loss);
+
 #ifdef __cplusplus
 }
 #endif

@@ -2,8 +2,8 @@
 
 Preferred: the reference's own task-parallel engine (engine<float>,
 engine.hpp:65-254) compiled from /root/reference by oracle/ref/build.sh into
-oracle/_ref/znn_ref (kind "reference"), run on all host cores; configs whose
-round exceeds the budget report the per-edge estimate (see znn_ref.cpp).
+oracle/_ref/znn_ref (kind "reference"), real rounds timed on all host
+threads (no extrapolation).
 Fallback: the plain-C double oracle (kind "port", 1 core), timed on a
 bounded per-edge sample of every conv layer and extrapolated by edge count.
 """
@@ -38,47 +38,51 @@ def physical_cores():
     return os.cpu_count() or 1
 
 
-def run(cfg, budget_s=20.0, mode=None):
+def threads():
+    """All host threads the reference engine can use (its worker pool)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run(cfg, warmup=1, rounds=1, mode=None, budget_s=3000.0, port_budget_s=20.0):
+    """Real rounds of the reference engine when oracle/_ref/znn_ref is built,
+    else the oracle port on a bounded per-edge sample."""
     if os.path.exists(REF_BIN):
-        return run_reference_engine(cfg, budget_s, mode or ("auto" if cfg.engine == "auto" else "direct"))
-    return run_port(cfg, budget_s)
+        return run_reference_engine(cfg, warmup, rounds, mode or "auto", budget_s)
+    return run_port(cfg, port_budget_s)
 
 
-def run_reference_engine(cfg, budget_s, mode="direct"):
-    threads = physical_cores()
+def run_reference_engine(cfg, warmup, rounds, mode="auto", budget_s=3000.0):
+    """engine<float>::run (engine.hpp:198-254) compiled from /root/reference:
+    `warmup` rounds, then up to `rounds` measured rounds (one patch each, the
+    reference's unit of work) with wall time around each; mode "auto" runs the
+    reference's own autotune_modes first (its default policy, trainer.hpp:41)."""
+    nthr = threads()
     spec_path = os.path.join("/tmp", f"znn_ref_{cfg.name}_{os.getpid()}.spec")
     with open(spec_path, "w") as f:
         f.write(cfg.netspec())
     od = ",".join(str(v) for v in cfg.out_dims)
-    # predicted round time from the reference's own per-edge task bodies
-    est = subprocess.run([REF_BIN, "estimate", spec_path, od, str(threads)], capture_output=True, text=True,
-                         timeout=900)
-    if est.returncode == 0:
-        e = json.loads(est.stdout.strip().splitlines()[-1])
-        if e["round_seconds"] * 2.0 > budget_s:
-            os.unlink(spec_path)
-            out_vox = int(np.prod(cfg.out_dims))
-            return {"value": out_vox / e["round_seconds"], "unit": "voxels/s", "cores": threads,
-                    "kind": "reference", "dtype": "f32", "estimated": True,
-                    "sample": f"one full {cfg.name} round exceeds the {budget_s:.0f}s budget: every edge signature's "
-                              f"reference task bodies (conv_valid_direct + conv_full_direct(reflect) + "
-                              f"kernel_gradient_direct, transfer/filter/pool fwd+bwd; engine.hpp:582-829) timed "
-                              f"single-threaded (median of 3), summed over all {cfg.name} edges and divided by "
-                              f"{threads} threads (the paper's linear speedup, optimistic for the CPU)"}
-    cmd = [REF_BIN, "bench", spec_path, od, str(threads), str(budget_s), mode]
-    out = subprocess.run(cmd, capture_output=True, text=True, timeout=budget_s * 20 + 600)
+    cmd = [REF_BIN, "bench", spec_path, od, str(nthr), str(int(warmup)), str(int(rounds)), mode, str(budget_s)]
+    t0 = time.perf_counter()
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=budget_s * 3 + 600)
+    wall = time.perf_counter() - t0
     os.unlink(spec_path)
     if out.returncode != 0:
         raise RuntimeError(f"reference engine failed: {out.stderr[-400:]}")
     res = json.loads(out.stdout.strip().splitlines()[-1])
     out_vox = int(np.prod(cfg.out_dims))
     value = out_vox * res["rounds"] / res["seconds"]
-    return {"value": value, "unit": "voxels/s", "cores": threads, "kind": "reference",
-            "dtype": "f32",
-            "sample": f"{res['rounds']} measured round(s) (1 patch each, after {res['warmup']} warm-up round) of "
-                      f"the reference engine<float> (compiled from /root/reference, oracle/ref/build.sh) on "
-                      f"{cfg.name} at full size, conv mode {res['mode']}, {threads} worker threads, wall time "
-                      f"around the measured rounds"}
+    return {"value": value, "unit": "voxels/s", "cores": nthr, "physical_cores": physical_cores(),
+            "kind": "reference", "dtype": "f32", "mode": res["mode"], "rounds": res["rounds"],
+            "warmup_rounds": res["warmup"], "seconds": res["seconds"], "warmup_seconds": res["warmup_seconds"],
+            "autotune_seconds": res.get("autotune_seconds", 0.0), "round_seconds": res.get("round_seconds"),
+            "process_wall_s": wall,
+            "sample": f"{res['rounds']} measured round(s) of the reference engine<float> (compiled from "
+                      f"/root/reference by oracle/ref/build.sh) on {cfg.name} at full size, one patch per round "
+                      f"(the reference's unit of work), after {res['warmup']} warm-up round(s); conv mode "
+                      f"{res['mode']}; {nthr} worker threads; wall time around each measured round"}
 
 
 def run_port(cfg, budget_s):

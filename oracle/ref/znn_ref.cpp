@@ -2,9 +2,15 @@
 // with the Eigen-subset shim; see build.sh). TEST / BASELINE INFRASTRUCTURE
 // ONLY — never linked into the product.
 //
-//   znn_ref bench <spec> <x,y,z> <threads> <budget_s> <direct|auto|fft>
+//   znn_ref bench <spec> <x,y,z> <threads> <warmup> <rounds> <direct|auto|fft> [budget_s]
 //       times the reference task engine (engine<float>, engine.hpp:65-254) on
-//       one patch per round; prints {"rounds","warmup","seconds",...} JSON
+//       one patch per round: <warmup> rounds in one run(), then <rounds>
+//       measured rounds (one run() each, wall time around each; stops early
+//       once budget_s would be exceeded); prints {"rounds","warmup","seconds",
+//       "round_seconds",...} JSON
+//   znn_ref tune <spec> <x,y,z> <trials>
+//       the reference's autotune_modes (trainer.hpp:181-250): per-signature
+//       direct / FFT times and choices
 //   znn_ref estimate <spec> <x,y,z> <threads>
 //       per-edge task-body timing of one round, extrapolated (see estimate())
 //   znn_ref round <spec> <x,y,z> <params.f64> <inputs.f64> <labels.f64> <eta> <out.f64>
@@ -93,8 +99,10 @@ int bench(int argc, char** argv) {
     const std::string spec = read_file(argv[2]);
     const vec3i od = v3(argv[3]);
     const int threads = std::atoi(argv[4]);
-    const double budget = std::atof(argv[5]);
-    const std::string mode = argv[6];
+    const int warmup = std::atoi(argv[5]);
+    const int rounds = std::atoi(argv[6]);
+    const std::string mode = argv[7];
+    const double budget = argc > 8 ? std::atof(argv[8]) : 1e30;
     auto g = parse_netspec<float>(spec, od);
     init_weights(g, 1);
 
@@ -125,29 +133,62 @@ int bench(int argc, char** argv) {
     cfg.memoize = true;
     cfg.learning_rate = 0.01f;
     std::string chosen = "direct";
+    using clk = std::chrono::steady_clock;
+    double tune_s = 0;
     if (mode == "fft") {
         cfg.edge_modes.assign(g.edges.size(), conv_engine::fft);
         chosen = "fft";
     } else if (mode == "auto") {
-        cfg.edge_modes = autotune_modes(g, 3);
+        const auto t0 = clk::now();
+        cfg.edge_modes = autotune_modes(g, 3);  // the reference's default policy (trainer.hpp:41)
+        tune_s = std::chrono::duration<double>(clk::now() - t0).count();
         int nf = 0;
         for (auto m : cfg.edge_modes) nf += m == conv_engine::fft;
         chosen = "auto(" + std::to_string(nf) + " fft edges)";
     }
     engine<float> eng(g, compute_priorities(g), cfg);
-    using clk = std::chrono::steady_clock;
+    // warm-up rounds (pools, plans) in one pipelined run, as train() runs them
     auto t0 = clk::now();
-    eng.run(1, src);  // warm-up round: pools, plans
+    if (warmup > 0) eng.run(warmup, src);
     const double warm = std::chrono::duration<double>(clk::now() - t0).count();
-    std::int64_t rounds = std::int64_t(budget / std::max(warm, 1e-6));
-    if (rounds < 1) rounds = 1;
-    if (rounds > 1000) rounds = 1000;
+    // measured rounds one run() call each (no overlap with the warm-up or
+    // each other), wall time around each; stop early past the budget
+    std::vector<double> per;
     t0 = clk::now();
-    eng.run(rounds, src);
+    for (int r = 0; r < rounds; ++r) {
+        const auto a = clk::now();
+        eng.run(1, src);
+        per.push_back(std::chrono::duration<double>(clk::now() - a).count());
+        if (std::chrono::duration<double>(clk::now() - t0).count() + warm + per.back() > budget) break;
+    }
     const double sec = std::chrono::duration<double>(clk::now() - t0).count();
-    std::printf("{\"rounds\": %lld, \"warmup\": 1, \"seconds\": %.6f, \"warmup_seconds\": %.6f, \"threads\": %d, "
-                "\"mode\": \"%s\"}\n",
-                (long long)rounds, sec, warm, threads, chosen.c_str());
+    std::printf("{\"rounds\": %zu, \"warmup\": %d, \"seconds\": %.6f, \"warmup_seconds\": %.6f, "
+                "\"autotune_seconds\": %.3f, \"threads\": %d, \"mode\": \"%s\", \"round_seconds\": [",
+                per.size(), warmup, sec, warm, tune_s, threads, chosen.c_str());
+    for (size_t i = 0; i < per.size(); ++i) std::printf("%s%.4f", i ? ", " : "", per[i]);
+    std::printf("]}\n");
+    return 0;
+}
+
+// The reference's own layerwise autotuner (autotune_modes, trainer.hpp:
+// 181-250) on a netspec: per signature the direct and FFT fwd+bwd+upd
+// times and the choice, without running a round.
+int tune(int argc, char** argv) {
+    const std::string spec = read_file(argv[2]);
+    auto g = parse_netspec<float>(spec, v3(argv[3]));
+    init_weights(g, 1);
+    std::vector<autotune_choice<float>> rep;
+    auto modes = autotune_modes(g, std::atoi(argv[4]), &rep);
+    int nf = 0;
+    for (auto m : modes) nf += m == conv_engine::fft;
+    std::printf("{\"fft_edges\": %d, \"signatures\": [", nf);
+    for (size_t i = 0; i < rep.size(); ++i)
+        std::printf("%s{\"in\": \"%s\", \"k\": \"%s\", \"s\": \"%s\", \"direct_s\": %.5f, \"fft_s\": %.5f, "
+                    "\"chosen\": \"%s\"}",
+                    i ? ", " : "", rep[i].image_dims.str().c_str(), rep[i].kernel_dims.str().c_str(),
+                    rep[i].sparsity.str().c_str(), rep[i].direct_seconds, rep[i].fft_seconds,
+                    rep[i].chosen == conv_engine::fft ? "fft" : "direct");
+    std::printf("]}\n");
     return 0;
 }
 
@@ -273,7 +314,8 @@ int conv(int argc, char** argv) {
 int main(int argc, char** argv) {
     try {
         const std::string cmd = argc > 1 ? argv[1] : "";
-        if (cmd == "bench" && argc == 7) return bench(argc, argv);
+        if (cmd == "bench" && (argc == 8 || argc == 9)) return bench(argc, argv);
+        if (cmd == "tune" && argc == 5) return tune(argc, argv);
         if (cmd == "round" && argc == 9) return round_(argc, argv);
         if (cmd == "estimate" && argc == 5) return estimate(argc, argv);
         if (cmd == "maxfilter" && argc == 8) return maxfilter(argc, argv);

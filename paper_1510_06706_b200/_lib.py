@@ -29,6 +29,12 @@ EXPORTS = [
     "znn_net_step_host", "znn_net_forward_backward", "znn_net_apply_update", "znn_net_train_step",
     "znn_net_grad_buffer", "znn_net_forward", "znn_net_group_info",
     "znn_net_get_group_image", "znn_net_get_mask", "znn_fft_cmac_time", "znn_fma_peak_tflops",
+    "znn_fft_plan_create", "znn_fft_plan_destroy", "znn_fft_plan_info", "znn_fft_conv_fwd",
+    "znn_fft_conv_bwd", "znn_fft_plan_counts", "znn_autotune_layer",
+    "znn_comm_unique_id", "znn_comm_create", "znn_comm_destroy", "znn_allreduce", "znn_net_train_step_dp",
+    "znn_net_set_graph", "znn_net_graph_captured", "znn_mem_stats",
+    "znn_volume_write", "znn_volume_read", "znn_loader_open_dir", "znn_loader_open_host",
+    "znn_loader_size", "znn_loader_destroy", "znn_net_step_loader", "znn_profile_enable", "znn_profile_report",
 ]
 
 
@@ -111,6 +117,30 @@ def lib():
         "znn_net_get_mask": (ci, [vp, ci, P32]),
         "znn_fft_cmac_time": (ci, [vp, ci, i64, i64, i64, P64, P64, P64, ci, Pf, P64]),
         "znn_fma_peak_tflops": (ci, [vp, Pf]),
+        "znn_fft_plan_create": (ci, [vp, i64, i64, i64, P64, P64, P64, ctypes.POINTER(vp)]),
+        "znn_fft_plan_destroy": (ci, [vp]),
+        "znn_fft_plan_info": (ci, [vp, P64, P64, P64]),
+        "znn_fft_conv_fwd": (ci, [vp, vp, vp, vp, ci, vp]),
+        "znn_fft_conv_bwd": (ci, [vp, vp, vp, vp, vp]),
+        "znn_fft_plan_counts": (ci, [vp, P64]),
+        "znn_autotune_layer": (ci, [vp, i64, i64, i64, P64, P64, P64, ci, ctypes.POINTER(ci), Pf]),
+        "znn_comm_unique_id": (ci, [vp]),
+        "znn_comm_create": (ci, [vp, vp, ci, ci, ctypes.POINTER(vp)]),
+        "znn_comm_destroy": (ci, [vp]),
+        "znn_allreduce": (ci, [vp, vp, i64]),
+        "znn_net_train_step_dp": (ci, [vp, vp, vp, vp, Pd]),
+        "znn_net_set_graph": (ci, [vp, ci]),
+        "znn_net_graph_captured": (ci, [vp, ctypes.POINTER(ci)]),
+        "znn_mem_stats": (ci, [vp, P64]),
+        "znn_volume_write": (ci, [ctypes.c_char_p, P64, vp]),
+        "znn_volume_read": (ci, [ctypes.c_char_p, P64, vp, i64]),
+        "znn_loader_open_dir": (ci, [vp, ctypes.c_char_p, i64, ctypes.POINTER(vp)]),
+        "znn_loader_open_host": (ci, [vp, vp, vp, i64, i64, ctypes.POINTER(vp)]),
+        "znn_loader_size": (ci, [vp, P64]),
+        "znn_loader_destroy": (ci, [vp]),
+        "znn_net_step_loader": (ci, [vp, vp, Pd]),
+        "znn_profile_enable": (ci, [vp, ci]),
+        "znn_profile_report": (ci, [vp, ctypes.c_char_p, i64]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

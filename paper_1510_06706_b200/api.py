@@ -195,6 +195,30 @@ class Net:
         self._c(lib().znn_net_forward(self._h, ctypes.c_void_p(ip), _fptr(out)))
         return out
 
+    def set_graph(self, on=True):
+        """CUDA-graph mode for train_step / step_host / step_loader (the first
+        step eager, then one captured graph per input buffer pair)."""
+        self._c(lib().znn_net_set_graph(self._h, 1 if on else 0))
+
+    def graph_captured(self) -> bool:
+        v = ctypes.c_int()
+        self._c(lib().znn_net_graph_captured(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
+    def train_step_dp(self, comm, inputs_dev, labels_dev, sync_loss=True):
+        """Data-parallel step: per-layer NCCL allreduce overlapped with the backward, then the update."""
+        ip = inputs_dev if isinstance(inputs_dev, int) else inputs_dev.data_ptr()
+        lp = labels_dev if isinstance(labels_dev, int) else labels_dev.data_ptr()
+        loss = ctypes.c_double()
+        self._c(lib().znn_net_train_step_dp(self._h, comm.handle, ctypes.c_void_p(ip), ctypes.c_void_p(lp),
+                                            ctypes.byref(loss) if sync_loss else None))
+        return loss.value if sync_loss else None
+
+    def step_loader(self, loader) -> float:
+        loss = ctypes.c_double()
+        self._c(lib().znn_net_step_loader(self._h, loader.handle, ctypes.byref(loss)))
+        return loss.value
+
     def group_info(self, g):
         maps, d = ctypes.c_int64(), (ctypes.c_int64 * 3)()
         self._c(lib().znn_net_group_info(self._h, g, ctypes.byref(maps), d))
@@ -365,3 +389,174 @@ class ops:
         check(lib().znn_fma_peak_tflops(ctx.handle, ctypes.byref(t)), ctx.handle)
         return t.value
 
+
+
+def mem_stats(ctx: Context) -> dict:
+    """Device free/total bytes and the library's own device allocations so far."""
+    out = (ctypes.c_int64 * 4)()
+    check(lib().znn_mem_stats(ctx.handle, out), ctx.handle)
+    return {"free": int(out[0]), "total": int(out[1]), "allocs": int(out[2]), "alloc_bytes": int(out[3])}
+
+
+class FftPlan:
+    """FFT engine for one fully connected layer (fft_plan_cache + memo_store,
+    fft.hpp:57-192 / conv_fft.hpp:127-192): forward memoises the image and
+    kernel spectra; backward gives dx (optional) and dw from that memo."""
+
+    def __init__(self, ctx: Context, B, f_in, f_out, n, k, s=(1, 1, 1)):
+        self.ctx = ctx
+        self.B, self.f_in, self.f_out = int(B), int(f_in), int(f_out)
+        self.n, self.k, self.s = tuple(n), tuple(k), tuple(s)
+        self.m = tuple(self.n[a] - self.s[a] * (self.k[a] - 1) for a in range(3))
+        self._h = ctypes.c_void_p()
+        check(lib().znn_fft_plan_create(ctx.handle, self.B, self.f_in, self.f_out, v3(n), v3(k), v3(s),
+                                        ctypes.byref(self._h)), ctx.handle)
+
+    def info(self):
+        pads, bins, kb = (ctypes.c_int64 * 3)(), ctypes.c_int64(), ctypes.c_int64()
+        check(lib().znn_fft_plan_info(self._h, pads, ctypes.byref(bins), ctypes.byref(kb)), self.ctx.handle)
+        return {"pads": tuple(pads), "bins": bins.value, "kernel_spectrum_bytes": kb.value}
+
+    def forward(self, x, w, bias=None, act="none"):
+        import torch
+        y = torch.empty((self.B, self.f_out) + self.m, device=x.device, dtype=torch.float32)
+        check(lib().znn_fft_conv_fwd(self._h, _ptr(x), _ptr(w), _ptr(bias), ACT[act], _ptr(y)), self.ctx.handle)
+        return y
+
+    def backward(self, g, w, want_dx=True):
+        import torch
+        dw = torch.empty((self.f_out, self.f_in) + self.k, device=g.device, dtype=torch.float32)
+        dx = torch.empty((self.B, self.f_in) + self.n, device=g.device, dtype=torch.float32) if want_dx else None
+        check(lib().znn_fft_conv_bwd(self._h, _ptr(g), _ptr(w), _ptr(dw), _ptr(dx)), self.ctx.handle)
+        return dx, dw
+
+    def counts(self):
+        out = (ctypes.c_int64 * 9)()
+        check(lib().znn_fft_plan_counts(self._h, out), self.ctx.handle)
+        keys = [f"{p}_{k}" for p in ("fwd", "bwd", "upd") for k in ("image", "kernel", "inverse")]
+        return dict(zip(keys, [int(v) for v in out]))
+
+    def close(self):
+        if self._h:
+            lib().znn_fft_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def autotune_layer(ctx: Context, B, f_in, f_out, n, k, s=(1, 1, 1), trials=3):
+    """Per-layer engine choice by device timing (autotune_modes, trainer.hpp:181-250):
+    returns (engine name, {engine: median ms of fwd+dgrad+wgrad})."""
+    chosen = ctypes.c_int()
+    ms = (ctypes.c_float * 3)()
+    check(lib().znn_autotune_layer(ctx.handle, int(B), int(f_in), int(f_out), v3(n), v3(k), v3(s), int(trials),
+                                   ctypes.byref(chosen), ms), ctx.handle)
+    names = {0: "direct", 1: "fft", 3: "simt"}
+    times = {nm: float(ms[i]) for i, nm in enumerate(("direct", "fft", "simt")) if ms[i] >= 0}
+    return names[chosen.value], times
+
+
+class Comm:
+    """NCCL communicator of one rank (znn_comm); the 128-byte id comes from
+    comm_unique_id() on rank 0 and is shared by the caller."""
+
+    def __init__(self, ctx: Context, unique_id: bytes, nranks: int, rank: int):
+        self.ctx = ctx
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        self._h = ctypes.c_void_p()
+        check(lib().znn_comm_create(ctx.handle, buf, int(nranks), int(rank), ctypes.byref(self._h)), ctx.handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def allreduce(self, t):
+        check(lib().znn_allreduce(self._h, _ptr(t), t.numel()), self.ctx.handle)
+
+    def close(self):
+        if self._h:
+            lib().znn_comm_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().znn_comm_unique_id(buf))
+    return buf.raw
+
+
+def write_volume(path: str, vol: np.ndarray):
+    """ZNNV file (volume_io.hpp:15-86) from a 3-D float array (x-major)."""
+    v = np.ascontiguousarray(vol, dtype=np.float32)
+    assert v.ndim == 3
+    check(lib().znn_volume_write(path.encode(), v3(v.shape), v.ctypes.data_as(ctypes.c_void_p)))
+
+
+def read_volume(path: str) -> np.ndarray:
+    d = (ctypes.c_int64 * 3)()
+    check(lib().znn_volume_read(path.encode(), d, None, 0))
+    out = np.empty(tuple(d), dtype=np.float32)
+    check(lib().znn_volume_read(path.encode(), d, out.ctypes.data_as(ctypes.c_void_p), out.size))
+    return out
+
+
+class Loader:
+    """Data provider (trainer.hpp:87-166) with pinned double-buffered H2D:
+    from a directory (inputs/ + labels/ ZNNV files) or host arrays."""
+
+    def __init__(self, net: Net, directory: str = None, inputs=None, labels=None, shard_offset: int = 0):
+        self.net = net
+        self._h = ctypes.c_void_p()
+        self._keep = None
+        if directory is not None:
+            check(lib().znn_loader_open_dir(net._h, directory.encode(), int(shard_offset), ctypes.byref(self._h)),
+                  net.ctx.handle)
+        else:
+            ip = inputs.data_ptr() if hasattr(inputs, "data_ptr") else inputs.ctypes.data
+            lp = labels.data_ptr() if hasattr(labels, "data_ptr") else labels.ctypes.data
+            samples = inputs.shape[0]
+            self._keep = (inputs, labels)
+            check(lib().znn_loader_open_host(net._h, ctypes.c_void_p(ip), ctypes.c_void_p(lp), int(samples),
+                                             int(shard_offset), ctypes.byref(self._h)), net.ctx.handle)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __len__(self):
+        n = ctypes.c_int64()
+        check(lib().znn_loader_size(self._h, ctypes.byref(n)))
+        return n.value
+
+    def close(self):
+        if self._h:
+            lib().znn_loader_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def profile_enable(ctx: Context, on=True):
+    check(lib().znn_profile_enable(ctx.handle, 1 if on else 0), ctx.handle)
+
+
+def profile_report(ctx: Context):
+    """[{kernel, launches, ms, bytes, flops}] recorded since the last report."""
+    import json
+    buf = ctypes.create_string_buffer(1 << 20)
+    check(lib().znn_profile_report(ctx.handle, buf, len(buf)), ctx.handle)
+    return json.loads(buf.value.decode())

@@ -5,66 +5,40 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
 #include <vector>
 
+#include "capi_internal.hpp"
 #include "fft.hpp"
-#include "net.hpp"
-#include "ops.hpp"
-
-struct znn_ctx_s {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    std::string err;
-    znn_gpu::scratch ws;
-};
-
-struct znn_net_s {
-    znn_ctx ctx = nullptr;
-    std::unique_ptr<znn_exec::executor> ex;
-};
 
 namespace {
 
-thread_local std::string g_orphan_err;
-
-template <typename F>
-int guarded(znn_ctx ctx, F&& body) {
-    std::string* err = ctx ? &ctx->err : &g_orphan_err;
-    try {
-        if (ctx) {
-            cudaError_t e = cudaSetDevice(ctx->device);
-            if (e != cudaSuccess) throw znn_gpu::cuda_error(cudaGetErrorString(e));
-        }
-        body();
-        return ZNN_OK;
-    } catch (const znn_gpu::shape_error& e) {
-        *err = e.what();
-        return ZNN_ERR_SHAPE;
-    } catch (const std::exception& e) {
-        *err = e.what();
-        return ZNN_ERR_RUNTIME;
-    }
-}
-
-znn_gpu::dims3 D(const int64_t* p) {
-    if (!p) throw znn_gpu::shape_error("null dims pointer");
-    return znn_gpu::dims3{p[0], p[1], p[2]};
-}
+using znn_capi::D;
+using znn_capi::g_orphan_err;
+using znn_capi::guarded;
 
 const int32_t* kinds_to_device(znn_ctx ctx, const int32_t* kinds_host, int64_t f) {
-    // small per-call upload into the context scratch tail
+    // per-map kinds into the context's grow-only device array (no per-call allocation)
     static thread_local std::vector<int32_t> tmp;
     tmp.assign(kinds_host, kinds_host + f);
     for (int32_t k : tmp)
         if (k < 0 || k > 3) throw znn_gpu::shape_error("transfer: unknown transfer kind");
-    int32_t* d = nullptr;
-    ZNN_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(int32_t) * size_t(f), ctx->stream));
-    ZNN_CUDA_CHECK(cudaMemcpyAsync(d, tmp.data(), sizeof(int32_t) * size_t(f), cudaMemcpyHostToDevice,
+    if (f > ctx->kinds_cap) {
+        if (ctx->kinds) {
+            ZNN_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+            cudaFree(ctx->kinds);
+            ctx->kinds = nullptr;
+            ctx->kinds_cap = 0;
+        }
+        znn_gpu::dmalloc(&ctx->kinds, sizeof(int32_t) * size_t(std::max<int64_t>(f, 256)));
+        ctx->kinds_cap = std::max<int64_t>(f, 256);
+    }
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(ctx->kinds, tmp.data(), sizeof(int32_t) * size_t(f), cudaMemcpyHostToDevice,
                                    ctx->stream));
-    return d;
+    return ctx->kinds;
 }
 
 }  // namespace
@@ -201,7 +175,6 @@ int znn_transfer_fwd(znn_ctx ctx, const float* x, int64_t B, int64_t f, int64_t 
     return guarded(ctx, [&] {
         const int32_t* kd = kinds_to_device(ctx, kinds_host, f);
         znn_gpu::transfer_fwd(ctx->stream, x, B, f, voxels, kd, bias, y);
-        ZNN_CUDA_CHECK(cudaFreeAsync(const_cast<int32_t*>(kd), ctx->stream));
     });
 }
 
@@ -211,7 +184,6 @@ int znn_transfer_bwd(znn_ctx ctx, const float* g, const float* xy, int from_outp
     return guarded(ctx, [&] {
         const int32_t* kd = kinds_to_device(ctx, kinds_host, f);
         znn_gpu::transfer_bwd(ctx->stream, g, xy, from_output != 0, B, f, voxels, kd, bias, gx, dbias, ctx->ws);
-        ZNN_CUDA_CHECK(cudaFreeAsync(const_cast<int32_t*>(kd), ctx->stream));
     });
 }
 
@@ -260,7 +232,9 @@ int znn_net_create(znn_ctx ctx, const char* netspec, const int64_t* out_dims,
         c.loss = cfg->loss;
         c.engine = cfg->engine == ZNN_CONV_AUTO ? ZNN_CONV_DIRECT : cfg->engine;
         c.sliding = cfg->sliding != 0;
-        c.keep_images = getenv("ZNN_KEEP_IMAGES") == nullptr || std::string(getenv("ZNN_KEEP_IMAGES")) != "0";
+        // per-group backward images only on request (tests/inspection); the
+        // default is two ping-pong gradient buffers
+        c.keep_images = getenv("ZNN_KEEP_IMAGES") != nullptr && std::string(getenv("ZNN_KEEP_IMAGES")) == "1";
         znn_host::v3 od{0, 0, 0};
         if (out_dims) od = znn_host::v3{out_dims[0], out_dims[1], out_dims[2]};
         auto* n = new znn_net_s;
@@ -365,7 +339,7 @@ int znn_net_forward_backward(znn_net net, const float* inputs_dev, const float* 
 int znn_net_train_step(znn_net net, const float* inputs_dev, const float* labels_dev, double* loss) {
     return guarded(net->ctx, [&] {
         net->ex->set_stream(net->ctx->stream);
-        const double l = net->ex->forward_backward(inputs_dev, labels_dev, loss != nullptr, true);
+        const double l = net->ex->train_step(inputs_dev, labels_dev, loss != nullptr);
         if (loss) *loss = l;
     });
 }

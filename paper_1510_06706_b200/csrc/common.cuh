@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 namespace znn_gpu {
 
@@ -33,14 +34,56 @@ inline void require(bool cond, const std::string& what) {
 // launch_check so the context can count its own launches (gpu_launches).
 struct launch_stats {
     int64_t launches = 0;
+    int64_t allocs = 0;        // device allocations made by the library itself
+    int64_t alloc_bytes = 0;
 };
 launch_stats& stats();
+
+// Every internal device allocation goes through dmalloc so the steady state
+// can be checked for zero allocations (reference acceptance.cpp:637-656).
+template <typename T>
+inline void dmalloc(T** p, size_t bytes) {
+    void* v = nullptr;
+    const cudaError_t e = cudaMalloc(&v, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw cuda_error("cudaMalloc(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+    }
+    stats().allocs++;
+    stats().alloc_bytes += int64_t(bytes);
+    *p = static_cast<T*>(v);
+}
 
 inline void launch_check(const char* what) {
     stats().launches++;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
+
+// In-step kernel timing (bench.py's roofline): with profiling on, a
+// prof_scope records a CUDA event pair on the launch stream around one
+// launch; report() aggregates per kernel label (launches, total ms, and the
+// algorithmic bytes / flops the caller declared per launch). Off by default;
+// never active inside a stream capture.
+struct prof_entry {
+    std::string name;
+    int64_t launches = 0;
+    double ms = 0, bytes = 0, flops = 0;
+};
+void prof_enable(bool on);
+bool prof_on();
+std::vector<prof_entry> prof_report();  // synchronises on the recorded events, then clears
+class prof_scope {
+public:
+    prof_scope(cudaStream_t st, std::string name, double bytes, double flops);
+    ~prof_scope();
+    prof_scope(const prof_scope&) = delete;
+    prof_scope& operator=(const prof_scope&) = delete;
+
+private:
+    cudaStream_t st_;
+    int slot_ = -1;
+};
 
 struct dims3 {
     int64_t x, y, z;

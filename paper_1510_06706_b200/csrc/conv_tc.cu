@@ -600,14 +600,27 @@ bool conv_tc_supported(const conv_shape& c, int pass) {
     return c.f_out >= 16 && c.n.vol() * c.f_in < (int64_t(1) << 31);
 }
 
+namespace {
+std::string tc_label(const char* k, const conv_shape& c) {
+    return std::string(k) + " f=" + std::to_string(c.f_in) + "->" + std::to_string(c.f_out) + " n=" +
+           std::to_string(c.n.x) + " k=" + std::to_string(c.k.x) + " s=" + std::to_string(c.s.x) + " B=" +
+           std::to_string(c.B);
+}
+double tc_flops(const conv_shape& c) { return 2.0 * double(c.B * c.f_in * c.f_out) * double(c.m.vol() * c.taps()); }
+}  // namespace
+
 void conv_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* w, const float* bias, int act,
                  float* y, scratch& ws) {
+    prof_scope ps(st, tc_label("conv_fwd_tc", c), 4.0 * double(c.B) * double(c.f_in * c.n.vol() + c.f_out * c.m.vol()),
+                  tc_flops(c));
     char* wsp = static_cast<char*>(ws.get(panel_bytes(int(c.f_in), int(c.f_out), c.taps())));
     launch_valid(st, c.B, int(c.f_in), int(c.f_out), int(c.f_in), c.n, c.k, c.s, x, w, 0, bias, act, y, wsp,
                  dims3{0, 0, 0}, c.n, "conv_fwd_tc");
 }
 
 void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const float* w, float* dx, scratch& ws) {
+    prof_scope ps(st, tc_label("conv_dgrad_tc", c), 4.0 * double(c.B) * double(c.f_in * c.n.vol() + c.f_out * c.m.vol()),
+                  tc_flops(c));
     const dims3 P{c.s.x * (c.k.x - 1), c.s.y * (c.k.y - 1), c.s.z * (c.k.z - 1)};
     const dims3 gd{c.m.x + 2 * P.x, c.m.y + 2 * P.y, c.m.z + 2 * P.z};
     const size_t gbytes = sizeof(float) * size_t(c.B * c.f_out * gd.vol());

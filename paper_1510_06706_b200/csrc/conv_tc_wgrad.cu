@@ -470,6 +470,12 @@ int64_t resident_ctas(int ntmax, size_t smem, int csize, bool pair, int ng) {
 
 void conv_wgrad_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* g, float* dw, float scale,
                    scratch& ws, const sgd_fuse* upd) {
+    prof_scope ps(st,
+                  "conv_wgrad_tc f=" + std::to_string(c.f_in) + "->" + std::to_string(c.f_out) + " n=" +
+                      std::to_string(c.n.x) + " k=" + std::to_string(c.k.x) + " s=" + std::to_string(c.s.x) +
+                      " B=" + std::to_string(c.B),
+                  4.0 * double(c.B) * double(c.f_in * c.n.vol() + c.f_out * c.m.vol()),
+                  2.0 * double(c.B * c.f_in * c.f_out) * double(c.m.vol() * c.taps()));
     wg_params p;
     p.f_in = int(c.f_in);
     p.f_out = int(c.f_out);

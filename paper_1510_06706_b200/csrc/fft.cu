@@ -1090,8 +1090,12 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_ss_k(const float2* __restri
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nl = lane & 7, bl = lane >> 3;
     const int nbb = (B + BB - 1) / BB;
-    const int n0 = int(blockIdx.x / nbb) * CNB, b0 = int(blockIdx.x % nbb) * BB;
-    const int64_t w0 = int64_t(blockIdx.y) * CBINS;
+    // 1-D grid: the (n block, patch block) tiles of one bin block adjacent
+    // (S rows re-read from L2), bin blocks outermost (no 65535 grid.y limit)
+    const int nxb = ((nn + CNB - 1) / CNB) * nbb;
+    const int bx = int(blockIdx.x % unsigned(nxb));
+    const int n0 = (bx / nbb) * CNB, b0 = (bx % nbb) * BB;
+    const int64_t w0 = int64_t(blockIdx.x / unsigned(nxb)) * CBINS;
     // staging: thread -> (row, pair q); K rows (rr, n) for rr = j, S rows
     // (rr, b) for rr = rs + j * (32 / BB); per chunk the sources advance by
     // CRC reduction steps
@@ -1216,8 +1220,11 @@ __global__ void __launch_bounds__(C_THREADS, 2) cmac_upd_ss_k(const float2* __re
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ol = lane & 7, il = lane >> 3;
     const int nib = (f + UI - 1) / UI;
-    const int i0 = int(blockIdx.x % nib) * UI, o0 = int(blockIdx.x / nib) * UO;
-    const int64_t w0 = int64_t(blockIdx.y) * CBINS;
+    // 1-D grid: (o block, i block) tiles of one bin block adjacent, bin blocks outermost
+    const int nxb = nib * ((fo + UO - 1) / UO);
+    const int bx = int(blockIdx.x % unsigned(nxb));
+    const int i0 = (bx % nib) * UI, o0 = (bx / nib) * UO;
+    const int64_t w0 = int64_t(blockIdx.x / unsigned(nxb)) * CBINS;
     // staging: thread -> (row, pair q); G rows (bb = j, o = trow), X rows
     // (bb = xb + 2 j, i = trow % 16); per chunk the sources advance UB patches
     const int q = threadIdx.x & 7, trow = threadIdx.x >> 3;  // trow < 32
@@ -1325,11 +1332,15 @@ struct plan {
 kpool::~kpool() { cudaFree(buf); }
 float2* kpool::get(int64_t need) {
     if (need > bytes) {
-        if (buf) ZNN_CUDA_CHECK(cudaFree(buf));
-        buf = nullptr;
-        ZNN_CUDA_CHECK(cudaMalloc(&buf, size_t(need)));
-        bytes = need;
         owner = nullptr;
+        if (buf) {
+            float2* old = buf;
+            buf = nullptr;  // consistent state even if the new allocation fails
+            bytes = 0;
+            ZNN_CUDA_CHECK(cudaFree(old));
+        }
+        znn_gpu::dmalloc(&buf, size_t(need));
+        bytes = need;
     }
     return buf;
 }
@@ -1415,7 +1426,9 @@ template <bool CONJ, int TB>
 void cmac_ss_launch(cudaStream_t st, const float2* S, const float2* K, float2* O, int B, int nr, int nn, int64_t kn,
                     int64_t kr, int64_t bins) {
     constexpr size_t smem = cmac_smem<TB>();
-    const dim3 grid(unsigned(ceil_div(nn, CNB) * ceil_div(B, 4 * TB)), unsigned(ceil_div(bins, CBINS)), 1u);
+    const int64_t nblk = ceil_div(nn, CNB) * ceil_div(B, 4 * TB) * ceil_div(bins, CBINS);
+    require(nblk < (int64_t(1) << 31), "fft cmac: grid exceeds 2^31 blocks");
+    const dim3 grid(unsigned(nblk), 1u, 1u);
     allow_smem(cmac_ss_k<CONJ, TB>, smem);
     cmac_ss_k<CONJ, TB><<<grid, C_THREADS, smem, st>>>(S, K, O, B, nr, nn, kn, kr, bins);
 }
@@ -1437,6 +1450,14 @@ void cmac_ss(cudaStream_t st, const float2* S, const float2* K, float2* O, int B
         go(std::integral_constant<int, 2>{});
     else
         go(std::integral_constant<int, 4>{});
+}
+
+void cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, int B, int f, int fo, int64_t bins) {
+    require(bins % 2 == 0, "fft cmac: odd bin count");
+    const int64_t nblk = ceil_div(f, UI) * ceil_div(fo, UO) * ceil_div(bins, CBINS);
+    require(nblk < (int64_t(1) << 31), "fft cmac: grid exceeds 2^31 blocks");
+    allow_smem(cmac_upd_ss_k, kUpdSmem);
+    cmac_upd_ss_k<<<unsigned(nblk), C_THREADS, kUpdSmem, st>>>(X, G, DK, B, f, fo, bins);
 }
 
 // forward 3D R2C of imgs real volumes (valid dims n, image stride in floats):
@@ -1580,6 +1601,21 @@ int64_t kernel_spectrum_bytes(const conv_shape& c) {
     return c.f_in * c.f_out * P.x * P.y * (P.z / 2 + 1) * int64_t(sizeof(float2));
 }
 
+int64_t image_spectrum_bytes(const conv_shape& c) {
+    const dims3 P = pads_for(c);
+    return c.B * c.f_in * P.x * P.y * (P.z / 2 + 1) * int64_t(sizeof(float2));
+}
+
+// the scratch-arena bytes conv_fwd / conv_bwd ask for (the larger of the two)
+int64_t workspace_bytes(const conv_shape& c) {
+    const dims3 P = pads_for(c);
+    const int64_t Zh = P.z / 2 + 1, bins = P.x * P.y * Zh, c8 = int64_t(sizeof(float2));
+    const int64_t fwd = c8 * (c.B * c.f_out * bins + c.B * c.f_out * Zh * c.m.x * c.m.y) + 1024;
+    const int64_t cc = std::max(c.B * c.f_in * Zh * c.n.x * c.n.y, c.f_out * c.f_in * Zh * c.k.x * c.k.y);
+    const int64_t bwd = c8 * (c.B * c.f_out * bins + c.B * c.f_in * bins + cc) + 2048;
+    return std::max(fwd, bwd);
+}
+
 bool supported(const conv_shape& c) {
     const dims3 P = pads_for(c);
     if (P.x > MAXP || P.y > MAXP || P.z > MAXP) return false;
@@ -1596,9 +1632,9 @@ plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool) {
     p->bins = p->P.x * p->P.y * p->Zh;
     p->B = c.B, p->f = c.f_in, p->fo = c.f_out;
     const dims3 e{c.s.x * (c.k.x - 1) + 1, c.s.y * (c.k.y - 1) + 1, c.s.z * (c.k.z - 1) + 1};
-    ZNN_CUDA_CHECK(cudaMalloc(&p->X, sizeof(float2) * size_t(c.B * c.f_in * p->bins)));
+    znn_gpu::dmalloc(&p->X, sizeof(float2) * size_t(c.B * c.f_in * p->bins));
     p->pool = std::move(pool);
-    if (!p->pool) ZNN_CUDA_CHECK(cudaMalloc(&p->K, sizeof(float2) * size_t(c.f_out * c.f_in * p->bins)));
+    if (!p->pool) znn_gpu::dmalloc(&p->K, sizeof(float2) * size_t(c.f_out * c.f_in * p->bins));
     (void)e;  // the dilated-kernel buffer is allocated on first use (dense-kernel path only)
     return p;
 }
@@ -1645,7 +1681,7 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
             p.k_valid = true;
         return;
     }
-    if (!p.dil) ZNN_CUDA_CHECK(cudaMalloc(&p.dil, sizeof(float) * size_t(nker * e.vol())));
+    if (!p.dil) znn_gpu::dmalloc(&p.dil, sizeof(float) * size_t(nker * e.vol()));
     ZNN_CUDA_CHECK(cudaMemsetAsync(p.dil, 0, sizeof(float) * size_t(nker * e.vol()), st));
     const int64_t ntaps = nker * c.k.vol();
     dilate_k<<<unsigned(std::min<int64_t>(ceil_div(ntaps, 256), 148 * 16)), 256, 0, st>>>(
@@ -1660,15 +1696,32 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
 
 }  // namespace
 
+namespace {
+std::string lbl(const char* k, const conv_shape& c, const plan& p) {
+    return std::string(k) + " f=" + std::to_string(c.f_in) + "->" + std::to_string(c.f_out) + " B=" +
+           std::to_string(c.B) + " P=" + std::to_string(p.P.y) + " bins=" + std::to_string(p.bins);
+}
+double cmac_bytes(const conv_shape& c, const plan& p) {
+    return 8.0 * double(p.bins) * double(c.f_in * c.f_out + c.B * c.f_in + c.B * c.f_out);
+}
+double cmac_flops(const conv_shape& c, const plan& p) { return 8.0 * double(c.B * c.f_in * c.f_out) * double(p.bins); }
+}  // namespace
+
 void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
               int act, float* y, znn_gpu::scratch& ws) {
     require(p.B == c.B && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
     const int64_t nker = c.f_out * c.f_in;
     // image spectra (memoised for the backward / update passes)
-    forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X);
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_image_fwd", c, p), double(c.B * c.f_in) * (4.0 * c.n.vol() + 8.0 * p.bins), 0);
+        forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X);
+    }
     p.cnt.fwd_image += c.B * c.f_in;
     // kernel spectra of the dilated kernels (memoised for the backward pass)
-    kernel_spectra(st, p, c, w);
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_kspec", c, p), 8.0 * double(nker) * double(p.bins), 0);
+        kernel_spectra(st, p, c, w);
+    }
     p.cnt.fwd_kernel += nker;
     const float2* K = kbuf(p);
     // Y = sum_i X * conj(K), one inverse per output node, crop + bias + transfer
@@ -1693,9 +1746,15 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     char* cur = static_cast<char*>(ws.get(sizeof(float2) * size_t(c.B * c.f_out * p.bins + ccount) + 1024));
     float2* Y = carve(cur, c.B * c.f_out * p.bins);
     float2* CB = carve(cur, ccount);
-    cmac_ss(st, p.X, K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_cmac_fwd", c, p), cmac_bytes(c, p), cmac_flops(c, p));
+        cmac_ss(st, p.X, K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
+    }
     launch_check("fft_cmac_fwd");
-    inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB);
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_image_inv", c, p), double(c.B * c.f_out) * (8.0 * p.bins + 4.0 * c.m.vol()), 0);
+        inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB);
+    }
     p.cnt.fwd_inverse += c.B * c.f_out;
 }
 
@@ -1760,23 +1819,34 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
         p.cnt.upd_inverse += c.f_out * c.f_in;
         return;
     }
-    forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out);
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_grad_fwd", c, p), double(nB * c.f_out) * (4.0 * c.m.vol() + 8.0 * p.bins), 0);
+        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out);
+    }
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
-        cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
+        {
+            znn_gpu::prof_scope ps(st, lbl("fft_cmac_dgrad", c, p), cmac_bytes(c, p), cmac_flops(c, p));
+            cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
+        }
         launch_check("fft_cmac_bwd");
-        inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB);
+        {
+            znn_gpu::prof_scope ps(st, lbl("fft_dgrad_inv", c, p), double(nB * c.f_in) * (8.0 * p.bins + 4.0 * c.n.vol()), 0);
+            inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB);
+        }
         p.cnt.bwd_inverse += nB * c.f_in;
     }
     // kernel gradient: one gradient-specific inverse per edge, sampled at s*w
     {
-        const dim3 gu(unsigned(ceil_div(c.f_in, UI) * ceil_div(c.f_out, UO)), unsigned(ceil_div(p.bins, CBINS)), 1u);
-        allow_smem(cmac_upd_ss_k, kUpdSmem);
-        cmac_upd_ss_k<<<gu, C_THREADS, kUpdSmem, st>>>(p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
+        znn_gpu::prof_scope ps(st, lbl("fft_cmac_upd", c, p), cmac_bytes(c, p), cmac_flops(c, p));
+        cmac_upd(st, p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
     }
     launch_check("fft_cmac_upd");
     k_clobbered(p);
-    kernel_gradient_inverse(st, p, c, DK, gw, CB);
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_dkinv", c, p), 8.0 * double(c.f_out * c.f_in) * double(p.bins), 0);
+        kernel_gradient_inverse(st, p, c, DK, gw, CB);
+    }
     p.cnt.upd_inverse += c.f_out * c.f_in;
 }
 
@@ -1800,9 +1870,7 @@ float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64
         } else if (which == 1) {
             cmac_ss(st, G, K, X, int(B), int(fo), int(f), 1, f, bins, false);
         } else {
-            const dim3 gu(unsigned(ceil_div(f, UI) * ceil_div(fo, UO)), unsigned(ceil_div(bins, CBINS)), 1u);
-            allow_smem(cmac_upd_ss_k, kUpdSmem);
-            cmac_upd_ss_k<<<gu, C_THREADS, kUpdSmem, st>>>(X, G, K, int(B), int(f), int(fo), bins);
+            cmac_upd(st, X, G, K, int(B), int(f), int(fo), bins);
         }
         launch_check("fft_cmac_probe");
     };

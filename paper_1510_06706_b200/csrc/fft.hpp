@@ -50,6 +50,8 @@ struct kpool {
 };
 
 int64_t kernel_spectrum_bytes(const conv_shape& c);
+int64_t image_spectrum_bytes(const conv_shape& c);  // the memoised X of a plan
+int64_t workspace_bytes(const conv_shape& c);       // scratch arena of conv_fwd / conv_bwd
 bool supported(const conv_shape& c);
 plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool = nullptr);
 const transform_counts& counts(const plan& p);

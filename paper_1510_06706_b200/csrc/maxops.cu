@@ -280,6 +280,8 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
                    float* y, int32_t* mask) {
     const dims3 m{n.x - s.x * (k.x - 1), n.y - s.y * (k.y - 1), n.z - s.z * (k.z - 1)};
     require(m.x > 0 && m.y > 0 && m.z > 0, "maxfilter_forward: effective window exceeds input");
+    prof_scope ps(st, "maxfilter_fwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
+                  double(maps) * (4.0 * double(n.vol()) + 8.0 * double(m.vol())), 0);
     require(n.vol() < (int64_t(1) << 31), "maxfilter_forward: map exceeds int32 mask range");
     auto* kf = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_fwd_k<2, 2, 2>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2>
@@ -293,6 +295,8 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
 void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
                    dims3 k, dims3 s, float* dx) {
     const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
+    prof_scope ps(st, "maxfilter_bwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
+                  double(maps) * (8.0 * double(m.vol()) + 4.0 * double(n.vol())), 0);
     if (k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2) && maps < 65536) {
         const dim3 grid(unsigned(ceil_div(n.y, YR)), unsigned(maps));
         auto* kk = s.x == 1 ? maxfilter2_bwd_k<1> : maxfilter2_bwd_k<2>;

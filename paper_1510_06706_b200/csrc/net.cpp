@@ -54,12 +54,15 @@ executor::executor(const std::string& netspec, const v3* out_dims, const train_c
 }
 
 executor::~executor() {
+    for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
+    for (auto& L : layers_) L.fft.reset();
+    kpool_.reset();
     for (void* p : owned_) cudaFree(p);
 }
 
 void* executor::dalloc(size_t bytes) {
     void* p = nullptr;
-    ZNN_CUDA_CHECK(cudaMalloc(&p, bytes < 16 ? 16 : bytes));
+    znn_gpu::dmalloc(&p, bytes < 16 ? 16 : bytes);
     owned_.push_back(p);
     return p;
 }
@@ -338,6 +341,7 @@ void executor::set_layer_engine(int conv_layer, int engine) {
         if (L.kind == lkind::conv) {
             if (ci == conv_layer) {
                 require(engine == 0 || engine == 1 || engine == 3, "set_layer_engine: unknown engine");
+                if (L.engine != engine) drop_fft_plans();  // the spectra memory plan depends on the engines
                 L.engine = engine;
                 return;
             }
@@ -346,31 +350,117 @@ void executor::set_layer_engine(int conv_layer, int engine) {
     throw znn_gpu::shape_error("set_layer_engine: no conv layer " + std::to_string(conv_layer));
 }
 
-// Kernel spectra stay resident per layer (the reference's memo) while their
-// sum fits ZNN_FFT_RESIDENT_GB (default 48); beyond that the largest layers
-// share one buffer and recompute their spectra in the backward pass when
-// another layer overwrote them (c5: conv2 52 GB + conv3 30 GB share one
-// 52 GB buffer, conv4-6 keep 22 GB resident).
-bool executor::fft_pooled(const layer& L) const {
-    const bool member = &L >= layers_.data() && &L < layers_.data() + layers_.size();
-    if (!member) return false;  // autotune trial copies own their spectra
-    double budget_gb = 48.0;
-    if (const char* e = std::getenv("ZNN_FFT_RESIDENT_GB")) budget_gb = std::atof(e);
+// Memory plan of the FFT layers' kernel spectra (the big per-layer object,
+// f*f'*bins complex: 52 GB for c5 conv2). At the first FFT plan the budget
+// for all kernel spectra (shared buffer + resident) is taken from
+// cudaMemGetInfo: free memory minus every FFT layer's memoised image spectra,
+// the largest FFT scratch need and a headroom (ZNN_MEM_HEADROOM_GB, 20).
+// Layers keep their own spectra (the reference's memo) unless the sum does
+// not fit; then the largest layers share one buffer (kpool) and a layer whose
+// spectra were overwritten since its forward recomputes them in the backward
+// pass. ZNN_FFT_RESIDENT_GB overrides the budget (0 = all layers share).
+void executor::plan_fft_memory() {
+    fft_decided_ = true;
+    fft_pool_members_.clear();
     std::vector<std::pair<int64_t, const layer*>> sz;
-    int64_t total = 0;
+    int64_t total = 0, xspec = 0, wsmax = 0;
     for (const auto& M : layers_)
         if (M.kind == lkind::conv && M.engine == 1 && znn_fft::supported(M.shape)) {
             sz.emplace_back(znn_fft::kernel_spectrum_bytes(M.shape), &M);
             total += sz.back().first;
+            xspec += znn_fft::image_spectrum_bytes(M.shape);
+            wsmax = std::max(wsmax, znn_fft::workspace_bytes(M.shape));
         }
+    if (sz.empty()) return;
     std::sort(sz.begin(), sz.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
-    const double budget = budget_gb * double(int64_t(1) << 30);
-    for (const auto& [bytes, M] : sz) {
-        if (double(total) <= budget) break;
-        if (M == &L) return true;
-        total -= bytes;
+    if (const char* e = std::getenv("ZNN_FFT_RESIDENT_GB")) {
+        fft_budget_ = std::atof(e) * double(int64_t(1) << 30);
+    } else {
+        size_t fr = 0, tot = 0;
+        ZNN_CUDA_CHECK(cudaMemGetInfo(&fr, &tot));
+        double head = 20.0;
+        if (const char* h = std::getenv("ZNN_MEM_HEADROOM_GB")) head = std::atof(h);
+        const double have = double(fr) + double(ws_.capacity());  // the arena is re-grown to wsmax
+        fft_budget_ = have - double(xspec) - double(wsmax) * 1.25 - head * double(int64_t(1) << 30);
     }
-    return false;
+    // smallest j: the j largest layers share one buffer (its size = the
+    // largest), the others stay resident; j = 1 saves nothing over j = 0
+    const size_t n = sz.size();
+    size_t j = 0;
+    double rest = double(total);
+    for (; j <= n; ++j) {
+        const double mem = (j == 0 ? 0.0 : double(sz[0].first)) + rest;
+        if (j != 1 && mem <= fft_budget_) break;
+        if (j < n) rest -= double(sz[j].first);
+    }
+    if (j > n) j = n;  // nothing fits: every FFT layer shares the buffer
+    for (size_t q = 0; q < j; ++q) fft_pool_members_.push_back(sz[q].second);
+}
+
+bool executor::fft_pooled(const layer& L) {
+    const bool member = &L >= layers_.data() && &L < layers_.data() + layers_.size();
+    if (!member) return false;  // autotune trial copies own their spectra
+    if (!fft_decided_) plan_fft_memory();
+    return std::find(fft_pool_members_.begin(), fft_pool_members_.end(), &L) != fft_pool_members_.end();
+}
+
+void executor::drop_fft_plans() {
+    drop_graph();
+    for (auto& L : layers_) L.fft.reset();
+    kpool_.reset();
+    fft_decided_ = false;
+}
+
+void executor::drop_graph() {
+    for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
+    graphs_.clear();
+    graph_warm_ = 0;
+    ws_.freeze(false);
+}
+
+void executor::set_graph_mode(bool on) {
+    if (!on) drop_graph();
+    graph_mode_ = on;
+}
+
+double executor::train_step(const float* in, const float* lab, bool sync_loss) {
+    if (!graph_mode_ || st_ == nullptr)  // the legacy default stream cannot be captured
+        return forward_backward(in, lab, sync_loss, true);
+    if (graph_warm_ < 1) {  // first step eager: plans, spectra buffers and the arena reach full size
+        ++graph_warm_;
+        return forward_backward(in, lab, sync_loss, true);
+    }
+    cudaGraphExec_t exec = nullptr;
+    for (const auto& g : graphs_)
+        if (g.in == in && g.lab == lab) exec = g.exec;
+    if (!exec) {
+        if (graphs_.size() >= 4) {  // bounded cache: start over
+            for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
+            graphs_.clear();
+        }
+        ws_.freeze(true);
+        cudaGraph_t g = nullptr;
+        ZNN_CUDA_CHECK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeRelaxed));
+        try {
+            forward_backward(in, lab, false, true);
+        } catch (...) {
+            cudaStreamEndCapture(st_, &g);
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            ws_.freeze(false);
+            throw;
+        }
+        ZNN_CUDA_CHECK(cudaStreamEndCapture(st_, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) {
+            ws_.freeze(false);
+            throw znn_gpu::cuda_error(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+        }
+        graphs_.push_back(step_graph{in, lab, exec});
+    }
+    ZNN_CUDA_CHECK(cudaGraphLaunch(exec, st_));
+    return sync_loss ? last_loss_device() : 0.0;
 }
 
 znn_fft::plan& executor::fft_plan(layer& L) {
@@ -480,6 +570,15 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
     }
     znn_gpu::loss_grad_async(st_, cfg_.loss, G.act, lab, B * G.maps * vol, 1.f / float(cfg_.global_batch),
                              G.grad, loss_dev_, ws_);
+    // parameters of a layer are contiguous in the flat buffer: conv weights
+    // [f_out][f_in][T] then the fused transfer's biases; a transfer layer's biases
+    auto grad_ready = [&](const layer& L) {
+        if (!grad_hook_) return;
+        if (L.kind == lkind::conv)
+            grad_hook_(L.w_off, L.shape.f_out * L.shape.f_in * L.shape.taps() + (L.fused ? L.shape.f_out : 0));
+        else if (L.kind == lkind::transfer)
+            grad_hook_(L.b_off, int64_t(L.edge_ids.size()));
+    };
     // backward in reverse layer order
     for (size_t li = layers_.size(); li-- > 0;) {
         layer& L = layers_[li];
@@ -499,6 +598,7 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                     if (update)
                         znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off,
                                               L.shape.f_out, cfg_.lr, cfg_.mu);
+                    grad_ready(L);
                     break;
                 }
                 if (L.fused) {
@@ -516,6 +616,7 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                     znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off,
                                           L.shape.f_out, cfg_.lr, cfg_.mu);
                 run_conv_bwd(L, O.grad, I.grad, L.in != 0, update);
+                grad_ready(L);
                 break;
             }
             case lkind::transfer:
@@ -525,6 +626,7 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                 if (update)
                     znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off, I.maps,
                                           cfg_.lr, cfg_.mu);
+                grad_ready(L);
                 break;
             case lkind::pool:
                 if (L.in != 0) znn_gpu::maxpool_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, I.grad);
@@ -551,7 +653,7 @@ double executor::step_host(const float* in_host, const float* labels_host) {
     const int64_t B = cfg_.batch;
     ZNN_CUDA_CHECK(cudaMemcpyAsync(in_stage_, in_host, sizeof(float) * size_t(B * in_per_patch()), cudaMemcpyHostToDevice, st_));
     ZNN_CUDA_CHECK(cudaMemcpyAsync(lab_stage_, labels_host, sizeof(float) * size_t(B * out_per_patch()), cudaMemcpyHostToDevice, st_));
-    forward_backward(in_stage_, lab_stage_, false, true);
+    train_step(in_stage_, lab_stage_, false);
     return last_loss_device();
 }
 
@@ -611,19 +713,28 @@ std::vector<int> executor::autotune(int trials) {
             layer T = L;
             T.engine = e;
             std::vector<float> ts;
-            for (int t = 0; t <= trials; ++t) {
-                ZNN_CUDA_CHECK(cudaEventRecord(a, st_));
-                run_conv_fwd(T);
-                run_conv_bwd(T, gout, gin, L.in != 0, false);
-                ZNN_CUDA_CHECK(cudaEventRecord(b, st_));
-                ZNN_CUDA_CHECK(cudaEventSynchronize(b));
-                float ms = 0.f;
-                ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
-                if (t > 0) ts.push_back(ms);  // first run warms plans and scratch
-                // a candidate whose first timed run is already 4x the best so far
-                // cannot win: skip its other trials (SIMT on a 120->120 layer
-                // takes seconds; the warm-up run also pays plan allocation)
-                if (t == 1 && ms > 4.f * best) break;
+            try {
+                for (int t = 0; t <= trials; ++t) {
+                    ZNN_CUDA_CHECK(cudaEventRecord(a, st_));
+                    run_conv_fwd(T);
+                    run_conv_bwd(T, gout, gin, L.in != 0, false);
+                    ZNN_CUDA_CHECK(cudaEventRecord(b, st_));
+                    ZNN_CUDA_CHECK(cudaEventSynchronize(b));
+                    float ms = 0.f;
+                    ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+                    if (t > 0) ts.push_back(ms);  // first run warms plans and scratch
+                    // a candidate whose first timed run is already 4x the best so far
+                    // cannot win: skip its other trials (SIMT on a 120->120 layer
+                    // takes seconds; the warm-up run also pays plan allocation)
+                    if (t == 1 && ms > 4.f * best) break;
+                }
+            } catch (const std::exception& ex) {
+                // a candidate that cannot run this layer (launch limits, memory)
+                // drops out instead of failing the whole autotune
+                cudaGetLastError();
+                cudaStreamSynchronize(st_);
+                report << " " << ename(e) << " failed(" << ex.what() << ")";
+                continue;
             }
             std::sort(ts.begin(), ts.end());
             const float med = ts[ts.size() / 2];
@@ -632,6 +743,7 @@ std::vector<int> executor::autotune(int trials) {
             if (med < best) best = med, best_e = e;
         }
         report << " -> " << ename(best_e) << "\n";
+        if (L.engine != best_e) drop_fft_plans();
         L.engine = best_e;
         chosen.push_back(best_e);
     }

@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -88,6 +89,21 @@ public:
     // training only — data parallelism needs the summed gradient first
     double forward_backward(const float* in_dev, const float* labels_dev, bool sync_loss = true,
                             bool update = false);
+    // single-process SGD step (forward_backward with the fused update); with
+    // graph mode on, the second call onwards replays one captured CUDA graph
+    // of the whole step (the scratch arena is frozen: no allocation)
+    double train_step(const float* in_dev, const float* labels_dev, bool sync_loss);
+    void set_graph_mode(bool on);
+    bool graph_captured() const { return !graphs_.empty(); }
+    int64_t batch() const { return cfg_.batch; }
+    int64_t global_batch() const { return cfg_.global_batch; }
+    // called at issue time, in backward order, once a layer's slice of the
+    // flat gradient buffer [off, off + count) is final on the stream
+    // (data-parallel bucketed allreduce)
+    void set_grad_hook(std::function<void(int64_t, int64_t)> h) { grad_hook_ = std::move(h); }
+    // bytes of device memory the kernel spectra of all FFT layers may use
+    // (pool + resident), from cudaMemGetInfo at first use
+    double fft_kernel_budget() const { return fft_budget_; }
     void apply_update();
     void forward(const float* in_dev);
     double step_host(const float* in_host, const float* labels_host);
@@ -111,7 +127,22 @@ private:
     void run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad, bool update,
                       const float* relu_y = nullptr, float* dbias = nullptr);
     znn_fft::plan& fft_plan(layer& L);
-    bool fft_pooled(const layer& L) const;
+    bool fft_pooled(const layer& L);
+    void plan_fft_memory();
+    void drop_fft_plans();
+    void drop_graph();
+    bool fft_decided_ = false;
+    double fft_budget_ = -1.0;
+    std::vector<const layer*> fft_pool_members_;
+    std::function<void(int64_t, int64_t)> grad_hook_;
+    bool graph_mode_ = false;
+    int graph_warm_ = 0;
+    struct step_graph {
+        const float* in;
+        const float* lab;
+        cudaGraphExec_t exec;
+    };
+    std::vector<step_graph> graphs_;  // one per (input, label) buffer pair (double-buffered loaders: 2)
     std::shared_ptr<znn_fft::kpool> kpool_;  // kernel spectra shared by the largest FFT layers
 
     train_cfg cfg_;

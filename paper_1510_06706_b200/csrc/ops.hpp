@@ -19,10 +19,15 @@ public:
     ~scratch();
     void* get(size_t bytes);
     size_t capacity() const { return cap_; }
+    // a frozen arena throws instead of growing (zero-allocation steady state)
+    void freeze(bool on) { frozen_ = on; }
+    int64_t grows() const { return grows_; }
 
 private:
     void* ptr_ = nullptr;
     size_t cap_ = 0;
+    bool frozen_ = false;
+    int64_t grows_ = 0;
 };
 
 // One fully connected conv layer: f_in maps of n -> f_out maps of m = n - s(k-1).

@@ -3,6 +3,8 @@
 // SGD(+momentum) update (engine.hpp:795,800). All HBM-bound: grid-stride
 // loops, vectorised where the layout allows, grids sized in multiples of the
 // 148 SMs.
+#include <algorithm>
+
 #include "ops.hpp"
 
 namespace znn_gpu {
@@ -216,15 +218,90 @@ scratch::~scratch() {
 
 void* scratch::get(size_t bytes) {
     if (bytes > cap_) {
+        if (frozen_)
+            throw cuda_error("scratch arena: " + std::to_string(bytes) + " bytes requested after the arena was "
+                             "frozen at " + std::to_string(cap_) + " (steady state must not allocate)");
         if (ptr_) {
             ZNN_CUDA_CHECK(cudaDeviceSynchronize());
-            ZNN_CUDA_CHECK(cudaFree(ptr_));
+            void* old = ptr_;
+            ptr_ = nullptr;  // consistent state even if the free or the new allocation fails
+            cap_ = 0;
+            ZNN_CUDA_CHECK(cudaFree(old));
         }
-        size_t want = bytes + bytes / 4 + 4096;
-        ZNN_CUDA_CHECK(cudaMalloc(&ptr_, want));
+        const size_t want = bytes + bytes / 4 + 4096;
+        dmalloc(&ptr_, want);
         cap_ = want;
+        ++grows_;
     }
     return ptr_;
+}
+
+namespace {
+struct prof_rec {
+    std::string name;
+    double bytes, flops;
+    cudaEvent_t a, b;
+};
+struct profiler {
+    bool on = false;
+    std::vector<prof_rec> recs;
+    std::vector<cudaEvent_t> spare;
+    cudaEvent_t take() {
+        if (!spare.empty()) {
+            cudaEvent_t e = spare.back();
+            spare.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        ZNN_CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+};
+profiler& prof() {
+    static profiler p;
+    return p;
+}
+}  // namespace
+
+void prof_enable(bool on) { prof().on = on; }
+bool prof_on() { return prof().on; }
+
+prof_scope::prof_scope(cudaStream_t st, std::string name, double bytes, double flops) : st_(st) {
+    profiler& P = prof();
+    if (!P.on) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    prof_rec r{std::move(name), bytes, flops, P.take(), P.take()};
+    ZNN_CUDA_CHECK(cudaEventRecord(r.a, st));
+    P.recs.push_back(std::move(r));
+    slot_ = int(P.recs.size()) - 1;
+}
+
+prof_scope::~prof_scope() {
+    if (slot_ >= 0) cudaEventRecord(prof().recs[size_t(slot_)].b, st_);
+}
+
+std::vector<prof_entry> prof_report() {
+    profiler& P = prof();
+    std::vector<prof_entry> out;
+    for (auto& r : P.recs) {
+        ZNN_CUDA_CHECK(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        ZNN_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+        auto it = std::find_if(out.begin(), out.end(), [&](const prof_entry& e) { return e.name == r.name; });
+        if (it == out.end()) {
+            out.push_back(prof_entry{r.name, 0, 0, 0, 0});
+            it = out.end() - 1;
+        }
+        it->launches++;
+        it->ms += ms;
+        it->bytes += r.bytes;
+        it->flops += r.flops;
+        P.spare.push_back(r.a);
+        P.spare.push_back(r.b);
+    }
+    P.recs.clear();
+    return out;
 }
 
 launch_stats& stats() {

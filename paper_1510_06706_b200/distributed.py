@@ -26,10 +26,17 @@ def shard_range(global_batch: int, world: int, rank: int):
 
 
 class DataParallelStep:
-    def __init__(self, net, world: int = 1, group=None):
+    """comm: the library's NCCL communicator (paper_1510_06706_b200.Comm):
+    the step is then znn_net_train_step_dp (one allreduce per layer, issued
+    as soon as that layer's gradient is final, on a communication stream
+    overlapping the remaining backward). Without it the flat gradient buffer
+    is summed with one torch.distributed allreduce (the gloo CPU tests)."""
+
+    def __init__(self, net, world: int = 1, group=None, comm=None):
         self.net = net
         self.world = world
         self.group = group
+        self.comm = comm
         self._grad = None
 
     def grad(self):
@@ -41,6 +48,8 @@ class DataParallelStep:
         if self.world == 1 and hasattr(self.net, "train_step"):
             # nothing to sum: the update is fused into the backward pass
             return self.net.train_step(inputs, labels, sync_loss=sync_loss)
+        if self.comm is not None:
+            return self.net.train_step_dp(self.comm, inputs, labels, sync_loss=sync_loss)
         loss = self.net.forward_backward(inputs, labels, sync_loss=sync_loss)
         if self.world > 1:
             import torch.distributed as dist

@@ -24,7 +24,7 @@ CASES = [
     (1, 1, 2, (19, 17, 18), (3, 3, 3), (1, 1, 1)),   # pads 20 (radix 4 x 5)
     (1, 2, 1, (37, 39, 33), (5, 5, 5), (2, 2, 2)),   # pads 40 (8 x 5)
     (1, 1, 1, (75, 70, 66), (5, 5, 5), (4, 4, 4)),   # xy pad 80 (8 x 10 = 8 x 2 x 5)
-    (16, 3, 4, (9, 8, 10), (3, 2, 3), (1, 2, 1)),    # B = 16: tensor-core CMAC (one 16-patch MMA tile)
+    (16, 3, 4, (9, 8, 10), (3, 2, 3), (1, 2, 1)),    # B = 16: one 16-patch CMAC tile
     (17, 5, 33, (8, 8, 8), (3, 3, 3), (1, 1, 1)),    # B = 17: two patch tiles, 33 outputs: two n blocks
 ]
 

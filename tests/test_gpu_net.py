@@ -5,7 +5,8 @@ tests/oracles.hpp:155-252) on the same seeded params / inputs / labels.
 c1 runs at its full BASELINE size; c2..c5 keep their exact layer structure
 (kernels, sparsities, filters, pools, widths divided, small output patch) so
 the scalar oracle finishes in seconds. Full-size layers are covered by
-test_gpu_ops.py (sampled) and test_gpu_properties.py."""
+test_gpu_ops.py (sampled, B=1) and test_gpu_fullsize.py (sampled, at the
+configs' own batch, FFT and direct)."""
 import numpy as np
 import pytest
 
@@ -164,25 +165,29 @@ def test_netspec_layered_and_errors(ctx):
 def test_fused_update_matches_phase_split(ctx, ci, engine):
     """train_step (SGD+momentum fused layer by layer, in the tensor-core
     weight-gradient epilogue) == forward_backward + apply_update, bit for bit,
-    over three momentum steps."""
-    from paper_1510_06706_b200._lib import ShapeError
+    over three momentum steps. engine "fft": every conv layer with a kernel
+    larger than 1^3 on the FFT engine, the 1^3 output layer direct (as the
+    autotuner and the bench run it)."""
     cfg = cases()[ci]
     params, x, lab = make_case(cfg, 5)
     xd, ld = torch.as_tensor(x, device="cuda"), torch.as_tensor(lab, device="cuda")
     nets = []
     for fused in (False, True):
-        try:
+        if engine == "fft":
+            net = gpu_net(ctx, cfg, "direct")
+            for li, L in enumerate(cfg.conv_layers()):
+                if np.prod(L.k) > 1:
+                    net.set_layer_engine(li, "fft")
+        else:
             net = gpu_net(ctx, cfg, engine)
-            net.set_params(params)
-            losses = []
-            for _ in range(3):
-                if fused:
-                    losses.append(net.train_step(xd, ld))
-                else:
-                    losses.append(net.forward_backward(xd, ld))
-                    net.apply_update()
-        except ShapeError as e:  # FFT unsupported for a layer shape of this config
-            pytest.skip(str(e))
+        net.set_params(params)
+        losses = []
+        for _ in range(3):
+            if fused:
+                losses.append(net.train_step(xd, ld))
+            else:
+                losses.append(net.forward_backward(xd, ld))
+                net.apply_update()
         nets.append((net.get_params(), net.get_gradients(), losses))
     (p0, g0, l0), (p1, g1, l1) = nets
     assert l0 == l1
