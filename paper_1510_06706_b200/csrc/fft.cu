@@ -1321,6 +1321,13 @@ struct plan {
     dims3 P{1, 1, 1};
     int64_t Zh = 1, bins = 1;
     int64_t B = 0, f = 0, fo = 0;
+    // polyphase plan of a dilated layer (sparsity s != 1): the layer runs as
+    // the undilated layer `ce` over the s_x s_y s_z phase sub-volumes of every
+    // patch (B*S "patches"); P, bins, X, K all belong to ce
+    bool poly = false;
+    conv_shape ce;
+    int64_t S = 1;
+    std::shared_ptr<znn_gpu::scratch> phase_ws;  // phase-split input / output tensors
     float2* X = nullptr;  // memo: image spectra of the layer input [B*f][bins]
     float2* K = nullptr;  // memo: kernel spectra [fo*f][bins] (own buffer; null when pooled)
     float* dil = nullptr; // dilated kernels [fo*f][e^3]
@@ -1366,12 +1373,34 @@ int64_t pad_axis(int64_t n) { return n <= 1 ? 1 : good_size(n); }
 // Any pad >= n per axis is exact (the circular wrap only touches zeros,
 // conv_fft.hpp:67-71). x and y share one pad (square xy planes, one compiled
 // plane kernel per size) unless the volume is 2-D (x = 1).
-dims3 pads_for(const conv_shape& c) {
+// A dilated convolution is s_x s_y s_z undilated ones on the phase
+// sub-volumes: with o = s q + r, y[s q + r] = sum_w x[s (q + w) + r] k[w] =
+// conv_valid(x_r, k)[q], x_r[p] = x[s p + r] (conv_direct.hpp:39-68 with the
+// dilated kernel of conv_direct.hpp:137-151). The adjoint and the kernel
+// gradient split the same way (the kernel gradient sums over the phases).
+// So the FFT engine transforms the phases at pad >= ceil(n / s) and the
+// UNDILATED kernel: kernel spectra shrink by s^3 (c5 conv2: 52 -> 6.6 GB,
+// conv3-5: 30 / 16 / 6.6 GB -> 0.5 / 0.3 / 0.1 GB) and the frequency-domain
+// sums over converging edges reuse each kernel-spectrum bin for B s^3 phase
+// images instead of B patches. ZNN_FFT_POLY=0 keeps the dilated-kernel path.
+bool use_poly(const conv_shape& c) {
+    if (c.s.x == 1 && c.s.y == 1 && c.s.z == 1) return false;
+    const char* e = std::getenv("ZNN_FFT_POLY");
+    return !(e && std::string(e) == "0");
+}
+conv_shape effective(const conv_shape& c) {
+    if (!use_poly(c)) return c;
+    const dims3 nr{ceil_div(c.n.x, c.s.x), ceil_div(c.n.y, c.s.y), ceil_div(c.n.z, c.s.z)};
+    return conv_shape::make(c.B * c.s.x * c.s.y * c.s.z, c.f_in, c.f_out, nr, c.k, dims3{1, 1, 1});
+}
+
+dims3 pads_for_eff(const conv_shape& c) {
     dims3 P{pad_axis(c.n.x), pad_axis(c.n.y), pad_axis(c.n.z)};
     if (P.x > 1) P.x = P.y = std::max(P.x, P.y);
     if (P.z % 2) P.z = good_size(P.z + 1);  // R2C axis must be even
     return P;
 }
+dims3 pads_for(const conv_shape& c) { return pads_for_eff(effective(c)); }
 
 // z passes: twiddles + per-line exchange buffers + the half-spectrum stash
 size_t smem_for(int P) { return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(xpitch(P)) + size_t(LINES) * size_t(P / 2 + 2)); }
@@ -1601,13 +1630,23 @@ int64_t kernel_spectrum_bytes(const conv_shape& c) {
     return c.f_in * c.f_out * P.x * P.y * (P.z / 2 + 1) * int64_t(sizeof(float2));
 }
 
-int64_t image_spectrum_bytes(const conv_shape& c) {
+int64_t image_spectrum_bytes(const conv_shape& c0) {
+    const conv_shape c = effective(c0);
     const dims3 P = pads_for(c);
     return c.B * c.f_in * P.x * P.y * (P.z / 2 + 1) * int64_t(sizeof(float2));
 }
 
+// phase-split tensors of a polyphase plan: input side [B S f nr] and output side [B S f' mr]
+int64_t phase_bytes(const conv_shape& c0) {
+    if (!use_poly(c0)) return 0;
+    const conv_shape c = effective(c0);
+    const int64_t a = c.B * c.f_in * c.n.vol(), b = c.B * c.f_out * c.m.vol();
+    return int64_t(sizeof(float)) * (a + b) + 1024;
+}
+
 // the scratch-arena bytes conv_fwd / conv_bwd ask for (the larger of the two)
-int64_t workspace_bytes(const conv_shape& c) {
+int64_t workspace_bytes(const conv_shape& c0) {
+    const conv_shape c = effective(c0);
     const dims3 P = pads_for(c);
     const int64_t Zh = P.z / 2 + 1, bins = P.x * P.y * Zh, c8 = int64_t(sizeof(float2));
     const int64_t fwd = c8 * (c.B * c.f_out * bins + c.B * c.f_out * Zh * c.m.x * c.m.y) + 1024;
@@ -1624,9 +1663,17 @@ bool supported(const conv_shape& c) {
     return true;
 }
 
-plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool) {
-    require(supported(c), "fft engine: layer unsupported (pad > 128 or spectra exceed the memory budget)");
+plan_ptr make_plan(const conv_shape& c0, std::shared_ptr<kpool> pool, std::shared_ptr<znn_gpu::scratch> phase_ws) {
+    require(supported(c0), "fft engine: layer unsupported (pad > 128 or spectra exceed the memory budget)");
+    const conv_shape c = effective(c0);
     plan_ptr p(new plan);
+    if (use_poly(c0)) {
+        p->poly = true;
+        p->ce = c;
+        p->S = c0.s.x * c0.s.y * c0.s.z;
+        p->phase_ws = phase_ws ? std::move(phase_ws) : std::make_shared<znn_gpu::scratch>();
+        p->phase_ws->get(size_t(phase_bytes(c0)));  // sized now: a step never grows it
+    }
     p->P = pads_for(c);
     p->Zh = p->P.z / 2 + 1;
     p->bins = p->P.x * p->P.y * p->Zh;
@@ -1707,8 +1754,8 @@ double cmac_bytes(const conv_shape& c, const plan& p) {
 double cmac_flops(const conv_shape& c, const plan& p) { return 8.0 * double(c.B * c.f_in * c.f_out) * double(p.bins); }
 }  // namespace
 
-void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
-              int act, float* y, znn_gpu::scratch& ws) {
+static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w,
+                          const float* bias, int act, float* y, znn_gpu::scratch& ws) {
     require(p.B == c.B && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
     const int64_t nker = c.f_out * c.f_in;
     // image spectra (memoised for the backward / update passes)
@@ -1778,7 +1825,7 @@ void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c
     inverse3d(st, p, DK, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
 }
 
-void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float* w, float* gw,
+static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const float* g, const float* w, float* gw,
               float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias) {
     const int64_t nB = c.B;
     const int64_t ccount = std::max(nB * c.f_in * p.Zh * c.n.x * c.n.y, c.f_out * c.f_in * p.Zh * c.k.x * c.k.y);
@@ -1850,9 +1897,145 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
     p.cnt.upd_inverse += c.f_out * c.f_in;
 }
 
-float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64_t* bins_out) {
+namespace {
+
+// space-to-batch: x [B][f][n] -> xp [B][S][f][nr] with xp[(b S + r) f + i][q] =
+// x[b][i][s q + r] (r = (rx sy + ry) sz + rz), optionally gated by a ReLU
+// output (g * (y > 0), the fused transfer backward). One warp per input
+// z-line: coalesced reads, and each store instruction fills sz phase lines
+// with runs of 32 / sz consecutive floats. Lanes beyond a phase's valid
+// length are never written (the caller zero-fills ragged phases).
+__global__ void __launch_bounds__(256) phase_split_k(const float* __restrict__ x, const float* __restrict__ gate,
+                                                     int64_t lines, int f, int nx, int ny, int nz, int sx, int sy,
+                                                     int sz, int nrx, int nry, int nrz, float* __restrict__ xp) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int S = sx * sy * sz;
+    for (int64_t ln = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); ln < lines; ln += warps) {
+        const int yy = int(ln % ny);
+        int64_t t = ln / ny;
+        const int xx = int(t % nx);
+        t /= nx;
+        const int i = int(t % f);
+        const int64_t b = t / f;
+        const int qx = xx / sx, rx = xx - qx * sx, qy = yy / sy, ry = yy - qy * sy;
+        const int64_t rb = (b * S + int64_t(rx * sy + ry) * sz) * f + i;  // image of phase (rx, ry, rz = 0)
+        const float* src = x + ln * nz;
+        const float* gsrc = gate ? gate + ln * nz : nullptr;
+        for (int z0 = 0; z0 < nz; z0 += 32) {
+            const int z = z0 + lane;
+            if (z < nz) {
+                float v = __ldcs(src + z);
+                if (gsrc && !(__ldcs(gsrc + z) > 0.f)) v = 0.f;
+                const int qz = z / sz, rz = z - qz * sz;
+                const int64_t img = rb + int64_t(rz) * f;
+                xp[((img * nrx + qx) * nry + qy) * nrz + qz] = v;
+            }
+        }
+    }
+}
+
+// batch-to-space: yp [B][S][f][mr] -> y [B][f][m], y[b][o][s q + r] =
+// yp[(b S + r) f + o][q]; one warp per output z-line, coalesced stores.
+__global__ void __launch_bounds__(256) phase_merge_k(const float* __restrict__ yp, int64_t lines, int f, int mx,
+                                                     int my, int mz, int sx, int sy, int sz, int mrx, int mry,
+                                                     int mrz, float* __restrict__ y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int S = sx * sy * sz;
+    for (int64_t ln = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); ln < lines; ln += warps) {
+        const int yy = int(ln % my);
+        int64_t t = ln / my;
+        const int xx = int(t % mx);
+        t /= mx;
+        const int o = int(t % f);
+        const int64_t b = t / f;
+        const int qx = xx / sx, rx = xx - qx * sx, qy = yy / sy, ry = yy - qy * sy;
+        const int64_t rb = (b * S + int64_t(rx * sy + ry) * sz) * f + o;
+        float* dst = y + ln * mz;
+        for (int z0 = 0; z0 < mz; z0 += 32) {
+            const int z = z0 + lane;
+            if (z < mz) {
+                const int qz = z / sz, rz = z - qz * sz;
+                const int64_t img = rb + int64_t(rz) * f;
+                __stcs(dst + z, __ldcs(yp + ((img * mrx + qx) * mry + qy) * mrz + qz));
+            }
+        }
+    }
+}
+
+unsigned warp_grid(int64_t lines) {
+    const int64_t blocks = ceil_div(lines, 8);  // 8 warps per 256-thread block
+    return unsigned(std::min<int64_t>(blocks, 148 * 16));
+}
+
+void phase_split(cudaStream_t st, const plan& p, const conv_shape& c, const float* x, const float* gate, int64_t maps,
+                 dims3 n, dims3 nr, float* xp) {
+    const bool ragged = nr.x * c.s.x != n.x || nr.y * c.s.y != n.y || nr.z * c.s.z != n.z;
+    if (ragged)  // phases shorter than nr: the missing voxels are the zero padding
+        ZNN_CUDA_CHECK(cudaMemsetAsync(xp, 0, sizeof(float) * size_t(c.B * p.S * maps * nr.vol()), st));
+    const int64_t lines = c.B * maps * n.x * n.y;
+    phase_split_k<<<warp_grid(lines), 256, 0, st>>>(x, gate, lines, int(maps), int(n.x), int(n.y), int(n.z),
+                                                     int(c.s.x), int(c.s.y), int(c.s.z), int(nr.x), int(nr.y),
+                                                     int(nr.z), xp);
+    launch_check("fft_phase_split");
+}
+
+void phase_merge(cudaStream_t st, const conv_shape& c, const float* yp, int64_t maps, dims3 m, dims3 mr, float* y) {
+    const int64_t lines = c.B * maps * m.x * m.y;
+    phase_merge_k<<<warp_grid(lines), 256, 0, st>>>(yp, lines, int(maps), int(m.x), int(m.y), int(m.z), int(c.s.x),
+                                                     int(c.s.y), int(c.s.z), int(mr.x), int(mr.y), int(mr.z), y);
+    launch_check("fft_phase_merge");
+}
+
+}  // namespace
+
+void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
+              int act, float* y, znn_gpu::scratch& ws) {
+    require(p.B == c.B * p.S && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
+    if (!p.poly) {
+        conv_fwd_core(st, p, c, x, w, bias, act, y, ws);
+        return;
+    }
+    const conv_shape& e = p.ce;
+    float* xp = static_cast<float*>(p.phase_ws->get(size_t(phase_bytes(c))));
+    float* yp = xp + ((e.B * e.f_in * e.n.vol() + 63) / 64) * 64;
+    {
+        znn_gpu::prof_scope ps(st, lbl("fft_phase_split", c, p), 8.0 * double(c.B * c.f_in * c.n.vol()), 0);
+        phase_split(st, p, c, x, nullptr, c.f_in, c.n, e.n, xp);
+    }
+    conv_fwd_core(st, p, e, xp, w, bias, act, yp, ws);  // bias + transfer per output map: phase-invariant
+    znn_gpu::prof_scope ps(st, lbl("fft_phase_merge", c, p), 8.0 * double(c.B * c.f_out * c.m.vol()), 0);
+    phase_merge(st, c, yp, c.f_out, c.m, e.m, y);
+}
+
+void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float* w, float* gw,
+              float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias) {
+    if (!p.poly) {
+        conv_bwd_core(st, p, c, g, w, gw, gin, ws, relu_y, dbias);
+        return;
+    }
+    const conv_shape& e = p.ce;
+    float* dxp = static_cast<float*>(p.phase_ws->get(size_t(phase_bytes(c))));
+    float* gp = dxp + ((e.B * e.f_in * e.n.vol() + 63) / 64) * 64;
+    {
+        // the gradient's phases, gated by the fused ReLU (its bias gradient is
+        // then the DC term of the gated phases' spectra, summed over B s^3)
+        znn_gpu::prof_scope ps(st, lbl("fft_phase_split", c, p),
+                               (relu_y ? 12.0 : 8.0) * double(c.B * c.f_out * c.m.vol()), 0);
+        phase_split(st, p, c, g, relu_y, c.f_out, c.m, e.m, gp);
+    }
+    conv_bwd_core(st, p, e, gp, w, gw, gin ? dxp : nullptr, ws, nullptr, dbias);
+    if (gin) {
+        znn_gpu::prof_scope ps(st, lbl("fft_phase_merge", c, p), 8.0 * double(c.B * c.f_in * c.n.vol()), 0);
+        phase_merge(st, c, dxp, c.f_in, c.n, e.n, gin);
+    }
+}
+
+float time_cmac(cudaStream_t st, int which, const conv_shape& c0, int reps, int64_t* bins_out) {
     require(which >= 0 && which <= 2 && reps > 0, "fft cmac probe: bad arguments");
-    require(supported(c), "fft cmac probe: layer unsupported by the FFT engine");
+    require(supported(c0), "fft cmac probe: layer unsupported by the FFT engine");
+    const conv_shape c = effective(c0);  // dilated layers: the phase images of the polyphase plan
     const dims3 P = pads_for(c);
     const int64_t bins = P.x * P.y * (P.z / 2 + 1), B = c.B, f = c.f_in, fo = c.f_out;
     if (bins_out) *bins_out = bins;

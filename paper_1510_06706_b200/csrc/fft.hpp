@@ -53,7 +53,11 @@ int64_t kernel_spectrum_bytes(const conv_shape& c);
 int64_t image_spectrum_bytes(const conv_shape& c);  // the memoised X of a plan
 int64_t workspace_bytes(const conv_shape& c);       // scratch arena of conv_fwd / conv_bwd
 bool supported(const conv_shape& c);
-plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool = nullptr);
+// phase_ws: arena for the phase-split tensors of dilated layers (shared by
+// the layers of one executor; a plan gets its own when null)
+plan_ptr make_plan(const conv_shape& c, std::shared_ptr<kpool> pool = nullptr,
+                   std::shared_ptr<znn_gpu::scratch> phase_ws = nullptr);
+int64_t phase_bytes(const conv_shape& c);  // phase-split tensors of a dilated layer (0 if none)
 const transform_counts& counts(const plan& p);
 void pad_dims(const plan& p, int64_t out[3]);
 

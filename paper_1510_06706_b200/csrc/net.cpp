@@ -57,6 +57,7 @@ executor::~executor() {
     for (auto& g : graphs_) cudaGraphExecDestroy(g.exec);
     for (auto& L : layers_) L.fft.reset();
     kpool_.reset();
+    phase_ws_.reset();
     for (void* p : owned_) cudaFree(p);
 }
 
@@ -363,13 +364,14 @@ void executor::plan_fft_memory() {
     fft_decided_ = true;
     fft_pool_members_.clear();
     std::vector<std::pair<int64_t, const layer*>> sz;
-    int64_t total = 0, xspec = 0, wsmax = 0;
+    int64_t total = 0, xspec = 0, wsmax = 0, phmax = 0;
     for (const auto& M : layers_)
         if (M.kind == lkind::conv && M.engine == 1 && znn_fft::supported(M.shape)) {
             sz.emplace_back(znn_fft::kernel_spectrum_bytes(M.shape), &M);
             total += sz.back().first;
             xspec += znn_fft::image_spectrum_bytes(M.shape);
             wsmax = std::max(wsmax, znn_fft::workspace_bytes(M.shape));
+            phmax = std::max(phmax, znn_fft::phase_bytes(M.shape));
         }
     if (sz.empty()) return;
     std::sort(sz.begin(), sz.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
@@ -381,7 +383,8 @@ void executor::plan_fft_memory() {
         double head = 20.0;
         if (const char* h = std::getenv("ZNN_MEM_HEADROOM_GB")) head = std::atof(h);
         const double have = double(fr) + double(ws_.capacity());  // the arena is re-grown to wsmax
-        fft_budget_ = have - double(xspec) - double(wsmax) * 1.25 - head * double(int64_t(1) << 30);
+        fft_budget_ = have - double(xspec) - double(wsmax) * 1.25 - double(phmax) -
+                      head * double(int64_t(1) << 30);
     }
     // smallest j: the j largest layers share one buffer (its size = the
     // largest), the others stay resident; j = 1 saves nothing over j = 0
@@ -408,6 +411,7 @@ void executor::drop_fft_plans() {
     drop_graph();
     for (auto& L : layers_) L.fft.reset();
     kpool_.reset();
+    phase_ws_.reset();
     fft_decided_ = false;
 }
 
@@ -470,7 +474,9 @@ znn_fft::plan& executor::fft_plan(layer& L) {
             if (!kpool_) kpool_ = std::make_shared<znn_fft::kpool>();
             pool = kpool_;
         }
-        L.fft = std::shared_ptr<znn_fft::plan>(znn_fft::make_plan(L.shape, pool).release(), znn_fft::plan_deleter());
+        if (!phase_ws_) phase_ws_ = std::make_shared<znn_gpu::scratch>();
+        L.fft = std::shared_ptr<znn_fft::plan>(znn_fft::make_plan(L.shape, pool, phase_ws_).release(),
+                                               znn_fft::plan_deleter());
     }
     return *L.fft;
 }

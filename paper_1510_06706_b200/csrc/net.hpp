@@ -144,6 +144,7 @@ private:
     };
     std::vector<step_graph> graphs_;  // one per (input, label) buffer pair (double-buffered loaders: 2)
     std::shared_ptr<znn_fft::kpool> kpool_;  // kernel spectra shared by the largest FFT layers
+    std::shared_ptr<znn_gpu::scratch> phase_ws_;  // phase-split tensors of the dilated FFT layers
 
     train_cfg cfg_;
     cudaStream_t st_ = nullptr;

@@ -220,3 +220,22 @@ def test_fft_xy_pipe_forward_variant(ctx, monkeypatch, shape):
     opt-in: slower than one plane per CTA for the forward) stays exact."""
     monkeypatch.setenv("ZNN_FFT_XY_PIPE", "1")
     test_fft_conv_fwd_matches_oracle(ctx, shape)
+
+
+@pytest.mark.parametrize("shape", [c for c in CASES if max(c[5]) > 1 and max(c[4]) > 1], ids=str)
+def test_fft_dilated_kernel_path(ctx, monkeypatch, shape):
+    """Dilated layers run as polyphase plans by default (s^3 undilated
+    convolutions on the phase sub-volumes); the dilated-kernel plan
+    (ZNN_FFT_POLY=0) stays exact too."""
+    monkeypatch.setenv("ZNN_FFT_POLY", "0")
+    test_fft_conv_fwd_matches_oracle(ctx, shape)
+
+
+def test_fft_polyphase_plan_shrinks_kernel_spectra(ctx):
+    """c5 conv2 (120 -> 120, 90^3, 5^3, s = 2): phases of 45^3 at pad 48,
+    kernel spectra 8x smaller than the dilated kernel's at pad 96."""
+    from paper_1510_06706_b200 import FftPlan
+    p = FftPlan(ctx, 1, 2, 2, (90, 90, 90), (5, 5, 5), (2, 2, 2))
+    info = p.info()
+    assert info["pads"] == (48, 48, 48) and info["bins"] == 48 * 48 * 25
+    p.close()

@@ -92,12 +92,18 @@ def _engines_for(shape):
     return out
 
 
-@pytest.mark.parametrize("engine", ["fft", "direct"])
+@pytest.mark.parametrize("engine", ["fft", "direct", "fft-dilated"])
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda t: f"{t[0]}-f{t[2]}x{t[3]}-n{t[4][0]}-k{t[5][0]}-s{t[6][0]}-B{t[1]}")
-def test_conv_layer_full_size(ctx, shape, engine):
+def test_conv_layer_full_size(ctx, shape, engine, monkeypatch):
+    """engine "fft": dilated layers run the polyphase plan (phases at the
+    undilated kernel's pad); "fft-dilated" (ZNN_FFT_POLY=0): the dilated
+    kernel at the full pad, checked on the c4 dilated layers."""
     from paper_1510_06706_b200 import FftPlan, ops
-    if engine not in _engines_for(shape):
-        pytest.skip("layer runs direct only (1 -> f' input layer of c5)")
+    if engine not in _engines_for(shape) + (["fft-dilated"] if shape[0] == "c4" and max(shape[6]) > 1 else []):
+        pytest.skip("layer runs direct only (1 -> f' input layer of c5), or no dilated-kernel variant")
+    if engine == "fft-dilated":
+        monkeypatch.setenv("ZNN_FFT_POLY", "0")
+        engine = "fft"
     name, B, fi, fo, n, k, s = shape
     rng = np.random.default_rng(abs(hash(shape)) % 2**32)
     x, w, bias, g, m = _data(shape, seed=len(n) * 1000 + fi + fo + n[0])
@@ -123,7 +129,7 @@ def test_fft_cmac_large_bin_grid(ctx):
     grid.y limit the round-1 CMAC launches had): forward and backward run and
     match the oracle."""
     from paper_1510_06706_b200 import FftPlan
-    B, fi, fo, n, k, s = 1, 2, 2, (100, 100, 100), (3, 3, 3), (2, 2, 2)
+    B, fi, fo, n, k, s = 1, 2, 2, (100, 100, 100), (3, 3, 3), (1, 1, 1)
     plan = FftPlan(ctx, B, fi, fo, n, k, s)
     assert plan.info()["bins"] == 128 * 128 * 65
     shape = ("big", B, fi, fo, n, k, s)
