@@ -719,6 +719,268 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_upd1_k(const float2* __res
     }
 }
 
+// ---- phase geometry of a dilated layer's polyphase plan: phase image
+// img = (b S + r) f + i of the original tensor [B][f][nx][ny][nz], phase
+// r = (rx sy + ry) sz + rz holds the voxels (s q + r) ----
+struct phase_geom {
+    int f, nx, ny, nz;     // original tensor (maps, dims)
+    int sx, sy, sz, zsh;   // sparsity; zsh = log2(sz) when sz is a power of two, else -1
+    int nrx, nry, nrz;     // phase dims
+};
+
+__device__ __forceinline__ void zsplit(int z, int sz, int zsh, int& q, int& r) {
+    if (zsh >= 0) {
+        q = z >> zsh;
+        r = z & (sz - 1);
+    } else {
+        q = z / sz;
+        r = z - q * sz;
+    }
+}
+
+// original-tensor line base of phase image img, phase line (qx, qy); -1 if
+// the line lies outside the original volume (ragged phase); *rz = z phase
+__device__ __forceinline__ int64_t phase_line(const phase_geom& G, int img, int qx, int qy, int* rz) {
+    const int S = G.sx * G.sy * G.sz;
+    const int b = img / (S * G.f), rem = img - b * S * G.f;
+    const int r = rem / G.f, i = rem - r * G.f;
+    const int rzz = r % G.sz, t = r / G.sz, ry = t % G.sy, rx = t / G.sy;
+    *rz = rzz;
+    const int x = G.sx * qx + rx, y = G.sy * qy + ry;
+    if (x >= G.nx || y >= G.ny) return -1;
+    return ((int64_t(b) * G.f + i) * G.nx + x) * G.ny * int64_t(G.nz) + int64_t(y) * G.nz;
+}
+
+// ---- fused 3D transforms of small pads (P <= 32): one CTA holds an
+// image's whole half spectrum [Zh][P][P] in shared memory and runs the z,
+// y and x line passes there, so each image is read once and its spectrum
+// written once (the split z / xy passes round-trip the spectrum through HBM
+// and leave most of a CTA idle on 12-24 point planes). Sources / outputs
+// are dense boxes or, for polyphase plans, the phases of the original
+// tensor addressed in place (no split / merge pass). ----
+constexpr int SMALLP = 32;
+
+struct cube_io {
+    const float* src;        // forward: real images (dense) or the original tensor (phased)
+    const float* gate;       // forward: fused ReLU backward gate (same addressing), or null
+    float* dst;              // inverse: output (dense box) or the original tensor (phased)
+    int64_t img_stride;      // dense addressing: floats between images
+    int nx, ny, nz;          // forward: valid input dims of an image
+    int xs, xc, ys, yc, zs, zc;  // inverse: kept voxels (step * i, i < count) per axis
+    int oy, oz;              // inverse dense box dims
+    int bias_mod, act;
+    float scale;
+    int phased;
+    phase_geom ph;
+};
+
+template <int P>
+constexpr size_t cube_smem() {
+    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(line_shape<P>::XP) +
+                             size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
+}
+
+template <int P>
+__global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* __restrict__ spec) {
+    constexpr int Zh = P / 2 + 1, PYP = P + 1;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* cube = xbuf + LINES * line_shape<P>::XP;  // [Zh][P][PYP]
+    fill_twiddles<P>(tw);
+    const int img = blockIdx.x;
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * line_shape<P>::XP;
+    __syncthreads();
+    // z lines (R2C) of the valid (x, y) lines
+    const int nl1 = a.nx * a.ny;
+    for (int b0 = 0; b0 < nl1; b0 += LINES) {
+        const int ln = b0 + l;
+        const bool ok = ln < nl1;
+        const int x = ok ? ln / a.ny : 0, y = ok ? ln - (ln / a.ny) * a.ny : 0;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) v[n2] = make_float2(0.f, 0.f);
+        if (ok && t < R1) {
+            if (a.phased) {
+                int rz;
+                const int64_t base = phase_line(a.ph, img, x, y, &rz);
+                if (base >= 0) {
+#pragma unroll
+                    for (int n2 = 0; n2 < R2; ++n2) {
+                        const int z = rz + a.ph.sz * (t + R1 * n2);
+                        if (t + R1 * n2 < a.nz && z < a.ph.nz) {
+                            float val = __ldg(a.src + base + z);
+                            if (a.gate && !(__ldg(a.gate + base + z) > 0.f)) val = 0.f;
+                            v[n2].x = val;
+                        }
+                    }
+                }
+            } else {
+                const int64_t base = int64_t(img) * a.img_stride + (int64_t(x) * a.ny + y) * a.nz;
+#pragma unroll
+                for (int n2 = 0; n2 < R2; ++n2) {
+                    const int z = t + R1 * n2;
+                    if (z < a.nz) {
+                        float val = __ldg(a.src + base + z);
+                        if (a.gate && !(__ldg(a.gate + base + z) > 0.f)) val = 0.f;
+                        v[n2].x = val;
+                    }
+                }
+            }
+        }
+        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+            if (ok && k < Zh) cube[(k * P + x) * PYP + y] = val;
+        });
+    }
+    __syncthreads();
+    // y lines of the valid rows x < nx (columns y >= ny are the zero padding)
+    const int nl2 = Zh * a.nx;
+    for (int b0 = 0; b0 < nl2; b0 += LINES) {
+        const int ln = b0 + l;
+        const bool ok = ln < nl2;
+        const int zb = ok ? ln / a.nx : 0, x = ok ? ln - (ln / a.nx) * a.nx : 0;
+        float2* row = cube + (zb * P + x) * PYP;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            const int y = t + R1 * n2;
+            v[n2] = (ok && t < R1 && y < a.ny) ? row[y] : make_float2(0.f, 0.f);
+        }
+        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+            if (ok) row[k] = val;
+        });
+    }
+    __syncthreads();
+    // x lines of every column (rows x >= nx are the zero padding)
+    const int nl3 = Zh * P;
+    for (int b0 = 0; b0 < nl3; b0 += LINES) {
+        const int ln = b0 + l;
+        const bool ok = ln < nl3;
+        const int zb = ok ? ln / P : 0, y = ok ? ln - (ln / P) * P : 0;
+        float2* col = cube + zb * P * PYP + y;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            const int x = t + R1 * n2;
+            v[n2] = (ok && t < R1 && x < a.nx) ? col[x * PYP] : make_float2(0.f, 0.f);
+        }
+        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+            if (ok) col[k * PYP] = val;
+        });
+    }
+    __syncthreads();
+    // the whole half spectrum out, [Zh][P][P], two bins per 16-byte store
+    float4* g4 = reinterpret_cast<float4*>(spec + int64_t(img) * (Zh * P * P));
+    for (int idx = threadIdx.x; idx < Zh * P * P / 2; idx += THREADS) {
+        const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+        const float2 u = cube[(zb * P + x) * PYP + y], w = cube[(zb * P + x) * PYP + y + 1];
+        __stcs(g4 + idx, make_float4(u.x, u.y, w.x, w.y));
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __restrict__ spec, cube_io a,
+                                                            const float* __restrict__ bias) {
+    constexpr int Zh = P / 2 + 1, PYP = P + 1;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* cube = xbuf + LINES * line_shape<P>::XP;
+    fill_twiddles<P>(tw);
+    const int img = blockIdx.x;
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * line_shape<P>::XP;
+    const float4* g4 = reinterpret_cast<const float4*>(spec + int64_t(img) * (Zh * P * P));
+    for (int idx = threadIdx.x; idx < Zh * P * P / 2; idx += THREADS) {
+        const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+        const float4 u = __ldcs(g4 + idx);
+        cube[(zb * P + x) * PYP + y] = make_float2(u.x, u.y);
+        cube[(zb * P + x) * PYP + y + 1] = make_float2(u.z, u.w);
+    }
+    __syncthreads();
+    // x lines (columns), keep rows xs * i, i < xc, compacted into rows i
+    const int nl1 = Zh * P;
+    for (int b0 = 0; b0 < nl1; b0 += LINES) {
+        const int ln = b0 + l;
+        const bool ok = ln < nl1;
+        const int zb = ok ? ln / P : 0, y = ok ? ln - (ln / P) * P : 0;
+        float2* col = cube + zb * P * PYP + y;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? col[(t + R1 * n2) * PYP] : make_float2(0.f, 0.f);
+        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+            const int i = k / a.xs;
+            if (ok && i * a.xs == k && i < a.xc) col[i * PYP] = val;
+        });
+    }
+    __syncthreads();
+    // y lines of the kept rows, keep columns ys * j, j < yc
+    const int nl2 = Zh * a.xc;
+    for (int b0 = 0; b0 < nl2; b0 += LINES) {
+        const int ln = b0 + l;
+        const bool ok = ln < nl2;
+        const int zb = ok ? ln / a.xc : 0, i = ok ? ln - (ln / a.xc) * a.xc : 0;
+        float2* row = cube + (zb * P + i) * PYP;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? row[t + R1 * n2] : make_float2(0.f, 0.f);
+        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+            const int j = k / a.ys;
+            if (ok && j * a.ys == k && j < a.yc) row[j] = val;
+        });
+    }
+    __syncthreads();
+    // z lines (C2R) of the kept (i, j), keep zs * q, q < zc; scale, bias, transfer
+    const int nl3 = a.xc * a.yc;
+    const float bv = bias ? bias[img % a.bias_mod] : 0.f;
+    for (int b0 = 0; b0 < nl3; b0 += LINES) {
+        const int ln = b0 + l;
+        const bool ok = ln < nl3;
+        const int i = ok ? ln / a.yc : 0, j = ok ? ln - (ln / a.yc) * a.yc : 0;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            const int zz = t + R1 * n2;
+            float2 val = make_float2(0.f, 0.f);
+            if (ok && t < R1) {
+                if (zz < Zh) {
+                    val = cube[(zz * P + i) * PYP + j];
+                } else {  // Hermitian symmetry of a real signal
+                    const float2 c = cube[((P - zz) * P + i) * PYP + j];
+                    val = make_float2(c.x, -c.y);
+                }
+            }
+            v[n2] = val;
+        }
+        int64_t base = -1;
+        int rz = 0;
+        if (ok) {
+            if (a.phased)
+                base = phase_line(a.ph, img, i, j, &rz);
+            else
+                base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + j) * a.oz;
+        }
+        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+            const int q = k / a.zs;
+            if (base >= 0 && q * a.zs == k && q < a.zc) {
+                float r = val.x * a.scale + bv;
+                if (a.act == 2) r = r > 0.f ? r : 0.f;
+                else if (a.act == 0) r = 1.f / (1.f + expf(-r));
+                else if (a.act == 1) r = tanhf(r);
+                if (a.phased) {
+                    const int z = rz + a.ph.sz * q;
+                    if (z < a.ph.nz) a.dst[base + z] = r;
+                } else {
+                    a.dst[base + q] = r;
+                }
+            }
+        });
+    }
+}
+
 struct zinv_args {
     int xc, yc;                        // kept block per z-bin plane (compact input)
     int z_step, z_cnt;                 // kept z voxels (selection starts at 0)
@@ -1516,9 +1778,38 @@ __global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec
 
 // gate: optional ReLU output gating the input (fused transfer backward);
 // dbias (with gate): receives the per-map sum over the batch (imgs = B * dmaps)
+bool small_cube(const plan& p) {
+    return p.P.x == p.P.y && p.P.y == p.P.z && p.P.x > 1 && p.P.x <= SMALLP && !std::getenv("ZNN_FFT_NO_CUBE");
+}
+
+// ph: the images are the phases of an original tensor (polyphase plan, small
+// cubes only): read in place, no split pass
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
                float2* spec, bool z_only = false, const float* gate = nullptr, float* dbias = nullptr,
-               int64_t dmaps = 1) {
+               int64_t dmaps = 1, const phase_geom* ph = nullptr) {
+    if (!z_only && small_cube(p)) {
+        cube_io a{};
+        a.src = in, a.gate = gate, a.img_stride = in_img_stride;
+        a.nx = int(n.x), a.ny = int(n.y), a.nz = int(n.z);
+        a.phased = ph ? 1 : 0;
+        if (ph) a.ph = *ph;
+        require(imgs < (int64_t(1) << 31), "fft: too many images");
+        dispatch_pad(int(p.P.x), [&](auto pc) {
+            constexpr int PP = decltype(pc)::value;
+            if constexpr (PP <= SMALLP) {
+                allow_smem(fft3_fwd_small_k<PP>, cube_smem<PP>());
+                fft3_fwd_small_k<PP><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(a, spec);
+            }
+        });
+        launch_check("fft3_fwd_small");
+        if (dbias) {  // the DC bin of each image's spectrum is its voxel sum
+            dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y, 1, 1,
+                                                       int(p.P.y), dbias);
+            launch_check("fft_dc_bias");
+        }
+        return;
+    }
+    require(ph == nullptr, "fft: phase addressing needs the small-cube transforms");
     const int64_t nlines = imgs * n.x * n.y;
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
@@ -1563,9 +1854,33 @@ void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 c
 // written as a dense box [imgs][cnt.x][cnt.y][cnt.z] (image stride given);
 // cbuf holds the compact kept planes between the two passes
 void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs, dims3 step, dims3 cnt, float* out,
-               int64_t out_img_stride, const float* bias, int bias_mod, int act, float2* cbuf) {
+               int64_t out_img_stride, const float* bias, int bias_mod, int act, float2* cbuf,
+               const phase_geom* ph = nullptr) {
     require(step.x * (cnt.x - 1) < p.P.x && step.y * (cnt.y - 1) < p.P.y && step.z * (cnt.z - 1) < p.P.z,
             "fft: kept voxels outside the padded volume");
+    if (small_cube(p)) {
+        cube_io a{};
+        a.dst = out, a.img_stride = out_img_stride;
+        a.xs = int(step.x), a.xc = int(cnt.x), a.ys = int(step.y), a.yc = int(cnt.y), a.zs = int(step.z),
+        a.zc = int(cnt.z);
+        a.oy = int(cnt.y), a.oz = int(cnt.z);
+        a.bias_mod = bias_mod > 0 ? bias_mod : 1;
+        a.act = act;
+        a.scale = float(1.0 / double(p.P.x * p.P.y * p.P.z));
+        a.phased = ph ? 1 : 0;
+        if (ph) a.ph = *ph;
+        require(imgs < (int64_t(1) << 31), "fft: too many images");
+        dispatch_pad(int(p.P.x), [&](auto pc) {
+            constexpr int PP = decltype(pc)::value;
+            if constexpr (PP <= SMALLP) {
+                allow_smem(fft3_inv_small_k<PP>, cube_smem<PP>());
+                fft3_inv_small_k<PP><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(spec, a, bias);
+            }
+        });
+        launch_check("fft3_inv_small");
+        return;
+    }
+    require(ph == nullptr, "fft: phase addressing needs the small-cube transforms");
     const int64_t planes = imgs * p.Zh;
     dispatch_pad(int(p.P.y), [&](auto pc) {
         constexpr int PY = decltype(pc)::value;
@@ -1755,13 +2070,14 @@ double cmac_flops(const conv_shape& c, const plan& p) { return 8.0 * double(c.B 
 }  // namespace
 
 static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w,
-                          const float* bias, int act, float* y, znn_gpu::scratch& ws) {
+                          const float* bias, int act, float* y, znn_gpu::scratch& ws,
+                          const phase_geom* ph_in = nullptr, const phase_geom* ph_out = nullptr) {
     require(p.B == c.B && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
     const int64_t nker = c.f_out * c.f_in;
     // image spectra (memoised for the backward / update passes)
     {
         znn_gpu::prof_scope ps(st, lbl("fft_image_fwd", c, p), double(c.B * c.f_in) * (4.0 * c.n.vol() + 8.0 * p.bins), 0);
-        forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X);
+        forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X, false, nullptr, nullptr, 1, ph_in);
     }
     p.cnt.fwd_image += c.B * c.f_in;
     // kernel spectra of the dilated kernels (memoised for the backward pass)
@@ -1800,7 +2116,7 @@ static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     launch_check("fft_cmac_fwd");
     {
         znn_gpu::prof_scope ps(st, lbl("fft_image_inv", c, p), double(c.B * c.f_out) * (8.0 * p.bins + 4.0 * c.m.vol()), 0);
-        inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB);
+        inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB, ph_out);
     }
     p.cnt.fwd_inverse += c.B * c.f_out;
 }
@@ -1826,7 +2142,8 @@ void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c
 }
 
 static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const float* g, const float* w, float* gw,
-              float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias) {
+              float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias,
+              const phase_geom* ph_g = nullptr, const phase_geom* ph_dx = nullptr) {
     const int64_t nB = c.B;
     const int64_t ccount = std::max(nB * c.f_in * p.Zh * c.n.x * c.n.y, c.f_out * c.f_in * p.Zh * c.k.x * c.k.y);
     const size_t need = sizeof(float2) * size_t(nB * c.f_out * p.bins + (gin ? nB * c.f_in * p.bins : 0) + ccount) +
@@ -1868,7 +2185,7 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     }
     {
         znn_gpu::prof_scope ps(st, lbl("fft_grad_fwd", c, p), double(nB * c.f_out) * (4.0 * c.m.vol() + 8.0 * p.bins), 0);
-        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out);
+        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out, ph_g);
     }
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
@@ -1879,7 +2196,7 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
         launch_check("fft_cmac_bwd");
         {
             znn_gpu::prof_scope ps(st, lbl("fft_dgrad_inv", c, p), double(nB * c.f_in) * (8.0 * p.bins + 4.0 * c.n.vol()), 0);
-            inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB);
+            inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB, ph_dx);
         }
         p.cnt.bwd_inverse += nB * c.f_in;
     }
@@ -1901,72 +2218,62 @@ namespace {
 
 // space-to-batch: x [B][f][n] -> xp [B][S][f][nr] with xp[(b S + r) f + i][q] =
 // x[b][i][s q + r] (r = (rx sy + ry) sz + rz), optionally gated by a ReLU
-// output (g * (y > 0), the fused transfer backward). One warp per input
-// z-line: coalesced reads, and each store instruction fills sz phase lines
-// with runs of 32 / sz consecutive floats. Lanes beyond a phase's valid
-// length are never written (the caller zero-fills ragged phases).
+// output (g * (y > 0), the fused transfer backward). Block = 8 z-lines
+// (threadIdx.y) of one (image, x); lanes walk z: coalesced 128-byte reads,
+// each store instruction fills sz phase lines with runs of 32 / sz floats.
+// All index math is 32-bit except the two line bases. Voxels of a ragged
+// phase beyond its valid length are never written (the caller zero-fills).
 __global__ void __launch_bounds__(256) phase_split_k(const float* __restrict__ x, const float* __restrict__ gate,
-                                                     int64_t lines, int f, int nx, int ny, int nz, int sx, int sy,
-                                                     int sz, int nrx, int nry, int nrz, float* __restrict__ xp) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    const int S = sx * sy * sz;
-    for (int64_t ln = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); ln < lines; ln += warps) {
-        const int yy = int(ln % ny);
-        int64_t t = ln / ny;
-        const int xx = int(t % nx);
-        t /= nx;
-        const int i = int(t % f);
-        const int64_t b = t / f;
-        const int qx = xx / sx, rx = xx - qx * sx, qy = yy / sy, ry = yy - qy * sy;
-        const int64_t rb = (b * S + int64_t(rx * sy + ry) * sz) * f + i;  // image of phase (rx, ry, rz = 0)
-        const float* src = x + ln * nz;
-        const float* gsrc = gate ? gate + ln * nz : nullptr;
-        for (int z0 = 0; z0 < nz; z0 += 32) {
-            const int z = z0 + lane;
-            if (z < nz) {
-                float v = __ldcs(src + z);
-                if (gsrc && !(__ldcs(gsrc + z) > 0.f)) v = 0.f;
-                const int qz = z / sz, rz = z - qz * sz;
-                const int64_t img = rb + int64_t(rz) * f;
-                xp[((img * nrx + qx) * nry + qy) * nrz + qz] = v;
-            }
-        }
+                                                     phase_geom G, float* __restrict__ xp) {
+    const int yy = blockIdx.x * 8 + threadIdx.y;
+    if (yy >= G.ny) return;
+    const int xx = blockIdx.y, img = blockIdx.z;
+    const int b = img / G.f, i = img - b * G.f;
+    const int qx = xx / G.sx, rx = xx - qx * G.sx, qy = yy / G.sy, ry = yy - qy * G.sy;
+    const int S = G.sx * G.sy * G.sz;
+    const int64_t src = ((int64_t(img) * G.nx + xx) * G.ny + yy) * G.nz;
+    const int rb = (b * S + (rx * G.sy + ry) * G.sz) * G.f + i;  // phase image of rz = 0
+    const int64_t pl = int64_t(G.nrx) * G.nry * G.nrz;            // phase image volume
+    const int64_t dst0 = (int64_t(qx) * G.nry + qy) * G.nrz;
+    for (int z = threadIdx.x; z < G.nz; z += 32) {
+        float v = __ldcs(x + src + z);
+        if (gate && !(__ldcs(gate + src + z) > 0.f)) v = 0.f;
+        int qz, rz;
+        zsplit(z, G.sz, G.zsh, qz, rz);
+        xp[int64_t(rb + rz * G.f) * pl + dst0 + qz] = v;
     }
 }
 
 // batch-to-space: yp [B][S][f][mr] -> y [B][f][m], y[b][o][s q + r] =
-// yp[(b S + r) f + o][q]; one warp per output z-line, coalesced stores.
-__global__ void __launch_bounds__(256) phase_merge_k(const float* __restrict__ yp, int64_t lines, int f, int mx,
-                                                     int my, int mz, int sx, int sy, int sz, int mrx, int mry,
-                                                     int mrz, float* __restrict__ y) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-    const int S = sx * sy * sz;
-    for (int64_t ln = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); ln < lines; ln += warps) {
-        const int yy = int(ln % my);
-        int64_t t = ln / my;
-        const int xx = int(t % mx);
-        t /= mx;
-        const int o = int(t % f);
-        const int64_t b = t / f;
-        const int qx = xx / sx, rx = xx - qx * sx, qy = yy / sy, ry = yy - qy * sy;
-        const int64_t rb = (b * S + int64_t(rx * sy + ry) * sz) * f + o;
-        float* dst = y + ln * mz;
-        for (int z0 = 0; z0 < mz; z0 += 32) {
-            const int z = z0 + lane;
-            if (z < mz) {
-                const int qz = z / sz, rz = z - qz * sz;
-                const int64_t img = rb + int64_t(rz) * f;
-                __stcs(dst + z, __ldcs(yp + ((img * mrx + qx) * mry + qy) * mrz + qz));
-            }
-        }
+// yp[(b S + r) f + o][q]; same block shape, coalesced stores.
+__global__ void __launch_bounds__(256) phase_merge_k(const float* __restrict__ yp, phase_geom G,
+                                                     float* __restrict__ y) {
+    const int yy = blockIdx.x * 8 + threadIdx.y;
+    if (yy >= G.ny) return;
+    const int xx = blockIdx.y, img = blockIdx.z;
+    const int b = img / G.f, o = img - b * G.f;
+    const int qx = xx / G.sx, rx = xx - qx * G.sx, qy = yy / G.sy, ry = yy - qy * G.sy;
+    const int S = G.sx * G.sy * G.sz;
+    const int64_t dst = ((int64_t(img) * G.nx + xx) * G.ny + yy) * G.nz;
+    const int rb = (b * S + (rx * G.sy + ry) * G.sz) * G.f + o;
+    const int64_t pl = int64_t(G.nrx) * G.nry * G.nrz;
+    const int64_t src0 = (int64_t(qx) * G.nry + qy) * G.nrz;
+    for (int z = threadIdx.x; z < G.nz; z += 32) {
+        int qz, rz;
+        zsplit(z, G.sz, G.zsh, qz, rz);
+        __stcs(y + dst + z, __ldcs(yp + int64_t(rb + rz * G.f) * pl + src0 + qz));
     }
 }
 
-unsigned warp_grid(int64_t lines) {
-    const int64_t blocks = ceil_div(lines, 8);  // 8 warps per 256-thread block
-    return unsigned(std::min<int64_t>(blocks, 148 * 16));
+phase_geom geom(const conv_shape& c, int64_t maps, dims3 n, dims3 nr) {
+    phase_geom G;
+    G.f = int(maps), G.nx = int(n.x), G.ny = int(n.y), G.nz = int(n.z);
+    G.sx = int(c.s.x), G.sy = int(c.s.y), G.sz = int(c.s.z);
+    G.zsh = -1;
+    for (int k = 0; k < 8; ++k)
+        if ((1 << k) == G.sz) G.zsh = k;
+    G.nrx = int(nr.x), G.nry = int(nr.y), G.nrz = int(nr.z);
+    return G;
 }
 
 void phase_split(cudaStream_t st, const plan& p, const conv_shape& c, const float* x, const float* gate, int64_t maps,
@@ -1974,17 +2281,16 @@ void phase_split(cudaStream_t st, const plan& p, const conv_shape& c, const floa
     const bool ragged = nr.x * c.s.x != n.x || nr.y * c.s.y != n.y || nr.z * c.s.z != n.z;
     if (ragged)  // phases shorter than nr: the missing voxels are the zero padding
         ZNN_CUDA_CHECK(cudaMemsetAsync(xp, 0, sizeof(float) * size_t(c.B * p.S * maps * nr.vol()), st));
-    const int64_t lines = c.B * maps * n.x * n.y;
-    phase_split_k<<<warp_grid(lines), 256, 0, st>>>(x, gate, lines, int(maps), int(n.x), int(n.y), int(n.z),
-                                                     int(c.s.x), int(c.s.y), int(c.s.z), int(nr.x), int(nr.y),
-                                                     int(nr.z), xp);
+    require(c.B * maps < 65536 && n.x < 65536, "fft phase split: grid exceeds 65535");
+    const dim3 grid(unsigned(ceil_div(n.y, 8)), unsigned(n.x), unsigned(c.B * maps));
+    phase_split_k<<<grid, dim3(32, 8, 1), 0, st>>>(x, gate, geom(c, maps, n, nr), xp);
     launch_check("fft_phase_split");
 }
 
 void phase_merge(cudaStream_t st, const conv_shape& c, const float* yp, int64_t maps, dims3 m, dims3 mr, float* y) {
-    const int64_t lines = c.B * maps * m.x * m.y;
-    phase_merge_k<<<warp_grid(lines), 256, 0, st>>>(yp, lines, int(maps), int(m.x), int(m.y), int(m.z), int(c.s.x),
-                                                     int(c.s.y), int(c.s.z), int(mr.x), int(mr.y), int(mr.z), y);
+    require(c.B * maps < 65536 && m.x < 65536, "fft phase merge: grid exceeds 65535");
+    const dim3 grid(unsigned(ceil_div(m.y, 8)), unsigned(m.x), unsigned(c.B * maps));
+    phase_merge_k<<<grid, dim3(32, 8, 1), 0, st>>>(yp, geom(c, maps, m, mr), y);
     launch_check("fft_phase_merge");
 }
 
@@ -1998,6 +2304,11 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
         return;
     }
     const conv_shape& e = p.ce;
+    if (small_cube(p) && !fused1_ok(p, e)) {  // phases read / written in place by the fused 3D transforms
+        const phase_geom gi = geom(c, c.f_in, c.n, e.n), go = geom(c, c.f_out, c.m, e.m);
+        conv_fwd_core(st, p, e, x, w, bias, act, y, ws, &gi, &go);
+        return;
+    }
     float* xp = static_cast<float*>(p.phase_ws->get(size_t(phase_bytes(c))));
     float* yp = xp + ((e.B * e.f_in * e.n.vol() + 63) / 64) * 64;
     {
@@ -2016,6 +2327,11 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
         return;
     }
     const conv_shape& e = p.ce;
+    if (small_cube(p) && !fused1_ok(p, e)) {
+        const phase_geom gg = geom(c, c.f_out, c.m, e.m), gx = geom(c, c.f_in, c.n, e.n);
+        conv_bwd_core(st, p, e, g, w, gw, gin, ws, relu_y, dbias, &gg, &gx);
+        return;
+    }
     float* dxp = static_cast<float*>(p.phase_ws->get(size_t(phase_bytes(c))));
     float* gp = dxp + ((e.B * e.f_in * e.n.vol() + 63) / 64) * 64;
     {

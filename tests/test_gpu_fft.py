@@ -206,7 +206,7 @@ def test_roofline_probes(ctx):
     engine's own bin count for a layer shape, and the measured 3-register
     FFMA rate is a plausible B200 figure."""
     from paper_1510_06706_b200 import ops
-    ms, bins = ops.fft_cmac_time(ctx, 2, 4, 8, 6, (20, 18, 16), (3, 3, 3), (2, 2, 2), reps=2)
+    ms, bins = ops.fft_cmac_time(ctx, 2, 4, 8, 6, (20, 18, 16), (3, 3, 3), (1, 1, 1), reps=2)
     assert ms > 0 and bins == 20 * 20 * (16 // 2 + 1)  # pads: x, y 20 (square planes), z 16
     for which in (0, 1):
         assert ops.fft_cmac_time(ctx, which, 4, 8, 6, (20, 18, 16), (3, 3, 3), (2, 2, 2), reps=1)[0] > 0
@@ -239,3 +239,34 @@ def test_fft_polyphase_plan_shrinks_kernel_spectra(ctx):
     info = p.info()
     assert info["pads"] == (48, 48, 48) and info["bins"] == 48 * 48 * 25
     p.close()
+
+
+@pytest.mark.parametrize("shape", [CASES[2], CASES[4], CASES[6]], ids=str)
+def test_fft_split_passes_without_small_cubes(ctx, monkeypatch, shape):
+    """Small pads run the fused single-CTA 3D transforms (phases addressed in
+    place); with ZNN_FFT_NO_CUBE=1 the same layers take the z + xy passes and
+    the explicit phase split / merge kernels, and stay exact."""
+    monkeypatch.setenv("ZNN_FFT_NO_CUBE", "1")
+    test_fft_conv_fwd_matches_oracle(ctx, shape)
+
+
+@pytest.mark.parametrize("cube", ["1", "0"])
+def test_fft_net_step_small_cube_and_split_paths(ctx, monkeypatch, cube):
+    """One scaled-c4 step (7^3 kernels, sparsities 2 and 4: polyphase layers at
+    small pads) with and without the fused small-cube transforms matches the
+    oracle (fwd 1e-4, gradients and updated weights 1e-3)."""
+    from paper_1510_06706_b200 import configs as C
+    if cube == "0":
+        monkeypatch.setenv("ZNN_FFT_NO_CUBE", "1")
+    cfg = C.scaled("c4", 16, (2, 2, 2), batch=3)
+    nconv = len(cfg.conv_layers())
+    engines = ["fft"] * (nconv - 1) + ["direct"]
+    net, params, x, lab, loss, grads, newp = _net_one_step(ctx, cfg, engines)
+    g = O.parse_netspec(cfg.netspec(), cfg.out_dims)
+    ins = [[x[b, 0]] for b in range(cfg.batch)]
+    labs = [[lab[b, o] for o in range(lab.shape[1])] for b in range(cfg.batch)]
+    rl, rg, rp, _ = O.train_step(g, params.astype(np.float64), np.zeros(params.size), ins, labs, cfg.lr,
+                                 cfg.momentum, cfg.loss)
+    assert abs(loss - rl) / (abs(rl) + 1) < 1e-4
+    assert O.max_rel_error(grads, rg) < 1e-3
+    assert O.max_rel_error(newp, rp) < 1e-3
