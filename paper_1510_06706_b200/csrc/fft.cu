@@ -738,17 +738,27 @@ __device__ __forceinline__ void zsplit(int z, int sz, int zsh, int& q, int& r) {
     }
 }
 
-// original-tensor line base of phase image img, phase line (qx, qy); -1 if
-// the line lies outside the original volume (ragged phase); *rz = z phase
-__device__ __forceinline__ int64_t phase_line(const phase_geom& G, int img, int qx, int qy, int* rz) {
+// phase image img = (b S + r) f + i decoded once per CTA
+struct phase_img {
+    int64_t base;  // offset of map (b, i) in the original tensor
+    int rx, ry, rz;
+};
+__device__ __forceinline__ phase_img phase_decode(const phase_geom& G, int img) {
     const int S = G.sx * G.sy * G.sz;
     const int b = img / (S * G.f), rem = img - b * S * G.f;
     const int r = rem / G.f, i = rem - r * G.f;
-    const int rzz = r % G.sz, t = r / G.sz, ry = t % G.sy, rx = t / G.sy;
-    *rz = rzz;
-    const int x = G.sx * qx + rx, y = G.sy * qy + ry;
+    phase_img d;
+    d.rz = r % G.sz;
+    const int t = r / G.sz;
+    d.ry = t % G.sy, d.rx = t / G.sy;
+    d.base = (int64_t(b) * G.f + i) * G.nx * G.ny * int64_t(G.nz);
+    return d;
+}
+// original-tensor base of phase line (qx, qy); -1 outside the volume (ragged phase)
+__device__ __forceinline__ int64_t phase_line(const phase_geom& G, const phase_img& d, int qx, int qy) {
+    const int x = G.sx * qx + d.rx, y = G.sy * qy + d.ry;
     if (x >= G.nx || y >= G.ny) return -1;
-    return ((int64_t(b) * G.f + i) * G.nx + x) * G.ny * int64_t(G.nz) + int64_t(y) * G.nz;
+    return d.base + (int64_t(x) * G.ny + y) * G.nz;
 }
 
 // ---- fused 3D transforms of small pads (P <= 32): one CTA holds an
@@ -779,6 +789,14 @@ constexpr size_t cube_smem() {
     return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(line_shape<P>::XP) +
                              size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
 }
+// the forward stages the whole real image in shared memory first (every load
+// of the CTA in flight at once) when it fits beside the cube
+template <int P>
+constexpr bool cube_pref() { return P <= 24; }
+template <int P>
+constexpr size_t cube_fwd_smem() {
+    return cube_smem<P>() + (cube_pref<P>() ? sizeof(float) * size_t(P) * P * P : 0);
+}
 
 template <int P>
 __global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* __restrict__ spec) {
@@ -788,13 +806,49 @@ __global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* _
     float2* tw = sm;
     float2* xbuf = tw + P;
     float2* cube = xbuf + LINES * line_shape<P>::XP;  // [Zh][P][PYP]
+    float* inb = reinterpret_cast<float*>(cube + Zh * P * PYP);  // [nx][ny][nz] (cube_pref)
     fill_twiddles<P>(tw);
     const int img = blockIdx.x;
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     float2* xb = xbuf + l * line_shape<P>::XP;
+    phase_img pd{};
+    if (a.phased) pd = phase_decode(a.ph, img);
+    // source of voxel (x, y, z) of this image: -1 = zero padding
+    auto src_of = [&](int x, int y, int z) -> int64_t {
+        if (a.phased) {
+            const int64_t b = phase_line(a.ph, pd, x, y);
+            const int zz = pd.rz + a.ph.sz * z;
+            return (b >= 0 && zz < a.ph.nz) ? b + zz : -1;
+        }
+        return int64_t(img) * a.img_stride + (int64_t(x) * a.ny + y) * a.nz + z;
+    };
+    const int nl1 = a.nx * a.ny;
+    if constexpr (cube_pref<P>()) {
+        // the whole real image into shared memory, 8 loads in flight per thread
+        const int total = nl1 * a.nz;
+        for (int i0 = threadIdx.x; i0 < total; i0 += 8 * THREADS) {
+            float v8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int idx = i0 + u * THREADS;
+                v8[u] = 0.f;
+                if (idx < total) {
+                    const int ln = idx / a.nz, z = idx - ln * a.nz;
+                    const int64_t o = src_of(ln / a.ny, ln - (ln / a.ny) * a.ny, z);
+                    if (o >= 0) {
+                        float val = __ldg(a.src + o);
+                        if (a.gate && !(__ldg(a.gate + o) > 0.f)) val = 0.f;
+                        v8[u] = val;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (i0 + u * THREADS < total) inb[i0 + u * THREADS] = v8[u];
+        }
+    }
     __syncthreads();
     // z lines (R2C) of the valid (x, y) lines
-    const int nl1 = a.nx * a.ny;
     for (int b0 = 0; b0 < nl1; b0 += LINES) {
         const int ln = b0 + l;
         const bool ok = ln < nl1;
@@ -803,29 +857,19 @@ __global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* _
 #pragma unroll
         for (int n2 = 0; n2 < R2; ++n2) v[n2] = make_float2(0.f, 0.f);
         if (ok && t < R1) {
-            if (a.phased) {
-                int rz;
-                const int64_t base = phase_line(a.ph, img, x, y, &rz);
-                if (base >= 0) {
 #pragma unroll
-                    for (int n2 = 0; n2 < R2; ++n2) {
-                        const int z = rz + a.ph.sz * (t + R1 * n2);
-                        if (t + R1 * n2 < a.nz && z < a.ph.nz) {
-                            float val = __ldg(a.src + base + z);
-                            if (a.gate && !(__ldg(a.gate + base + z) > 0.f)) val = 0.f;
+            for (int n2 = 0; n2 < R2; ++n2) {
+                const int z = t + R1 * n2;
+                if (z < a.nz) {
+                    if constexpr (cube_pref<P>()) {
+                        v[n2].x = inb[ln * a.nz + z];
+                    } else {
+                        const int64_t o = src_of(x, y, z);
+                        if (o >= 0) {
+                            float val = __ldg(a.src + o);
+                            if (a.gate && !(__ldg(a.gate + o) > 0.f)) val = 0.f;
                             v[n2].x = val;
                         }
-                    }
-                }
-            } else {
-                const int64_t base = int64_t(img) * a.img_stride + (int64_t(x) * a.ny + y) * a.nz;
-#pragma unroll
-                for (int n2 = 0; n2 < R2; ++n2) {
-                    const int z = t + R1 * n2;
-                    if (z < a.nz) {
-                        float val = __ldg(a.src + base + z);
-                        if (a.gate && !(__ldg(a.gate + base + z) > 0.f)) val = 0.f;
-                        v[n2].x = val;
                     }
                 }
             }
@@ -894,12 +938,24 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
     const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
     float2* xb = xbuf + l * line_shape<P>::XP;
     const float4* g4 = reinterpret_cast<const float4*>(spec + int64_t(img) * (Zh * P * P));
-    for (int idx = threadIdx.x; idx < Zh * P * P / 2; idx += THREADS) {
-        const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
-        const float4 u = __ldcs(g4 + idx);
-        cube[(zb * P + x) * PYP + y] = make_float2(u.x, u.y);
-        cube[(zb * P + x) * PYP + y + 1] = make_float2(u.z, u.w);
+    constexpr int NV = Zh * P * P / 2;
+    for (int i0 = threadIdx.x; i0 < NV; i0 += 4 * THREADS) {  // 4 x 16-byte loads in flight per thread
+        float4 u4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * THREADS < NV) u4[u] = __ldcs(g4 + i0 + u * THREADS);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = i0 + u * THREADS;
+            if (idx < NV) {
+                const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+                cube[(zb * P + x) * PYP + y] = make_float2(u4[u].x, u4[u].y);
+                cube[(zb * P + x) * PYP + y + 1] = make_float2(u4[u].z, u4[u].w);
+            }
+        }
     }
+    phase_img pd{};
+    if (a.phased) pd = phase_decode(a.ph, img);
     __syncthreads();
     // x lines (columns), keep rows xs * i, i < xc, compacted into rows i
     const int nl1 = Zh * P;
@@ -956,10 +1012,10 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
             v[n2] = val;
         }
         int64_t base = -1;
-        int rz = 0;
+        const int rz = pd.rz;
         if (ok) {
             if (a.phased)
-                base = phase_line(a.ph, img, i, j, &rz);
+                base = phase_line(a.ph, pd, i, j);
             else
                 base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + j) * a.oz;
         }
@@ -1797,8 +1853,8 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
             if constexpr (PP <= SMALLP) {
-                allow_smem(fft3_fwd_small_k<PP>, cube_smem<PP>());
-                fft3_fwd_small_k<PP><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(a, spec);
+                allow_smem(fft3_fwd_small_k<PP>, cube_fwd_smem<PP>());
+                fft3_fwd_small_k<PP><<<unsigned(imgs), THREADS, cube_fwd_smem<PP>(), st>>>(a, spec);
             }
         });
         launch_check("fft3_fwd_small");
