@@ -792,7 +792,7 @@ constexpr size_t cube_smem() {
 // the forward stages the whole real image in shared memory first (every load
 // of the CTA in flight at once) when it fits beside the cube
 template <int P>
-constexpr bool cube_pref() { return P <= 24; }
+constexpr bool cube_pref() { return P <= 20; }
 template <int P>
 constexpr size_t cube_fwd_smem() {
     return cube_smem<P>() + (cube_pref<P>() ? sizeof(float) * size_t(P) * P * P : 0);
@@ -824,27 +824,37 @@ __global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* _
     };
     const int nl1 = a.nx * a.ny;
     if constexpr (cube_pref<P>()) {
-        // the whole real image into shared memory, 8 loads in flight per thread
-        const int total = nl1 * a.nz;
-        for (int i0 = threadIdx.x; i0 < total; i0 += 8 * THREADS) {
-            float v8[8];
+        // the whole real image into shared memory: a warp per z-line (lanes
+        // along z, nz <= 32), four lines' loads in flight per warp
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int l0 = warp; l0 < nl1; l0 += 4 * (THREADS / 32)) {
+            float v4[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int idx = i0 + u * THREADS;
-                v8[u] = 0.f;
-                if (idx < total) {
-                    const int ln = idx / a.nz, z = idx - ln * a.nz;
-                    const int64_t o = src_of(ln / a.ny, ln - (ln / a.ny) * a.ny, z);
+            for (int u = 0; u < 4; ++u) {
+                const int ln = l0 + u * (THREADS / 32);
+                v4[u] = 0.f;
+                if (ln < nl1 && lane < a.nz) {
+                    const int x = ln / a.ny, y = ln - x * a.ny;
+                    int64_t o;
+                    if (a.phased) {
+                        const int64_t b = phase_line(a.ph, pd, x, y);
+                        const int zz = pd.rz + a.ph.sz * lane;
+                        o = (b >= 0 && zz < a.ph.nz) ? b + zz : -1;
+                    } else {
+                        o = int64_t(img) * a.img_stride + int64_t(ln) * a.nz + lane;
+                    }
                     if (o >= 0) {
                         float val = __ldg(a.src + o);
                         if (a.gate && !(__ldg(a.gate + o) > 0.f)) val = 0.f;
-                        v8[u] = val;
+                        v4[u] = val;
                     }
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (i0 + u * THREADS < total) inb[i0 + u * THREADS] = v8[u];
+            for (int u = 0; u < 4; ++u) {
+                const int ln = l0 + u * (THREADS / 32);
+                if (ln < nl1 && lane < a.nz) inb[ln * a.nz + lane] = v4[u];
+            }
         }
     }
     __syncthreads();
@@ -924,7 +934,7 @@ __global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* _
     }
 }
 
-template <int P>
+template <int P, bool UNIT>  // UNIT: every kept voxel step is 1 (no per-output division)
 __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __restrict__ spec, cube_io a,
                                                             const float* __restrict__ bias) {
     constexpr int Zh = P / 2 + 1, PYP = P + 1;
@@ -968,8 +978,8 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
 #pragma unroll
         for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? col[(t + R1 * n2) * PYP] : make_float2(0.f, 0.f);
         line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
-            const int i = k / a.xs;
-            if (ok && i * a.xs == k && i < a.xc) col[i * PYP] = val;
+            const int i = UNIT ? k : k / a.xs;
+            if (ok && (UNIT || i * a.xs == k) && i < a.xc) col[i * PYP] = val;
         });
     }
     __syncthreads();
@@ -984,8 +994,8 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
 #pragma unroll
         for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? row[t + R1 * n2] : make_float2(0.f, 0.f);
         line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
-            const int j = k / a.ys;
-            if (ok && j * a.ys == k && j < a.yc) row[j] = val;
+            const int j = UNIT ? k : k / a.ys;
+            if (ok && (UNIT || j * a.ys == k) && j < a.yc) row[j] = val;
         });
     }
     __syncthreads();
@@ -1020,8 +1030,8 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
                 base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + j) * a.oz;
         }
         line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
-            const int q = k / a.zs;
-            if (base >= 0 && q * a.zs == k && q < a.zc) {
+            const int q = UNIT ? k : k / a.zs;
+            if (base >= 0 && (UNIT || q * a.zs == k) && q < a.zc) {
                 float r = val.x * a.scale + bv;
                 if (a.act == 2) r = r > 0.f ? r : 0.f;
                 else if (a.act == 0) r = 1.f / (1.f + expf(-r));
@@ -1929,8 +1939,13 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
             if constexpr (PP <= SMALLP) {
-                allow_smem(fft3_inv_small_k<PP>, cube_smem<PP>());
-                fft3_inv_small_k<PP><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(spec, a, bias);
+                if (a.xs == 1 && a.ys == 1 && a.zs == 1) {
+                    allow_smem(fft3_inv_small_k<PP, true>, cube_smem<PP>());
+                    fft3_inv_small_k<PP, true><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(spec, a, bias);
+                } else {
+                    allow_smem(fft3_inv_small_k<PP, false>, cube_smem<PP>());
+                    fft3_inv_small_k<PP, false><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(spec, a, bias);
+                }
             }
         });
         launch_check("fft3_inv_small");

@@ -1,5 +1,5 @@
 """Per-layer gradient comparison FFT vs direct engine (debug helper, not a
-test): python tests/_fft_grad_check.py [config] [width_div]"""
+test): python tools/_fft_grad_check.py [config] [width_div]"""
 import sys
 import numpy as np
 import torch

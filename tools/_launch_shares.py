@@ -1,5 +1,5 @@
 """Per-kernel shares of an ncu launch list (profiling helper, not a test):
-python tests/_launch_shares.py launches.csv
+python tools/_launch_shares.py launches.csv
 The csv is `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --csv` output; times are cold-cache and serialised,
 so compare shares, not absolutes."""

@@ -1,5 +1,5 @@
 """Per-layer, per-pass device timings of one config's conv layers (profiling
-helper, not a test): python tests/_layer_times.py c5 [engine ...]"""
+helper, not a test): python tools/_layer_times.py c5 [engine ...]"""
 import sys
 
 import numpy as np

@@ -1,5 +1,5 @@
 """Key counters per kernel from ncu reports (profiling helper, not a test):
-python tests/_ncu_summary.py report.ncu-rep [...]"""
+python tools/_ncu_summary.py report.ncu-rep [...]"""
 import csv
 import io
 import subprocess

@@ -1,5 +1,5 @@
 """Run W+K training steps of a config with fixed per-layer engines (profiling
-helper, not a test): python tests/_net_steps.py c4 fft,fft,fft,direct|auto [steps]"""
+helper, not a test): python tools/_net_steps.py c4 fft,fft,fft,direct|auto [steps]"""
 import sys
 import time
 

@@ -1,5 +1,5 @@
 """One fwd / dgrad / wgrad launch of a conv layer shape, for ncu captures
-(profiling helper, not a test): python tests/_prof_conv.py B fi fo n k s"""
+(profiling helper, not a test): python tools/_prof_conv.py B fi fo n k s"""
 import sys
 
 import torch

@@ -1,5 +1,5 @@
 """Device time and achieved HBM GB/s of the pointwise / max-filter passes at
-c5 sizes (profiling helper, not a test): python tests/_pw_times.py [B]"""
+c5 sizes (profiling helper, not a test): python tools/_pw_times.py [B]"""
 import sys
 
 import torch

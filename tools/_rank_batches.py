@@ -1,6 +1,6 @@
 """Per-rank step time of a config at the local batch each of N data-parallel
 ranks would hold (B/N), autotuned per batch (profiling helper, not a test):
-python tests/_rank_batches.py c5 16 8 4 2 1"""
+python tools/_rank_batches.py c5 16 8 4 2 1"""
 import sys
 import time
 

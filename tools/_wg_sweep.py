@@ -1,6 +1,6 @@
 """Weight-gradient device time of c5's conv layers under environment
 overrides (profiling helper, not a test):
-python tests/_wg_sweep.py c5 ZNN_WGRAD_SPLITS=0,5,10,20"""
+python tools/_wg_sweep.py c5 ZNN_WGRAD_SPLITS=0,5,10,20"""
 import os
 import sys
 
