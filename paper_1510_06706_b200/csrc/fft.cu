@@ -252,7 +252,8 @@ __device__ __forceinline__ void line_fft(float2* v, float2* xb, const float2* tw
 template <int P>
 __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__ in, int64_t in_img_stride, int nx,
                                                         int ny, int nz, int64_t nlines, float2* __restrict__ spec,
-                                                        int Px, int Py, const float* __restrict__ gate) {
+                                                        int Px, int Py, const float* __restrict__ gate,
+                                                        phase_geom ph, int phased) {
     constexpr int Zh = P / 2 + 1;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
@@ -272,20 +273,28 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
         const uint32_t im = uint32_t(line) / pl;
         const int r = int(uint32_t(line) - im * pl);
         const int x = r / ny, y = r - (r / ny) * ny;
-        const int64_t off = int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
-        const float* src = in + off;
-        if (t < R1) {
+        // element j of the line: off + z0 + zs * j (phased: the phase's voxels of
+        // the original tensor, valid below zlim; dense: contiguous)
+        int64_t off = int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
+        int z0 = 0, zs = 1, zlim = nz;
+        if (phased) {
+            const phase_img pd = phase_decode(ph, int(im));
+            off = phase_line(ph, pd, x, y);
+            z0 = pd.rz, zs = ph.sz, zlim = off >= 0 ? ph.nz : 0;
+        }
+        if (t < R1 && off >= 0) {
+            const float* src = in + off;
 #pragma unroll
             for (int n2 = 0; n2 < R2; ++n2) {
-                const int j = t + R1 * n2;
-                if (j < nz) v[n2].x = __ldg(src + j);
+                const int j = t + R1 * n2, z = z0 + zs * j;
+                if (j < nz && z < zlim) v[n2].x = __ldg(src + z);
             }
             if (gate) {  // fused ReLU backward: g * (y > 0) (transfer.hpp:99-106, ReLU'(0) = 0)
                 const float* gp = gate + off;
 #pragma unroll
                 for (int n2 = 0; n2 < R2; ++n2) {
-                    const int j = t + R1 * n2;
-                    if (j < nz && !(__ldg(gp + j) > 0.f)) v[n2].x = 0.f;
+                    const int j = t + R1 * n2, z = z0 + zs * j;
+                    if (j < nz && z < zlim && !(__ldg(gp + z) > 0.f)) v[n2].x = 0.f;
                 }
             }
         }
@@ -792,7 +801,7 @@ constexpr size_t cube_smem() {
 // the forward stages the whole real image in shared memory first (every load
 // of the CTA in flight at once) when it fits beside the cube
 template <int P>
-constexpr bool cube_pref() { return P <= 20; }
+constexpr bool cube_pref() { return false; }  // staging the image cost occupancy (measured slower); kept for reference
 template <int P>
 constexpr size_t cube_fwd_smem() {
     return cube_smem<P>() + (cube_pref<P>() ? sizeof(float) * size_t(P) * P * P : 0);
@@ -858,32 +867,41 @@ __global__ void __launch_bounds__(THREADS) fft3_fwd_small_k(cube_io a, float2* _
         }
     }
     __syncthreads();
-    // z lines (R2C) of the valid (x, y) lines
+    // z lines (R2C) of the valid (x, y) lines; the next group's loads are
+    // issued before this group's transform (register double buffer)
+    auto load_line = [&](int ln, float (&r)[R2]) {
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) r[n2] = 0.f;
+        if (ln < nl1 && t < R1) {
+            const int x = ln / a.ny, y = ln - (ln / a.ny) * a.ny;
+#pragma unroll
+            for (int n2 = 0; n2 < R2; ++n2) {
+                const int z = t + R1 * n2;
+                if (z < a.nz) {
+                    if constexpr (cube_pref<P>()) {
+                        r[n2] = inb[ln * a.nz + z];
+                    } else {
+                        const int64_t o = src_of(x, y, z);
+                        if (o >= 0) {
+                            float val = __ldg(a.src + o);
+                            if (a.gate && !(__ldg(a.gate + o) > 0.f)) val = 0.f;
+                            r[n2] = val;
+                        }
+                    }
+                }
+            }
+        }
+    };
+    float nxt[R2];
+    load_line(l, nxt);
     for (int b0 = 0; b0 < nl1; b0 += LINES) {
         const int ln = b0 + l;
         const bool ok = ln < nl1;
         const int x = ok ? ln / a.ny : 0, y = ok ? ln - (ln / a.ny) * a.ny : 0;
         float2 v[R2];
 #pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) v[n2] = make_float2(0.f, 0.f);
-        if (ok && t < R1) {
-#pragma unroll
-            for (int n2 = 0; n2 < R2; ++n2) {
-                const int z = t + R1 * n2;
-                if (z < a.nz) {
-                    if constexpr (cube_pref<P>()) {
-                        v[n2].x = inb[ln * a.nz + z];
-                    } else {
-                        const int64_t o = src_of(x, y, z);
-                        if (o >= 0) {
-                            float val = __ldg(a.src + o);
-                            if (a.gate && !(__ldg(a.gate + o) > 0.f)) val = 0.f;
-                            v[n2].x = val;
-                        }
-                    }
-                }
-            }
-        }
+        for (int n2 = 0; n2 < R2; ++n2) v[n2] = make_float2(nxt[n2], 0.f);
+        load_line(ln + LINES, nxt);
         line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
             if (ok && k < Zh) cube[(k * P + x) * PYP + y] = val;
         });
@@ -1056,6 +1074,8 @@ struct zinv_args {
     int oy, oz;                        // output box dims (y, z)
     int act;                           // ZNN_ACT_* (3 = none)
     int bias_mod;                      // bias index = img % bias_mod
+    int phased;                        // outputs are the phases of an original tensor (ph)
+    phase_geom ph;
 };
 
 // ---- z pass, inverse (C2R) of the compact kept lines, crop / tap selection
@@ -1068,6 +1088,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
     extern __shared__ float2 sm[];
     __shared__ int64_t ibase[LINES], obase[LINES];
     __shared__ float bvals[LINES];
+    __shared__ int ozoff[LINES];
     float2* tw = sm;
     float2* xbuf = tw + P;
     float2* stash = xbuf + LINES * line_shape<P>::XP;  // LINES x (Zh + 1)
@@ -1081,7 +1102,14 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
         const int r = int(uint32_t(line) - im * per);
         const int xi = r / g.yc, yi = r - (r / g.yc) * g.yc;
         ibase[l] = int64_t(im) * Zh * per + r;
-        obase[l] = int64_t(im) * g.out_img_stride + (int64_t(xi) * g.oy + yi) * g.oz;
+        if (g.phased) {  // write the phase's voxels of the original tensor in place
+            const phase_img pd = phase_decode(g.ph, int(im));
+            obase[l] = phase_line(g.ph, pd, xi, yi);
+            ozoff[l] = pd.rz;
+        } else {
+            obase[l] = int64_t(im) * g.out_img_stride + (int64_t(xi) * g.oy + yi) * g.oz;
+            ozoff[l] = 0;
+        }
         bvals[l] = bias ? bias[im % uint32_t(g.bias_mod)] : 0.f;
     }
     __syncthreads();
@@ -1123,16 +1151,19 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
         }
         v[n2] = val;
     }
-    float* dst = out + (ok ? obase[l] : 0);
+    const bool wok = ok && obase[l] >= 0;  // phased: ragged phase lines outside the tensor
+    float* dst = out + (wok ? obase[l] + ozoff[l] : 0);
+    const int zst = g.phased ? g.ph.sz : 1;
+    const int zlim = g.phased ? g.ph.nz - (wok ? ozoff[l] : 0) : 1 << 30;
     const float bv = ok ? bvals[l] : 0.f;
     line_fft<P, true>(v, xbuf + l * line_shape<P>::XP, tw, t, [&](int k, float2 val) {
         const int q = k / g.z_step;
-        if (ok && q * g.z_step == k && q < g.z_cnt) {
+        if (wok && q * g.z_step == k && q < g.z_cnt && zst * q < zlim) {
             float r = val.x * g.scale + bv;
             if (g.act == 2) r = r > 0.f ? r : 0.f;
             else if (g.act == 0) r = 1.f / (1.f + expf(-r));
             else if (g.act == 1) r = tanhf(r);
-            dst[q] = r;
+            dst[zst * q] = r;
         }
     });
 }
@@ -1875,14 +1906,15 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         }
         return;
     }
-    require(ph == nullptr, "fft: phase addressing needs the small-cube transforms");
+    require(ph == nullptr || !z_only, "fft: phase addressing with a z-only pass");
     const int64_t nlines = imgs * n.x * n.y;
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
         allow_smem(fft_z_fwd_k<PP>, smem_for(PP));
         fft_z_fwd_k<PP><<<unsigned(ceil_div(nlines, LINES)), THREADS, smem_for(PP), st>>>(
-            in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate);
+            in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate,
+            ph ? *ph : phase_geom{}, ph ? 1 : 0);
     });
     launch_check("fft_z_fwd");
     if (dbias) {
@@ -1914,7 +1946,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
 }
 
 void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 cnt, float* out, int64_t out_img_stride,
-               const float* bias, int bias_mod, int act, const float2* cbuf);
+               const float* bias, int bias_mod, int act, const float2* cbuf, const phase_geom* ph = nullptr);
 
 // inverse 3D C2R keeping voxels (x,y,z) = (step*i) for i < cnt per axis,
 // written as a dense box [imgs][cnt.x][cnt.y][cnt.z] (image stride given);
@@ -1951,7 +1983,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         launch_check("fft3_inv_small");
         return;
     }
-    require(ph == nullptr, "fft: phase addressing needs the small-cube transforms");
+
     const int64_t planes = imgs * p.Zh;
     dispatch_pad(int(p.P.y), [&](auto pc) {
         constexpr int PY = decltype(pc)::value;
@@ -1971,13 +2003,15 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         }
     });
     launch_check("fft_xy_inv");
-    inverse_z(st, p, imgs, step, cnt, out, out_img_stride, bias, bias_mod, act, cbuf);
+    inverse_z(st, p, imgs, step, cnt, out, out_img_stride, bias, bias_mod, act, cbuf, ph);
 }
 
 // z pass of an inverse: C2R of the compact kept planes in cbuf
 void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 cnt, float* out, int64_t out_img_stride,
-               const float* bias, int bias_mod, int act, const float2* cbuf) {
+               const float* bias, int bias_mod, int act, const float2* cbuf, const phase_geom* ph) {
     zinv_args g;
+    g.phased = ph ? 1 : 0;
+    g.ph = ph ? *ph : phase_geom{};
     g.xc = int(cnt.x), g.yc = int(cnt.y);
     g.z_step = int(step.z), g.z_cnt = int(cnt.z);
     g.nlines = imgs * cnt.x * cnt.y;
@@ -2375,7 +2409,9 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
         return;
     }
     const conv_shape& e = p.ce;
-    if (small_cube(p) && !fused1_ok(p, e)) {  // phases read / written in place by the fused 3D transforms
+    // phases read / written in place by the transforms (no split / merge
+    // pass); ZNN_FFT_PHASE_SPLIT=1 keeps the explicit split / merge kernels
+    if (!fused1_ok(p, e) && !std::getenv("ZNN_FFT_PHASE_SPLIT")) {
         const phase_geom gi = geom(c, c.f_in, c.n, e.n), go = geom(c, c.f_out, c.m, e.m);
         conv_fwd_core(st, p, e, x, w, bias, act, y, ws, &gi, &go);
         return;
@@ -2398,7 +2434,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
         return;
     }
     const conv_shape& e = p.ce;
-    if (small_cube(p) && !fused1_ok(p, e)) {
+    if (!fused1_ok(p, e) && !std::getenv("ZNN_FFT_PHASE_SPLIT")) {
         const phase_geom gg = geom(c, c.f_out, c.m, e.m), gx = geom(c, c.f_in, c.n, e.n);
         conv_bwd_core(st, p, e, g, w, gw, gin, ws, relu_y, dbias, &gg, &gx);
         return;
