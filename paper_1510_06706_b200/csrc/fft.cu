@@ -247,6 +247,48 @@ __device__ __forceinline__ void line_fft(float2* v, float2* xb, const float2* tw
     __syncwarp();
 }
 
+// ---- phase geometry of a dilated layer's polyphase plan: phase image
+// img = (b S + r) f + i of the original tensor [B][f][nx][ny][nz], phase
+// r = (rx sy + ry) sz + rz holds the voxels (s q + r) ----
+struct phase_geom {
+    int f, nx, ny, nz;     // original tensor (maps, dims)
+    int sx, sy, sz, zsh;   // sparsity; zsh = log2(sz) when sz is a power of two, else -1
+    int nrx, nry, nrz;     // phase dims
+};
+
+__device__ __forceinline__ void zsplit(int z, int sz, int zsh, int& q, int& r) {
+    if (zsh >= 0) {
+        q = z >> zsh;
+        r = z & (sz - 1);
+    } else {
+        q = z / sz;
+        r = z - q * sz;
+    }
+}
+
+// phase image img = (b S + r) f + i decoded once per CTA
+struct phase_img {
+    int64_t base;  // offset of map (b, i) in the original tensor
+    int rx, ry, rz;
+};
+__device__ __forceinline__ phase_img phase_decode(const phase_geom& G, int img) {
+    const int S = G.sx * G.sy * G.sz;
+    const int b = img / (S * G.f), rem = img - b * S * G.f;
+    const int r = rem / G.f, i = rem - r * G.f;
+    phase_img d;
+    d.rz = r % G.sz;
+    const int t = r / G.sz;
+    d.ry = t % G.sy, d.rx = t / G.sy;
+    d.base = (int64_t(b) * G.f + i) * G.nx * G.ny * int64_t(G.nz);
+    return d;
+}
+// original-tensor base of phase line (qx, qy); -1 outside the volume (ragged phase)
+__device__ __forceinline__ int64_t phase_line(const phase_geom& G, const phase_img& d, int qx, int qy) {
+    const int x = G.sx * qx + d.rx, y = G.sy * qy + d.ry;
+    if (x >= G.nx || y >= G.ny) return -1;
+    return d.base + (int64_t(x) * G.ny + y) * G.nz;
+}
+
 // ---- z pass, forward (R2C): lines (img, x < nx, y < ny) of the real input,
 // half spectra stored transposed: spec[img][zb][x][y] ----
 template <int P>
@@ -726,48 +768,6 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_upd1_k(const float2* __res
             if (e < P * P) dk[e] = acc[i];
         }
     }
-}
-
-// ---- phase geometry of a dilated layer's polyphase plan: phase image
-// img = (b S + r) f + i of the original tensor [B][f][nx][ny][nz], phase
-// r = (rx sy + ry) sz + rz holds the voxels (s q + r) ----
-struct phase_geom {
-    int f, nx, ny, nz;     // original tensor (maps, dims)
-    int sx, sy, sz, zsh;   // sparsity; zsh = log2(sz) when sz is a power of two, else -1
-    int nrx, nry, nrz;     // phase dims
-};
-
-__device__ __forceinline__ void zsplit(int z, int sz, int zsh, int& q, int& r) {
-    if (zsh >= 0) {
-        q = z >> zsh;
-        r = z & (sz - 1);
-    } else {
-        q = z / sz;
-        r = z - q * sz;
-    }
-}
-
-// phase image img = (b S + r) f + i decoded once per CTA
-struct phase_img {
-    int64_t base;  // offset of map (b, i) in the original tensor
-    int rx, ry, rz;
-};
-__device__ __forceinline__ phase_img phase_decode(const phase_geom& G, int img) {
-    const int S = G.sx * G.sy * G.sz;
-    const int b = img / (S * G.f), rem = img - b * S * G.f;
-    const int r = rem / G.f, i = rem - r * G.f;
-    phase_img d;
-    d.rz = r % G.sz;
-    const int t = r / G.sz;
-    d.ry = t % G.sy, d.rx = t / G.sy;
-    d.base = (int64_t(b) * G.f + i) * G.nx * G.ny * int64_t(G.nz);
-    return d;
-}
-// original-tensor base of phase line (qx, qy); -1 outside the volume (ragged phase)
-__device__ __forceinline__ int64_t phase_line(const phase_geom& G, const phase_img& d, int qx, int qy) {
-    const int x = G.sx * qx + d.rx, y = G.sy * qy + d.ry;
-    if (x >= G.nx || y >= G.ny) return -1;
-    return d.base + (int64_t(x) * G.ny + y) * G.nz;
 }
 
 // ---- fused 3D transforms of small pads (P <= 32): one CTA holds an
