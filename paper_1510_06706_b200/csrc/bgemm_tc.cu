@@ -1,0 +1,344 @@
+// Frequency-domain sums over converging edges (the CMACs of the FFT engine,
+// conv_fft.hpp:38-125 summed by merge_payload, engine.hpp:345-353) as
+// per-bin complex GEMMs on the tcgen05 tensor cores, 3xTF32.
+//
+// For the polyphase plans of dilated layers every kernel-spectrum bin feeds
+// B s^3 phase images (c5 conv3-5: 1024), so per bin the three sums are
+// real GEMMs with a large reuse dimension:
+//   fwd  : Y[n][o]  = sum_i X[n][i] conj K[o][i]   D[n][(o,c')]  = A(X)  . B(K)
+//   dgrad: DX[n][i] = sum_o G[n][o] K[o][i]         D[n][(i,c')]  = A(G)  . B(K^T)
+//   upd  : dK[o][i] = sum_n X[n][i] conj G[n][o]    D[o][(i,c')]  = A(G^T). B(X^T)
+// with complex numbers embedded as (re, im) pairs along K and the output
+// columns (o, c') interleaved, so D rows are the natural complex layout. A
+// rows are the natural complex rows of the left operand; B rows come in two
+// variants per column ((re, im) and a swapped / negated copy), e.g. for fwd
+// Yr = sum (Xr Kr + Xi Ki) = A . (Kr, Ki), Yi = sum (Xi Kr - Xr Ki) = A . (-Ki, Kr).
+//
+// Spectra live image-major ([img][bins], bins contiguous: what the
+// transforms produce). prep_k transposes them bin-major ([bin][row][k]) and
+// splits fp32 into hi (the raw value: the MMA reads the top 19 bits) and
+// lo = x - tf32(x); unprep_k transposes D back. The GEMM kernel is a TMA ->
+// tcgen05 pipeline: per CTA one (bin, 128-row tile), K in 32-wide chunks
+// (SWIZZLE_128B K-major tiles, 2 stages), D (N <= 256 columns) in TMEM,
+// D += Ahi Bhi + Ahi Blo + Alo Bhi.
+#include <cuda.h>
+
+#include <algorithm>
+
+#include "bgemm_tc.hpp"
+#include "tc_common.cuh"
+
+namespace znn_gpu {
+
+CUtensorMap make_panel_map_rows(const float* ptr, int64_t cols, int64_t rows, int box_rows);
+
+namespace {
+
+using namespace znn_tc;
+
+constexpr int TB = 32;  // transpose tile (images or k-side indices) x bins
+
+// variant code: bit0 swap (re, im) -> (im, re), bit1 negate the first, bit2 the second
+__device__ __forceinline__ float2 variant(float2 z, int code) {
+    float2 r = (code & 1) ? make_float2(z.y, z.x) : z;
+    if (code & 2) r.x = -r.x;
+    if (code & 4) r.y = -r.y;
+    return r;
+}
+
+// S [img = p * F + q][bins] complex -> hi / lo [bin][row][k] fp32.
+// ROWQ = false: row = p (rows R = Pn), k = 2 q + c (K = 2 F)        (A of fwd / dgrad)
+// ROWQ = true : row = q or (q, c') (NV = 1 or 2 variants), k = 2 p + c (K = 2 Pn)
+// ROWQ = false with NV = 2: row = (p, c'), k = 2 q + c                 (B of fwd)
+// block: one row-side index, TB k-side indices x TB bins; threads 32 x 8
+template <bool ROWQ, int NV>
+__global__ void __launch_bounds__(256) prep_k(const float2* __restrict__ S, int64_t bins, int Pn, int F, int v0,
+                                              int v1, float* __restrict__ hi, float* __restrict__ lo) {
+    __shared__ float2 tile[TB][TB + 1];
+    const int rs = blockIdx.z;                // row-side index (p, or q when ROWQ)
+    const int j0 = blockIdx.y * TB;           // k-side indices (q, or p when ROWQ)
+    const int64_t w0 = int64_t(blockIdx.x) * TB;
+    const int nk = ROWQ ? Pn : F;             // k-side extent
+    const int K = 2 * nk;
+    const int R = (ROWQ ? F : Pn) * NV;       // rows per bin
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int jj = ty; jj < TB; jj += 8) {
+        const int j = j0 + jj;
+        const int64_t w = w0 + tx;
+        float2 v = make_float2(0.f, 0.f);
+        if (j < nk && w < bins) {
+            const int64_t img = ROWQ ? int64_t(j) * F + rs : int64_t(rs) * F + j;
+            v = __ldcs(S + img * bins + w);
+        }
+        tile[jj][tx] = v;
+    }
+    __syncthreads();
+    // out row (bin, rs, c'): the k-side pairs j0..j0+TB as 2 TB consecutive floats
+    for (int ww = ty; ww < TB; ww += 8) {
+        const int64_t w = w0 + ww;
+        if (w >= bins) continue;
+#pragma unroll
+        for (int cv = 0; cv < NV; ++cv) {
+            const int code = cv == 0 ? v0 : v1;
+            const int64_t row = int64_t(rs) * NV + cv;
+            float* oh = hi + (w * R + row) * K + 2 * j0;
+            float* ol = lo + (w * R + row) * K + 2 * j0;
+            // lanes write floats tx and tx + 32 of the 64-float segment
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int e = tx + 32 * h, jj = e >> 1;
+                if (j0 + jj < nk) {
+                    const float2 z = variant(tile[jj][ww], code);
+                    const float x = (e & 1) ? z.y : z.x;
+                    const float xh = tf32_hi(x);
+                    oh[e] = x;
+                    ol[e] = x - xh;
+                }
+            }
+        }
+    }
+}
+
+// D [bin][p][2 Q] fp32 (complex rows) -> S [p * Q + q][bins] complex
+__global__ void __launch_bounds__(256) unprep_k(const float* __restrict__ D, int64_t bins, int Pn, int Q,
+                                                int ldd, float2* __restrict__ S) {
+    __shared__ float2 tile[TB][TB + 1];
+    const int p = blockIdx.z, q0 = blockIdx.y * TB;
+    const int64_t w0 = int64_t(blockIdx.x) * TB;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int ww = ty; ww < TB; ww += 8) {
+        const int64_t w = w0 + ww;
+        float2 v = make_float2(0.f, 0.f);
+        if (w < bins && q0 + tx < Q) v = *reinterpret_cast<const float2*>(D + (w * Pn + p) * int64_t(ldd) + 2 * (q0 + tx));
+        tile[ww][tx] = v;
+    }
+    __syncthreads();
+    for (int qq = ty; qq < TB; qq += 8) {
+        const int q = q0 + qq;
+        const int64_t w = w0 + tx;
+        if (q < Q && w < bins) __stcs(S + (int64_t(p) * Q + q) * bins + w, tile[tx][qq]);
+    }
+}
+
+constexpr int BM = 128;   // rows per CTA tile (TMEM lanes)
+constexpr int BKC = 32;   // K per stage (one 128-byte swizzle row)
+constexpr int STAGES = 2;
+
+struct bg_params {
+    int M, N, K;          // per bin: D[M][N] = sum_k A[M][k] B[N][k]
+    int ldd;              // D row pitch (floats)
+    int mtiles;
+};
+
+// warps 0-3: epilogue (TMEM lane quarter = warp); warp 4: TMA; warp 5: TMEM alloc + MMA issue
+__global__ void __launch_bounds__(192, 1)
+bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
+           const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
+           float* __restrict__ D, bg_params p) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t* base_ptr = smem_raw + (base - raw);
+    const uint32_t a_bytes = BM * 128u, b_bytes = uint32_t(p.N) * 128u;
+    const uint32_t stage_bytes = 2u * a_bytes + 2u * b_bytes;
+    const uint32_t bar_base = base + STAGES * stage_bytes;
+    auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
+    auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(STAGES + s); };
+    const uint32_t acc_bar = bar_base + 8u * uint32_t(2 * STAGES);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * STAGES + 2));
+
+    const int warp = threadIdx.x >> 5;
+    const int mt = int(blockIdx.x % unsigned(p.mtiles));
+    const int64_t bin = blockIdx.x / unsigned(p.mtiles);
+    const int m0 = mt * BM;
+    const int nchunks = (p.K + BKC - 1) / BKC;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        mbar_init(acc_bar, 1);
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(smem_u32(tmem_slot), 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // TMA producer: per chunk A hi|lo (128 rows) then B hi|lo (N rows)
+        const int arow = int(bin * p.M + m0), brow = int(bin * p.N);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            mbar_wait(empty_bar(s), ph ^ 1u);
+            const uint32_t st0 = base + uint32_t(s) * stage_bytes;
+            asm volatile(
+                "{\n\t.reg .pred pe;\n\t"
+                "elect.sync _|pe, 0xffffffff;\n\t"
+                "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(full_bar(s)),
+                "r"(stage_bytes)
+                : "memory");
+            tma_w(full_bar(s), st0, &tA_hi, c * BKC, arow);
+            tma_w(full_bar(s), st0 + a_bytes, &tA_lo, c * BKC, arow);
+            tma_w(full_bar(s), st0 + 2u * a_bytes, &tB_hi, c * BKC, brow);
+            tma_w(full_bar(s), st0 + 2u * a_bytes + b_bytes, &tB_lo, c * BKC, brow);
+            if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+    } else if (warp == 5) {
+        const uint32_t idesc = idesc_tf32(BM, p.N);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int c = 0; c < nchunks; ++c) {
+            mbar_wait(full_bar(s), ph);
+            tc_fence_after();
+            const uint32_t a_hi = base + uint32_t(s) * stage_bytes, a_lo = a_hi + a_bytes;
+            const uint32_t b_hi = a_hi + 2u * a_bytes, b_lo = b_hi + b_bytes;
+            const int ksteps = min(BKC, p.K - c * BKC) / 8;
+            for (int kk = 0; kk < ksteps; ++kk) {
+                const uint32_t ko = uint32_t(kk) * 32u;  // 8 fp32 along K
+                const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
+                const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
+                mma_tf32_w(tmem, ah, bh, idesc, (c == 0 && kk == 0) ? 0u : 1u);
+                mma_tf32_w(tmem, ah, bl, idesc, 1u);
+                mma_tf32_w(tmem, al, bh, idesc, 1u);
+            }
+            mma_commit_w(empty_bar(s));
+            if (c == nchunks - 1) mma_commit_w(acc_bar);
+            if (++s == STAGES) s = 0, ph ^= 1u;
+        }
+    } else {
+        // epilogue: lane = row of the tile
+        mbar_wait(acc_bar, 0);
+        tc_fence_after();
+        const int r = threadIdx.x;  // 0..127
+        const uint32_t lane_base = uint32_t(warp * 32) << 16;
+        const int row = m0 + r;
+        float* drow = D + (bin * p.M + row) * int64_t(p.ldd);
+        for (int c0 = 0; c0 < p.N; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + lane_base + uint32_t(c0), v);
+            tmem_wait_ld();
+            if (row < p.M) {
+#pragma unroll
+                for (int q = 0; q < 16; q += 4)
+                    *reinterpret_cast<float4*>(drow + c0 + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        __syncwarp();
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+template <bool ROWQ, int NV>
+void prep(cudaStream_t st, const float2* S, int64_t bins, int Pn, int F, int v0, int v1, float* hi, float* lo) {
+    const int nk = ROWQ ? Pn : F, rsn = ROWQ ? F : Pn;
+    require(rsn < 65536 && ceil_div(nk, TB) < 65536, "tc cmac: prep grid exceeds 65535");
+    const dim3 grid(unsigned(ceil_div(bins, TB)), unsigned(ceil_div(nk, TB)), unsigned(rsn));
+    prep_k<ROWQ, NV><<<grid, dim3(32, 8, 1), 0, st>>>(S, bins, Pn, F, v0, v1, hi, lo);
+    launch_check("tc_cmac_prep");
+}
+
+void unprep(cudaStream_t st, const float* Dp, int64_t bins, int Pn, int Q, int ldd, float2* S) {
+    require(Pn < 65536, "tc cmac: unprep grid exceeds 65535");
+    const dim3 grid(unsigned(ceil_div(bins, TB)), unsigned(ceil_div(Q, TB)), unsigned(Pn));
+    unprep_k<<<grid, dim3(32, 8, 1), 0, st>>>(Dp, bins, Pn, Q, ldd, S);
+    launch_check("tc_cmac_unprep");
+}
+
+void bgemm(cudaStream_t st, const float* Ahi, const float* Alo, const float* Bhi, const float* Blo, float* Dp,
+           int64_t nb, int M, int N, int K) {
+    require(N % 16 == 0 && N <= 256 && K % 8 == 0 && K % 4 == 0, "tc cmac: bad GEMM shape");
+    require(nb * M < (int64_t(1) << 31) && nb * N < (int64_t(1) << 31), "tc cmac: operand rows exceed 2^31");
+    const CUtensorMap ah = make_panel_map_rows(Ahi, K, nb * M, BM), al = make_panel_map_rows(Alo, K, nb * M, BM);
+    const CUtensorMap bh = make_panel_map_rows(Bhi, K, nb * N, N), bl = make_panel_map_rows(Blo, K, nb * N, N);
+    bg_params p{M, N, K, N, int(ceil_div(M, BM))};
+    const size_t smem = size_t(STAGES) * (2 * BM * 128 + 2 * size_t(N) * 128) + 1024 + 256;
+    const int64_t ctas = nb * p.mtiles;
+    require(ctas < (int64_t(1) << 31), "tc cmac: grid too large");
+    ZNN_CUDA_CHECK(cudaFuncSetAttribute(bgemm_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    bgemm_tc_k<<<unsigned(ctas), 192, smem, st>>>(ah, al, bh, bl, Dp, p);
+    launch_check("tc_cmac_gemm");
+}
+
+}  // namespace
+
+int64_t tc_cmac_bytes(int64_t Bn, int64_t f, int64_t fo, int64_t bins) {
+    // A hi|lo + B hi|lo + D for the largest of the three GEMMs
+    const int64_t fwd = 2 * bins * Bn * 2 * f + 2 * bins * 2 * fo * 2 * f + bins * Bn * 2 * fo;
+    const int64_t dgr = 2 * bins * Bn * 2 * fo + 2 * bins * 2 * f * 2 * fo + bins * Bn * 2 * f;
+    const int64_t upd = 2 * bins * fo * 2 * Bn + 2 * bins * 2 * f * 2 * Bn + bins * fo * 2 * f;
+    return int64_t(sizeof(float)) * std::max(fwd, std::max(dgr, upd)) + 4096;
+}
+
+bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo) {
+    // N = 2 f' (fwd), 2 f (dgrad / upd) <= 256 and multiple of 16; reuse large enough to pay the prep
+    return Bn >= 256 && 2 * f <= 256 && 2 * fo <= 256 && (2 * f) % 16 == 0 && (2 * fo) % 16 == 0 && f % 4 == 0 &&
+           fo % 4 == 0;
+}
+
+namespace {
+float* carve_f(char*& cur, int64_t n) {
+    float* p = reinterpret_cast<float*>(cur);
+    cur += ((int64_t(sizeof(float)) * n + 1023) / 1024) * 1024;
+    return p;
+}
+}  // namespace
+
+// Y[n][o] = sum_i X[n][i] conj K[o][i]; X [n f + i][bins], K [o f + i][bins], Y [n fo + o][bins]
+void tc_cmac_fwd(cudaStream_t st, const float2* X, const float2* K, float2* Y, int64_t Bn, int64_t f, int64_t fo,
+                 int64_t bins, void* ws) {
+    char* cur = static_cast<char*>(ws);
+    const int kk = int(2 * f), nn = int(2 * fo);
+    float* Ah = carve_f(cur, bins * Bn * kk);
+    float* Al = carve_f(cur, bins * Bn * kk);
+    float* Bh = carve_f(cur, bins * nn * kk);
+    float* Bl = carve_f(cur, bins * nn * kk);
+    float* Dp = carve_f(cur, bins * Bn * nn);
+    prep<false, 1>(st, X, bins, int(Bn), int(f), 0, 0, Ah, Al);
+    prep<false, 2>(st, K, bins, int(fo), int(f), 0, 1 | 2, Bh, Bl);  // rows (o, re): (Kr, Ki); (o, im): (-Ki, Kr)
+    bgemm(st, Ah, Al, Bh, Bl, Dp, bins, int(Bn), nn, kk);
+    unprep(st, Dp, bins, int(Bn), int(fo), nn, Y);
+}
+
+// DX[n][i] = sum_o G[n][o] K[o][i]; G [n fo + o][bins], DX [n f + i][bins]
+void tc_cmac_dgrad(cudaStream_t st, const float2* G, const float2* K, float2* DX, int64_t Bn, int64_t f, int64_t fo,
+                   int64_t bins, void* ws) {
+    char* cur = static_cast<char*>(ws);
+    const int kk = int(2 * fo), nn = int(2 * f);
+    float* Ah = carve_f(cur, bins * Bn * kk);
+    float* Al = carve_f(cur, bins * Bn * kk);
+    float* Bh = carve_f(cur, bins * nn * kk);
+    float* Bl = carve_f(cur, bins * nn * kk);
+    float* Dp = carve_f(cur, bins * Bn * nn);
+    prep<false, 1>(st, G, bins, int(Bn), int(fo), 0, 0, Ah, Al);
+    // rows (i, re): (Kr, -Ki) over o; (i, im): (Ki, Kr); K images = o f + i: p = o, q = i
+    prep<true, 2>(st, K, bins, int(fo), int(f), 4, 1, Bh, Bl);
+    bgemm(st, Ah, Al, Bh, Bl, Dp, bins, int(Bn), nn, kk);
+    unprep(st, Dp, bins, int(Bn), int(f), nn, DX);
+}
+
+// dK[o][i] = sum_n X[n][i] conj G[n][o]; dK [o f + i][bins]
+void tc_cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, int64_t Bn, int64_t f, int64_t fo,
+                 int64_t bins, void* ws) {
+    char* cur = static_cast<char*>(ws);
+    const int kk = int(2 * Bn), nn = int(2 * f);
+    float* Ah = carve_f(cur, bins * fo * kk);
+    float* Al = carve_f(cur, bins * fo * kk);
+    float* Bh = carve_f(cur, bins * nn * kk);
+    float* Bl = carve_f(cur, bins * nn * kk);
+    float* Dp = carve_f(cur, bins * fo * nn);
+    prep<true, 1>(st, G, bins, int(Bn), int(fo), 0, 0, Ah, Al);     // rows o: (Gr, Gi) over n
+    prep<true, 2>(st, X, bins, int(Bn), int(f), 0, 1 | 4, Bh, Bl);  // rows (i, re): (Xr, Xi); (i, im): (Xi, -Xr)
+    bgemm(st, Ah, Al, Bh, Bl, Dp, bins, int(fo), nn, kk);
+    unprep(st, Dp, bins, int(fo), int(f), nn, DK);
+}
+
+}  // namespace znn_gpu

@@ -24,6 +24,7 @@
 #include <string>
 #include <type_traits>
 
+#include "bgemm_tc.hpp"
 #include "fft.hpp"
 
 namespace znn_fft {
@@ -1686,7 +1687,9 @@ struct plan {
     bool poly = false;
     conv_shape ce;
     int64_t S = 1;
-    std::shared_ptr<znn_gpu::scratch> phase_ws;  // phase-split input / output tensors
+    std::shared_ptr<znn_gpu::scratch> phase_ws;  // engine arena: phase-split tensors, then the tensor-core CMAC operands
+    int64_t ph_bytes = 0;    // phase-split tensors (explicit split path)
+    bool tc = false;         // frequency-domain sums on the tensor cores (bgemm_tc.cu)
     float2* X = nullptr;  // memo: image spectra of the layer input [B*f][bins]
     float2* K = nullptr;  // memo: kernel spectra [fo*f][bins] (own buffer; null when pooled)
     float* dil = nullptr; // dilated kernels [fo*f][e^3]
@@ -2057,11 +2060,32 @@ int64_t image_spectrum_bytes(const conv_shape& c0) {
 }
 
 // phase-split tensors of a polyphase plan: input side [B S f nr] and output side [B S f' mr]
-int64_t phase_bytes(const conv_shape& c0) {
+int64_t split_bytes(const conv_shape& c0) {
     if (!use_poly(c0)) return 0;
     const conv_shape c = effective(c0);
     const int64_t a = c.B * c.f_in * c.n.vol(), b = c.B * c.f_out * c.m.vol();
-    return int64_t(sizeof(float)) * (a + b) + 1024;
+    return ((int64_t(sizeof(float)) * (a + b) + 1024 + 4095) / 4096) * 4096;
+}
+
+// the CMACs run as per-bin tensor-core GEMMs when every kernel-spectrum bin
+// is reused by enough images (polyphase plans: B s^3); ZNN_FFT_TC=0 keeps the
+// register-tiled FMA kernels
+bool use_tc(const conv_shape& c0) {
+    const char* e = std::getenv("ZNN_FFT_TC");
+    if (e && std::string(e) == "0") return false;
+    const conv_shape c = effective(c0);
+    return znn_gpu::tc_cmac_supported(c.B, c.f_in, c.f_out);
+}
+
+// the engine arena of a plan: explicit phase split tensors + tensor-core CMAC operands
+int64_t phase_bytes(const conv_shape& c0) {
+    int64_t b = split_bytes(c0);
+    if (use_tc(c0)) {
+        const conv_shape c = effective(c0);
+        const dims3 P = pads_for(c);
+        b += znn_gpu::tc_cmac_bytes(c.B, c.f_in, c.f_out, P.x * P.y * (P.z / 2 + 1));
+    }
+    return b;
 }
 
 // the scratch-arena bytes conv_fwd / conv_bwd ask for (the larger of the two)
@@ -2091,6 +2115,10 @@ plan_ptr make_plan(const conv_shape& c0, std::shared_ptr<kpool> pool, std::share
         p->poly = true;
         p->ce = c;
         p->S = c0.s.x * c0.s.y * c0.s.z;
+    }
+    p->tc = use_tc(c0);
+    p->ph_bytes = split_bytes(c0);
+    if (p->poly || p->tc) {
         p->phase_ws = phase_ws ? std::move(phase_ws) : std::make_shared<znn_gpu::scratch>();
         p->phase_ws->get(size_t(phase_bytes(c0)));  // sized now: a step never grows it
     }
@@ -2164,6 +2192,11 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
 }  // namespace
 
 namespace {
+// tensor-core CMAC operands: the engine arena past the phase-split tensors
+void* tc_ws(plan& p) {
+    char* base = static_cast<char*>(p.phase_ws->get(p.phase_ws->capacity()));
+    return base + p.ph_bytes;
+}
 std::string lbl(const char* k, const conv_shape& c, const plan& p) {
     return std::string(k) + " f=" + std::to_string(c.f_in) + "->" + std::to_string(c.f_out) + " B=" +
            std::to_string(c.B) + " P=" + std::to_string(p.P.y) + " bins=" + std::to_string(p.bins);
@@ -2216,7 +2249,10 @@ static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     float2* CB = carve(cur, ccount);
     {
         znn_gpu::prof_scope ps(st, lbl("fft_cmac_fwd", c, p), cmac_bytes(c, p), cmac_flops(c, p));
-        cmac_ss(st, p.X, K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
+        if (p.tc)
+            znn_gpu::tc_cmac_fwd(st, p.X, K, Y, c.B, c.f_in, c.f_out, p.bins, tc_ws(p));
+        else
+            cmac_ss(st, p.X, K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
     }
     launch_check("fft_cmac_fwd");
     {
@@ -2296,7 +2332,10 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     if (gin) {
         {
             znn_gpu::prof_scope ps(st, lbl("fft_cmac_dgrad", c, p), cmac_bytes(c, p), cmac_flops(c, p));
-            cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
+            if (p.tc)
+                znn_gpu::tc_cmac_dgrad(st, G, K, DX, nB, c.f_in, c.f_out, p.bins, tc_ws(p));
+            else
+                cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
         }
         launch_check("fft_cmac_bwd");
         {
@@ -2308,7 +2347,10 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     // kernel gradient: one gradient-specific inverse per edge, sampled at s*w
     {
         znn_gpu::prof_scope ps(st, lbl("fft_cmac_upd", c, p), cmac_bytes(c, p), cmac_flops(c, p));
-        cmac_upd(st, p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
+        if (p.tc)
+            znn_gpu::tc_cmac_upd(st, p.X, G, DK, nB, c.f_in, c.f_out, p.bins, tc_ws(p));
+        else
+            cmac_upd(st, p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
     }
     launch_check("fft_cmac_upd");
     k_clobbered(p);
@@ -2416,7 +2458,7 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
         conv_fwd_core(st, p, e, x, w, bias, act, y, ws, &gi, &go);
         return;
     }
-    float* xp = static_cast<float*>(p.phase_ws->get(size_t(phase_bytes(c))));
+    float* xp = static_cast<float*>(p.phase_ws->get(size_t(p.ph_bytes)));
     float* yp = xp + ((e.B * e.f_in * e.n.vol() + 63) / 64) * 64;
     {
         znn_gpu::prof_scope ps(st, lbl("fft_phase_split", c, p), 8.0 * double(c.B * c.f_in * c.n.vol()), 0);
@@ -2439,7 +2481,7 @@ void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const
         conv_bwd_core(st, p, e, g, w, gw, gin, ws, relu_y, dbias, &gg, &gx);
         return;
     }
-    float* dxp = static_cast<float*>(p.phase_ws->get(size_t(phase_bytes(c))));
+    float* dxp = static_cast<float*>(p.phase_ws->get(size_t(p.ph_bytes)));
     float* gp = dxp + ((e.B * e.f_in * e.n.vol() + 63) / 64) * 64;
     {
         // the gradient's phases, gated by the fused ReLU (its bias gradient is

@@ -205,6 +205,26 @@ __device__ __forceinline__ void mma_commit_mc_w(uint32_t bar, uint16_t mask) {
         "h"(mask)
         : "memory");
 }
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, issued by one elected lane of a converged warp
+__device__ __forceinline__ void mma_tf32_w(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred pe, pa;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "setp.ne.b32 pa, %4, 0;\n\t"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, pa;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// one 2D TMA box into shared memory, issued by one elected lane of a converged
+// warp; completion counted on `bar` (armed separately with expect_tx)
+__device__ __forceinline__ void tma_w(uint32_t bar, uint32_t dst, const CUtensorMap* m, int c0, int c1) {
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "@pe cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
 // L2 prefetch of a TMA box (no shared memory, no barrier)
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(

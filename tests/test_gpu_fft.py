@@ -274,3 +274,37 @@ def test_fft_net_step_small_cube_and_split_paths(ctx, monkeypatch, cube):
     assert abs(loss - rl) / (abs(rl) + 1) < 1e-4
     assert O.max_rel_error(grads, rg) < 1e-3
     assert O.max_rel_error(newp, rp) < 1e-3
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+@pytest.mark.parametrize("shape", [(4, 16, 16, (20, 20, 20), (3, 3, 3), (4, 4, 4)),
+                                   (2, 24, 8, (17, 18, 16), (3, 2, 3), (2, 4, 4))], ids=str)
+def test_fft_tensor_core_cmacs(ctx, monkeypatch, shape, tc):
+    """The frequency-domain sums as per-bin tcgen05 GEMMs (polyphase plans
+    with B s^3 >= 256 phase images: here 256), forward, data gradient and
+    kernel gradient against the oracle; ZNN_FFT_TC=0 runs the same layer on
+    the register-tiled FMA kernels."""
+    from paper_1510_06706_b200 import FftPlan
+    monkeypatch.setenv("ZNN_FFT_TC", tc)
+    B, fi, fo, n, k, s = shape
+    m = tuple(n[a] - s[a] * (k[a] - 1) for a in range(3))
+    rng = np.random.default_rng(21)
+    x = rng.uniform(0, 1, size=(B, fi) + n).astype(np.float32)
+    w = rng.uniform(-0.2, 0.2, size=(fo, fi) + k).astype(np.float32)
+    g = rng.uniform(-1, 1, size=(B, fo) + m).astype(np.float32)
+    plan = FftPlan(ctx, B, fi, fo, n, k, s)
+    y = plan.forward(cuda(x), cuda(w), act="none").cpu().numpy()
+    dx, dw = plan.backward(cuda(g), cuda(w))
+    dx, dw = dx.cpu().numpy(), dw.cpu().numpy()
+    plan.close()
+    for b in range(B):
+        for o in range(0, fo, 3):
+            ref = sum(O.conv_valid(x[b, i], w[o, i], s) for i in range(fi))
+            assert O.max_rel_error(y[b, o], ref) < 1e-4, ("fwd", b, o)
+        for i in range(0, fi, 5):
+            ref = sum(O.conv_full(g[b, o], O.reflect(w[o, i]), s) for o in range(fo))
+            assert O.max_rel_error(dx[b, i], ref) < 1e-3, ("dgrad", b, i)
+    for o in range(0, fo, 3):
+        for i in range(0, fi, 5):
+            ref = sum(O.kernel_grad(x[b, i], g[b, o], k, s) for b in range(B))
+            assert O.max_rel_error(dw[o, i], ref) < 1e-3, ("wgrad", o, i)
