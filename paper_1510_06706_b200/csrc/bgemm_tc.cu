@@ -46,21 +46,21 @@ __device__ __forceinline__ float2 variant(float2 z, int code) {
     return r;
 }
 
-// S [img = p * F + q][bins] complex -> hi / lo [bin][row][k] fp32.
-// ROWQ = false: row = p (rows R = Pn), k = 2 q + c (K = 2 F)        (A of fwd / dgrad)
-// ROWQ = true : row = q or (q, c') (NV = 1 or 2 variants), k = 2 p + c (K = 2 Pn)
-// ROWQ = false with NV = 2: row = (p, c'), k = 2 q + c                 (B of fwd)
+// S [img = p * F + q][bins] complex -> T [bin][row][k] fp32, the bin-major
+// operand the GEMM's TMA reads (hi / lo and B's row variants are made in
+// shared memory by the GEMM). ROWQ = false: row = p (R = Pn), k = 2 q + c
+// (K = 2 F); ROWQ = true: row = q (R = F), k = 2 p + c (K = 2 Pn).
 // block: one row-side index, TB k-side indices x TB bins; threads 32 x 8
-template <bool ROWQ, int NV>
-__global__ void __launch_bounds__(256) prep_k(const float2* __restrict__ S, int64_t bins, int Pn, int F, int v0,
-                                              int v1, float* __restrict__ hi, float* __restrict__ lo) {
+template <bool ROWQ>
+__global__ void __launch_bounds__(256) prep_k(const float2* __restrict__ S, int64_t bins, int Pn, int F,
+                                              float* __restrict__ T) {
     __shared__ float2 tile[TB][TB + 1];
     const int rs = blockIdx.z;                // row-side index (p, or q when ROWQ)
     const int j0 = blockIdx.y * TB;           // k-side indices (q, or p when ROWQ)
     const int64_t w0 = int64_t(blockIdx.x) * TB;
     const int nk = ROWQ ? Pn : F;             // k-side extent
     const int K = 2 * nk;
-    const int R = (ROWQ ? F : Pn) * NV;       // rows per bin
+    const int R = ROWQ ? F : Pn;              // rows per bin
     const int tx = threadIdx.x, ty = threadIdx.y;
     for (int jj = ty; jj < TB; jj += 8) {
         const int j = j0 + jj;
@@ -73,27 +73,17 @@ __global__ void __launch_bounds__(256) prep_k(const float2* __restrict__ S, int6
         tile[jj][tx] = v;
     }
     __syncthreads();
-    // out row (bin, rs, c'): the k-side pairs j0..j0+TB as 2 TB consecutive floats
+    // out row (bin, rs): the k-side pairs j0..j0+TB as 2 TB consecutive floats
     for (int ww = ty; ww < TB; ww += 8) {
         const int64_t w = w0 + ww;
         if (w >= bins) continue;
+        float* o = T + (w * R + rs) * K + 2 * j0;
 #pragma unroll
-        for (int cv = 0; cv < NV; ++cv) {
-            const int code = cv == 0 ? v0 : v1;
-            const int64_t row = int64_t(rs) * NV + cv;
-            float* oh = hi + (w * R + row) * K + 2 * j0;
-            float* ol = lo + (w * R + row) * K + 2 * j0;
-            // lanes write floats tx and tx + 32 of the 64-float segment
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int e = tx + 32 * h, jj = e >> 1;
-                if (j0 + jj < nk) {
-                    const float2 z = variant(tile[jj][ww], code);
-                    const float x = (e & 1) ? z.y : z.x;
-                    const float xh = tf32_hi(x);
-                    oh[e] = x;
-                    ol[e] = x - xh;
-                }
+        for (int h = 0; h < 2; ++h) {
+            const int e = tx + 32 * h, jj = e >> 1;
+            if (j0 + jj < nk) {
+                const float2 z = tile[jj][ww];
+                o[e] = (e & 1) ? z.y : z.x;
             }
         }
     }
@@ -126,26 +116,46 @@ constexpr int STAGES = 2;
 
 struct bg_params {
     int M, N, K;          // per bin: D[M][N] = sum_k A[M][k] B[N][k]
+    int NB;               // raw B rows per bin loaded by TMA (N, or N / 2 with two variants per row)
+    int v0, v1;           // variant codes of B rows 2r, 2r + 1 (NB = N / 2)
     int ldd;              // D row pitch (floats)
     int mtiles;
 };
 
-// warps 0-3: epilogue (TMEM lane quarter = warp); warp 4: TMA; warp 5: TMEM alloc + MMA issue
+// the 16-byte chunk q of row r of a 128B-swizzled K-major tile
+__device__ __forceinline__ uint32_t sw_chunk(uint32_t r, uint32_t q) { return r * 128u + (((q ^ (r & 7u)) & 7u) << 4); }
+
+__device__ __forceinline__ float4 lo4(float4 v) {
+    return make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
+}
+__device__ __forceinline__ float4 var4(float4 v, int code) {  // two complex pairs
+    const float2 a = variant(make_float2(v.x, v.y), code), b = variant(make_float2(v.z, v.w), code);
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// warps 0-3: operand expansion during the K loop (lo = x - tf32(x) of A and
+// B, B's row variants), then the epilogue (TMEM lane quarter = warp);
+// warp 4: TMA; warp 5: TMEM alloc + MMA issue. Stage layout:
+// [A raw = A hi][A lo][B raw][B hi][B lo] (B hi = B raw when NB == N).
 __global__ void __launch_bounds__(192, 1)
-bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
-           const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
-           float* __restrict__ D, bg_params p) {
+bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, float* __restrict__ D,
+           bg_params p) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* base_ptr = smem_raw + (base - raw);
-    const uint32_t a_bytes = BM * 128u, b_bytes = uint32_t(p.N) * 128u;
-    const uint32_t stage_bytes = 2u * a_bytes + 2u * b_bytes;
+    const bool expand = p.NB != p.N;
+    const uint32_t a_bytes = BM * 128u, braw_bytes = uint32_t(p.NB) * 128u, b_bytes = uint32_t(p.N) * 128u;
+    const uint32_t off_alo = a_bytes, off_braw = 2u * a_bytes, off_bhi = off_braw + (expand ? braw_bytes : 0u);
+    const uint32_t off_blo = off_bhi + b_bytes;
+    const uint32_t stage_bytes = ((off_blo + b_bytes + 1023u) / 1024u) * 1024u;
+    const uint32_t tma_bytes = a_bytes + braw_bytes;
     const uint32_t bar_base = base + STAGES * stage_bytes;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
-    auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(STAGES + s); };
-    const uint32_t acc_bar = bar_base + 8u * uint32_t(2 * STAGES);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(2 * STAGES + 2));
+    auto conv_bar = [&](int s) { return bar_base + 8u * uint32_t(STAGES + s); };
+    auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(2 * STAGES + s); };
+    const uint32_t acc_bar = bar_base + 8u * uint32_t(3 * STAGES);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(3 * STAGES + 2));
 
     const int warp = threadIdx.x >> 5;
     const int mt = int(blockIdx.x % unsigned(p.mtiles));
@@ -156,6 +166,7 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CU
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar(s), 1);
+            mbar_init(conv_bar(s), 128);
             mbar_init(empty_bar(s), 1);
         }
         mbar_init(acc_bar, 1);
@@ -168,8 +179,8 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CU
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 4) {
-        // TMA producer: per chunk A hi|lo (128 rows) then B hi|lo (N rows)
-        const int arow = int(bin * p.M + m0), brow = int(bin * p.N);
+        // TMA producer: per chunk the raw A tile (128 rows) and raw B tile (NB rows)
+        const int arow = int(bin * p.M + m0), brow = int(bin * p.NB);
         int s = 0;
         uint32_t ph = 0;
         for (int c = 0; c < nchunks; ++c) {
@@ -179,12 +190,10 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CU
                 "{\n\t.reg .pred pe;\n\t"
                 "elect.sync _|pe, 0xffffffff;\n\t"
                 "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(full_bar(s)),
-                "r"(stage_bytes)
+                "r"(tma_bytes)
                 : "memory");
-            tma_w(full_bar(s), st0, &tA_hi, c * BKC, arow);
-            tma_w(full_bar(s), st0 + a_bytes, &tA_lo, c * BKC, arow);
-            tma_w(full_bar(s), st0 + 2u * a_bytes, &tB_hi, c * BKC, brow);
-            tma_w(full_bar(s), st0 + 2u * a_bytes + b_bytes, &tB_lo, c * BKC, brow);
+            tma_w(full_bar(s), st0, &tA, c * BKC, arow);
+            tma_w(full_bar(s), st0 + off_braw, &tB, c * BKC, brow);
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
     } else if (warp == 5) {
@@ -192,10 +201,10 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CU
         int s = 0;
         uint32_t ph = 0;
         for (int c = 0; c < nchunks; ++c) {
-            mbar_wait(full_bar(s), ph);
+            mbar_wait(conv_bar(s), ph);
             tc_fence_after();
-            const uint32_t a_hi = base + uint32_t(s) * stage_bytes, a_lo = a_hi + a_bytes;
-            const uint32_t b_hi = a_hi + 2u * a_bytes, b_lo = b_hi + b_bytes;
+            const uint32_t st0 = base + uint32_t(s) * stage_bytes;
+            const uint32_t a_hi = st0, a_lo = st0 + off_alo, b_hi = st0 + off_bhi, b_lo = st0 + off_blo;
             const int ksteps = min(BKC, p.K - c * BKC) / 8;
             for (int kk = 0; kk < ksteps; ++kk) {
                 const uint32_t ko = uint32_t(kk) * 32u;  // 8 fp32 along K
@@ -210,12 +219,46 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CU
             if (++s == STAGES) s = 0, ph ^= 1u;
         }
     } else {
-        // epilogue: lane = row of the tile
+        const int t = threadIdx.x;  // 0..127
+        // ---- operand expansion of every stage ----
+        {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(full_bar(s), ph);
+                uint8_t* st0 = base_ptr + size_t(s) * stage_bytes;
+                for (int i = t; i < BM * 8; i += 128) {  // A lo
+                    const uint32_t o = sw_chunk(uint32_t(i >> 3), uint32_t(i & 7));
+                    *reinterpret_cast<float4*>(st0 + off_alo + o) = lo4(*reinterpret_cast<const float4*>(st0 + o));
+                }
+                if (expand) {  // B rows 2r + c' = variant c' of raw row r, hi and lo
+                    for (int i = t; i < p.NB * 8; i += 128) {
+                        const uint32_t r = uint32_t(i >> 3), q = uint32_t(i & 7);
+                        const float4 v = *reinterpret_cast<const float4*>(st0 + off_braw + sw_chunk(r, q));
+                        const float4 h0 = var4(v, p.v0), h1 = var4(v, p.v1);
+                        const uint32_t o0 = sw_chunk(2u * r, q), o1 = sw_chunk(2u * r + 1u, q);
+                        *reinterpret_cast<float4*>(st0 + off_bhi + o0) = h0;
+                        *reinterpret_cast<float4*>(st0 + off_bhi + o1) = h1;
+                        *reinterpret_cast<float4*>(st0 + off_blo + o0) = lo4(h0);
+                        *reinterpret_cast<float4*>(st0 + off_blo + o1) = lo4(h1);
+                    }
+                } else {
+                    for (int i = t; i < p.N * 8; i += 128) {
+                        const uint32_t o = sw_chunk(uint32_t(i >> 3), uint32_t(i & 7));
+                        *reinterpret_cast<float4*>(st0 + off_blo + o) =
+                            lo4(*reinterpret_cast<const float4*>(st0 + off_braw + o));
+                    }
+                }
+                fence_proxy_async();  // generic-proxy writes -> visible to the tensor cores
+                mbar_arrive(conv_bar(s));
+                if (++s == STAGES) s = 0, ph ^= 1u;
+            }
+        }
+        // ---- epilogue: lane = row of the tile ----
         mbar_wait(acc_bar, 0);
         tc_fence_after();
-        const int r = threadIdx.x;  // 0..127
         const uint32_t lane_base = uint32_t(warp * 32) << 16;
-        const int row = m0 + r;
+        const int row = m0 + t;
         float* drow = D + (bin * p.M + row) * int64_t(p.ldd);
         for (int c0 = 0; c0 < p.N; c0 += 16) {
             float v[16];
@@ -237,12 +280,13 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CU
     }
 }
 
-template <bool ROWQ, int NV>
-void prep(cudaStream_t st, const float2* S, int64_t bins, int Pn, int F, int v0, int v1, float* hi, float* lo) {
+// S [img = p * F + q][bins] complex -> T [bin][row][k] fp32 (transpose only)
+template <bool ROWQ>
+void prep(cudaStream_t st, const float2* S, int64_t bins, int Pn, int F, float* T) {
     const int nk = ROWQ ? Pn : F, rsn = ROWQ ? F : Pn;
     require(rsn < 65536 && ceil_div(nk, TB) < 65536, "tc cmac: prep grid exceeds 65535");
     const dim3 grid(unsigned(ceil_div(bins, TB)), unsigned(ceil_div(nk, TB)), unsigned(rsn));
-    prep_k<ROWQ, NV><<<grid, dim3(32, 8, 1), 0, st>>>(S, bins, Pn, F, v0, v1, hi, lo);
+    prep_k<ROWQ><<<grid, dim3(32, 8, 1), 0, st>>>(S, bins, Pn, F, T);
     launch_check("tc_cmac_prep");
 }
 
@@ -253,35 +297,38 @@ void unprep(cudaStream_t st, const float* Dp, int64_t bins, int Pn, int Q, int l
     launch_check("tc_cmac_unprep");
 }
 
-void bgemm(cudaStream_t st, const float* Ahi, const float* Alo, const float* Bhi, const float* Blo, float* Dp,
-           int64_t nb, int M, int N, int K) {
-    require(N % 16 == 0 && N <= 256 && K % 8 == 0 && K % 4 == 0, "tc cmac: bad GEMM shape");
-    require(nb * M < (int64_t(1) << 31) && nb * N < (int64_t(1) << 31), "tc cmac: operand rows exceed 2^31");
-    const CUtensorMap ah = make_panel_map_rows(Ahi, K, nb * M, BM), al = make_panel_map_rows(Alo, K, nb * M, BM);
-    const CUtensorMap bh = make_panel_map_rows(Bhi, K, nb * N, N), bl = make_panel_map_rows(Blo, K, nb * N, N);
-    bg_params p{M, N, K, N, int(ceil_div(M, BM))};
-    const size_t smem = size_t(STAGES) * (2 * BM * 128 + 2 * size_t(N) * 128) + 1024 + 256;
+// D[bin][M][N] = A[bin][M][K] . B[bin][N][K]^T with B rows 2r + c' = variant
+// c' of the raw row r (raw B: [bin][N / 2][K])
+void bgemm(cudaStream_t st, const float* A, const float* B, float* Dp, int64_t nb, int M, int N, int K, int v0, int v1) {
+    require(N % 16 == 0 && N <= 256 && K % 8 == 0, "tc cmac: bad GEMM shape");
+    const int NB = N / 2;
+    require(nb * M < (int64_t(1) << 31) && nb * NB < (int64_t(1) << 31), "tc cmac: operand rows exceed 2^31");
+    const CUtensorMap ta = make_panel_map_rows(A, K, nb * M, BM), tb = make_panel_map_rows(B, K, nb * NB, NB);
+    bg_params p{M, N, K, NB, v0, v1, N, int(ceil_div(M, BM))};
+    const size_t stage = ((size_t(2 * BM * 128 + NB * 128 + 2 * N * 128) + 1023) / 1024) * 1024;
+    const size_t smem = size_t(STAGES) * stage + 1024 + 256;
+    require(smem <= 227 * 1024, "tc cmac: stage does not fit in shared memory");
     const int64_t ctas = nb * p.mtiles;
     require(ctas < (int64_t(1) << 31), "tc cmac: grid too large");
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(bgemm_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    bgemm_tc_k<<<unsigned(ctas), 192, smem, st>>>(ah, al, bh, bl, Dp, p);
+    bgemm_tc_k<<<unsigned(ctas), 192, smem, st>>>(ta, tb, Dp, p);
     launch_check("tc_cmac_gemm");
 }
 
 }  // namespace
 
 int64_t tc_cmac_bytes(int64_t Bn, int64_t f, int64_t fo, int64_t bins) {
-    // A hi|lo + B hi|lo + D for the largest of the three GEMMs
-    const int64_t fwd = 2 * bins * Bn * 2 * f + 2 * bins * 2 * fo * 2 * f + bins * Bn * 2 * fo;
-    const int64_t dgr = 2 * bins * Bn * 2 * fo + 2 * bins * 2 * f * 2 * fo + bins * Bn * 2 * f;
-    const int64_t upd = 2 * bins * fo * 2 * Bn + 2 * bins * 2 * f * 2 * Bn + bins * fo * 2 * f;
+    // bin-major A + raw B + D of the largest of the three GEMMs
+    const int64_t fwd = bins * Bn * 2 * f + bins * fo * 2 * f + bins * Bn * 2 * fo;
+    const int64_t dgr = bins * Bn * 2 * fo + bins * f * 2 * fo + bins * Bn * 2 * f;
+    const int64_t upd = bins * fo * 2 * Bn + bins * f * 2 * Bn + bins * fo * 2 * f;
     return int64_t(sizeof(float)) * std::max(fwd, std::max(dgr, upd)) + 4096;
 }
 
 bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo) {
-    // N = 2 f' (fwd), 2 f (dgrad / upd) <= 256 and multiple of 16; reuse large enough to pay the prep
-    return Bn >= 256 && 2 * f <= 256 && 2 * fo <= 256 && (2 * f) % 16 == 0 && (2 * fo) % 16 == 0 && f % 4 == 0 &&
-           fo % 4 == 0;
+    // N = 2 f' (fwd), 2 f (dgrad / upd) <= 256 and a multiple of 16; enough
+    // reuse per kernel-spectrum bin to pay the operand transposes
+    return Bn >= 128 && 2 * f <= 256 && 2 * fo <= 256 && (2 * f) % 16 == 0 && (2 * fo) % 16 == 0;
 }
 
 namespace {
@@ -297,14 +344,13 @@ void tc_cmac_fwd(cudaStream_t st, const float2* X, const float2* K, float2* Y, i
                  int64_t bins, void* ws) {
     char* cur = static_cast<char*>(ws);
     const int kk = int(2 * f), nn = int(2 * fo);
-    float* Ah = carve_f(cur, bins * Bn * kk);
-    float* Al = carve_f(cur, bins * Bn * kk);
-    float* Bh = carve_f(cur, bins * nn * kk);
-    float* Bl = carve_f(cur, bins * nn * kk);
+    float* A = carve_f(cur, bins * Bn * kk);
+    float* B = carve_f(cur, bins * fo * kk);
     float* Dp = carve_f(cur, bins * Bn * nn);
-    prep<false, 1>(st, X, bins, int(Bn), int(f), 0, 0, Ah, Al);
-    prep<false, 2>(st, K, bins, int(fo), int(f), 0, 1 | 2, Bh, Bl);  // rows (o, re): (Kr, Ki); (o, im): (-Ki, Kr)
-    bgemm(st, Ah, Al, Bh, Bl, Dp, bins, int(Bn), nn, kk);
+    prep<false>(st, X, bins, int(Bn), int(f), A);
+    prep<false>(st, K, bins, int(fo), int(f), B);
+    // rows (o, re): (Kr, Ki) over i; (o, im): (-Ki, Kr)
+    bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 0, 1 | 2);
     unprep(st, Dp, bins, int(Bn), int(fo), nn, Y);
 }
 
@@ -313,15 +359,13 @@ void tc_cmac_dgrad(cudaStream_t st, const float2* G, const float2* K, float2* DX
                    int64_t bins, void* ws) {
     char* cur = static_cast<char*>(ws);
     const int kk = int(2 * fo), nn = int(2 * f);
-    float* Ah = carve_f(cur, bins * Bn * kk);
-    float* Al = carve_f(cur, bins * Bn * kk);
-    float* Bh = carve_f(cur, bins * nn * kk);
-    float* Bl = carve_f(cur, bins * nn * kk);
+    float* A = carve_f(cur, bins * Bn * kk);
+    float* B = carve_f(cur, bins * f * kk);
     float* Dp = carve_f(cur, bins * Bn * nn);
-    prep<false, 1>(st, G, bins, int(Bn), int(fo), 0, 0, Ah, Al);
-    // rows (i, re): (Kr, -Ki) over o; (i, im): (Ki, Kr); K images = o f + i: p = o, q = i
-    prep<true, 2>(st, K, bins, int(fo), int(f), 4, 1, Bh, Bl);
-    bgemm(st, Ah, Al, Bh, Bl, Dp, bins, int(Bn), nn, kk);
+    prep<false>(st, G, bins, int(Bn), int(fo), A);
+    prep<true>(st, K, bins, int(fo), int(f), B);  // K images o f + i: rows i, k = (o, c)
+    // rows (i, re): (Kr, -Ki) over o; (i, im): (Ki, Kr)
+    bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 4, 1);
     unprep(st, Dp, bins, int(Bn), int(f), nn, DX);
 }
 
@@ -330,14 +374,13 @@ void tc_cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, 
                  int64_t bins, void* ws) {
     char* cur = static_cast<char*>(ws);
     const int kk = int(2 * Bn), nn = int(2 * f);
-    float* Ah = carve_f(cur, bins * fo * kk);
-    float* Al = carve_f(cur, bins * fo * kk);
-    float* Bh = carve_f(cur, bins * nn * kk);
-    float* Bl = carve_f(cur, bins * nn * kk);
+    float* A = carve_f(cur, bins * fo * kk);
+    float* B = carve_f(cur, bins * f * kk);
     float* Dp = carve_f(cur, bins * fo * nn);
-    prep<true, 1>(st, G, bins, int(Bn), int(fo), 0, 0, Ah, Al);     // rows o: (Gr, Gi) over n
-    prep<true, 2>(st, X, bins, int(Bn), int(f), 0, 1 | 4, Bh, Bl);  // rows (i, re): (Xr, Xi); (i, im): (Xi, -Xr)
-    bgemm(st, Ah, Al, Bh, Bl, Dp, bins, int(fo), nn, kk);
+    prep<true>(st, G, bins, int(Bn), int(fo), A);  // rows o: (Gr, Gi) over n
+    prep<true>(st, X, bins, int(Bn), int(f), B);   // rows i: (Xr, Xi) over n
+    // rows (i, re): (Xr, Xi); (i, im): (Xi, -Xr)
+    bgemm(st, A, B, Dp, bins, int(fo), nn, kk, 0, 1 | 4);
     unprep(st, Dp, bins, int(fo), int(f), nn, DK);
 }
 

@@ -10,11 +10,13 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 python - "$C" "$L" <<'PY'
 import csv, sys, collections
 C, L = sys.argv[1], sys.argv[2]
-rows = list(csv.reader(open(f"gpurun_out/launches_{C}{L}.csv")))
+lines = open(f"gpurun_out/launches_{C}{L}.csv").read().splitlines()
+rows = list(csv.reader(lines[[i for i, l in enumerate(lines) if l.startswith("\"ID\"")][0]:]))
 hdr = rows[0]
 ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
 agg = collections.OrderedDict()
-for r in rows[2:]:
+for r in rows[1:]:
+    if len(r) < len(hdr): continue
     k = r[ik][:60]
     d = agg.setdefault(k, collections.defaultdict(float))
     try:
