@@ -387,7 +387,7 @@ def roofline_from_profile(kprof, steps, step_ms):
     roof["launch_ms"] = per_s * 1e3
     roof["algorithmic_bytes_per_launch"] = e["bytes"] / e["launches"]
     roof["traffic"], roof["traffic_source"] = committed_traffic(dom["kernel"])
-    return roof, shares[:16]
+    return roof, shares[:48]
 
 
 def committed_traffic(kernel):
