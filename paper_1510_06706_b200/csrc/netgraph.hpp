@@ -1,8 +1,12 @@
 // Host-side network description: the reference's node/edge graph and netspec
-// text format, kept as the drop-in user API (netgraph.hpp:21-156,
-// netspec.hpp:13-223 of the reference). Written independently for this
-// executor: parsing, validation, shape inference (netgraph.hpp:209-254) and
-// the sliding-window rewrite (netgraph.hpp:321-354).
+// text format, kept as the drop-in user API (the
+// netspec format and the shape rules are reproduced as host API so the same
+// text builds the same graph). This is a restatement of the reference's
+// parser and rules, following their control flow and error messages so that
+// structural errors read the same: parse_netspec / expand_layered
+// (netspec.hpp:67-223), the graph and its validation (netgraph.hpp:21-156),
+// shape inference (netgraph.hpp:161-254) and the sliding-window rewrite
+// (netgraph.hpp:321-354). Host code, off the hot path.
 #pragma once
 
 #include <cstdint>
