@@ -18,9 +18,9 @@
 // transforms produce). prep_k transposes them bin-major ([bin][row][k]) and
 // splits fp32 into hi (the raw value: the MMA reads the top 19 bits) and
 // lo = x - tf32(x); unprep_k transposes D back. The GEMM kernel is a TMA ->
-// tcgen05 pipeline: per CTA one (bin, 128-row tile), K in 32-wide chunks
-// (SWIZZLE_128B K-major tiles, 2 stages), D (N <= 256 columns) in TMEM,
-// D += Ahi Bhi + Ahi Blo + Alo Bhi.
+// tcgen05 pipeline: persistent CTAs over (bin, 128-row) tiles, K in 32-wide
+// chunks (SWIZZLE_128B K-major tiles, 2 stages), D (N <= 256 columns) in a
+// double-buffered TMEM accumulator, D += Ahi Bhi + Ahi Blo + Alo Bhi.
 #include <cuda.h>
 
 #include <algorithm>
@@ -133,13 +133,20 @@ __device__ __forceinline__ float4 var4(float4 v, int code) {  // two complex pai
     return make_float4(a.x, a.y, b.x, b.y);
 }
 
-// warps 0-3: operand expansion during the K loop (lo = x - tf32(x) of A and
-// B, B's row variants), then the epilogue (TMEM lane quarter = warp);
-// warp 4: TMA; warp 5: TMEM alloc + MMA issue. Stage layout:
-// [A raw = A hi][A lo][B raw][B hi][B lo] (B hi = B raw when NB == N).
-__global__ void __launch_bounds__(192, 1)
+// Persistent: one CTA per SM walks the (bin, 128-row) tiles t = blockIdx.x,
+// blockIdx.x + gridDim.x, ...; the stage ring runs across tiles and the
+// accumulator is double-buffered in TMEM (2 x 256 columns), so the drain of
+// tile t overlaps the loads and MMAs of tile t + 1.
+// warps 0-3: operand expansion (lo = x - tf32(x) of A and B, B's two row
+//            variants) of every stage;
+// warps 4-7: epilogue (TMEM lane quarter = warp % 4): drain D rows to HBM;
+// warp 8   : TMA of the raw A (128 rows) and raw B (NB rows) tiles;
+// warp 9   : TMEM allocation and the MMA issue (Ahi.Bhi + Ahi.Blo + Alo.Bhi).
+// Stage layout: [A raw = A hi][A lo][B raw][B hi][B lo] (B hi = B raw when NB == N).
+constexpr int BG_THREADS = 320;
+__global__ void __launch_bounds__(BG_THREADS, 1)
 bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, float* __restrict__ D,
-           bg_params p) {
+           bg_params p, int64_t ntiles) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -154,13 +161,11 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUten
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
     auto conv_bar = [&](int s) { return bar_base + 8u * uint32_t(STAGES + s); };
     auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(2 * STAGES + s); };
-    const uint32_t acc_bar = bar_base + 8u * uint32_t(3 * STAGES);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(3 * STAGES + 2));
+    auto accf_bar = [&](int b) { return bar_base + 8u * uint32_t(3 * STAGES + b); };
+    auto acce_bar = [&](int b) { return bar_base + 8u * uint32_t(3 * STAGES + 2 + b); };
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(3 * STAGES + 4));
 
     const int warp = threadIdx.x >> 5;
-    const int mt = int(blockIdx.x % unsigned(p.mtiles));
-    const int64_t bin = blockIdx.x / unsigned(p.mtiles);
-    const int m0 = mt * BM;
     const int nchunks = (p.K + BKC - 1) / BKC;
 
     if (threadIdx.x == 0) {
@@ -169,70 +174,83 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUten
             mbar_init(conv_bar(s), 128);
             mbar_init(empty_bar(s), 1);
         }
-        mbar_init(acc_bar, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(accf_bar(b), 1);
+            mbar_init(acce_bar(b), 128);
+        }
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc(smem_u32(tmem_slot), 256);
+    if (warp == 9) tmem_alloc(smem_u32(tmem_slot), 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 4) {
-        // TMA producer: per chunk the raw A tile (128 rows) and raw B tile (NB rows)
-        const int arow = int(bin * p.M + m0), brow = int(bin * p.NB);
+    if (warp == 8) {
         int s = 0;
         uint32_t ph = 0;
-        for (int c = 0; c < nchunks; ++c) {
-            mbar_wait(empty_bar(s), ph ^ 1u);
-            const uint32_t st0 = base + uint32_t(s) * stage_bytes;
-            asm volatile(
-                "{\n\t.reg .pred pe;\n\t"
-                "elect.sync _|pe, 0xffffffff;\n\t"
-                "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(full_bar(s)),
-                "r"(tma_bytes)
-                : "memory");
-            tma_w(full_bar(s), st0, &tA, c * BKC, arow);
-            tma_w(full_bar(s), st0 + off_braw, &tB, c * BKC, brow);
-            if (++s == STAGES) s = 0, ph ^= 1u;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int64_t bin = t / p.mtiles;
+            const int m0 = int(t - bin * p.mtiles) * BM;
+            const int arow = int(bin * p.M + m0), brow = int(bin * p.NB);
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                const uint32_t st0 = base + uint32_t(s) * stage_bytes;
+                asm volatile(
+                    "{\n\t.reg .pred pe;\n\t"
+                    "elect.sync _|pe, 0xffffffff;\n\t"
+                    "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(full_bar(s)),
+                    "r"(tma_bytes)
+                    : "memory");
+                tma_w(full_bar(s), st0, &tA, c * BKC, arow);
+                tma_w(full_bar(s), st0 + off_braw, &tB, c * BKC, brow);
+                if (++s == STAGES) s = 0, ph ^= 1u;
+            }
         }
-    } else if (warp == 5) {
+    } else if (warp == 9) {
         const uint32_t idesc = idesc_tf32(BM, p.N);
         int s = 0;
         uint32_t ph = 0;
-        for (int c = 0; c < nchunks; ++c) {
-            mbar_wait(conv_bar(s), ph);
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int b = it & 1;
+            mbar_wait(acce_bar(b), uint32_t((it >> 1) & 1) ^ 1u);  // the epilogue drained this buffer
             tc_fence_after();
-            const uint32_t st0 = base + uint32_t(s) * stage_bytes;
-            const uint32_t a_hi = st0, a_lo = st0 + off_alo, b_hi = st0 + off_bhi, b_lo = st0 + off_blo;
-            const int ksteps = min(BKC, p.K - c * BKC) / 8;
-            for (int kk = 0; kk < ksteps; ++kk) {
-                const uint32_t ko = uint32_t(kk) * 32u;  // 8 fp32 along K
-                const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
-                const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
-                mma_tf32_w(tmem, ah, bh, idesc, (c == 0 && kk == 0) ? 0u : 1u);
-                mma_tf32_w(tmem, ah, bl, idesc, 1u);
-                mma_tf32_w(tmem, al, bh, idesc, 1u);
+            const uint32_t d = tmem + uint32_t(b) * 256u;
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(conv_bar(s), ph);
+                tc_fence_after();
+                const uint32_t st0 = base + uint32_t(s) * stage_bytes;
+                const uint32_t a_hi = st0, a_lo = st0 + off_alo, b_hi = st0 + off_bhi, b_lo = st0 + off_blo;
+                const int ksteps = min(BKC, p.K - c * BKC) / 8;
+                for (int kk = 0; kk < ksteps; ++kk) {
+                    const uint32_t ko = uint32_t(kk) * 32u;  // 8 fp32 along K
+                    const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
+                    const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
+                    mma_tf32_w(d, ah, bh, idesc, (c == 0 && kk == 0) ? 0u : 1u);
+                    mma_tf32_w(d, ah, bl, idesc, 1u);
+                    mma_tf32_w(d, al, bh, idesc, 1u);
+                }
+                mma_commit_w(empty_bar(s));
+                if (++s == STAGES) s = 0, ph ^= 1u;
             }
-            mma_commit_w(empty_bar(s));
-            if (c == nchunks - 1) mma_commit_w(acc_bar);
-            if (++s == STAGES) s = 0, ph ^= 1u;
+            mma_commit_w(accf_bar(b));
         }
-    } else {
-        const int t = threadIdx.x;  // 0..127
+    } else if (warp < 4) {
         // ---- operand expansion of every stage ----
-        {
-            int s = 0;
-            uint32_t ph = 0;
+        const int t0 = threadIdx.x;  // 0..127
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             for (int c = 0; c < nchunks; ++c) {
                 mbar_wait(full_bar(s), ph);
                 uint8_t* st0 = base_ptr + size_t(s) * stage_bytes;
-                for (int i = t; i < BM * 8; i += 128) {  // A lo
+                for (int i = t0; i < BM * 8; i += 128) {  // A lo
                     const uint32_t o = sw_chunk(uint32_t(i >> 3), uint32_t(i & 7));
                     *reinterpret_cast<float4*>(st0 + off_alo + o) = lo4(*reinterpret_cast<const float4*>(st0 + o));
                 }
                 if (expand) {  // B rows 2r + c' = variant c' of raw row r, hi and lo
-                    for (int i = t; i < p.NB * 8; i += 128) {
+                    for (int i = t0; i < p.NB * 8; i += 128) {
                         const uint32_t r = uint32_t(i >> 3), q = uint32_t(i & 7);
                         const float4 v = *reinterpret_cast<const float4*>(st0 + off_braw + sw_chunk(r, q));
                         const float4 h0 = var4(v, p.v0), h1 = var4(v, p.v1);
@@ -243,7 +261,7 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUten
                         *reinterpret_cast<float4*>(st0 + off_blo + o1) = lo4(h1);
                     }
                 } else {
-                    for (int i = t; i < p.N * 8; i += 128) {
+                    for (int i = t0; i < p.N * 8; i += 128) {
                         const uint32_t o = sw_chunk(uint32_t(i >> 3), uint32_t(i & 7));
                         *reinterpret_cast<float4*>(st0 + off_blo + o) =
                             lo4(*reinterpret_cast<const float4*>(st0 + off_braw + o));
@@ -254,29 +272,39 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUten
                 if (++s == STAGES) s = 0, ph ^= 1u;
             }
         }
-        // ---- epilogue: lane = row of the tile ----
-        mbar_wait(acc_bar, 0);
-        tc_fence_after();
-        const uint32_t lane_base = uint32_t(warp * 32) << 16;
-        const int row = m0 + t;
-        float* drow = D + (bin * p.M + row) * int64_t(p.ldd);
-        for (int c0 = 0; c0 < p.N; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem + lane_base + uint32_t(c0), v);
-            tmem_wait_ld();
-            if (row < p.M) {
+    } else {
+        // ---- epilogue: warps 4-7, lane = row of the tile ----
+        const int r = threadIdx.x - 128;  // 0..127
+        const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            const int b = it & 1;
+            const int64_t bin = t / p.mtiles;
+            const int row = int(t - bin * p.mtiles) * BM + r;
+            mbar_wait(accf_bar(b), uint32_t((it >> 1) & 1));
+            tc_fence_after();
+            float* drow = D + (bin * p.M + row) * int64_t(p.ldd);
+            const uint32_t acol = tmem + lane_base + uint32_t(b) * 256u;
+            for (int c0 = 0; c0 < p.N; c0 += 16) {
+                float v[16];
+                tmem_ld16(acol + uint32_t(c0), v);
+                tmem_wait_ld();
+                if (row < p.M) {
 #pragma unroll
-                for (int q = 0; q < 16; q += 4)
-                    *reinterpret_cast<float4*>(drow + c0 + q) = make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]);
+                    for (int q = 0; q < 16; q += 4)
+                        __stcs(reinterpret_cast<float4*>(drow + c0 + q), make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+                }
             }
+            tc_fence_before();
+            mbar_arrive(acce_bar(b));
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 5) {
+    if (warp == 9) {
         __syncwarp();
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 
@@ -308,10 +336,13 @@ void bgemm(cudaStream_t st, const float* A, const float* B, float* Dp, int64_t n
     const size_t stage = ((size_t(2 * BM * 128 + NB * 128 + 2 * N * 128) + 1023) / 1024) * 1024;
     const size_t smem = size_t(STAGES) * stage + 1024 + 256;
     require(smem <= 227 * 1024, "tc cmac: stage does not fit in shared memory");
-    const int64_t ctas = nb * p.mtiles;
-    require(ctas < (int64_t(1) << 31), "tc cmac: grid too large");
+    const int64_t ntiles = nb * p.mtiles;
+    int dev = 0, sms = 148;
+    ZNN_CUDA_CHECK(cudaGetDevice(&dev));
+    ZNN_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const unsigned grid = unsigned(std::min<int64_t>(ntiles, sms));  // persistent: one CTA per SM
     ZNN_CUDA_CHECK(cudaFuncSetAttribute(bgemm_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    bgemm_tc_k<<<unsigned(ctas), 192, smem, st>>>(ta, tb, Dp, p);
+    bgemm_tc_k<<<grid, BG_THREADS, smem, st>>>(ta, tb, Dp, p, ntiles);
     launch_check("tc_cmac_gemm");
 }
 
