@@ -1066,6 +1066,197 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
     }
 }
 
+// ---- small cubes, one line per thread (P <= 24): a thread holds a whole
+// P-point line in registers and transforms it with the register codelets
+// (dft_r, natural-order output), so a pass over Zh*P lines is one or two
+// iterations of the CTA with no exchange buffer and no warp sync; the cube
+// needs only the twiddle table beside it (more CTAs per SM) ----
+constexpr int REGP = 24;
+constexpr int RTHREADS = 256;
+
+template <int P>
+constexpr size_t cube_reg_smem() {
+    return sizeof(float2) * (size_t(P) + size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
+}
+
+template <int P>
+__global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __restrict__ spec) {
+    constexpr int Zh = P / 2 + 1, PYP = P + 1;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* cube = tw + P;  // [Zh][P][PYP]
+    fill_twiddles<P>(tw);
+    const int img = blockIdx.x;
+    phase_img pd{};
+    if (a.phased) pd = phase_decode(a.ph, img);
+    __syncthreads();
+    // z lines (R2C) of the valid (x, y) lines, read straight from HBM / L2
+    const int nl1 = a.nx * a.ny;
+    for (int ln = threadIdx.x; ln < nl1; ln += RTHREADS) {
+        const int x = ln / a.ny, y = ln - x * a.ny;
+        float2 v[P];
+        int64_t base;
+        int z0 = 0, zs = 1, zlim = a.nz;
+        if (a.phased) {
+            base = phase_line(a.ph, pd, x, y);
+            z0 = pd.rz, zs = a.ph.sz, zlim = base >= 0 ? a.ph.nz : 0;
+        } else {
+            base = int64_t(img) * a.img_stride + int64_t(ln) * a.nz;
+        }
+#pragma unroll
+        for (int z = 0; z < P; ++z) {
+            float val = 0.f;
+            const int zz = z0 + zs * z;
+            if (z < a.nz && zz < zlim) {
+                val = __ldg(a.src + base + zz);
+                if (a.gate && !(__ldg(a.gate + base + zz) > 0.f)) val = 0.f;
+            }
+            v[z] = make_float2(val, 0.f);
+        }
+        dft_r<P, P, false>(v, tw);
+#pragma unroll
+        for (int k = 0; k < Zh; ++k) cube[(k * P + x) * PYP + y] = v[k];
+    }
+    __syncthreads();
+    // y lines of the valid rows x < nx (columns y >= ny are the zero padding)
+    for (int ln = threadIdx.x; ln < Zh * a.nx; ln += RTHREADS) {
+        const int zb = ln / a.nx, x = ln - zb * a.nx;
+        float2* row = cube + (zb * P + x) * PYP;
+        float2 v[P];
+#pragma unroll
+        for (int y = 0; y < P; ++y) v[y] = y < a.ny ? row[y] : make_float2(0.f, 0.f);
+        dft_r<P, P, false>(v, tw);
+#pragma unroll
+        for (int k = 0; k < P; ++k) row[k] = v[k];
+    }
+    __syncthreads();
+    // x lines of every column (rows x >= nx are the zero padding)
+    for (int ln = threadIdx.x; ln < Zh * P; ln += RTHREADS) {
+        const int zb = ln / P, y = ln - zb * P;
+        float2* col = cube + zb * P * PYP + y;
+        float2 v[P];
+#pragma unroll
+        for (int x = 0; x < P; ++x) v[x] = x < a.nx ? col[x * PYP] : make_float2(0.f, 0.f);
+        dft_r<P, P, false>(v, tw);
+#pragma unroll
+        for (int k = 0; k < P; ++k) col[k * PYP] = v[k];
+    }
+    __syncthreads();
+    float4* g4 = reinterpret_cast<float4*>(spec + int64_t(img) * (Zh * P * P));
+    for (int idx = threadIdx.x; idx < Zh * P * P / 2; idx += RTHREADS) {
+        const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+        const float2 u = cube[(zb * P + x) * PYP + y], w = cube[(zb * P + x) * PYP + y + 1];
+        __stcs(g4 + idx, make_float4(u.x, u.y, w.x, w.y));
+    }
+}
+
+template <int P, bool UNIT>
+__global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restrict__ spec, cube_io a,
+                                                           const float* __restrict__ bias) {
+    constexpr int Zh = P / 2 + 1, PYP = P + 1;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* cube = tw + P;
+    fill_twiddles<P>(tw);
+    const int img = blockIdx.x;
+    const float4* g4 = reinterpret_cast<const float4*>(spec + int64_t(img) * (Zh * P * P));
+    constexpr int NV = Zh * P * P / 2;
+    for (int i0 = threadIdx.x; i0 < NV; i0 += 4 * RTHREADS) {
+        float4 u4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * RTHREADS < NV) u4[u] = __ldcs(g4 + i0 + u * RTHREADS);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = i0 + u * RTHREADS;
+            if (idx < NV) {
+                const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+                cube[(zb * P + x) * PYP + y] = make_float2(u4[u].x, u4[u].y);
+                cube[(zb * P + x) * PYP + y + 1] = make_float2(u4[u].z, u4[u].w);
+            }
+        }
+    }
+    phase_img pd{};
+    if (a.phased) pd = phase_decode(a.ph, img);
+    __syncthreads();
+    // x lines (columns), keep rows xs * i, i < xc
+    for (int ln = threadIdx.x; ln < Zh * P; ln += RTHREADS) {
+        const int zb = ln / P, y = ln - zb * P;
+        float2* col = cube + zb * P * PYP + y;
+        float2 v[P];
+#pragma unroll
+        for (int x = 0; x < P; ++x) v[x] = col[x * PYP];
+        dft_r<P, P, true>(v, tw);
+        if (UNIT) {
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+                if (i < a.xc) col[i * PYP] = v[i];
+        } else {
+            for (int i = 0; i < a.xc; ++i) col[i * PYP] = v[i * a.xs];  // dynamic index: local memory
+        }
+    }
+    __syncthreads();
+    // y lines of the kept rows, keep columns ys * j, j < yc
+    for (int ln = threadIdx.x; ln < Zh * a.xc; ln += RTHREADS) {
+        const int zb = ln / a.xc, i = ln - zb * a.xc;
+        float2* row = cube + (zb * P + i) * PYP;
+        float2 v[P];
+#pragma unroll
+        for (int y = 0; y < P; ++y) v[y] = row[y];
+        dft_r<P, P, true>(v, tw);
+        if (UNIT) {
+#pragma unroll
+            for (int j = 0; j < P; ++j)
+                if (j < a.yc) row[j] = v[j];
+        } else {
+            for (int j = 0; j < a.yc; ++j) row[j] = v[j * a.ys];
+        }
+    }
+    __syncthreads();
+    // z lines (C2R) of the kept (i, j), keep zs * q, q < zc; scale, bias, transfer
+    const float bv = bias ? bias[img % a.bias_mod] : 0.f;
+    for (int ln = threadIdx.x; ln < a.xc * a.yc; ln += RTHREADS) {
+        const int i = ln / a.yc, j = ln - i * a.yc;
+        float2 v[P];
+#pragma unroll
+        for (int z = 0; z < P; ++z) {
+            if (z < Zh) {
+                v[z] = cube[(z * P + i) * PYP + j];
+            } else {  // Hermitian symmetry of a real signal
+                const float2 c = cube[((P - z) * P + i) * PYP + j];
+                v[z] = make_float2(c.x, -c.y);
+            }
+        }
+        dft_r<P, P, true>(v, tw);
+        int64_t base;
+        int z0 = 0, zst = 1, zlim = 1 << 30;
+        if (a.phased) {
+            base = phase_line(a.ph, pd, i, j);
+            z0 = pd.rz, zst = a.ph.sz, zlim = a.ph.nz;
+        } else {
+            base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + j) * a.oz;
+        }
+        if (base < 0) continue;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            const int k = UNIT ? q : q * a.zs;
+            if (q < a.zc && k < P && z0 + zst * q < zlim) {
+                float r = v[UNIT ? q : 0].x;
+                if (!UNIT) {  // rare (dense-kernel dK inverse): pick v[k] without dynamic register indexing
+#pragma unroll
+                    for (int kk = 0; kk < P; ++kk)
+                        if (kk == k) r = v[kk].x;
+                }
+                r = r * a.scale + bv;
+                if (a.act == 2) r = r > 0.f ? r : 0.f;
+                else if (a.act == 0) r = 1.f / (1.f + expf(-r));
+                else if (a.act == 1) r = tanhf(r);
+                a.dst[base + z0 + zst * q] = r;
+            }
+        }
+    }
+}
+
 struct zinv_args {
     int xc, yc;                        // kept block per z-bin plane (compact input)
     int z_step, z_cnt;                 // kept z voxels (selection starts at 0)
@@ -1896,6 +2087,13 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
+            if constexpr (PP <= REGP) {
+                if (!std::getenv("ZNN_FFT_CUBE_LINES")) {
+                    allow_smem(fft3_fwd_reg_k<PP>, cube_reg_smem<PP>());
+                    fft3_fwd_reg_k<PP><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP>(), st>>>(a, spec);
+                    return;
+                }
+            }
             if constexpr (PP <= SMALLP) {
                 allow_smem(fft3_fwd_small_k<PP>, cube_fwd_smem<PP>());
                 fft3_fwd_small_k<PP><<<unsigned(imgs), THREADS, cube_fwd_smem<PP>(), st>>>(a, spec);
@@ -1973,6 +2171,19 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
+            if constexpr (PP <= REGP) {
+                if (!std::getenv("ZNN_FFT_CUBE_LINES")) {
+                    if (a.xs == 1 && a.ys == 1 && a.zs == 1) {
+                        allow_smem(fft3_inv_reg_k<PP, true>, cube_reg_smem<PP>());
+                        fft3_inv_reg_k<PP, true><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP>(), st>>>(spec, a, bias);
+                    } else {
+                        allow_smem(fft3_inv_reg_k<PP, false>, cube_reg_smem<PP>());
+                        fft3_inv_reg_k<PP, false><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP>(), st>>>(spec, a,
+                                                                                                         bias);
+                    }
+                    return;
+                }
+            }
             if constexpr (PP <= SMALLP) {
                 if (a.xs == 1 && a.ys == 1 && a.zs == 1) {
                     allow_smem(fft3_inv_small_k<PP, true>, cube_smem<PP>());

@@ -252,12 +252,14 @@ def test_fft_split_passes_without_small_cubes(ctx, monkeypatch, shape):
     test_fft_conv_fwd_matches_oracle(ctx, shape)
 
 
-@pytest.mark.parametrize("cube", ["1", "0", "split"])
+@pytest.mark.parametrize("cube", ["1", "lines", "0", "split"])
 def test_fft_net_step_small_cube_and_split_paths(ctx, monkeypatch, cube):
     """One scaled-c4 step (7^3 kernels, sparsities 2 and 4: polyphase layers at
     small pads) with and without the fused small-cube transforms matches the
     oracle (fwd 1e-4, gradients and updated weights 1e-3)."""
     from paper_1510_06706_b200 import configs as C
+    if cube == "lines":  # small cubes with 8-thread line transforms instead of one line per thread
+        monkeypatch.setenv("ZNN_FFT_CUBE_LINES", "1")
     if cube in ("0", "split"):
         monkeypatch.setenv("ZNN_FFT_NO_CUBE", "1")
     if cube == "split":  # explicit phase split / merge kernels instead of in-place phase addressing
