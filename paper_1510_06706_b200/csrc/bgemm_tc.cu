@@ -24,7 +24,6 @@
 #include <cuda.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "bgemm_tc.hpp"
 #include "tc_common.cuh"
@@ -121,11 +120,6 @@ struct bg_params {
     int v0, v1;           // variant codes of B rows 2r, 2r + 1 (NB = N / 2)
     int ldd;              // D row pitch (floats)
     int mtiles;
-    // direct epilogue (S != null): D row p, complex column q goes straight to
-    // the image-major spectrum S[(p * Q + q)][bins] (no transpose pass)
-    float2* S;
-    int Q;
-    int64_t bins;
 };
 
 // the 16-byte chunk q of row r of a 128B-swizzled K-major tile
@@ -290,25 +284,15 @@ bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUten
             mbar_wait(accf_bar(b), uint32_t((it >> 1) & 1));
             tc_fence_after();
             float* drow = D + (bin * p.M + row) * int64_t(p.ldd);
-            float2* srow = p.S ? p.S + int64_t(row) * p.Q * p.bins + bin : nullptr;
             const uint32_t acol = tmem + lane_base + uint32_t(b) * 256u;
             for (int c0 = 0; c0 < p.N; c0 += 16) {
                 float v[16];
                 tmem_ld16(acol + uint32_t(c0), v);
                 tmem_wait_ld();
                 if (row < p.M) {
-                    if (srow) {  // 8-byte stores; the tiles of neighbouring bins fill each sector in L2
 #pragma unroll
-                        for (int q = 0; q < 16; q += 2) {
-                            const int qq = (c0 + q) >> 1;
-                            if (qq < p.Q) srow[int64_t(qq) * p.bins] = make_float2(v[q], v[q + 1]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 16; q += 4)
-                            __stcs(reinterpret_cast<float4*>(drow + c0 + q),
-                                   make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
-                    }
+                    for (int q = 0; q < 16; q += 4)
+                        __stcs(reinterpret_cast<float4*>(drow + c0 + q), make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
                 }
             }
             tc_fence_before();
@@ -343,13 +327,12 @@ void unprep(cudaStream_t st, const float* Dp, int64_t bins, int Pn, int Q, int l
 
 // D[bin][M][N] = A[bin][M][K] . B[bin][N][K]^T with B rows 2r + c' = variant
 // c' of the raw row r (raw B: [bin][N / 2][K])
-void bgemm(cudaStream_t st, const float* A, const float* B, float* Dp, int64_t nb, int M, int N, int K, int v0, int v1,
-           float2* S = nullptr) {
+void bgemm(cudaStream_t st, const float* A, const float* B, float* Dp, int64_t nb, int M, int N, int K, int v0, int v1) {
     require(N % 16 == 0 && N <= 256 && K % 8 == 0, "tc cmac: bad GEMM shape");
     const int NB = N / 2;
     require(nb * M < (int64_t(1) << 31) && nb * NB < (int64_t(1) << 31), "tc cmac: operand rows exceed 2^31");
     const CUtensorMap ta = make_panel_map_rows(A, K, nb * M, BM), tb = make_panel_map_rows(B, K, nb * NB, NB);
-    bg_params p{M, N, K, NB, v0, v1, N, int(ceil_div(M, BM)), S, N / 2, nb};
+    bg_params p{M, N, K, NB, v0, v1, N, int(ceil_div(M, BM))};
     const size_t stage = ((size_t(2 * BM * 128 + NB * 128 + 2 * N * 128) + 1023) / 1024) * 1024;
     const size_t smem = size_t(STAGES) * stage + 1024 + 256;
     require(smem <= 227 * 1024, "tc cmac: stage does not fit in shared memory");
@@ -380,7 +363,6 @@ bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo) {
 }
 
 namespace {
-bool direct_out() { return !std::getenv("ZNN_TC_UNPREP"); }
 float* carve_f(char*& cur, int64_t n) {
     float* p = reinterpret_cast<float*>(cur);
     cur += ((int64_t(sizeof(float)) * n + 1023) / 1024) * 1024;
@@ -399,12 +381,8 @@ void tc_cmac_fwd(cudaStream_t st, const float2* X, const float2* K, float2* Y, i
     prep<false>(st, X, bins, int(Bn), int(f), A);
     prep<false>(st, K, bins, int(fo), int(f), B);
     // rows (o, re): (Kr, Ki) over i; (o, im): (-Ki, Kr)
-    if (direct_out()) {
-        bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 0, 1 | 2, Y);
-    } else {
-        bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 0, 1 | 2);
-        unprep(st, Dp, bins, int(Bn), int(fo), nn, Y);
-    }
+    bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 0, 1 | 2);
+    unprep(st, Dp, bins, int(Bn), int(fo), nn, Y);
 }
 
 // DX[n][i] = sum_o G[n][o] K[o][i]; G [n fo + o][bins], DX [n f + i][bins]
@@ -418,12 +396,8 @@ void tc_cmac_dgrad(cudaStream_t st, const float2* G, const float2* K, float2* DX
     prep<false>(st, G, bins, int(Bn), int(fo), A);
     prep<true>(st, K, bins, int(fo), int(f), B);  // K images o f + i: rows i, k = (o, c)
     // rows (i, re): (Kr, -Ki) over o; (i, im): (Ki, Kr)
-    if (direct_out()) {
-        bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 4, 1, DX);
-    } else {
-        bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 4, 1);
-        unprep(st, Dp, bins, int(Bn), int(f), nn, DX);
-    }
+    bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 4, 1);
+    unprep(st, Dp, bins, int(Bn), int(f), nn, DX);
 }
 
 // dK[o][i] = sum_n X[n][i] conj G[n][o]; dK [o f + i][bins]
@@ -437,12 +411,8 @@ void tc_cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, 
     prep<true>(st, G, bins, int(Bn), int(fo), A);  // rows o: (Gr, Gi) over n
     prep<true>(st, X, bins, int(Bn), int(f), B);   // rows i: (Xr, Xi) over n
     // rows (i, re): (Xr, Xi); (i, im): (Xi, -Xr)
-    if (direct_out()) {
-        bgemm(st, A, B, Dp, bins, int(fo), nn, kk, 0, 1 | 4, DK);
-    } else {
-        bgemm(st, A, B, Dp, bins, int(fo), nn, kk, 0, 1 | 4);
-        unprep(st, Dp, bins, int(fo), int(f), nn, DK);
-    }
+    bgemm(st, A, B, Dp, bins, int(fo), nn, kk, 0, 1 | 4);
+    unprep(st, Dp, bins, int(fo), int(f), nn, DK);
 }
 
 }  // namespace znn_gpu

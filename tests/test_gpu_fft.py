@@ -278,7 +278,7 @@ def test_fft_net_step_small_cube_and_split_paths(ctx, monkeypatch, cube):
     assert O.max_rel_error(newp, rp) < 1e-3
 
 
-@pytest.mark.parametrize("tc", ["1", "unprep", "0"])
+@pytest.mark.parametrize("tc", ["1", "0"])
 @pytest.mark.parametrize("shape", [(4, 16, 16, (20, 20, 20), (3, 3, 3), (4, 4, 4)),
                                    (2, 24, 8, (17, 18, 16), (3, 2, 3), (2, 4, 4))], ids=str)
 def test_fft_tensor_core_cmacs(ctx, monkeypatch, shape, tc):
@@ -287,9 +287,7 @@ def test_fft_tensor_core_cmacs(ctx, monkeypatch, shape, tc):
     kernel gradient against the oracle; ZNN_FFT_TC=0 runs the same layer on
     the register-tiled FMA kernels."""
     from paper_1510_06706_b200 import FftPlan
-    monkeypatch.setenv("ZNN_FFT_TC", "0" if tc == "0" else "1")
-    if tc == "unprep":  # the GEMM's product through a bin-major buffer + transpose instead of direct stores
-        monkeypatch.setenv("ZNN_TC_UNPREP", "1")
+    monkeypatch.setenv("ZNN_FFT_TC", tc)
     B, fi, fo, n, k, s = shape
     m = tuple(n[a] - s[a] * (k[a] - 1) for a in range(3))
     rng = np.random.default_rng(21)
