@@ -296,7 +296,7 @@ template <int P>
 __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__ in, int64_t in_img_stride, int nx,
                                                         int ny, int nz, int64_t nlines, float2* __restrict__ spec,
                                                         int Px, int Py, const float* __restrict__ gate,
-                                                        phase_geom ph, int phased, int img0) {
+                                                        phase_geom ph, int phased) {
     constexpr int Zh = P / 2 + 1;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
@@ -320,8 +320,8 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
         // the original tensor, valid below zlim; dense: contiguous)
         int64_t off = int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
         int z0 = 0, zs = 1, zlim = nz;
-        if (phased) {  // img0: first image of this launch (chunked transforms)
-            const phase_img pd = phase_decode(ph, int(im) + img0);
+        if (phased) {
+            const phase_img pd = phase_decode(ph, int(im));
             off = phase_line(ph, pd, x, y);
             z0 = pd.rz, zs = ph.sz, zlim = off >= 0 ? ph.nz : 0;
         }
@@ -1268,7 +1268,6 @@ struct zinv_args {
     int bias_mod;                      // bias index = img % bias_mod
     int phased;                        // outputs are the phases of an original tensor (ph)
     phase_geom ph;
-    int img0;                          // first image of this launch (chunked transforms)
 };
 
 // ---- z pass, inverse (C2R) of the compact kept lines, crop / tap selection
@@ -1296,14 +1295,14 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
         const int xi = r / g.yc, yi = r - (r / g.yc) * g.yc;
         ibase[l] = int64_t(im) * Zh * per + r;
         if (g.phased) {  // write the phase's voxels of the original tensor in place
-            const phase_img pd = phase_decode(g.ph, int(im) + g.img0);
+            const phase_img pd = phase_decode(g.ph, int(im));
             obase[l] = phase_line(g.ph, pd, xi, yi);
             ozoff[l] = pd.rz;
         } else {
             obase[l] = int64_t(im) * g.out_img_stride + (int64_t(xi) * g.oy + yi) * g.oz;
             ozoff[l] = 0;
         }
-        bvals[l] = bias ? bias[(im + uint32_t(g.img0)) % uint32_t(g.bias_mod)] : 0.f;
+        bvals[l] = bias ? bias[im % uint32_t(g.bias_mod)] : 0.f;
     }
     __syncthreads();
     // coalesced gather: a warp reads one z-bin of 32 consecutive lines; all of
@@ -2070,26 +2069,6 @@ __global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec
 
 // gate: optional ReLU output gating the input (fused transfer backward);
 // dbias (with gate): receives the per-map sum over the batch (imgs = B * dmaps)
-void z_fwd_launch(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
-                  float2* spec, const float* gate, const phase_geom* ph, int img0);
-void xy_fwd_launch(cudaStream_t st, const plan& p, float2* spec, int64_t planes, dims3 n);
-
-// images per launch of the two-pass (z, xy) transforms: a chunk's
-// intermediate (Zh P^2 complex per image) should stay L2-resident
-// (ZNN_FFT_CHUNK = images per chunk, 0 = one launch for all)
-int64_t fft_chunk(const plan& p, int64_t imgs, bool z_only) {
-    if (z_only || p.P.x == 1) return imgs;
-    int64_t ch = 0;
-    const int64_t per = p.Zh * p.P.x * p.P.y * int64_t(sizeof(float2));
-    if (const char* e = std::getenv("ZNN_FFT_CHUNK")) {
-        ch = std::atoll(e);
-    } else {
-        ch = (int64_t(48) << 20) / per;  // ~48 MB of intermediate per chunk
-    }
-    if (ch <= 0) return imgs;
-    return std::max<int64_t>(ch, 1);
-}
-
 bool small_cube(const plan& p) {
     return p.P.x == p.P.y && p.P.y == p.P.z && p.P.x > 1 && p.P.x <= SMALLP && !std::getenv("ZNN_FFT_NO_CUBE");
 }
@@ -2129,37 +2108,6 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         return;
     }
     require(ph == nullptr || !z_only, "fft: phase addressing with a z-only pass");
-    const int64_t ch = fft_chunk(p, imgs, z_only);
-    if (ch < imgs) {
-        // chunks of images whose z-pass output (the xy pass's input) stays in
-        // L2 between the two passes: the spectrum crosses HBM once, not three times
-        const int64_t istride = p.Zh * p.P.x * p.P.y;
-        for (int64_t i0 = 0; i0 < imgs; i0 += ch) {
-            const int64_t cnt = std::min(ch, imgs - i0);
-            const float* cin = ph ? in : in + i0 * in_img_stride;
-            const float* cg = (gate && !ph) ? gate + i0 * in_img_stride : gate;
-            z_fwd_launch(st, p, cin, in_img_stride, n, cnt, spec + i0 * istride, cg, ph, int(i0));
-            xy_fwd_launch(st, p, spec + i0 * istride, cnt * p.Zh, n);
-        }
-        if (dbias) {  // the DC bin of each image's spectrum is its voxel sum
-            dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), istride, 1, 1,
-                                                       int(p.P.y), dbias);
-            launch_check("fft_dc_bias");
-        }
-        return;
-    }
-    z_fwd_launch(st, p, in, in_img_stride, n, imgs, spec, gate, ph, 0);
-    if (dbias) {
-        dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y,
-                                                   int(n.x), int(n.y), int(p.P.y), dbias);
-        launch_check("fft_dc_bias");
-    }
-    if (z_only) return;
-    xy_fwd_launch(st, p, spec, imgs * p.Zh, n);
-}
-
-void z_fwd_launch(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
-                  float2* spec, const float* gate, const phase_geom* ph, int img0) {
     const int64_t nlines = imgs * n.x * n.y;
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
@@ -2167,12 +2115,16 @@ void z_fwd_launch(cudaStream_t st, const plan& p, const float* in, int64_t in_im
         allow_smem(fft_z_fwd_k<PP>, smem_for(PP));
         fft_z_fwd_k<PP><<<unsigned(ceil_div(nlines, LINES)), THREADS, smem_for(PP), st>>>(
             in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate,
-            ph ? *ph : phase_geom{}, ph ? 1 : 0, img0);
+            ph ? *ph : phase_geom{}, ph ? 1 : 0);
     });
     launch_check("fft_z_fwd");
-}
-
-void xy_fwd_launch(cudaStream_t st, const plan& p, float2* spec, int64_t planes, dims3 n) {
+    if (dbias) {
+        dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y,
+                                                   int(n.x), int(n.y), int(p.P.y), dbias);
+        launch_check("fft_dc_bias");
+    }
+    if (z_only) return;
+    const int64_t planes = imgs * p.Zh;
     dispatch_pad(int(p.P.y), [&](auto pc) {
         constexpr int PY = decltype(pc)::value;
         if (p.P.x == 1) {
@@ -2195,10 +2147,7 @@ void xy_fwd_launch(cudaStream_t st, const plan& p, float2* spec, int64_t planes,
 }
 
 void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 cnt, float* out, int64_t out_img_stride,
-               const float* bias, int bias_mod, int act, const float2* cbuf, const phase_geom* ph = nullptr,
-               int img0 = 0);
-void xy_inv_launch(cudaStream_t st, const plan& p, const float2* spec, int64_t planes, dims3 step, dims3 cnt,
-                   float2* cbuf);
+               const float* bias, int bias_mod, int act, const float2* cbuf, const phase_geom* ph = nullptr);
 
 // inverse 3D C2R keeping voxels (x,y,z) = (step*i) for i < cnt per axis,
 // written as a dense box [imgs][cnt.x][cnt.y][cnt.z] (image stride given);
@@ -2249,24 +2198,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         return;
     }
 
-    const int64_t ch = fft_chunk(p, imgs, false);
-    if (ch < imgs) {
-        // chunks whose compact planes (the z pass's input) stay in L2
-        const int64_t istride = p.Zh * p.P.x * p.P.y;
-        for (int64_t i0 = 0; i0 < imgs; i0 += ch) {
-            const int64_t n = std::min(ch, imgs - i0);
-            xy_inv_launch(st, p, spec + i0 * istride, n * p.Zh, step, cnt, cbuf);
-            inverse_z(st, p, n, step, cnt, ph ? out : out + i0 * out_img_stride, out_img_stride, bias, bias_mod, act,
-                      cbuf, ph, int(i0));
-        }
-        return;
-    }
-    xy_inv_launch(st, p, spec, imgs * p.Zh, step, cnt, cbuf);
-    inverse_z(st, p, imgs, step, cnt, out, out_img_stride, bias, bias_mod, act, cbuf, ph);
-}
-
-void xy_inv_launch(cudaStream_t st, const plan& p, const float2* spec, int64_t planes, dims3 step, dims3 cnt,
-                   float2* cbuf) {
+    const int64_t planes = imgs * p.Zh;
     dispatch_pad(int(p.P.y), [&](auto pc) {
         constexpr int PY = decltype(pc)::value;
         if (p.P.x == 1) {
@@ -2285,13 +2217,13 @@ void xy_inv_launch(cudaStream_t st, const plan& p, const float2* spec, int64_t p
         }
     });
     launch_check("fft_xy_inv");
+    inverse_z(st, p, imgs, step, cnt, out, out_img_stride, bias, bias_mod, act, cbuf, ph);
 }
 
 // z pass of an inverse: C2R of the compact kept planes in cbuf
 void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 cnt, float* out, int64_t out_img_stride,
-               const float* bias, int bias_mod, int act, const float2* cbuf, const phase_geom* ph, int img0) {
+               const float* bias, int bias_mod, int act, const float2* cbuf, const phase_geom* ph) {
     zinv_args g;
-    g.img0 = img0;
     g.phased = ph ? 1 : 0;
     g.ph = ph ? *ph : phase_geom{};
     g.xc = int(cnt.x), g.yc = int(cnt.y);

@@ -310,38 +310,3 @@ def test_fft_tensor_core_cmacs(ctx, monkeypatch, shape, tc):
         for i in range(0, fi, 5):
             ref = sum(O.kernel_grad(x[b, i], g[b, o], k, s) for b in range(B))
             assert O.max_rel_error(dw[o, i], ref) < 1e-3, ("wgrad", o, i)
-
-
-@pytest.mark.parametrize("chunk", ["5", "0"])
-@pytest.mark.parametrize("shape", [(2, 3, 4, (40, 38, 36), (3, 3, 3), (1, 1, 1)),
-                                   (2, 3, 2, (80, 79, 78), (3, 3, 3), (2, 2, 2))], ids=str)
-def test_fft_chunked_two_pass_transforms(ctx, monkeypatch, shape, chunk):
-    """Pads above 32 run the z + xy passes in chunks of images (the
-    intermediate stays in L2); ragged chunks (5 images of 6 / 48) and the
-    unchunked launch match the oracle, forward, data and kernel gradients."""
-    from paper_1510_06706_b200 import FftPlan
-    monkeypatch.setenv("ZNN_FFT_CHUNK", chunk)
-    B, fi, fo, n, k, s = shape
-    m = tuple(n[a] - s[a] * (k[a] - 1) for a in range(3))
-    rng = np.random.default_rng(4)
-    x = rng.uniform(0, 1, size=(B, fi) + n).astype(np.float32)
-    w = rng.uniform(-0.3, 0.3, size=(fo, fi) + k).astype(np.float32)
-    bias = rng.uniform(-0.1, 0.1, size=fo).astype(np.float32)
-    g = rng.uniform(-1, 1, size=(B, fo) + m).astype(np.float32)
-    plan = FftPlan(ctx, B, fi, fo, n, k, s)
-    assert min(plan.info()["pads"]) > 32
-    y = plan.forward(cuda(x), cuda(w), bias=cuda(bias), act="tanh").cpu().numpy()
-    dx, dw = plan.backward(cuda(g), cuda(w))
-    dx, dw = dx.cpu().numpy(), dw.cpu().numpy()
-    plan.close()
-    for b in range(B):
-        for o in range(fo):
-            ref = np.tanh(sum(O.conv_valid(x[b, i], w[o, i], s) for i in range(fi)) + bias[o])
-            assert O.max_rel_error(y[b, o], ref) < 1e-4
-        for i in range(fi):
-            ref = sum(O.conv_full(g[b, o], O.reflect(w[o, i]), s) for o in range(fo))
-            assert O.max_rel_error(dx[b, i], ref) < 1e-3
-    for o in range(fo):
-        for i in range(fi):
-            ref = sum(O.kernel_grad(x[b, i], g[b, o], k, s) for b in range(B))
-            assert O.max_rel_error(dw[o, i], ref) < 1e-3
