@@ -290,6 +290,21 @@ __device__ __forceinline__ int64_t phase_line(const phase_geom& G, const phase_i
     return d.base + (int64_t(x) * G.ny + y) * G.nz;
 }
 
+// Line order of the z passes over phase images: the sz z-phases of one
+// original z-line are adjacent lines (line = ((g * pl) + xy) * sz + rz with
+// g = (b, rx, ry, map)), so the thread groups of a warp read / write the
+// interleaved voxels of the same original line together: whole sectors
+// instead of every sz-th float from a different CTA. Returns the phase image.
+__device__ __forceinline__ uint32_t phase_pair_line(const phase_geom& G, uint32_t line, uint32_t pl, uint32_t* xy) {
+    const uint32_t sz = uint32_t(G.sz);
+    const uint32_t rz = line % sz, l2 = line / sz;
+    const uint32_t g = l2 / pl;
+    *xy = l2 - g * pl;
+    const uint32_t f = uint32_t(G.f), sxy = uint32_t(G.sx * G.sy);
+    const uint32_t i = g % f, t = g / f, rxy = t % sxy, b = t / sxy;
+    return ((b * sxy + rxy) * sz + rz) * f + i;
+}
+
 // ---- z pass, forward (R2C): lines (img, x < nx, y < ny) of the real input,
 // half spectra stored transposed: spec[img][zb][x][y] ----
 template <int P>
@@ -313,8 +328,14 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
     for (int n2 = 0; n2 < R2; ++n2) v[n2] = make_float2(0.f, 0.f);
     if (ok) {  // 32-bit decode (nlines < 2^32, checked on the host)
         const uint32_t pl = uint32_t(nx) * uint32_t(ny);
-        const uint32_t im = uint32_t(line) / pl;
-        const int r = int(uint32_t(line) - im * pl);
+        uint32_t im, rr;
+        if (phased) {
+            im = phase_pair_line(ph, uint32_t(line), pl, &rr);
+        } else {
+            im = uint32_t(line) / pl;
+            rr = uint32_t(line) - im * pl;
+        }
+        const int r = int(rr);
         const int x = r / ny, y = r - (r / ny) * ny;
         // element j of the line: off + z0 + zs * j (phased: the phase's voxels of
         // the original tensor, valid below zlim; dense: contiguous)
@@ -1290,8 +1311,14 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
     const bool ok = line < g.nlines;
     if (ok && t == 0) {  // 32-bit decode (nlines < 2^32, checked on the host)
         const uint32_t per = uint32_t(g.xc) * uint32_t(g.yc);
-        const uint32_t im = uint32_t(line) / per;
-        const int r = int(uint32_t(line) - im * per);
+        uint32_t im, rr;
+        if (g.phased) {
+            im = phase_pair_line(g.ph, uint32_t(line), per, &rr);
+        } else {
+            im = uint32_t(line) / per;
+            rr = uint32_t(line) - im * per;
+        }
+        const int r = int(rr);
         const int xi = r / g.yc, yi = r - (r / g.yc) * g.yc;
         ibase[l] = int64_t(im) * Zh * per + r;
         if (g.phased) {  // write the phase's voxels of the original tensor in place
