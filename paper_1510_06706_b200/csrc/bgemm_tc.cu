@@ -3,24 +3,29 @@
 // per-bin complex GEMMs on the tcgen05 tensor cores, 3xTF32.
 //
 // For the polyphase plans of dilated layers every kernel-spectrum bin feeds
-// B s^3 phase images (c5 conv3-5: 1024), so per bin the three sums are
-// real GEMMs with a large reuse dimension:
-//   fwd  : Y[n][o]  = sum_i X[n][i] conj K[o][i]   D[n][(o,c')]  = A(X)  . B(K)
-//   dgrad: DX[n][i] = sum_o G[n][o] K[o][i]         D[n][(i,c')]  = A(G)  . B(K^T)
-//   upd  : dK[o][i] = sum_n X[n][i] conj G[n][o]    D[o][(i,c')]  = A(G^T). B(X^T)
-// with complex numbers embedded as (re, im) pairs along K and the output
-// columns (o, c') interleaved, so D rows are the natural complex layout. A
-// rows are the natural complex rows of the left operand; B rows come in two
-// variants per column ((re, im) and a swapped / negated copy), e.g. for fwd
-// Yr = sum (Xr Kr + Xi Ki) = A . (Kr, Ki), Yi = sum (Xi Kr - Xr Ki) = A . (-Ki, Kr).
+// B s^3 phase images (c5: 128 at conv2, 1024 at conv3-5), so per bin the
+// three sums are real GEMMs with a large reuse dimension:
+//   fwd  : Y[n][o]  = sum_i X[n][i] conj K[o][i]
+//   dgrad: DX[n][i] = sum_o G[n][o] K[o][i]
+//   upd  : dK[o][i] = sum_n X[n][i] conj G[n][o]
+// Complex numbers are (re, im) pairs along K. The B operand is always the raw
+// right-hand spectrum (rows = output columns, K = (index, re / im)); the real
+// and imaginary outputs are two accumulators D_r = A . B, D_i = A' . B whose
+// left operands are per-element variants of the left spectrum, e.g. fwd:
+// Yr = sum Xr Kr + Xi Ki -> A = (Xr, Xi), Yi = sum Xi Kr - Xr Ki -> A' = (Xi, -Xr).
 //
-// Spectra live image-major ([img][bins], bins contiguous: what the
-// transforms produce). prep_k transposes them bin-major ([bin][row][k]) and
-// splits fp32 into hi (the raw value: the MMA reads the top 19 bits) and
-// lo = x - tf32(x); unprep_k transposes D back. The GEMM kernel is a TMA ->
-// tcgen05 pipeline: persistent CTAs over (bin, 128-row) tiles, K in 32-wide
-// chunks (SWIZZLE_128B K-major tiles, 2 stages), D (N <= 256 columns) in a
-// double-buffered TMEM accumulator, D += Ahi Bhi + Ahi Blo + Alo Bhi.
+// Operands come straight from the group-layout spectra (bgemm_tc.hpp) by 4-D
+// TMA boxes (a 128-row x 16-complex tile, or a 16-row x all-columns tile for
+// the operands that are transposed within the bin). Kernel layout:
+//   * A (and A') hi / lo live in TMEM (tcgen05.mma A-from-TMEM form), written
+//     by 8 expansion warps from the raw tile: no A copies in shared memory;
+//   * B hi / lo are written by the same warps in the canonical 128B-swizzled
+//     K-major layout (transposing where the box is K-outer);
+//   * one MMA warp issues D_r += Ahi Bhi + Ahi Blo + Alo Bhi and the same for
+//     D_i (M = 128 rows, N <= 128), 3 smem stages, 2 TMEM A buffers;
+//   * 4 epilogue warps drain D (D_r / D_i interleaved into complex) through a
+//     shared staging tile and TMA tensor stores into the group-layout output.
+// Persistent CTAs walk the (bin, 128-row tile) list.
 #include <cuda.h>
 
 #include <algorithm>
@@ -30,13 +35,33 @@
 
 namespace znn_gpu {
 
-CUtensorMap make_panel_map_rows(const float* ptr, int64_t cols, int64_t rows, int box_rows);
+void* tensor_map_encoder();  // conv_tc.cu
 
 namespace {
 
 using namespace znn_tc;
 
-constexpr int TB = 32;  // transpose tile (images or k-side indices) x bins
+typedef CUresult (*encode_fn_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 4-D view of a group-layout spectrum with R row-side images x F maps:
+// (2 kGrp floats of a group-bin, bin, group = map / kGrp, row); box (2 kGrp, 1, bq, br)
+CUtensorMap grp_map(const float2* ptr, int64_t bins, int64_t F, int64_t R, int bq, int br) {
+    CUtensorMap m;
+    const int64_t fq = F / kGrp;
+    constexpr int64_t gb = 8 * kGrp;  // bytes of a group-bin
+    const cuuint64_t dims[4] = {2 * kGrp, cuuint64_t(bins), cuuint64_t(fq), cuuint64_t(R)};
+    const cuuint64_t strides[3] = {gb, cuuint64_t(bins) * gb, cuuint64_t(fq * bins) * gb};
+    const cuuint32_t box[4] = {2 * kGrp, 1, cuuint32_t(bq), cuuint32_t(br)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    auto enc = reinterpret_cast<encode_fn_t>(tensor_map_encoder());
+    CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float2*>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled (group spectrum) failed: " + std::to_string(int(r)));
+    return m;
+}
 
 // variant code: bit0 swap (re, im) -> (im, re), bit1 negate the first, bit2 the second
 __device__ __forceinline__ float2 variant(float2 z, int code) {
@@ -45,374 +70,400 @@ __device__ __forceinline__ float2 variant(float2 z, int code) {
     if (code & 4) r.y = -r.y;
     return r;
 }
-
-// S [img = p * F + q][bins] complex -> T [bin][row][k] fp32, the bin-major
-// operand the GEMM's TMA reads (hi / lo and B's row variants are made in
-// shared memory by the GEMM). ROWQ = false: row = p (R = Pn), k = 2 q + c
-// (K = 2 F); ROWQ = true: row = q (R = F), k = 2 p + c (K = 2 Pn).
-// block: one row-side index, TB k-side indices x TB bins; threads 32 x 8
-template <bool ROWQ>
-__global__ void __launch_bounds__(256) prep_k(const float2* __restrict__ S, int64_t bins, int Pn, int F,
-                                              float* __restrict__ T) {
-    __shared__ float2 tile[TB][TB + 1];
-    const int rs = blockIdx.z;                // row-side index (p, or q when ROWQ)
-    const int j0 = blockIdx.y * TB;           // k-side indices (q, or p when ROWQ)
-    const int64_t w0 = int64_t(blockIdx.x) * TB;
-    const int nk = ROWQ ? Pn : F;             // k-side extent
-    const int K = 2 * nk;
-    const int R = ROWQ ? F : Pn;              // rows per bin
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    for (int jj = ty; jj < TB; jj += 8) {
-        const int j = j0 + jj;
-        const int64_t w = w0 + tx;
-        float2 v = make_float2(0.f, 0.f);
-        if (j < nk && w < bins) {
-            const int64_t img = ROWQ ? int64_t(j) * F + rs : int64_t(rs) * F + j;
-            v = __ldcs(S + img * bins + w);
-        }
-        tile[jj][tx] = v;
-    }
-    __syncthreads();
-    // out row (bin, rs): the k-side pairs j0..j0+TB as 2 TB consecutive floats
-    for (int ww = ty; ww < TB; ww += 8) {
-        const int64_t w = w0 + ww;
-        if (w >= bins) continue;
-        float* o = T + (w * R + rs) * K + 2 * j0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int e = tx + 32 * h, jj = e >> 1;
-            if (j0 + jj < nk) {
-                const float2 z = tile[jj][ww];
-                o[e] = (e & 1) ? z.y : z.x;
-            }
-        }
-    }
-}
-
-// D [bin][p][2 Q] fp32 (complex rows) -> S [p * Q + q][bins] complex
-__global__ void __launch_bounds__(256) unprep_k(const float* __restrict__ D, int64_t bins, int Pn, int Q,
-                                                int ldd, float2* __restrict__ S) {
-    __shared__ float2 tile[TB][TB + 1];
-    const int p = blockIdx.z, q0 = blockIdx.y * TB;
-    const int64_t w0 = int64_t(blockIdx.x) * TB;
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    for (int ww = ty; ww < TB; ww += 8) {
-        const int64_t w = w0 + ww;
-        float2 v = make_float2(0.f, 0.f);
-        if (w < bins && q0 + tx < Q) v = *reinterpret_cast<const float2*>(D + (w * Pn + p) * int64_t(ldd) + 2 * (q0 + tx));
-        tile[ww][tx] = v;
-    }
-    __syncthreads();
-    for (int qq = ty; qq < TB; qq += 8) {
-        const int q = q0 + qq;
-        const int64_t w = w0 + tx;
-        if (q < Q && w < bins) __stcs(S + (int64_t(p) * Q + q) * bins + w, tile[tx][qq]);
-    }
-}
-
-constexpr int BM = 128;   // rows per CTA tile (TMEM lanes)
-constexpr int BKC = 32;   // K per stage (one 128-byte swizzle row)
-constexpr int STAGES = 2;
-
-struct bg_params {
-    int M, N, K;          // per bin: D[M][N] = sum_k A[M][k] B[N][k]
-    int NB;               // raw B rows per bin loaded by TMA (N, or N / 2 with two variants per row)
-    int v0, v1;           // variant codes of B rows 2r, 2r + 1 (NB = N / 2)
-    int ldd;              // D row pitch (floats)
-    int mtiles;
-};
-
-// the 16-byte chunk q of row r of a 128B-swizzled K-major tile
-__device__ __forceinline__ uint32_t sw_chunk(uint32_t r, uint32_t q) { return r * 128u + (((q ^ (r & 7u)) & 7u) << 4); }
-
 __device__ __forceinline__ float4 lo4(float4 v) {
     return make_float4(v.x - tf32_hi(v.x), v.y - tf32_hi(v.y), v.z - tf32_hi(v.z), v.w - tf32_hi(v.w));
 }
-__device__ __forceinline__ float4 var4(float4 v, int code) {  // two complex pairs
-    const float2 a = variant(make_float2(v.x, v.y), code), b = variant(make_float2(v.z, v.w), code);
-    return make_float4(a.x, a.y, b.x, b.y);
+// byte offset of 16-byte chunk q of row r in a 128B-swizzled K-major tile
+__device__ __forceinline__ uint32_t sw_chunk(uint32_t r, uint32_t q) { return r * 128u + (((q ^ (r & 7u)) & 7u) << 4); }
+
+__device__ __forceinline__ void tma4_w(uint32_t bar, uint32_t dst, const CUtensorMap* m, int c1, int c2, int c3) {
+    asm volatile(
+        "{\n\t.reg .pred pe;\n\t"
+        "elect.sync _|pe, 0xffffffff;\n\t"
+        "@pe cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n\t}" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma4_store(const CUtensorMap* m, uint32_t src, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(0), "r"(c1), "r"(c2), "r"(c3), "r"(src)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            addr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+        "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+        "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
 }
 
-// Persistent: one CTA per SM walks the (bin, 128-row) tiles t = blockIdx.x,
-// blockIdx.x + gridDim.x, ...; the stage ring runs across tiles and the
-// accumulator is double-buffered in TMEM (2 x 256 columns), so the drain of
-// tile t overlaps the loads and MMAs of tile t + 1.
-// warps 0-3: operand expansion (lo = x - tf32(x) of A and B, B's two row
-//            variants) of every stage;
-// warps 4-7: epilogue (TMEM lane quarter = warp % 4): drain D rows to HBM;
-// warp 8   : TMA of the raw A (128 rows) and raw B (NB rows) tiles;
-// warp 9   : TMEM allocation and the MMA issue (Ahi.Bhi + Ahi.Blo + Alo.Bhi).
-// Stage layout: [A raw = A hi][A lo][B raw][B hi][B lo] (B hi = B raw when NB == N).
-constexpr int BG_THREADS = 320;
-__global__ void __launch_bounds__(BG_THREADS, 1)
-bgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, float* __restrict__ D,
-           bg_params p, int64_t ntiles) {
+// two 16-column TMEM loads of this thread's lane and their completion wait in
+// one asm statement (the outputs cannot be consumed before the wait)
+__device__ __forceinline__ void tmem_ld16_pair(uint32_t addr0, uint32_t addr1, float (&a)[16], float (&b)[16]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(addr0), "r"(addr1)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = __uint_as_float(r[i]), b[i] = __uint_as_float(r[16 + i]);
+}
+
+constexpr int CG_STAGES = 3;
+constexpr uint32_t BOX_BYTES = 16384;            // one operand tile (128 x 32 floats, or 16 x <= 128 complex)
+constexpr uint32_t STAGE_BYTES = 4 * BOX_BYTES;  // [A raw][B raw][B hi][B lo]
+constexpr uint32_t STG_BYTES = 32768;            // output staging: 128 rows x 32 complex
+constexpr int CG_THREADS = 448;                  // warps 0-7 expansion, 8-11 epilogue, 12 TMA, 13 MMA
+constexpr size_t CG_SMEM = 1024 + CG_STAGES * size_t(STAGE_BYTES) + STG_BYTES + 256;
+
+struct cg_params {
+    int M, N, nmma;       // D rows, D columns (complex), MMA N (N rounded up to 16)
+    int nchunks, klast;   // K chunks of 16 complex; K steps (8 floats) of the last chunk
+    int mtiles;
+    int a_trans, b_trans; // operand tile is K-outer (16 rows of K x all columns)
+    int aq, bq;           // groups per row of the A / B tensors
+    int va, vap;          // variant codes of A and A'
+    int nob;              // 32-column output blocks
+    uint32_t tx_bytes;    // A box + B box
+};
+
+__global__ void __launch_bounds__(CG_THREADS, 1)
+cgemm_tc_k(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+           const __grid_constant__ CUtensorMap tD, cg_params p, int64_t ntiles) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     uint8_t* base_ptr = smem_raw + (base - raw);
-    const bool expand = p.NB != p.N;
-    const uint32_t a_bytes = BM * 128u, braw_bytes = uint32_t(p.NB) * 128u, b_bytes = uint32_t(p.N) * 128u;
-    const uint32_t off_alo = a_bytes, off_braw = 2u * a_bytes, off_bhi = off_braw + (expand ? braw_bytes : 0u);
-    const uint32_t off_blo = off_bhi + b_bytes;
-    const uint32_t stage_bytes = ((off_blo + b_bytes + 1023u) / 1024u) * 1024u;
-    const uint32_t tma_bytes = a_bytes + braw_bytes;
-    const uint32_t bar_base = base + STAGES * stage_bytes;
+    const uint32_t stg = base + CG_STAGES * STAGE_BYTES;
+    uint8_t* stg_ptr = base_ptr + CG_STAGES * STAGE_BYTES;
+    const uint32_t bar_base = stg + STG_BYTES;
     auto full_bar = [&](int s) { return bar_base + 8u * uint32_t(s); };
-    auto conv_bar = [&](int s) { return bar_base + 8u * uint32_t(STAGES + s); };
-    auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(2 * STAGES + s); };
-    auto accf_bar = [&](int b) { return bar_base + 8u * uint32_t(3 * STAGES + b); };
-    auto acce_bar = [&](int b) { return bar_base + 8u * uint32_t(3 * STAGES + 2 + b); };
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (bar_base - base) + 8u * uint32_t(3 * STAGES + 4));
+    auto conv_bar = [&](int s) { return bar_base + 8u * uint32_t(CG_STAGES + s); };
+    auto empty_bar = [&](int s) { return bar_base + 8u * uint32_t(2 * CG_STAGES + s); };
+    auto aempty_bar = [&](int b) { return bar_base + 8u * uint32_t(3 * CG_STAGES + b); };
+    const uint32_t accf_bar = bar_base + 8u * uint32_t(3 * CG_STAGES + 2);
+    const uint32_t acce_bar = accf_bar + 8u;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base_ptr + (acce_bar + 8u - base));
 
-    const int warp = threadIdx.x >> 5;
-    const int nchunks = (p.K + BKC - 1) / BKC;
-
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < CG_STAGES; ++s) {
             mbar_init(full_bar(s), 1);
-            mbar_init(conv_bar(s), 128);
+            mbar_init(conv_bar(s), 256);
             mbar_init(empty_bar(s), 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(accf_bar(b), 1);
-            mbar_init(acce_bar(b), 128);
-        }
+        mbar_init(aempty_bar(0), 1);
+        mbar_init(aempty_bar(1), 1);
+        mbar_init(accf_bar, 1);
+        mbar_init(acce_bar, 128);
         fence_barrier_init();
     }
-    if (warp == 9) tmem_alloc(smem_u32(tmem_slot), 512);
+    if (warp == 13) tmem_alloc(smem_u32(tmem_slot), 512);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem = *tmem_slot;  // D_r: cols [0, 128), D_i: [128, 256), A buffers: [256, 384), [384, 512)
 
-    if (warp == 8) {
+    if (warp == 12) {
+        // ---- TMA producer ----
         int s = 0;
         uint32_t ph = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int64_t bin = t / p.mtiles;
-            const int m0 = int(t - bin * p.mtiles) * BM;
-            const int arow = int(bin * p.M + m0), brow = int(bin * p.NB);
-            for (int c = 0; c < nchunks; ++c) {
+            const int m0 = int(t - bin * p.mtiles) * 128;
+            for (int c = 0; c < p.nchunks; ++c) {
                 mbar_wait(empty_bar(s), ph ^ 1u);
-                const uint32_t st0 = base + uint32_t(s) * stage_bytes;
+                const uint32_t st0 = base + uint32_t(s) * STAGE_BYTES;
                 asm volatile(
                     "{\n\t.reg .pred pe;\n\t"
                     "elect.sync _|pe, 0xffffffff;\n\t"
                     "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(full_bar(s)),
-                    "r"(tma_bytes)
+                    "r"(p.tx_bytes)
                     : "memory");
-                tma_w(full_bar(s), st0, &tA, c * BKC, arow);
-                tma_w(full_bar(s), st0 + off_braw, &tB, c * BKC, brow);
-                if (++s == STAGES) s = 0, ph ^= 1u;
+                if (p.a_trans)
+                    tma4_w(full_bar(s), st0, &tA, int(bin), 0, 16 * c);
+                else
+                    tma4_w(full_bar(s), st0, &tA, int(bin), (16 / kGrp) * c, m0);
+                if (p.b_trans)
+                    tma4_w(full_bar(s), st0 + BOX_BYTES, &tB, int(bin), 0, 16 * c);
+                else
+                    tma4_w(full_bar(s), st0 + BOX_BYTES, &tB, int(bin), (16 / kGrp) * c, 0);
+                if (++s == CG_STAGES) s = 0, ph ^= 1u;
             }
         }
-    } else if (warp == 9) {
-        const uint32_t idesc = idesc_tf32(BM, p.N);
+    } else if (warp == 13) {
+        // ---- MMA issue ----
+        const uint32_t idesc = idesc_tf32(128, p.nmma);
+        const uint32_t d_r = tmem, d_i = tmem + 128u;
         int s = 0;
         uint32_t ph = 0;
+        int g = 0;  // global chunk counter (TMEM A buffer = g & 1)
         int it = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int b = it & 1;
-            mbar_wait(acce_bar(b), uint32_t((it >> 1) & 1) ^ 1u);  // the epilogue drained this buffer
+            mbar_wait(acce_bar, uint32_t(it & 1) ^ 1u);  // the epilogue drained the previous tile's D
             tc_fence_after();
-            const uint32_t d = tmem + uint32_t(b) * 256u;
-            for (int c = 0; c < nchunks; ++c) {
+            for (int c = 0; c < p.nchunks; ++c, ++g) {
                 mbar_wait(conv_bar(s), ph);
                 tc_fence_after();
-                const uint32_t st0 = base + uint32_t(s) * stage_bytes;
-                const uint32_t a_hi = st0, a_lo = st0 + off_alo, b_hi = st0 + off_bhi, b_lo = st0 + off_blo;
-                const int ksteps = min(BKC, p.K - c * BKC) / 8;
-                for (int kk = 0; kk < ksteps; ++kk) {
-                    const uint32_t ko = uint32_t(kk) * 32u;  // 8 fp32 along K
-                    const uint64_t ah = sw128_desc(a_hi + ko), al = sw128_desc(a_lo + ko);
-                    const uint64_t bh = sw128_desc(b_hi + ko), bl = sw128_desc(b_lo + ko);
-                    mma_tf32_w(d, ah, bh, idesc, (c == 0 && kk == 0) ? 0u : 1u);
-                    mma_tf32_w(d, ah, bl, idesc, 1u);
-                    mma_tf32_w(d, al, bh, idesc, 1u);
+                const uint32_t st0 = base + uint32_t(s) * STAGE_BYTES;
+                const uint32_t bhi = st0 + 2 * BOX_BYTES, blo = st0 + 3 * BOX_BYTES;
+                const uint32_t a0 = tmem + 256u + 128u * uint32_t(g & 1);
+                const int ks = (c == p.nchunks - 1) ? p.klast : 4;
+                for (int kk = 0; kk < ks; ++kk) {
+                    const uint64_t bh = sw128_desc(bhi + uint32_t(kk) * 32u), bl = sw128_desc(blo + uint32_t(kk) * 32u);
+                    const uint32_t a = a0 + uint32_t(kk) * 8u;
+                    const uint32_t acc = (c == 0 && kk == 0) ? 0u : 1u;
+                    mma_tf32_ts_w(d_r, a, bh, idesc, acc);
+                    mma_tf32_ts_w(d_r, a, bl, idesc, 1u);
+                    mma_tf32_ts_w(d_r, a + 32u, bh, idesc, 1u);
+                    mma_tf32_ts_w(d_i, a + 64u, bh, idesc, acc);
+                    mma_tf32_ts_w(d_i, a + 64u, bl, idesc, 1u);
+                    mma_tf32_ts_w(d_i, a + 96u, bh, idesc, 1u);
                 }
                 mma_commit_w(empty_bar(s));
-                if (++s == STAGES) s = 0, ph ^= 1u;
+                mma_commit_w(aempty_bar(g & 1));
+                if (++s == CG_STAGES) s = 0, ph ^= 1u;
             }
-            mma_commit_w(accf_bar(b));
+            mma_commit_w(accf_bar);
         }
-    } else if (warp < 4) {
-        // ---- operand expansion of every stage ----
-        const int t0 = threadIdx.x;  // 0..127
+    } else if (warp < 8) {
+        // ---- operand expansion: A -> TMEM (hi, lo, A' hi, A' lo), B -> smem hi / lo ----
+        const int q = warp & 3, h = warp >> 2;
+        const int row = q * 32 + lane;  // TMEM lane = A row
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        const int tid = threadIdx.x;    // 0..255
         int s = 0;
         uint32_t ph = 0;
+        int g = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int c = 0; c < nchunks; ++c) {
+            for (int c = 0; c < p.nchunks; ++c, ++g) {
                 mbar_wait(full_bar(s), ph);
-                uint8_t* st0 = base_ptr + size_t(s) * stage_bytes;
-                for (int i = t0; i < BM * 8; i += 128) {  // A lo
-                    const uint32_t o = sw_chunk(uint32_t(i >> 3), uint32_t(i & 7));
-                    *reinterpret_cast<float4*>(st0 + off_alo + o) = lo4(*reinterpret_cast<const float4*>(st0 + o));
-                }
-                if (expand) {  // B rows 2r + c' = variant c' of raw row r, hi and lo
-                    for (int i = t0; i < p.NB * 8; i += 128) {
-                        const uint32_t r = uint32_t(i >> 3), q = uint32_t(i & 7);
-                        const float4 v = *reinterpret_cast<const float4*>(st0 + off_braw + sw_chunk(r, q));
-                        const float4 h0 = var4(v, p.v0), h1 = var4(v, p.v1);
-                        const uint32_t o0 = sw_chunk(2u * r, q), o1 = sw_chunk(2u * r + 1u, q);
-                        *reinterpret_cast<float4*>(st0 + off_bhi + o0) = h0;
-                        *reinterpret_cast<float4*>(st0 + off_bhi + o1) = h1;
-                        *reinterpret_cast<float4*>(st0 + off_blo + o0) = lo4(h0);
-                        *reinterpret_cast<float4*>(st0 + off_blo + o1) = lo4(h1);
+                mbar_wait(aempty_bar(g & 1), uint32_t((g >> 1) & 1) ^ 1u);
+                tc_fence_after();
+                uint8_t* st0 = base_ptr + size_t(s) * STAGE_BYTES;
+                // A: 8 complex (16 floats) of this row: K floats [16 h, 16 h + 16) of the chunk
+                float2 x[8];
+                if (p.a_trans) {  // tile [16 k-rows][aq groups][2 kGrp floats]; A row = column index
+                    const float2* src = reinterpret_cast<const float2*>(st0);
+                    const bool ok = row < p.M;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        x[u] = ok ? src[(8 * h + u) * (p.aq * kGrp) + row] : make_float2(0.f, 0.f);
+                } else {  // tile [128 rows][32 floats]: chunks 4h..4h+3 of the row, rotated by lane (bank spread)
+                    const float4* src = reinterpret_cast<const float4*>(st0 + size_t(row) * 128);
+                    float4 t4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) t4[u] = src[4 * h + ((u + lane) & 3)];
+                    const int rot = lane & 3;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int src_i = (k - rot) & 3;  // t4[u] holds chunk (u + rot) & 3
+                        float4 v = t4[0];
+                        if (src_i == 1) v = t4[1];
+                        if (src_i == 2) v = t4[2];
+                        if (src_i == 3) v = t4[3];
+                        x[2 * k] = make_float2(v.x, v.y);
+                        x[2 * k + 1] = make_float2(v.z, v.w);
                     }
-                } else {
-                    for (int i = t0; i < p.N * 8; i += 128) {
-                        const uint32_t o = sw_chunk(uint32_t(i >> 3), uint32_t(i & 7));
-                        *reinterpret_cast<float4*>(st0 + off_blo + o) =
-                            lo4(*reinterpret_cast<const float4*>(st0 + off_braw + o));
+                }
+                {
+                    float vh[16], vl[16], wh[16], wl[16];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const float2 lo = make_float2(x[u].x - tf32_hi(x[u].x), x[u].y - tf32_hi(x[u].y));
+                        const float2 a = variant(x[u], p.va), al = variant(lo, p.va);
+                        const float2 b = variant(x[u], p.vap), bl = variant(lo, p.vap);
+                        vh[2 * u] = a.x, vh[2 * u + 1] = a.y;
+                        vl[2 * u] = al.x, vl[2 * u + 1] = al.y;
+                        wh[2 * u] = b.x, wh[2 * u + 1] = b.y;
+                        wl[2 * u] = bl.x, wl[2 * u + 1] = bl.y;
+                    }
+                    const uint32_t a0 = tmem + lane_base + 256u + 128u * uint32_t(g & 1) + uint32_t(16 * h);
+                    tmem_st16(a0, vh);
+                    tmem_st16(a0 + 32u, vl);
+                    tmem_st16(a0 + 64u, wh);
+                    tmem_st16(a0 + 96u, wl);
+                }
+                // B: rows = output columns (128, zero / unused beyond N), 8 chunks of 16 bytes
+                uint8_t* bhi = st0 + 2 * BOX_BYTES;
+                uint8_t* blo = st0 + 3 * BOX_BYTES;
+                if (p.b_trans) {  // tile [16 k-rows][bq groups][2 kGrp floats]: transpose into K-major rows
+                    const float2* src = reinterpret_cast<const float2*>(st0 + BOX_BYTES);
+                    const int ncol = p.bq * kGrp;
+#pragma unroll
+                    for (int tt = 0; tt < 4; ++tt) {
+                        const int u = tid + 256 * tt;
+                        const int i = u & 127, j = u >> 7;
+                        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (i < ncol) {
+                            const float2 a = src[(2 * j) * ncol + i], b = src[(2 * j + 1) * ncol + i];
+                            v = make_float4(a.x, a.y, b.x, b.y);
+                        }
+                        const uint32_t o = sw_chunk(uint32_t(i), uint32_t(j));
+                        *reinterpret_cast<float4*>(bhi + o) = v;
+                        *reinterpret_cast<float4*>(blo + o) = lo4(v);
+                    }
+                } else {  // tile [128 rows][32 floats]
+                    const uint8_t* src = st0 + BOX_BYTES;
+#pragma unroll
+                    for (int tt = 0; tt < 4; ++tt) {
+                        const int u = tid + 256 * tt;
+                        const int r = u >> 3, j = u & 7;
+                        const float4 v = *reinterpret_cast<const float4*>(src + r * 128 + j * 16);
+                        const uint32_t o = sw_chunk(uint32_t(r), uint32_t(j));
+                        *reinterpret_cast<float4*>(bhi + o) = v;
+                        *reinterpret_cast<float4*>(blo + o) = lo4(v);
                     }
                 }
-                fence_proxy_async();  // generic-proxy writes -> visible to the tensor cores
+                tmem_wait_st();
+                tc_fence_before();
+                fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
                 mbar_arrive(conv_bar(s));
-                if (++s == STAGES) s = 0, ph ^= 1u;
+                if (++s == CG_STAGES) s = 0, ph ^= 1u;
             }
         }
     } else {
-        // ---- epilogue: warps 4-7, lane = row of the tile ----
-        const int r = threadIdx.x - 128;  // 0..127
-        const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+        // ---- epilogue: warps 8-11 (TMEM lane quarter = warp % 4), row = lane of the tile ----
+        const int q = warp & 3;
+        const int r = q * 32 + lane;
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        const bool leader = threadIdx.x == 256;
         int it = 0;
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-            const int b = it & 1;
             const int64_t bin = t / p.mtiles;
-            const int row = int(t - bin * p.mtiles) * BM + r;
-            mbar_wait(accf_bar(b), uint32_t((it >> 1) & 1));
+            const int m0 = int(t - bin * p.mtiles) * 128;
+            mbar_wait(accf_bar, uint32_t(it & 1));
             tc_fence_after();
-            float* drow = D + (bin * p.M + row) * int64_t(p.ldd);
-            const uint32_t acol = tmem + lane_base + uint32_t(b) * 256u;
-            for (int c0 = 0; c0 < p.N; c0 += 16) {
-                float v[16];
-                tmem_ld16(acol + uint32_t(c0), v);
-                tmem_wait_ld();
-                if (row < p.M) {
+            for (int ob = 0; ob < p.nob; ++ob) {
+                // the staging tile is free once the previous TMA store has read it
+                if (leader) bulk_wait_read0();
+                epi_bar();
+                // row r: 32 complex = 16 chunks of 16 bytes, chunk k = (re, im) of columns 2k, 2k + 1;
+                // within each half row the chunk order rotates with the lane, so a
+                // warp's 16-byte stores cover all 8 bank groups (4 wavefronts)
+                float4* dst = reinterpret_cast<float4*>(stg_ptr + size_t(r) * 256);
+                const int rot = lane & 7;
 #pragma unroll
-                    for (int q = 0; q < 16; q += 4)
-                        __stcs(reinterpret_cast<float4*>(drow + c0 + q), make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+                for (int hh = 0; hh < 2; ++hh) {
+                    float dr[16], di[16];
+                    const uint32_t col = uint32_t(32 * ob + 16 * hh);
+                    tmem_ld16_pair(tmem + lane_base + col, tmem + lane_base + 128u + col, dr, di);
+                    if (ob == p.nob - 1 && hh == 1) {  // D fully read: the next tile's MMAs may start
+                        tc_fence_before();
+                        mbar_arrive(acce_bar);
+                    }
+                    float4 c[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) c[k] = make_float4(dr[2 * k], di[2 * k], dr[2 * k + 1], di[2 * k + 1]);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int k = (u + rot) & 7;
+                        const float4 a0 = (k & 1) ? c[1] : c[0], a1 = (k & 1) ? c[3] : c[2];
+                        const float4 a2 = (k & 1) ? c[5] : c[4], a3 = (k & 1) ? c[7] : c[6];
+                        const float4 b0 = (k & 2) ? a1 : a0, b1 = (k & 2) ? a3 : a2;
+                        dst[8 * hh + k] = (k & 4) ? b1 : b0;
+                    }
                 }
+                fence_proxy_async();
+                epi_bar();
+                if (leader) tma4_store(&tD, stg, int(bin), (32 / kGrp) * ob, m0);
             }
-            tc_fence_before();
-            mbar_arrive(acce_bar(b));
         }
+        if (leader) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 9) {
+    if (warp == 13) {
         __syncwarp();
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
 }
 
-// S [img = p * F + q][bins] complex -> T [bin][row][k] fp32 (transpose only)
-template <bool ROWQ>
-void prep(cudaStream_t st, const float2* S, int64_t bins, int Pn, int F, float* T) {
-    const int nk = ROWQ ? Pn : F, rsn = ROWQ ? F : Pn;
-    require(rsn < 65536 && ceil_div(nk, TB) < 65536, "tc cmac: prep grid exceeds 65535");
-    const dim3 grid(unsigned(ceil_div(bins, TB)), unsigned(ceil_div(nk, TB)), unsigned(rsn));
-    prep_k<ROWQ><<<grid, dim3(32, 8, 1), 0, st>>>(S, bins, Pn, F, T);
-    launch_check("tc_cmac_prep");
-}
-
-void unprep(cudaStream_t st, const float* Dp, int64_t bins, int Pn, int Q, int ldd, float2* S) {
-    require(Pn < 65536, "tc cmac: unprep grid exceeds 65535");
-    const dim3 grid(unsigned(ceil_div(bins, TB)), unsigned(ceil_div(Q, TB)), unsigned(Pn));
-    unprep_k<<<grid, dim3(32, 8, 1), 0, st>>>(Dp, bins, Pn, Q, ldd, S);
-    launch_check("tc_cmac_unprep");
-}
-
-// D[bin][M][N] = A[bin][M][K] . B[bin][N][K]^T with B rows 2r + c' = variant
-// c' of the raw row r (raw B: [bin][N / 2][K])
-void bgemm(cudaStream_t st, const float* A, const float* B, float* Dp, int64_t nb, int M, int N, int K, int v0, int v1) {
-    require(N % 16 == 0 && N <= 256 && K % 8 == 0, "tc cmac: bad GEMM shape");
-    const int NB = N / 2;
-    require(nb * M < (int64_t(1) << 31) && nb * NB < (int64_t(1) << 31), "tc cmac: operand rows exceed 2^31");
-    const CUtensorMap ta = make_panel_map_rows(A, K, nb * M, BM), tb = make_panel_map_rows(B, K, nb * NB, NB);
-    bg_params p{M, N, K, NB, v0, v1, N, int(ceil_div(M, BM))};
-    const size_t stage = ((size_t(2 * BM * 128 + NB * 128 + 2 * N * 128) + 1023) / 1024) * 1024;
-    const size_t smem = size_t(STAGES) * stage + 1024 + 256;
-    require(smem <= 227 * 1024, "tc cmac: stage does not fit in shared memory");
-    const int64_t ntiles = nb * p.mtiles;
+// mode 0 fwd, 1 dgrad, 2 upd
+void cgemm(cudaStream_t st, int mode, const float2* Ap, const float2* Bp, float2* Dp, int64_t Bn, int64_t f,
+           int64_t fo, int64_t bins) {
+    require(tc_cmac_supported(Bn, f, fo), "tc cmac: unsupported shape");
+    require(bins < (int64_t(1) << 31), "tc cmac: too many bins");
+    cg_params p{};
+    CUtensorMap ta, tb, td;
+    int64_t kdim = 0;  // complex K extent
+    if (mode == 0) {            // A = X [Bn][f] rows n; B = K [fo][f] rows o; D = Y [Bn][fo]
+        p.M = int(Bn), p.N = int(fo), kdim = f;
+        p.a_trans = 0, p.b_trans = 0;
+        ta = grp_map(Ap, bins, f, Bn, 16 / kGrp, 128);
+        tb = grp_map(Bp, bins, f, fo, 16 / kGrp, 128);
+        td = grp_map(Dp, bins, fo, Bn, 32 / kGrp, 128);
+        p.va = 0, p.vap = 1 | 4;  // A = (re, im), A' = (im, -re)
+    } else if (mode == 1) {     // A = G [Bn][fo] rows n; B = K [fo][f] K-outer (rows o), columns i; D = DX [Bn][f]
+        p.M = int(Bn), p.N = int(f), kdim = fo;
+        p.a_trans = 0, p.b_trans = 1;
+        ta = grp_map(Ap, bins, fo, Bn, 16 / kGrp, 128);
+        tb = grp_map(Bp, bins, f, fo, int(f / kGrp), 16);
+        td = grp_map(Dp, bins, f, Bn, 32 / kGrp, 128);
+        p.va = 4, p.vap = 1;      // A = (re, -im), A' = (im, re)
+    } else {                    // A = G [Bn][fo] K-outer (rows n), columns o; B = X [Bn][f] K-outer; D = DK [fo][f]
+        p.M = int(fo), p.N = int(f), kdim = Bn;
+        p.a_trans = 1, p.b_trans = 1;
+        ta = grp_map(Ap, bins, fo, Bn, int(fo / kGrp), 16);
+        tb = grp_map(Bp, bins, f, Bn, int(f / kGrp), 16);
+        td = grp_map(Dp, bins, f, fo, 32 / kGrp, 128);
+        p.va = 0, p.vap = 1 | 2;  // A = (re, im), A' = (-im, re)
+    }
+    p.aq = int((mode == 0 ? f : fo) / kGrp);
+    p.bq = int(f / kGrp);
+    p.nmma = ((p.N + 15) / 16) * 16;
+    p.nchunks = int(ceil_div(kdim, 16));
+    p.klast = int(ceil_div(2 * (kdim - 16 * (p.nchunks - 1)), 8));
+    p.mtiles = mode == 2 ? 1 : int(ceil_div(Bn, 128));
+    p.nob = int(ceil_div(p.N, 32));
+    const uint32_t a_box = p.a_trans ? uint32_t(16 * p.aq * kGrp * 8) : BOX_BYTES;
+    const uint32_t b_box = p.b_trans ? uint32_t(16 * p.bq * kGrp * 8) : BOX_BYTES;
+    p.tx_bytes = a_box + b_box;
+    const int64_t ntiles = bins * p.mtiles;
     int dev = 0, sms = 148;
     ZNN_CUDA_CHECK(cudaGetDevice(&dev));
     ZNN_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const unsigned grid = unsigned(std::min<int64_t>(ntiles, sms));  // persistent: one CTA per SM
-    ZNN_CUDA_CHECK(cudaFuncSetAttribute(bgemm_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    bgemm_tc_k<<<grid, BG_THREADS, smem, st>>>(ta, tb, Dp, p, ntiles);
+    ZNN_CUDA_CHECK(cudaFuncSetAttribute(cgemm_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CG_SMEM)));
+    cgemm_tc_k<<<grid, CG_THREADS, CG_SMEM, st>>>(ta, tb, td, p, ntiles);
     launch_check("tc_cmac_gemm");
 }
 
 }  // namespace
 
-int64_t tc_cmac_bytes(int64_t Bn, int64_t f, int64_t fo, int64_t bins) {
-    // bin-major A + raw B + D of the largest of the three GEMMs
-    const int64_t fwd = bins * Bn * 2 * f + bins * fo * 2 * f + bins * Bn * 2 * fo;
-    const int64_t dgr = bins * Bn * 2 * fo + bins * f * 2 * fo + bins * Bn * 2 * f;
-    const int64_t upd = bins * fo * 2 * Bn + bins * f * 2 * Bn + bins * fo * 2 * f;
-    return int64_t(sizeof(float)) * std::max(fwd, std::max(dgr, upd)) + 4096;
-}
-
 bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo) {
-    // N = 2 f' (fwd), 2 f (dgrad / upd) <= 256 and a multiple of 16; enough
-    // reuse per kernel-spectrum bin to pay the operand transposes
-    return Bn >= 128 && 2 * f <= 256 && 2 * fo <= 256 && (2 * f) % 16 == 0 && (2 * fo) % 16 == 0;
+    return Bn >= 128 && f <= 128 && fo <= 128 && f % 8 == 0 && fo % 8 == 0;
 }
 
-namespace {
-float* carve_f(char*& cur, int64_t n) {
-    float* p = reinterpret_cast<float*>(cur);
-    cur += ((int64_t(sizeof(float)) * n + 1023) / 1024) * 1024;
-    return p;
-}
-}  // namespace
-
-// Y[n][o] = sum_i X[n][i] conj K[o][i]; X [n f + i][bins], K [o f + i][bins], Y [n fo + o][bins]
 void tc_cmac_fwd(cudaStream_t st, const float2* X, const float2* K, float2* Y, int64_t Bn, int64_t f, int64_t fo,
-                 int64_t bins, void* ws) {
-    char* cur = static_cast<char*>(ws);
-    const int kk = int(2 * f), nn = int(2 * fo);
-    float* A = carve_f(cur, bins * Bn * kk);
-    float* B = carve_f(cur, bins * fo * kk);
-    float* Dp = carve_f(cur, bins * Bn * nn);
-    prep<false>(st, X, bins, int(Bn), int(f), A);
-    prep<false>(st, K, bins, int(fo), int(f), B);
-    // rows (o, re): (Kr, Ki) over i; (o, im): (-Ki, Kr)
-    bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 0, 1 | 2);
-    unprep(st, Dp, bins, int(Bn), int(fo), nn, Y);
+                 int64_t bins) {
+    cgemm(st, 0, X, K, Y, Bn, f, fo, bins);
 }
-
-// DX[n][i] = sum_o G[n][o] K[o][i]; G [n fo + o][bins], DX [n f + i][bins]
 void tc_cmac_dgrad(cudaStream_t st, const float2* G, const float2* K, float2* DX, int64_t Bn, int64_t f, int64_t fo,
-                   int64_t bins, void* ws) {
-    char* cur = static_cast<char*>(ws);
-    const int kk = int(2 * fo), nn = int(2 * f);
-    float* A = carve_f(cur, bins * Bn * kk);
-    float* B = carve_f(cur, bins * f * kk);
-    float* Dp = carve_f(cur, bins * Bn * nn);
-    prep<false>(st, G, bins, int(Bn), int(fo), A);
-    prep<true>(st, K, bins, int(fo), int(f), B);  // K images o f + i: rows i, k = (o, c)
-    // rows (i, re): (Kr, -Ki) over o; (i, im): (Ki, Kr)
-    bgemm(st, A, B, Dp, bins, int(Bn), nn, kk, 4, 1);
-    unprep(st, Dp, bins, int(Bn), int(f), nn, DX);
+                   int64_t bins) {
+    cgemm(st, 1, G, K, DX, Bn, f, fo, bins);
 }
-
-// dK[o][i] = sum_n X[n][i] conj G[n][o]; dK [o f + i][bins]
 void tc_cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, int64_t Bn, int64_t f, int64_t fo,
-                 int64_t bins, void* ws) {
-    char* cur = static_cast<char*>(ws);
-    const int kk = int(2 * Bn), nn = int(2 * f);
-    float* A = carve_f(cur, bins * fo * kk);
-    float* B = carve_f(cur, bins * f * kk);
-    float* Dp = carve_f(cur, bins * fo * nn);
-    prep<true>(st, G, bins, int(Bn), int(fo), A);  // rows o: (Gr, Gi) over n
-    prep<true>(st, X, bins, int(Bn), int(f), B);   // rows i: (Xr, Xi) over n
-    // rows (i, re): (Xr, Xi); (i, im): (Xi, -Xr)
-    bgemm(st, A, B, Dp, bins, int(fo), nn, kk, 0, 1 | 4);
-    unprep(st, Dp, bins, int(fo), int(f), nn, DK);
+                 int64_t bins) {
+    cgemm(st, 2, G, X, DK, Bn, f, fo, bins);
 }
 
 }  // namespace znn_gpu

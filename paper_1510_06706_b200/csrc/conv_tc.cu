@@ -570,6 +570,9 @@ size_t panel_bytes(int f_src, int n_real, int64_t T) {
 
 // 2D TMA map over a row-major fp32 panel [rows][cols] (cols * 4 B a multiple
 // of 16), box = 32 columns (one 128 B swizzle row) x box_rows rows, SWIZZLE_128B.
+// the driver entry point of cuTensorMapEncodeTiled (shared with bgemm_tc.cu)
+void* tensor_map_encoder() { return reinterpret_cast<void*>(encoder()); }
+
 CUtensorMap make_panel_map_rows(const float* ptr, int64_t cols, int64_t rows, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};

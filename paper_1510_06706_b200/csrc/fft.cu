@@ -305,13 +305,41 @@ __device__ __forceinline__ uint32_t phase_pair_line(const phase_geom& G, uint32_
     return ((b * sxy + rxy) * sz + rz) * f + i;
 }
 
+// Group layout (tensor-core plans, bgemm_tc.hpp: GRP = 8 maps interleaved
+// bin by bin). "quad" flags below mean "spectra in the group layout".
+// Group line order: the GRP maps of a group are adjacent lines, so a warp's
+// transposed z-bin stores fill whole group-bins (64 bytes). Dense: line =
+// (group * pl + xy) * GRP + t. Phased: the z-phases stay adjacent inside each
+// map: line = (((g * pl + xy) * GRP + t) * sz + rz) with g = (b, rx, ry, map
+// group). Returns the image.
+constexpr int GRP = znn_gpu::kGrp;
+__device__ __forceinline__ uint32_t quad_line(uint32_t line, uint32_t pl, uint32_t* xy) {
+    const uint32_t t = line % GRP, l2 = line / GRP, qd = l2 / pl;
+    *xy = l2 - qd * pl;
+    return qd * GRP + t;
+}
+__device__ __forceinline__ uint32_t phase_quad_line(const phase_geom& G, uint32_t line, uint32_t pl, uint32_t* xy) {
+    const uint32_t sz = uint32_t(G.sz);
+    const uint32_t rz = line % sz, l2 = line / sz;
+    const uint32_t t = l2 % GRP, l3 = l2 / GRP;
+    const uint32_t g = l3 / pl;
+    *xy = l3 - g * pl;
+    const uint32_t fq = uint32_t(G.f) / GRP, sxy = uint32_t(G.sx * G.sy);
+    const uint32_t iq = g % fq, rest = g / fq, rxy = rest % sxy, b = rest / sxy;
+    return ((b * sxy + rxy) * sz + rz) * uint32_t(G.f) + iq * GRP + t;
+}
+// float2 index of (img, bin) in a spectrum: image-major, or group layout
+__device__ __forceinline__ int64_t spec_at(int quad, int64_t img, int64_t bins, int64_t bin) {
+    return quad ? ((img / GRP) * bins + bin) * GRP + (img % GRP) : img * bins + bin;
+}
+
 // ---- z pass, forward (R2C): lines (img, x < nx, y < ny) of the real input,
 // half spectra stored transposed: spec[img][zb][x][y] ----
 template <int P>
 __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__ in, int64_t in_img_stride, int nx,
                                                         int ny, int nz, int64_t nlines, float2* __restrict__ spec,
                                                         int Px, int Py, const float* __restrict__ gate,
-                                                        phase_geom ph, int phased) {
+                                                        phase_geom ph, int phased, int quad) {
     constexpr int Zh = P / 2 + 1;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
@@ -330,7 +358,9 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
         const uint32_t pl = uint32_t(nx) * uint32_t(ny);
         uint32_t im, rr;
         if (phased) {
-            im = phase_pair_line(ph, uint32_t(line), pl, &rr);
+            im = quad ? phase_quad_line(ph, uint32_t(line), pl, &rr) : phase_pair_line(ph, uint32_t(line), pl, &rr);
+        } else if (quad) {
+            im = quad_line(uint32_t(line), pl, &rr);
         } else {
             im = uint32_t(line) / pl;
             rr = uint32_t(line) - im * pl;
@@ -362,7 +392,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
                 }
             }
         }
-        if (t == 0) obase[l] = (int64_t(im) * Zh * Px + x) * Py + y;
+        if (t == 0) obase[l] = spec_at(quad, im, int64_t(Zh) * Px * Py, int64_t(x) * Py + y);
     }
     __syncthreads();  // twiddles
     float2* st = stash + l * (Zh + 1);
@@ -371,7 +401,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
     });
     __syncthreads();
     // transposed store: a warp writes one z-bin of 32 consecutive lines
-    const int64_t zstride = int64_t(Px) * Py;
+    const int64_t zstride = int64_t(Px) * Py * (quad ? GRP : 1);
     for (int idx = threadIdx.x; idx < LINES * Zh; idx += THREADS) {
         const int l2 = idx % LINES, zb = idx / LINES;
         if (int64_t(blockIdx.x) * LINES + l2 < nlines) spec[obase[l2] + zb * zstride] = stash[l2 * (Zh + 1) + zb];
@@ -813,6 +843,7 @@ struct cube_io {
     float scale;
     int phased;
     phase_geom ph;
+    int quad;                // spectra in the group layout (bgemm_tc.hpp)
 };
 
 template <int P>
@@ -1095,34 +1126,83 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
 constexpr int REGP = 24;
 constexpr int RTHREADS = 256;
 
-template <int P>
+// NI images per CTA: NI = 1 image-major spectra; NI > 1 (tensor-core plans) the
+// NI consecutive images of a group, whose bins are NI * 8-byte pieces of the
+// group layout's group-bins (bgemm_tc.hpp): whole 16 / 32-byte pieces per bin
+template <int P, int NI = 1>
 constexpr size_t cube_reg_smem() {
-    return sizeof(float2) * (size_t(P) + size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
+    return sizeof(float2) * (size_t(P) + size_t(NI) * size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
+}
+// images per CTA of the group-layout cube kernels: four cubes when they fit
+// in ~80 KB (whole 32-byte sectors per bin), else two
+// (ZNN_FFT_GRP_NI = 1 / 2 / 4 overrides: 1 = one image per CTA, 8-byte pieces merged in L2)
+int grp_ni_env(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    const int v = e ? std::atoi(e) : dflt;
+    return (v == 1 || v == 2 || v == 4) ? v : dflt;
+}
+// measured on c5 (in-step, four transforms per layer): P = 20 one image per
+// CTA (26.7 ms vs 30.6 / 29.1 for two / four: the 37 KB cubes keep six CTAs
+// per SM), P = 16 two (11.1 vs 12.3 / 11.3), P <= 12 four
+template <int P>
+int cube_grp_ni() { return grp_ni_env("ZNN_FFT_GRP_NI", P >= 20 ? 1 : (P >= 16 ? 2 : 4)); }
+
+// group-layout piece of NI images at one bin: NI float2 <-> NI / 2 float4
+template <int NI>
+__device__ __forceinline__ void grp_put(float2* __restrict__ dst, const float2 (&v)[NI]) {
+    if constexpr (NI == 1) {
+        __stcs(dst, v[0]);
+    } else {
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+        for (int j = 0; j < NI / 2; ++j)
+            __stcs(d4 + j, make_float4(v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y));
+    }
+}
+template <int NI>
+__device__ __forceinline__ void grp_get(const float2* __restrict__ src, float2 (&v)[NI]) {
+    if constexpr (NI == 1) {
+        v[0] = __ldcs(src);
+    } else {
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+#pragma unroll
+        for (int j = 0; j < NI / 2; ++j) {
+            const float4 u = __ldcs(s4 + j);
+            v[2 * j] = make_float2(u.x, u.y);
+            v[2 * j + 1] = make_float2(u.z, u.w);
+        }
+    }
 }
 
-template <int P>
+template <int P, int NI, bool GL = (NI > 1)>
 __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __restrict__ spec) {
-    constexpr int Zh = P / 2 + 1, PYP = P + 1;
+    constexpr int Zh = P / 2 + 1, PYP = P + 1, CV = Zh * P * PYP, NB = Zh * P * P;
     extern __shared__ float2 sm[];
     float2* tw = sm;
-    float2* cube = tw + P;  // [Zh][P][PYP]
+    float2* cubes = tw + P;  // NI x [Zh][P][PYP]
     fill_twiddles<P>(tw);
-    const int img = blockIdx.x;
-    phase_img pd{};
-    if (a.phased) pd = phase_decode(a.ph, img);
+    const int img0 = blockIdx.x * NI;
+    phase_img pds[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) pds[j] = a.phased ? phase_decode(a.ph, img0 + j) : phase_img{};
     __syncthreads();
     // z lines (R2C) of the valid (x, y) lines, read straight from HBM / L2
     const int nl1 = a.nx * a.ny;
-    for (int ln = threadIdx.x; ln < nl1; ln += RTHREADS) {
-        const int x = ln / a.ny, y = ln - x * a.ny;
+    for (int ln = threadIdx.x; ln < NI * nl1; ln += RTHREADS) {
+        const int j = NI == 1 ? 0 : ln / nl1, l1 = ln - j * nl1;
+        const int x = l1 / a.ny, y = l1 - x * a.ny;
         float2 v[P];
         int64_t base;
         int z0 = 0, zs = 1, zlim = a.nz;
         if (a.phased) {
+            phase_img pd = pds[0];
+#pragma unroll
+            for (int jj = 1; jj < NI; ++jj)
+                if (jj == j) pd = pds[jj];
             base = phase_line(a.ph, pd, x, y);
             z0 = pd.rz, zs = a.ph.sz, zlim = base >= 0 ? a.ph.nz : 0;
         } else {
-            base = int64_t(img) * a.img_stride + int64_t(ln) * a.nz;
+            base = int64_t(img0 + j) * a.img_stride + int64_t(l1) * a.nz;
         }
 #pragma unroll
         for (int z = 0; z < P; ++z) {
@@ -1135,14 +1215,16 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
             v[z] = make_float2(val, 0.f);
         }
         dft_r<P, P, false>(v, tw);
+        float2* cube = cubes + j * CV;
 #pragma unroll
         for (int k = 0; k < Zh; ++k) cube[(k * P + x) * PYP + y] = v[k];
     }
     __syncthreads();
     // y lines of the valid rows x < nx (columns y >= ny are the zero padding)
-    for (int ln = threadIdx.x; ln < Zh * a.nx; ln += RTHREADS) {
-        const int zb = ln / a.nx, x = ln - zb * a.nx;
-        float2* row = cube + (zb * P + x) * PYP;
+    for (int ln = threadIdx.x; ln < NI * Zh * a.nx; ln += RTHREADS) {
+        const int j = NI == 1 ? 0 : ln / (Zh * a.nx), l2 = ln - j * (Zh * a.nx);
+        const int zb = l2 / a.nx, x = l2 - zb * a.nx;
+        float2* row = cubes + j * CV + (zb * P + x) * PYP;
         float2 v[P];
 #pragma unroll
         for (int y = 0; y < P; ++y) v[y] = y < a.ny ? row[y] : make_float2(0.f, 0.f);
@@ -1152,9 +1234,10 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
     }
     __syncthreads();
     // x lines of every column (rows x >= nx are the zero padding)
-    for (int ln = threadIdx.x; ln < Zh * P; ln += RTHREADS) {
-        const int zb = ln / P, y = ln - zb * P;
-        float2* col = cube + zb * P * PYP + y;
+    for (int ln = threadIdx.x; ln < NI * Zh * P; ln += RTHREADS) {
+        const int j = NI == 1 ? 0 : ln / (Zh * P), l3 = ln - j * (Zh * P);
+        const int zb = l3 / P, y = l3 - zb * P;
+        float2* col = cubes + j * CV + zb * P * PYP + y;
         float2 v[P];
 #pragma unroll
         for (int x = 0; x < P; ++x) v[x] = x < a.nx ? col[x * PYP] : make_float2(0.f, 0.f);
@@ -1163,47 +1246,80 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
         for (int k = 0; k < P; ++k) col[k * PYP] = v[k];
     }
     __syncthreads();
-    float4* g4 = reinterpret_cast<float4*>(spec + int64_t(img) * (Zh * P * P));
-    for (int idx = threadIdx.x; idx < Zh * P * P / 2; idx += RTHREADS) {
-        const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
-        const float2 u = cube[(zb * P + x) * PYP + y], w = cube[(zb * P + x) * PYP + y + 1];
-        __stcs(g4 + idx, make_float4(u.x, u.y, w.x, w.y));
+    if constexpr (!GL) {
+        float4* g4 = reinterpret_cast<float4*>(spec + int64_t(img0) * NB);
+        for (int idx = threadIdx.x; idx < NB / 2; idx += RTHREADS) {
+            const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+            const float2 u = cubes[(zb * P + x) * PYP + y], w = cubes[(zb * P + x) * PYP + y + 1];
+            __stcs(g4 + idx, make_float4(u.x, u.y, w.x, w.y));
+        }
+    } else {  // group layout: one NI * 8-byte piece per bin
+        float2* dst = spec + (int64_t(img0 / GRP) * NB) * GRP + (img0 % GRP);
+        for (int b = threadIdx.x; b < NB; b += RTHREADS) {
+            const int zb = b / (P * P), r = b - zb * (P * P), x = r / P, y = r - x * P;
+            float2 v[NI];
+#pragma unroll
+            for (int j = 0; j < NI; ++j) v[j] = cubes[j * CV + (zb * P + x) * PYP + y];
+            grp_put<NI>(dst + int64_t(b) * GRP, v);
+        }
     }
 }
 
-template <int P, bool UNIT>
+template <int P, int NI, bool UNIT, bool GL = (NI > 1)>
 __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restrict__ spec, cube_io a,
                                                            const float* __restrict__ bias) {
-    constexpr int Zh = P / 2 + 1, PYP = P + 1;
+    constexpr int Zh = P / 2 + 1, PYP = P + 1, CV = Zh * P * PYP, NB = Zh * P * P;
     extern __shared__ float2 sm[];
     float2* tw = sm;
-    float2* cube = tw + P;
+    float2* cubes = tw + P;
     fill_twiddles<P>(tw);
-    const int img = blockIdx.x;
-    const float4* g4 = reinterpret_cast<const float4*>(spec + int64_t(img) * (Zh * P * P));
-    constexpr int NV = Zh * P * P / 2;
-    for (int i0 = threadIdx.x; i0 < NV; i0 += 4 * RTHREADS) {
-        float4 u4[4];
+    const int img0 = blockIdx.x * NI;
+    if constexpr (!GL) {
+        const float4* g4 = reinterpret_cast<const float4*>(spec + int64_t(img0) * NB);
+        constexpr int NV = NB / 2;
+        for (int i0 = threadIdx.x; i0 < NV; i0 += 4 * RTHREADS) {
+            float4 u4[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (i0 + u * RTHREADS < NV) u4[u] = __ldcs(g4 + i0 + u * RTHREADS);
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * RTHREADS < NV) u4[u] = __ldcs(g4 + i0 + u * RTHREADS);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int idx = i0 + u * RTHREADS;
-            if (idx < NV) {
-                const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
-                cube[(zb * P + x) * PYP + y] = make_float2(u4[u].x, u4[u].y);
-                cube[(zb * P + x) * PYP + y + 1] = make_float2(u4[u].z, u4[u].w);
+            for (int u = 0; u < 4; ++u) {
+                const int idx = i0 + u * RTHREADS;
+                if (idx < NV) {
+                    const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
+                    cubes[(zb * P + x) * PYP + y] = make_float2(u4[u].x, u4[u].y);
+                    cubes[(zb * P + x) * PYP + y + 1] = make_float2(u4[u].z, u4[u].w);
+                }
+            }
+        }
+    } else {
+        const float2* src = spec + (int64_t(img0 / GRP) * NB) * GRP + (img0 % GRP);
+        for (int b0 = threadIdx.x; b0 < NB; b0 += 2 * RTHREADS) {  // two bins' loads in flight per thread
+            float2 v0[NI], v1[NI];
+            const int b1 = b0 + RTHREADS;
+            grp_get<NI>(src + int64_t(b0) * GRP, v0);
+            if (b1 < NB) grp_get<NI>(src + int64_t(b1) * GRP, v1);
+            {
+                const int zb = b0 / (P * P), r = b0 - zb * (P * P), x = r / P, y = r - x * P;
+#pragma unroll
+                for (int j = 0; j < NI; ++j) cubes[j * CV + (zb * P + x) * PYP + y] = v0[j];
+            }
+            if (b1 < NB) {
+                const int zb = b1 / (P * P), r = b1 - zb * (P * P), x = r / P, y = r - x * P;
+#pragma unroll
+                for (int j = 0; j < NI; ++j) cubes[j * CV + (zb * P + x) * PYP + y] = v1[j];
             }
         }
     }
-    phase_img pd{};
-    if (a.phased) pd = phase_decode(a.ph, img);
+    phase_img pds[NI];
+#pragma unroll
+    for (int j = 0; j < NI; ++j) pds[j] = a.phased ? phase_decode(a.ph, img0 + j) : phase_img{};
     __syncthreads();
     // x lines (columns), keep rows xs * i, i < xc
-    for (int ln = threadIdx.x; ln < Zh * P; ln += RTHREADS) {
-        const int zb = ln / P, y = ln - zb * P;
-        float2* col = cube + zb * P * PYP + y;
+    for (int ln = threadIdx.x; ln < NI * Zh * P; ln += RTHREADS) {
+        const int j = NI == 1 ? 0 : ln / (Zh * P), l1 = ln - j * (Zh * P);
+        const int zb = l1 / P, y = l1 - zb * P;
+        float2* col = cubes + j * CV + zb * P * PYP + y;
         float2 v[P];
 #pragma unroll
         for (int x = 0; x < P; ++x) v[x] = col[x * PYP];
@@ -1218,44 +1334,53 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     }
     __syncthreads();
     // y lines of the kept rows, keep columns ys * j, j < yc
-    for (int ln = threadIdx.x; ln < Zh * a.xc; ln += RTHREADS) {
-        const int zb = ln / a.xc, i = ln - zb * a.xc;
-        float2* row = cube + (zb * P + i) * PYP;
+    for (int ln = threadIdx.x; ln < NI * Zh * a.xc; ln += RTHREADS) {
+        const int j = NI == 1 ? 0 : ln / (Zh * a.xc), l2 = ln - j * (Zh * a.xc);
+        const int zb = l2 / a.xc, i = l2 - zb * a.xc;
+        float2* row = cubes + j * CV + (zb * P + i) * PYP;
         float2 v[P];
 #pragma unroll
         for (int y = 0; y < P; ++y) v[y] = row[y];
         dft_r<P, P, true>(v, tw);
         if (UNIT) {
 #pragma unroll
-            for (int j = 0; j < P; ++j)
-                if (j < a.yc) row[j] = v[j];
+            for (int jj = 0; jj < P; ++jj)
+                if (jj < a.yc) row[jj] = v[jj];
         } else {
-            for (int j = 0; j < a.yc; ++j) row[j] = v[j * a.ys];
+            for (int jj = 0; jj < a.yc; ++jj) row[jj] = v[jj * a.ys];
         }
     }
     __syncthreads();
     // z lines (C2R) of the kept (i, j), keep zs * q, q < zc; scale, bias, transfer
-    const float bv = bias ? bias[img % a.bias_mod] : 0.f;
-    for (int ln = threadIdx.x; ln < a.xc * a.yc; ln += RTHREADS) {
-        const int i = ln / a.yc, j = ln - i * a.yc;
+    const int nl3 = a.xc * a.yc;
+    for (int ln = threadIdx.x; ln < NI * nl3; ln += RTHREADS) {
+        const int j = NI == 1 ? 0 : ln / nl3, l3 = ln - j * nl3;
+        const int i = l3 / a.yc, jj = l3 - i * a.yc;
+        const int img = img0 + j;
+        const float2* cube = cubes + j * CV;
         float2 v[P];
 #pragma unroll
         for (int z = 0; z < P; ++z) {
             if (z < Zh) {
-                v[z] = cube[(z * P + i) * PYP + j];
+                v[z] = cube[(z * P + i) * PYP + jj];
             } else {  // Hermitian symmetry of a real signal
-                const float2 c = cube[((P - z) * P + i) * PYP + j];
+                const float2 c = cube[((P - z) * P + i) * PYP + jj];
                 v[z] = make_float2(c.x, -c.y);
             }
         }
         dft_r<P, P, true>(v, tw);
+        const float bv = bias ? bias[img % a.bias_mod] : 0.f;
         int64_t base;
         int z0 = 0, zst = 1, zlim = 1 << 30;
         if (a.phased) {
-            base = phase_line(a.ph, pd, i, j);
+            phase_img pd = pds[0];
+#pragma unroll
+            for (int q = 1; q < NI; ++q)
+                if (q == j) pd = pds[q];
+            base = phase_line(a.ph, pd, i, jj);
             z0 = pd.rz, zst = a.ph.sz, zlim = a.ph.nz;
         } else {
-            base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + j) * a.oz;
+            base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + jj) * a.oz;
         }
         if (base < 0) continue;
 #pragma unroll
@@ -1275,6 +1400,145 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
                 a.dst[base + z0 + zst * q] = r;
             }
         }
+    }
+}
+
+// ---- group-layout xy passes (tensor-core plans, square planes): one CTA
+// takes the z-bin plane of NI consecutive images of a group (item = (group,
+// zb, part)), loading / storing one NI * 8-byte piece per bin ----
+template <int P, int NI>
+constexpr size_t smem_xy_grp() {
+    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(line_shape<P>::XP) + size_t(NI) * P * (P + 1));
+}
+template <int P, int NI>
+__global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__ spec, int nx, int ny, int Zh) {
+    constexpr int PYP = P + 1, PV = P * PYP, H = GRP / NI;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2, XP = line_shape<P>::XP;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* pls = xbuf + LINES * XP;  // NI x [P][PYP]
+    const int64_t q = blockIdx.x;
+    const int part = int(q % H);
+    const int64_t rest = q / H;
+    const int zb = int(rest % Zh);
+    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * GRP + part * NI;
+    fill_twiddles<P>(tw);
+    for (int e = threadIdx.x; e < nx * ny; e += THREADS) {  // the valid region the z pass wrote
+        const int x = e / ny, y = e - (e / ny) * ny;
+        float2 v[NI];
+        grp_get<NI>(gq + (x * P + y) * GRP, v);
+#pragma unroll
+        for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v[j];
+    }
+    __syncthreads();
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * XP;
+    for (int r0 = 0; r0 < NI * nx; r0 += LINES) {  // rows (y transforms) of the valid rows
+        const int ln = r0 + l;
+        const bool ok = ln < NI * nx;
+        const int j = ok ? ln / nx : 0, x = ok ? ln - j * nx : 0;
+        float2* row = pls + j * PV + x * PYP;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            const int y = t + R1 * n2;
+            v[n2] = (ok && t < R1 && y < ny) ? row[y] : make_float2(0.f, 0.f);
+        }
+        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+            if (ok) row[k] = val;
+        });
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < NI * P; c0 += LINES) {  // columns (x transforms); rows >= nx are zero
+        const int ln = c0 + l;
+        const bool ok = ln < NI * P;
+        const int j = ok ? ln / P : 0, y = ok ? ln - j * P : 0;
+        float2* col = pls + j * PV + y;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) {
+            const int x = t + R1 * n2;
+            v[n2] = (ok && t < R1 && x < nx) ? col[x * PYP] : make_float2(0.f, 0.f);
+        }
+        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
+            if (ok) col[k * PYP] = val;
+        });
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * P; e += THREADS) {
+        const int x = e / P, y = e - x * P;
+        float2 v[NI];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) v[j] = pls[j * PV + x * PYP + y];
+        grp_put<NI>(gq + e * GRP, v);
+    }
+}
+
+// inverse: the group-plane piece -> compact kept blocks [xc][yc] of the NI
+// images, written image-major (plane img * Zh + zb) for the z pass
+template <int P, int NI>
+__global__ void __launch_bounds__(THREADS) fft_xy_inv_grp_k(const float2* __restrict__ spec, float2* __restrict__ out,
+                                                             int x_step, int xc, int y_step, int yc, int Zh) {
+    constexpr int PYP = P + 1, PV = P * PYP, H = GRP / NI;
+    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2, XP = line_shape<P>::XP;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* xbuf = tw + P;
+    float2* pls = xbuf + LINES * XP;
+    const int64_t q = blockIdx.x;
+    const int part = int(q % H);
+    const int64_t rest = q / H;
+    const int zb = int(rest % Zh);
+    const int64_t grp = rest / Zh;
+    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * GRP + part * NI;
+    fill_twiddles<P>(tw);
+    for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * THREADS) {
+        float2 v0[NI], v1[NI];
+        const int e1 = e0 + THREADS;
+        grp_get<NI>(gq + e0 * GRP, v0);
+        if (e1 < P * P) grp_get<NI>(gq + e1 * GRP, v1);
+        {
+            const int x = e0 / P, y = e0 - x * P;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v0[j];
+        }
+        if (e1 < P * P) {
+            const int x = e1 / P, y = e1 - x * P;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v1[j];
+        }
+    }
+    __syncthreads();
+    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
+    float2* xb = xbuf + l * XP;
+    for (int c0 = 0; c0 < NI * P; c0 += LINES) {  // column inverses, keep rows x_step * i
+        const int ln = c0 + l;
+        const bool ok = ln < NI * P;
+        const int j = ok ? ln / P : 0, y = ok ? ln - j * P : 0;
+        float2* col = pls + j * PV + y;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? col[(t + R1 * n2) * PYP] : make_float2(0.f, 0.f);
+        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+            const int i = k / x_step;
+            if (ok && i * x_step == k && i < xc) col[i * PYP] = val;
+        });
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < NI * xc; r0 += LINES) {  // row inverses of the kept rows
+        const int ln = r0 + l;
+        const bool ok = ln < NI * xc;
+        const int j = ok ? ln / xc : 0, i = ok ? ln - j * xc : 0;
+        const float2* row = pls + j * PV + i * PYP;
+        float2 v[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? row[t + R1 * n2] : make_float2(0.f, 0.f);
+        float2* o = out + ((grp * GRP + part * NI + j) * Zh + zb) * (int64_t(xc) * yc) + i * yc;
+        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
+            const int jj = k / y_step;
+            if (ok && jj * y_step == k && jj < yc) o[jj] = val;
+        });
     }
 }
 
@@ -1423,10 +1687,25 @@ __host__ __device__ constexpr int ks_planes(int P) { return KS_THREADS / (P / 2)
 // of one plane, keeps its U[a][wy..wy+1] in registers and walks the rows:
 // K[wx] = sum_a U[a] t^a with t = e(-wx sx) by Horner (one broadcast twiddle
 // load and 8 kx FMAs per 16-byte store).
+// group layout (tensor-core plans): planes ordered ((ker group * Zh + wz) *
+// GRP + t), a step takes a multiple of GRP planes, threads (plane group, column
+// pair, t) with t fastest, so a group's kernels write their group-bins together
+__device__ __forceinline__ void plane_decode(int quad, int64_t q, int Zh, int64_t& ker, int& wz) {
+    if (quad) {
+        const int64_t r = q / GRP;
+        const int64_t kq = r / Zh;
+        wz = int(r - kq * Zh);
+        ker = kq * GRP + (q % GRP);
+    } else {
+        ker = q / Zh;
+        wz = int(q - ker * Zh);
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ w, int64_t planes, int Zh, int Pz,
                                                       int kx, int ky, int kz, int sx, int sy, int sz,
-                                                      float2* __restrict__ K) {
+                                                      float2* __restrict__ K, int quad) {
     constexpr int CP = P / 2;
     constexpr int G = ks_planes(P);
     __shared__ float2 tw[P];                  // exp(-2 pi i m / P)
@@ -1444,18 +1723,27 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
         twz[m] = make_float2(cs, sn);
     }
     const int taps = kx * ky * kz, kxy = kx * ky;
-    const int g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
+    const int Gs = quad ? (G / GRP) * GRP : G;  // planes per step
+    int g, cp;
+    if (quad) {
+        const int t4 = threadIdx.x % GRP, rest = threadIdx.x / GRP;
+        cp = rest % CP;
+        g = (rest / CP) * GRP + t4;
+    } else {
+        g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
+    }
     const int mx = sx % P;
-    for (int64_t q0 = int64_t(blockIdx.x) * G; q0 < planes; q0 += int64_t(gridDim.x) * G) {
+    for (int64_t q0 = int64_t(blockIdx.x) * Gs; q0 < planes; q0 += int64_t(gridDim.x) * Gs) {
         __syncthreads();  // twiddles ready / previous planes' U consumed
         // T[g][a][b] = sum_c w[a][b][c] e(-wz c sz)
-        for (int t = threadIdx.x; t < G * kxy; t += KS_THREADS) {
+        for (int t = threadIdx.x; t < Gs * kxy; t += KS_THREADS) {
             const int gg = t / kxy, ab = t - gg * kxy;
             const int64_t q = q0 + gg;
             float2 acc = make_float2(0.f, 0.f);
             if (q < planes) {
-                const int64_t ker = q / Zh;
-                const int wz = int(q - ker * Zh);
+                int64_t ker;
+                int wz;
+                plane_decode(quad, q, Zh, ker, wz);
                 const float* wk = w + ker * taps + ab * kz;
                 const int mz = (wz * sz) % Pz;
                 int m = 0;
@@ -1472,7 +1760,7 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
         }
         __syncthreads();
         // U[g][a][wy] = sum_b T[g][a][b] e(-wy b sy), two columns per entry
-        for (int t = threadIdx.x; t < G * kx * CP; t += KS_THREADS) {
+        for (int t = threadIdx.x; t < Gs * kx * CP; t += KS_THREADS) {
             const int gg = t / (kx * CP), r = t - gg * (kx * CP), a = r / CP, pr = r - (r / CP) * CP;
             const int my0 = (2 * pr * sy) % P, my1 = ((2 * pr + 1) * sy) % P;
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1490,11 +1778,18 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
         }
         __syncthreads();
         const int64_t q = q0 + g;
-        if (g < G && q < planes) {
+        if (g < Gs && q < planes) {
             float4 u[KMAX];
 #pragma unroll
             for (int a = 0; a < KMAX; ++a) u[a] = a < kx ? U[(g * KMAX + a) * CP + cp] : make_float4(0.f, 0.f, 0.f, 0.f);
             float4* out = reinterpret_cast<float4*>(K + q * (int64_t(P) * P)) + cp;
+            float2* outq = nullptr;  // group: bin (wx, 2 cp) of kernel ker at ((ker / GRP) bins + bin) GRP + ker % GRP
+            if (quad) {
+                int64_t ker;
+                int wz;
+                plane_decode(quad, q, Zh, ker, wz);
+                outq = K + ((ker / GRP) * int64_t(Zh) * P * P + int64_t(wz) * P * P + 2 * cp) * GRP + (ker % GRP);
+            }
             int m = 0;
             for (int wx = 0; wx < P; ++wx) {
                 const float2 t = tw[m];
@@ -1514,7 +1809,12 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
                     case 2: acc = hs(acc, u[1]); [[fallthrough]];
                     default: acc = hs(acc, u[0]);
                 }
-                __stcs(out + wx * CP, acc);
+                if (quad) {
+                    __stcs(outq + wx * P * GRP, make_float2(acc.x, acc.y));
+                    __stcs(outq + wx * P * GRP + GRP, make_float2(acc.z, acc.w));
+                } else {
+                    __stcs(out + wx * CP, acc);
+                }
                 m += mx;
                 if (m >= P) m -= P;
             }
@@ -1529,7 +1829,8 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
 // products over the columns. out: compact [plane][a][b].
 template <int P>
 __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __restrict__ DK, int64_t planes, int kx,
-                                                         int ky, int sx, int sy, float2* __restrict__ out) {
+                                                         int ky, int sx, int sy, float2* __restrict__ out, int Zh,
+                                                         int quad) {
     constexpr int CP = P / 2;                  // column pairs per plane
     constexpr int G = ks_planes(P);            // planes per CTA step
     __shared__ float2 tw[P];                   // exp(-2 pi i m / P); the inverse uses conj
@@ -1553,13 +1854,28 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
             const int b = t / P, wy = t - (t / P) * P;
             twb[t] = tw[(wy * ((b * sy) % P)) % P];
         }
-    const int g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
+    const int Gs = quad ? (G / GRP) * GRP : G;  // planes per step (group layout: see kspec_k)
+    int g, cp;
+    if (quad) {
+        const int t4 = threadIdx.x % GRP, rest = threadIdx.x / GRP;
+        cp = rest % CP;
+        g = (rest / CP) * GRP + t4;
+    } else {
+        g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t q0 = int64_t(blockIdx.x) * G; q0 < planes; q0 += int64_t(gridDim.x) * G) {
+    for (int64_t q0 = int64_t(blockIdx.x) * Gs; q0 < planes; q0 += int64_t(gridDim.x) * Gs) {
         __syncthreads();  // tables ready / previous W consumed
         const int64_t q = q0 + g;
-        if (g < G && q < planes) {
+        if (g < Gs && q < planes) {
             const float4* src = reinterpret_cast<const float4*>(DK + q * (int64_t(P) * P)) + cp;
+            const float2* srcq = nullptr;
+            if (quad) {
+                int64_t ker;
+                int zb;
+                plane_decode(quad, q, Zh, ker, zb);
+                srcq = DK + ((ker / GRP) * int64_t(Zh) * P * P + int64_t(zb) * P * P + 2 * cp) * GRP + (ker % GRP);
+            }
             float4 acc[KMAX];
 #pragma unroll
             for (int a = 0; a < KMAX; ++a) acc[a] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1569,7 +1885,14 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
             for (int wx0 = 0; wx0 < P; wx0 += RG) {
                 float4 vr[RG];
 #pragma unroll
-                for (int j = 0; j < RG; ++j) vr[j] = __ldcs(src + (wx0 + j) * CP);
+                for (int j = 0; j < RG; ++j) {
+                    if (quad) {
+                        const float2 a0 = __ldcs(srcq + (wx0 + j) * P * GRP), a1 = __ldcs(srcq + (wx0 + j) * P * GRP + GRP);
+                        vr[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
+                    } else {
+                        vr[j] = __ldcs(src + (wx0 + j) * CP);
+                    }
+                }
 #pragma unroll
                 for (int j = 0; j < RG; ++j) {
                 const int wx = wx0 + j;
@@ -1597,10 +1920,17 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
         }
         __syncthreads();
         // outputs (g, a, b): warp dot products over wy
-        const int nout = G * kx * ky;
+        const int nout = Gs * kx * ky;
         for (int o = warp; o < nout; o += KS_THREADS / 32) {
             const int gg = o / (kx * ky), r = o - gg * (kx * ky), a = r / ky, b = r - (r / ky) * ky;
-            const int64_t qq = q0 + gg;
+            int64_t qq = q0 + gg;
+            const bool valid = qq < planes;
+            if (quad && valid) {  // compact output stays in image-major plane order (ker * Zh + zb)
+                int64_t ker;
+                int zb;
+                plane_decode(quad, qq, Zh, ker, zb);
+                qq = ker * Zh + zb;
+            }
             float2 acc = make_float2(0.f, 0.f);
             for (int wy = lane; wy < P; wy += 32) {
                 const float2 v = W[(gg * KMAX + a) * P + wy];
@@ -1612,7 +1942,7 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
                 acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
                 acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
             }
-            if (lane == 0 && qq < planes) out[qq * (kx * ky) + a * ky + b] = acc;
+            if (lane == 0 && valid) out[qq * (kx * ky) + a * ky + b] = acc;
         }
     }
 }
@@ -1905,7 +2235,7 @@ struct plan {
     bool poly = false;
     conv_shape ce;
     int64_t S = 1;
-    std::shared_ptr<znn_gpu::scratch> phase_ws;  // engine arena: phase-split tensors, then the tensor-core CMAC operands
+    std::shared_ptr<znn_gpu::scratch> phase_ws;  // engine arena: phase-split tensors (explicit split path)
     int64_t ph_bytes = 0;    // phase-split tensors (explicit split path)
     bool tc = false;         // frequency-domain sums on the tensor cores (bgemm_tc.cu)
     float2* X = nullptr;  // memo: image spectra of the layer input [B*f][bins]
@@ -2075,14 +2405,14 @@ void cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, int
 // 108-121): sum over patches and voxels of the gated gradient = the DC term,
 // here the sum over the valid (x, y) lines of the z pass's zb = 0 plane
 __global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec, int B, int fo, int64_t img_stride,
-                                                 int nx, int ny, int py, float* __restrict__ dbias) {
+                                                 int nx, int ny, int py, float* __restrict__ dbias, int quad) {
     const int o = blockIdx.x;
     double acc = 0.0;
     const int64_t per = int64_t(nx) * ny, total = int64_t(B) * per;
     for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
         const int64_t b = i / per, r = i - b * per;
         const int x = int(r / ny), y = int(r - (r / ny) * ny);
-        acc += double(spec[(b * fo + o) * img_stride + int64_t(x) * py + y].x);
+        acc += double(spec[spec_at(quad, b * fo + o, img_stride, int64_t(x) * py + y)].x);
     }
     __shared__ double red[256];
     red[threadIdx.x] = acc;
@@ -2105,23 +2435,40 @@ bool small_cube(const plan& p) {
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
                float2* spec, bool z_only = false, const float* gate = nullptr, float* dbias = nullptr,
                int64_t dmaps = 1, const phase_geom* ph = nullptr) {
+    const int quad = p.tc ? 1 : 0;  // tensor-core plans keep every spectrum in the group layout
     if (!z_only && small_cube(p)) {
         cube_io a{};
         a.src = in, a.gate = gate, a.img_stride = in_img_stride;
         a.nx = int(n.x), a.ny = int(n.y), a.nz = int(n.z);
         a.phased = ph ? 1 : 0;
         if (ph) a.ph = *ph;
+        a.quad = quad;
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
             if constexpr (PP <= REGP) {
+                if (quad) {  // group layout: NI images per CTA (use_tc keeps these plans on this path)
+                    auto run = [&](auto ni) {
+                        constexpr int NI = decltype(ni)::value;
+                        require(imgs % NI == 0, "fft: group-layout images not a multiple of the CTA's images");
+                        allow_smem(fft3_fwd_reg_k<PP, NI, true>, cube_reg_smem<PP, NI>());
+                        fft3_fwd_reg_k<PP, NI, true><<<unsigned(imgs / NI), RTHREADS, cube_reg_smem<PP, NI>(), st>>>(
+                            a, spec);
+                    };
+                    const int ni = cube_grp_ni<PP>();
+                    if (ni == 1) run(std::integral_constant<int, 1>{});
+                    else if (ni == 2) run(std::integral_constant<int, 2>{});
+                    else run(std::integral_constant<int, 4>{});
+                    return;
+                }
                 if (!std::getenv("ZNN_FFT_CUBE_LINES")) {
-                    allow_smem(fft3_fwd_reg_k<PP>, cube_reg_smem<PP>());
-                    fft3_fwd_reg_k<PP><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP>(), st>>>(a, spec);
+                    allow_smem(fft3_fwd_reg_k<PP, 1>, cube_reg_smem<PP, 1>());
+                    fft3_fwd_reg_k<PP, 1><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP, 1>(), st>>>(a, spec);
                     return;
                 }
             }
             if constexpr (PP <= SMALLP) {
+                require(!quad, "fft: group layout needs the register cube kernels (pad <= 24)");
                 allow_smem(fft3_fwd_small_k<PP>, cube_fwd_smem<PP>());
                 fft3_fwd_small_k<PP><<<unsigned(imgs), THREADS, cube_fwd_smem<PP>(), st>>>(a, spec);
             }
@@ -2129,7 +2476,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         launch_check("fft3_fwd_small");
         if (dbias) {  // the DC bin of each image's spectrum is its voxel sum
             dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y, 1, 1,
-                                                       int(p.P.y), dbias);
+                                                       int(p.P.y), dbias, quad);
             launch_check("fft_dc_bias");
         }
         return;
@@ -2142,12 +2489,12 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         allow_smem(fft_z_fwd_k<PP>, smem_for(PP));
         fft_z_fwd_k<PP><<<unsigned(ceil_div(nlines, LINES)), THREADS, smem_for(PP), st>>>(
             in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate,
-            ph ? *ph : phase_geom{}, ph ? 1 : 0);
+            ph ? *ph : phase_geom{}, ph ? 1 : 0, quad);
     });
     launch_check("fft_z_fwd");
     if (dbias) {
         dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y,
-                                                   int(n.x), int(n.y), int(p.P.y), dbias);
+                                                   int(n.x), int(n.y), int(p.P.y), dbias, quad);
         launch_check("fft_dc_bias");
     }
     if (z_only) return;
@@ -2157,6 +2504,20 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         if (p.P.x == 1) {
             allow_smem(fft_xy_fwd_k<1, PY>, smem_xy(1, PY));
             fft_xy_fwd_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(spec, planes, int(n.x), int(n.y));
+        } else if (quad) {  // group layout: XY_NI planes per CTA
+            if constexpr (PY <= 64) {
+                auto run = [&](auto ni) {
+                    constexpr int NI = decltype(ni)::value;
+                    require(planes % NI == 0, "fft: group-layout planes not a multiple of the CTA's planes");
+                    allow_smem(fft_xy_fwd_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
+                    fft_xy_fwd_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
+                        spec, int(n.x), int(n.y), int(p.Zh));
+                };
+                const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
+                if (ni == 1) run(std::integral_constant<int, 1>{});
+                else if (ni == 2) run(std::integral_constant<int, 2>{});
+                else run(std::integral_constant<int, 4>{});
+            }
         } else if (smem_pipe(PY) > size_t(220) * 1024 || !std::getenv("ZNN_FFT_XY_PIPE")) {
             // one plane per CTA, two CTAs per SM: faster than the persistent
             // double-buffered pass for the forward (c5: 9.1 vs 10.5 ms at P = 96,
@@ -2184,6 +2545,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                const phase_geom* ph = nullptr) {
     require(step.x * (cnt.x - 1) < p.P.x && step.y * (cnt.y - 1) < p.P.y && step.z * (cnt.z - 1) < p.P.z,
             "fft: kept voxels outside the padded volume");
+    const int quad = p.tc ? 1 : 0;
     if (small_cube(p)) {
         cube_io a{};
         a.dst = out, a.img_stride = out_img_stride;
@@ -2195,30 +2557,45 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         a.scale = float(1.0 / double(p.P.x * p.P.y * p.P.z));
         a.phased = ph ? 1 : 0;
         if (ph) a.ph = *ph;
+        a.quad = quad;
         require(imgs < (int64_t(1) << 31), "fft: too many images");
+        const bool unit = a.xs == 1 && a.ys == 1 && a.zs == 1;
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
+            auto go = [&](auto k, int64_t ctas, int threads, size_t sm) {
+                allow_smem(k, sm);
+                k<<<unsigned(ctas), threads, sm, st>>>(spec, a, bias);
+            };
             if constexpr (PP <= REGP) {
+                if (quad) {
+                    auto run = [&](auto ni) {
+                        constexpr int NI = decltype(ni)::value;
+                        require(imgs % NI == 0, "fft: group-layout images not a multiple of the CTA's images");
+                        if (unit)
+                            go(fft3_inv_reg_k<PP, NI, true, true>, imgs / NI, RTHREADS, cube_reg_smem<PP, NI>());
+                        else
+                            go(fft3_inv_reg_k<PP, NI, false, true>, imgs / NI, RTHREADS, cube_reg_smem<PP, NI>());
+                    };
+                    const int ni = cube_grp_ni<PP>();
+                    if (ni == 1) run(std::integral_constant<int, 1>{});
+                    else if (ni == 2) run(std::integral_constant<int, 2>{});
+                    else run(std::integral_constant<int, 4>{});
+                    return;
+                }
                 if (!std::getenv("ZNN_FFT_CUBE_LINES")) {
-                    if (a.xs == 1 && a.ys == 1 && a.zs == 1) {
-                        allow_smem(fft3_inv_reg_k<PP, true>, cube_reg_smem<PP>());
-                        fft3_inv_reg_k<PP, true><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP>(), st>>>(spec, a, bias);
-                    } else {
-                        allow_smem(fft3_inv_reg_k<PP, false>, cube_reg_smem<PP>());
-                        fft3_inv_reg_k<PP, false><<<unsigned(imgs), RTHREADS, cube_reg_smem<PP>(), st>>>(spec, a,
-                                                                                                         bias);
-                    }
+                    if (unit)
+                        go(fft3_inv_reg_k<PP, 1, true>, imgs, RTHREADS, cube_reg_smem<PP, 1>());
+                    else
+                        go(fft3_inv_reg_k<PP, 1, false>, imgs, RTHREADS, cube_reg_smem<PP, 1>());
                     return;
                 }
             }
             if constexpr (PP <= SMALLP) {
-                if (a.xs == 1 && a.ys == 1 && a.zs == 1) {
-                    allow_smem(fft3_inv_small_k<PP, true>, cube_smem<PP>());
-                    fft3_inv_small_k<PP, true><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(spec, a, bias);
-                } else {
-                    allow_smem(fft3_inv_small_k<PP, false>, cube_smem<PP>());
-                    fft3_inv_small_k<PP, false><<<unsigned(imgs), THREADS, cube_smem<PP>(), st>>>(spec, a, bias);
-                }
+                require(!quad, "fft: group layout needs the register cube kernels (pad <= 24)");
+                if (unit)
+                    go(fft3_inv_small_k<PP, true>, imgs, THREADS, cube_smem<PP>());
+                else
+                    go(fft3_inv_small_k<PP, false>, imgs, THREADS, cube_smem<PP>());
             }
         });
         launch_check("fft3_inv_small");
@@ -2232,6 +2609,20 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
             allow_smem(fft_xy_inv_k<1, PY>, smem_xy(1, PY));
             fft_xy_inv_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
+        } else if (quad) {  // group layout: XY_NI planes per CTA
+            if constexpr (PY <= 64) {
+                auto run = [&](auto ni) {
+                    constexpr int NI = decltype(ni)::value;
+                    require(planes % NI == 0, "fft: group-layout planes not a multiple of the CTA's planes");
+                    allow_smem(fft_xy_inv_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
+                    fft_xy_inv_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
+                        spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh));
+                };
+                const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
+                if (ni == 1) run(std::integral_constant<int, 1>{});
+                else if (ni == 2) run(std::integral_constant<int, 2>{});
+                else run(std::integral_constant<int, 4>{});
+            }
         } else if (smem_pipe(PY) > size_t(220) * 1024) {  // two 128^2 planes do not fit: single buffer
             allow_smem(fft_xy_inv_k<PY, PY>, smem_xy(PY, PY));
             fft_xy_inv_k<PY, PY><<<unsigned(planes), THREADS, smem_xy(PY, PY), st>>>(
@@ -2308,23 +2699,22 @@ int64_t split_bytes(const conv_shape& c0) {
 // the CMACs run as per-bin tensor-core GEMMs when every kernel-spectrum bin
 // is reused by enough images (polyphase plans: B s^3); ZNN_FFT_TC=0 keeps the
 // register-tiled FMA kernels
+// (square xy planes: the quad-layout transforms)
 bool use_tc(const conv_shape& c0) {
     const char* e = std::getenv("ZNN_FFT_TC");
     if (e && std::string(e) == "0") return false;
     const conv_shape c = effective(c0);
-    return znn_gpu::tc_cmac_supported(c.B, c.f_in, c.f_out);
+    const dims3 P = pads_for_eff(c);
+    // group-layout transforms: square xy planes; kernel-spectrum steps of >= GRP
+    // planes (P <= 64); bins per image divisible by GRP
+    const bool cube = P.x == P.z && P.x <= SMALLP && !std::getenv("ZNN_FFT_NO_CUBE");
+    if (cube && (P.x > REGP || std::getenv("ZNN_FFT_CUBE_LINES"))) return false;
+    return P.x == P.y && P.x > 1 && P.x <= 64 && (P.x * P.y * (P.z / 2 + 1)) % GRP == 0 &&
+           znn_gpu::tc_cmac_supported(c.B, c.f_in, c.f_out);
 }
 
-// the engine arena of a plan: explicit phase split tensors + tensor-core CMAC operands
-int64_t phase_bytes(const conv_shape& c0) {
-    int64_t b = split_bytes(c0);
-    if (use_tc(c0)) {
-        const conv_shape c = effective(c0);
-        const dims3 P = pads_for(c);
-        b += znn_gpu::tc_cmac_bytes(c.B, c.f_in, c.f_out, P.x * P.y * (P.z / 2 + 1));
-    }
-    return b;
-}
+// the engine arena of a plan: explicit phase split tensors
+int64_t phase_bytes(const conv_shape& c0) { return split_bytes(c0); }
 
 // the scratch-arena bytes conv_fwd / conv_bwd ask for (the larger of the two)
 int64_t workspace_bytes(const conv_shape& c0) {
@@ -2402,10 +2792,11 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
         const int64_t planes = nker * p.Zh;
         dispatch_pad(int(p.P.y), [&](auto pc) {
             constexpr int PY = decltype(pc)::value;
-            constexpr int G = ks_planes(PY);
+            constexpr int G0 = ks_planes(PY);
+            const int G = p.tc ? (G0 / GRP) * GRP : G0;
             kspec_k<PY><<<unsigned(std::min<int64_t>((planes + G - 1) / G, 148 * 8)), KS_THREADS, 0, st>>>(
                 w, planes, int(p.Zh), int(p.P.z), int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y),
-                int(c.s.z), K);
+                int(c.s.z), K, p.tc ? 1 : 0);
         });
         launch_check("fft_kspec");
         if (p.pool)
@@ -2430,11 +2821,6 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
 }  // namespace
 
 namespace {
-// tensor-core CMAC operands: the engine arena past the phase-split tensors
-void* tc_ws(plan& p) {
-    char* base = static_cast<char*>(p.phase_ws->get(p.phase_ws->capacity()));
-    return base + p.ph_bytes;
-}
 std::string lbl(const char* k, const conv_shape& c, const plan& p) {
     return std::string(k) + " f=" + std::to_string(c.f_in) + "->" + std::to_string(c.f_out) + " B=" +
            std::to_string(c.B) + " P=" + std::to_string(p.P.y) + " bins=" + std::to_string(p.bins);
@@ -2488,7 +2874,7 @@ static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     {
         znn_gpu::prof_scope ps(st, lbl("fft_cmac_fwd", c, p), cmac_bytes(c, p), cmac_flops(c, p));
         if (p.tc)
-            znn_gpu::tc_cmac_fwd(st, p.X, K, Y, c.B, c.f_in, c.f_out, p.bins, tc_ws(p));
+            znn_gpu::tc_cmac_fwd(st, p.X, K, Y, c.B, c.f_in, c.f_out, p.bins);
         else
             cmac_ss(st, p.X, K, Y, int(c.B), int(c.f_in), int(c.f_out), int64_t(c.f_in), 1, p.bins, true);
     }
@@ -2508,10 +2894,11 @@ void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c
         const int64_t planes = nker * p.Zh;
         dispatch_pad(int(p.P.y), [&](auto pc) {
             constexpr int PY = decltype(pc)::value;
-            constexpr int G = ks_planes(PY);
+            constexpr int G0 = ks_planes(PY);
+            const int G = p.tc ? (G0 / GRP) * GRP : G0;
             const int64_t steps = (planes + G - 1) / G;
             dkinv_xy_k<PY><<<unsigned(std::min<int64_t>(steps, 148 * 8)), KS_THREADS, 0, st>>>(
-                DK, planes, int(c.k.x), int(c.k.y), int(c.s.x), int(c.s.y), CB);
+                DK, planes, int(c.k.x), int(c.k.y), int(c.s.x), int(c.s.y), CB, int(p.Zh), p.tc ? 1 : 0);
         });
         launch_check("fft_dkinv_xy");
         inverse_z(st, p, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
@@ -2571,7 +2958,7 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
         {
             znn_gpu::prof_scope ps(st, lbl("fft_cmac_dgrad", c, p), cmac_bytes(c, p), cmac_flops(c, p));
             if (p.tc)
-                znn_gpu::tc_cmac_dgrad(st, G, K, DX, nB, c.f_in, c.f_out, p.bins, tc_ws(p));
+                znn_gpu::tc_cmac_dgrad(st, G, K, DX, nB, c.f_in, c.f_out, p.bins);
             else
                 cmac_ss(st, G, K, DX, int(nB), int(c.f_out), int(c.f_in), 1, int64_t(c.f_in), p.bins, false);
         }
@@ -2586,7 +2973,7 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     {
         znn_gpu::prof_scope ps(st, lbl("fft_cmac_upd", c, p), cmac_bytes(c, p), cmac_flops(c, p));
         if (p.tc)
-            znn_gpu::tc_cmac_upd(st, p.X, G, DK, nB, c.f_in, c.f_out, p.bins, tc_ws(p));
+            znn_gpu::tc_cmac_upd(st, p.X, G, DK, nB, c.f_in, c.f_out, p.bins);
         else
             cmac_upd(st, p.X, G, DK, int(nB), int(c.f_in), int(c.f_out), p.bins);
     }
