@@ -305,32 +305,30 @@ __device__ __forceinline__ uint32_t phase_pair_line(const phase_geom& G, uint32_
     return ((b * sxy + rxy) * sz + rz) * f + i;
 }
 
-// Group layout (tensor-core plans, bgemm_tc.hpp: GRP = 8 maps interleaved
-// bin by bin). "quad" flags below mean "spectra in the group layout".
-// Group line order: the GRP maps of a group are adjacent lines, so a warp's
-// transposed z-bin stores fill whole group-bins (64 bytes). Dense: line =
-// (group * pl + xy) * GRP + t. Phased: the z-phases stay adjacent inside each
-// map: line = (((g * pl + xy) * GRP + t) * sz + rz) with g = (b, rx, ry, map
-// group). Returns the image.
-constexpr int GRP = znn_gpu::kGrp;
-__device__ __forceinline__ uint32_t quad_line(uint32_t line, uint32_t pl, uint32_t* xy) {
-    const uint32_t t = line % GRP, l2 = line / GRP, qd = l2 / pl;
-    *xy = l2 - qd * pl;
-    return qd * GRP + t;
+// Row-bin-major spectra (tensor-core plans, bgemm_tc.hpp): element (img =
+// r F + c, bin) at (r bins + bin) F + c. "gF" arguments below are F for such
+// spectra and 0 for image-major ones. Line order of the z passes: the F maps
+// of a row are adjacent lines, so a warp's transposed z-bin stores are whole
+// runs of maps. Dense: line = (r * pl + xy) * F + c. Phased: the z-phases stay
+// adjacent inside each map: line = (((g * pl + xy) * F + c) * sz + rz) with
+// g = (b, rx, ry). Returns the image.
+__device__ __forceinline__ uint32_t rbm_line(uint32_t line, uint32_t pl, uint32_t F, uint32_t* xy) {
+    const uint32_t c = line % F, l2 = line / F, r = l2 / pl;
+    *xy = l2 - r * pl;
+    return r * F + c;
 }
-__device__ __forceinline__ uint32_t phase_quad_line(const phase_geom& G, uint32_t line, uint32_t pl, uint32_t* xy) {
-    const uint32_t sz = uint32_t(G.sz);
+__device__ __forceinline__ uint32_t phase_rbm_line(const phase_geom& G, uint32_t line, uint32_t pl, uint32_t* xy) {
+    const uint32_t sz = uint32_t(G.sz), F = uint32_t(G.f);
     const uint32_t rz = line % sz, l2 = line / sz;
-    const uint32_t t = l2 % GRP, l3 = l2 / GRP;
+    const uint32_t c = l2 % F, l3 = l2 / F;
     const uint32_t g = l3 / pl;
     *xy = l3 - g * pl;
-    const uint32_t fq = uint32_t(G.f) / GRP, sxy = uint32_t(G.sx * G.sy);
-    const uint32_t iq = g % fq, rest = g / fq, rxy = rest % sxy, b = rest / sxy;
-    return ((b * sxy + rxy) * sz + rz) * uint32_t(G.f) + iq * GRP + t;
+    const uint32_t sxy = uint32_t(G.sx * G.sy), rxy = g % sxy, b = g / sxy;
+    return ((b * sxy + rxy) * sz + rz) * F + c;
 }
-// float2 index of (img, bin) in a spectrum: image-major, or group layout
-__device__ __forceinline__ int64_t spec_at(int quad, int64_t img, int64_t bins, int64_t bin) {
-    return quad ? ((img / GRP) * bins + bin) * GRP + (img % GRP) : img * bins + bin;
+// float2 index of (img, bin) in a spectrum: image-major (gF = 0) or row-bin-major
+__device__ __forceinline__ int64_t spec_at(int gF, int64_t img, int64_t bins, int64_t bin) {
+    return gF ? ((img / gF) * bins + bin) * gF + (img % gF) : img * bins + bin;
 }
 
 // ---- z pass, forward (R2C): lines (img, x < nx, y < ny) of the real input,
@@ -339,7 +337,7 @@ template <int P>
 __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__ in, int64_t in_img_stride, int nx,
                                                         int ny, int nz, int64_t nlines, float2* __restrict__ spec,
                                                         int Px, int Py, const float* __restrict__ gate,
-                                                        phase_geom ph, int phased, int quad) {
+                                                        phase_geom ph, int phased, int gF) {
     constexpr int Zh = P / 2 + 1;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2;
     extern __shared__ float2 sm[];
@@ -358,9 +356,9 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
         const uint32_t pl = uint32_t(nx) * uint32_t(ny);
         uint32_t im, rr;
         if (phased) {
-            im = quad ? phase_quad_line(ph, uint32_t(line), pl, &rr) : phase_pair_line(ph, uint32_t(line), pl, &rr);
-        } else if (quad) {
-            im = quad_line(uint32_t(line), pl, &rr);
+            im = gF ? phase_rbm_line(ph, uint32_t(line), pl, &rr) : phase_pair_line(ph, uint32_t(line), pl, &rr);
+        } else if (gF) {
+            im = rbm_line(uint32_t(line), pl, uint32_t(gF), &rr);
         } else {
             im = uint32_t(line) / pl;
             rr = uint32_t(line) - im * pl;
@@ -392,7 +390,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
                 }
             }
         }
-        if (t == 0) obase[l] = spec_at(quad, im, int64_t(Zh) * Px * Py, int64_t(x) * Py + y);
+        if (t == 0) obase[l] = spec_at(gF, im, int64_t(Zh) * Px * Py, int64_t(x) * Py + y);
     }
     __syncthreads();  // twiddles
     float2* st = stash + l * (Zh + 1);
@@ -401,7 +399,7 @@ __global__ void __launch_bounds__(THREADS) fft_z_fwd_k(const float* __restrict__
     });
     __syncthreads();
     // transposed store: a warp writes one z-bin of 32 consecutive lines
-    const int64_t zstride = int64_t(Px) * Py * (quad ? GRP : 1);
+    const int64_t zstride = int64_t(Px) * Py * (gF ? gF : 1);
     for (int idx = threadIdx.x; idx < LINES * Zh; idx += THREADS) {
         const int l2 = idx % LINES, zb = idx / LINES;
         if (int64_t(blockIdx.x) * LINES + l2 < nlines) spec[obase[l2] + zb * zstride] = stash[l2 * (Zh + 1) + zb];
@@ -843,7 +841,7 @@ struct cube_io {
     float scale;
     int phased;
     phase_geom ph;
-    int quad;                // spectra in the group layout (bgemm_tc.hpp)
+    int gF;                  // row-bin-major spectra: maps per row (0: image-major)
 };
 
 template <int P>
@@ -1128,12 +1126,12 @@ constexpr int RTHREADS = 256;
 
 // NI images per CTA: NI = 1 image-major spectra; NI > 1 (tensor-core plans) the
 // NI consecutive images of a group, whose bins are NI * 8-byte pieces of the
-// group layout's group-bins (bgemm_tc.hpp): whole 16 / 32-byte pieces per bin
+// row-bin-major layout's group-bins (bgemm_tc.hpp): whole 16 / 32-byte pieces per bin
 template <int P, int NI = 1>
 constexpr size_t cube_reg_smem() {
     return sizeof(float2) * (size_t(P) + size_t(NI) * size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
 }
-// images per CTA of the group-layout cube kernels: four cubes when they fit
+// images per CTA of the row-bin-major cube kernels: four cubes when they fit
 // in ~80 KB (whole 32-byte sectors per bin), else two
 // (ZNN_FFT_GRP_NI = 1 / 2 / 4 overrides: 1 = one image per CTA, 8-byte pieces merged in L2)
 int grp_ni_env(const char* name, int dflt) {
@@ -1141,13 +1139,13 @@ int grp_ni_env(const char* name, int dflt) {
     const int v = e ? std::atoi(e) : dflt;
     return (v == 1 || v == 2 || v == 4) ? v : dflt;
 }
-// measured on c5 (in-step, four transforms per layer): P = 20 one image per
-// CTA (26.7 ms vs 30.6 / 29.1 for two / four: the 37 KB cubes keep six CTAs
-// per SM), P = 16 two (11.1 vs 12.3 / 11.3), P <= 12 four
+// measured on c5 with row-bin-major spectra (in-step, four transforms per
+// layer): four images per CTA at every pad (P = 20: 30.4 ms vs 31.0 / 37.5 for
+// one / two; P = 16: 12.1 vs 14.5 / 12.3; P = 12: 4.7 vs 4.9 for two)
 template <int P>
-int cube_grp_ni() { return grp_ni_env("ZNN_FFT_GRP_NI", P >= 20 ? 1 : (P >= 16 ? 2 : 4)); }
+int cube_grp_ni() { return grp_ni_env("ZNN_FFT_GRP_NI", 4); }
 
-// group-layout piece of NI images at one bin: NI float2 <-> NI / 2 float4
+// row-bin-major piece of NI images at one bin: NI float2 <-> NI / 2 float4
 template <int NI>
 __device__ __forceinline__ void grp_put(float2* __restrict__ dst, const float2 (&v)[NI]) {
     if constexpr (NI == 1) {
@@ -1253,14 +1251,15 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
             const float2 u = cubes[(zb * P + x) * PYP + y], w = cubes[(zb * P + x) * PYP + y + 1];
             __stcs(g4 + idx, make_float4(u.x, u.y, w.x, w.y));
         }
-    } else {  // group layout: one NI * 8-byte piece per bin
-        float2* dst = spec + (int64_t(img0 / GRP) * NB) * GRP + (img0 % GRP);
+    } else {  // row-bin-major layout: one NI * 8-byte piece per bin
+        const int F = a.gF;
+        float2* dst = spec + (int64_t(img0 / F) * NB) * F + (img0 % F);
         for (int b = threadIdx.x; b < NB; b += RTHREADS) {
             const int zb = b / (P * P), r = b - zb * (P * P), x = r / P, y = r - x * P;
             float2 v[NI];
 #pragma unroll
             for (int j = 0; j < NI; ++j) v[j] = cubes[j * CV + (zb * P + x) * PYP + y];
-            grp_put<NI>(dst + int64_t(b) * GRP, v);
+            grp_put<NI>(dst + int64_t(b) * F, v);
         }
     }
 }
@@ -1293,12 +1292,13 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
             }
         }
     } else {
-        const float2* src = spec + (int64_t(img0 / GRP) * NB) * GRP + (img0 % GRP);
+        const int F = a.gF;
+        const float2* src = spec + (int64_t(img0 / F) * NB) * F + (img0 % F);
         for (int b0 = threadIdx.x; b0 < NB; b0 += 2 * RTHREADS) {  // two bins' loads in flight per thread
             float2 v0[NI], v1[NI];
             const int b1 = b0 + RTHREADS;
-            grp_get<NI>(src + int64_t(b0) * GRP, v0);
-            if (b1 < NB) grp_get<NI>(src + int64_t(b1) * GRP, v1);
+            grp_get<NI>(src + int64_t(b0) * F, v0);
+            if (b1 < NB) grp_get<NI>(src + int64_t(b1) * F, v1);
             {
                 const int zb = b0 / (P * P), r = b0 - zb * (P * P), x = r / P, y = r - x * P;
 #pragma unroll
@@ -1403,7 +1403,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     }
 }
 
-// ---- group-layout xy passes (tensor-core plans, square planes): one CTA
+// ---- row-bin-major xy passes (tensor-core plans, square planes): one CTA
 // takes the z-bin plane of NI consecutive images of a group (item = (group,
 // zb, part)), loading / storing one NI * 8-byte piece per bin ----
 template <int P, int NI>
@@ -1411,8 +1411,10 @@ constexpr size_t smem_xy_grp() {
     return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(line_shape<P>::XP) + size_t(NI) * P * (P + 1));
 }
 template <int P, int NI>
-__global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__ spec, int nx, int ny, int Zh) {
-    constexpr int PYP = P + 1, PV = P * PYP, H = GRP / NI;
+__global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__ spec, int nx, int ny, int Zh,
+                                                             int F) {
+    constexpr int PYP = P + 1, PV = P * PYP;
+    const int H = F / NI;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2, XP = line_shape<P>::XP;
     extern __shared__ float2 sm[];
     float2* tw = sm;
@@ -1422,12 +1424,12 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__
     const int part = int(q % H);
     const int64_t rest = q / H;
     const int zb = int(rest % Zh);
-    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * GRP + part * NI;
+    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
     fill_twiddles<P>(tw);
     for (int e = threadIdx.x; e < nx * ny; e += THREADS) {  // the valid region the z pass wrote
         const int x = e / ny, y = e - (e / ny) * ny;
         float2 v[NI];
-        grp_get<NI>(gq + (x * P + y) * GRP, v);
+        grp_get<NI>(gq + (x * P + y) * F, v);
 #pragma unroll
         for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v[j];
     }
@@ -1471,7 +1473,7 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__
         float2 v[NI];
 #pragma unroll
         for (int j = 0; j < NI; ++j) v[j] = pls[j * PV + x * PYP + y];
-        grp_put<NI>(gq + e * GRP, v);
+        grp_put<NI>(gq + e * F, v);
     }
 }
 
@@ -1479,8 +1481,9 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__
 // images, written image-major (plane img * Zh + zb) for the z pass
 template <int P, int NI>
 __global__ void __launch_bounds__(THREADS) fft_xy_inv_grp_k(const float2* __restrict__ spec, float2* __restrict__ out,
-                                                             int x_step, int xc, int y_step, int yc, int Zh) {
-    constexpr int PYP = P + 1, PV = P * PYP, H = GRP / NI;
+                                                             int x_step, int xc, int y_step, int yc, int Zh, int F) {
+    constexpr int PYP = P + 1, PV = P * PYP;
+    const int H = F / NI;
     constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2, XP = line_shape<P>::XP;
     extern __shared__ float2 sm[];
     float2* tw = sm;
@@ -1491,13 +1494,13 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_grp_k(const float2* __rest
     const int64_t rest = q / H;
     const int zb = int(rest % Zh);
     const int64_t grp = rest / Zh;
-    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * GRP + part * NI;
+    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
     fill_twiddles<P>(tw);
     for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * THREADS) {
         float2 v0[NI], v1[NI];
         const int e1 = e0 + THREADS;
-        grp_get<NI>(gq + e0 * GRP, v0);
-        if (e1 < P * P) grp_get<NI>(gq + e1 * GRP, v1);
+        grp_get<NI>(gq + e0 * F, v0);
+        if (e1 < P * P) grp_get<NI>(gq + e1 * F, v1);
         {
             const int x = e0 / P, y = e0 - x * P;
 #pragma unroll
@@ -1534,7 +1537,7 @@ __global__ void __launch_bounds__(THREADS) fft_xy_inv_grp_k(const float2* __rest
         float2 v[R2];
 #pragma unroll
         for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? row[t + R1 * n2] : make_float2(0.f, 0.f);
-        float2* o = out + ((grp * GRP + part * NI + j) * Zh + zb) * (int64_t(xc) * yc) + i * yc;
+        float2* o = out + ((grp * F + part * NI + j) * Zh + zb) * (int64_t(xc) * yc) + i * yc;
         line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
             const int jj = k / y_step;
             if (ok && jj * y_step == k && jj < yc) o[jj] = val;
@@ -1687,25 +1690,30 @@ __host__ __device__ constexpr int ks_planes(int P) { return KS_THREADS / (P / 2)
 // of one plane, keeps its U[a][wy..wy+1] in registers and walks the rows:
 // K[wx] = sum_a U[a] t^a with t = e(-wx sx) by Horner (one broadcast twiddle
 // load and 8 kx FMAs per 16-byte store).
-// group layout (tensor-core plans): planes ordered ((ker group * Zh + wz) *
-// GRP + t), a step takes a multiple of GRP planes, threads (plane group, column
-// pair, t) with t fastest, so a group's kernels write their group-bins together
-__device__ __forceinline__ void plane_decode(int quad, int64_t q, int Zh, int64_t& ker, int& wz) {
-    if (quad) {
-        const int64_t r = q / GRP;
-        const int64_t kq = r / Zh;
-        wz = int(r - kq * Zh);
-        ker = kq * GRP + (q % GRP);
+// row-bin-major kernel spectra (tensor-core plans, ker = o F + i): planes
+// ordered ((o * Zh + wz) * F + i), threads (column pair, plane) with the plane
+// fastest, so consecutive maps i of one (o, wz) write their shared runs together
+__device__ __forceinline__ void plane_decode(int gF, int64_t q, int Zh, int64_t& ker, int& wz) {
+    if (gF) {
+        const int64_t r = q / gF;
+        const int64_t o = r / Zh;
+        wz = int(r - o * Zh);
+        ker = o * gF + (q % gF);
     } else {
         ker = q / Zh;
         wz = int(q - ker * Zh);
     }
 }
+// float2 index of bin (wz, wx = 0, wy) of kernel ker = o F + i (row-bin-major)
+__device__ __forceinline__ int64_t kspec_rbm(int gF, int64_t ker, int Zh, int P, int wz, int wy) {
+    const int64_t o = ker / gF, i = ker - o * gF;
+    return ((o * Zh + wz) * int64_t(P) * P + wy) * gF + i;
+}
 
 template <int P>
 __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ w, int64_t planes, int Zh, int Pz,
                                                       int kx, int ky, int kz, int sx, int sy, int sz,
-                                                      float2* __restrict__ K, int quad) {
+                                                      float2* __restrict__ K, int gF) {
     constexpr int CP = P / 2;
     constexpr int G = ks_planes(P);
     __shared__ float2 tw[P];                  // exp(-2 pi i m / P)
@@ -1723,12 +1731,12 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
         twz[m] = make_float2(cs, sn);
     }
     const int taps = kx * ky * kz, kxy = kx * ky;
-    const int Gs = quad ? (G / GRP) * GRP : G;  // planes per step
+    // planes per step: row-bin-major steps take a multiple of 8 consecutive maps
+    // (aligned runs of whole sectors; F is a multiple of 8)
+    const int Gs = gF ? (G / 8) * 8 : G;
     int g, cp;
-    if (quad) {
-        const int t4 = threadIdx.x % GRP, rest = threadIdx.x / GRP;
-        cp = rest % CP;
-        g = (rest / CP) * GRP + t4;
+    if (gF) {
+        g = threadIdx.x % Gs, cp = threadIdx.x / Gs;
     } else {
         g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
     }
@@ -1743,7 +1751,7 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
             if (q < planes) {
                 int64_t ker;
                 int wz;
-                plane_decode(quad, q, Zh, ker, wz);
+                plane_decode(gF, q, Zh, ker, wz);
                 const float* wk = w + ker * taps + ab * kz;
                 const int mz = (wz * sz) % Pz;
                 int m = 0;
@@ -1778,17 +1786,17 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
         }
         __syncthreads();
         const int64_t q = q0 + g;
-        if (g < Gs && q < planes) {
+        if (g < Gs && cp < CP && q < planes) {
             float4 u[KMAX];
 #pragma unroll
             for (int a = 0; a < KMAX; ++a) u[a] = a < kx ? U[(g * KMAX + a) * CP + cp] : make_float4(0.f, 0.f, 0.f, 0.f);
             float4* out = reinterpret_cast<float4*>(K + q * (int64_t(P) * P)) + cp;
-            float2* outq = nullptr;  // group: bin (wx, 2 cp) of kernel ker at ((ker / GRP) bins + bin) GRP + ker % GRP
-            if (quad) {
+            float2* outq = nullptr;  // row-bin-major: bin (wx, 2 cp) of this kernel
+            if (gF) {
                 int64_t ker;
                 int wz;
-                plane_decode(quad, q, Zh, ker, wz);
-                outq = K + ((ker / GRP) * int64_t(Zh) * P * P + int64_t(wz) * P * P + 2 * cp) * GRP + (ker % GRP);
+                plane_decode(gF, q, Zh, ker, wz);
+                outq = K + kspec_rbm(gF, ker, Zh, P, wz, 2 * cp);
             }
             int m = 0;
             for (int wx = 0; wx < P; ++wx) {
@@ -1809,9 +1817,9 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
                     case 2: acc = hs(acc, u[1]); [[fallthrough]];
                     default: acc = hs(acc, u[0]);
                 }
-                if (quad) {
-                    __stcs(outq + wx * P * GRP, make_float2(acc.x, acc.y));
-                    __stcs(outq + wx * P * GRP + GRP, make_float2(acc.z, acc.w));
+                if (gF) {
+                    __stcs(outq + int64_t(wx) * P * gF, make_float2(acc.x, acc.y));
+                    __stcs(outq + int64_t(wx) * P * gF + gF, make_float2(acc.z, acc.w));
                 } else {
                     __stcs(out + wx * CP, acc);
                 }
@@ -1830,7 +1838,7 @@ __global__ void __launch_bounds__(KS_THREADS) kspec_k(const float* __restrict__ 
 template <int P>
 __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __restrict__ DK, int64_t planes, int kx,
                                                          int ky, int sx, int sy, float2* __restrict__ out, int Zh,
-                                                         int quad) {
+                                                         int gF) {
     constexpr int CP = P / 2;                  // column pairs per plane
     constexpr int G = ks_planes(P);            // planes per CTA step
     __shared__ float2 tw[P];                   // exp(-2 pi i m / P); the inverse uses conj
@@ -1854,12 +1862,10 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
             const int b = t / P, wy = t - (t / P) * P;
             twb[t] = tw[(wy * ((b * sy) % P)) % P];
         }
-    const int Gs = quad ? (G / GRP) * GRP : G;  // planes per step (group layout: see kspec_k)
+    const int Gs = gF ? (G / 8) * 8 : G;  // planes per step (row-bin-major: see kspec_k)
     int g, cp;
-    if (quad) {
-        const int t4 = threadIdx.x % GRP, rest = threadIdx.x / GRP;
-        cp = rest % CP;
-        g = (rest / CP) * GRP + t4;
+    if (gF) {
+        g = threadIdx.x % Gs, cp = threadIdx.x / Gs;
     } else {
         g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
     }
@@ -1867,14 +1873,14 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
     for (int64_t q0 = int64_t(blockIdx.x) * Gs; q0 < planes; q0 += int64_t(gridDim.x) * Gs) {
         __syncthreads();  // tables ready / previous W consumed
         const int64_t q = q0 + g;
-        if (g < Gs && q < planes) {
+        if (g < Gs && cp < CP && q < planes) {
             const float4* src = reinterpret_cast<const float4*>(DK + q * (int64_t(P) * P)) + cp;
             const float2* srcq = nullptr;
-            if (quad) {
+            if (gF) {
                 int64_t ker;
                 int zb;
-                plane_decode(quad, q, Zh, ker, zb);
-                srcq = DK + ((ker / GRP) * int64_t(Zh) * P * P + int64_t(zb) * P * P + 2 * cp) * GRP + (ker % GRP);
+                plane_decode(gF, q, Zh, ker, zb);
+                srcq = DK + kspec_rbm(gF, ker, Zh, P, zb, 2 * cp);
             }
             float4 acc[KMAX];
 #pragma unroll
@@ -1886,8 +1892,9 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
                 float4 vr[RG];
 #pragma unroll
                 for (int j = 0; j < RG; ++j) {
-                    if (quad) {
-                        const float2 a0 = __ldcs(srcq + (wx0 + j) * P * GRP), a1 = __ldcs(srcq + (wx0 + j) * P * GRP + GRP);
+                    if (gF) {
+                        const float2 a0 = __ldcs(srcq + int64_t(wx0 + j) * P * gF),
+                                     a1 = __ldcs(srcq + int64_t(wx0 + j) * P * gF + gF);
                         vr[j] = make_float4(a0.x, a0.y, a1.x, a1.y);
                     } else {
                         vr[j] = __ldcs(src + (wx0 + j) * CP);
@@ -1925,10 +1932,10 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
             const int gg = o / (kx * ky), r = o - gg * (kx * ky), a = r / ky, b = r - (r / ky) * ky;
             int64_t qq = q0 + gg;
             const bool valid = qq < planes;
-            if (quad && valid) {  // compact output stays in image-major plane order (ker * Zh + zb)
+            if (gF && valid) {  // compact output stays in image-major plane order (ker * Zh + zb)
                 int64_t ker;
                 int zb;
-                plane_decode(quad, qq, Zh, ker, zb);
+                plane_decode(gF, qq, Zh, ker, zb);
                 qq = ker * Zh + zb;
             }
             float2 acc = make_float2(0.f, 0.f);
@@ -2405,14 +2412,14 @@ void cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, int
 // 108-121): sum over patches and voxels of the gated gradient = the DC term,
 // here the sum over the valid (x, y) lines of the z pass's zb = 0 plane
 __global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec, int B, int fo, int64_t img_stride,
-                                                 int nx, int ny, int py, float* __restrict__ dbias, int quad) {
+                                                 int nx, int ny, int py, float* __restrict__ dbias, int gF) {
     const int o = blockIdx.x;
     double acc = 0.0;
     const int64_t per = int64_t(nx) * ny, total = int64_t(B) * per;
     for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
         const int64_t b = i / per, r = i - b * per;
         const int x = int(r / ny), y = int(r - (r / ny) * ny);
-        acc += double(spec[spec_at(quad, b * fo + o, img_stride, int64_t(x) * py + y)].x);
+        acc += double(spec[spec_at(gF, b * fo + o, img_stride, int64_t(x) * py + y)].x);
     }
     __shared__ double red[256];
     red[threadIdx.x] = acc;
@@ -2434,23 +2441,25 @@ bool small_cube(const plan& p) {
 // cubes only): read in place, no split pass
 void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_stride, dims3 n, int64_t imgs,
                float2* spec, bool z_only = false, const float* gate = nullptr, float* dbias = nullptr,
-               int64_t dmaps = 1, const phase_geom* ph = nullptr) {
-    const int quad = p.tc ? 1 : 0;  // tensor-core plans keep every spectrum in the group layout
+               int64_t dmaps = 1, const phase_geom* ph = nullptr, int64_t maps = 0) {
+    // tensor-core plans keep every spectrum row-bin-major with F = maps
+    const int quad = p.tc ? int(maps) : 0;
+    require(!p.tc || (maps > 0 && imgs % maps == 0), "fft: row-bin-major spectrum needs its map count");
     if (!z_only && small_cube(p)) {
         cube_io a{};
         a.src = in, a.gate = gate, a.img_stride = in_img_stride;
         a.nx = int(n.x), a.ny = int(n.y), a.nz = int(n.z);
         a.phased = ph ? 1 : 0;
         if (ph) a.ph = *ph;
-        a.quad = quad;
+        a.gF = quad;
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
             if constexpr (PP <= REGP) {
-                if (quad) {  // group layout: NI images per CTA (use_tc keeps these plans on this path)
+                if (quad) {  // row-bin-major: NI images per CTA (use_tc keeps these plans on this path)
                     auto run = [&](auto ni) {
                         constexpr int NI = decltype(ni)::value;
-                        require(imgs % NI == 0, "fft: group-layout images not a multiple of the CTA's images");
+                        require(imgs % NI == 0, "fft: row-bin-major images not a multiple of the CTA's images");
                         allow_smem(fft3_fwd_reg_k<PP, NI, true>, cube_reg_smem<PP, NI>());
                         fft3_fwd_reg_k<PP, NI, true><<<unsigned(imgs / NI), RTHREADS, cube_reg_smem<PP, NI>(), st>>>(
                             a, spec);
@@ -2468,7 +2477,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
                 }
             }
             if constexpr (PP <= SMALLP) {
-                require(!quad, "fft: group layout needs the register cube kernels (pad <= 24)");
+                require(!quad, "fft: row-bin-major layout needs the register cube kernels (pad <= 24)");
                 allow_smem(fft3_fwd_small_k<PP>, cube_fwd_smem<PP>());
                 fft3_fwd_small_k<PP><<<unsigned(imgs), THREADS, cube_fwd_smem<PP>(), st>>>(a, spec);
             }
@@ -2504,14 +2513,14 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         if (p.P.x == 1) {
             allow_smem(fft_xy_fwd_k<1, PY>, smem_xy(1, PY));
             fft_xy_fwd_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(spec, planes, int(n.x), int(n.y));
-        } else if (quad) {  // group layout: XY_NI planes per CTA
+        } else if (quad) {  // row-bin-major layout: XY_NI planes per CTA
             if constexpr (PY <= 64) {
                 auto run = [&](auto ni) {
                     constexpr int NI = decltype(ni)::value;
-                    require(planes % NI == 0, "fft: group-layout planes not a multiple of the CTA's planes");
+                    require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
                     allow_smem(fft_xy_fwd_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
                     fft_xy_fwd_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
-                        spec, int(n.x), int(n.y), int(p.Zh));
+                        spec, int(n.x), int(n.y), int(p.Zh), quad);
                 };
                 const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
                 if (ni == 1) run(std::integral_constant<int, 1>{});
@@ -2542,10 +2551,11 @@ void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 c
 // cbuf holds the compact kept planes between the two passes
 void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs, dims3 step, dims3 cnt, float* out,
                int64_t out_img_stride, const float* bias, int bias_mod, int act, float2* cbuf,
-               const phase_geom* ph = nullptr) {
+               const phase_geom* ph = nullptr, int64_t maps = 0) {
     require(step.x * (cnt.x - 1) < p.P.x && step.y * (cnt.y - 1) < p.P.y && step.z * (cnt.z - 1) < p.P.z,
             "fft: kept voxels outside the padded volume");
-    const int quad = p.tc ? 1 : 0;
+    const int quad = p.tc ? int(maps) : 0;  // row-bin-major spectra: F = maps
+    require(!p.tc || (maps > 0 && imgs % maps == 0), "fft: row-bin-major spectrum needs its map count");
     if (small_cube(p)) {
         cube_io a{};
         a.dst = out, a.img_stride = out_img_stride;
@@ -2557,7 +2567,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         a.scale = float(1.0 / double(p.P.x * p.P.y * p.P.z));
         a.phased = ph ? 1 : 0;
         if (ph) a.ph = *ph;
-        a.quad = quad;
+        a.gF = quad;
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         const bool unit = a.xs == 1 && a.ys == 1 && a.zs == 1;
         dispatch_pad(int(p.P.x), [&](auto pc) {
@@ -2570,7 +2580,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                 if (quad) {
                     auto run = [&](auto ni) {
                         constexpr int NI = decltype(ni)::value;
-                        require(imgs % NI == 0, "fft: group-layout images not a multiple of the CTA's images");
+                        require(imgs % NI == 0, "fft: row-bin-major images not a multiple of the CTA's images");
                         if (unit)
                             go(fft3_inv_reg_k<PP, NI, true, true>, imgs / NI, RTHREADS, cube_reg_smem<PP, NI>());
                         else
@@ -2591,7 +2601,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                 }
             }
             if constexpr (PP <= SMALLP) {
-                require(!quad, "fft: group layout needs the register cube kernels (pad <= 24)");
+                require(!quad, "fft: row-bin-major layout needs the register cube kernels (pad <= 24)");
                 if (unit)
                     go(fft3_inv_small_k<PP, true>, imgs, THREADS, cube_smem<PP>());
                 else
@@ -2609,14 +2619,14 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
             allow_smem(fft_xy_inv_k<1, PY>, smem_xy(1, PY));
             fft_xy_inv_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
-        } else if (quad) {  // group layout: XY_NI planes per CTA
+        } else if (quad) {  // row-bin-major layout: XY_NI planes per CTA
             if constexpr (PY <= 64) {
                 auto run = [&](auto ni) {
                     constexpr int NI = decltype(ni)::value;
-                    require(planes % NI == 0, "fft: group-layout planes not a multiple of the CTA's planes");
+                    require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
                     allow_smem(fft_xy_inv_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
                     fft_xy_inv_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
-                        spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh));
+                        spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
                 };
                 const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
                 if (ni == 1) run(std::integral_constant<int, 1>{});
@@ -2699,18 +2709,15 @@ int64_t split_bytes(const conv_shape& c0) {
 // the CMACs run as per-bin tensor-core GEMMs when every kernel-spectrum bin
 // is reused by enough images (polyphase plans: B s^3); ZNN_FFT_TC=0 keeps the
 // register-tiled FMA kernels
-// (square xy planes: the quad-layout transforms)
+// (square xy planes of at most 64: the row-bin-major transforms)
 bool use_tc(const conv_shape& c0) {
     const char* e = std::getenv("ZNN_FFT_TC");
     if (e && std::string(e) == "0") return false;
     const conv_shape c = effective(c0);
     const dims3 P = pads_for_eff(c);
-    // group-layout transforms: square xy planes; kernel-spectrum steps of >= GRP
-    // planes (P <= 64); bins per image divisible by GRP
     const bool cube = P.x == P.z && P.x <= SMALLP && !std::getenv("ZNN_FFT_NO_CUBE");
     if (cube && (P.x > REGP || std::getenv("ZNN_FFT_CUBE_LINES"))) return false;
-    return P.x == P.y && P.x > 1 && P.x <= 64 && (P.x * P.y * (P.z / 2 + 1)) % GRP == 0 &&
-           znn_gpu::tc_cmac_supported(c.B, c.f_in, c.f_out);
+    return P.x == P.y && P.x > 1 && P.x <= 64 && znn_gpu::tc_cmac_supported(c.B, c.f_in, c.f_out);
 }
 
 // the engine arena of a plan: explicit phase split tensors
@@ -2793,10 +2800,10 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
         dispatch_pad(int(p.P.y), [&](auto pc) {
             constexpr int PY = decltype(pc)::value;
             constexpr int G0 = ks_planes(PY);
-            const int G = p.tc ? (G0 / GRP) * GRP : G0;
+            const int G = p.tc ? (G0 / 8) * 8 : G0;
             kspec_k<PY><<<unsigned(std::min<int64_t>((planes + G - 1) / G, 148 * 8)), KS_THREADS, 0, st>>>(
                 w, planes, int(p.Zh), int(p.P.z), int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y),
-                int(c.s.z), K, p.tc ? 1 : 0);
+                int(c.s.z), K, p.tc ? int(c.f_in) : 0);
         });
         launch_check("fft_kspec");
         if (p.pool)
@@ -2811,7 +2818,7 @@ void kernel_spectra(cudaStream_t st, plan& p, const conv_shape& c, const float* 
     dilate_k<<<unsigned(std::min<int64_t>(ceil_div(ntaps, 256), 148 * 16)), 256, 0, st>>>(
         w, ntaps, int(c.k.x), int(c.k.y), int(c.k.z), int(c.s.x), int(c.s.y), int(c.s.z), p.dil);
     launch_check("fft_dilate");
-    forward3d(st, p, p.dil, e.vol(), e, nker, K);
+    forward3d(st, p, p.dil, e.vol(), e, nker, K, false, nullptr, nullptr, 1, nullptr, c.f_in);
     if (p.pool)
         p.pool->owner = &p;
     else
@@ -2839,7 +2846,7 @@ static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     // image spectra (memoised for the backward / update passes)
     {
         znn_gpu::prof_scope ps(st, lbl("fft_image_fwd", c, p), double(c.B * c.f_in) * (4.0 * c.n.vol() + 8.0 * p.bins), 0);
-        forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X, false, nullptr, nullptr, 1, ph_in);
+        forward3d(st, p, x, c.n.vol(), c.n, c.B * c.f_in, p.X, false, nullptr, nullptr, 1, ph_in, c.f_in);
     }
     p.cnt.fwd_image += c.B * c.f_in;
     // kernel spectra of the dilated kernels (memoised for the backward pass)
@@ -2881,7 +2888,8 @@ static void conv_fwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     launch_check("fft_cmac_fwd");
     {
         znn_gpu::prof_scope ps(st, lbl("fft_image_inv", c, p), double(c.B * c.f_out) * (8.0 * p.bins + 4.0 * c.m.vol()), 0);
-        inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB, ph_out);
+        inverse3d(st, p, Y, c.B * c.f_out, dims3{1, 1, 1}, c.m, y, c.m.vol(), bias, int(c.f_out), act, CB, ph_out,
+                  c.f_out);
     }
     p.cnt.fwd_inverse += c.B * c.f_out;
 }
@@ -2895,16 +2903,16 @@ void kernel_gradient_inverse(cudaStream_t st, const plan& p, const conv_shape& c
         dispatch_pad(int(p.P.y), [&](auto pc) {
             constexpr int PY = decltype(pc)::value;
             constexpr int G0 = ks_planes(PY);
-            const int G = p.tc ? (G0 / GRP) * GRP : G0;
+            const int G = p.tc ? (G0 / 8) * 8 : G0;
             const int64_t steps = (planes + G - 1) / G;
             dkinv_xy_k<PY><<<unsigned(std::min<int64_t>(steps, 148 * 8)), KS_THREADS, 0, st>>>(
-                DK, planes, int(c.k.x), int(c.k.y), int(c.s.x), int(c.s.y), CB, int(p.Zh), p.tc ? 1 : 0);
+                DK, planes, int(c.k.x), int(c.k.y), int(c.s.x), int(c.s.y), CB, int(p.Zh), p.tc ? int(c.f_in) : 0);
         });
         launch_check("fft_dkinv_xy");
         inverse_z(st, p, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
         return;
     }
-    inverse3d(st, p, DK, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB);
+    inverse3d(st, p, DK, nker, c.s, c.k, gw, c.taps(), nullptr, 1, 3, CB, nullptr, c.f_in);
 }
 
 static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const float* g, const float* w, float* gw,
@@ -2951,7 +2959,7 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
     }
     {
         znn_gpu::prof_scope ps(st, lbl("fft_grad_fwd", c, p), double(nB * c.f_out) * (4.0 * c.m.vol() + 8.0 * p.bins), 0);
-        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out, ph_g);
+        forward3d(st, p, g, c.m.vol(), c.m, nB * c.f_out, G, false, relu_y, dbias, c.f_out, ph_g, c.f_out);
     }
     p.cnt.bwd_image += nB * c.f_out;
     if (gin) {
@@ -2965,7 +2973,7 @@ static void conv_bwd_core(cudaStream_t st, plan& p, const conv_shape& c, const f
         launch_check("fft_cmac_bwd");
         {
             znn_gpu::prof_scope ps(st, lbl("fft_dgrad_inv", c, p), double(nB * c.f_in) * (8.0 * p.bins + 4.0 * c.n.vol()), 0);
-            inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB, ph_dx);
+            inverse3d(st, p, DX, nB * c.f_in, dims3{1, 1, 1}, c.n, gin, c.n.vol(), nullptr, 1, 3, CB, ph_dx, c.f_in);
         }
         p.cnt.bwd_inverse += nB * c.f_in;
     }
