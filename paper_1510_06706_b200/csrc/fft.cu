@@ -554,6 +554,14 @@ __device__ __forceinline__ void cp_async16p(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// 4-byte async copy, zero-filled when !ok
+__device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, bool ok) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(gmem), "r"(ok ? 4 : 0) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
@@ -1654,6 +1662,208 @@ __global__ void __launch_bounds__(THREADS) fft_z_inv_k(const float2* __restrict_
     });
 }
 
+// ---- z passes with one line PAIR per thread (pads 40..64): two real lines
+// are the real and imaginary parts of one complex P-point FFT held in
+// registers (Hermitian split / merge), so there is no exchange buffer, no
+// warp sync and half the arithmetic of a complex transform per real line.
+// A warp owns 64 consecutive lines (lane l: lines l and l + 32); the global
+// side goes through a per-warp staging tile so loads and stores are
+// warp-cooperative along z (the per-thread lines are far apart in memory). ----
+constexpr int ZR_THREADS = 128;
+constexpr int ZR_LINES = 2 * ZR_THREADS;
+__host__ __device__ constexpr int zr_pitch(int P) { return (P % 2) ? P : P + 1; }  // odd: conflict-free rows
+template <int P>
+constexpr size_t zr_smem(bool gated = false) { return sizeof(float) * size_t(ZR_LINES) * size_t(zr_pitch(P)) * (gated ? 2 : 1); }
+
+template <int P>
+__global__ void __launch_bounds__(ZR_THREADS) fft_z_fwd_reg_k(const float* __restrict__ in, int64_t in_img_stride,
+                                                              int nx, int ny, int nz, int64_t nlines,
+                                                              float2* __restrict__ spec, int Px, int Py,
+                                                              const float* __restrict__ gate, phase_geom ph,
+                                                              int phased, int gF) {
+    constexpr int Zh = P / 2 + 1, SP = zr_pitch(P);
+    __shared__ float2 tw[P];
+    __shared__ int64_t obase[ZR_LINES];
+    extern __shared__ float stage[];  // [ZR_LINES][SP]
+    fill_twiddles<P>(tw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t wl0 = int64_t(blockIdx.x) * ZR_LINES + warp * 64;  // this warp's first line
+    float* wst = stage + warp * 64 * SP;
+    const uint32_t pl = uint32_t(nx) * uint32_t(ny);
+    // each lane decodes its two lines (lane, lane + 32): source offset (-1: none),
+    // first z, z stride and z limit
+    int64_t soff[2];
+    int sz0[2], szs[2], szl[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int l = lane + 32 * h;
+        const int64_t line = wl0 + l;
+        soff[h] = -1, sz0[h] = 0, szs[h] = 1, szl[h] = 0;
+        int64_t ob = -1;
+        if (line < nlines) {  // 32-bit decode, as fft_z_fwd_k
+            uint32_t im, rr;
+            if (phased) {
+                im = gF ? phase_rbm_line(ph, uint32_t(line), pl, &rr) : phase_pair_line(ph, uint32_t(line), pl, &rr);
+            } else if (gF) {
+                im = rbm_line(uint32_t(line), pl, uint32_t(gF), &rr);
+            } else {
+                im = uint32_t(line) / pl;
+                rr = uint32_t(line) - im * pl;
+            }
+            const int r = int(rr), x = r / ny, y = r - (r / ny) * ny;
+            soff[h] = int64_t(im) * in_img_stride + (int64_t(x) * ny + y) * nz;
+            szl[h] = nz;
+            if (phased) {
+                const phase_img pd = phase_decode(ph, int(im));
+                soff[h] = phase_line(ph, pd, x, y);
+                sz0[h] = pd.rz, szs[h] = ph.sz, szl[h] = soff[h] >= 0 ? ph.nz : 0;
+            }
+            ob = spec_at(gF, im, int64_t(Zh) * Px * Py, int64_t(x) * Py + y);
+        }
+        obase[warp * 64 + l] = ob;
+    }
+    // warp-cooperative async copies into the staging tile (lanes along z, zero
+    // fill past the line), every line of the warp in flight at once; line l's
+    // parameters come from lane l % 32. With a gate the gate values go to a
+    // second tile.
+    constexpr int NJ = (P + 31) / 32;
+    float* gst = gate ? stage + ZR_LINES * SP : nullptr;
+    for (int l = 0; l < 64; ++l) {
+        const int src = l & 31;
+        const bool hi = l >= 32;  // (uniform)
+        const int64_t off = __shfl_sync(0xffffffffu, hi ? soff[1] : soff[0], src);
+        const int z0 = __shfl_sync(0xffffffffu, hi ? sz0[1] : sz0[0], src);
+        const int zs = __shfl_sync(0xffffffffu, hi ? szs[1] : szs[0], src);
+        const int zl = __shfl_sync(0xffffffffu, hi ? szl[1] : szl[0], src);
+#pragma unroll
+        for (int jj = 0; jj < NJ; ++jj) {
+            const int j = jj * 32 + lane, z = z0 + zs * j;
+            if (j < P) {
+                const bool ok = off >= 0 && j < nz && z < zl;
+                const int64_t e = ok ? off + z : 0;
+                cp_async4z(wst + l * SP + j, in + e, ok);
+                if (gate) cp_async4z(gst + (warp * 64 + l) * SP + j, gate + e, ok);
+            }
+        }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();  // twiddles, obase
+    float2 v[P];
+    {
+        const float* a = wst + lane * SP;
+        const float* b = wst + (lane + 32) * SP;
+        if (gate) {  // fused ReLU backward: g * (y > 0) (transfer.hpp:99-106, ReLU'(0) = 0)
+            const float* ga = gst + (warp * 64 + lane) * SP;
+            const float* gb = ga + 32 * SP;
+#pragma unroll
+            for (int j = 0; j < P; ++j) v[j] = make_float2(ga[j] > 0.f ? a[j] : 0.f, gb[j] > 0.f ? b[j] : 0.f);
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) v[j] = make_float2(a[j], b[j]);
+        }
+    }
+    dft_r<P, P, false>(v, tw);
+    // split: X1[k] = (Z[k] + conj Z[P-k]) / 2, X2[k] = (Z[k] - conj Z[P-k]) / (2 i)
+    const int64_t o1 = obase[warp * 64 + lane], o2 = obase[warp * 64 + lane + 32];
+    const int64_t zstride = int64_t(Px) * Py * (gF ? gF : 1);
+#pragma unroll
+    for (int k = 0; k < Zh; ++k) {
+        const float2 zk = v[k], zm = v[(P - k) % P];
+        const float2 x1 = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+        const float2 x2 = make_float2(0.5f * (zk.y + zm.y), 0.5f * (zm.x - zk.x));
+        if (o1 >= 0) spec[o1 + k * zstride] = x1;
+        if (o2 >= 0) spec[o2 + k * zstride] = x2;
+    }
+}
+
+// inverse (C2R) of the compact kept planes, line pairs per thread as above;
+// the P outputs go through the staging tile, so any crop / tap stride is a
+// shared-memory index and the stores are warp-cooperative along z
+template <int P>
+__global__ void __launch_bounds__(ZR_THREADS) fft_z_inv_reg_k(const float2* __restrict__ cspec, zinv_args g,
+                                                              const float* __restrict__ bias, float* __restrict__ out) {
+    constexpr int Zh = P / 2 + 1, SP = zr_pitch(P);
+    __shared__ float2 tw[P];
+    __shared__ int64_t obase[ZR_LINES];
+    __shared__ float bvals[ZR_LINES];
+    __shared__ int ozoff[ZR_LINES];
+    extern __shared__ float stage[];
+    fill_twiddles<P>(tw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t wl0 = int64_t(blockIdx.x) * ZR_LINES + warp * 64;
+    const uint32_t per = uint32_t(g.xc) * uint32_t(g.yc);
+    const int64_t zstride = int64_t(g.xc) * g.yc;
+    int64_t ib[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // decode this thread's two lines
+        const int l = lane + 32 * h;
+        const int64_t line = wl0 + l;
+        ib[h] = -1;
+        int64_t ob = -1;
+        int oz = 0;
+        float bv = 0.f;
+        if (line < g.nlines) {
+            uint32_t im, rr;
+            if (g.phased) {
+                im = phase_pair_line(g.ph, uint32_t(line), per, &rr);
+            } else {
+                im = uint32_t(line) / per;
+                rr = uint32_t(line) - im * per;
+            }
+            const int r = int(rr), xi = r / g.yc, yi = r - (r / g.yc) * g.yc;
+            ib[h] = int64_t(im) * Zh * per + r;
+            if (g.phased) {
+                const phase_img pd = phase_decode(g.ph, int(im));
+                ob = phase_line(g.ph, pd, xi, yi);
+                oz = pd.rz;
+            } else {
+                ob = int64_t(im) * g.out_img_stride + (int64_t(xi) * g.oy + yi) * g.oz;
+            }
+            bv = bias ? bias[im % uint32_t(g.bias_mod)] : 0.f;
+        }
+        obase[warp * 64 + l] = ob;
+        ozoff[warp * 64 + l] = oz;
+        bvals[warp * 64 + l] = bv;
+    }
+    float2 v[P];
+#pragma unroll
+    for (int k = 0; k < Zh; ++k) {  // Z = X1 + i X2 (and its Hermitian extension)
+        const float2 a = ib[0] >= 0 ? __ldcs(cspec + ib[0] + k * zstride) : make_float2(0.f, 0.f);
+        const float2 b = ib[1] >= 0 ? __ldcs(cspec + ib[1] + k * zstride) : make_float2(0.f, 0.f);
+        v[k] = make_float2(a.x - b.y, a.y + b.x);
+        if (k > 0 && k < P - k) v[P - k] = make_float2(a.x + b.y, b.x - a.y);
+    }
+    dft_r<P, P, true>(v, tw);
+    __syncthreads();  // twiddles read; per-line tables ready
+    float* wst = stage + warp * 64 * SP;
+    {
+        const float b1 = bvals[warp * 64 + lane], b2 = bvals[warp * 64 + lane + 32];
+        float* a = wst + lane * SP;
+        float* b = wst + (lane + 32) * SP;
+#pragma unroll
+        for (int z = 0; z < P; ++z) {
+            float r1 = v[z].x * g.scale + b1, r2 = v[z].y * g.scale + b2;
+            if (g.act == 2) r1 = r1 > 0.f ? r1 : 0.f, r2 = r2 > 0.f ? r2 : 0.f;
+            else if (g.act == 0) r1 = 1.f / (1.f + expf(-r1)), r2 = 1.f / (1.f + expf(-r2));
+            else if (g.act == 1) r1 = tanhf(r1), r2 = tanhf(r2);
+            a[z] = r1;
+            b[z] = r2;
+        }
+    }
+    __syncwarp();
+    const int zst = g.phased ? g.ph.sz : 1;
+    for (int l = 0; l < 64; ++l) {  // warp-cooperative stores of each line (lanes along the kept z)
+        const int64_t ob = obase[warp * 64 + l];
+        if (ob < 0) continue;  // (uniform) past the end, or a ragged phase line outside the tensor
+        const int oz = ozoff[warp * 64 + l];
+        const int zlim = g.phased ? g.ph.nz - oz : 1 << 30;
+        float* dst = out + ob + oz;
+        for (int q = lane; q < g.z_cnt; q += 32)
+            if (zst * q < zlim) dst[zst * q] = wst[l * SP + q * g.z_step];
+    }
+}
+
 // dilated kernels: dil[e][f_in][s*w] = w[e][f_in][w], zeros elsewhere (conv_direct.hpp:137-151)
 // dilated kernels [nker][ex][ey][ez]: the volume is zeroed by a memset, then
 // one thread per tap (coalesced reads of w) scatters it to its lattice site
@@ -1981,9 +2191,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
     const int n = int(pred) << 4;  // 16 bytes, or zero-fill when out of range
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(gmem), "r"(n) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 template <int TB>
 constexpr size_t cmac_smem() {
@@ -2495,6 +2702,15 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
+        if constexpr (PP >= 40 && PP <= 64) {
+            if (!std::getenv("ZNN_FFT_Z_LINES")) {  // line pairs in registers (ZNN_FFT_Z_LINES=1: 8 threads per line)
+                allow_smem(fft_z_fwd_reg_k<PP>, zr_smem<PP>(true));
+                fft_z_fwd_reg_k<PP><<<unsigned(ceil_div(nlines, ZR_LINES)), ZR_THREADS, zr_smem<PP>(gate != nullptr), st>>>(
+                    in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate,
+                    ph ? *ph : phase_geom{}, ph ? 1 : 0, quad);
+                return;
+            }
+        }
         allow_smem(fft_z_fwd_k<PP>, smem_for(PP));
         fft_z_fwd_k<PP><<<unsigned(ceil_div(nlines, LINES)), THREADS, smem_for(PP), st>>>(
             in, in_img_stride, int(n.x), int(n.y), int(n.z), nlines, spec, int(p.P.x), int(p.P.y), gate,
@@ -2665,6 +2881,14 @@ void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 c
     g.bias_mod = bias_mod > 0 ? bias_mod : 1;
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
+        if constexpr (PP >= 40 && PP <= 64) {
+            if (!std::getenv("ZNN_FFT_Z_LINES")) {
+                allow_smem(fft_z_inv_reg_k<PP>, zr_smem<PP>());
+                fft_z_inv_reg_k<PP><<<unsigned(ceil_div(g.nlines, ZR_LINES)), ZR_THREADS, zr_smem<PP>(), st>>>(
+                    cbuf, g, bias, out);
+                return;
+            }
+        }
         allow_smem(fft_z_inv_k<PP>, smem_for(PP));
         fft_z_inv_k<PP><<<unsigned(ceil_div(g.nlines, LINES)), THREADS, smem_for(PP), st>>>(cbuf, g, bias, out);
     });
