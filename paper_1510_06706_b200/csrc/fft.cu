@@ -1133,8 +1133,8 @@ constexpr int REGP = 24;
 constexpr int RTHREADS = 256;
 
 // NI images per CTA: NI = 1 image-major spectra; NI > 1 (tensor-core plans) the
-// NI consecutive images of a group, whose bins are NI * 8-byte pieces of the
-// row-bin-major layout's group-bins (bgemm_tc.hpp): whole 16 / 32-byte pieces per bin
+// NI consecutive maps of one row of a row-bin-major spectrum (bgemm_tc.hpp),
+// whose bins are NI * 8-byte pieces: whole 16 / 32-byte pieces per bin
 template <int P, int NI = 1>
 constexpr size_t cube_reg_smem() {
     return sizeof(float2) * (size_t(P) + size_t(NI) * size_t(P / 2 + 1) * size_t(P) * size_t(P + 1));
@@ -1412,7 +1412,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
 }
 
 // ---- row-bin-major xy passes (tensor-core plans, square planes): one CTA
-// takes the z-bin plane of NI consecutive images of a group (item = (group,
+// takes the z-bin plane of NI consecutive maps of one row (item = (row,
 // zb, part)), loading / storing one NI * 8-byte piece per bin ----
 template <int P, int NI>
 constexpr size_t smem_xy_grp() {
@@ -1485,7 +1485,155 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__
     }
 }
 
-// inverse: the group-plane piece -> compact kept blocks [xc][yc] of the NI
+// register variants (one line per thread, the P-point transform in registers,
+// no exchange buffer): XR_THREADS threads take the NI planes' rows, then their
+// columns, one pass each
+constexpr int XR_THREADS = 256;
+template <int P, int NI>
+constexpr size_t smem_xy_reg() {
+    return sizeof(float2) * (size_t(P) + size_t(NI) * P * (P + 1));
+}
+template <int P, int NI>
+__global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restrict__ spec, int nx, int ny, int Zh,
+                                                                int F) {
+    constexpr int PYP = P + 1, PV = P * PYP;
+    const int H = F / NI;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* pls = tw + P;  // NI x [P][PYP]
+    const int64_t q = blockIdx.x;
+    const int part = int(q % H);
+    const int64_t rest = q / H;
+    const int zb = int(rest % Zh);
+    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
+    fill_twiddles<P>(tw);
+    for (int e0 = threadIdx.x; e0 < nx * ny; e0 += 2 * XR_THREADS) {  // the valid region the z pass wrote
+        float2 v0[NI], v1[NI];
+        const int e1 = e0 + XR_THREADS;
+        const int x0 = e0 / ny, y0 = e0 - x0 * ny, x1 = e1 / ny, y1 = e1 - x1 * ny;
+        grp_get<NI>(gq + (x0 * P + y0) * F, v0);
+        if (e1 < nx * ny) grp_get<NI>(gq + (x1 * P + y1) * F, v1);
+#pragma unroll
+        for (int j = 0; j < NI; ++j) pls[j * PV + x0 * PYP + y0] = v0[j];
+        if (e1 < nx * ny) {
+#pragma unroll
+            for (int j = 0; j < NI; ++j) pls[j * PV + x1 * PYP + y1] = v1[j];
+        }
+    }
+    __syncthreads();
+    for (int ln = threadIdx.x; ln < NI * nx; ln += XR_THREADS) {  // rows (y transforms) of the valid rows
+        const int j = ln / nx, x = ln - j * nx;
+        float2* row = pls + j * PV + x * PYP;
+        float2 v[P];
+#pragma unroll
+        for (int y = 0; y < P; ++y) v[y] = y < ny ? row[y] : make_float2(0.f, 0.f);
+        dft_r<P, P, false>(v, tw);
+#pragma unroll
+        for (int k = 0; k < P; ++k) row[k] = v[k];
+    }
+    __syncthreads();
+    for (int ln = threadIdx.x; ln < NI * P; ln += XR_THREADS) {  // columns (x transforms); rows >= nx are zero
+        const int j = ln / P, y = ln - j * P;
+        float2* col = pls + j * PV + y;
+        float2 v[P];
+#pragma unroll
+        for (int x = 0; x < P; ++x) v[x] = x < nx ? col[x * PYP] : make_float2(0.f, 0.f);
+        dft_r<P, P, false>(v, tw);
+#pragma unroll
+        for (int k = 0; k < P; ++k) col[k * PYP] = v[k];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < P * P; e += XR_THREADS) {
+        const int x = e / P, y = e - x * P;
+        float2 v[NI];
+#pragma unroll
+        for (int j = 0; j < NI; ++j) v[j] = pls[j * PV + x * PYP + y];
+        grp_put<NI>(gq + e * F, v);
+    }
+}
+
+template <int P, int NI, bool UNIT>  // UNIT: unit kept-voxel steps (no per-output division)
+__global__ void __launch_bounds__(XR_THREADS) fft_xy_inv_reg_k(const float2* __restrict__ spec, float2* __restrict__ out,
+                                                                int x_step, int xc, int y_step, int yc, int Zh, int F) {
+    constexpr int PYP = P + 1, PV = P * PYP;
+    const int H = F / NI;
+    extern __shared__ float2 sm[];
+    float2* tw = sm;
+    float2* pls = tw + P;
+    const int64_t q = blockIdx.x;
+    const int part = int(q % H);
+    const int64_t rest = q / H;
+    const int zb = int(rest % Zh);
+    const int64_t grp = rest / Zh;
+    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
+    fill_twiddles<P>(tw);
+    for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * XR_THREADS) {
+        float2 v0[NI], v1[NI];
+        const int e1 = e0 + XR_THREADS;
+        grp_get<NI>(gq + e0 * F, v0);
+        if (e1 < P * P) grp_get<NI>(gq + e1 * F, v1);
+        {
+            const int x = e0 / P, y = e0 - x * P;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v0[j];
+        }
+        if (e1 < P * P) {
+            const int x = e1 / P, y = e1 - x * P;
+#pragma unroll
+            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v1[j];
+        }
+    }
+    __syncthreads();
+    for (int ln = threadIdx.x; ln < NI * P; ln += XR_THREADS) {  // column inverses, keep rows x_step * i
+        const int j = ln / P, y = ln - j * P;
+        float2* col = pls + j * PV + y;
+        float2 v[P];
+#pragma unroll
+        for (int x = 0; x < P; ++x) v[x] = col[x * PYP];
+        dft_r<P, P, true>(v, tw);
+        if constexpr (UNIT) {
+#pragma unroll
+            for (int i = 0; i < P; ++i)
+                if (i < xc) col[i * PYP] = v[i];
+        } else {
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const int i = k / x_step;
+                if (i * x_step == k && i < xc) col[i * PYP] = v[k];
+            }
+        }
+    }
+    __syncthreads();
+    for (int ln = threadIdx.x; ln < NI * xc; ln += XR_THREADS) {  // row inverses of the kept rows
+        const int j = ln / xc, i = ln - j * xc;
+        const float2* row = pls + j * PV + i * PYP;
+        float2 v[P];
+#pragma unroll
+        for (int y = 0; y < P; ++y) v[y] = row[y];
+        dft_r<P, P, true>(v, tw);
+        float2* o = pls + j * PV + i * PYP;  // the kept columns back into the row (already in registers)
+        if constexpr (UNIT) {
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj)
+                if (jj < yc) o[jj] = v[jj];
+        } else {
+#pragma unroll
+            for (int k = 0; k < P; ++k) {
+                const int jj = k / y_step;
+                if (jj * y_step == k && jj < yc) o[jj] = v[k];
+            }
+        }
+    }
+    __syncthreads();
+    // coalesced stores of the NI compact blocks (plane img * Zh + zb, [xc][yc])
+    const int blk = xc * yc;
+    for (int e = threadIdx.x; e < NI * blk; e += XR_THREADS) {
+        const int j = e / blk, r = e - j * blk, i = r / yc, jj = r - i * yc;
+        out[((grp * F + part * NI + j) * Zh + zb) * int64_t(blk) + r] = pls[j * PV + i * PYP + jj];
+    }
+}
+
+// inverse: the row-bin-major piece -> compact kept blocks [xc][yc] of the NI
 // images, written image-major (plane img * Zh + zb) for the z pass
 template <int P, int NI>
 __global__ void __launch_bounds__(THREADS) fft_xy_inv_grp_k(const float2* __restrict__ spec, float2* __restrict__ out,
@@ -2734,6 +2882,12 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
                 auto run = [&](auto ni) {
                     constexpr int NI = decltype(ni)::value;
                     require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
+                    if (!std::getenv("ZNN_FFT_XY_LINES")) {  // one line per thread in registers
+                        allow_smem(fft_xy_fwd_reg_k<PY, NI>, smem_xy_reg<PY, NI>());
+                        fft_xy_fwd_reg_k<PY, NI><<<unsigned(planes / NI), XR_THREADS, smem_xy_reg<PY, NI>(), st>>>(
+                            spec, int(n.x), int(n.y), int(p.Zh), quad);
+                        return;
+                    }
                     allow_smem(fft_xy_fwd_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
                     fft_xy_fwd_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
                         spec, int(n.x), int(n.y), int(p.Zh), quad);
@@ -2840,6 +2994,18 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                 auto run = [&](auto ni) {
                     constexpr int NI = decltype(ni)::value;
                     require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
+                    if (!std::getenv("ZNN_FFT_XY_LINES")) {
+                        auto go = [&](auto kern) {
+                            allow_smem(kern, smem_xy_reg<PY, NI>());
+                            kern<<<unsigned(planes / NI), XR_THREADS, smem_xy_reg<PY, NI>(), st>>>(
+                                spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
+                        };
+                        if (step.x == 1 && step.y == 1)
+                            go(fft_xy_inv_reg_k<PY, NI, true>);
+                        else
+                            go(fft_xy_inv_reg_k<PY, NI, false>);
+                        return;
+                    }
                     allow_smem(fft_xy_inv_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
                     fft_xy_inv_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
                         spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
