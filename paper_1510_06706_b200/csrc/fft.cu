@@ -1131,6 +1131,10 @@ __global__ void __launch_bounds__(THREADS) fft3_inv_small_k(const float2* __rest
 // needs only the twiddle table beside it (more CTAs per SM) ----
 constexpr int REGP = 24;
 constexpr int RTHREADS = 256;
+// threads of a cube CTA: 512 when it holds four cubes (one CTA per SM at
+// P = 20: the extra warps hide the load latency), else 256
+template <int NI>
+__host__ __device__ constexpr int cube_threads() { return NI >= 4 ? 512 : RTHREADS; }
 
 // NI images per CTA: NI = 1 image-major spectra; NI > 1 (tensor-core plans) the
 // NI consecutive maps of one row of a row-bin-major spectrum (bgemm_tc.hpp),
@@ -1181,7 +1185,8 @@ __device__ __forceinline__ void grp_get(const float2* __restrict__ src, float2 (
 }
 
 template <int P, int NI, bool GL = (NI > 1)>
-__global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __restrict__ spec) {
+__global__ void __launch_bounds__(cube_threads<NI>()) fft3_fwd_reg_k(cube_io a, float2* __restrict__ spec) {
+    constexpr int CT = cube_threads<NI>();
     constexpr int Zh = P / 2 + 1, PYP = P + 1, CV = Zh * P * PYP, NB = Zh * P * P;
     extern __shared__ float2 sm[];
     float2* tw = sm;
@@ -1194,7 +1199,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
     __syncthreads();
     // z lines (R2C) of the valid (x, y) lines, read straight from HBM / L2
     const int nl1 = a.nx * a.ny;
-    for (int ln = threadIdx.x; ln < NI * nl1; ln += RTHREADS) {
+    for (int ln = threadIdx.x; ln < NI * nl1; ln += CT) {
         const int j = NI == 1 ? 0 : ln / nl1, l1 = ln - j * nl1;
         const int x = l1 / a.ny, y = l1 - x * a.ny;
         float2 v[P];
@@ -1227,7 +1232,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
     }
     __syncthreads();
     // y lines of the valid rows x < nx (columns y >= ny are the zero padding)
-    for (int ln = threadIdx.x; ln < NI * Zh * a.nx; ln += RTHREADS) {
+    for (int ln = threadIdx.x; ln < NI * Zh * a.nx; ln += CT) {
         const int j = NI == 1 ? 0 : ln / (Zh * a.nx), l2 = ln - j * (Zh * a.nx);
         const int zb = l2 / a.nx, x = l2 - zb * a.nx;
         float2* row = cubes + j * CV + (zb * P + x) * PYP;
@@ -1240,7 +1245,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
     }
     __syncthreads();
     // x lines of every column (rows x >= nx are the zero padding)
-    for (int ln = threadIdx.x; ln < NI * Zh * P; ln += RTHREADS) {
+    for (int ln = threadIdx.x; ln < NI * Zh * P; ln += CT) {
         const int j = NI == 1 ? 0 : ln / (Zh * P), l3 = ln - j * (Zh * P);
         const int zb = l3 / P, y = l3 - zb * P;
         float2* col = cubes + j * CV + zb * P * PYP + y;
@@ -1254,7 +1259,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
     __syncthreads();
     if constexpr (!GL) {
         float4* g4 = reinterpret_cast<float4*>(spec + int64_t(img0) * NB);
-        for (int idx = threadIdx.x; idx < NB / 2; idx += RTHREADS) {
+        for (int idx = threadIdx.x; idx < NB / 2; idx += CT) {
             const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
             const float2 u = cubes[(zb * P + x) * PYP + y], w = cubes[(zb * P + x) * PYP + y + 1];
             __stcs(g4 + idx, make_float4(u.x, u.y, w.x, w.y));
@@ -1262,7 +1267,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
     } else {  // row-bin-major layout: one NI * 8-byte piece per bin
         const int F = a.gF;
         float2* dst = spec + (int64_t(img0 / F) * NB) * F + (img0 % F);
-        for (int b = threadIdx.x; b < NB; b += RTHREADS) {
+        for (int b = threadIdx.x; b < NB; b += CT) {
             const int zb = b / (P * P), r = b - zb * (P * P), x = r / P, y = r - x * P;
             float2 v[NI];
 #pragma unroll
@@ -1273,8 +1278,9 @@ __global__ void __launch_bounds__(RTHREADS) fft3_fwd_reg_k(cube_io a, float2* __
 }
 
 template <int P, int NI, bool UNIT, bool GL = (NI > 1)>
-__global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restrict__ spec, cube_io a,
+__global__ void __launch_bounds__(cube_threads<NI>()) fft3_inv_reg_k(const float2* __restrict__ spec, cube_io a,
                                                            const float* __restrict__ bias) {
+    constexpr int CT = cube_threads<NI>();
     constexpr int Zh = P / 2 + 1, PYP = P + 1, CV = Zh * P * PYP, NB = Zh * P * P;
     extern __shared__ float2 sm[];
     float2* tw = sm;
@@ -1284,14 +1290,14 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     if constexpr (!GL) {
         const float4* g4 = reinterpret_cast<const float4*>(spec + int64_t(img0) * NB);
         constexpr int NV = NB / 2;
-        for (int i0 = threadIdx.x; i0 < NV; i0 += 4 * RTHREADS) {
+        for (int i0 = threadIdx.x; i0 < NV; i0 += 4 * CT) {
             float4 u4[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (i0 + u * RTHREADS < NV) u4[u] = __ldcs(g4 + i0 + u * RTHREADS);
+                if (i0 + u * CT < NV) u4[u] = __ldcs(g4 + i0 + u * CT);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int idx = i0 + u * RTHREADS;
+                const int idx = i0 + u * CT;
                 if (idx < NV) {
                     const int e = 2 * idx, zb = e / (P * P), r = e - zb * (P * P), x = r / P, y = r - x * P;
                     cubes[(zb * P + x) * PYP + y] = make_float2(u4[u].x, u4[u].y);
@@ -1302,9 +1308,9 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     } else {
         const int F = a.gF;
         const float2* src = spec + (int64_t(img0 / F) * NB) * F + (img0 % F);
-        for (int b0 = threadIdx.x; b0 < NB; b0 += 2 * RTHREADS) {  // two bins' loads in flight per thread
+        for (int b0 = threadIdx.x; b0 < NB; b0 += 2 * CT) {  // two bins' loads in flight per thread
             float2 v0[NI], v1[NI];
-            const int b1 = b0 + RTHREADS;
+            const int b1 = b0 + CT;
             grp_get<NI>(src + int64_t(b0) * F, v0);
             if (b1 < NB) grp_get<NI>(src + int64_t(b1) * F, v1);
             {
@@ -1324,7 +1330,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     for (int j = 0; j < NI; ++j) pds[j] = a.phased ? phase_decode(a.ph, img0 + j) : phase_img{};
     __syncthreads();
     // x lines (columns), keep rows xs * i, i < xc
-    for (int ln = threadIdx.x; ln < NI * Zh * P; ln += RTHREADS) {
+    for (int ln = threadIdx.x; ln < NI * Zh * P; ln += CT) {
         const int j = NI == 1 ? 0 : ln / (Zh * P), l1 = ln - j * (Zh * P);
         const int zb = l1 / P, y = l1 - zb * P;
         float2* col = cubes + j * CV + zb * P * PYP + y;
@@ -1342,7 +1348,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     }
     __syncthreads();
     // y lines of the kept rows, keep columns ys * j, j < yc
-    for (int ln = threadIdx.x; ln < NI * Zh * a.xc; ln += RTHREADS) {
+    for (int ln = threadIdx.x; ln < NI * Zh * a.xc; ln += CT) {
         const int j = NI == 1 ? 0 : ln / (Zh * a.xc), l2 = ln - j * (Zh * a.xc);
         const int zb = l2 / a.xc, i = l2 - zb * a.xc;
         float2* row = cubes + j * CV + (zb * P + i) * PYP;
@@ -1361,7 +1367,7 @@ __global__ void __launch_bounds__(RTHREADS) fft3_inv_reg_k(const float2* __restr
     __syncthreads();
     // z lines (C2R) of the kept (i, j), keep zs * q, q < zc; scale, bias, transfer
     const int nl3 = a.xc * a.yc;
-    for (int ln = threadIdx.x; ln < NI * nl3; ln += RTHREADS) {
+    for (int ln = threadIdx.x; ln < NI * nl3; ln += CT) {
         const int j = NI == 1 ? 0 : ln / nl3, l3 = ln - j * nl3;
         const int i = l3 / a.yc, jj = l3 - i * a.yc;
         const int img = img0 + j;
@@ -2816,7 +2822,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
                         constexpr int NI = decltype(ni)::value;
                         require(imgs % NI == 0, "fft: row-bin-major images not a multiple of the CTA's images");
                         allow_smem(fft3_fwd_reg_k<PP, NI, true>, cube_reg_smem<PP, NI>());
-                        fft3_fwd_reg_k<PP, NI, true><<<unsigned(imgs / NI), RTHREADS, cube_reg_smem<PP, NI>(), st>>>(
+                        fft3_fwd_reg_k<PP, NI, true><<<unsigned(imgs / NI), cube_threads<NI>(), cube_reg_smem<PP, NI>(), st>>>(
                             a, spec);
                     };
                     const int ni = cube_grp_ni<PP>();
@@ -2850,7 +2856,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
     require(nlines < (int64_t(1) << 32), "fft: too many transform lines");
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
-        if constexpr (PP >= 40 && PP <= 64) {
+        if constexpr (PP >= 8 && PP <= 64) {
             if (!std::getenv("ZNN_FFT_Z_LINES")) {  // line pairs in registers (ZNN_FFT_Z_LINES=1: 8 threads per line)
                 allow_smem(fft_z_fwd_reg_k<PP>, zr_smem<PP>(true));
                 fft_z_fwd_reg_k<PP><<<unsigned(ceil_div(nlines, ZR_LINES)), ZR_THREADS, zr_smem<PP>(gate != nullptr), st>>>(
@@ -2952,9 +2958,9 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                         constexpr int NI = decltype(ni)::value;
                         require(imgs % NI == 0, "fft: row-bin-major images not a multiple of the CTA's images");
                         if (unit)
-                            go(fft3_inv_reg_k<PP, NI, true, true>, imgs / NI, RTHREADS, cube_reg_smem<PP, NI>());
+                            go(fft3_inv_reg_k<PP, NI, true, true>, imgs / NI, cube_threads<NI>(), cube_reg_smem<PP, NI>());
                         else
-                            go(fft3_inv_reg_k<PP, NI, false, true>, imgs / NI, RTHREADS, cube_reg_smem<PP, NI>());
+                            go(fft3_inv_reg_k<PP, NI, false, true>, imgs / NI, cube_threads<NI>(), cube_reg_smem<PP, NI>());
                     };
                     const int ni = cube_grp_ni<PP>();
                     if (ni == 1) run(std::integral_constant<int, 1>{});
@@ -3047,7 +3053,7 @@ void inverse_z(cudaStream_t st, const plan& p, int64_t imgs, dims3 step, dims3 c
     g.bias_mod = bias_mod > 0 ? bias_mod : 1;
     dispatch_pad(int(p.P.z), [&](auto pc) {
         constexpr int PP = decltype(pc)::value;
-        if constexpr (PP >= 40 && PP <= 64) {
+        if constexpr (PP >= 8 && PP <= 64) {
             if (!std::getenv("ZNN_FFT_Z_LINES")) {
                 allow_smem(fft_z_inv_reg_k<PP>, zr_smem<PP>());
                 fft_z_inv_reg_k<PP><<<unsigned(ceil_div(g.nlines, ZR_LINES)), ZR_THREADS, zr_smem<PP>(), st>>>(

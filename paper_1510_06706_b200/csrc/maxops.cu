@@ -1,7 +1,9 @@
 // Max-pooling and dense (dilated) max-filtering with argmax masks
 // (maxops.hpp:32-182). HBM-bound; a thread per output voxel forward and per
 // input voxel backward (gather formulation: deterministic, no atomics).
-// Mask = int32 flat index into the per-map input volume.
+// Mask = int32 flat index into the per-map input volume (the reference's
+// record), or, for the executor's internal max-filters, a one-byte window
+// code (a ky + b) kz + c: a quarter of the mask traffic (HBM-bound passes).
 //
 // Tie rule: the reference resolves ties to the lexicographically smallest
 // (x,y,z) source, i.e. the lowest flat index (maxops.hpp:79-82 strict '>'
@@ -26,11 +28,12 @@ inline dim3 vblock() { return dim3(ZL, YR, 1); }
 
 // KX/KY/KZ > 0: compile-time window (fully unrolled, the common 2^3 and
 // 1x2x2 filters); 0: runtime window.
-template <int KX, int KY, int KZ>
+template <int KX, int KY, int KZ, typename M>
 __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restrict__ x, int nx, int ny, int nz,
                                                            int mx, int my, int mz, int kx_, int ky_, int kz_, int sx,
                                                            int sy, int sz, float* __restrict__ y,
-                                                           int32_t* __restrict__ mask) {
+                                                           M* __restrict__ mask) {
+    constexpr bool CODE = sizeof(M) == 1;
     const int kx = KX ? KX : kx_, ky = KY ? KY : ky_, kz = KZ ? KZ : kz_;
     const int j = blockIdx.x * YR + threadIdx.y, i = blockIdx.y;
     if (j >= my) return;
@@ -41,7 +44,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
     const int rbase = (i * ny + j) * nz;
     const float* xr = xm + rbase;
     float* yr = y + orow;
-    int32_t* mr = mask + orow;
+    M* mr = mask + orow;
     if constexpr (KX > 0) {
         // one 64-bit pointer per window row (a, b), advanced along z: the
         // loads need no per-element 64-bit index arithmetic
@@ -59,7 +62,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
 #pragma unroll
                     for (int c = 0; c < KZ; ++c) v[a][b][c] = __ldg(q[a][b] + c * sz);
             float best = v[0][0][0];
-            int best_off = 0;
+            int best_off = 0, best_code = 0;
 #pragma unroll
             for (int a = 0; a < KX; ++a)
 #pragma unroll
@@ -69,9 +72,13 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
                         if (v[a][b][c] > best) {  // strict: ties keep the lexicographically first source
                             best = v[a][b][c];
                             best_off = a * dx + b * dy + c * sz;
+                            best_code = (a * KY + b) * KZ + c;
                         }
             __stcs(yr + l, best);
-            __stcs(mr + l, rbase + l + best_off);
+            if constexpr (CODE)
+                mr[l] = M(best_code);
+            else
+                __stcs(mr + l, M(rbase + l + best_off));
 #pragma unroll
             for (int a = 0; a < KX; ++a)
 #pragma unroll
@@ -80,7 +87,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
     } else {
         for (int l = threadIdx.x; l < mz; l += ZL) {
             const int base = rbase + l;
-            int best_idx = base;
+            int best_idx = base, best_code = 0;
             float best = __ldg(xm + base);
             for (int a = 0; a < kx; ++a)
                 for (int b = 0; b < ky; ++b)
@@ -90,10 +97,14 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
                         if (v > best) {  // strict: ties keep the lexicographically first source
                             best = v;
                             best_idx = idx;
+                            best_code = (a * ky + b) * kz + c;
                         }
                     }
             __stcs(yr + l, best);
-            __stcs(mr + l, best_idx);
+            if constexpr (CODE)
+                mr[l] = M(best_code);
+            else
+                __stcs(mr + l, M(best_idx));
         }
     }
 }
@@ -101,18 +112,19 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
 // dx[t] = sum over windows o whose argmax is t of g[o]; windows visited in
 // ascending flat order of o, the order the reference accumulates in
 // (maxops.hpp:176-181), so fp32 sums match it bit for bit.
-template <int KX, int KY, int KZ>
+template <int KX, int KY, int KZ, typename M>
 __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restrict__ g,
-                                                           const int32_t* __restrict__ mask, int nx, int ny, int nz,
+                                                           const M* __restrict__ mask, int nx, int ny, int nz,
                                                            int mx, int my, int mz, int kx_, int ky_, int kz_, int sx,
                                                            int sy, int sz, float* __restrict__ dx) {
+    constexpr bool CODE = sizeof(M) == 1;
     const int kx = KX ? KX : kx_, ky = KY ? KY : ky_, kz = KZ ? KZ : kz_;
     const int tj = blockIdx.x * YR + threadIdx.y, ti = blockIdx.y;
     if (tj >= ny) return;
     const int64_t map = blockIdx.z;
     const int64_t mv = int64_t(mx) * my * mz;
     const float* gm = g + map * mv;
-    const int32_t* mm = mask + map * mv;
+    const M* mm = mask + map * mv;
     float* drow = dx + map * (int64_t(nx) * ny * nz) + (int64_t(ti) * ny + tj) * nz;
     // rows whose every window origin t - s*w is inside the output volume skip
     // the per-window bounds tests (the common case away from the faces)
@@ -130,9 +142,9 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
                     for (int c = kz - 1; c >= 0; --c) {
                         // both loads issued together: no mask -> g dependent round trip
                         const int o = o0 - (sx * a * my + sy * b) * mz - sz * c;
-                        const int mv = __ldg(mm + o);
+                        const int mv = int(__ldg(mm + o));
                         const float gv = __ldg(gm + o);
-                        acc += (mv == tr) ? gv : 0.f;
+                        acc += (mv == (CODE ? (a * ky + b) * kz + c : tr)) ? gv : 0.f;
                     }
             __stcs(drow + tl, acc);
             continue;
@@ -150,7 +162,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
                     const int ol = tl - sz * c;
                     if (ol < 0 || ol >= mz) continue;
                     const int o = (oi * my + oj) * mz + ol;
-                    if (__ldg(mm + o) == tr) acc += __ldg(gm + o);
+                    if (int(__ldg(mm + o)) == (CODE ? (a * ky + b) * kz + c : tr)) acc += __ldg(gm + o);
                 }
             }
         }
@@ -164,17 +176,18 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
 // serve input planes oi and oi + SX, half the loads of maxfilter_bwd_k.
 // Block = 32 z-lanes x 8 y-rows, grid = (y tiles, maps). Sums in ascending
 // window order like maxfilter_bwd_k.
-template <int SX>
+template <int SX, typename M>
 __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restrict__ g,
-                                                            const int32_t* __restrict__ mask, int nx, int ny,
+                                                            const M* __restrict__ mask, int nx, int ny,
                                                             int nz, int mx, int my, int mz, int sy, int sz,
                                                             float* __restrict__ dx) {
+    constexpr bool CODE = sizeof(M) == 1;
     const int tj = blockIdx.x * YR + threadIdx.y;
     if (tj >= ny) return;
     const int64_t map = blockIdx.y;
     const int64_t pin = int64_t(ny) * nz, pout = int64_t(my) * mz;
     const float* gm = g + map * (pout * mx);
-    const int32_t* mm = mask + map * (pout * mx);
+    const M* mm = mask + map * (pout * mx);
     float* dm = dx + map * (pin * nx);
     for (int tl = threadIdx.x; tl < nz; tl += ZL) {
         // window rows (b, c) in descending order = ascending output index
@@ -195,14 +208,14 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
         for (int k = 0; k < SX; ++k)
 #pragma unroll
             for (int q = 0; q < 4; ++q) rm[k][q] = -1, rg[k][q] = 0.f;
-        const int32_t* mp = mm;
+        const M* mp = mm;
         const float* gp = gm;
         auto fetch = [&](int oi, int slot) {
             const bool pok = oi < mx;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const bool ok = pok && rok[q];
-                rm[slot][q] = ok ? __ldg(mp + roff[q]) : -1;
+                rm[slot][q] = ok ? int(__ldg(mp + roff[q])) : -1;
                 rg[slot][q] = ok ? __ldg(gp + roff[q]) : 0.f;
             }
             mp += pout;
@@ -214,10 +227,13 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
         for (int ti = 0; ti < nx; ++ti) {
             fetch(ti + 1, SX + 1);
             float acc = 0.f;
+            // window (a, b, c) with b = 1 - (q >> 1), c = 1 - (q & 1): code (2 a + b) 2 + c
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc += (rm[0][q] == tr) ? rg[0][q] : 0.f;  // a = 1: plane ti - SX
+            for (int q = 0; q < 4; ++q)  // a = 1: plane ti - SX
+                acc += (rm[0][q] == (CODE ? 4 + 2 * (1 - (q >> 1)) + (1 - (q & 1)) : tr)) ? rg[0][q] : 0.f;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc += (rm[SX][q] == tr) ? rg[SX][q] : 0.f;  // a = 0: plane ti
+            for (int q = 0; q < 4; ++q)  // a = 0: plane ti
+                acc += (rm[SX][q] == (CODE ? 2 * (1 - (q >> 1)) + (1 - (q & 1)) : tr)) ? rg[SX][q] : 0.f;
             __stcs(dp, acc);
             dp += pin;
             tr += int(pin);
@@ -276,42 +292,63 @@ __global__ void __launch_bounds__(ZL * YR) maxpool_bwd_k(const float* __restrict
 
 }  // namespace
 
-void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s,
-                   float* y, int32_t* mask) {
+namespace {
+template <typename M>
+void maxfilter_fwd_t(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y, M* mask) {
     const dims3 m{n.x - s.x * (k.x - 1), n.y - s.y * (k.y - 1), n.z - s.z * (k.z - 1)};
     require(m.x > 0 && m.y > 0 && m.z > 0, "maxfilter_forward: effective window exceeds input");
     prof_scope ps(st, "maxfilter_fwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
-                  double(maps) * (4.0 * double(n.vol()) + 8.0 * double(m.vol())), 0);
+                  double(maps) * (4.0 * double(n.vol()) + (4.0 + sizeof(M)) * double(m.vol())), 0);
     require(n.vol() < (int64_t(1) << 31), "maxfilter_forward: map exceeds int32 mask range");
-    auto* kf = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_fwd_k<2, 2, 2>
-               : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2>
-                                                    : maxfilter_fwd_k<0, 0, 0>;
+    require(sizeof(M) == 4 || k.vol() <= 256, "maxfilter_forward: window too large for one-byte codes");
+    auto* kf = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_fwd_k<2, 2, 2, M>
+               : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2, M>
+                                                    : maxfilter_fwd_k<0, 0, 0, M>;
     kf<<<vgrid(m.y, m.x, maps), vblock(), 0, st>>>(x, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
                                                   int(k.x), int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), y,
                                                   mask);
     launch_check("maxfilter_fwd");
 }
 
-void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
-                   dims3 k, dims3 s, float* dx) {
+template <typename M>
+void maxfilter_bwd_t(cudaStream_t st, const float* g, const M* mask, int64_t maps, dims3 m, dims3 k, dims3 s,
+                     float* dx) {
     const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
     prof_scope ps(st, "maxfilter_bwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
-                  double(maps) * (8.0 * double(m.vol()) + 4.0 * double(n.vol())), 0);
+                  double(maps) * ((4.0 + sizeof(M)) * double(m.vol()) + 4.0 * double(n.vol())), 0);
     if (k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2) && maps < 65536) {
         const dim3 grid(unsigned(ceil_div(n.y, YR)), unsigned(maps));
-        auto* kk = s.x == 1 ? maxfilter2_bwd_k<1> : maxfilter2_bwd_k<2>;
+        auto* kk = s.x == 1 ? maxfilter2_bwd_k<1, M> : maxfilter2_bwd_k<2, M>;
         kk<<<grid, vblock(), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
                                       int(s.y), int(s.z), dx);
         launch_check("maxfilter_bwd");
         return;
     }
-    auto* kb = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_bwd_k<2, 2, 2>
-               : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_bwd_k<1, 2, 2>
-                                                    : maxfilter_bwd_k<0, 0, 0>;
+    auto* kb = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_bwd_k<2, 2, 2, M>
+               : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_bwd_k<1, 2, 2, M>
+                                                    : maxfilter_bwd_k<0, 0, 0, M>;
     kb<<<vgrid(n.y, n.x, maps), vblock(), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y),
                                                   int(m.z), int(k.x), int(k.y), int(k.z), int(s.x), int(s.y),
                                                   int(s.z), dx);
     launch_check("maxfilter_bwd");
+}
+}  // namespace
+
+void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y,
+                   int32_t* mask) {
+    maxfilter_fwd_t(st, x, maps, n, k, s, y, mask);
+}
+void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y,
+                   uint8_t* code) {
+    maxfilter_fwd_t(st, x, maps, n, k, s, y, code);
+}
+void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m, dims3 k, dims3 s,
+                   float* dx) {
+    maxfilter_bwd_t(st, g, mask, maps, m, k, s, dx);
+}
+void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m, dims3 k, dims3 s,
+                   float* dx) {
+    maxfilter_bwd_t(st, g, code, maps, m, k, s, dx);
 }
 
 void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p, float* y,

@@ -268,11 +268,15 @@ void executor::allocate() {
         if (j > 0 && G.materialized) G.act = static_cast<float*>(dalloc(sizeof(float) * size_t(n)));
         if (cfg_.keep_images && G.materialized) G.grad = static_cast<float*>(dalloc(sizeof(float) * size_t(n)));
     }
-    for (const auto& L : layers_)
-        if (L.kind == lkind::pool || L.kind == lkind::filter) {
-            group& G = groups_[size_t(L.out)];
-            G.mask = static_cast<int32_t*>(dalloc(sizeof(int32_t) * size_t(B * G.maps * G.dims.vol())));
+    for (const auto& L : layers_) {
+        group& G = groups_[size_t(L.out)];
+        const size_t nv = size_t(B * G.maps * G.dims.vol());
+        if (L.kind == lkind::pool) G.mask = static_cast<int32_t*>(dalloc(sizeof(int32_t) * nv));
+        if (L.kind == lkind::filter) {
+            require(L.k.vol() <= 256, "max-filter window exceeds 256 taps");
+            G.code = static_cast<uint8_t*>(dalloc(nv));
         }
+    }
     if (!cfg_.keep_images) {
         gbuf_[0] = static_cast<float*>(dalloc(sizeof(float) * size_t(maxsz)));
         gbuf_[1] = static_cast<float*>(dalloc(sizeof(float) * size_t(maxsz)));
@@ -552,7 +556,7 @@ void executor::run_forward(const float* in_dev) {
                 break;
             case lkind::pool: znn_gpu::maxpool_fwd(st_, I.act, B * I.maps, I.dims, L.k, O.act, O.mask); break;
             case lkind::filter:
-                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.mask);
+                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.code);
                 break;
         }
     }
@@ -638,7 +642,7 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                 if (L.in != 0) znn_gpu::maxpool_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, I.grad);
                 break;
             case lkind::filter:
-                if (L.in != 0) znn_gpu::maxfilter_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, L.s, I.grad);
+                if (L.in != 0) znn_gpu::maxfilter_bwd(st_, O.grad, O.code, B * I.maps, O.dims, L.k, L.s, I.grad);
                 break;
         }
     }
@@ -687,10 +691,31 @@ void executor::group_image(int gi, int which, float* host) {
 
 void executor::group_mask(int gi, int32_t* host) {
     const group& G = groups_.at(size_t(gi));
-    require(G.mask != nullptr, "group mask: group " + std::to_string(gi) + " has no argmax record");
-    ZNN_CUDA_CHECK(cudaMemcpyAsync(host, G.mask, sizeof(int32_t) * size_t(cfg_.batch * G.maps * G.dims.vol()),
-                                   cudaMemcpyDeviceToHost, st_));
+    require(G.mask != nullptr || G.code != nullptr,
+            "group mask: group " + std::to_string(gi) + " has no argmax record");
+    const int64_t n = cfg_.batch * G.maps * G.dims.vol();
+    if (G.mask) {
+        ZNN_CUDA_CHECK(cudaMemcpyAsync(host, G.mask, sizeof(int32_t) * size_t(n), cudaMemcpyDeviceToHost, st_));
+        ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+        return;
+    }
+    // max-filter window codes -> the reference's flat input index per output voxel
+    std::vector<uint8_t> code(static_cast<size_t>(n));
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(code.data(), G.code, size_t(n), cudaMemcpyDeviceToHost, st_));
     ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+    const layer* P = nullptr;
+    for (const auto& L : layers_)
+        if (L.kind == lkind::filter && L.out == gi) P = &L;
+    require(P != nullptr, "group mask: no max-filter produces group " + std::to_string(gi));
+    const dims3 in = groups_[size_t(P->in)].dims, m = G.dims, k = P->k, s = P->s;
+    const int64_t mv = m.vol();
+    for (int64_t e = 0; e < n; ++e) {
+        const int64_t v = e % mv;
+        const int64_t i = v / (m.y * m.z), j = (v / m.z) % m.y, l = v % m.z;
+        const int c = code[size_t(e)];
+        const int64_t a = c / (k.y * k.z), b = (c / k.z) % k.y, cz = c % k.z;
+        host[e] = int32_t(((i + s.x * a) * in.y + (j + s.y * b)) * in.z + (l + s.z * cz));
+    }
 }
 
 std::vector<int> executor::autotune(int trials) {

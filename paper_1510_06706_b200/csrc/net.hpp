@@ -28,7 +28,8 @@ struct group {
     dims3 dims{1, 1, 1};
     float* act = nullptr;    // forward image [B][maps][vol] (null when fused away)
     float* grad = nullptr;   // backward image (kept per group only with keep_images)
-    int32_t* mask = nullptr; // argmax record when produced by pool/filter
+    int32_t* mask = nullptr; // argmax record (flat index) when produced by a pool
+    uint8_t* code = nullptr; // argmax record (window code) when produced by a max-filter
     bool materialized = true;
 };
 

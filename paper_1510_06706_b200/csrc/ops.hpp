@@ -89,5 +89,11 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
                    float* y, int32_t* mask);
 void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m,
                    dims3 k, dims3 s, float* dx);
+// one-byte window codes (a ky + b) kz + c instead of flat indices (windows of
+// at most 256 taps; the executor's internal max-filters)
+void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s,
+                   float* y, uint8_t* code);
+void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m,
+                   dims3 k, dims3 s, float* dx);
 
 }  // namespace znn_gpu
