@@ -616,6 +616,10 @@ void conv_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const flo
                  float* y, scratch& ws) {
     prof_scope ps(st, tc_label("conv_fwd_tc", c), 4.0 * double(c.B) * double(c.f_in * c.n.vol() + c.f_out * c.m.vol()),
                   tc_flops(c));
+    if (conv1_tc_supported(c) && !std::getenv("ZNN_CONV1_GENERIC")) {  // weights-resident single-input-map kernel
+        conv1_fwd_tc(st, c, x, w, bias, act, y);
+        return;
+    }
     char* wsp = static_cast<char*>(ws.get(panel_bytes(int(c.f_in), int(c.f_out), c.taps())));
     launch_valid(st, c.B, int(c.f_in), int(c.f_out), int(c.f_in), c.n, c.k, c.s, x, w, 0, bias, act, y, wsp,
                  dims3{0, 0, 0}, c.n, "conv_fwd_tc");

@@ -52,6 +52,11 @@ void conv_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const flo
                  const float* bias, int act, float* y, scratch& ws);
 void conv_dgrad_tc(cudaStream_t st, const conv_shape& c, const float* g, const float* w,
                    float* dx, scratch& ws);
+// single-input-map forward (conv1_tc.cu): weights resident in shared memory,
+// persistent CTAs, double-buffered TMEM accumulator
+bool conv1_tc_supported(const conv_shape& c);
+void conv1_fwd_tc(cudaStream_t st, const conv_shape& c, const float* x, const float* w, const float* bias, int act,
+                  float* y);
 // SGD(+momentum) applied in a kernel epilogue right where the gradient is
 // final (v = mu v + g; w -= lr v, the arithmetic of sgd_momentum)
 struct sgd_fuse {
