@@ -1495,13 +1495,18 @@ __global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__
 // no exchange buffer): XR_THREADS threads take the NI planes' rows, then their
 // columns, one pass each
 constexpr int XR_THREADS = 256;
+// threads of a register xy CTA: the NI planes' column lines (one pass), at
+// most 256 (P = 48, NI = 4: 192, two CTAs per SM at ~170 registers)
+template <int P, int NI>
+__host__ __device__ constexpr int xr_threads() { return (NI * P + 31) / 32 * 32 < XR_THREADS ? (NI * P + 31) / 32 * 32 : XR_THREADS; }
 template <int P, int NI>
 constexpr size_t smem_xy_reg() {
     return sizeof(float2) * (size_t(P) + size_t(NI) * P * (P + 1));
 }
 template <int P, int NI>
-__global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restrict__ spec, int nx, int ny, int Zh,
+__global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_fwd_reg_k(float2* __restrict__ spec, int nx, int ny, int Zh,
                                                                 int F) {
+    constexpr int XT = xr_threads<P, NI>();
     constexpr int PYP = P + 1, PV = P * PYP;
     const int H = F / NI;
     extern __shared__ float2 sm[];
@@ -1513,9 +1518,9 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restric
     const int zb = int(rest % Zh);
     float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
     fill_twiddles<P>(tw);
-    for (int e0 = threadIdx.x; e0 < nx * ny; e0 += 2 * XR_THREADS) {  // the valid region the z pass wrote
+    for (int e0 = threadIdx.x; e0 < nx * ny; e0 += 2 * XT) {  // the valid region the z pass wrote
         float2 v0[NI], v1[NI];
-        const int e1 = e0 + XR_THREADS;
+        const int e1 = e0 + XT;
         const int x0 = e0 / ny, y0 = e0 - x0 * ny, x1 = e1 / ny, y1 = e1 - x1 * ny;
         grp_get<NI>(gq + (x0 * P + y0) * F, v0);
         if (e1 < nx * ny) grp_get<NI>(gq + (x1 * P + y1) * F, v1);
@@ -1527,7 +1532,7 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restric
         }
     }
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * nx; ln += XR_THREADS) {  // rows (y transforms) of the valid rows
+    for (int ln = threadIdx.x; ln < NI * nx; ln += XT) {  // rows (y transforms) of the valid rows
         const int j = ln / nx, x = ln - j * nx;
         float2* row = pls + j * PV + x * PYP;
         float2 v[P];
@@ -1538,7 +1543,7 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restric
         for (int k = 0; k < P; ++k) row[k] = v[k];
     }
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * P; ln += XR_THREADS) {  // columns (x transforms); rows >= nx are zero
+    for (int ln = threadIdx.x; ln < NI * P; ln += XT) {  // columns (x transforms); rows >= nx are zero
         const int j = ln / P, y = ln - j * P;
         float2* col = pls + j * PV + y;
         float2 v[P];
@@ -1549,7 +1554,7 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restric
         for (int k = 0; k < P; ++k) col[k * PYP] = v[k];
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < P * P; e += XR_THREADS) {
+    for (int e = threadIdx.x; e < P * P; e += XT) {
         const int x = e / P, y = e - x * P;
         float2 v[NI];
 #pragma unroll
@@ -1559,8 +1564,9 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_fwd_reg_k(float2* __restric
 }
 
 template <int P, int NI, bool UNIT>  // UNIT: unit kept-voxel steps (no per-output division)
-__global__ void __launch_bounds__(XR_THREADS) fft_xy_inv_reg_k(const float2* __restrict__ spec, float2* __restrict__ out,
+__global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_inv_reg_k(const float2* __restrict__ spec, float2* __restrict__ out,
                                                                 int x_step, int xc, int y_step, int yc, int Zh, int F) {
+    constexpr int XT = xr_threads<P, NI>();
     constexpr int PYP = P + 1, PV = P * PYP;
     const int H = F / NI;
     extern __shared__ float2 sm[];
@@ -1573,9 +1579,9 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_inv_reg_k(const float2* __r
     const int64_t grp = rest / Zh;
     const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
     fill_twiddles<P>(tw);
-    for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * XR_THREADS) {
+    for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * XT) {
         float2 v0[NI], v1[NI];
-        const int e1 = e0 + XR_THREADS;
+        const int e1 = e0 + XT;
         grp_get<NI>(gq + e0 * F, v0);
         if (e1 < P * P) grp_get<NI>(gq + e1 * F, v1);
         {
@@ -1590,7 +1596,7 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_inv_reg_k(const float2* __r
         }
     }
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * P; ln += XR_THREADS) {  // column inverses, keep rows x_step * i
+    for (int ln = threadIdx.x; ln < NI * P; ln += XT) {  // column inverses, keep rows x_step * i
         const int j = ln / P, y = ln - j * P;
         float2* col = pls + j * PV + y;
         float2 v[P];
@@ -1610,7 +1616,7 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_inv_reg_k(const float2* __r
         }
     }
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * xc; ln += XR_THREADS) {  // row inverses of the kept rows
+    for (int ln = threadIdx.x; ln < NI * xc; ln += XT) {  // row inverses of the kept rows
         const int j = ln / xc, i = ln - j * xc;
         const float2* row = pls + j * PV + i * PYP;
         float2 v[P];
@@ -1633,7 +1639,7 @@ __global__ void __launch_bounds__(XR_THREADS) fft_xy_inv_reg_k(const float2* __r
     __syncthreads();
     // coalesced stores of the NI compact blocks (plane img * Zh + zb, [xc][yc])
     const int blk = xc * yc;
-    for (int e = threadIdx.x; e < NI * blk; e += XR_THREADS) {
+    for (int e = threadIdx.x; e < NI * blk; e += XT) {
         const int j = e / blk, r = e - j * blk, i = r / yc, jj = r - i * yc;
         out[((grp * F + part * NI + j) * Zh + zb) * int64_t(blk) + r] = pls[j * PV + i * PYP + jj];
     }
@@ -2890,7 +2896,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
                     require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
                     if (!std::getenv("ZNN_FFT_XY_LINES")) {  // one line per thread in registers
                         allow_smem(fft_xy_fwd_reg_k<PY, NI>, smem_xy_reg<PY, NI>());
-                        fft_xy_fwd_reg_k<PY, NI><<<unsigned(planes / NI), XR_THREADS, smem_xy_reg<PY, NI>(), st>>>(
+                        fft_xy_fwd_reg_k<PY, NI><<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
                             spec, int(n.x), int(n.y), int(p.Zh), quad);
                         return;
                     }
@@ -3003,7 +3009,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                     if (!std::getenv("ZNN_FFT_XY_LINES")) {
                         auto go = [&](auto kern) {
                             allow_smem(kern, smem_xy_reg<PY, NI>());
-                            kern<<<unsigned(planes / NI), XR_THREADS, smem_xy_reg<PY, NI>(), st>>>(
+                            kern<<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
                                 spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
                         };
                         if (step.x == 1 && step.y == 1)
