@@ -462,7 +462,7 @@ void cgemm(cudaStream_t st, int mode, const float2* Ap, const float2* Bp, float2
 }  // namespace
 
 bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo) {
-    return Bn >= 128 && f <= 128 && fo <= 128 && f % 8 == 0 && fo % 8 == 0;
+    return Bn >= 64 && f <= 128 && fo <= 128 && f % 8 == 0 && fo % 8 == 0;
 }
 
 void tc_cmac_fwd(cudaStream_t st, const float2* X, const float2* K, float2* Y, int64_t Bn, int64_t f, int64_t fo,

@@ -1420,77 +1420,6 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_inv_reg_k(const float
 // ---- row-bin-major xy passes (tensor-core plans, square planes): one CTA
 // takes the z-bin plane of NI consecutive maps of one row (item = (row,
 // zb, part)), loading / storing one NI * 8-byte piece per bin ----
-template <int P, int NI>
-constexpr size_t smem_xy_grp() {
-    return sizeof(float2) * (size_t(P) + size_t(LINES) * size_t(line_shape<P>::XP) + size_t(NI) * P * (P + 1));
-}
-template <int P, int NI>
-__global__ void __launch_bounds__(THREADS) fft_xy_fwd_grp_k(float2* __restrict__ spec, int nx, int ny, int Zh,
-                                                             int F) {
-    constexpr int PYP = P + 1, PV = P * PYP;
-    const int H = F / NI;
-    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2, XP = line_shape<P>::XP;
-    extern __shared__ float2 sm[];
-    float2* tw = sm;
-    float2* xbuf = tw + P;
-    float2* pls = xbuf + LINES * XP;  // NI x [P][PYP]
-    const int64_t q = blockIdx.x;
-    const int part = int(q % H);
-    const int64_t rest = q / H;
-    const int zb = int(rest % Zh);
-    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
-    fill_twiddles<P>(tw);
-    for (int e = threadIdx.x; e < nx * ny; e += THREADS) {  // the valid region the z pass wrote
-        const int x = e / ny, y = e - (e / ny) * ny;
-        float2 v[NI];
-        grp_get<NI>(gq + (x * P + y) * F, v);
-#pragma unroll
-        for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v[j];
-    }
-    __syncthreads();
-    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* xb = xbuf + l * XP;
-    for (int r0 = 0; r0 < NI * nx; r0 += LINES) {  // rows (y transforms) of the valid rows
-        const int ln = r0 + l;
-        const bool ok = ln < NI * nx;
-        const int j = ok ? ln / nx : 0, x = ok ? ln - j * nx : 0;
-        float2* row = pls + j * PV + x * PYP;
-        float2 v[R2];
-#pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) {
-            const int y = t + R1 * n2;
-            v[n2] = (ok && t < R1 && y < ny) ? row[y] : make_float2(0.f, 0.f);
-        }
-        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
-            if (ok) row[k] = val;
-        });
-    }
-    __syncthreads();
-    for (int c0 = 0; c0 < NI * P; c0 += LINES) {  // columns (x transforms); rows >= nx are zero
-        const int ln = c0 + l;
-        const bool ok = ln < NI * P;
-        const int j = ok ? ln / P : 0, y = ok ? ln - j * P : 0;
-        float2* col = pls + j * PV + y;
-        float2 v[R2];
-#pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) {
-            const int x = t + R1 * n2;
-            v[n2] = (ok && t < R1 && x < nx) ? col[x * PYP] : make_float2(0.f, 0.f);
-        }
-        line_fft<P, false>(v, xb, tw, t, [&](int k, float2 val) {
-            if (ok) col[k * PYP] = val;
-        });
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < P * P; e += THREADS) {
-        const int x = e / P, y = e - x * P;
-        float2 v[NI];
-#pragma unroll
-        for (int j = 0; j < NI; ++j) v[j] = pls[j * PV + x * PYP + y];
-        grp_put<NI>(gq + e * F, v);
-    }
-}
-
 // register variants (one line per thread, the P-point transform in registers,
 // no exchange buffer): XR_THREADS threads take the NI planes' rows, then their
 // columns, one pass each
@@ -1518,19 +1447,16 @@ __global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_fwd_reg_k(float2* 
     const int zb = int(rest % Zh);
     float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
     fill_twiddles<P>(tw);
-    for (int e0 = threadIdx.x; e0 < nx * ny; e0 += 2 * XT) {  // the valid region the z pass wrote
-        float2 v0[NI], v1[NI];
-        const int e1 = e0 + XT;
-        const int x0 = e0 / ny, y0 = e0 - x0 * ny, x1 = e1 / ny, y1 = e1 - x1 * ny;
-        grp_get<NI>(gq + (x0 * P + y0) * F, v0);
-        if (e1 < nx * ny) grp_get<NI>(gq + (x1 * P + y1) * F, v1);
+    // the valid region the z pass wrote: async 8-byte copies, every load of the
+    // CTA in flight at once (the kernel runs at ~12 warps per SM)
+    for (int e = threadIdx.x; e < nx * ny; e += XT) {
+        const int x = e / ny, y = e - x * ny;
+        const float2* src = gq + (x * P + y) * F;
 #pragma unroll
-        for (int j = 0; j < NI; ++j) pls[j * PV + x0 * PYP + y0] = v0[j];
-        if (e1 < nx * ny) {
-#pragma unroll
-            for (int j = 0; j < NI; ++j) pls[j * PV + x1 * PYP + y1] = v1[j];
-        }
+        for (int j = 0; j < NI; ++j) cp_async8(pls + j * PV + x * PYP + y, src + j);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     for (int ln = threadIdx.x; ln < NI * nx; ln += XT) {  // rows (y transforms) of the valid rows
         const int j = ln / nx, x = ln - j * nx;
@@ -1579,22 +1505,14 @@ __global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_inv_reg_k(const fl
     const int64_t grp = rest / Zh;
     const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
     fill_twiddles<P>(tw);
-    for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * XT) {
-        float2 v0[NI], v1[NI];
-        const int e1 = e0 + XT;
-        grp_get<NI>(gq + e0 * F, v0);
-        if (e1 < P * P) grp_get<NI>(gq + e1 * F, v1);
-        {
-            const int x = e0 / P, y = e0 - x * P;
+    for (int e = threadIdx.x; e < P * P; e += XT) {  // async 8-byte copies, all in flight
+        const int x = e / P, y = e - x * P;
+        const float2* src = gq + e * F;
 #pragma unroll
-            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v0[j];
-        }
-        if (e1 < P * P) {
-            const int x = e1 / P, y = e1 - x * P;
-#pragma unroll
-            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v1[j];
-        }
+        for (int j = 0; j < NI; ++j) cp_async8(pls + j * PV + x * PYP + y, src + j);
     }
+    cp_async_commit();
+    cp_async_wait<0>();
     __syncthreads();
     for (int ln = threadIdx.x; ln < NI * P; ln += XT) {  // column inverses, keep rows x_step * i
         const int j = ln / P, y = ln - j * P;
@@ -1645,73 +1563,6 @@ __global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_inv_reg_k(const fl
     }
 }
 
-// inverse: the row-bin-major piece -> compact kept blocks [xc][yc] of the NI
-// images, written image-major (plane img * Zh + zb) for the z pass
-template <int P, int NI>
-__global__ void __launch_bounds__(THREADS) fft_xy_inv_grp_k(const float2* __restrict__ spec, float2* __restrict__ out,
-                                                             int x_step, int xc, int y_step, int yc, int Zh, int F) {
-    constexpr int PYP = P + 1, PV = P * PYP;
-    const int H = F / NI;
-    constexpr int R1 = line_shape<P>::R1, R2 = line_shape<P>::R2, XP = line_shape<P>::XP;
-    extern __shared__ float2 sm[];
-    float2* tw = sm;
-    float2* xbuf = tw + P;
-    float2* pls = xbuf + LINES * XP;
-    const int64_t q = blockIdx.x;
-    const int part = int(q % H);
-    const int64_t rest = q / H;
-    const int zb = int(rest % Zh);
-    const int64_t grp = rest / Zh;
-    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
-    fill_twiddles<P>(tw);
-    for (int e0 = threadIdx.x; e0 < P * P; e0 += 2 * THREADS) {
-        float2 v0[NI], v1[NI];
-        const int e1 = e0 + THREADS;
-        grp_get<NI>(gq + e0 * F, v0);
-        if (e1 < P * P) grp_get<NI>(gq + e1 * F, v1);
-        {
-            const int x = e0 / P, y = e0 - x * P;
-#pragma unroll
-            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v0[j];
-        }
-        if (e1 < P * P) {
-            const int x = e1 / P, y = e1 - x * P;
-#pragma unroll
-            for (int j = 0; j < NI; ++j) pls[j * PV + x * PYP + y] = v1[j];
-        }
-    }
-    __syncthreads();
-    const int l = threadIdx.x / TPL, t = threadIdx.x % TPL;
-    float2* xb = xbuf + l * XP;
-    for (int c0 = 0; c0 < NI * P; c0 += LINES) {  // column inverses, keep rows x_step * i
-        const int ln = c0 + l;
-        const bool ok = ln < NI * P;
-        const int j = ok ? ln / P : 0, y = ok ? ln - j * P : 0;
-        float2* col = pls + j * PV + y;
-        float2 v[R2];
-#pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? col[(t + R1 * n2) * PYP] : make_float2(0.f, 0.f);
-        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
-            const int i = k / x_step;
-            if (ok && i * x_step == k && i < xc) col[i * PYP] = val;
-        });
-    }
-    __syncthreads();
-    for (int r0 = 0; r0 < NI * xc; r0 += LINES) {  // row inverses of the kept rows
-        const int ln = r0 + l;
-        const bool ok = ln < NI * xc;
-        const int j = ok ? ln / xc : 0, i = ok ? ln - j * xc : 0;
-        const float2* row = pls + j * PV + i * PYP;
-        float2 v[R2];
-#pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) v[n2] = (ok && t < R1) ? row[t + R1 * n2] : make_float2(0.f, 0.f);
-        float2* o = out + ((grp * F + part * NI + j) * Zh + zb) * (int64_t(xc) * yc) + i * yc;
-        line_fft<P, true>(v, xb, tw, t, [&](int k, float2 val) {
-            const int jj = k / y_step;
-            if (ok && jj * y_step == k && jj < yc) o[jj] = val;
-        });
-    }
-}
 
 struct zinv_args {
     int xc, yc;                        // kept block per z-bin plane (compact input)
@@ -2894,14 +2745,8 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
                 auto run = [&](auto ni) {
                     constexpr int NI = decltype(ni)::value;
                     require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
-                    if (!std::getenv("ZNN_FFT_XY_LINES")) {  // one line per thread in registers
-                        allow_smem(fft_xy_fwd_reg_k<PY, NI>, smem_xy_reg<PY, NI>());
-                        fft_xy_fwd_reg_k<PY, NI><<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
-                            spec, int(n.x), int(n.y), int(p.Zh), quad);
-                        return;
-                    }
-                    allow_smem(fft_xy_fwd_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
-                    fft_xy_fwd_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
+                    allow_smem(fft_xy_fwd_reg_k<PY, NI>, smem_xy_reg<PY, NI>());
+                    fft_xy_fwd_reg_k<PY, NI><<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
                         spec, int(n.x), int(n.y), int(p.Zh), quad);
                 };
                 const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
@@ -3006,21 +2851,15 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                 auto run = [&](auto ni) {
                     constexpr int NI = decltype(ni)::value;
                     require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
-                    if (!std::getenv("ZNN_FFT_XY_LINES")) {
-                        auto go = [&](auto kern) {
-                            allow_smem(kern, smem_xy_reg<PY, NI>());
-                            kern<<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
-                                spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
-                        };
-                        if (step.x == 1 && step.y == 1)
-                            go(fft_xy_inv_reg_k<PY, NI, true>);
-                        else
-                            go(fft_xy_inv_reg_k<PY, NI, false>);
-                        return;
-                    }
-                    allow_smem(fft_xy_inv_grp_k<PY, NI>, smem_xy_grp<PY, NI>());
-                    fft_xy_inv_grp_k<PY, NI><<<unsigned(planes / NI), THREADS, smem_xy_grp<PY, NI>(), st>>>(
-                        spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
+                    auto go = [&](auto kern) {
+                        allow_smem(kern, smem_xy_reg<PY, NI>());
+                        kern<<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
+                            spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
+                    };
+                    if (step.x == 1 && step.y == 1)
+                        go(fft_xy_inv_reg_k<PY, NI, true>);
+                    else
+                        go(fft_xy_inv_reg_k<PY, NI, false>);
                 };
                 const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
                 if (ni == 1) run(std::integral_constant<int, 1>{});
