@@ -32,6 +32,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "bgemm_tc.hpp"
 #include "tc_common.cuh"
@@ -462,7 +463,8 @@ void cgemm(cudaStream_t st, int mode, const float2* Ap, const float2* Bp, float2
 }  // namespace
 
 bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo) {
-    return Bn >= 64 && f <= 128 && fo <= 128 && f % 8 == 0 && fo % 8 == 0;
+    const char* e = std::getenv("ZNN_TC_MIN_BN");
+    return Bn >= (e ? std::atoi(e) : 32) && f <= 128 && fo <= 128 && f % 8 == 0 && fo % 8 == 0;
 }
 
 void tc_cmac_fwd(cudaStream_t st, const float2* X, const float2* K, float2* Y, int64_t Bn, int64_t f, int64_t fo,

@@ -20,7 +20,7 @@
 namespace znn_gpu {
 
 // shapes the kernels take: f, f' <= 128 and multiples of 8 (N of one MMA),
-// Bn >= 64 phase images (reuse of every kernel-spectrum bin; below, the
+// Bn >= 32 phase images (reuse of every kernel-spectrum bin; below, the
 // register-tiled FMA CMACs are faster: an M = 128 tile would be mostly empty)
 bool tc_cmac_supported(int64_t Bn, int64_t f, int64_t fo);
 // row-bin-major spectra: X [Bn][f], K [fo][f], G / Y [Bn][fo], DX [Bn][f], DK [fo][f]

@@ -1796,16 +1796,15 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_inv_reg_k(const float2* __re
                                                               const float* __restrict__ bias, float* __restrict__ out) {
     constexpr int Zh = P / 2 + 1, SP = zr_pitch(P);
     __shared__ float2 tw[P];
-    __shared__ int64_t obase[ZR_LINES];
     __shared__ float bvals[ZR_LINES];
-    __shared__ int ozoff[ZR_LINES];
     extern __shared__ float stage[];
     fill_twiddles<P>(tw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t wl0 = int64_t(blockIdx.x) * ZR_LINES + warp * 64;
     const uint32_t per = uint32_t(g.xc) * uint32_t(g.yc);
     const int64_t zstride = int64_t(g.xc) * g.yc;
-    int64_t ib[2];
+    int64_t ib[2], obh[2];
+    int ozh[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // decode this thread's two lines
         const int l = lane + 32 * h;
@@ -1833,8 +1832,7 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_inv_reg_k(const float2* __re
             }
             bv = bias ? bias[im % uint32_t(g.bias_mod)] : 0.f;
         }
-        obase[warp * 64 + l] = ob;
-        ozoff[warp * 64 + l] = oz;
+        obh[h] = ob, ozh[h] = oz;
         bvals[warp * 64 + l] = bv;
     }
     float2 v[P];
@@ -1863,15 +1861,34 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_inv_reg_k(const float2* __re
         }
     }
     __syncwarp();
+    // warp-cooperative stores of each line (lanes along the kept z); line l's
+    // output base comes from lane l % 32 by shuffles, the per-lane z offsets
+    // and staging indices are loop invariant
     const int zst = g.phased ? g.ph.sz : 1;
-    for (int l = 0; l < 64; ++l) {  // warp-cooperative stores of each line (lanes along the kept z)
-        const int64_t ob = obase[warp * 64 + l];
+    constexpr int NQ = (P + 31) / 32;
+    int zo[NQ], so[NQ];
+    bool qa[NQ];
+#pragma unroll
+    for (int u = 0; u < NQ; ++u) {
+        const int q = lane + 32 * u;
+        qa[u] = q < g.z_cnt;
+        zo[u] = zst * q;
+        so[u] = q * g.z_step;
+    }
+    const int znz = g.phased ? g.ph.nz : 1 << 30;
+#pragma unroll 4
+    for (int l = 0; l < 64; ++l) {
+        const int src = l & 31;
+        const bool hi = l >= 32;  // (uniform)
+        const int64_t ob = __shfl_sync(0xffffffffu, hi ? obh[1] : obh[0], src);
+        const int oz = __shfl_sync(0xffffffffu, hi ? ozh[1] : ozh[0], src);
         if (ob < 0) continue;  // (uniform) past the end, or a ragged phase line outside the tensor
-        const int oz = ozoff[warp * 64 + l];
-        const int zlim = g.phased ? g.ph.nz - oz : 1 << 30;
         float* dst = out + ob + oz;
-        for (int q = lane; q < g.z_cnt; q += 32)
-            if (zst * q < zlim) dst[zst * q] = wst[l * SP + q * g.z_step];
+        const float* sl = wst + l * SP;
+        const int zlim = znz - oz;
+#pragma unroll
+        for (int u = 0; u < NQ; ++u)
+            if (qa[u] && zo[u] < zlim) dst[zo[u]] = sl[so[u]];
     }
 }
 
