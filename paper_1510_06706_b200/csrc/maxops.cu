@@ -28,11 +28,15 @@ inline dim3 vblock() { return dim3(ZL, YR, 1); }
 
 // KX/KY/KZ > 0: compile-time window (fully unrolled, the common 2^3 and
 // 1x2x2 filters); 0: runtime window.
+// gate (window codes only): a window whose maximum is not > 0 gets code bit 7
+// set, so the backward passes no gradient through it: the ReLU backward of
+// the layer feeding the filter (ReLU'(0) = 0, transfer.hpp:99-106), folded in
+// exactly because the argmax voxel holds the window's maximum
 template <int KX, int KY, int KZ, typename M>
 __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restrict__ x, int nx, int ny, int nz,
                                                            int mx, int my, int mz, int kx_, int ky_, int kz_, int sx,
                                                            int sy, int sz, float* __restrict__ y,
-                                                           M* __restrict__ mask) {
+                                                           M* __restrict__ mask, int gate) {
     constexpr bool CODE = sizeof(M) == 1;
     const int kx = KX ? KX : kx_, ky = KY ? KY : ky_, kz = KZ ? KZ : kz_;
     const int j = blockIdx.x * YR + threadIdx.y, i = blockIdx.y;
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
                         }
             __stcs(yr + l, best);
             if constexpr (CODE)
-                mr[l] = M(best_code);
+                mr[l] = M(best_code | ((gate && !(best > 0.f)) ? 0x80 : 0));
             else
                 __stcs(mr + l, M(rbase + l + best_off));
 #pragma unroll
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
                     }
             __stcs(yr + l, best);
             if constexpr (CODE)
-                mr[l] = M(best_code);
+                mr[l] = M(best_code | ((gate && !(best > 0.f)) ? 0x80 : 0));
             else
                 __stcs(mr + l, M(best_idx));
         }
@@ -294,19 +298,20 @@ __global__ void __launch_bounds__(ZL * YR) maxpool_bwd_k(const float* __restrict
 
 namespace {
 template <typename M>
-void maxfilter_fwd_t(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y, M* mask) {
+void maxfilter_fwd_t(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y, M* mask,
+                     int gate = 0) {
     const dims3 m{n.x - s.x * (k.x - 1), n.y - s.y * (k.y - 1), n.z - s.z * (k.z - 1)};
     require(m.x > 0 && m.y > 0 && m.z > 0, "maxfilter_forward: effective window exceeds input");
     prof_scope ps(st, "maxfilter_fwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
                   double(maps) * (4.0 * double(n.vol()) + (4.0 + sizeof(M)) * double(m.vol())), 0);
     require(n.vol() < (int64_t(1) << 31), "maxfilter_forward: map exceeds int32 mask range");
-    require(sizeof(M) == 4 || k.vol() <= 256, "maxfilter_forward: window too large for one-byte codes");
+    require(sizeof(M) == 4 || k.vol() <= (gate ? 128 : 256), "maxfilter_forward: window too large for one-byte codes");
     auto* kf = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_fwd_k<2, 2, 2, M>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2, M>
                                                     : maxfilter_fwd_k<0, 0, 0, M>;
     kf<<<vgrid(m.y, m.x, maps), vblock(), 0, st>>>(x, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
                                                   int(k.x), int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), y,
-                                                  mask);
+                                                  mask, gate);
     launch_check("maxfilter_fwd");
 }
 
@@ -339,8 +344,8 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
     maxfilter_fwd_t(st, x, maps, n, k, s, y, mask);
 }
 void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y,
-                   uint8_t* code) {
-    maxfilter_fwd_t(st, x, maps, n, k, s, y, code);
+                   uint8_t* code, bool relu_gate) {
+    maxfilter_fwd_t(st, x, maps, n, k, s, y, code, relu_gate ? 1 : 0);
 }
 void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m, dims3 k, dims3 s,
                    float* dx) {

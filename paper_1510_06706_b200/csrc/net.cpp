@@ -277,6 +277,22 @@ void executor::allocate() {
             G.code = static_cast<uint8_t*>(dalloc(nv));
         }
     }
+    // a max-filter whose input is the ReLU output of a fused conv layer (and
+    // its only consumer) folds that ReLU backward into its window codes; the
+    // conv's backward then skips its own gate (ZNN_NO_RELU_FUSION=1: off)
+    if (!std::getenv("ZNN_NO_RELU_FUSION")) {
+        for (auto& F : layers_) {
+            if (F.kind != lkind::filter || F.k.vol() > 128) continue;
+            int consumers = 0;
+            for (const auto& L2 : layers_) consumers += L2.in == F.in;
+            for (auto& C : layers_)
+                if (C.kind == lkind::conv && C.out == F.in && C.fused && C.fused_act == 2 &&
+                    consumers == 1) {
+                    F.relu_gate = true;
+                    C.pregated = true;
+                }
+        }
+    }
     if (!cfg_.keep_images) {
         gbuf_[0] = static_cast<float*>(dalloc(sizeof(float) * size_t(maxsz)));
         gbuf_[1] = static_cast<float*>(dalloc(sizeof(float) * size_t(maxsz)));
@@ -556,7 +572,7 @@ void executor::run_forward(const float* in_dev) {
                 break;
             case lkind::pool: znn_gpu::maxpool_fwd(st_, I.act, B * I.maps, I.dims, L.k, O.act, O.mask); break;
             case lkind::filter:
-                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.code);
+                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.code, L.relu_gate);
                 break;
         }
     }
@@ -604,7 +620,8 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                 const bool fuse_relu = L.fused && L.engine == 1 && !ce_here && L.fused_act == 2 &&
                                        !std::getenv("ZNN_NO_RELU_FUSION");
                 if (fuse_relu) {
-                    run_conv_bwd(L, O.grad, I.grad, L.in != 0, update, O.act, grads_ + L.b_off);
+                    run_conv_bwd(L, O.grad, I.grad, L.in != 0, update, L.pregated ? nullptr : O.act,
+                                 grads_ + L.b_off);
                     if (update)
                         znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off,
                                               L.shape.f_out, cfg_.lr, cfg_.mu);
@@ -712,7 +729,7 @@ void executor::group_mask(int gi, int32_t* host) {
     for (int64_t e = 0; e < n; ++e) {
         const int64_t v = e % mv;
         const int64_t i = v / (m.y * m.z), j = (v / m.z) % m.y, l = v % m.z;
-        const int c = code[size_t(e)];
+        const int c = code[size_t(e)] & 0x7F;  // (bit 7: the ReLU gate, not part of the argmax)
         const int64_t a = c / (k.y * k.z), b = (c / k.z) % k.y, cz = c % k.z;
         host[e] = int32_t(((i + s.x * a) * in.y + (j + s.y * b)) * in.z + (l + s.z * cz));
     }

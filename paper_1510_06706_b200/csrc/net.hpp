@@ -52,6 +52,8 @@ struct layer {
     int32_t* none_dev = nullptr;  // identity kinds (CE: loss already gave a - d)
     // pool / filter
     dims3 k{1, 1, 1}, s{1, 1, 1};
+    bool relu_gate = false;     // filter: its codes carry the ReLU backward of the conv feeding it
+    bool pregated = false;      // conv with fused ReLU: the gradient arrives gated (by a relu_gate filter)
     std::vector<int> edge_ids;  // reference edges covered (map order)
     std::vector<int> transfer_edge_ids;
 };

@@ -96,8 +96,10 @@ void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t
                    dims3 k, dims3 s, float* dx);
 // one-byte window codes (a ky + b) kz + c instead of flat indices (windows of
 // at most 256 taps; the executor's internal max-filters)
+// relu_gate: windows whose maximum is not > 0 get code bit 7 (the backward
+// then also applies the ReLU backward of the layer feeding the filter)
 void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s,
-                   float* y, uint8_t* code);
+                   float* y, uint8_t* code, bool relu_gate = false);
 void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m,
                    dims3 k, dims3 s, float* dx);
 
