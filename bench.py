@@ -141,8 +141,13 @@ def run_reference(args):
     from paper_1510_06706_b200 import configs
     cfg = configs.CONFIGS[args.config]
     out_vox = int(np.prod(cfg.out_dims))
-    cb = cpu_baseline(cfg, warmup=args.warmup, rounds=args.steps,
-                      budget_s=float(os.environ.get("ZNN_REF_BUDGET_S", "3000")))
+    # A c5 reference round takes ~55 s on 16 host threads, so the run is bounded
+    # to a few minutes: at most ZNN_REF_WARMUP_MAX (1) warm-up rounds (pools and
+    # plans are built in the first one) and measured rounds until the
+    # ZNN_REF_BUDGET_S (240 s) budget, at least one; "steps" says how many ran.
+    warm = min(args.warmup, int(os.environ.get("ZNN_REF_WARMUP_MAX", "1")))
+    cb = cpu_baseline(cfg, warmup=warm, rounds=args.steps,
+                      budget_s=float(os.environ.get("ZNN_REF_BUDGET_S", "240")))
     v = cb["value"]
     steps = int(cb.get("rounds", args.steps))
     line = {"metric": "train_output_voxels_per_s", "value": v, "unit": "voxels/s", "n_gpus": args.gpus,
