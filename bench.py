@@ -33,6 +33,9 @@ def parse():
     p.add_argument("--config", default=os.environ.get("ZNN_BENCH_CONFIG", "c5"))
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--engine", default=None)
+    p.add_argument("--layer-engines", default=None,
+                   help="comma list (direct|fft|simt per conv layer) instead of the autotuner: "
+                        "ncu captures of the step without the tuner's candidate launches")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
@@ -187,6 +190,9 @@ def run_ours(args):
 
     cfg = configs.CONFIGS[args.config]
     engine = args.engine or cfg.engine
+    fixed = args.layer_engines.split(",") if args.layer_engines else None
+    if fixed:
+        engine = "direct"
     B = cfg.batch
     lo, hi = shard_range(B, world, rank)
     Bl = hi - lo
@@ -196,6 +202,11 @@ def run_ours(args):
     net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=Bl, global_batch=B, lr=cfg.lr,
               momentum=cfg.momentum, loss=cfg.loss, engine=engine)
     net.set_params(configs.init_params(cfg, 2026))
+    if fixed:
+        for i, e in enumerate(fixed):
+            net.set_layer_engine(i, e)
+        net.engines = [{"direct": 0, "fft": 1, "simt": 3}[e] for e in fixed]
+        engine = "fixed:" + args.layer_engines
     comm = None
     if world > 1:  # the library's own NCCL communicator (per-layer allreduce buckets overlap the backward)
         uid = [comm_unique_id() if rank == 0 else None]
