@@ -850,6 +850,7 @@ struct cube_io {
     int phased;
     phase_geom ph;
     int gF;                  // row-bin-major spectra: maps per row (0: image-major)
+    int vec4;                // dense z lines of whole float4s (16-byte aligned): vector loads / stores
 };
 
 template <int P>
@@ -1215,15 +1216,36 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_fwd_reg_k(cube_io a, 
         } else {
             base = int64_t(img0 + j) * a.img_stride + int64_t(l1) * a.nz;
         }
+        if (a.vec4) {  // dense images (phase-major tensors): a line is nz / 4 aligned float4s
+            const float4* __restrict__ p4 = reinterpret_cast<const float4*>(a.src + base);
+            const float4* __restrict__ g4 = a.gate ? reinterpret_cast<const float4*>(a.gate + base) : nullptr;
 #pragma unroll
-        for (int z = 0; z < P; ++z) {
-            float val = 0.f;
-            const int zz = z0 + zs * z;
-            if (z < a.nz && zz < zlim) {
-                val = __ldg(a.src + base + zz);
-                if (a.gate && !(__ldg(a.gate + base + zz) > 0.f)) val = 0.f;
+            for (int z4 = 0; z4 < (P + 3) / 4; ++z4) {
+                float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (4 * z4 < a.nz) {
+                    u = __ldg(p4 + z4);
+                    if (g4) {
+                        const float4 gt = __ldg(g4 + z4);
+                        u.x = gt.x > 0.f ? u.x : 0.f, u.y = gt.y > 0.f ? u.y : 0.f;
+                        u.z = gt.z > 0.f ? u.z : 0.f, u.w = gt.w > 0.f ? u.w : 0.f;
+                    }
+                }
+                if (4 * z4 < P) v[4 * z4] = make_float2(u.x, 0.f);
+                if (4 * z4 + 1 < P) v[4 * z4 + 1 < P ? 4 * z4 + 1 : 0] = make_float2(u.y, 0.f);
+                if (4 * z4 + 2 < P) v[4 * z4 + 2 < P ? 4 * z4 + 2 : 0] = make_float2(u.z, 0.f);
+                if (4 * z4 + 3 < P) v[4 * z4 + 3 < P ? 4 * z4 + 3 : 0] = make_float2(u.w, 0.f);
             }
-            v[z] = make_float2(val, 0.f);
+        } else {
+#pragma unroll
+            for (int z = 0; z < P; ++z) {
+                float val = 0.f;
+                const int zz = z0 + zs * z;
+                if (z < a.nz && zz < zlim) {
+                    val = __ldg(a.src + base + zz);
+                    if (a.gate && !(__ldg(a.gate + base + zz) > 0.f)) val = 0.f;
+                }
+                v[z] = make_float2(val, 0.f);
+            }
         }
         dft_r<P, P, false>(v, tw);
         float2* cube = cubes + j * CV;
@@ -1397,6 +1419,24 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_inv_reg_k(const float
             base = int64_t(img) * a.img_stride + (int64_t(i) * a.oy + jj) * a.oz;
         }
         if (base < 0) continue;
+        if constexpr (UNIT) {
+            if (a.vec4) {  // dense output lines of zc / 4 aligned float4s (phase-major tensors)
+                auto fin = [&](float x) {
+                    float r = x * a.scale + bv;
+                    if (a.act == 2) r = r > 0.f ? r : 0.f;
+                    else if (a.act == 0) r = 1.f / (1.f + expf(-r));
+                    else if (a.act == 1) r = tanhf(r);
+                    return r;
+                };
+                float4* __restrict__ d4 = reinterpret_cast<float4*>(a.dst + base);
+#pragma unroll
+                for (int q4 = 0; q4 < P / 4; ++q4)
+                    if (4 * q4 < a.zc)
+                        d4[q4] = make_float4(fin(v[4 * q4].x), fin(v[4 * q4 + 1].x), fin(v[4 * q4 + 2].x),
+                                             fin(v[4 * q4 + 3].x));
+                continue;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < P; ++q) {
             const int k = UNIT ? q : q * a.zs;
@@ -2687,6 +2727,8 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         a.phased = ph ? 1 : 0;
         if (ph) a.ph = *ph;
         a.gF = quad;
+        a.vec4 = !ph && n.z % 4 == 0 && in_img_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(gate) & 15) == 0;
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
@@ -2814,6 +2856,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
         a.gF = quad;
         require(imgs < (int64_t(1) << 31), "fft: too many images");
         const bool unit = a.xs == 1 && a.ys == 1 && a.zs == 1;
+        a.vec4 = !ph && unit && cnt.z % 4 == 0 && out_img_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
         dispatch_pad(int(p.P.x), [&](auto pc) {
             constexpr int PP = decltype(pc)::value;
             auto go = [&](auto k, int64_t ctas, int threads, size_t sm) {
@@ -3334,9 +3377,21 @@ void phase_merge(cudaStream_t st, const conv_shape& c, const float* yp, int64_t 
 
 }  // namespace
 
+// A dilated layer's tensors may be phase-major ([B s^3][maps][n / s], the
+// dense images of the polyphase plan) instead of the natural [B][maps][n]:
+// a convolution with sparsity s maps phase r of its input to phase r of its
+// output, so a chain of FFT layers with one sparsity never needs the
+// interleaved order in between (the executor decides, net.cpp)
+bool phase_major_ok(const conv_shape& c) {
+    if (!use_poly(c) || c.f_in == 1 || std::getenv("ZNN_FFT_PHASE_SPLIT")) return false;
+    return c.n.x % c.s.x == 0 && c.n.y % c.s.y == 0 && c.n.z % c.s.z == 0 && c.m.x % c.s.x == 0 &&
+           c.m.y % c.s.y == 0 && c.m.z % c.s.z == 0;
+}
+
 void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
-              int act, float* y, znn_gpu::scratch& ws) {
+              int act, float* y, znn_gpu::scratch& ws, bool x_pm, bool y_pm) {
     require(p.B == c.B * p.S && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");
+    require((!x_pm && !y_pm) || (p.poly && phase_major_ok(c)), "fft engine: phase-major tensors need a polyphase plan");
     if (!p.poly) {
         conv_fwd_core(st, p, c, x, w, bias, act, y, ws);
         return;
@@ -3346,7 +3401,7 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
     // pass); ZNN_FFT_PHASE_SPLIT=1 keeps the explicit split / merge kernels
     if (!fused1_ok(p, e) && !std::getenv("ZNN_FFT_PHASE_SPLIT")) {
         const phase_geom gi = geom(c, c.f_in, c.n, e.n), go = geom(c, c.f_out, c.m, e.m);
-        conv_fwd_core(st, p, e, x, w, bias, act, y, ws, &gi, &go);
+        conv_fwd_core(st, p, e, x, w, bias, act, y, ws, x_pm ? nullptr : &gi, y_pm ? nullptr : &go);
         return;
     }
     float* xp = static_cast<float*>(p.phase_ws->get(size_t(p.ph_bytes)));
@@ -3361,15 +3416,17 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
 }
 
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float*, const float* g, const float* w, float* gw,
-              float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias) {
+              float* gin, znn_gpu::scratch& ws, const float* relu_y, float* dbias, bool x_pm, bool y_pm) {
+    require((!x_pm && !y_pm) || (p.poly && phase_major_ok(c)), "fft engine: phase-major tensors need a polyphase plan");
     if (!p.poly) {
         conv_bwd_core(st, p, c, g, w, gw, gin, ws, relu_y, dbias);
         return;
     }
     const conv_shape& e = p.ce;
     if (!fused1_ok(p, e) && !std::getenv("ZNN_FFT_PHASE_SPLIT")) {
+        // g and the gate relu_y share the output tensor's order, gin the input's
         const phase_geom gg = geom(c, c.f_out, c.m, e.m), gx = geom(c, c.f_in, c.n, e.n);
-        conv_bwd_core(st, p, e, g, w, gw, gin, ws, relu_y, dbias, &gg, &gx);
+        conv_bwd_core(st, p, e, g, w, gw, gin, ws, relu_y, dbias, y_pm ? nullptr : &gg, x_pm ? nullptr : &gx);
         return;
     }
     float* dxp = static_cast<float*>(p.phase_ws->get(size_t(p.ph_bytes)));

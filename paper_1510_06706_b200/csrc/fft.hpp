@@ -63,8 +63,12 @@ void pad_dims(const plan& p, int64_t out[3]);
 
 // forward: y = act(bias + sum_i IFFT(X_i * conj(K_oi))) cropped (conv_fft.hpp:38-60);
 // memoises X (image spectra) and K (kernel spectra) in the plan.
+// x_pm / y_pm: the input / output tensor is phase-major ([B s^3][maps][n / s],
+// phase r = (rx sy + ry) sz + rz) instead of [B][maps][n]; phase_major_ok(c)
+// says whether the layer's plan can take such tensors.
+bool phase_major_ok(const conv_shape& c);
 void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w,
-              const float* bias, int act, float* y, znn_gpu::scratch& ws);
+              const float* bias, int act, float* y, znn_gpu::scratch& ws, bool x_pm = false, bool y_pm = false);
 // backward + update from the memo: gin = IFFT(sum_o G_o * K_oi) (no conjugate,
 // conv_fft.hpp:67-96, skipped when gin == nullptr) and
 // gw = IFFT(sum_b X_bi * conj(G_bo))[s*w] (conv_fft.hpp:98-125). With relu_y,
@@ -72,7 +76,7 @@ void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, con
 // and dbias[o] receives its bias gradient (the DC term summed over patches).
 void conv_bwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* g,
               const float* w, float* gw, float* gin, znn_gpu::scratch& ws, const float* relu_y = nullptr,
-              float* dbias = nullptr);
+              float* dbias = nullptr, bool x_pm = false, bool y_pm = false);
 
 // average device time (ms) of one CMAC launch on synthetic spectra (roofline probe)
 float time_cmac(cudaStream_t st, int which, const conv_shape& c, int reps, int64_t* bins_out);

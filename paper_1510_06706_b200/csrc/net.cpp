@@ -521,7 +521,8 @@ void executor::run_conv_fwd(layer& L) {
     const float* bias = L.fused ? params_ + L.b_off : nullptr;
     const int act = L.fused ? L.fused_act : 3;
     if (L.engine == 1) {
-        znn_fft::conv_fwd(st_, fft_plan(L), L.shape, x, w, bias, act, y, ws_);
+        znn_fft::conv_fwd(st_, fft_plan(L), L.shape, x, w, bias, act, y, ws_, groups_[size_t(L.in)].pm,
+                          groups_[size_t(L.out)].pm);
     } else if (L.engine == 0 && znn_gpu::conv_tc_supported(L.shape, 0)) {
         znn_gpu::conv_fwd_tc(st_, L.shape, x, w, bias, act, y, ws_);
     } else {
@@ -536,7 +537,8 @@ void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad
     float* gw = grads_ + L.w_off;
     const int64_t wcount = L.shape.f_out * L.shape.f_in * L.shape.taps();
     if (L.engine == 1) {
-        znn_fft::conv_bwd(st_, fft_plan(L), L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_, relu_y, dbias);
+        znn_fft::conv_bwd(st_, fft_plan(L), L.shape, x, g_out, w, gw, need_dgrad ? g_in : nullptr, ws_, relu_y, dbias,
+                          groups_[size_t(L.in)].pm, groups_[size_t(L.out)].pm);
         if (update) znn_gpu::sgd_momentum(st_, w, vel_ + L.w_off, gw, wcount, cfg_.lr, cfg_.mu);
         return;
     }
@@ -559,7 +561,46 @@ void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad
     if (need_dgrad && !update) dgrad();
 }
 
+// Tensor order of the groups between FFT layers. A convolution with sparsity
+// s maps phase r of its input (voxels s q + r) to phase r of its output, so a
+// group written by one polyphase FFT layer and read by another of the same
+// sparsity (c5: conv3 -> conv4 -> conv5, s = 4) stays phase-major: both
+// layers' transforms then read / write dense phase images with whole-sector
+// vector accesses instead of every s-th float of the interleaved tensor, and
+// so do the gradient of that group and the fused ReLU gate. Nothing else may
+// touch the group: the producer's transfer is fused (ReLU gate inside the
+// gradient transform) or absent. ZNN_PHASE_MAJOR=0: natural order everywhere.
+void executor::plan_layouts() {
+    const char* env = std::getenv("ZNN_PHASE_MAJOR");
+    const bool on = !(env && std::string(env) == "0") && !cfg_.keep_images;
+    const bool relu_fusion = !std::getenv("ZNN_NO_RELU_FUSION");
+    std::string note;
+    for (size_t j = 1; j + 1 < groups_.size(); ++j) {
+        group& G = groups_[j];
+        const layer *A = nullptr, *C = nullptr;
+        int np = 0, nc = 0;
+        for (const auto& L : layers_) {
+            if (L.out == int(j)) A = &L, ++np;
+            if (L.in == int(j)) C = &L, ++nc;
+        }
+        bool pm = on && G.materialized && np == 1 && nc == 1 && A->kind == lkind::conv && C->kind == lkind::conv &&
+                  A->engine == 1 && C->engine == 1 && znn_fft::supported(A->shape) && znn_fft::supported(C->shape) &&
+                  znn_fft::phase_major_ok(A->shape) && znn_fft::phase_major_ok(C->shape) &&
+                  A->shape.s.x == C->shape.s.x && A->shape.s.y == C->shape.s.y && A->shape.s.z == C->shape.s.z &&
+                  (!A->fused || (A->fused_act == 2 && relu_fusion && !A->pregated));
+        if (pm != G.pm) drop_graph();
+        G.pm = pm;
+        G.pm_s = pm ? A->shape.s : dims3{1, 1, 1};
+        if (pm) note += " " + std::to_string(j);
+    }
+    if (note != layout_note_) {
+        layout_note_ = note;
+        if (!note.empty()) desc_ += "phase-major groups:" + note + "\n";
+    }
+}
+
 void executor::run_forward(const float* in_dev) {
+    plan_layouts();
     groups_[0].act = const_cast<float*>(in_dev);
     const int64_t B = cfg_.batch;
     for (auto& L : layers_) {
@@ -701,9 +742,28 @@ void executor::group_image(int gi, int which, float* host) {
     require(G.materialized, "group image: group " + std::to_string(gi) + " is fused away");
     const float* src = which == 0 ? G.act : G.grad;
     require(src != nullptr, "group image: image not available");
-    ZNN_CUDA_CHECK(cudaMemcpyAsync(host, src, sizeof(float) * size_t(cfg_.batch * G.maps * G.dims.vol()),
-                                   cudaMemcpyDeviceToHost, st_));
+    const int64_t total = cfg_.batch * G.maps * G.dims.vol();
+    if (!G.pm) {
+        ZNN_CUDA_CHECK(cudaMemcpyAsync(host, src, sizeof(float) * size_t(total), cudaMemcpyDeviceToHost, st_));
+        ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+        return;
+    }
+    // phase-major group: back to [B][maps][x][y][z] on the host
+    std::vector<float> pmv(static_cast<size_t>(total));
+    ZNN_CUDA_CHECK(cudaMemcpyAsync(pmv.data(), src, sizeof(float) * size_t(total), cudaMemcpyDeviceToHost, st_));
     ZNN_CUDA_CHECK(cudaStreamSynchronize(st_));
+    const dims3 s = G.pm_s, n = G.dims, q{n.x / s.x, n.y / s.y, n.z / s.z};
+    const int64_t S = s.vol();
+    for (int64_t b = 0; b < cfg_.batch; ++b)
+        for (int64_t m = 0; m < G.maps; ++m)
+            for (int64_t x = 0; x < n.x; ++x)
+                for (int64_t y = 0; y < n.y; ++y)
+                    for (int64_t z = 0; z < n.z; ++z) {
+                        const int64_t r = ((x % s.x) * s.y + (y % s.y)) * s.z + (z % s.z);
+                        const int64_t img = (b * S + r) * G.maps + m;
+                        host[((b * G.maps + m) * n.x + x) * n.y * n.z + y * n.z + z] =
+                            pmv[size_t(((img * q.x + x / s.x) * q.y + y / s.y) * q.z + z / s.z)];
+                    }
 }
 
 void executor::group_mask(int gi, int32_t* host) {
@@ -742,6 +802,7 @@ std::vector<int> executor::autotune(int trials) {
     ZNN_CUDA_CHECK(cudaEventCreate(&a));
     ZNN_CUDA_CHECK(cudaEventCreate(&b));
     std::ostringstream report;  // appended to describe(): per-layer median fwd+bwd+upd times
+    for (auto& G : groups_) G.pm = false;  // candidates are timed on natural-order tensors
     int ci = 0;
     for (auto& L : layers_) {
         if (L.kind != lkind::conv) continue;

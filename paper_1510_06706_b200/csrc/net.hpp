@@ -31,6 +31,11 @@ struct group {
     int32_t* mask = nullptr; // argmax record (flat index) when produced by a pool
     uint8_t* code = nullptr; // argmax record (window code) when produced by a max-filter
     bool materialized = true;
+    // phase-major order [B s^3][maps][dims / s] (phase r = (rx sy + ry) sz + rz holds
+    // the voxels s q + r) instead of [B][maps][dims]: between two FFT layers
+    // of the same sparsity (executor::plan_layouts)
+    bool pm = false;
+    dims3 pm_s{1, 1, 1};
 };
 
 enum class lkind { conv, transfer, pool, filter };
@@ -132,6 +137,7 @@ private:
     znn_fft::plan& fft_plan(layer& L);
     bool fft_pooled(const layer& L);
     void plan_fft_memory();
+    void plan_layouts();
     void drop_fft_plans();
     void drop_graph();
     bool fft_decided_ = false;
@@ -155,6 +161,7 @@ private:
     std::vector<group> groups_;
     std::vector<layer> layers_;
     std::string desc_;
+    std::string layout_note_;  // phase-major groups currently planned
     int64_t flat_ = 0;
     float* params_ = nullptr;
     float* grads_ = nullptr;

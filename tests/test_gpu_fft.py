@@ -310,3 +310,36 @@ def test_fft_tensor_core_cmacs(ctx, monkeypatch, shape, tc):
         for i in range(0, fi, 5):
             ref = sum(O.kernel_grad(x[b, i], g[b, o], k, s) for b in range(B))
             assert O.max_rel_error(dw[o, i], ref) < 1e-3, ("wgrad", o, i)
+
+
+def test_phase_major_groups_between_fft_layers(ctx, monkeypatch):
+    """Groups between FFT layers of one sparsity (scaled c5: conv3 -> conv4 ->
+    conv5, s = 4, dims divisible by 4) are kept phase-major by the executor:
+    one step matches the oracle (fwd 1e-4, gradients and updated weights 1e-3),
+    the group images read back in natural order equal the natural-order run's,
+    and so do the gradients."""
+    from paper_1510_06706_b200 import configs as C
+    cfg = C.scaled("c5", 30, (4, 4, 4), batch=2)
+    nconv = len(cfg.conv_layers())
+    engines = ["fft"] * (nconv - 1) + ["direct"]
+    net, params, x, lab, loss, grads, newp = _net_one_step(ctx, cfg, engines)
+    desc = net.describe()
+    assert "phase-major groups:" in desc, desc
+    pm = [int(t) for t in desc.split("phase-major groups:")[-1].split("\n")[0].split()]
+    assert len(pm) == 2, desc  # conv3 -> conv4 and conv4 -> conv5
+    imgs = {g: net.group_image(g, 0) for g in pm}
+    g = O.parse_netspec(cfg.netspec(), cfg.out_dims)
+    ins = [[x[b, 0]] for b in range(cfg.batch)]
+    labs = [[lab[b, o] for o in range(lab.shape[1])] for b in range(cfg.batch)]
+    rl, rg, rp, _ = O.train_step(g, params.astype(np.float64), np.zeros(params.size), ins, labs, cfg.lr,
+                                 cfg.momentum, cfg.loss)
+    assert abs(loss - rl) / (abs(rl) + 1) < 1e-4
+    assert O.max_rel_error(grads, rg) < 1e-3
+    assert O.max_rel_error(newp, rp) < 1e-3
+    monkeypatch.setenv("ZNN_PHASE_MAJOR", "0")
+    net2, _, _, _, loss2, grads2, newp2 = _net_one_step(ctx, cfg, engines)
+    assert "phase-major groups:" not in net2.describe()
+    for gi, im in imgs.items():
+        assert O.max_rel_error(im, net2.group_image(gi, 0)) < 1e-6
+    assert abs(loss - loss2) / (abs(loss2) + 1) < 1e-6
+    assert O.max_rel_error(grads, grads2) < 1e-5

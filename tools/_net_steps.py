@@ -31,7 +31,8 @@ elif engines:
 for i in range(steps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    net.forward_backward(x, lab, sync_loss=False)
+    loss = net.forward_backward(x, lab, sync_loss=(i == steps - 1))
     net.apply_update()
     torch.cuda.synchronize()
-    print(f'step {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms', flush=True)
+    print(f'step {i}: {(time.perf_counter() - t0) * 1e3:.2f} ms' + (f' loss {loss:.9g}' if i == steps - 1 else ''), flush=True)
+print('\n'.join(l for l in net.describe().splitlines() if 'phase-major' in l), flush=True)
