@@ -3388,6 +3388,16 @@ bool phase_major_ok(const conv_shape& c) {
            c.m.y % c.s.y == 0 && c.m.z % c.s.z == 0;
 }
 
+// phase-major input pays off for a producer that has to scatter into it (the
+// max-filters) only where the strided in-place phase reads are the bound: the
+// fused small-cube transforms (the z passes at larger pads already read whole
+// sectors by pairing the z-phases of a line)
+bool phase_major_pays(const conv_shape& c) {
+    if (!phase_major_ok(c)) return false;
+    const dims3 P = pads_for(c);
+    return P.x == P.y && P.y == P.z && P.x > 1 && P.x <= REGP;
+}
+
 void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w, const float* bias,
               int act, float* y, znn_gpu::scratch& ws, bool x_pm, bool y_pm) {
     require(p.B == c.B * p.S && p.f == c.f_in && p.fo == c.f_out, "fft engine: plan/layer mismatch");

@@ -67,6 +67,7 @@ void pad_dims(const plan& p, int64_t out[3]);
 // phase r = (rx sy + ry) sz + rz) instead of [B][maps][n]; phase_major_ok(c)
 // says whether the layer's plan can take such tensors.
 bool phase_major_ok(const conv_shape& c);
+bool phase_major_pays(const conv_shape& c);  // worth a scattering producer (small-cube plans)
 void conv_fwd(cudaStream_t st, plan& p, const conv_shape& c, const float* x, const float* w,
               const float* bias, int act, float* y, znn_gpu::scratch& ws, bool x_pm = false, bool y_pm = false);
 // backward + update from the memo: gin = IFFT(sum_o G_o * K_oi) (no conjugate,

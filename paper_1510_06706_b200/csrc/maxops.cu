@@ -26,17 +26,33 @@ inline dim3 vgrid(int64_t y, int64_t x, int64_t maps) {
 }
 inline dim3 vblock() { return dim3(ZL, YR, 1); }
 
+// phase-major addressing of an output volume [maps = B f][mx][my][mz] stored
+// as [B S][f][mx / sx][my / sy][mz / sz] (ops.hpp pm_order)
+struct pm_dev {
+    int on, f, sx, sy, sz, zsh;
+    int qy, qz;        // phase image dims (y, z)
+    int64_t qvol;      // voxels of one phase image
+};
+// offset of row (i, j) of map `map`, z-phase 0, q = 0; voxel l of the row is at
+// + (l & (sz - 1)) * f * qvol + (l >> zsh)
+__device__ __forceinline__ int64_t pm_row(const pm_dev& P, int64_t map, int i, int j) {
+    const int64_t b = map / P.f, c = map - b * P.f;
+    const int rx = i % P.sx, ry = j % P.sy;
+    const int64_t img = (b * (P.sx * P.sy * P.sz) + (rx * P.sy + ry) * P.sz) * P.f + c;
+    return img * P.qvol + (int64_t(i / P.sx) * P.qy + j / P.sy) * P.qz;
+}
+
 // KX/KY/KZ > 0: compile-time window (fully unrolled, the common 2^3 and
 // 1x2x2 filters); 0: runtime window.
 // gate (window codes only): a window whose maximum is not > 0 gets code bit 7
 // set, so the backward passes no gradient through it: the ReLU backward of
 // the layer feeding the filter (ReLU'(0) = 0, transfer.hpp:99-106), folded in
 // exactly because the argmax voxel holds the window's maximum
-template <int KX, int KY, int KZ, typename M>
+template <int KX, int KY, int KZ, typename M, bool PM = false>
 __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restrict__ x, int nx, int ny, int nz,
                                                            int mx, int my, int mz, int kx_, int ky_, int kz_, int sx,
                                                            int sy, int sz, float* __restrict__ y,
-                                                           M* __restrict__ mask, int gate) {
+                                                           M* __restrict__ mask, int gate, pm_dev pm) {
     constexpr bool CODE = sizeof(M) == 1;
     const int kx = KX ? KX : kx_, ky = KY ? KY : ky_, kz = KZ ? KZ : kz_;
     const int j = blockIdx.x * YR + threadIdx.y, i = blockIdx.y;
@@ -44,6 +60,23 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
     const int64_t map = blockIdx.z;
     const float* xm = x + map * (int64_t(nx) * ny * nz);
     const int64_t orow = map * (int64_t(mx) * my * mz) + (int64_t(i) * my + j) * mz;
+    // phase-major output: voxel l of the row goes to its z-phase's image; a
+    // thread's voxels l = lane + 32 t share one z-phase (sz divides 32), so it
+    // keeps one pointer into that image, advanced 32 / sz per step
+    float* ypm = nullptr;
+    int ypm_step = 0;
+    if constexpr (PM) {
+        ypm = y + pm_row(pm, map, i, j) + int64_t(threadIdx.x & (pm.sz - 1)) * pm.f * pm.qvol + (threadIdx.x >> pm.zsh);
+        ypm_step = ZL >> pm.zsh;
+    }
+    auto put = [&](float* yr_, int l, float v) {
+        if constexpr (PM) {
+            __stcs(ypm, v);
+            ypm += ypm_step;
+        } else {
+            __stcs(yr_ + l, v);
+        }
+    };
     const int dx = sx * ny * nz, dy = sy * nz;
     const int rbase = (i * ny + j) * nz;
     const float* xr = xm + rbase;
@@ -78,7 +111,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
                             best_off = a * dx + b * dy + c * sz;
                             best_code = (a * KY + b) * KZ + c;
                         }
-            __stcs(yr + l, best);
+            put(yr, l, best);
             if constexpr (CODE)
                 mr[l] = M(best_code | ((gate && !(best > 0.f)) ? 0x80 : 0));
             else
@@ -104,7 +137,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
                             best_code = (a * ky + b) * kz + c;
                         }
                     }
-            __stcs(yr + l, best);
+            put(yr, l, best);
             if constexpr (CODE)
                 mr[l] = M(best_code | ((gate && !(best > 0.f)) ? 0x80 : 0));
             else
@@ -180,22 +213,28 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
 // serve input planes oi and oi + SX, half the loads of maxfilter_bwd_k.
 // Block = 32 z-lanes x 8 y-rows, grid = (y tiles, maps). Sums in ascending
 // window order like maxfilter_bwd_k.
-template <int SX, typename M>
+template <int SX, typename M, bool PM = false>
 __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restrict__ g,
                                                             const M* __restrict__ mask, int nx, int ny,
                                                             int nz, int mx, int my, int mz, int sy, int sz,
-                                                            float* __restrict__ dx) {
+                                                            float* __restrict__ dx, pm_dev pm) {
     constexpr bool CODE = sizeof(M) == 1;
     const int tj = blockIdx.x * YR + threadIdx.y;
     if (tj >= ny) return;
     const int64_t map = blockIdx.y;
     const int64_t pin = int64_t(ny) * nz, pout = int64_t(my) * mz;
-    const float* gm = g + map * (pout * mx);
+    // phase-major gradient: plane oi of map (b, c) starts at gpm0 + (oi % sx) * pxs + (oi / sx) * qy * qz,
+    // its voxel (oj, ol) at + goff[q]
+    const float* gm = PM ? g + pm_row(pm, map, 0, 0) : g + map * (pout * mx);
+    // plane oi -> oi + 1: the next x-phase's images, or back to x-phase 0 one phase-image plane on
+    const int64_t pxs = PM ? int64_t(pm.sy) * pm.sz * pm.f * pm.qvol : 0;
+    const int64_t pwrap = PM ? int64_t(pm.qy) * pm.qz - (pm.sx - 1) * pxs : 0;
     const M* mm = mask + map * (pout * mx);
     float* dm = dx + map * (pin * nx);
     for (int tl = threadIdx.x; tl < nz; tl += ZL) {
         // window rows (b, c) in descending order = ascending output index
         int roff[4];
+        int goff[4];
         bool rok[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -203,6 +242,10 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
             const int oj = tj - sy * b, ol = tl - sz * c;
             rok[q] = oj >= 0 && oj < my && ol >= 0 && ol < mz;
             roff[q] = rok[q] ? oj * mz + ol : 0;
+            goff[q] = roff[q];
+            if (PM && rok[q])
+                goff[q] = ((oj % pm.sy) * pm.sz + (ol & (pm.sz - 1))) * pm.f * int(pm.qvol) + (oj / pm.sy) * pm.qz +
+                          (ol >> pm.zsh);
         }
         // ring[k]: (mask, g) of output plane ti - SX + k, k <= SX + 1 (the
         // last one is the next iteration's plane, loaded a plane ahead)
@@ -214,16 +257,22 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
             for (int q = 0; q < 4; ++q) rm[k][q] = -1, rg[k][q] = 0.f;
         const M* mp = mm;
         const float* gp = gm;
+        int rxp = 0;  // x-phase of the plane gp points at
         auto fetch = [&](int oi, int slot) {
             const bool pok = oi < mx;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const bool ok = pok && rok[q];
                 rm[slot][q] = ok ? int(__ldg(mp + roff[q])) : -1;
-                rg[slot][q] = ok ? __ldg(gp + roff[q]) : 0.f;
+                rg[slot][q] = ok ? __ldg(gp + goff[q]) : 0.f;
             }
             mp += pout;
-            gp += pout;
+            if constexpr (PM) {
+                if (++rxp == pm.sx) rxp = 0, gp += pwrap;
+                else gp += pxs;
+            } else {
+                gp += pout;
+            }
         };
         fetch(0, SX);
         float* dp = dm + tj * nz + tl;
@@ -297,38 +346,59 @@ __global__ void __launch_bounds__(ZL * YR) maxpool_bwd_k(const float* __restrict
 }  // namespace
 
 namespace {
+pm_dev pm_device(const pm_order& pm, int64_t maps, dims3 m) {
+    pm_dev d{};
+    if (!pm.on) return d;
+    int zsh = -1;
+    for (int b = 0; b < 8; ++b)
+        if ((int64_t(1) << b) == pm.s.z) zsh = b;
+    require(zsh >= 0 && pm.f > 0 && maps % pm.f == 0 && m.x % pm.s.x == 0 && m.y % pm.s.y == 0 && m.z % pm.s.z == 0,
+            "maxfilter: phase-major order needs dims divisible by the sparsity (power-of-two along z)");
+    d.on = 1, d.f = pm.f, d.sx = int(pm.s.x), d.sy = int(pm.s.y), d.sz = int(pm.s.z), d.zsh = zsh;
+    d.qy = int(m.y / pm.s.y), d.qz = int(m.z / pm.s.z);
+    d.qvol = (m.x / pm.s.x) * int64_t(d.qy) * d.qz;
+    require(pm.s.vol() * pm.f * d.qvol < (int64_t(1) << 31), "maxfilter: phase-major patch exceeds the int32 offset range");
+    return d;
+}
+
 template <typename M>
 void maxfilter_fwd_t(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y, M* mask,
-                     int gate = 0) {
+                     int gate = 0, pm_order pm = {}) {
     const dims3 m{n.x - s.x * (k.x - 1), n.y - s.y * (k.y - 1), n.z - s.z * (k.z - 1)};
     require(m.x > 0 && m.y > 0 && m.z > 0, "maxfilter_forward: effective window exceeds input");
     prof_scope ps(st, "maxfilter_fwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
                   double(maps) * (4.0 * double(n.vol()) + (4.0 + sizeof(M)) * double(m.vol())), 0);
     require(n.vol() < (int64_t(1) << 31), "maxfilter_forward: map exceeds int32 mask range");
     require(sizeof(M) == 4 || k.vol() <= (gate ? 128 : 256), "maxfilter_forward: window too large for one-byte codes");
-    auto* kf = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_fwd_k<2, 2, 2, M>
+    const pm_dev pd = pm_device(pm, maps, m);
+    require(!pm.on || (k.x == 2 && k.y == 2 && k.z == 2 && ZL % pm.s.z == 0),
+            "maxfilter_forward: phase-major output is written by the 2^3 kernel only");
+    auto* kf = pm.on                                ? maxfilter_fwd_k<2, 2, 2, M, true>
+               : (k.x == 2 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<2, 2, 2, M>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2, M>
                                                     : maxfilter_fwd_k<0, 0, 0, M>;
     kf<<<vgrid(m.y, m.x, maps), vblock(), 0, st>>>(x, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
                                                   int(k.x), int(k.y), int(k.z), int(s.x), int(s.y), int(s.z), y,
-                                                  mask, gate);
+                                                  mask, gate, pd);
     launch_check("maxfilter_fwd");
 }
 
 template <typename M>
 void maxfilter_bwd_t(cudaStream_t st, const float* g, const M* mask, int64_t maps, dims3 m, dims3 k, dims3 s,
-                     float* dx) {
+                     float* dx, pm_order pm = {}) {
     const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
     prof_scope ps(st, "maxfilter_bwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
                   double(maps) * ((4.0 + sizeof(M)) * double(m.vol()) + 4.0 * double(n.vol())), 0);
     if (k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2) && maps < 65536) {
         const dim3 grid(unsigned(ceil_div(n.y, YR)), unsigned(maps));
-        auto* kk = s.x == 1 ? maxfilter2_bwd_k<1, M> : maxfilter2_bwd_k<2, M>;
+        auto* kk = pm.on ? (s.x == 1 ? maxfilter2_bwd_k<1, M, true> : maxfilter2_bwd_k<2, M, true>)
+                         : (s.x == 1 ? maxfilter2_bwd_k<1, M> : maxfilter2_bwd_k<2, M>);
         kk<<<grid, vblock(), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
-                                      int(s.y), int(s.z), dx);
+                                      int(s.y), int(s.z), dx, pm_device(pm, maps, m));
         launch_check("maxfilter_bwd");
         return;
     }
+    require(!pm.on, "maxfilter_backward: phase-major gradients are read by the 2^3 kernel only");
     auto* kb = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_bwd_k<2, 2, 2, M>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_bwd_k<1, 2, 2, M>
                                                     : maxfilter_bwd_k<0, 0, 0, M>;
@@ -344,16 +414,16 @@ void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3
     maxfilter_fwd_t(st, x, maps, n, k, s, y, mask);
 }
 void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s, float* y,
-                   uint8_t* code, bool relu_gate) {
-    maxfilter_fwd_t(st, x, maps, n, k, s, y, code, relu_gate ? 1 : 0);
+                   uint8_t* code, bool relu_gate, pm_order pm) {
+    maxfilter_fwd_t(st, x, maps, n, k, s, y, code, relu_gate ? 1 : 0, pm);
 }
 void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t maps, dims3 m, dims3 k, dims3 s,
                    float* dx) {
     maxfilter_bwd_t(st, g, mask, maps, m, k, s, dx);
 }
 void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m, dims3 k, dims3 s,
-                   float* dx) {
-    maxfilter_bwd_t(st, g, code, maps, m, k, s, dx);
+                   float* dx, pm_order pm) {
+    maxfilter_bwd_t(st, g, code, maps, m, k, s, dx, pm);
 }
 
 void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p, float* y,

@@ -569,11 +569,15 @@ void executor::run_conv_bwd(layer& L, float* g_out, float* g_in, bool need_dgrad
 // vector accesses instead of every s-th float of the interleaved tensor, and
 // so do the gradient of that group and the fused ReLU gate. Nothing else may
 // touch the group: the producer's transfer is fused (ReLU gate inside the
-// gradient transform) or absent. ZNN_PHASE_MAJOR=0: natural order everywhere.
+// gradient transform) or absent. A 2^3 max-filter feeding an FFT layer writes
+// its output (and reads its gradient) in that layer's phase order too
+// (ZNN_PHASE_MAJOR_FILTER=0: not). ZNN_PHASE_MAJOR=0: natural order everywhere.
 void executor::plan_layouts() {
     const char* env = std::getenv("ZNN_PHASE_MAJOR");
     const bool on = !(env && std::string(env) == "0") && !cfg_.keep_images;
     const bool relu_fusion = !std::getenv("ZNN_NO_RELU_FUSION");
+    const char* fenv = std::getenv("ZNN_PHASE_MAJOR_FILTER");
+    const bool filter_pm = !(fenv && std::string(fenv) == "0");
     std::string note;
     for (size_t j = 1; j + 1 < groups_.size(); ++j) {
         group& G = groups_[j];
@@ -583,14 +587,23 @@ void executor::plan_layouts() {
             if (L.out == int(j)) A = &L, ++np;
             if (L.in == int(j)) C = &L, ++nc;
         }
-        bool pm = on && G.materialized && np == 1 && nc == 1 && A->kind == lkind::conv && C->kind == lkind::conv &&
-                  A->engine == 1 && C->engine == 1 && znn_fft::supported(A->shape) && znn_fft::supported(C->shape) &&
-                  znn_fft::phase_major_ok(A->shape) && znn_fft::phase_major_ok(C->shape) &&
-                  A->shape.s.x == C->shape.s.x && A->shape.s.y == C->shape.s.y && A->shape.s.z == C->shape.s.z &&
-                  (!A->fused || (A->fused_act == 2 && relu_fusion && !A->pregated));
+        const bool consumer_ok = on && G.materialized && np == 1 && nc == 1 && C->kind == lkind::conv &&
+                                 C->engine == 1 && znn_fft::supported(C->shape) && znn_fft::phase_major_ok(C->shape);
+        bool pm = false;
+        if (consumer_ok && A->kind == lkind::conv) {
+            pm = A->engine == 1 && znn_fft::supported(A->shape) && znn_fft::phase_major_ok(A->shape) &&
+                 A->shape.s.x == C->shape.s.x && A->shape.s.y == C->shape.s.y && A->shape.s.z == C->shape.s.z &&
+                 (!A->fused || (A->fused_act == 2 && relu_fusion && !A->pregated));
+        } else if (consumer_ok && A->kind == lkind::filter && filter_pm) {
+            // a 2^3 max-filter writes its output / reads its gradient in the consumer's phase order
+            const int64_t sz = C->shape.s.z;
+            pm = znn_fft::phase_major_pays(C->shape) && A->k.x == 2 && A->k.y == 2 && A->k.z == 2 &&
+                 (A->s.x == 1 || A->s.x == 2) && G.code != nullptr && 32 % sz == 0 &&
+                 cfg_.batch * G.maps < 65536 && (sz & (sz - 1)) == 0;
+        }
         if (pm != G.pm) drop_graph();
         G.pm = pm;
-        G.pm_s = pm ? A->shape.s : dims3{1, 1, 1};
+        G.pm_s = pm ? C->shape.s : dims3{1, 1, 1};
         if (pm) note += " " + std::to_string(j);
     }
     if (note != layout_note_) {
@@ -613,7 +626,8 @@ void executor::run_forward(const float* in_dev) {
                 break;
             case lkind::pool: znn_gpu::maxpool_fwd(st_, I.act, B * I.maps, I.dims, L.k, O.act, O.mask); break;
             case lkind::filter:
-                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.code, L.relu_gate);
+                znn_gpu::maxfilter_fwd(st_, I.act, B * I.maps, I.dims, L.k, L.s, O.act, O.code, L.relu_gate,
+                                       znn_gpu::pm_order{O.pm ? 1 : 0, int(O.maps), O.pm_s});
                 break;
         }
     }
@@ -700,7 +714,9 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                 if (L.in != 0) znn_gpu::maxpool_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, I.grad);
                 break;
             case lkind::filter:
-                if (L.in != 0) znn_gpu::maxfilter_bwd(st_, O.grad, O.code, B * I.maps, O.dims, L.k, L.s, I.grad);
+                if (L.in != 0)
+                    znn_gpu::maxfilter_bwd(st_, O.grad, O.code, B * I.maps, O.dims, L.k, L.s, I.grad,
+                                           znn_gpu::pm_order{O.pm ? 1 : 0, int(O.maps), O.pm_s});
                 break;
         }
     }

@@ -98,9 +98,17 @@ void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t
 // at most 256 taps; the executor's internal max-filters)
 // relu_gate: windows whose maximum is not > 0 get code bit 7 (the backward
 // then also applies the ReLU backward of the layer feeding the filter)
+// pm: the filter's output image y (forward) / its gradient g (backward) is
+// phase-major for sparsity pm.s ([B S][pm.f][m / s], phase (rx sy + ry) sz + rz,
+// maps = B pm.f, power-of-two sz) instead of [maps][m]: the order the FFT
+// layer consuming it wants (executor::plan_layouts); codes stay natural
+struct pm_order {
+    int on = 0, f = 1;
+    dims3 s{1, 1, 1};
+};
 void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s,
-                   float* y, uint8_t* code, bool relu_gate = false);
+                   float* y, uint8_t* code, bool relu_gate = false, pm_order pm = {});
 void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m,
-                   dims3 k, dims3 s, float* dx);
+                   dims3 k, dims3 s, float* dx, pm_order pm = {});
 
 }  // namespace znn_gpu

@@ -312,13 +312,16 @@ def test_fft_tensor_core_cmacs(ctx, monkeypatch, shape, tc):
             assert O.max_rel_error(dw[o, i], ref) < 1e-3, ("wgrad", o, i)
 
 
-def test_phase_major_groups_between_fft_layers(ctx, monkeypatch):
+@pytest.mark.parametrize("filt", ["1", "0"])
+def test_phase_major_groups_between_fft_layers(ctx, monkeypatch, filt):
     """Groups between FFT layers of one sparsity (scaled c5: conv3 -> conv4 ->
-    conv5, s = 4, dims divisible by 4) are kept phase-major by the executor:
-    one step matches the oracle (fwd 1e-4, gradients and updated weights 1e-3),
+    conv5, s = 4, dims divisible by 4) and, with filt, the outputs of the 2^3
+    max-filters feeding FFT layers are kept phase-major by the executor: one
+    step matches the oracle (fwd 1e-4, gradients and updated weights 1e-3),
     the group images read back in natural order equal the natural-order run's,
     and so do the gradients."""
     from paper_1510_06706_b200 import configs as C
+    monkeypatch.setenv("ZNN_PHASE_MAJOR_FILTER", filt)
     cfg = C.scaled("c5", 30, (4, 4, 4), batch=2)
     nconv = len(cfg.conv_layers())
     engines = ["fft"] * (nconv - 1) + ["direct"]
@@ -326,7 +329,8 @@ def test_phase_major_groups_between_fft_layers(ctx, monkeypatch):
     desc = net.describe()
     assert "phase-major groups:" in desc, desc
     pm = [int(t) for t in desc.split("phase-major groups:")[-1].split("\n")[0].split()]
-    assert len(pm) == 2, desc  # conv3 -> conv4 and conv4 -> conv5
+    # conv3 -> conv4 and conv4 -> conv5 (+ filter -> conv3, whose plan runs the small-cube transforms)
+    assert len(pm) == (3 if filt == "1" else 2), desc
     imgs = {g: net.group_image(g, 0) for g in pm}
     g = O.parse_netspec(cfg.netspec(), cfg.out_dims)
     ins = [[x[b, 0]] for b in range(cfg.batch)]
