@@ -10,6 +10,10 @@
 // scan; maxops.hpp:106-110 for the separable filter). A direct window scan
 // in lexicographic order with strict '>' selects the same source, so masks
 // are bit-identical on identical inputs.
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+
 #include "ops.hpp"
 
 namespace znn_gpu {
@@ -146,6 +150,70 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_fwd_k(const float* __restri
     }
 }
 
+// Forward of the 2^3 max-filter with one-byte codes and x-stride SX (1 or 2):
+// a thread owns one (y, z) column of the output and walks its x-planes; input
+// plane i + SX's four window-row values are loaded once and serve output
+// planes i (a = 1) and i + SX (a = 0): half the loads of maxfilter_fwd_k.
+// Block = whole z rows (up to 128 lanes) x y-rows, grid = (y tiles, maps).
+// Same scan order (a, b, c) and strict '>' as maxfilter_fwd_k: same codes.
+template <int SX, bool PM>
+__global__ void __launch_bounds__(ZL * YR) maxfilter2_fwd_k(const float* __restrict__ x, int nx, int ny, int nz, int mx,
+                                                            int my, int mz, int sy, int sz, float* __restrict__ y,
+                                                            uint8_t* __restrict__ code, int gate, pm_dev pm) {
+    const int j = blockIdx.x * blockDim.y + threadIdx.y;
+    if (j >= my) return;
+    const int64_t map = blockIdx.y;
+    const int64_t pin = int64_t(ny) * nz, pout = int64_t(my) * mz;
+    const float* xm = x + map * (pin * nx);
+    const int64_t pxs = PM ? int64_t(pm.sy) * pm.sz * pm.f * pm.qvol : 0;
+    const int64_t pwrap = PM ? int64_t(pm.qy) * pm.qz - (pm.sx - 1) * pxs : 0;
+    for (int l = threadIdx.x; l < mz; l += blockDim.x) {
+        const float* xp = xm + j * nz + l;  // window row (b, c) of a plane at xp + b sy nz + c sz
+        const int o01 = sz, o10 = sy * nz, o11 = sy * nz + sz;
+        float v[SX + 2][4];  // planes i .. i + SX + 1 (the last one is loaded a plane ahead of use)
+#pragma unroll
+        for (int k = 0; k <= SX; ++k) {
+            v[k][0] = __ldg(xp), v[k][1] = __ldg(xp + o01), v[k][2] = __ldg(xp + o10), v[k][3] = __ldg(xp + o11);
+            xp += pin;
+        }
+        uint8_t* cp = code + map * (pout * mx) + j * mz + l;
+        float* yp;
+        int rxp = 0;
+        if constexpr (PM)
+            yp = y + pm_row(pm, map, 0, j) + int64_t(l & (pm.sz - 1)) * pm.f * pm.qvol + (l >> pm.zsh);
+        else
+            yp = y + map * (pout * mx) + j * mz + l;
+        for (int i = 0; i < mx; ++i) {
+            if (i + SX + 1 < nx) {
+                v[SX + 1][0] = __ldg(xp), v[SX + 1][1] = __ldg(xp + o01), v[SX + 1][2] = __ldg(xp + o10),
+                          v[SX + 1][3] = __ldg(xp + o11);
+                xp += pin;
+            }
+            float best = v[0][0];
+            int bc = 0;
+#pragma unroll
+            for (int q = 1; q < 4; ++q)
+                if (v[0][q] > best) best = v[0][q], bc = q;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (v[SX][q] > best) best = v[SX][q], bc = 4 + q;
+            __stcs(yp, best);
+            *cp = uint8_t(bc | ((gate && !(best > 0.f)) ? 0x80 : 0));
+            cp += pout;
+            if constexpr (PM) {
+                if (++rxp == pm.sx) rxp = 0, yp += pwrap;
+                else yp += pxs;
+            } else {
+                yp += pout;
+            }
+#pragma unroll
+            for (int k = 0; k <= SX; ++k)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[k][q] = v[k + 1][q];
+        }
+    }
+}
+
 // dx[t] = sum over windows o whose argmax is t of g[o]; windows visited in
 // ascending flat order of o, the order the reference accumulates in
 // (maxops.hpp:176-181), so fp32 sums match it bit for bit.
@@ -219,7 +287,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
                                                             int nz, int mx, int my, int mz, int sy, int sz,
                                                             float* __restrict__ dx, pm_dev pm) {
     constexpr bool CODE = sizeof(M) == 1;
-    const int tj = blockIdx.x * YR + threadIdx.y;
+    const int tj = blockIdx.x * blockDim.y + threadIdx.y;
     if (tj >= ny) return;
     const int64_t map = blockIdx.y;
     const int64_t pin = int64_t(ny) * nz, pout = int64_t(my) * mz;
@@ -231,7 +299,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
     const int64_t pwrap = PM ? int64_t(pm.qy) * pm.qz - (pm.sx - 1) * pxs : 0;
     const M* mm = mask + map * (pout * mx);
     float* dm = dx + map * (pin * nx);
-    for (int tl = threadIdx.x; tl < nz; tl += ZL) {
+    for (int tl = threadIdx.x; tl < nz; tl += blockDim.x) {
         // window rows (b, c) in descending order = ascending output index
         int roff[4];
         int goff[4];
@@ -373,6 +441,21 @@ void maxfilter_fwd_t(cudaStream_t st, const float* x, int64_t maps, dims3 n, dim
     const pm_dev pd = pm_device(pm, maps, m);
     require(!pm.on || (k.x == 2 && k.y == 2 && k.z == 2 && ZL % pm.s.z == 0),
             "maxfilter_forward: phase-major output is written by the 2^3 kernel only");
+    if constexpr (sizeof(M) == 1) {
+        // one-byte codes, 2^3 window: the x-walking kernel (ZNN_MAXFILTER_WALK=0: a thread per output voxel)
+        const char* e = std::getenv("ZNN_MAXFILTER_WALK");
+        if (k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2) && maps < 65536 && m.x > s.x &&
+            !(e && std::string(e) == "0")) {
+            const unsigned bx = unsigned(std::min<int64_t>(4, ceil_div(m.z, ZL))) * ZL, by = (ZL * YR) / bx;
+            const dim3 grid(unsigned(ceil_div(m.y, int64_t(by))), unsigned(maps));
+            auto* kw = pm.on ? (s.x == 1 ? maxfilter2_fwd_k<1, true> : maxfilter2_fwd_k<2, true>)
+                             : (s.x == 1 ? maxfilter2_fwd_k<1, false> : maxfilter2_fwd_k<2, false>);
+            kw<<<grid, dim3(bx, by, 1), 0, st>>>(x, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z), int(s.y),
+                                                 int(s.z), y, mask, gate, pd);
+            launch_check("maxfilter_fwd");
+            return;
+        }
+    }
     auto* kf = pm.on                                ? maxfilter_fwd_k<2, 2, 2, M, true>
                : (k.x == 2 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<2, 2, 2, M>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_fwd_k<1, 2, 2, M>
@@ -390,11 +473,16 @@ void maxfilter_bwd_t(cudaStream_t st, const float* g, const M* mask, int64_t map
     prof_scope ps(st, "maxfilter_bwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
                   double(maps) * ((4.0 + sizeof(M)) * double(m.vol()) + 4.0 * double(n.vol())), 0);
     if (k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2) && maps < 65536) {
-        const dim3 grid(unsigned(ceil_div(n.y, YR)), unsigned(maps));
+        // a block spans whole z rows (up to 128 lanes) so one walk along x reads
+        // every sector of a gradient / code plane once: with 32-lane blocks the
+        // three z chunks of a 91-voxel row walked the planes one after another
+        // and re-read the sectors they share from DRAM (2.6x the read traffic)
+        const unsigned bx = unsigned(std::min<int64_t>(4, ceil_div(n.z, ZL))) * ZL, by = (ZL * YR) / bx;
+        const dim3 grid(unsigned(ceil_div(n.y, int64_t(by))), unsigned(maps));
         auto* kk = pm.on ? (s.x == 1 ? maxfilter2_bwd_k<1, M, true> : maxfilter2_bwd_k<2, M, true>)
                          : (s.x == 1 ? maxfilter2_bwd_k<1, M> : maxfilter2_bwd_k<2, M>);
-        kk<<<grid, vblock(), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
-                                      int(s.y), int(s.z), dx, pm_device(pm, maps, m));
+        kk<<<grid, dim3(bx, by, 1), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
+                                             int(s.y), int(s.z), dx, pm_device(pm, maps, m));
         launch_check("maxfilter_bwd");
         return;
     }

@@ -689,8 +689,12 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                         znn_gpu::transfer_bwd(st_, O.grad, O.act, true, B, L.shape.f_out, O.dims.vol(),
                                               L.none_dev, params_ + L.b_off, O.grad, grads_ + L.b_off, ws_);
                     } else {
-                        znn_gpu::transfer_bwd(st_, O.grad, O.act, true, B, L.shape.f_out, O.dims.vol(),
-                                              L.kinds_dev, params_ + L.b_off, O.grad, grads_ + L.b_off, ws_);
+                        // pregated (the max-filter's codes applied this ReLU's backward): the
+                        // gradient is final, only its per-map sums (the bias gradient) remain
+                        const bool sum_only = L.pregated && L.fused_act == 2;
+                        znn_gpu::transfer_bwd(st_, O.grad, sum_only ? nullptr : O.act, true, B, L.shape.f_out,
+                                              O.dims.vol(), L.kinds_dev, params_ + L.b_off, O.grad,
+                                              grads_ + L.b_off, ws_);
                     }
                 }
                 // the bias gradient is final here (transfer_bwd above): update it

@@ -53,6 +53,10 @@ __global__ void __launch_bounds__(kThreads) transfer_bwd_k(const float* __restri
         const int64_t v = v0 + e * kThreads;
         if (v < vox) {
             const int64_t i = off + v;
+            if (xy == nullptr) {  // gradient already gated (max-filter codes): bias gradient only
+                acc += __ldg(g + i);
+                continue;
+            }
             const float yv = __ldcs(xy + i), gv = __ldcs(g + i);
             const float d = from_output ? act_deriv_out(kind, yv) : act_deriv_in(kind, yv + b);
             const float r = gv * d;
