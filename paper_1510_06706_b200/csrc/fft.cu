@@ -1458,148 +1458,156 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_inv_reg_k(const float
 }
 
 // ---- row-bin-major xy passes (tensor-core plans, square planes): one CTA
-// takes the z-bin plane of NI consecutive maps of one row (item = (row,
-// zb, part)), loading / storing one NI * 8-byte piece per bin ----
-// register variants (one line per thread, the P-point transform in registers,
-// no exchange buffer): XR_THREADS threads take the NI planes' rows, then their
-// columns, one pass each
-constexpr int XR_THREADS = 256;
-// threads of a register xy CTA: the NI planes' column lines (one pass), at
-// most 256 (P = 48, NI = 4: 192, two CTAs per SM at ~170 registers)
-template <int P, int NI>
-__host__ __device__ constexpr int xr_threads() { return (NI * P + 31) / 32 * 32 < XR_THREADS ? (NI * P + 31) / 32 * 32 : XR_THREADS; }
-template <int P, int NI>
-constexpr size_t smem_xy_reg() {
-    return sizeof(float2) * (size_t(P) + size_t(NI) * P * (P + 1));
-}
-template <int P, int NI>
-__global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_fwd_reg_k(float2* __restrict__ spec, int nx, int ny, int Zh,
-                                                                int F) {
-    constexpr int XT = xr_threads<P, NI>();
-    constexpr int PYP = P + 1, PV = P * PYP;
-    const int H = F / NI;
-    extern __shared__ float2 sm[];
+// takes the z-bin plane of 4 consecutive maps of one row (item = (row, zb,
+// part)); per bin the four maps are one 32-byte piece of the spectrum.
+// Register variants: one line per thread, the P-point transform in registers,
+// no exchange buffer; XP_T threads take the 4 planes' rows, then their
+// columns, one pass each.
+// The planes sit in shared memory as two PAIRS ([P][P + 1] bins of two
+// adjacent float2: maps 2 h, 2 h + 1), so a lane pair moves a bin's 32-byte
+// piece as two 16-byte halves of one sector (cp.async in, float4 out): with
+// four separate planes every 8-byte copy was its own shared-memory wavefront
+// and its own sector request (the pass ran at 84% of the L1 pipe). Lines are
+// taken by lanes (map of the pair fastest, then the line), which keeps the
+// line passes free of bank conflicts at the 16-byte bin pitch; the second
+// pair is offset by 64 B so the two 16-byte slots of one bin fall in
+// different bank groups.
+constexpr int XP_NI = 4;
+template <int P>
+__host__ __device__ constexpr int xp_threads() { return (4 * P + 31) / 32 * 32 < 256 ? (4 * P + 31) / 32 * 32 : 256; }
+template <int P>
+__host__ __device__ constexpr int xp_pair() { return P * (P + 1) * 2 + 8; }  // float2 per plane pair
+template <int P>
+__host__ __device__ constexpr int xp_tw() { return (P + 1) & ~1; }            // twiddles, 16-byte multiple
+template <int P>
+constexpr size_t smem_xy_pair() { return sizeof(float2) * (size_t(xp_tw<P>()) + 2 * size_t(xp_pair<P>())); }
+
+template <int P>
+__global__ void __launch_bounds__(xp_threads<P>()) fft_xy_fwd_pair_k(float2* __restrict__ spec, int nx, int ny, int Zh,
+                                                             int F) {
+    constexpr int XT = xp_threads<P>();
+    constexpr int PYP = P + 1, PP = xp_pair<P>();
+    const int H = F / XP_NI;
+    extern __shared__ __align__(16) float2 sm[];
     float2* tw = sm;
-    float2* pls = tw + P;  // NI x [P][PYP]
+    float2* pls = sm + xp_tw<P>();  // 2 x [P][PYP][2]
     const int64_t q = blockIdx.x;
     const int part = int(q % H);
     const int64_t rest = q / H;
     const int zb = int(rest % Zh);
-    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
+    float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * XP_NI;
     fill_twiddles<P>(tw);
-    // the valid region the z pass wrote: async 8-byte copies, every load of the
-    // CTA in flight at once (the kernel runs at ~12 warps per SM)
-    for (int e = threadIdx.x; e < nx * ny; e += XT) {
+    // the valid region the z pass wrote: 16-byte async copies, every load of the CTA in flight at once
+    for (int e2 = threadIdx.x; e2 < 2 * nx * ny; e2 += XT) {
+        const int e = e2 >> 1, h = e2 & 1;
         const int x = e / ny, y = e - x * ny;
-        const float2* src = gq + (x * P + y) * F;
-#pragma unroll
-        for (int j = 0; j < NI; ++j) cp_async8(pls + j * PV + x * PYP + y, src + j);
+        cp_async16p(pls + h * PP + (x * PYP + y) * 2, gq + (x * P + y) * F + 2 * h);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * nx; ln += XT) {  // rows (y transforms) of the valid rows
-        const int j = ln / nx, x = ln - j * nx;
-        float2* row = pls + j * PV + x * PYP;
+    for (int ln = threadIdx.x; ln < 4 * nx; ln += XT) {  // rows (y transforms) of the valid rows
+        const int jj = ln & 1, r = ln >> 1, h = r / nx, x = r - h * nx;
+        float2* row = pls + h * PP + x * PYP * 2 + jj;
         float2 v[P];
 #pragma unroll
-        for (int y = 0; y < P; ++y) v[y] = y < ny ? row[y] : make_float2(0.f, 0.f);
+        for (int y = 0; y < P; ++y) v[y] = y < ny ? row[2 * y] : make_float2(0.f, 0.f);
         dft_r<P, P, false>(v, tw);
 #pragma unroll
-        for (int k = 0; k < P; ++k) row[k] = v[k];
+        for (int k = 0; k < P; ++k) row[2 * k] = v[k];
     }
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * P; ln += XT) {  // columns (x transforms); rows >= nx are zero
-        const int j = ln / P, y = ln - j * P;
-        float2* col = pls + j * PV + y;
+    for (int ln = threadIdx.x; ln < 4 * P; ln += XT) {  // columns (x transforms); rows >= nx are zero
+        const int jj = ln & 1, r = ln >> 1, h = r / P, y = r - h * P;
+        float2* col = pls + h * PP + y * 2 + jj;
         float2 v[P];
 #pragma unroll
-        for (int x = 0; x < P; ++x) v[x] = x < nx ? col[x * PYP] : make_float2(0.f, 0.f);
+        for (int x = 0; x < P; ++x) v[x] = x < nx ? col[x * PYP * 2] : make_float2(0.f, 0.f);
         dft_r<P, P, false>(v, tw);
 #pragma unroll
-        for (int k = 0; k < P; ++k) col[k * PYP] = v[k];
+        for (int k = 0; k < P; ++k) col[k * PYP * 2] = v[k];
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < P * P; e += XT) {
+    for (int e2 = threadIdx.x; e2 < 2 * P * P; e2 += XT) {  // a lane pair stores a bin's 32-byte piece
+        const int e = e2 >> 1, h = e2 & 1;
         const int x = e / P, y = e - x * P;
-        float2 v[NI];
-#pragma unroll
-        for (int j = 0; j < NI; ++j) v[j] = pls[j * PV + x * PYP + y];
-        grp_put<NI>(gq + e * F, v);
+        const float4 u = *reinterpret_cast<const float4*>(pls + h * PP + (x * PYP + y) * 2);
+        __stcs(reinterpret_cast<float4*>(gq + e * F + 2 * h), u);
     }
 }
 
-template <int P, int NI, bool UNIT>  // UNIT: unit kept-voxel steps (no per-output division)
-__global__ void __launch_bounds__(xr_threads<P, NI>()) fft_xy_inv_reg_k(const float2* __restrict__ spec, float2* __restrict__ out,
-                                                                int x_step, int xc, int y_step, int yc, int Zh, int F) {
-    constexpr int XT = xr_threads<P, NI>();
-    constexpr int PYP = P + 1, PV = P * PYP;
-    const int H = F / NI;
-    extern __shared__ float2 sm[];
+template <int P, bool UNIT>  // UNIT: unit kept-voxel steps (no per-output division)
+__global__ void __launch_bounds__(xp_threads<P>()) fft_xy_inv_pair_k(const float2* __restrict__ spec, float2* __restrict__ out,
+                                                             int x_step, int xc, int y_step, int yc, int Zh, int F) {
+    constexpr int XT = xp_threads<P>();
+    constexpr int PYP = P + 1, PP = xp_pair<P>();
+    const int H = F / XP_NI;
+    extern __shared__ __align__(16) float2 sm[];
     float2* tw = sm;
-    float2* pls = tw + P;
+    float2* pls = sm + xp_tw<P>();
     const int64_t q = blockIdx.x;
     const int part = int(q % H);
     const int64_t rest = q / H;
     const int zb = int(rest % Zh);
     const int64_t grp = rest / Zh;
-    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * NI;
+    const float2* gq = spec + (grp * Zh * P * P + int64_t(zb) * P * P) * F + part * XP_NI;
     fill_twiddles<P>(tw);
-    for (int e = threadIdx.x; e < P * P; e += XT) {  // async 8-byte copies, all in flight
+    for (int e2 = threadIdx.x; e2 < 2 * P * P; e2 += XT) {  // 16-byte async copies, all in flight
+        const int e = e2 >> 1, h = e2 & 1;
         const int x = e / P, y = e - x * P;
-        const float2* src = gq + e * F;
-#pragma unroll
-        for (int j = 0; j < NI; ++j) cp_async8(pls + j * PV + x * PYP + y, src + j);
+        cp_async16p(pls + h * PP + (x * PYP + y) * 2, gq + e * F + 2 * h);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * P; ln += XT) {  // column inverses, keep rows x_step * i
-        const int j = ln / P, y = ln - j * P;
-        float2* col = pls + j * PV + y;
+    for (int ln = threadIdx.x; ln < 4 * P; ln += XT) {  // column inverses, keep rows x_step * i
+        const int jj = ln & 1, r = ln >> 1, h = r / P, y = r - h * P;
+        float2* col = pls + h * PP + y * 2 + jj;
         float2 v[P];
 #pragma unroll
-        for (int x = 0; x < P; ++x) v[x] = col[x * PYP];
+        for (int x = 0; x < P; ++x) v[x] = col[x * PYP * 2];
         dft_r<P, P, true>(v, tw);
         if constexpr (UNIT) {
 #pragma unroll
             for (int i = 0; i < P; ++i)
-                if (i < xc) col[i * PYP] = v[i];
+                if (i < xc) col[i * PYP * 2] = v[i];
         } else {
 #pragma unroll
             for (int k = 0; k < P; ++k) {
                 const int i = k / x_step;
-                if (i * x_step == k && i < xc) col[i * PYP] = v[k];
+                if (i * x_step == k && i < xc) col[i * PYP * 2] = v[k];
             }
         }
     }
     __syncthreads();
-    for (int ln = threadIdx.x; ln < NI * xc; ln += XT) {  // row inverses of the kept rows
-        const int j = ln / xc, i = ln - j * xc;
-        const float2* row = pls + j * PV + i * PYP;
+    for (int ln = threadIdx.x; ln < 4 * xc; ln += XT) {  // row inverses of the kept rows
+        const int jj = ln & 1, r = ln >> 1, h = r / xc, i = r - h * xc;
+        float2* row = pls + h * PP + i * PYP * 2 + jj;
         float2 v[P];
 #pragma unroll
-        for (int y = 0; y < P; ++y) v[y] = row[y];
+        for (int y = 0; y < P; ++y) v[y] = row[2 * y];
         dft_r<P, P, true>(v, tw);
-        float2* o = pls + j * PV + i * PYP;  // the kept columns back into the row (already in registers)
-        if constexpr (UNIT) {
+        if constexpr (UNIT) {  // the kept columns back into the row (already in registers)
 #pragma unroll
-            for (int jj = 0; jj < P; ++jj)
-                if (jj < yc) o[jj] = v[jj];
+            for (int c = 0; c < P; ++c)
+                if (c < yc) row[2 * c] = v[c];
         } else {
 #pragma unroll
             for (int k = 0; k < P; ++k) {
-                const int jj = k / y_step;
-                if (jj * y_step == k && jj < yc) o[jj] = v[k];
+                const int c = k / y_step;
+                if (c * y_step == k && c < yc) row[2 * c] = v[k];
             }
         }
     }
     __syncthreads();
-    // coalesced stores of the NI compact blocks (plane img * Zh + zb, [xc][yc])
+    // coalesced stores of the 4 compact blocks (plane img * Zh + zb, [xc][yc]): even / odd lanes
+    // take the two maps of a pair (adjacent float2 in shared memory, 128-byte runs per map)
     const int blk = xc * yc;
-    for (int e = threadIdx.x; e < NI * blk; e += XT) {
-        const int j = e / blk, r = e - j * blk, i = r / yc, jj = r - i * yc;
-        out[((grp * F + part * NI + j) * Zh + zb) * int64_t(blk) + r] = pls[j * PV + i * PYP + jj];
+    for (int e = threadIdx.x; e < 4 * blk; e += XT) {
+        const int h = e / (2 * blk), rem = e - h * 2 * blk, r = rem >> 1, jj = rem & 1;
+        const int i = r / yc, c = r - i * yc;
+        out[((grp * F + part * XP_NI + 2 * h + jj) * Zh + zb) * int64_t(blk) + r] =
+            pls[h * PP + (i * PYP + c) * 2 + jj];
     }
 }
 
@@ -2799,19 +2807,12 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         if (p.P.x == 1) {
             allow_smem(fft_xy_fwd_k<1, PY>, smem_xy(1, PY));
             fft_xy_fwd_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(spec, planes, int(n.x), int(n.y));
-        } else if (quad) {  // row-bin-major layout: XY_NI planes per CTA
+        } else if (quad) {  // row-bin-major layout: the planes of 4 maps per CTA
             if constexpr (PY <= 64) {
-                auto run = [&](auto ni) {
-                    constexpr int NI = decltype(ni)::value;
-                    require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
-                    allow_smem(fft_xy_fwd_reg_k<PY, NI>, smem_xy_reg<PY, NI>());
-                    fft_xy_fwd_reg_k<PY, NI><<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
-                        spec, int(n.x), int(n.y), int(p.Zh), quad);
-                };
-                const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
-                if (ni == 1) run(std::integral_constant<int, 1>{});
-                else if (ni == 2) run(std::integral_constant<int, 2>{});
-                else run(std::integral_constant<int, 4>{});
+                require(planes % XP_NI == 0 && quad % XP_NI == 0, "fft: row-bin-major maps not a multiple of 4");
+                allow_smem(fft_xy_fwd_pair_k<PY>, smem_xy_pair<PY>());
+                fft_xy_fwd_pair_k<PY><<<unsigned(planes / XP_NI), xp_threads<PY>(), smem_xy_pair<PY>(), st>>>(
+                    spec, int(n.x), int(n.y), int(p.Zh), quad);
             }
         } else if (smem_pipe(PY) > size_t(220) * 1024 || !std::getenv("ZNN_FFT_XY_PIPE")) {
             // one plane per CTA, two CTAs per SM: faster than the persistent
@@ -2906,25 +2907,18 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
             allow_smem(fft_xy_inv_k<1, PY>, smem_xy(1, PY));
             fft_xy_inv_k<1, PY><<<unsigned(planes), THREADS, smem_xy(1, PY), st>>>(
                 spec, cbuf, planes, int(step.x), int(cnt.x), int(step.y), int(cnt.y));
-        } else if (quad) {  // row-bin-major layout: XY_NI planes per CTA
+        } else if (quad) {  // row-bin-major layout: the planes of 4 maps per CTA
             if constexpr (PY <= 64) {
-                auto run = [&](auto ni) {
-                    constexpr int NI = decltype(ni)::value;
-                    require(planes % NI == 0, "fft: row-bin-major planes not a multiple of the CTA's planes");
-                    auto go = [&](auto kern) {
-                        allow_smem(kern, smem_xy_reg<PY, NI>());
-                        kern<<<unsigned(planes / NI), xr_threads<PY, NI>(), smem_xy_reg<PY, NI>(), st>>>(
-                            spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
-                    };
-                    if (step.x == 1 && step.y == 1)
-                        go(fft_xy_inv_reg_k<PY, NI, true>);
-                    else
-                        go(fft_xy_inv_reg_k<PY, NI, false>);
+                require(planes % XP_NI == 0 && quad % XP_NI == 0, "fft: row-bin-major maps not a multiple of 4");
+                auto go = [&](auto kern) {
+                    allow_smem(kern, smem_xy_pair<PY>());
+                    kern<<<unsigned(planes / XP_NI), xp_threads<PY>(), smem_xy_pair<PY>(), st>>>(
+                        spec, cbuf, int(step.x), int(cnt.x), int(step.y), int(cnt.y), int(p.Zh), quad);
                 };
-                const int ni = grp_ni_env("ZNN_FFT_XY_NI", 4);
-                if (ni == 1) run(std::integral_constant<int, 1>{});
-                else if (ni == 2) run(std::integral_constant<int, 2>{});
-                else run(std::integral_constant<int, 4>{});
+                if (step.x == 1 && step.y == 1)
+                    go(fft_xy_inv_pair_k<PY, true>);
+                else
+                    go(fft_xy_inv_pair_k<PY, false>);
             }
         } else if (smem_pipe(PY) > size_t(220) * 1024) {  // two 128^2 planes do not fit: single buffer
             allow_smem(fft_xy_inv_k<PY, PY>, smem_xy(PY, PY));
