@@ -1289,6 +1289,16 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_fwd_reg_k(cube_io a, 
     } else {  // row-bin-major layout: one NI * 8-byte piece per bin
         const int F = a.gF;
         float2* dst = spec + (int64_t(img0 / F) * NB) * F + (img0 % F);
+        if constexpr (NI == 4) {
+            // a lane pair stores a bin's 32-byte piece as the two 16-byte halves of one sector
+            for (int b2 = threadIdx.x; b2 < 2 * NB; b2 += CT) {
+                const int b = b2 >> 1, h = b2 & 1;
+                const int zb = b / (P * P), r = b - zb * (P * P), x = r / P, y = r - x * P;
+                const int off = (zb * P + x) * PYP + y;
+                const float2 u = cubes[(2 * h) * CV + off], w = cubes[(2 * h + 1) * CV + off];
+                __stcs(reinterpret_cast<float4*>(dst + int64_t(b) * F + 2 * h), make_float4(u.x, u.y, w.x, w.y));
+            }
+        } else
         for (int b = threadIdx.x; b < NB; b += CT) {
             const int zb = b / (P * P), r = b - zb * (P * P), x = r / P, y = r - x * P;
             float2 v[NI];
