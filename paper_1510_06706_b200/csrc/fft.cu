@@ -1155,8 +1155,12 @@ int grp_ni_env(const char* name, int dflt) {
 // measured on c5 with row-bin-major spectra (in-step, four transforms per
 // layer): four images per CTA at every pad (P = 20: 30.4 ms vs 31.0 / 37.5 for
 // one / two; P = 16: 12.1 vs 14.5 / 12.3; P = 12: 4.7 vs 4.9 for two)
+// with phase-major tensors and lane-pair stores (in-step, c5): the inverse at
+// P = 16 runs faster with two cubes per CTA (three CTAs per SM: dgrad 1.65 vs
+// 2.00 ms, image 1.31 vs 1.83); P = 20 inverses need the whole 32-byte pieces
+// (3.8 vs 7.1 ms), forwards are within 5% either way
 template <int P>
-int cube_grp_ni() { return grp_ni_env("ZNN_FFT_GRP_NI", 4); }
+int cube_grp_ni(bool inverse = false) { return grp_ni_env("ZNN_FFT_GRP_NI", inverse && P == 16 ? 2 : 4); }
 
 // row-bin-major piece of NI images at one bin: NI float2 <-> NI / 2 float4
 template <int NI>
@@ -2884,7 +2888,7 @@ void inverse3d(cudaStream_t st, const plan& p, const float2* spec, int64_t imgs,
                         else
                             go(fft3_inv_reg_k<PP, NI, false, true>, imgs / NI, cube_threads<NI>(), cube_reg_smem<PP, NI>());
                     };
-                    const int ni = cube_grp_ni<PP>();
+                    const int ni = cube_grp_ni<PP>(true);
                     if (ni == 1) run(std::integral_constant<int, 1>{});
                     else if (ni == 2) run(std::integral_constant<int, 2>{});
                     else run(std::integral_constant<int, 4>{});
