@@ -2169,7 +2169,6 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
     } else {
         g = threadIdx.x / CP, cp = threadIdx.x - (threadIdx.x / CP) * CP;
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int64_t q0 = int64_t(blockIdx.x) * Gs; q0 < planes; q0 += int64_t(gridDim.x) * Gs) {
         __syncthreads();  // tables ready / previous W consumed
         const int64_t q = q0 + g;
@@ -2226,30 +2225,29 @@ __global__ void __launch_bounds__(KS_THREADS, 3) dkinv_xy_k(const float2* __rest
                 }
         }
         __syncthreads();
-        // outputs (g, a, b): warp dot products over wy
+        // outputs (g, a, b): one thread per output, a serial dot product over wy
+        // (a warp per output spent ~50 instructions per warp on 20-48 terms and a
+        // shuffle tree: this phase, not the streaming read above, bound the small pads)
         const int nout = Gs * kx * ky;
-        for (int o = warp; o < nout; o += KS_THREADS / 32) {
+        for (int o = threadIdx.x; o < nout; o += KS_THREADS) {
             const int gg = o / (kx * ky), r = o - gg * (kx * ky), a = r / ky, b = r - (r / ky) * ky;
             int64_t qq = q0 + gg;
-            const bool valid = qq < planes;
-            if (gF && valid) {  // compact output stays in image-major plane order (ker * Zh + zb)
+            if (qq >= planes) continue;
+            if (gF) {  // compact output stays in image-major plane order (ker * Zh + zb)
                 int64_t ker;
                 int zb;
                 plane_decode(gF, qq, Zh, ker, zb);
                 qq = ker * Zh + zb;
             }
+            const float2* Wr = W + (gg * KMAX + a) * P;
             float2 acc = make_float2(0.f, 0.f);
-            for (int wy = lane; wy < P; wy += 32) {
-                const float2 v = W[(gg * KMAX + a) * P + wy];
+#pragma unroll 4
+            for (int wy = 0; wy < P; ++wy) {
+                const float2 v = Wr[wy];
                 const float2 e = TWB ? twb[TWB ? b * P + wy : 0] : tw[(wy * ((b * sy) % P)) % P];
                 cmacc(acc.x, acc.y, v.x, v.y, e.x, e.y);
             }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-            }
-            if (lane == 0 && valid) out[qq * (kx * ky) + a * ky + b] = acc;
+            out[qq * (kx * ky) + a * ky + b] = acc;
         }
     }
 }

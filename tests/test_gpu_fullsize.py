@@ -139,3 +139,45 @@ def test_fft_cmac_large_bin_grid(ctx):
     torch.cuda.synchronize()
     _check(shape, y, dx, dw, x, w, bias, g, m, np.random.default_rng(0))
     plan.close()
+
+
+def _c5_step(ctx, engines, steps=2):
+    """`steps` training steps of full-size c5 (B = 16) with fixed engines:
+    loss of the last step, gradients, updated parameters."""
+    from paper_1510_06706_b200 import Net, configs
+    cfg = configs.CONFIGS["c5"]
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    x = torch.rand((cfg.batch, cfg.in_maps) + tuple(cfg.in_dims), device="cuda", generator=gen)
+    lab = (torch.rand((cfg.batch, cfg.layers[-1].width) + tuple(cfg.out_dims), device="cuda", generator=gen) < 0.5).float()
+    net = Net(ctx, cfg.netspec(), cfg.out_dims, batch=cfg.batch, lr=cfg.lr, momentum=cfg.momentum, loss=cfg.loss)
+    for i, e in enumerate(engines):
+        net.set_layer_engine(i, e)
+    net.set_params(configs.init_params(cfg, 3))
+    for _ in range(steps - 1):
+        net.forward_backward(x, lab, sync_loss=False)
+        net.apply_update()
+    loss = net.forward_backward(x, lab)
+    grads = net.get_gradients()
+    desc = net.describe()
+    net.close()
+    del x, lab
+    torch.cuda.empty_cache()
+    return loss, grads, desc
+
+
+def test_c5_phase_major_step_equals_natural_order(ctx, monkeypatch):
+    """The benchmarked c5 step keeps the groups filter -> conv3 -> conv4 -> conv5
+    phase-major (executor::plan_layouts). At full size (B = 16, 120 maps) two
+    steps with the bench's engines give the same loss and gradients as the
+    natural-order run, whose FFT layers the tests above check against the
+    oracle shape by shape; the per-layer arithmetic is identical (the same
+    transforms over the same phase images), so the tolerance is 1e-5."""
+    engines = ["direct", "fft", "fft", "fft", "fft", "simt"]
+    loss_pm, g_pm, desc = _c5_step(ctx, engines)
+    assert "phase-major groups:" in desc and len(desc.split("phase-major groups:")[-1].split("\n")[0].split()) == 3, desc
+    monkeypatch.setenv("ZNN_PHASE_MAJOR", "0")
+    loss_nat, g_nat, desc0 = _c5_step(ctx, engines)
+    assert "phase-major groups:" not in desc0
+    assert np.isfinite(loss_pm) and abs(loss_pm - loss_nat) / (abs(loss_nat) + 1) < 1e-6
+    assert O.max_rel_error(g_pm, g_nat) < 1e-5

@@ -9,9 +9,10 @@ import torch
 
 sys.path.insert(0, '.')
 from paper_1510_06706_b200 import Context, Net, configs as C  # noqa: E402
+from paper_1510_06706_b200.api import profile_enable, profile_report  # noqa: E402
 
 name = sys.argv[1]
-batches = [int(v) for v in sys.argv[2:]]
+batches = [int(v) for v in sys.argv[2:] if not v.startswith('--')]
 ctx = Context(0)
 for Bl in batches:
     cfg = C.CONFIGS[name]
@@ -35,6 +36,14 @@ for Bl in batches:
     N = cfg.batch // Bl
     print(f'{name} local batch {Bl:2d} (N = {N}): {ms:8.2f} ms/step, engines {net.engines}, '
           f'projected {N}-GPU throughput {cfg.batch * np.prod(cfg.out_dims) / (ms * 1e-3):.3g} voxels/s', flush=True)
+    if '--shares' in sys.argv:
+        profile_report(ctx)
+        profile_enable(ctx, True)
+        net.train_step(x, lab, sync_loss=False)
+        torch.cuda.synchronize()
+        profile_enable(ctx, False)
+        for e in sorted(profile_report(ctx), key=lambda e: -e['ms'])[:22]:
+            print(f"   {e['ms']:7.3f} ms  {e['kernel']}", flush=True)
     net.close()
     del x, lab
     torch.cuda.empty_cache()
