@@ -37,6 +37,9 @@ def parse():
                    help="comma list (direct|fft|simt per conv layer) instead of the autotuner: "
                         "ncu captures of the step without the tuner's candidate launches")
     p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                   help="N > 1: strong = the config's batch sharded over the ranks (default; the SGD trajectory "
+                        "of the 1-GPU run), weak = every rank takes the config's whole batch (global batch x N)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
 
@@ -194,8 +197,11 @@ def run_ours(args):
     if fixed:
         engine = "direct"
     B = cfg.batch
-    lo, hi = shard_range(B, world, rank)
-    Bl = hi - lo
+    if args.scaling == "weak" and world > 1:  # per-rank work fixed: the global batch grows with the ranks
+        Bl, B = cfg.batch, cfg.batch * world
+    else:
+        lo, hi = shard_range(B, world, rank)
+        Bl = hi - lo
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
     ctx = Context(local, stream)
@@ -321,7 +327,7 @@ def run_ours(args):
     line = {
         "metric": "train_output_voxels_per_s", "value": value, "unit": "voxels/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": args.scaling if world > 1 else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "global_batch": B, "per_gpu_batch": Bl, "in_dims": cfg.in_dims,
                    "out_dims": cfg.out_dims, "parallelism": f"dp{world}", "engine": engine,
                    "conv_engines": [{0: "direct", 1: "fft", 3: "direct-simt"}.get(e, str(e)) for e in engines]

@@ -318,10 +318,11 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
                 goff[q] = ((oj % pm.sy) * pm.sz + (ol & (pm.sz - 1))) * pm.f * int(pm.qvol) + (oj / pm.sy) * pm.qz +
                           (ol >> pm.zsh);
         }
-        // ring[k]: (mask, g) of output plane ti - SX + k, k <= SX + 1 (the
-        // last one is the next iteration's plane, loaded a plane ahead)
-        int rm[SX + 2][4];
-        float rg[SX + 2][4];
+        // ring[k]: (mask, g) of output plane ti - SX + k, k <= SX + D (the
+        // last D are the next iterations' planes, loaded ahead of use)
+        constexpr int D = SX == 1 ? 2 : 1;
+        int rm[SX + 1 + D][4];
+        float rg[SX + 1 + D][4];
 #pragma unroll
         for (int k = 0; k < SX; ++k)
 #pragma unroll
@@ -345,11 +346,12 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
                 gp += pout;
             }
         };
-        fetch(0, SX);
+#pragma unroll
+        for (int k = 0; k < D; ++k) fetch(k, SX + k);
         float* dp = dm + tj * nz + tl;
         int tr = tj * nz + tl;
         for (int ti = 0; ti < nx; ++ti) {
-            fetch(ti + 1, SX + 1);
+            fetch(ti + D, SX + D);
             float acc = 0.f;
             // window (a, b, c) with b = 1 - (q >> 1), c = 1 - (q & 1): code (2 a + b) 2 + c
 #pragma unroll
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
             dp += pin;
             tr += int(pin);
 #pragma unroll
-            for (int k = 0; k <= SX; ++k)
+            for (int k = 0; k < SX + D; ++k)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) rm[k][q] = rm[k + 1][q], rg[k][q] = rg[k + 1][q];
         }
