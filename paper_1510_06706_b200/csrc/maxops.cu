@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
         }
         // ring[k]: (mask, g) of output plane ti - SX + k, k <= SX + D (the
         // last D are the next iterations' planes, loaded ahead of use)
-        constexpr int D = SX == 1 ? 2 : 1;
+        constexpr int D = 1;  // (two planes ahead measured slower here: 5.2 vs 4.6 ms at n = 91)
         int rm[SX + 1 + D][4];
         float rg[SX + 1 + D][4];
 #pragma unroll
