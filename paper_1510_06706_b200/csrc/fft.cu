@@ -1486,6 +1486,10 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_inv_reg_k(const float
 // line passes free of bank conflicts at the 16-byte bin pitch; the second
 // pair is offset by 64 B so the two 16-byte slots of one bin fall in
 // different bank groups.
+// exact floor(n / d) for 0 <= n < 2^15, 0 < d < 2^13 (inv = 1 / d): the loops
+// below index by runtime plane dims, and a 32-bit division is ~25 instructions
+__device__ __forceinline__ int fdiv_small(int n, float inv) { return int((float(n) + 0.5f) * inv); }
+
 constexpr int XP_NI = 4;
 template <int P>
 __host__ __device__ constexpr int xp_threads() { return (4 * P + 31) / 32 * 32 < 256 ? (4 * P + 31) / 32 * 32 : 256; }
@@ -1512,16 +1516,17 @@ __global__ void __launch_bounds__(xp_threads<P>()) fft_xy_fwd_pair_k(float2* __r
     float2* gq = spec + ((rest / Zh) * Zh * P * P + int64_t(zb) * P * P) * F + part * XP_NI;
     fill_twiddles<P>(tw);
     // the valid region the z pass wrote: 16-byte async copies, every load of the CTA in flight at once
+    const float inv_ny = 1.f / float(ny);
     for (int e2 = threadIdx.x; e2 < 2 * nx * ny; e2 += XT) {
         const int e = e2 >> 1, h = e2 & 1;
-        const int x = e / ny, y = e - x * ny;
+        const int x = fdiv_small(e, inv_ny), y = e - x * ny;
         cp_async16p(pls + h * PP + (x * PYP + y) * 2, gq + (x * P + y) * F + 2 * h);
     }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     for (int ln = threadIdx.x; ln < 4 * nx; ln += XT) {  // rows (y transforms) of the valid rows
-        const int jj = ln & 1, r = ln >> 1, h = r / nx, x = r - h * nx;
+        const int jj = ln & 1, r = ln >> 1, h = r >= nx ? 1 : 0, x = r - h * nx;
         float2* row = pls + h * PP + x * PYP * 2 + jj;
         float2 v[P];
 #pragma unroll
@@ -1595,7 +1600,7 @@ __global__ void __launch_bounds__(xp_threads<P>()) fft_xy_inv_pair_k(const float
     }
     __syncthreads();
     for (int ln = threadIdx.x; ln < 4 * xc; ln += XT) {  // row inverses of the kept rows
-        const int jj = ln & 1, r = ln >> 1, h = r / xc, i = r - h * xc;
+        const int jj = ln & 1, r = ln >> 1, h = r >= xc ? 1 : 0, i = r - h * xc;
         float2* row = pls + h * PP + i * PYP * 2 + jj;
         float2 v[P];
 #pragma unroll
@@ -1617,9 +1622,10 @@ __global__ void __launch_bounds__(xp_threads<P>()) fft_xy_inv_pair_k(const float
     // coalesced stores of the 4 compact blocks (plane img * Zh + zb, [xc][yc]): even / odd lanes
     // take the two maps of a pair (adjacent float2 in shared memory, 128-byte runs per map)
     const int blk = xc * yc;
+    const float inv_yc = 1.f / float(yc);
     for (int e = threadIdx.x; e < 4 * blk; e += XT) {
-        const int h = e / (2 * blk), rem = e - h * 2 * blk, r = rem >> 1, jj = rem & 1;
-        const int i = r / yc, c = r - i * yc;
+        const int h = e >= 2 * blk ? 1 : 0, rem = e - h * 2 * blk, r = rem >> 1, jj = rem & 1;
+        const int i = fdiv_small(r, inv_yc), c = r - i * yc;
         out[((grp * F + part * XP_NI + 2 * h + jj) * Zh + zb) * int64_t(blk) + r] =
             pls[h * PP + (i * PYP + c) * 2 + jj];
     }
