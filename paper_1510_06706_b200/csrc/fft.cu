@@ -554,6 +554,11 @@ __device__ __forceinline__ void cp_async16p(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// 8-byte async copy, zero-filled when !ok
+__device__ __forceinline__ void cp_async8z(void* smem, const void* gmem, bool ok) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(gmem), "r"(ok ? 8 : 0) : "memory");
+}
 // 4-byte async copy, zero-filled when !ok
 __device__ __forceinline__ void cp_async4z(void* smem, const void* gmem, bool ok) {
     const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -1769,13 +1774,20 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_fwd_reg_k(const float* __res
     const int64_t wl0 = int64_t(blockIdx.x) * ZR_LINES + warp * 64;  // this warp's first line
     float* wst = stage + warp * 64 * SP;
     const uint32_t pl = uint32_t(nx) * uint32_t(ny);
-    // each lane decodes its two lines (lane, lane + 32): source offset (-1: none),
-    // first z, z stride and z limit
+    // pair2 (sparsity 2 along z, row-bin-major line order): lines 2 t, 2 t + 1
+    // are the two z-phases of one original line, so thread t takes that pair:
+    // its complex input is the original line read as float2s, staged by plain
+    // contiguous 8-byte copies (a third of the staging instructions of the
+    // per-phase 4-byte copies, which were most of this kernel's issue slots)
+    const bool pair2 = phased && gF && ph.sz == 2 && !(ph.nz & 1) && !(nz > ph.nz / 2) &&
+                       ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(gate)) & 7) == 0;
+    // each lane decodes its two lines (lane, lane + 32; pair2: 2 lane, 2 lane + 1):
+    // source offset (-1: none), first z, z stride and z limit
     int64_t soff[2];
     int sz0[2], szs[2], szl[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        const int l = lane + 32 * h;
+        const int l = pair2 ? 2 * lane + h : lane + 32 * h;
         const int64_t line = wl0 + l;
         soff[h] = -1, sz0[h] = 0, szs[h] = 1, szl[h] = 0;
         int64_t ob = -1;
@@ -1807,6 +1819,23 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_fwd_reg_k(const float* __res
     // second tile.
     constexpr int NJ = (P + 31) / 32;
     float* gst = gate ? stage + ZR_LINES * SP : nullptr;
+    if (pair2) {
+        float2* wst2 = reinterpret_cast<float2*>(wst);                                  // [32 original lines][SP]
+        float2* gst2 = gate ? reinterpret_cast<float2*>(gst + warp * 64 * SP) : nullptr;
+        for (int l = 0; l < 32; ++l) {
+            const int64_t off = __shfl_sync(0xffffffffu, soff[0], l);
+#pragma unroll
+            for (int jj = 0; jj < NJ; ++jj) {
+                const int j = jj * 32 + lane;
+                if (j < P) {
+                    const bool ok = off >= 0 && j < nz;
+                    const int64_t e = ok ? off + 2 * j : 0;
+                    cp_async8z(wst2 + l * SP + j, in + e, ok);
+                    if (gate) cp_async8z(gst2 + l * SP + j, gate + e, ok);
+                }
+            }
+        }
+    } else
     for (int l = 0; l < 64; ++l) {
         const int src = l & 31;
         const bool hi = l >= 32;  // (uniform)
@@ -1829,7 +1858,20 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_fwd_reg_k(const float* __res
     cp_async_wait<0>();
     __syncthreads();  // twiddles, obase
     float2 v[P];
-    {
+    if (pair2) {
+        const float2* a2 = reinterpret_cast<const float2*>(wst) + lane * SP;
+        if (gate) {
+            const float2* g2 = reinterpret_cast<const float2*>(gst + warp * 64 * SP) + lane * SP;
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const float2 av = a2[j], gv = g2[j];
+                v[j] = make_float2(gv.x > 0.f ? av.x : 0.f, gv.y > 0.f ? av.y : 0.f);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) v[j] = a2[j];
+        }
+    } else {
         const float* a = wst + lane * SP;
         const float* b = wst + (lane + 32) * SP;
         if (gate) {  // fused ReLU backward: g * (y > 0) (transfer.hpp:99-106, ReLU'(0) = 0)
@@ -1844,7 +1886,8 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_fwd_reg_k(const float* __res
     }
     dft_r<P, P, false>(v, tw);
     // split: X1[k] = (Z[k] + conj Z[P-k]) / 2, X2[k] = (Z[k] - conj Z[P-k]) / (2 i)
-    const int64_t o1 = obase[warp * 64 + lane], o2 = obase[warp * 64 + lane + 32];
+    const int64_t o1 = obase[warp * 64 + (pair2 ? 2 * lane : lane)],
+                  o2 = obase[warp * 64 + (pair2 ? 2 * lane + 1 : lane + 32)];
     const int64_t zstride = int64_t(Px) * Py * (gF ? gF : 1);
 #pragma unroll
     for (int k = 0; k < Zh; ++k) {
