@@ -1914,11 +1914,17 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_inv_reg_k(const float2* __re
     const int64_t wl0 = int64_t(blockIdx.x) * ZR_LINES + warp * 64;
     const uint32_t per = uint32_t(g.xc) * uint32_t(g.yc);
     const int64_t zstride = int64_t(g.xc) * g.yc;
+    // pair2 (sparsity 2 along z): lines 2 t, 2 t + 1 are the two z-phases of one
+    // original line; thread t takes that pair, its two real outputs per z are
+    // adjacent voxels of the original line, staged as float2s and stored by
+    // contiguous 8-byte stores (see fft_z_fwd_reg_k)
+    const bool pair2 = g.phased && g.ph.sz == 2 && !(g.ph.nz & 1) && g.z_step == 1 && 2 * g.z_cnt <= g.ph.nz &&
+                       (reinterpret_cast<uintptr_t>(out) & 7) == 0;
     int64_t ib[2], obh[2];
     int ozh[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {  // decode this thread's two lines
-        const int l = lane + 32 * h;
+        const int l = pair2 ? 2 * lane + h : lane + 32 * h;
         const int64_t line = wl0 + l;
         ib[h] = -1;
         int64_t ob = -1;
@@ -1958,20 +1964,41 @@ __global__ void __launch_bounds__(ZR_THREADS) fft_z_inv_reg_k(const float2* __re
     __syncthreads();  // twiddles read; per-line tables ready
     float* wst = stage + warp * 64 * SP;
     {
-        const float b1 = bvals[warp * 64 + lane], b2 = bvals[warp * 64 + lane + 32];
+        const float b1 = bvals[warp * 64 + (pair2 ? 2 * lane : lane)],
+                    b2 = bvals[warp * 64 + (pair2 ? 2 * lane + 1 : lane + 32)];
         float* a = wst + lane * SP;
         float* b = wst + (lane + 32) * SP;
+        float2* ab = reinterpret_cast<float2*>(wst) + lane * SP;  // pair2: [32 original lines][SP] float2
 #pragma unroll
         for (int z = 0; z < P; ++z) {
             float r1 = v[z].x * g.scale + b1, r2 = v[z].y * g.scale + b2;
             if (g.act == 2) r1 = r1 > 0.f ? r1 : 0.f, r2 = r2 > 0.f ? r2 : 0.f;
             else if (g.act == 0) r1 = 1.f / (1.f + expf(-r1)), r2 = 1.f / (1.f + expf(-r2));
             else if (g.act == 1) r1 = tanhf(r1), r2 = tanhf(r2);
-            a[z] = r1;
-            b[z] = r2;
+            if (pair2) {
+                ab[z] = make_float2(r1, r2);
+            } else {
+                a[z] = r1;
+                b[z] = r2;
+            }
         }
     }
     __syncwarp();
+    if (pair2) {
+        constexpr int NQ2 = (P + 31) / 32;
+        const float2* wst2 = reinterpret_cast<const float2*>(wst);
+        for (int l = 0; l < 32; ++l) {
+            const int64_t ob = __shfl_sync(0xffffffffu, obh[0], l);
+            if (ob < 0) continue;  // (uniform)
+            float2* dst = reinterpret_cast<float2*>(out + ob);
+#pragma unroll
+            for (int u = 0; u < NQ2; ++u) {
+                const int q = lane + 32 * u;
+                if (q < g.z_cnt) dst[q] = wst2[l * SP + q];
+            }
+        }
+        return;
+    }
     // warp-cooperative stores of each line (lanes along the kept z); line l's
     // output base comes from lane l % 32 by shuffles, the per-lane z offsets
     // and staging indices are loop invariant
