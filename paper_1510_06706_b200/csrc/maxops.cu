@@ -284,15 +284,27 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter_bwd_k(const float* __restri
 // serve input planes oi and oi + SX, half the loads of maxfilter_bwd_k.
 // Block = 32 z-lanes x 8 y-rows, grid = (y tiles, maps). Sums in ascending
 // window order like maxfilter_bwd_k.
-template <int SX, typename M, bool PM = false>
-__global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restrict__ g,
-                                                            const M* __restrict__ mask, int nx, int ny,
-                                                            int nz, int mx, int my, int mz, int sy, int sz,
-                                                            float* __restrict__ dx, pm_dev pm) {
+template <int SX, typename M, bool PM, bool SUM>
+__device__ __forceinline__ void maxfilter2_bwd_body(const float* __restrict__ g, const M* __restrict__ mask, int nx,
+                                                    int ny, int nz, int mx, int my, int mz, int sy, int sz,
+                                                    float* __restrict__ dx, pm_dev pm, float* __restrict__ part,
+                                                    int part_f) {
     constexpr bool CODE = sizeof(M) == 1;
     const int tj = blockIdx.x * blockDim.y + threadIdx.y;
-    if (tj >= ny) return;
     const int64_t map = blockIdx.y;
+    // part: per-warp partial sums of dx in fixed order, part[(c * B + b) * cols + blockIdx.x * warps + warp]
+    // with map = b f + c (a warp is one z-row segment: its lanes share tj and leave together)
+    const int nwarp = (blockDim.x * blockDim.y) >> 5, warp = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+    float* pslot = nullptr;
+    if (SUM && part) {
+        const int64_t b = map / part_f, c = map - b * part_f, B = gridDim.y / part_f;
+        pslot = part + (c * B + b) * (int64_t(gridDim.x) * nwarp) + blockIdx.x * nwarp + warp;
+    }
+    if (tj >= ny) {
+        if (pslot && (threadIdx.x & 31) == 0) *pslot = 0.f;
+        return;
+    }
+    float tsum = 0.f;
     const int64_t pin = int64_t(ny) * nz, pout = int64_t(my) * mz;
     // phase-major gradient: plane oi of map (b, c) starts at gpm0 + (oi % sx) * pxs + (oi / sx) * qy * qz,
     // its voxel (oj, ol) at + goff[q]
@@ -361,6 +373,7 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
             for (int q = 0; q < 4; ++q)  // a = 0: plane ti
                 acc += (rm[SX][q] == (CODE ? 2 * (1 - (q >> 1)) + (1 - (q & 1)) : tr)) ? rg[SX][q] : 0.f;
             __stcs(dp, acc);
+            if constexpr (SUM) tsum += acc;
             dp += pin;
             tr += int(pin);
 #pragma unroll
@@ -369,6 +382,25 @@ __global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restr
                 for (int q = 0; q < 4; ++q) rm[k][q] = rm[k + 1][q], rg[k][q] = rg[k + 1][q];
         }
     }
+    if (SUM && pslot) {
+        for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+        if ((threadIdx.x & 31) == 0) *pslot = tsum;
+    }
+}
+template <int SX, typename M, bool PM = false>
+__global__ void __launch_bounds__(ZL * YR) maxfilter2_bwd_k(const float* __restrict__ g, const M* __restrict__ mask,
+                                                            int nx, int ny, int nz, int mx, int my, int mz, int sy,
+                                                            int sz, float* __restrict__ dx, pm_dev pm) {
+    maxfilter2_bwd_body<SX, M, PM, false>(g, mask, nx, ny, nz, mx, my, mz, sy, sz, dx, pm, nullptr, 1);
+}
+// + per-warp partial sums of dx (64 registers: four blocks per SM as the plain kernel)
+template <int SX, typename M>
+__global__ void __launch_bounds__(ZL * YR, 4) maxfilter2_bwd_sum_k(const float* __restrict__ g,
+                                                                   const M* __restrict__ mask, int nx, int ny, int nz,
+                                                                   int mx, int my, int mz, int sy, int sz,
+                                                                   float* __restrict__ dx, float* __restrict__ part,
+                                                                   int part_f) {
+    maxfilter2_bwd_body<SX, M, false, true>(g, mask, nx, ny, nz, mx, my, mz, sy, sz, dx, pm_dev{}, part, part_f);
 }
 
 __global__ void __launch_bounds__(ZL * YR) maxpool_fwd_k(const float* __restrict__ x, int nx, int ny, int nz, int px,
@@ -471,9 +503,12 @@ void maxfilter_fwd_t(cudaStream_t st, const float* x, int64_t maps, dims3 n, dim
     launch_check("maxfilter_fwd");
 }
 
+}  // namespace
+int64_t maxfilter_bwd_sum_cols(dims3 m, dims3 k, dims3 s);
+namespace {
 template <typename M>
 void maxfilter_bwd_t(cudaStream_t st, const float* g, const M* mask, int64_t maps, dims3 m, dims3 k, dims3 s,
-                     float* dx, pm_order pm = {}) {
+                     float* dx, pm_order pm = {}, float* part = nullptr, int part_f = 1) {
     const dims3 n{m.x + s.x * (k.x - 1), m.y + s.y * (k.y - 1), m.z + s.z * (k.z - 1)};
     prof_scope ps(st, "maxfilter_bwd n=" + std::to_string(n.x) + " maps=" + std::to_string(maps),
                   double(maps) * ((4.0 + sizeof(M)) * double(m.vol()) + 4.0 * double(n.vol())), 0);
@@ -484,6 +519,17 @@ void maxfilter_bwd_t(cudaStream_t st, const float* g, const M* mask, int64_t map
         // and re-read the sectors they share from DRAM (2.6x the read traffic)
         const unsigned bx = unsigned(std::min<int64_t>(4, ceil_div(n.z, ZL))) * ZL, by = (ZL * YR) / bx;
         const dim3 grid(unsigned(ceil_div(n.y, int64_t(by))), unsigned(maps));
+        require(!part || (part_f > 0 && maps % part_f == 0 &&
+                          int64_t(grid.x) * ((bx * by) / 32) == maxfilter_bwd_sum_cols(m, k, s)),
+                "maxfilter_backward: bias partials need maps = B f");
+        require(!part || !pm.on, "maxfilter_backward: bias partials come with natural-order gradients only");
+        if (part) {
+            auto* ks = s.x == 1 ? maxfilter2_bwd_sum_k<1, M> : maxfilter2_bwd_sum_k<2, M>;
+            ks<<<grid, dim3(bx, by, 1), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
+                                                 int(s.y), int(s.z), dx, part, part_f);
+            launch_check("maxfilter_bwd");
+            return;
+        }
         auto* kk = pm.on ? (s.x == 1 ? maxfilter2_bwd_k<1, M, true> : maxfilter2_bwd_k<2, M, true>)
                          : (s.x == 1 ? maxfilter2_bwd_k<1, M> : maxfilter2_bwd_k<2, M>);
         kk<<<grid, dim3(bx, by, 1), 0, st>>>(g, mask, int(n.x), int(n.y), int(n.z), int(m.x), int(m.y), int(m.z),
@@ -491,7 +537,7 @@ void maxfilter_bwd_t(cudaStream_t st, const float* g, const M* mask, int64_t map
         launch_check("maxfilter_bwd");
         return;
     }
-    require(!pm.on, "maxfilter_backward: phase-major gradients are read by the 2^3 kernel only");
+    require(!pm.on && !part, "maxfilter_backward: phase-major gradients / bias partials need the 2^3 kernel");
     auto* kb = (k.x == 2 && k.y == 2 && k.z == 2)   ? maxfilter_bwd_k<2, 2, 2, M>
                : (k.x == 1 && k.y == 2 && k.z == 2) ? maxfilter_bwd_k<1, 2, 2, M>
                                                     : maxfilter_bwd_k<0, 0, 0, M>;
@@ -515,8 +561,15 @@ void maxfilter_bwd(cudaStream_t st, const float* g, const int32_t* mask, int64_t
     maxfilter_bwd_t(st, g, mask, maps, m, k, s, dx);
 }
 void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m, dims3 k, dims3 s,
-                   float* dx, pm_order pm) {
-    maxfilter_bwd_t(st, g, code, maps, m, k, s, dx, pm);
+                   float* dx, pm_order pm, float* sum_part, int sum_f) {
+    maxfilter_bwd_t(st, g, code, maps, m, k, s, dx, pm, sum_part, sum_f);
+}
+
+int64_t maxfilter_bwd_sum_cols(dims3 m, dims3 k, dims3 s) {
+    if (!(k.x == 2 && k.y == 2 && k.z == 2 && (s.x == 1 || s.x == 2))) return 0;
+    const dims3 n{m.x + s.x, m.y + s.y, m.z + s.z};
+    const int64_t bx = std::min<int64_t>(4, ceil_div(n.z, ZL)) * ZL, by = (ZL * YR) / bx;
+    return ceil_div(n.y, by) * ((bx * by) / 32);  // y tiles x warps per block
 }
 
 void maxpool_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 p, float* y,

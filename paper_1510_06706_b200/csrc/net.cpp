@@ -675,8 +675,10 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                 const bool fuse_relu = L.fused && L.engine == 1 && !ce_here && L.fused_act == 2 &&
                                        !std::getenv("ZNN_NO_RELU_FUSION");
                 if (fuse_relu) {
+                    // (bias_summed: the max-filter backward above already left this layer's bias gradient)
                     run_conv_bwd(L, O.grad, I.grad, L.in != 0, update, L.pregated ? nullptr : O.act,
-                                 grads_ + L.b_off);
+                                 L.bias_summed ? nullptr : grads_ + L.b_off);
+                    L.bias_summed = false;
                     if (update)
                         znn_gpu::sgd_momentum(st_, params_ + L.b_off, vel_ + L.b_off, grads_ + L.b_off,
                                               L.shape.f_out, cfg_.lr, cfg_.mu);
@@ -688,6 +690,8 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                     if (ce_here) {
                         znn_gpu::transfer_bwd(st_, O.grad, O.act, true, B, L.shape.f_out, O.dims.vol(),
                                               L.none_dev, params_ + L.b_off, O.grad, grads_ + L.b_off, ws_);
+                    } else if (L.bias_summed) {
+                        L.bias_summed = false;  // the max-filter backward above left the bias gradient
                     } else {
                         // pregated (the max-filter's codes applied this ReLU's backward): the
                         // gradient is final, only its per-map sums (the bias gradient) remain
@@ -718,9 +722,25 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                 if (L.in != 0) znn_gpu::maxpool_bwd(st_, O.grad, O.mask, B * I.maps, O.dims, L.k, I.grad);
                 break;
             case lkind::filter:
-                if (L.in != 0)
+                if (L.in != 0) {
+                    // the conv layer below with a fused ReLU whose backward this filter's codes
+                    // carry: its bias gradient is the per-map sum of the gradient written here,
+                    // taken from the kernel's per-block partial sums (no extra pass over it)
+                    layer* below = nullptr;
+                    const int64_t cols = znn_gpu::maxfilter_bwd_sum_cols(O.dims, L.k, L.s);
+                    if (L.relu_gate && cols > 0 && B * I.maps < 65536 && !O.pm)  // (the phase-major variant keeps its registers)
+                        for (auto& C : layers_)
+                            if (C.kind == lkind::conv && C.out == L.in && C.pregated && C.fused && C.fused_act == 2)
+                                below = &C;
+                    float* part = below ? static_cast<float*>(ws_.get(sizeof(float) * size_t(B * I.maps * cols)))
+                                        : nullptr;
                     znn_gpu::maxfilter_bwd(st_, O.grad, O.code, B * I.maps, O.dims, L.k, L.s, I.grad,
-                                           znn_gpu::pm_order{O.pm ? 1 : 0, int(O.maps), O.pm_s});
+                                           znn_gpu::pm_order{O.pm ? 1 : 0, int(O.maps), O.pm_s}, part, int(I.maps));
+                    if (below) {
+                        znn_gpu::reduce_rows(st_, part, I.maps, B * cols, grads_ + below->b_off);
+                        below->bias_summed = true;
+                    }
+                }
                 break;
         }
     }

@@ -59,6 +59,7 @@ struct layer {
     dims3 k{1, 1, 1}, s{1, 1, 1};
     bool relu_gate = false;     // filter: its codes carry the ReLU backward of the conv feeding it
     bool pregated = false;      // conv with fused ReLU: the gradient arrives gated (by a relu_gate filter)
+    bool bias_summed = false;   // this backward pass: the filter above already left the bias gradient
     std::vector<int> edge_ids;  // reference edges covered (map order)
     std::vector<int> transfer_edge_ids;
 };

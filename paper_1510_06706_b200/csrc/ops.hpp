@@ -108,7 +108,14 @@ struct pm_order {
 };
 void maxfilter_fwd(cudaStream_t st, const float* x, int64_t maps, dims3 n, dims3 k, dims3 s,
                    float* y, uint8_t* code, bool relu_gate = false, pm_order pm = {});
+// sum_part (2^3 windows, natural-order g only): the kernel also leaves per-warp partial sums of dx,
+// [sum_f][maps / sum_f][maxfilter_bwd_sum_cols] floats; reduce_rows over the last two
+// gives the per-map sums over the batch = the bias gradient of a ReLU layer whose
+// backward the codes carry (no separate pass over dx)
 void maxfilter_bwd(cudaStream_t st, const float* g, const uint8_t* code, int64_t maps, dims3 m,
-                   dims3 k, dims3 s, float* dx, pm_order pm = {});
+                   dims3 k, dims3 s, float* dx, pm_order pm = {}, float* sum_part = nullptr, int sum_f = 1);
+int64_t maxfilter_bwd_sum_cols(dims3 m, dims3 k, dims3 s);  // 0: this window has no partial-sum path
+// out[r] = sum of part[r][0..cols) in fixed order (deterministic)
+void reduce_rows(cudaStream_t st, const float* part, int64_t rows, int64_t cols, float* out);
 
 }  // namespace znn_gpu

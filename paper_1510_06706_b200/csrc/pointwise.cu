@@ -179,6 +179,11 @@ void transfer_bwd(cudaStream_t st, const float* g, const float* xy, bool from_ou
     }
 }
 
+void reduce_rows(cudaStream_t st, const float* part, int64_t rows, int64_t cols, float* out) {
+    reduce_rows_k<<<unsigned(rows), 128, 0, st>>>(part, rows, cols, out);
+    launch_check("reduce_rows");
+}
+
 void loss_grad_async(cudaStream_t st, int kind, const float* a, const float* d, int64_t count,
                      float scale, float* grad, double* loss_dev, scratch& ws) {
     const int blocks = grid_for(count, 4);
