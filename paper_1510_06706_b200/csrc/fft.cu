@@ -2782,7 +2782,7 @@ void cmac_upd(cudaStream_t st, const float2* X, const float2* G, float2* DK, int
 // bias gradient of a fused transfer edge from the spectra (transfer.hpp:
 // 108-121): sum over patches and voxels of the gated gradient = the DC term,
 // here the sum over the valid (x, y) lines of the z pass's zb = 0 plane
-__global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec, int B, int fo, int64_t img_stride,
+__global__ void __launch_bounds__(1024) dc_bias_k(const float2* __restrict__ spec, int B, int fo, int64_t img_stride,
                                                  int nx, int ny, int py, float* __restrict__ dbias, int gF) {
     const int o = blockIdx.x;
     double acc = 0.0;
@@ -2792,10 +2792,10 @@ __global__ void __launch_bounds__(256) dc_bias_k(const float2* __restrict__ spec
         const int x = int(r / ny), y = int(r - (r / ny) * ny);
         acc += double(spec[spec_at(gF, b * fo + o, img_stride, int64_t(x) * py + y)].x);
     }
-    __shared__ double red[256];
+    __shared__ double red[1024];
     red[threadIdx.x] = acc;
     __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
+    for (int w = int(blockDim.x) / 2; w > 0; w >>= 1) {
         if (int(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
@@ -2857,7 +2857,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
         });
         launch_check("fft3_fwd_small");
         if (dbias) {  // the DC bin of each image's spectrum is its voxel sum
-            dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y, 1, 1,
+            dc_bias_k<<<unsigned(dmaps), 1024, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y, 1, 1,
                                                        int(p.P.y), dbias, quad);
             launch_check("fft_dc_bias");
         }
@@ -2884,7 +2884,7 @@ void forward3d(cudaStream_t st, const plan& p, const float* in, int64_t in_img_s
     });
     launch_check("fft_z_fwd");
     if (dbias) {
-        dc_bias_k<<<unsigned(dmaps), 256, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y,
+        dc_bias_k<<<unsigned(dmaps), 1024, 0, st>>>(spec, int(imgs / dmaps), int(dmaps), p.Zh * p.P.x * p.P.y,
                                                    int(n.x), int(n.y), int(p.P.y), dbias, quad);
         launch_check("fft_dc_bias");
     }

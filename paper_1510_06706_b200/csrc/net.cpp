@@ -728,9 +728,14 @@ double executor::forward_backward(const float* in_dev, const float* labels_dev, 
                     // taken from the kernel's per-block partial sums (no extra pass over it)
                     layer* below = nullptr;
                     const int64_t cols = znn_gpu::maxfilter_bwd_sum_cols(O.dims, L.k, L.s);
-                    if (L.relu_gate && cols > 0 && B * I.maps < 65536 && !O.pm)  // (the phase-major variant keeps its registers)
+                    // (the phase-major variant keeps its registers; the inspection mode keeps the
+                    // plain sum-only pass, whose summation order does not depend on the tensor order)
+                    if (L.relu_gate && cols > 0 && B * I.maps < 65536 && !O.pm && !cfg_.keep_images)
                         for (auto& C : layers_)
-                            if (C.kind == lkind::conv && C.out == L.in && C.pregated && C.fused && C.fused_act == 2)
+                            // (an FFT layer takes its bias gradient from the DC bins of the
+                            // gradient spectra it forms anyway, in double)
+                            if (C.kind == lkind::conv && C.out == L.in && C.pregated && C.fused && C.fused_act == 2 &&
+                                C.engine != 1)
                                 below = &C;
                     float* part = below ? static_cast<float*>(ws_.get(sizeof(float) * size_t(B * I.maps * cols)))
                                         : nullptr;
