@@ -1,4 +1,5 @@
 #!/usr/bin/env bash
+# max-filter / pointwise check: net-level parity then the per-kernel lines of a c5 bench step
 set -u
 mkdir -p gpurun_out
 timeout 600 python -m pytest -x -q -m gpu tests/test_gpu_net.py > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_quick.log
