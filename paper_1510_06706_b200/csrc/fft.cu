@@ -1209,6 +1209,53 @@ __global__ void __launch_bounds__(cube_threads<NI>()) fft3_fwd_reg_k(cube_io a, 
     __syncthreads();
     // z lines (R2C) of the valid (x, y) lines, read straight from HBM / L2
     const int nl1 = a.nx * a.ny;
+    bool z_done = false;
+    if constexpr (NI >= 4 && P >= 20) {
+        // one CTA per SM (four 37 KB cubes): nothing else hides the loads of a
+        // round, so the next round's dense line is fetched before this round's
+        // transform (phase-major tensors: Q4 float4s per line, + the gate's)
+        if (a.vec4) {
+            constexpr int Q4 = (P + 3) / 4;
+            float4 cur[Q4], curg[Q4];
+            auto fetch = [&](int ln, float4 (&u)[Q4], float4 (&gt)[Q4]) {
+                const int j = ln / nl1, l1 = ln - j * nl1;
+                const int64_t base = int64_t(img0 + j) * a.img_stride + int64_t(l1) * a.nz;
+                const float4* __restrict__ p4 = reinterpret_cast<const float4*>(a.src + base);
+                const float4* __restrict__ g4 = a.gate ? reinterpret_cast<const float4*>(a.gate + base) : nullptr;
+#pragma unroll
+                for (int z4 = 0; z4 < Q4; ++z4) {
+                    const bool in = 4 * z4 < a.nz;
+                    u[z4] = in ? __ldg(p4 + z4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    gt[z4] = (in && g4) ? __ldg(g4 + z4) : make_float4(1.f, 1.f, 1.f, 1.f);
+                }
+            };
+            const int total = NI * nl1;
+            if (int(threadIdx.x) < total) fetch(threadIdx.x, cur, curg);
+            for (int ln = threadIdx.x; ln < total; ln += CT) {
+                float4 nxt[Q4], nxtg[Q4];
+                if (ln + CT < total) fetch(ln + CT, nxt, nxtg);
+                const int j = ln / nl1, l1 = ln - j * nl1;
+                const int x = l1 / a.ny, y = l1 - x * a.ny;
+                float2 v[P];
+#pragma unroll
+                for (int z4 = 0; z4 < Q4; ++z4) {
+                    const float4 u = cur[z4], gt = curg[z4];
+                    if (4 * z4 < P) v[4 * z4] = make_float2(gt.x > 0.f ? u.x : 0.f, 0.f);
+                    if (4 * z4 + 1 < P) v[4 * z4 + 1 < P ? 4 * z4 + 1 : 0] = make_float2(gt.y > 0.f ? u.y : 0.f, 0.f);
+                    if (4 * z4 + 2 < P) v[4 * z4 + 2 < P ? 4 * z4 + 2 : 0] = make_float2(gt.z > 0.f ? u.z : 0.f, 0.f);
+                    if (4 * z4 + 3 < P) v[4 * z4 + 3 < P ? 4 * z4 + 3 : 0] = make_float2(gt.w > 0.f ? u.w : 0.f, 0.f);
+                }
+                dft_r<P, P, false>(v, tw);
+                float2* cube = cubes + j * CV;
+#pragma unroll
+                for (int k = 0; k < Zh; ++k) cube[(k * P + x) * PYP + y] = v[k];
+#pragma unroll
+                for (int z4 = 0; z4 < Q4; ++z4) cur[z4] = nxt[z4], curg[z4] = nxtg[z4];
+            }
+            z_done = true;
+        }
+    }
+    if (!z_done)
     for (int ln = threadIdx.x; ln < NI * nl1; ln += CT) {
         const int j = NI == 1 ? 0 : ln / nl1, l1 = ln - j * nl1;
         const int x = l1 / a.ny, y = l1 - x * a.ny;
